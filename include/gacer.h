@@ -1,0 +1,246 @@
+/*
+ * gacer.h -- C ABI of the B200-native GACER multi-tenant executor.
+ *
+ * GACER (arXiv 2304.11745, "Granularity-Aware ConcurrEncy Regulation for
+ * Multi-Tenant Deep Learning") regulates the concurrent execution of N tenant
+ * DNNs M_1..M_n on one GPU (§4.1 l.603-607) with
+ *   - spatial regulation: an operator O^B is decomposed into chunks
+ *     O^{B^1},...,O^{B^j}, sum B^j = B (Eq. 5, l.657-668), selected by a mask
+ *     list and list_B (l.683-684); plus channel split (north_star addition);
+ *   - temporal regulation: per-model pointer lists P_n forming Matrix_P
+ *     (Eq. 7, l.742-753) that cut every DFG into segments; same-index
+ *     segments of all models form a cluster deployed together (Eq. 6,
+ *     l.723-739); a pointer is a synchronisation point (l.767-771).
+ *
+ * This library executes one *round* (every registered tenant's forward once)
+ * under such a plan with ONE persistent sm_100a kernel: operator chunks are
+ * pulled from per-tenant device work queues, pointers are enforced by
+ * device-side cluster counters (no host stream events), producer->consumer
+ * order by device-side dependency counters.
+ *
+ * Conventions (all calls):
+ *   - return value >= 0 on success (an id where documented), else a negative
+ *     gacer_status; gacer_last_error() then holds a message.
+ *   - all pointer arguments are HOST pointers unless named *_dev.
+ *   - the library is not thread-safe; one process drives one GPU.
+ *   - a CUDA error is sticky: every later call returns GACER_E_CUDA.
+ */
+#ifndef GACER_H_
+#define GACER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+typedef enum {
+  GACER_OK = 0,
+  GACER_E_INVALID_ARG = -1,
+  GACER_E_DUPLICATE_ID = -2,            /* two ops share an id */
+  GACER_E_UNKNOWN_PREDECESSOR = -3,     /* pred id not in the graph */
+  GACER_E_CYCLE = -4,                   /* dependency cycle */
+  GACER_E_UNSUPPORTED_OP = -5,          /* op kind / pattern not lowered               */
+  GACER_E_CHUNK_SUM_MISMATCH = -6,      /* sum of list_B != B (Eq. 5, l.662)            */
+  GACER_E_MASKED_OP_MISSING_CHUNKS = -7,/* axis set but no sizes */
+  GACER_E_CUT_OUT_OF_RANGE = -8,        /* pointer outside [0, n_ops] */
+  GACER_E_UNSORTED_CUTS = -9,           /* pointers decrease */
+  GACER_E_POINTER_COUNT_MISMATCH = -10, /* "Each P has the same number of pointers" (l.753) */
+  GACER_E_STATE = -11,                  /* call out of order (no init / no tenants / unbound I/O) */
+  GACER_E_OOM = -12,
+  GACER_E_CUDA = -13,                   /* sticky CUDA error */
+  GACER_E_DEADLOCK = -14,               /* device watchdog fired (spin budget exceeded) */
+  GACER_E_SHAPE = -15                   /* inconsistent tensor shapes in the graph */
+} gacer_status;
+
+/* ------------------------------------------------------------- operators */
+/* PyTorch eval-mode semantics. */
+typedef enum {
+  GACER_OP_CONV2D = 1,  /* c_in c_out kh kw stride pad_h pad_w groups (1 or c_in==c_out); weight OIHW */
+  GACER_OP_LINEAR = 2,  /* c_in c_out; weight [c_out][c_in]; input flattened in NCHW order */
+  GACER_OP_MAXPOOL = 3, /* kh kw stride pad_h pad_w; floor mode, -inf padding */
+  GACER_OP_AVGPOOL = 4, /* kh kw stride pad_h pad_w; flags & COUNT_INCLUDE_PAD */
+  GACER_OP_GAP = 5,     /* adaptive average pool to 1x1 */
+  GACER_OP_ADD = 6,     /* 2 preds, elementwise */
+  GACER_OP_CONCAT = 7,  /* n preds, channel axis */
+  GACER_OP_BN = 8,      /* inference BatchNorm2d: bn_gamma/beta/mean/var [c_out], bn_eps */
+  GACER_OP_RELU = 9,
+  GACER_OP_RELU6 = 10,
+  GACER_OP_FLATTEN = 11, /* NCHW-order flatten (identity on the data; reorders LINEAR weights) */
+  GACER_OP_DROPOUT = 12  /* identity (inference) */
+} gacer_op_kind;
+
+typedef enum { GACER_DTYPE_BF16 = 1, GACER_DTYPE_FP32 = 2 } gacer_dtype;
+typedef enum { GACER_AXIS_NONE = 0, GACER_AXIS_BATCH = 1, GACER_AXIS_CHANNEL = 2 } gacer_axis;
+enum { GACER_FLAG_BIAS = 1, GACER_FLAG_COUNT_INCLUDE_PAD = 2 };
+
+/* One operator O_{n,i} (SPEC OperatorSpec S:27).
+ * Parameter arrays are HOST float32 arrays; they are copied (and, for BF16
+ * graphs, rounded to bf16 RNE and repacked) during gacer_register_tenant, so
+ * the caller may free them on return.  Unused fields are ignored. */
+typedef struct {
+  int32_t id;                 /* unique within the tenant, >= 1; id 0 = the graph input */
+  int32_t kind;               /* gacer_op_kind */
+  int32_t n_preds;
+  const int32_t* preds;       /* predecessor ids, each < this op's position in issue order */
+  int32_t c_in, c_out, kh, kw, stride, pad_h, pad_w, groups;
+  int32_t flags;              /* GACER_FLAG_* */
+  const float* weight;        /* CONV2D: [c_out][c_in/groups][kh][kw]; LINEAR: [c_out][c_in] */
+  const float* bias;          /* [c_out] when flags & GACER_FLAG_BIAS */
+  const float* bn_gamma;      /* BN: [c_out] each */
+  const float* bn_beta;
+  const float* bn_mean;
+  const float* bn_var;
+  float bn_eps;
+} gacer_op_desc;
+
+/* A tenant DFG M_n = [O_{n,1},...,O_{n,i}] in topological issue order
+ * (l.605-607).  The last op is the tenant's output. */
+typedef struct {
+  int32_t n_ops;
+  const gacer_op_desc* ops;
+  int32_t in_c, in_h, in_w;   /* per-sample input shape (C, H, W) */
+  int32_t dtype;              /* gacer_dtype of activations/weights on the GPU */
+  int32_t train;              /* must be 0 in this version (training tenants: not built yet) */
+  float lr, momentum;
+} gacer_graph;
+
+/* Spatial regulation for one operator: the mask entry and list_B (l.667,
+ * l.683-684).  op_index is the 1-based position of the op in the tenant's
+ * ORIGINAL (pre-fusion) op list.  axis BATCH: sizes sum to the batch (Eq. 5);
+ * axis CHANNEL: sizes sum to c_out.  sm_budget is reserved (may be NULL). */
+typedef struct {
+  int32_t tenant;
+  int32_t op_index;
+  int32_t axis;               /* gacer_axis */
+  int32_t n_chunks;
+  const int32_t* sizes;       /* [n_chunks], each >= 1 */
+  const int32_t* sm_budget;   /* reserved, may be NULL */
+} gacer_chunking;
+
+typedef struct {
+  int32_t n;
+  const gacer_chunking* items; /* ops not listed: mask(O) = 0 (not decomposed) */
+} gacer_decomposition;
+
+/* Matrix_P (Eq. 7, l.742-753): cuts[t * n_pointers + j] is the j-th pointer
+ * of tenant t (registration order).  A cut p is the segment boundary after
+ * original op p; cuts are non-decreasing in [0, n_ops]; repeated / zero cuts
+ * give empty segments (the paper's [None], Eq. 6 l.730).  Cluster k = the
+ * k-th segment of every tenant; no op of cluster k+1 starts before every op
+ * of cluster k has finished. */
+typedef struct {
+  int32_t n_tenants;          /* must equal the number of registered tenants */
+  int32_t n_pointers;         /* |P_n|, the same for every tenant */
+  const int32_t* cuts;        /* [n_tenants][n_pointers] */
+} gacer_sync_pointers;
+
+/* Execution mode of gacer_run_round*.  EXECUTOR is the method; the other two
+ * are the paper's baselines run on the SAME tile functions. */
+typedef enum {
+  GACER_MODE_EXECUTOR = 0,    /* one persistent multi-tenant kernel per round */
+  GACER_MODE_SEQUENTIAL = 1,  /* "CuDNN-Seq": one kernel per fused op, one stream, tenant after tenant */
+  GACER_MODE_MULTISTREAM = 2  /* "Stream-Parallel": one kernel per fused op, one stream per tenant */
+} gacer_mode;
+
+typedef enum {
+  GACER_PARTITION_WORK_CONSERVING = 0, /* each CTA prefers one tenant, steals from the others */
+  GACER_PARTITION_STRICT = 1           /* each CTA serves only its tenant (SM share per tenant) */
+} gacer_partition;
+
+typedef struct {
+  int32_t num_ctas;           /* executor grid; 0 = #SMs */
+  int32_t partition;          /* gacer_partition */
+  int32_t watchdog_ms;        /* device spin budget before GACER_E_DEADLOCK; 0 = 2000 */
+  int32_t trace;              /* 1 = record per-item (tenant, op, sm, t0, t1) */
+} gacer_options;
+
+typedef struct {
+  double last_round_ms;       /* device time of the last round (CUDA events) */
+  int64_t n_items;            /* work items per round under the current plan */
+  int32_t n_clusters;         /* |P| + 1 */
+  int32_t n_fused_ops;        /* lowered ops over all tenants */
+  int32_t kernel_launches;    /* kernels launched by the last round */
+  int32_t n_tenants;
+  double tensor_flops;        /* algorithmic conv+FC FLOPs per round (2*MAC) */
+  double cc_bytes;            /* algorithmic bytes of the CUDA-core ops per round */
+} gacer_round_stats;
+
+typedef struct {
+  int32_t n_orig_ops;         /* ops given at registration */
+  int32_t n_fused_ops;        /* ops after conv+BN+add+act fusion */
+  int32_t batch;
+  int32_t in_c_pad;           /* channel stride of the NHWC input buffer */
+  int32_t in_h, in_w;
+  int32_t out_features;       /* output row length (float32) */
+  int64_t in_bytes;           /* bytes of the input buffer: batch*in_h*in_w*in_c_pad*elem */
+  int64_t out_bytes;          /* batch*out_features*4 */
+  double flops;               /* algorithmic FLOPs of one forward */
+} gacer_tenant_info;
+
+/* ------------------------------------------------------------------ calls */
+
+/* Bind the calling process to `cuda_device` (>= 0).  cuda_device = -1 opens
+ * a HOST-ONLY instance: registration and plan compilation run (validation,
+ * lowering, Eq. 6/7 segmentation) but nothing touches a GPU and run calls
+ * return GACER_E_STATE.  opts may be NULL (defaults). */
+int gacer_init(int cuda_device, const gacer_options* opts);
+int gacer_shutdown(void);
+
+/* Register tenant M_n with its batch B (>= 1).  Validates the DFG (ids,
+ * predecessors, acyclicity, topological issue order, shapes), fuses
+ * conv+BN(+add)(+ReLU/ReLU6), linear(+ReLU), elides dropout/flatten, turns
+ * concat into channel-offset writes, and (device mode) packs the weights
+ * into library-owned device memory.  Resets the regulation to the identity
+ * plan (no chunks, no pointers).  Returns the tenant id (0, 1, ...). */
+int gacer_register_tenant(const gacer_graph* graph, int32_t batch);
+
+int gacer_get_tenant_info(int tenant, gacer_tenant_info* out);
+
+/* Bind caller-owned DEVICE buffers.  input_dev: NHWC [B][in_h][in_w][in_c_pad]
+ * of the graph dtype, padding channels zero.  output_dev: float32
+ * [B][out_features] -- the last op's output in NHWC order [B][H][W][C]
+ * (logits [B][classes] for a 1x1 output).  Both 16-byte aligned; both must
+ * outlive every round that uses them. */
+int gacer_bind_io(int tenant, const void* input_dev, void* output_dev);
+
+/* Install a regulation plan (mask/list_B/list_C and Matrix_P).  Either
+ * argument may be NULL (no decomposition / no pointers).  Atomic: on error
+ * the previous plan stays in force. */
+int gacer_set_regulation(const gacer_decomposition* decomposition,
+                         const gacer_sync_pointers* sync_pointers);
+
+/* Cluster index of every ORIGINAL op of `tenant` under the current plan
+ * (out[i] for op i+1), i.e. Eq. 6/7 as compiled.  n = capacity of out. */
+int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n);
+
+int gacer_set_mode(int mode);               /* gacer_mode */
+
+/* One round: every tenant's forward once on its bound input.
+ * gacer_run_round blocks until the outputs are visible;
+ * gacer_run_round_async enqueues on `stream` (a cudaStream_t; NULL = the
+ * library stream) and returns. */
+int gacer_run_round(void);
+int gacer_run_round_async(void* stream);
+
+/* End-to-end round with HOST buffers: copies host_inputs[t] (layout as
+ * gacer_bind_io, pinned memory recommended) to the bound device inputs, runs
+ * the round, copies every output to host_outputs[t]; blocks.  Arrays are
+ * indexed by tenant id. */
+int gacer_run_round_host(const void* const* host_inputs, void* const* host_outputs);
+
+int gacer_get_stats(gacer_round_stats* out);
+
+/* Trace of the last executor round (options.trace = 1): up to `cap` records
+ * of 6 int64 each: tenant, fused op, sm id, item index, t_start_ns, t_end_ns.
+ * Returns the number of records written. */
+int gacer_get_trace(int64_t* records, int32_t cap);
+
+const char* gacer_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GACER_H_ */

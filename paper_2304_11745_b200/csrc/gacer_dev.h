@@ -1,0 +1,108 @@
+// gacer_dev.h -- structures shared by the host runtime (host.cpp) and the
+// sm_100a kernels (executor.cu).  Plain old data, uploaded once per
+// registration / plan.
+#pragma once
+#include <stdint.h>
+
+namespace gacer {
+
+// ---------------------------------------------------------------- op kinds
+// Lowered ("fused") operator kinds executed by the device.
+enum DevKind : int32_t {
+  DK_GEMM = 1,     // bf16 implicit-GEMM conv (im2col A) or swap-AB linear, tcgen05 + TMEM
+  DK_DW = 2,       // depthwise 3x3-style conv (groups == C), CUDA cores
+  DK_MAXPOOL = 3,
+  DK_AVGPOOL = 4,
+  DK_GAP = 5,
+  DK_SIMT_GEMM = 6,// fp32 conv / linear on CUDA cores (FFMA), fixed K order
+  DK_ELTWISE = 7,  // y = act(a [+ b]) standalone elementwise
+};
+
+enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2 };
+
+// GEMM tile geometry
+constexpr int BM = 128;           // rows per tile (UMMA M)
+constexpr int BK = 64;            // bf16 elements per K-block = one 128-byte swizzle row
+constexpr int BN_MAX = 128;       // max UMMA N per tile
+constexpr int STAGES = 4;         // smem ring depth
+constexpr int NTHREADS = 256;     // threads per CTA (8 warps)
+constexpr int CC_TASKS_PER_THREAD = 4;
+
+struct OpDev {
+  int32_t kind;            // DevKind
+  int32_t tenant;
+  int32_t act;             // Act
+  int32_t out_f32;         // output dtype: 1 = float32, 0 = bf16 (or f32 for fp32 tenants: see elem)
+  int32_t f32;             // 1 = fp32 tenant (inputs/weights fp32), 0 = bf16
+  int32_t swap;            // GEMM: 1 = swap-AB linear (A = weights, B = activations)
+  int32_t cip;             // avgpool count_include_pad
+  int32_t has_skip;
+
+  // input activation tensor, NHWC: elem(n,h,w,c) = in[((n*H + h)*W + w)*ldi + c]
+  const void* in;
+  int32_t B, H, W, C, ldi; // C = channels read (multiple of 8 for bf16)
+  // output tensor NHWC (Ho x Wo pixels, Cout channels), row stride ldo
+  void* out;
+  int32_t Ho, Wo, Cout, ldo;
+  // residual operand (same shape/layout as out), row stride lds
+  const void* skip;
+  int32_t lds, pad0;
+
+  int32_t kh, kw, stride, ph, pw, pad1;
+
+  // GEMM view
+  int32_t M, N, K;         // conv: M = B*Ho*Wo, N = Cout, K = kh*kw*C;  swap: M = Cout, N = B, K = C_flat
+  int32_t Kpad;            // multiple of BK (weights row length)
+  int32_t tiles_m, tiles_n;
+  int32_t bm, bn;          // tile sizes (GEMM: bm = 128; CC ops: pixel rows / channels per tile)
+  int32_t split_k, nkb;    // nkb = Kpad / BK
+  const void* wt;          // packed weights: bf16 [Npad or Mpad][Kpad] K-major (fp32 [Cout][K] for SIMT);
+                           // DW: [kh*kw][C] channel-minor
+  int32_t ldw, pad2;
+  const void* act_b;       // swap-AB: activations as the B operand, row stride ldb (elements)
+  int32_t ldb, pad3;
+  const float* scale;      // [Cout] folded BN scale (1 if no BN)
+  const float* bias;       // [Cout] folded BN shift + conv bias
+  float* partial;          // split-K workspace [tiles][split][BM*bn] fp32
+  uint32_t* tile_cnt;      // split-K arrival counters [tiles]
+};
+
+// One work item: one output tile (mt, nt) of one op, K-slice ks.
+struct Item {
+  int32_t op;
+  int32_t mt, nt, ks;
+  int32_t dep_begin, dep_count;
+  int32_t chunk;           // global chunk counter id (released on completion)
+  int32_t cluster;
+};
+
+struct Dep {
+  int32_t counter;         // chunk counter id
+  uint32_t target;         // items of that chunk per round
+};
+
+struct Seg {                // queue segment for (tenant, cluster)
+  int32_t begin, size;
+};
+
+struct ExecParams {
+  const OpDev* ops;
+  const Item* items;
+  const Dep* deps;
+  const int32_t* queue;     // item ids, grouped by segment
+  const Seg* segs;          // [n_tenants * n_clusters]
+  const int32_t* cta_pref;  // [num_ctas * n_tenants] tenant preference (-1 = none)
+  uint32_t* heads;          // [n_tenants * n_clusters] claim counters (reset by last CTA)
+  uint32_t* chunk_done;     // [n_chunks] epoch-accumulated completion counts
+  uint32_t* cluster_done;   // [n_clusters] epoch-accumulated
+  const uint32_t* cluster_total; // [n_clusters] items per round
+  uint32_t* exit_count;
+  int32_t* error;           // device error flag (deadlock watchdog)
+  int64_t* trace;           // optional [n_items * 6]
+  int32_t n_tenants, n_clusters;
+  uint32_t epoch;           // round number since plan install, >= 1
+  int32_t n_heads;
+  int64_t watchdog_ns;
+};
+
+}  // namespace gacer

@@ -1,0 +1,1312 @@
+// host.cpp -- C ABI of the GACER executor (include/gacer.h).
+//
+// Registration lowers a tenant DFG (§4.1 l.605-607) into fused
+// device ops; gacer_set_regulation compiles the paper's regulation variables
+// -- mask/list_B (§4.2 l.657-685, Eq. 5) and Matrix_P (§4.3 l.742-753,
+// Eq. 6/7) -- into per-(tenant, cluster) work queues, per-item dependency
+// lists and cluster totals that the persistent kernel enforces on-device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/gacer.h"
+#include "gacer_dev.h"
+
+namespace gacer {
+int executor_smem_bytes();
+cudaError_t configure_kernels();
+cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s);
+cudaError_t launch_op(const OpDev* ops_dev, int op_idx, int kind, int n_blocks, cudaStream_t s);
+}  // namespace gacer
+
+using namespace gacer;
+
+namespace {
+
+thread_local std::string g_err;
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+constexpr int kSplitSms = 148;  // split-K is a function of the layer shape only (bit-identity, H4)
+
+int roundup(int a, int b) { return (a + b - 1) / b * b; }
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+int pow2ceil(int a) { int p = 1; while (p < a) p <<= 1; return p; }
+
+uint16_t f32_to_bf16_rne(float f);
+float f32_to_bf16_round_trip(float f) {
+  const uint32_t u = static_cast<uint32_t>(f32_to_bf16_rne(f)) << 16;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return static_cast<uint16_t>(u >> 16);  // inf/nan
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// ---------------------------------------------------------------- tenants
+struct Tensor {
+  int C = 0, H = 0, W = 0;
+  int buf = -1;          // storage buffer id; -1 = graph input, -2 = user output
+  int coff = 0, ldc = 0;
+  int producer_orig = -1;  // original op producing it (-1 = input)
+  std::vector<int> writers;  // fused ops writing (a slice of) it
+  bool sliced = false;     // storage is a slice of a concat tensor
+};
+
+struct FusedOp {
+  int kind = 0;
+  int head = -1, last = -1;  // original op indices (0-based)
+  std::vector<int> members;
+  int in_t = -1, skip_t = -1, out_t = -1;
+  int act = ACT_NONE;
+  bool swap = false;
+  // geometry
+  int Cin = 0, H = 0, W = 0, Cout = 0, Ho = 0, Wo = 0;
+  int kh = 1, kw = 1, stride = 1, ph = 0, pw = 0;
+  int cread = 0;  // channels read per tap (K = kh*kw*cread)
+  int M = 0, N = 0, K = 0, Kpad = 0, tiles_m = 1, tiles_n = 1, bm = 0, bn = 0, split_k = 1, nkb = 0;
+  bool cip = true;
+  // packed params (host)
+  std::vector<uint16_t> w_bf16;
+  std::vector<float> w_f32;
+  std::vector<float> scale, bias;
+  // device
+  void* d_w = nullptr;
+  float* d_scale = nullptr;
+  float* d_bias = nullptr;
+  float* d_partial = nullptr;
+  uint32_t* d_tile_cnt = nullptr;
+  double flops = 0, bytes = 0;
+  bool rows_are_pixels = true;  // output pixel rows are the GEMM/tile M axis
+};
+
+struct Tenant {
+  int batch = 0, dtype = 0, n_orig = 0;
+  int in_c = 0, in_h = 0, in_w = 0, in_c_pad = 0;
+  std::vector<int> orig_kind;
+  std::vector<int> orig_out_c;    // c_out for chunk validation
+  std::vector<int> orig_tensor;   // tensor id of each original op's output
+  std::vector<int> orig_fused;    // fused op containing the original op (-1 for aliases)
+  std::vector<Tensor> tensors;    // tensor 0 = graph input
+  std::vector<FusedOp> fops;
+  int out_t = -1;
+  int out_features = 0;
+  std::vector<void*> bufs;        // device activation buffers
+  std::vector<size_t> buf_bytes;
+  const void* in_dev = nullptr;
+  void* out_dev = nullptr;
+  double flops = 0;
+  int op_base = 0;                // index of fops[0] in the global op table
+};
+
+// ---------------------------------------------------------------- plan
+struct Chunking {
+  int axis = GACER_AXIS_NONE;
+  std::vector<int> sizes;
+};
+
+struct Plan {
+  int n_clusters = 1;
+  std::vector<std::vector<int>> cuts;               // [tenant][pointer]
+  std::map<std::pair<int, int>, Chunking> chunks;   // (tenant, orig op 0-based) -> chunking
+  // compiled
+  std::vector<Item> items;
+  std::vector<Dep> deps;
+  std::vector<int32_t> queue;
+  std::vector<Seg> segs;
+  std::vector<uint32_t> cluster_total;
+  int n_chunk_counters = 0;
+  std::vector<std::vector<int>> fop_cluster;        // [tenant][fused op]
+};
+
+struct State {
+  bool inited = false;
+  bool host_only = true;
+  int device = -1;
+  int num_sms = 148;
+  gacer_options opts{};
+  cudaStream_t stream = nullptr;
+  std::vector<cudaStream_t> tstreams;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<Tenant> tenants;
+  Plan plan;
+  int mode = GACER_MODE_EXECUTOR;
+  bool sticky_cuda = false;
+  // device op table
+  OpDev* d_ops = nullptr;
+  std::vector<OpDev> h_ops;
+  // device plan
+  Item* d_items = nullptr;
+  Dep* d_deps = nullptr;
+  int32_t* d_queue = nullptr;
+  Seg* d_segs = nullptr;
+  int32_t* d_pref = nullptr;
+  uint32_t* d_heads = nullptr;
+  uint32_t* d_chunk_done = nullptr;
+  uint32_t* d_cluster_done = nullptr;
+  uint32_t* d_cluster_total = nullptr;
+  uint32_t* d_exit = nullptr;
+  int32_t* d_error = nullptr;
+  int64_t* d_trace = nullptr;
+  uint32_t epoch = 0;
+  int grid = 0;
+  double last_ms = 0;
+  int last_launches = 0;
+};
+State S;
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      S.sticky_cuda = true;                                                              \
+      return set_err(GACER_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));     \
+    }                                                                                    \
+  } while (0)
+
+template <class T>
+int dev_upload(T** dptr, const T* src, size_t n) {
+  if (*dptr) { cudaFree(*dptr); *dptr = nullptr; }
+  if (n == 0) return 0;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), n * sizeof(T)));
+  if (src) CUDA_TRY(cudaMemcpy(*dptr, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  else CUDA_TRY(cudaMemset(*dptr, 0, n * sizeof(T)));
+  return 0;
+}
+
+bool is_alias(int k) { return k == GACER_OP_FLATTEN || k == GACER_OP_DROPOUT || k == GACER_OP_CONCAT; }
+
+// ------------------------------------------------------------------------
+// registration: validation + shape inference + fusion + packing
+// ------------------------------------------------------------------------
+int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
+  const int n = g->n_ops;
+  if (n <= 0 || !g->ops) return set_err(GACER_E_INVALID_ARG, "graph has no ops");
+  if (batch < 1) return set_err(GACER_E_INVALID_ARG, "batch must be >= 1");
+  if (g->dtype != GACER_DTYPE_BF16 && g->dtype != GACER_DTYPE_FP32)
+    return set_err(GACER_E_INVALID_ARG, "unknown dtype %d", g->dtype);
+  if (g->train) return set_err(GACER_E_UNSUPPORTED_OP, "training tenants are not supported in this version");
+  if (g->in_c < 1 || g->in_h < 1 || g->in_w < 1) return set_err(GACER_E_SHAPE, "bad input shape");
+  const bool f32 = g->dtype == GACER_DTYPE_FP32;
+  T.batch = batch;
+  T.dtype = g->dtype;
+  T.n_orig = n;
+  T.in_c = g->in_c; T.in_h = g->in_h; T.in_w = g->in_w;
+  T.in_c_pad = roundup(g->in_c, 8);
+
+  // ---- ids, predecessors, cycles, issue order (SPEC S:56 error set)
+  std::map<int, int> pos;
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    if (o.id < 1) return set_err(GACER_E_INVALID_ARG, "op %d: id must be >= 1", i + 1);
+    if (pos.count(o.id)) return set_err(GACER_E_DUPLICATE_ID, "duplicate op id %d", o.id);
+    pos[o.id] = i;
+  }
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    if (o.n_preds < 0 || (o.n_preds > 0 && !o.preds)) return set_err(GACER_E_INVALID_ARG, "op %d: bad preds", o.id);
+    for (int j = 0; j < o.n_preds; ++j)
+      if (o.preds[j] != 0 && !pos.count(o.preds[j]))
+        return set_err(GACER_E_UNKNOWN_PREDECESSOR, "op %d: unknown predecessor %d", o.id, o.preds[j]);
+  }
+  {  // cycle detection (iterative DFS colouring)
+    std::vector<int> color(n, 0);
+    for (int s0 = 0; s0 < n; ++s0) {
+      if (color[s0]) continue;
+      std::vector<std::pair<int, int>> st{{s0, 0}};
+      color[s0] = 1;
+      while (!st.empty()) {
+        auto& [v, j] = st.back();
+        const gacer_op_desc& o = g->ops[v];
+        if (j < o.n_preds) {
+          const int pid = o.preds[j++];
+          if (pid == 0) continue;
+          const int u = pos[pid];
+          if (color[u] == 1) return set_err(GACER_E_CYCLE, "dependency cycle through op %d", g->ops[u].id);
+          if (color[u] == 0) { color[u] = 1; st.push_back({u, 0}); }
+        } else {
+          color[v] = 2;
+          st.pop_back();
+        }
+      }
+    }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < g->ops[i].n_preds; ++j) {
+      const int pid = g->ops[i].preds[j];
+      if (pid != 0 && pos[pid] >= i)
+        return set_err(GACER_E_INVALID_ARG, "op %d: predecessor %d is not earlier in issue order", g->ops[i].id, pid);
+    }
+
+  // ---- shape inference; tensors
+  T.tensors.clear();
+  Tensor tin;
+  tin.C = g->in_c; tin.H = g->in_h; tin.W = g->in_w; tin.buf = -1; tin.ldc = T.in_c_pad;
+  T.tensors.push_back(tin);
+  T.orig_kind.assign(n, 0);
+  T.orig_out_c.assign(n, 0);
+  T.orig_tensor.assign(n, -1);
+  std::vector<std::vector<int>> consumers(n + 1);  // by original op (index+1; 0 = input) -> consumer op idx
+  auto tens_of = [&](int pid) { return pid == 0 ? 0 : T.orig_tensor[pos[pid]]; };
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    T.orig_kind[i] = o.kind;
+    auto need_preds = [&](int k) -> int {
+      if (o.n_preds != k) return set_err(GACER_E_INVALID_ARG, "op %d: expected %d predecessors", o.id, k);
+      return 0;
+    };
+    int rc = 0;
+    switch (o.kind) {
+      case GACER_OP_ADD: rc = need_preds(2); break;
+      case GACER_OP_CONCAT: if (o.n_preds < 1) rc = set_err(GACER_E_INVALID_ARG, "concat needs preds"); break;
+      case GACER_OP_CONV2D: case GACER_OP_LINEAR: case GACER_OP_MAXPOOL: case GACER_OP_AVGPOOL:
+      case GACER_OP_GAP: case GACER_OP_BN: case GACER_OP_RELU: case GACER_OP_RELU6:
+      case GACER_OP_FLATTEN: case GACER_OP_DROPOUT: rc = need_preds(1); break;
+      default: rc = set_err(GACER_E_UNSUPPORTED_OP, "op %d: unknown kind %d", o.id, o.kind);
+    }
+    if (rc) return rc;
+    for (int j = 0; j < o.n_preds; ++j) consumers[o.preds[j] == 0 ? 0 : pos[o.preds[j]] + 1].push_back(i);
+    const Tensor& x = T.tensors[tens_of(o.preds[0])];
+    Tensor y;
+    y.producer_orig = i;
+    switch (o.kind) {
+      case GACER_OP_CONV2D: {
+        if (o.c_in != x.C) return set_err(GACER_E_SHAPE, "op %d: c_in %d != input channels %d", o.id, o.c_in, x.C);
+        if (o.kh < 1 || o.kw < 1 || o.stride < 1 || o.pad_h < 0 || o.pad_w < 0 || o.groups < 1 || o.c_out < 1)
+          return set_err(GACER_E_INVALID_ARG, "op %d: bad conv params", o.id);
+        if (o.c_in % o.groups || o.c_out % o.groups) return set_err(GACER_E_SHAPE, "op %d: groups", o.id);
+        if (o.groups != 1 && !(o.groups == o.c_in && o.c_in == o.c_out))
+          return set_err(GACER_E_UNSUPPORTED_OP, "op %d: grouped conv with 1 < groups < C", o.id);
+        if (!o.weight) return set_err(GACER_E_INVALID_ARG, "op %d: missing weight", o.id);
+        y.C = o.c_out;
+        y.H = (x.H + 2 * o.pad_h - o.kh) / o.stride + 1;
+        y.W = (x.W + 2 * o.pad_w - o.kw) / o.stride + 1;
+        if (y.H < 1 || y.W < 1) return set_err(GACER_E_SHAPE, "op %d: empty output", o.id);
+        T.orig_out_c[i] = o.c_out;
+        break;
+      }
+      case GACER_OP_LINEAR:
+        if (o.c_in != x.C * x.H * x.W)
+          return set_err(GACER_E_SHAPE, "op %d: linear c_in %d != %d", o.id, o.c_in, x.C * x.H * x.W);
+        if (!o.weight || o.c_out < 1) return set_err(GACER_E_INVALID_ARG, "op %d: linear params", o.id);
+        y.C = o.c_out; y.H = 1; y.W = 1;
+        T.orig_out_c[i] = o.c_out;
+        break;
+      case GACER_OP_MAXPOOL: case GACER_OP_AVGPOOL:
+        if (o.kh < 1 || o.kw < 1 || o.stride < 1 || o.pad_h < 0 || o.pad_w < 0)
+          return set_err(GACER_E_INVALID_ARG, "op %d: bad pool params", o.id);
+        y.C = x.C;
+        y.H = (x.H + 2 * o.pad_h - o.kh) / o.stride + 1;
+        y.W = (x.W + 2 * o.pad_w - o.kw) / o.stride + 1;
+        if (y.H < 1 || y.W < 1) return set_err(GACER_E_SHAPE, "op %d: empty output", o.id);
+        T.orig_out_c[i] = x.C;
+        break;
+      case GACER_OP_GAP:
+        y.C = x.C; y.H = 1; y.W = 1; T.orig_out_c[i] = x.C;
+        break;
+      case GACER_OP_BN:
+        if (o.c_out != 0 && o.c_out != x.C) return set_err(GACER_E_SHAPE, "op %d: bn channels", o.id);
+        if (!o.bn_gamma || !o.bn_beta || !o.bn_mean || !o.bn_var)
+          return set_err(GACER_E_INVALID_ARG, "op %d: missing BN params", o.id);
+        y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;
+        break;
+      case GACER_OP_RELU: case GACER_OP_RELU6: case GACER_OP_DROPOUT:
+        y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;
+        break;
+      case GACER_OP_FLATTEN:
+        y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;   // data unchanged (NHWC storage)
+        break;
+      case GACER_OP_ADD: {
+        const Tensor& b = T.tensors[tens_of(o.preds[1])];
+        if (b.C != x.C || b.H != x.H || b.W != x.W) return set_err(GACER_E_SHAPE, "op %d: add shapes", o.id);
+        y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;
+        break;
+      }
+      case GACER_OP_CONCAT: {
+        int c = 0;
+        for (int j = 0; j < o.n_preds; ++j) {
+          const Tensor& b = T.tensors[tens_of(o.preds[j])];
+          if (b.H != x.H || b.W != x.W) return set_err(GACER_E_SHAPE, "op %d: concat spatial sizes", o.id);
+          c += b.C;
+        }
+        y.C = c; y.H = x.H; y.W = x.W; T.orig_out_c[i] = c;
+        break;
+      }
+    }
+    if (o.kind == GACER_OP_FLATTEN || o.kind == GACER_OP_DROPOUT) {
+      T.orig_tensor[i] = tens_of(o.preds[0]);  // alias
+    } else {
+      T.orig_tensor[i] = static_cast<int>(T.tensors.size());
+      T.tensors.push_back(y);
+    }
+  }
+
+  // effective consumers: look through flatten / dropout aliases
+  std::function<void(int, std::vector<int>&)> eff;
+  eff = [&](int node, std::vector<int>& out) {  // node: orig index + 1 (0 = input)
+    for (int c : consumers[node]) {
+      const int k = g->ops[c].kind;
+      if (k == GACER_OP_FLATTEN || k == GACER_OP_DROPOUT) eff(c + 1, out);
+      else out.push_back(c);
+    }
+  };
+  auto single_consumer = [&](int orig) -> int {
+    std::vector<int> cs;
+    eff(orig + 1, cs);
+    return cs.size() == 1 ? cs[0] : -1;
+  };
+  const int last_op = n - 1;
+  // the graph output is the last op's tensor; it may not be fused further
+  const int out_tensor = T.orig_tensor[last_op];
+
+  // ---- fusion
+  T.orig_fused.assign(n, -1);
+  std::vector<char> taken(n, 0);
+  T.fops.clear();
+  for (int i = 0; i < n; ++i) {
+    if (taken[i]) continue;
+    const gacer_op_desc& o = g->ops[i];
+    if (is_alias(o.kind)) continue;
+    FusedOp F;
+    F.head = i;
+    F.members = {i};
+    taken[i] = 1;
+    F.in_t = tens_of(o.preds[0]);
+    int tail = i;
+    auto try_extend = [&](bool allow_bn, bool allow_add) {
+      bool has_bn = false, has_add = false;
+      for (;;) {
+        if (T.orig_tensor[tail] == out_tensor) break;
+        const int c = single_consumer(tail);
+        if (c < 0 || taken[c]) break;
+        const gacer_op_desc& co = g->ops[c];
+        if (co.kind == GACER_OP_BN && allow_bn && !has_bn && !has_add) {
+          has_bn = true;
+        } else if (co.kind == GACER_OP_ADD && allow_add && !has_add) {
+          const int a = tens_of(co.preds[0]), b = tens_of(co.preds[1]);
+          const int mine = T.orig_tensor[tail];
+          const int other = (a == mine) ? b : a;
+          if (a == b || other == 0) break;  // x + x or a skip from the raw input: not fused
+          F.skip_t = other;
+          has_add = true;
+        } else if (co.kind == GACER_OP_RELU || co.kind == GACER_OP_RELU6) {
+          F.act = co.kind == GACER_OP_RELU ? ACT_RELU : ACT_RELU6;
+          F.members.push_back(c);
+          taken[c] = 1;
+          tail = c;
+          break;
+        } else {
+          break;
+        }
+        F.members.push_back(c);
+        taken[c] = 1;
+        tail = c;
+      }
+    };
+    switch (o.kind) {
+      case GACER_OP_CONV2D: {
+        const bool dw = o.groups > 1;
+        F.kind = f32 ? (dw ? DK_DW : DK_SIMT_GEMM) : (dw ? DK_DW : DK_GEMM);
+        try_extend(true, true);
+        break;
+      }
+      case GACER_OP_LINEAR:
+        F.kind = f32 ? DK_SIMT_GEMM : DK_GEMM;
+        try_extend(false, false);
+        break;
+      case GACER_OP_MAXPOOL: F.kind = DK_MAXPOOL; break;
+      case GACER_OP_AVGPOOL: F.kind = DK_AVGPOOL; F.cip = (o.flags & GACER_FLAG_COUNT_INCLUDE_PAD) != 0; break;
+      case GACER_OP_GAP: F.kind = DK_GAP; break;
+      case GACER_OP_ADD: {
+        F.kind = DK_ELTWISE;
+        F.skip_t = tens_of(o.preds[1]);
+        try_extend(false, false);
+        break;
+      }
+      case GACER_OP_RELU: case GACER_OP_RELU6:
+        F.kind = DK_ELTWISE;
+        F.act = o.kind == GACER_OP_RELU ? ACT_RELU : ACT_RELU6;
+        break;
+      case GACER_OP_BN:
+        return set_err(GACER_E_UNSUPPORTED_OP, "op %d: BatchNorm not preceded by a fusable conv", o.id);
+      default:
+        return set_err(GACER_E_UNSUPPORTED_OP, "op %d: kind %d not lowered", o.id, o.kind);
+    }
+    F.last = tail;
+    F.out_t = T.orig_tensor[tail];
+    const int fi = static_cast<int>(T.fops.size());
+    for (int m : F.members) T.orig_fused[m] = fi;
+    T.fops.push_back(std::move(F));
+  }
+  // order fused ops by their last member (topological: see DESIGN.md)
+  {
+    std::vector<int> idx(T.fops.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<int>(i);
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return T.fops[a].last < T.fops[b].last; });
+    std::vector<FusedOp> sorted;
+    std::vector<int> remap(idx.size());
+    for (size_t i = 0; i < idx.size(); ++i) { remap[idx[i]] = static_cast<int>(i); sorted.push_back(std::move(T.fops[idx[i]])); }
+    T.fops = std::move(sorted);
+    for (int& f : T.orig_fused) if (f >= 0) f = remap[f];
+  }
+  for (size_t fi = 0; fi < T.fops.size(); ++fi) T.tensors[T.fops[fi].out_t].writers.push_back(static_cast<int>(fi));
+
+  // ---- storage: user output, concat slices, own buffers
+  T.out_t = out_tensor;
+  {
+    Tensor& ot = T.tensors[out_tensor];
+    if (ot.producer_orig >= 0 && g->ops[ot.producer_orig].kind == GACER_OP_CONCAT)
+      return set_err(GACER_E_UNSUPPORTED_OP, "graph output may not be a concat");
+    if (ot.writers.empty()) return set_err(GACER_E_UNSUPPORTED_OP, "graph output is the raw input");
+    ot.buf = -2;
+    ot.coff = 0;
+    T.out_features = ot.C * ot.H * ot.W;   // float32 NHWC [B][H][W][C] ([B][C] when 1x1)
+    ot.ldc = ot.C;
+  }
+  // concat slices: outermost first (reverse issue order)
+  for (int i = n - 1; i >= 0; --i) {
+    if (g->ops[i].kind != GACER_OP_CONCAT) continue;
+    const int ct = T.orig_tensor[i];
+    Tensor& C = T.tensors[ct];
+    if (C.buf == -1 && !C.sliced) {
+      C.buf = static_cast<int>(T.bufs.size());
+      T.bufs.push_back(nullptr);
+      C.ldc = C.C;
+      C.coff = 0;
+    }
+    int off = 0;
+    for (int j = 0; j < g->ops[i].n_preds; ++j) {
+      const int pt = tens_of(g->ops[i].preds[j]);
+      Tensor& P = T.tensors[pt];
+      std::vector<int> cs;
+      eff(P.producer_orig + 1, cs);
+      if (pt == 0 || cs.size() != 1 || P.sliced || P.buf == -2)
+        return set_err(GACER_E_UNSUPPORTED_OP, "concat op %d: input %d must be an op output consumed only by the concat",
+                       g->ops[i].id, g->ops[i].preds[j]);
+      P.buf = C.buf;
+      P.coff = C.coff + off;
+      P.ldc = C.ldc;
+      P.sliced = true;
+      off += P.C;
+    }
+  }
+  // concat tensor writers = writers of its slices (recursively)
+  for (int i = 0; i < n; ++i) {
+    if (g->ops[i].kind != GACER_OP_CONCAT) continue;
+    Tensor& C = T.tensors[T.orig_tensor[i]];
+    for (int j = 0; j < g->ops[i].n_preds; ++j) {
+      const Tensor& P = T.tensors[tens_of(g->ops[i].preds[j])];
+      C.writers.insert(C.writers.end(), P.writers.begin(), P.writers.end());
+    }
+  }
+  for (size_t t = 1; t < T.tensors.size(); ++t) {
+    Tensor& X = T.tensors[t];
+    if (X.buf == -1 && !X.sliced && !X.writers.empty()) {
+      X.buf = static_cast<int>(T.bufs.size());
+      T.bufs.push_back(nullptr);
+      X.ldc = X.C;
+      X.coff = 0;
+    }
+  }
+  T.buf_bytes.assign(T.bufs.size(), 0);
+  const int elem = f32 ? 4 : 2;
+  for (size_t t = 1; t < T.tensors.size(); ++t) {
+    const Tensor& X = T.tensors[t];
+    if (X.buf >= 0 && !X.sliced)
+      T.buf_bytes[X.buf] = std::max(T.buf_bytes[X.buf], static_cast<size_t>(batch) * X.H * X.W * X.ldc * elem);
+  }
+
+  // ---- per fused op geometry + packing
+  T.flops = 0;
+  for (FusedOp& F : T.fops) {
+    const gacer_op_desc& o = g->ops[F.head];
+    const Tensor& X = T.tensors[F.in_t];
+    const Tensor& Y = T.tensors[F.out_t];
+    F.Cin = X.C; F.H = X.H; F.W = X.W;
+    F.Cout = Y.C; F.Ho = Y.H; F.Wo = Y.W;
+    if (F.in_t != 0 && X.C % 8 && F.kind != DK_SIMT_GEMM)
+      return set_err(GACER_E_UNSUPPORTED_OP, "op %d: channel count %d not a multiple of 8", o.id, X.C);
+    if ((Y.coff % 8) || (Y.ldc % 8 && Y.buf != -2)) return set_err(GACER_E_UNSUPPORTED_OP, "op %d: unaligned concat slice", o.id);
+    if (F.skip_t >= 0) {
+      const Tensor& Sk = T.tensors[F.skip_t];
+      if (Sk.C != Y.C || Sk.H != Y.H || Sk.W != Y.W) return set_err(GACER_E_SHAPE, "op %d: residual shape", o.id);
+    }
+    // folded scale / bias (fp64 -> fp32), SURVEY Q3
+    auto fold = [&](int cout, const float* conv_bias) {
+      F.scale.assign(cout, 1.0f);
+      F.bias.assign(cout, 0.0f);
+      const gacer_op_desc* bn = nullptr;
+      for (int m : F.members) if (g->ops[m].kind == GACER_OP_BN) bn = &g->ops[m];
+      for (int c = 0; c < cout; ++c) {
+        const double cb = conv_bias ? conv_bias[c] : 0.0;
+        if (bn) {
+          const double s = static_cast<double>(bn->bn_gamma[c]) /
+                           std::sqrt(static_cast<double>(bn->bn_var[c]) + static_cast<double>(bn->bn_eps));
+          F.scale[c] = static_cast<float>(s);
+          F.bias[c] = static_cast<float>(static_cast<double>(bn->bn_beta[c]) - static_cast<double>(bn->bn_mean[c]) * s + cb * s);
+        } else {
+          F.bias[c] = static_cast<float>(cb);
+        }
+      }
+    };
+    const float* cbias = (o.flags & GACER_FLAG_BIAS) ? o.bias : nullptr;
+    if ((o.flags & GACER_FLAG_BIAS) && !o.bias) return set_err(GACER_E_INVALID_ARG, "op %d: missing bias", o.id);
+    const int B = batch;
+    if (F.kind == DK_GEMM || F.kind == DK_SIMT_GEMM) {
+      const bool lin = o.kind == GACER_OP_LINEAR;
+      if (lin) { F.kh = X.H; F.kw = X.W; F.stride = 1; F.ph = F.pw = 0; }
+      else { F.kh = o.kh; F.kw = o.kw; F.stride = o.stride; F.ph = o.pad_h; F.pw = o.pad_w; }
+      F.flops = 2.0 * B * F.Ho * F.Wo * F.Cout * static_cast<double>(F.Cin) * F.kh * F.kw;
+      fold(F.Cout, cbias);
+      // weights in (tap, channel) K order; linear weights are NCHW-flatten ordered (c, h, w)
+      auto wval = [&](int co, int c, int r, int s) -> float {
+        if (lin) return o.weight[static_cast<size_t>(co) * o.c_in + (static_cast<size_t>(c) * X.H + r) * X.W + s];
+        return o.weight[((static_cast<size_t>(co) * o.c_in + c) * o.kh + r) * o.kw + s];
+      };
+      if (F.kind == DK_SIMT_GEMM) {
+        F.cread = F.Cin;
+        F.K = F.kh * F.kw * F.cread;
+        F.M = B * F.Ho * F.Wo; F.N = F.Cout;
+        F.bm = 64; F.bn = 64;
+        F.tiles_m = cdiv(F.M, F.bm); F.tiles_n = cdiv(F.Cout, F.bn);
+        F.w_f32.assign(static_cast<size_t>(F.Cout) * F.K, 0.0f);
+        for (int co = 0; co < F.Cout; ++co)
+          for (int r = 0; r < F.kh; ++r)
+            for (int s = 0; s < F.kw; ++s)
+              for (int c = 0; c < F.Cin; ++c)
+                F.w_f32[static_cast<size_t>(co) * F.K + (r * F.kw + s) * F.cread + c] = wval(co, c, r, s);
+      } else {
+        F.cread = roundup(F.Cin, 8);
+        if (F.in_t == 0 && F.cread > X.ldc) return set_err(GACER_E_UNSUPPORTED_OP, "input padding");
+        F.K = F.kh * F.kw * F.cread;
+        F.Kpad = roundup(F.K, BK);
+        F.nkb = F.Kpad / BK;
+        F.swap = lin && X.ldc == X.C && F.skip_t < 0;
+        size_t rows;
+        if (F.swap) {
+          F.rows_are_pixels = false;
+          F.M = F.Cout; F.N = B;
+          F.tiles_m = cdiv(F.Cout, BM);
+          F.bn = std::min(BN_MAX, roundup(B, 16));
+          F.tiles_n = cdiv(B, F.bn);
+          rows = static_cast<size_t>(F.tiles_m) * BM;
+        } else {
+          F.M = B * F.Ho * F.Wo; F.N = F.Cout;
+          F.tiles_m = cdiv(F.M, BM);
+          F.bn = F.Cout >= BN_MAX ? BN_MAX : roundup(F.Cout, 16);
+          F.tiles_n = cdiv(F.Cout, F.bn);
+          rows = static_cast<size_t>(F.tiles_n) * F.bn;
+        }
+        F.bm = BM;
+        // split-K: a function of the layer shape only (same in every mode/plan)
+        const int tiles = F.tiles_m * F.tiles_n;
+        int sk = 1;
+        while (sk < 16 && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 4) sk *= 2;
+        F.split_k = sk;
+        F.w_bf16.assign(rows * F.Kpad, 0);
+        for (int co = 0; co < F.Cout; ++co)
+          for (int r = 0; r < F.kh; ++r)
+            for (int s = 0; s < F.kw; ++s)
+              for (int c = 0; c < F.Cin; ++c)
+                F.w_bf16[static_cast<size_t>(co) * F.Kpad + (r * F.kw + s) * F.cread + c] =
+                    f32_to_bf16_rne(wval(co, c, r, s));
+        F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
+        F.bias.resize(roundup(F.Cout, 8) + 8, 0.0f);
+      }
+    } else if (F.kind == DK_DW) {
+      F.kh = o.kh; F.kw = o.kw; F.stride = o.stride; F.ph = o.pad_h; F.pw = o.pad_w;
+      F.flops = 2.0 * B * F.Ho * F.Wo * F.Cout * F.kh * F.kw;
+      fold(F.Cout, cbias);
+      F.w_f32.assign(static_cast<size_t>(F.kh) * F.kw * F.Cout, 0.0f);
+      for (int c = 0; c < F.Cout; ++c)
+        for (int r = 0; r < F.kh; ++r)
+          for (int s = 0; s < F.kw; ++s) {
+            const float w = o.weight[(static_cast<size_t>(c) * o.kh + r) * o.kw + s];
+            F.w_f32[(r * F.kw + s) * F.Cout + c] = f32 ? w : f32_to_bf16_round_trip(w);
+          }
+      F.M = B * F.Ho * F.Wo;
+    } else if (F.kind == DK_MAXPOOL || F.kind == DK_AVGPOOL) {
+      F.kh = o.kh; F.kw = o.kw; F.stride = o.stride; F.ph = o.pad_h; F.pw = o.pad_w;
+      F.M = B * F.Ho * F.Wo;
+    } else if (F.kind == DK_GAP) {
+      F.M = B;
+    } else if (F.kind == DK_ELTWISE) {
+      F.M = B * F.Ho * F.Wo;
+      fold(F.Cout, nullptr);
+    }
+    if (F.kind != DK_GEMM && F.kind != DK_SIMT_GEMM) {
+      F.bn = std::min(64, pow2ceil(roundup(F.Cout, 8)));
+      const int G = F.bn / 8;
+      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : CC_TASKS_PER_THREAD * (NTHREADS / G);
+      F.tiles_m = cdiv(F.M, F.bm);
+      F.tiles_n = cdiv(F.Cout, F.bn);
+      F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
+      F.bias.resize(roundup(F.Cout, 8) + 8, 0.0f);
+    }
+    const double e = elem;
+    F.bytes = (static_cast<double>(B) * F.H * F.W * F.Cin + static_cast<double>(B) * F.Ho * F.Wo * F.Cout) * e +
+              (F.w_bf16.size() * 2.0 + F.w_f32.size() * 4.0);
+    T.flops += F.flops;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------
+// device residency of a tenant and the global op table
+// ------------------------------------------------------------------------
+namespace {
+
+size_t elem_size(const Tenant& T) { return T.dtype == GACER_DTYPE_FP32 ? 4 : 2; }
+
+char* tensor_addr(const Tenant& T, int t) {
+  const Tensor& X = T.tensors[t];
+  if (X.buf == -2) return static_cast<char*>(T.out_dev);  // float32 [B][features]
+  char* base = X.buf == -1 ? const_cast<char*>(static_cast<const char*>(T.in_dev))
+                           : static_cast<char*>(T.bufs[X.buf]);
+  if (!base) return nullptr;
+  return base + static_cast<size_t>(X.coff) * elem_size(T);
+}
+
+int upload_tenant(Tenant& T) {
+  for (size_t b = 0; b < T.bufs.size(); ++b)
+    if (T.buf_bytes[b]) CUDA_TRY(cudaMalloc(&T.bufs[b], T.buf_bytes[b]));
+  for (FusedOp& F : T.fops) {
+    if (!F.w_bf16.empty()) {
+      CUDA_TRY(cudaMalloc(&F.d_w, F.w_bf16.size() * 2));
+      CUDA_TRY(cudaMemcpy(F.d_w, F.w_bf16.data(), F.w_bf16.size() * 2, cudaMemcpyHostToDevice));
+    } else if (!F.w_f32.empty()) {
+      CUDA_TRY(cudaMalloc(&F.d_w, F.w_f32.size() * 4));
+      CUDA_TRY(cudaMemcpy(F.d_w, F.w_f32.data(), F.w_f32.size() * 4, cudaMemcpyHostToDevice));
+    }
+    if (!F.scale.empty()) {
+      if (int rc = dev_upload(&F.d_scale, F.scale.data(), F.scale.size())) return rc;
+      if (int rc = dev_upload(&F.d_bias, F.bias.data(), F.bias.size())) return rc;
+    }
+    if (F.kind == DK_GEMM && F.split_k > 1) {
+      const size_t tiles = static_cast<size_t>(F.tiles_m) * F.tiles_n;
+      CUDA_TRY(cudaMalloc(&F.d_partial, tiles * F.split_k * BM * F.bn * sizeof(float)));
+      if (int rc = dev_upload<uint32_t>(&F.d_tile_cnt, nullptr, tiles)) return rc;
+    }
+    // host copies of the packed weights are no longer needed
+    std::vector<uint16_t>().swap(F.w_bf16);
+    std::vector<float>().swap(F.w_f32);
+  }
+  return 0;
+}
+
+void free_tenant(Tenant& T) {
+  for (void* p : T.bufs) if (p) cudaFree(p);
+  for (FusedOp& F : T.fops) {
+    for (void* p : {static_cast<void*>(F.d_w), static_cast<void*>(F.d_scale), static_cast<void*>(F.d_bias),
+                    static_cast<void*>(F.d_partial), static_cast<void*>(F.d_tile_cnt)})
+      if (p) cudaFree(p);
+  }
+}
+
+OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
+  OpDev d;
+  std::memset(&d, 0, sizeof d);
+  const Tensor& X = T.tensors[F.in_t];
+  const Tensor& Y = T.tensors[F.out_t];
+  const bool f32 = T.dtype == GACER_DTYPE_FP32;
+  d.kind = F.kind;
+  d.tenant = tenant_id;
+  d.act = F.act;
+  d.out_f32 = (Y.buf == -2 || f32) ? 1 : 0;
+  d.f32 = f32 ? 1 : 0;
+  d.swap = F.swap ? 1 : 0;
+  d.cip = F.cip ? 1 : 0;
+  d.has_skip = F.skip_t >= 0 ? 1 : 0;
+  d.in = tensor_addr(T, F.in_t);
+  d.B = T.batch; d.H = F.H; d.W = F.W;
+  d.C = (F.kind == DK_GEMM) ? F.cread : F.Cin;
+  d.ldi = X.ldc;
+  d.out = tensor_addr(T, F.out_t);
+  d.Ho = F.Ho; d.Wo = F.Wo; d.Cout = F.Cout; d.ldo = Y.ldc;
+  if (F.skip_t >= 0) { d.skip = tensor_addr(T, F.skip_t); d.lds = T.tensors[F.skip_t].ldc; }
+  d.kh = F.kh; d.kw = F.kw; d.stride = F.stride; d.ph = F.ph; d.pw = F.pw;
+  d.M = F.M; d.N = F.N; d.K = F.K; d.Kpad = F.Kpad;
+  d.tiles_m = F.tiles_m; d.tiles_n = F.tiles_n; d.bm = F.bm; d.bn = F.bn;
+  d.split_k = F.split_k; d.nkb = F.nkb;
+  d.wt = F.d_w;
+  d.ldw = (F.kind == DK_GEMM) ? F.Kpad : F.K;
+  if (F.swap) { d.act_b = d.in; d.ldb = F.H * F.W * X.ldc; }
+  d.scale = F.d_scale; d.bias = F.d_bias;
+  d.partial = F.d_partial; d.tile_cnt = F.d_tile_cnt;
+  return d;
+}
+
+int rebuild_op_table() {
+  S.h_ops.clear();
+  for (size_t t = 0; t < S.tenants.size(); ++t) {
+    Tenant& T = S.tenants[t];
+    T.op_base = static_cast<int>(S.h_ops.size());
+    for (const FusedOp& F : T.fops) S.h_ops.push_back(make_opdev(T, static_cast<int>(t), F));
+  }
+  if (S.host_only) return 0;
+  return dev_upload(&S.d_ops, S.h_ops.data(), S.h_ops.size());
+}
+
+// ------------------------------------------------------------------------
+// plan compilation (Eq. 5 chunks -> tile ranges; Eq. 6/7 -> clusters)
+// ------------------------------------------------------------------------
+struct ChunkRange {
+  int m0, m1, n0, n1;  // tile ranges
+  int counter;
+  uint32_t n_items;
+};
+
+int cluster_of_orig(const Plan& P, int t, int orig0) {  // orig0: 0-based op index
+  if (P.cuts.empty()) return 0;
+  int k = 0;
+  for (int c : P.cuts[t]) if (c < orig0 + 1) ++k;  // cut p = boundary after op p
+  return k;
+}
+
+int compile_plan(Plan& P) {
+  const int nt = static_cast<int>(S.tenants.size());
+  P.n_clusters = (P.cuts.empty() ? 0 : static_cast<int>(P.cuts[0].size())) + 1;
+  P.items.clear(); P.deps.clear(); P.queue.clear(); P.segs.clear();
+  P.cluster_total.assign(P.n_clusters, 0);
+  P.fop_cluster.assign(nt, {});
+  std::vector<std::vector<std::vector<ChunkRange>>> cr(nt);
+  int counter = 0;
+  for (int t = 0; t < nt; ++t) {
+    const Tenant& T = S.tenants[t];
+    cr[t].resize(T.fops.size());
+    P.fop_cluster[t].resize(T.fops.size());
+    for (size_t f = 0; f < T.fops.size(); ++f) {
+      const FusedOp& F = T.fops[f];
+      P.fop_cluster[t][f] = cluster_of_orig(P, t, F.last);
+      const Chunking* ch = nullptr;
+      for (int m : F.members) {
+        auto it = P.chunks.find({t, m});
+        if (it == P.chunks.end()) continue;
+        if (ch && (ch->axis != it->second.axis || ch->sizes != it->second.sizes))
+          return set_err(GACER_E_INVALID_ARG, "tenant %d: fused ops %d and %d carry different chunkings", t,
+                         F.head + 1, m + 1);
+        ch = &it->second;
+      }
+      const int split = (F.kind == DK_GEMM) ? F.split_k : 1;
+      std::vector<ChunkRange>& ranges = cr[t][f];
+      if (!ch) {
+        ranges.push_back({0, F.tiles_m, 0, F.tiles_n, 0, 0});
+      } else {
+        // which tile axis carries the split, and units per tile along it
+        bool on_m;
+        long long unit;  // rows (or channels) per chunk unit
+        int tsz;
+        if (ch->axis == GACER_AXIS_BATCH) {
+          if (F.rows_are_pixels) { on_m = true; unit = (F.kind == DK_GAP) ? 1 : static_cast<long long>(F.Ho) * F.Wo; tsz = F.bm; }
+          else { on_m = false; unit = 1; tsz = F.bn; }
+        } else {
+          if (F.rows_are_pixels) { on_m = false; unit = 1; tsz = F.bn; }
+          else { on_m = true; unit = 1; tsz = BM; }
+        }
+        const int ntiles = on_m ? F.tiles_m : F.tiles_n;
+        long long u = 0;
+        for (int s : ch->sizes) {
+          const long long a = u * unit, b = (u + s) * unit;
+          int t0 = static_cast<int>((a + tsz - 1) / tsz), t1 = static_cast<int>((b + tsz - 1) / tsz);
+          t0 = std::min(t0, ntiles); t1 = std::min(t1, ntiles);
+          if (on_m) ranges.push_back({t0, t1, 0, F.tiles_n, 0, 0});
+          else ranges.push_back({0, F.tiles_m, t0, t1, 0, 0});
+          u += s;
+        }
+      }
+      for (ChunkRange& r : ranges) {
+        r.n_items = static_cast<uint32_t>(std::max(0, r.m1 - r.m0) * std::max(0, r.n1 - r.n0) * split);
+        r.counter = r.n_items ? counter++ : -1;
+      }
+    }
+  }
+  P.n_chunk_counters = counter;
+
+  // items, grouped by (tenant, cluster) segment, in issue order
+  std::vector<std::vector<std::vector<int32_t>>> seg_items(nt, std::vector<std::vector<int32_t>>(P.n_clusters));
+  for (int t = 0; t < nt; ++t) {
+    const Tenant& T = S.tenants[t];
+    for (size_t f = 0; f < T.fops.size(); ++f) {
+      const FusedOp& F = T.fops[f];
+      const int k = P.fop_cluster[t][f];
+      const int split = (F.kind == DK_GEMM) ? F.split_k : 1;
+      for (const ChunkRange& r : cr[t][f]) {
+        if (!r.n_items) continue;
+        for (int mt = r.m0; mt < r.m1; ++mt)
+          for (int ntile = r.n0; ntile < r.n1; ++ntile) {
+            // samples this tile needs
+            int s_lo, s_hi;
+            if (F.rows_are_pixels) {
+              const long long R = (F.kind == DK_GAP) ? 1 : static_cast<long long>(F.Ho) * F.Wo;
+              const long long r0 = static_cast<long long>(mt) * F.bm;
+              const long long r1 = std::min<long long>(F.M, r0 + F.bm);
+              s_lo = static_cast<int>(r0 / R);
+              s_hi = static_cast<int>((r1 - 1) / R);
+            } else {
+              s_lo = ntile * F.bn;
+              s_hi = std::min(T.batch, (ntile + 1) * F.bn) - 1;
+            }
+            std::set<int> dset;
+            std::vector<Dep> dl;
+            for (int tin : {F.in_t, F.skip_t}) {
+              if (tin < 0) continue;
+              for (int w : T.tensors[tin].writers) {
+                const FusedOp& Wf = T.fops[w];
+                int wm0 = 0, wm1 = Wf.tiles_m, wn0 = 0, wn1 = Wf.tiles_n;
+                if (Wf.rows_are_pixels) {
+                  const long long R = (Wf.kind == DK_GAP) ? 1 : static_cast<long long>(Wf.Ho) * Wf.Wo;
+                  wm0 = static_cast<int>((s_lo * R) / Wf.bm);
+                  wm1 = static_cast<int>(((s_hi + 1) * R - 1) / Wf.bm) + 1;
+                } else {
+                  wn0 = s_lo / Wf.bn;
+                  wn1 = s_hi / Wf.bn + 1;
+                }
+                for (const ChunkRange& q : cr[t][w]) {
+                  if (!q.n_items) continue;
+                  if (q.m1 <= wm0 || q.m0 >= wm1 || q.n1 <= wn0 || q.n0 >= wn1) continue;
+                  if (dset.insert(q.counter).second) dl.push_back({q.counter, q.n_items});
+                }
+              }
+            }
+            const int dep_begin = static_cast<int>(P.deps.size());
+            P.deps.insert(P.deps.end(), dl.begin(), dl.end());
+            for (int ks = 0; ks < split; ++ks) {
+              Item it;
+              it.op = T.op_base + static_cast<int>(f);
+              it.mt = mt; it.nt = ntile; it.ks = ks;
+              it.dep_begin = dep_begin;
+              it.dep_count = static_cast<int>(dl.size());
+              it.chunk = r.counter;
+              it.cluster = k;
+              seg_items[t][k].push_back(static_cast<int32_t>(P.items.size()));
+              P.items.push_back(it);
+              P.cluster_total[k] += 1;
+            }
+          }
+      }
+    }
+  }
+  P.segs.assign(static_cast<size_t>(nt) * P.n_clusters, Seg{0, 0});
+  for (int t = 0; t < nt; ++t)
+    for (int k = 0; k < P.n_clusters; ++k) {
+      Seg& sg = P.segs[static_cast<size_t>(t) * P.n_clusters + k];
+      sg.begin = static_cast<int>(P.queue.size());
+      sg.size = static_cast<int>(seg_items[t][k].size());
+      P.queue.insert(P.queue.end(), seg_items[t][k].begin(), seg_items[t][k].end());
+    }
+  return 0;
+}
+
+// SM partition: CTA c prefers tenant own[c] (shares proportional to tenant
+// FLOPs, at least one CTA each -- the resource share W of §4.1 l.597-601).
+std::vector<int32_t> make_pref(int grid) {
+  const int nt = static_cast<int>(S.tenants.size());
+  std::vector<double> w(nt);
+  double tot = 0;
+  for (int t = 0; t < nt; ++t) { w[t] = std::max(1.0, S.tenants[t].flops); tot += w[t]; }
+  std::vector<int> own(grid);
+  std::vector<double> got(nt, 0.0);
+  for (int c = 0; c < grid; ++c) {  // largest deficit first (weighted round robin)
+    int best = 0;
+    double bd = -1e300;
+    for (int t = 0; t < nt; ++t) {
+      const double deficit = w[t] / tot * (c + 1) - got[t];
+      if (deficit > bd) { bd = deficit; best = t; }
+    }
+    own[c] = best;
+    got[best] += 1.0;
+  }
+  std::vector<int32_t> pref(static_cast<size_t>(grid) * nt, -1);
+  for (int c = 0; c < grid; ++c) {
+    pref[static_cast<size_t>(c) * nt] = own[c];
+    if (S.opts.partition == GACER_PARTITION_STRICT) continue;
+    for (int j = 1; j < nt; ++j) pref[static_cast<size_t>(c) * nt + j] = (own[c] + j) % nt;
+  }
+  return pref;
+}
+
+int upload_plan() {
+  if (S.host_only) return 0;
+  Plan& P = S.plan;
+  S.grid = S.opts.num_ctas > 0 ? S.opts.num_ctas : S.num_sms;
+  std::vector<int32_t> pref = make_pref(S.grid);
+  const size_t nheads = static_cast<size_t>(S.tenants.size()) * P.n_clusters;
+  int rc;
+  if ((rc = dev_upload(&S.d_items, P.items.data(), P.items.size()))) return rc;
+  if ((rc = dev_upload(&S.d_deps, P.deps.data(), std::max<size_t>(1, P.deps.size())))) return rc;
+  if ((rc = dev_upload(&S.d_queue, P.queue.data(), std::max<size_t>(1, P.queue.size())))) return rc;
+  if ((rc = dev_upload(&S.d_segs, P.segs.data(), P.segs.size()))) return rc;
+  if ((rc = dev_upload(&S.d_pref, pref.data(), pref.size()))) return rc;
+  if ((rc = dev_upload<uint32_t>(&S.d_heads, nullptr, nheads))) return rc;
+  if ((rc = dev_upload<uint32_t>(&S.d_chunk_done, nullptr, std::max(1, P.n_chunk_counters)))) return rc;
+  if ((rc = dev_upload<uint32_t>(&S.d_cluster_done, nullptr, P.n_clusters))) return rc;
+  if ((rc = dev_upload(&S.d_cluster_total, P.cluster_total.data(), P.cluster_total.size()))) return rc;
+  if (!S.d_exit && (rc = dev_upload<uint32_t>(&S.d_exit, nullptr, 1))) return rc;
+  if (!S.d_error && (rc = dev_upload<int32_t>(&S.d_error, nullptr, 1))) return rc;
+  if (S.d_trace) { cudaFree(S.d_trace); S.d_trace = nullptr; }
+  if (S.opts.trace) CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * 6 * sizeof(int64_t)));
+  S.epoch = 0;
+  return 0;
+}
+
+int reset_device_counters() {
+  const Plan& P = S.plan;
+  CUDA_TRY(cudaMemset(S.d_heads, 0, S.tenants.size() * P.n_clusters * sizeof(uint32_t)));
+  CUDA_TRY(cudaMemset(S.d_chunk_done, 0, std::max(1, P.n_chunk_counters) * sizeof(uint32_t)));
+  CUDA_TRY(cudaMemset(S.d_cluster_done, 0, P.n_clusters * sizeof(uint32_t)));
+  CUDA_TRY(cudaMemset(S.d_exit, 0, sizeof(uint32_t)));
+  CUDA_TRY(cudaMemset(S.d_error, 0, sizeof(int32_t)));
+  for (Tenant& T : S.tenants)
+    for (FusedOp& F : T.fops)
+      if (F.d_tile_cnt) CUDA_TRY(cudaMemset(F.d_tile_cnt, 0, sizeof(uint32_t) * F.tiles_m * F.tiles_n));
+  S.epoch = 0;
+  return 0;
+}
+
+int check_ready() {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (S.sticky_cuda) return set_err(GACER_E_CUDA, "sticky CUDA error: %s", g_err.c_str());
+  if (S.host_only) return set_err(GACER_E_STATE, "host-only instance cannot run rounds");
+  if (S.tenants.empty()) return set_err(GACER_E_STATE, "no tenants registered");
+  for (size_t t = 0; t < S.tenants.size(); ++t)
+    if (!S.tenants[t].in_dev || !S.tenants[t].out_dev)
+      return set_err(GACER_E_STATE, "tenant %zu has unbound I/O", t);
+  return 0;
+}
+
+int enqueue_round(cudaStream_t st) {
+  if (int rc = check_ready()) return rc;
+  if (!st) st = S.stream;
+  CUDA_TRY(cudaEventRecord(S.ev0, st));
+  int launches = 0;
+  if (S.mode == GACER_MODE_EXECUTOR) {
+    if (S.epoch >= 0x7FFFFF00u / std::max<uint32_t>(1, 1 + static_cast<uint32_t>(S.plan.items.size()))) {
+      if (int rc = reset_device_counters()) return rc;  // keep epoch*target far from wrap
+    }
+    ExecParams p;
+    std::memset(&p, 0, sizeof p);
+    p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.queue = S.d_queue; p.segs = S.d_segs;
+    p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
+    p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
+    p.error = S.d_error; p.trace = S.d_trace;
+    p.n_tenants = static_cast<int>(S.tenants.size());
+    p.n_clusters = S.plan.n_clusters;
+    p.epoch = ++S.epoch;
+    p.n_heads = p.n_tenants * p.n_clusters;
+    p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
+    CUDA_TRY(launch_executor(p, S.grid, st));
+    launches = 1;
+  } else {
+    const bool ms = S.mode == GACER_MODE_MULTISTREAM;
+    if (ms) {
+      while (S.tstreams.size() < S.tenants.size()) {
+        cudaStream_t s;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        S.tstreams.push_back(s);
+      }
+    }
+    for (size_t t = 0; t < S.tenants.size(); ++t) {
+      cudaStream_t ts = st;
+      if (ms) {
+        ts = S.tstreams[t];
+        CUDA_TRY(cudaStreamWaitEvent(ts, S.ev0, 0));
+      }
+      const Tenant& T = S.tenants[t];
+      for (size_t f = 0; f < T.fops.size(); ++f) {
+        const FusedOp& F = T.fops[f];
+        const int nb = F.tiles_m * F.tiles_n * (F.kind == DK_GEMM ? F.split_k : 1);
+        CUDA_TRY(launch_op(S.d_ops, T.op_base + static_cast<int>(f), F.kind, nb, ts));
+        ++launches;
+      }
+    }
+    if (ms) {
+      for (size_t t = 0; t < S.tenants.size(); ++t) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(e, S.tstreams[t]));
+        CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
+        cudaEventDestroy(e);
+      }
+    }
+  }
+  CUDA_TRY(cudaEventRecord(S.ev1, st));
+  S.last_launches = launches;
+  return 0;
+}
+
+int finish_round() {
+  CUDA_TRY(cudaEventSynchronize(S.ev1));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, S.ev0, S.ev1));
+  S.last_ms = ms;
+  if (S.mode == GACER_MODE_EXECUTOR) {
+    int32_t err = 0;
+    CUDA_TRY(cudaMemcpy(&err, S.d_error, sizeof err, cudaMemcpyDeviceToHost));
+    if (err) {
+      reset_device_counters();
+      return set_err(GACER_E_DEADLOCK, "device watchdog fired (spin budget exceeded)");
+    }
+  }
+  return 0;
+}
+
+void free_plan_device() {
+  for (void* p : {static_cast<void*>(S.d_items), static_cast<void*>(S.d_deps), static_cast<void*>(S.d_queue),
+                  static_cast<void*>(S.d_segs), static_cast<void*>(S.d_pref), static_cast<void*>(S.d_heads),
+                  static_cast<void*>(S.d_chunk_done), static_cast<void*>(S.d_cluster_done),
+                  static_cast<void*>(S.d_cluster_total), static_cast<void*>(S.d_exit),
+                  static_cast<void*>(S.d_error), static_cast<void*>(S.d_trace)})
+    if (p) cudaFree(p);
+  S.d_items = nullptr; S.d_deps = nullptr; S.d_queue = nullptr; S.d_segs = nullptr; S.d_pref = nullptr;
+  S.d_heads = nullptr; S.d_chunk_done = nullptr; S.d_cluster_done = nullptr; S.d_cluster_total = nullptr;
+  S.d_exit = nullptr; S.d_error = nullptr; S.d_trace = nullptr;
+}
+
+}  // namespace
+
+// ========================================================================
+// C ABI
+// ========================================================================
+extern "C" {
+
+int gacer_init(int cuda_device, const gacer_options* opts) {
+  if (S.inited) gacer_shutdown();
+  S = State();
+  if (opts) S.opts = *opts;
+  S.host_only = cuda_device < 0;
+  S.device = cuda_device;
+  S.inited = true;
+  if (!S.host_only) {
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    CUDA_TRY(cudaDeviceGetAttribute(&S.num_sms, cudaDevAttrMultiProcessorCount, cuda_device));
+    int major = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device));
+    if (major != 10) {
+      S.inited = false;
+      return set_err(GACER_E_CUDA, "device %d is sm_%d0, this library is built for sm_100a", cuda_device, major);
+    }
+    CUDA_TRY(configure_kernels());
+    CUDA_TRY(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&S.ev0));
+    CUDA_TRY(cudaEventCreate(&S.ev1));
+  }
+  return GACER_OK;
+}
+
+int gacer_shutdown(void) {
+  if (!S.inited) return GACER_OK;
+  if (!S.host_only) {
+    cudaDeviceSynchronize();
+    for (Tenant& T : S.tenants) free_tenant(T);
+    free_plan_device();
+    if (S.d_ops) cudaFree(S.d_ops);
+    for (cudaStream_t s : S.tstreams) cudaStreamDestroy(s);
+    if (S.stream) cudaStreamDestroy(S.stream);
+    if (S.ev0) cudaEventDestroy(S.ev0);
+    if (S.ev1) cudaEventDestroy(S.ev1);
+  }
+  S = State();
+  return GACER_OK;
+}
+
+int gacer_register_tenant(const gacer_graph* graph, int32_t batch) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (S.sticky_cuda) return set_err(GACER_E_CUDA, "sticky CUDA error");
+  if (!graph) return set_err(GACER_E_INVALID_ARG, "graph is NULL");
+  Tenant T;
+  if (int rc = lower_tenant(graph, batch, T)) return rc;
+  if (!S.host_only) {
+    if (int rc = upload_tenant(T)) { free_tenant(T); return rc; }
+  }
+  S.tenants.push_back(std::move(T));
+  const int id = static_cast<int>(S.tenants.size()) - 1;
+  if (int rc = rebuild_op_table()) return rc;
+  // registration resets the plan to the identity plan
+  S.plan = Plan();
+  if (int rc = compile_plan(S.plan)) return rc;
+  if (int rc = upload_plan()) return rc;
+  return id;
+}
+
+int gacer_get_tenant_info(int tenant, gacer_tenant_info* out) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !out)
+    return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
+  const Tenant& T = S.tenants[tenant];
+  out->n_orig_ops = T.n_orig;
+  out->n_fused_ops = static_cast<int32_t>(T.fops.size());
+  out->batch = T.batch;
+  out->in_c_pad = T.in_c_pad;
+  out->in_h = T.in_h;
+  out->in_w = T.in_w;
+  out->out_features = T.out_features;
+  out->in_bytes = static_cast<int64_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
+  out->out_bytes = static_cast<int64_t>(T.batch) * T.out_features * 4;
+  out->flops = T.flops;
+  return GACER_OK;
+}
+
+int gacer_bind_io(int tenant, const void* input_dev, void* output_dev) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()))
+    return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
+  if (!input_dev || !output_dev) return set_err(GACER_E_INVALID_ARG, "NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(input_dev) | reinterpret_cast<uintptr_t>(output_dev)) & 15)
+    return set_err(GACER_E_INVALID_ARG, "buffers must be 16-byte aligned");
+  S.tenants[tenant].in_dev = input_dev;
+  S.tenants[tenant].out_dev = output_dev;
+  return rebuild_op_table();
+}
+
+int gacer_set_regulation(const gacer_decomposition* dec, const gacer_sync_pointers* sp) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (S.sticky_cuda) return set_err(GACER_E_CUDA, "sticky CUDA error");
+  const int nt = static_cast<int>(S.tenants.size());
+  if (nt == 0) return set_err(GACER_E_STATE, "no tenants registered");
+  Plan P;
+  if (sp) {
+    if (sp->n_tenants != nt) return set_err(GACER_E_INVALID_ARG, "sync_pointers for %d tenants, %d registered", sp->n_tenants, nt);
+    if (sp->n_pointers < 0) return set_err(GACER_E_POINTER_COUNT_MISMATCH, "negative pointer count");
+    if (sp->n_pointers > 0 && !sp->cuts) return set_err(GACER_E_INVALID_ARG, "cuts is NULL");
+    P.cuts.assign(nt, {});
+    for (int t = 0; t < nt; ++t) {
+      int prev = 0;
+      for (int j = 0; j < sp->n_pointers; ++j) {
+        const int c = sp->cuts[static_cast<size_t>(t) * sp->n_pointers + j];
+        if (c < 0 || c > S.tenants[t].n_orig)
+          return set_err(GACER_E_CUT_OUT_OF_RANGE, "tenant %d pointer %d = %d outside [0, %d]", t, j, c, S.tenants[t].n_orig);
+        if (c < prev) return set_err(GACER_E_UNSORTED_CUTS, "tenant %d pointers decrease at %d", t, j);
+        prev = c;
+        P.cuts[t].push_back(c);
+      }
+    }
+  }
+  if (dec) {
+    if (dec->n < 0 || (dec->n > 0 && !dec->items)) return set_err(GACER_E_INVALID_ARG, "bad decomposition");
+    for (int i = 0; i < dec->n; ++i) {
+      const gacer_chunking& c = dec->items[i];
+      if (c.tenant < 0 || c.tenant >= nt) return set_err(GACER_E_INVALID_ARG, "chunking %d: bad tenant", i);
+      const Tenant& T = S.tenants[c.tenant];
+      if (c.op_index < 1 || c.op_index > T.n_orig) return set_err(GACER_E_INVALID_ARG, "chunking %d: bad op_index", i);
+      if (c.axis == GACER_AXIS_NONE) continue;  // mask(O) = 0
+      if (c.axis != GACER_AXIS_BATCH && c.axis != GACER_AXIS_CHANNEL)
+        return set_err(GACER_E_INVALID_ARG, "chunking %d: bad axis", i);
+      if (c.n_chunks < 1 || !c.sizes)
+        return set_err(GACER_E_MASKED_OP_MISSING_CHUNKS, "chunking %d: decomposed op without list", i);
+      const int o = c.op_index - 1;
+      if (T.orig_fused[o] < 0) return set_err(GACER_E_INVALID_ARG, "chunking %d: op %d is an alias (flatten/dropout/concat)", i, c.op_index);
+      long long sum = 0;
+      for (int j = 0; j < c.n_chunks; ++j) {
+        if (c.sizes[j] < 1) return set_err(GACER_E_CHUNK_SUM_MISMATCH, "chunking %d: chunk size < 1", i);
+        sum += c.sizes[j];
+      }
+      const int want = c.axis == GACER_AXIS_BATCH ? T.batch : T.orig_out_c[o];
+      if (sum != want)
+        return set_err(GACER_E_CHUNK_SUM_MISMATCH, "chunking %d: sizes sum to %lld, expected %d (Eq. 5)", i, sum, want);
+      Chunking ch;
+      ch.axis = c.axis;
+      ch.sizes.assign(c.sizes, c.sizes + c.n_chunks);
+      if (!P.chunks.emplace(std::make_pair(c.tenant, o), ch).second)
+        return set_err(GACER_E_INVALID_ARG, "chunking %d: op %d decomposed twice", i, c.op_index);
+    }
+  }
+  if (int rc = compile_plan(P)) return rc;  // previous plan untouched on error
+  S.plan = std::move(P);
+  return upload_plan();
+}
+
+int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !out)
+    return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
+  const Tenant& T = S.tenants[tenant];
+  const int m = std::min(n, T.n_orig);
+  for (int i = 0; i < m; ++i) out[i] = cluster_of_orig(S.plan, tenant, i);
+  return m;
+}
+
+int gacer_set_mode(int mode) {
+  if (mode != GACER_MODE_EXECUTOR && mode != GACER_MODE_SEQUENTIAL && mode != GACER_MODE_MULTISTREAM)
+    return set_err(GACER_E_INVALID_ARG, "bad mode %d", mode);
+  S.mode = mode;
+  return GACER_OK;
+}
+
+int gacer_run_round_async(void* stream) { return enqueue_round(static_cast<cudaStream_t>(stream)); }
+
+int gacer_run_round(void) {
+  if (int rc = enqueue_round(S.stream)) return rc;
+  return finish_round();
+}
+
+int gacer_run_round_host(const void* const* host_inputs, void* const* host_outputs) {
+  if (int rc = check_ready()) return rc;
+  if (!host_inputs || !host_outputs) return set_err(GACER_E_INVALID_ARG, "NULL host arrays");
+  for (size_t t = 0; t < S.tenants.size(); ++t) {
+    const Tenant& T = S.tenants[t];
+    const size_t bytes = static_cast<size_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
+    CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(T.in_dev), host_inputs[t], bytes, cudaMemcpyHostToDevice, S.stream));
+  }
+  if (int rc = enqueue_round(S.stream)) return rc;
+  for (size_t t = 0; t < S.tenants.size(); ++t) {
+    const Tenant& T = S.tenants[t];
+    CUDA_TRY(cudaMemcpyAsync(host_outputs[t], T.out_dev, static_cast<size_t>(T.batch) * T.out_features * 4,
+                             cudaMemcpyDeviceToHost, S.stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(S.stream));
+  return finish_round();
+}
+
+int gacer_get_stats(gacer_round_stats* out) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (!out) return set_err(GACER_E_INVALID_ARG, "NULL");
+  std::memset(out, 0, sizeof *out);
+  out->last_round_ms = S.last_ms;
+  out->n_items = static_cast<int64_t>(S.plan.items.size());
+  out->n_clusters = S.plan.n_clusters;
+  out->kernel_launches = S.last_launches;
+  out->n_tenants = static_cast<int32_t>(S.tenants.size());
+  for (const Tenant& T : S.tenants) {
+    out->n_fused_ops += static_cast<int32_t>(T.fops.size());
+    for (const FusedOp& F : T.fops) {
+      if (F.kind == DK_GEMM || F.kind == DK_SIMT_GEMM) out->tensor_flops += F.flops;
+      else out->cc_bytes += F.bytes;
+    }
+  }
+  return GACER_OK;
+}
+
+int gacer_get_trace(int64_t* records, int32_t cap) {
+  if (!S.inited || S.host_only || !S.d_trace) return set_err(GACER_E_STATE, "tracing not enabled");
+  if (!records || cap < 0) return set_err(GACER_E_INVALID_ARG, "bad buffer");
+  const size_t n = std::min<size_t>(cap, S.plan.items.size());
+  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return static_cast<int>(n);
+}
+
+const char* gacer_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+"""Thin ctypes binding of libgacer.so (include/gacer.h).
+
+Argument marshalling only: every step of the path runs in the library and
+its sm_100a kernels.  There is no Python or CPU fallback -- if the library is
+missing this module raises at import of ``lib()``.
+
+Function names mirror the C ABI (gacer_init, gacer_register_tenant,
+gacer_set_regulation, gacer_run_round, ...).  ``graph_desc`` and
+``regulation_desc`` marshal the plain-data graph / plan descriptions used by
+the tests and bench into the C structs (keeping the backing arrays alive).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgacer.so")
+
+# ---------------------------------------------------------------- constants
+OK = 0
+E = {
+    -1: "GACER_E_INVALID_ARG", -2: "GACER_E_DUPLICATE_ID", -3: "GACER_E_UNKNOWN_PREDECESSOR",
+    -4: "GACER_E_CYCLE", -5: "GACER_E_UNSUPPORTED_OP", -6: "GACER_E_CHUNK_SUM_MISMATCH",
+    -7: "GACER_E_MASKED_OP_MISSING_CHUNKS", -8: "GACER_E_CUT_OUT_OF_RANGE", -9: "GACER_E_UNSORTED_CUTS",
+    -10: "GACER_E_POINTER_COUNT_MISMATCH", -11: "GACER_E_STATE", -12: "GACER_E_OOM", -13: "GACER_E_CUDA",
+    -14: "GACER_E_DEADLOCK", -15: "GACER_E_SHAPE",
+}
+STATUS = {v: k for k, v in E.items()}
+
+OP = {"conv": 1, "linear": 2, "maxpool": 3, "avgpool": 4, "gap": 5, "add": 6, "concat": 7,
+      "bn": 8, "relu": 9, "relu6": 10, "flatten": 11, "dropout": 12}
+DTYPE = {"bf16": 1, "fp32": 2}
+AXIS = {"none": 0, "batch": 1, "channel": 2}
+MODE = {"executor": 0, "sequential": 1, "multistream": 2}
+PARTITION = {"work_conserving": 0, "strict": 1}
+FLAG_BIAS, FLAG_CIP = 1, 2
+
+FP = C.POINTER(C.c_float)
+IP = C.POINTER(C.c_int32)
+
+
+class gacer_op_desc(C.Structure):
+    _fields_ = [("id", C.c_int32), ("kind", C.c_int32), ("n_preds", C.c_int32), ("preds", IP),
+                ("c_in", C.c_int32), ("c_out", C.c_int32), ("kh", C.c_int32), ("kw", C.c_int32),
+                ("stride", C.c_int32), ("pad_h", C.c_int32), ("pad_w", C.c_int32), ("groups", C.c_int32),
+                ("flags", C.c_int32), ("weight", FP), ("bias", FP), ("bn_gamma", FP), ("bn_beta", FP),
+                ("bn_mean", FP), ("bn_var", FP), ("bn_eps", C.c_float)]
+
+
+class gacer_graph(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("ops", C.POINTER(gacer_op_desc)), ("in_c", C.c_int32),
+                ("in_h", C.c_int32), ("in_w", C.c_int32), ("dtype", C.c_int32), ("train", C.c_int32),
+                ("lr", C.c_float), ("momentum", C.c_float)]
+
+
+class gacer_chunking(C.Structure):
+    _fields_ = [("tenant", C.c_int32), ("op_index", C.c_int32), ("axis", C.c_int32),
+                ("n_chunks", C.c_int32), ("sizes", IP), ("sm_budget", IP)]
+
+
+class gacer_decomposition(C.Structure):
+    _fields_ = [("n", C.c_int32), ("items", C.POINTER(gacer_chunking))]
+
+
+class gacer_sync_pointers(C.Structure):
+    _fields_ = [("n_tenants", C.c_int32), ("n_pointers", C.c_int32), ("cuts", IP)]
+
+
+class gacer_options(C.Structure):
+    _fields_ = [("num_ctas", C.c_int32), ("partition", C.c_int32), ("watchdog_ms", C.c_int32),
+                ("trace", C.c_int32)]
+
+
+class gacer_round_stats(C.Structure):
+    _fields_ = [("last_round_ms", C.c_double), ("n_items", C.c_int64), ("n_clusters", C.c_int32),
+                ("n_fused_ops", C.c_int32), ("kernel_launches", C.c_int32), ("n_tenants", C.c_int32),
+                ("tensor_flops", C.c_double), ("cc_bytes", C.c_double)]
+
+
+class gacer_tenant_info(C.Structure):
+    _fields_ = [("n_orig_ops", C.c_int32), ("n_fused_ops", C.c_int32), ("batch", C.c_int32),
+                ("in_c_pad", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32),
+                ("out_features", C.c_int32), ("in_bytes", C.c_int64), ("out_bytes", C.c_int64),
+                ("flops", C.c_double)]
+
+
+EXPORTS = {
+    "gacer_init": ([C.c_int, C.POINTER(gacer_options)], C.c_int),
+    "gacer_shutdown": ([], C.c_int),
+    "gacer_register_tenant": ([C.POINTER(gacer_graph), C.c_int32], C.c_int),
+    "gacer_get_tenant_info": ([C.c_int, C.POINTER(gacer_tenant_info)], C.c_int),
+    "gacer_bind_io": ([C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "gacer_set_regulation": ([C.POINTER(gacer_decomposition), C.POINTER(gacer_sync_pointers)], C.c_int),
+    "gacer_query_op_clusters": ([C.c_int, IP, C.c_int32], C.c_int),
+    "gacer_set_mode": ([C.c_int], C.c_int),
+    "gacer_run_round": ([], C.c_int),
+    "gacer_run_round_async": ([C.c_void_p], C.c_int),
+    "gacer_run_round_host": ([C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
+    "gacer_get_stats": ([C.POINTER(gacer_round_stats)], C.c_int),
+    "gacer_get_trace": ([C.POINTER(C.c_int64), C.c_int32], C.c_int),
+    "gacer_last_error": ([], C.c_char_p),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libgacer.so (built in-tree by __graft_entry__.build()).  Raises if
+    absent: there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        _lib = C.CDLL(LIB_PATH)
+        for name, (args, res) in EXPORTS.items():
+            f = getattr(_lib, name)
+            f.argtypes = args
+            f.restype = res
+    return _lib
+
+
+class GacerError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{E.get(code, code)}: {msg}")
+        self.code = code
+        self.name = E.get(code, str(code))
+
+
+def _check(rc):
+    if rc < 0:
+        raise GacerError(rc, lib().gacer_last_error().decode())
+    return rc
+
+
+# ---------------------------------------------------------------- marshalling
+def _fptr(a, keep):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    keep.append(a)
+    return a.ctypes.data_as(FP)
+
+
+def _iptr(a, keep):
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    keep.append(a)
+    return a.ctypes.data_as(IP)
+
+
+def graph_desc(graph, params, dtype="bf16"):
+    """Marshal a plain-data tenant graph (``graph.ops`` list of dicts,
+    ``graph.in_c/in_h/in_w``) and its parameters into a gacer_graph.
+    Returns (struct, keepalive)."""
+    keep = []
+    n = len(graph.ops)
+    arr = (gacer_op_desc * n)()
+    for i, op in enumerate(graph.ops):
+        d = arr[i]
+        d.id = op["id"]
+        d.kind = OP[op["kind"]]
+        d.n_preds = len(op["preds"])
+        d.preds = _iptr(op["preds"], keep)
+        p = params.get(op["id"], {})
+        k = op["kind"]
+        if k == "conv":
+            d.c_in, d.c_out, d.kh, d.kw = op["c_in"], op["c_out"], op["kh"], op["kw"]
+            d.stride, d.pad_h, d.pad_w, d.groups = op["stride"], op["ph"], op["pw"], op["groups"]
+        elif k == "linear":
+            d.c_in, d.c_out = op["c_in"], op["c_out"]
+        elif k in ("maxpool", "avgpool"):
+            d.kh, d.kw, d.stride, d.pad_h, d.pad_w = op["kh"], op["kw"], op["stride"], op["ph"], op["pw"]
+            if k == "avgpool" and op.get("cip", True):
+                d.flags |= FLAG_CIP
+        elif k == "bn":
+            d.c_out = op["c"]
+            d.bn_eps = op["eps"]
+            d.bn_gamma = _fptr(p["gamma"], keep)
+            d.bn_beta = _fptr(p["beta"], keep)
+            d.bn_mean = _fptr(p["mean"], keep)
+            d.bn_var = _fptr(p["var"], keep)
+        if "w" in p:
+            d.weight = _fptr(p["w"], keep)
+        if "b" in p:
+            d.bias = _fptr(p["b"], keep)
+            d.flags |= FLAG_BIAS
+    keep.append(arr)
+    g = gacer_graph(n_ops=n, ops=C.cast(arr, C.POINTER(gacer_op_desc)), in_c=graph.in_c,
+                    in_h=graph.in_h, in_w=graph.in_w, dtype=DTYPE[dtype], train=0, lr=0.0, momentum=0.0)
+    return g, keep
+
+
+def regulation_desc(decomposition=None, pointers=None, n_tenants=None):
+    """decomposition: list of (tenant, op_index (1-based), axis, sizes);
+    pointers: list (per tenant) of cut lists.  Returns (dec*, ptr*, keep)."""
+    keep = []
+    dp = None
+    if decomposition is not None:
+        n = len(decomposition)
+        arr = (gacer_chunking * max(n, 1))()
+        for i, (t, oi, axis, sizes) in enumerate(decomposition):
+            arr[i].tenant, arr[i].op_index = t, oi
+            arr[i].axis = AXIS[axis] if isinstance(axis, str) else axis
+            arr[i].n_chunks = len(sizes) if sizes is not None else 0
+            arr[i].sizes = _iptr(sizes, keep) if sizes is not None else None
+            arr[i].sm_budget = None
+        keep.append(arr)
+        dec = gacer_decomposition(n=n, items=C.cast(arr, C.POINTER(gacer_chunking)))
+        keep.append(dec)
+        dp = C.pointer(dec)
+    pp = None
+    if pointers is not None:
+        nt = len(pointers) if n_tenants is None else n_tenants
+        npt = len(pointers[0]) if pointers else 0
+        flat = np.zeros(max(1, nt * npt), dtype=np.int32)
+        for t, cuts in enumerate(pointers):
+            flat[t * npt:(t + 1) * npt] = cuts
+        sp = gacer_sync_pointers(n_tenants=nt, n_pointers=npt, cuts=_iptr(flat, keep))
+        keep.append(sp)
+        pp = C.pointer(sp)
+    return dp, pp, keep
+
+
+# ---------------------------------------------------------------- calls
+def gacer_init(device=0, num_ctas=0, partition="work_conserving", watchdog_ms=0, trace=False):
+    o = gacer_options(num_ctas=num_ctas, partition=PARTITION[partition], watchdog_ms=watchdog_ms,
+                      trace=int(trace))
+    return _check(lib().gacer_init(device, C.byref(o)))
+
+
+def gacer_shutdown():
+    return _check(lib().gacer_shutdown())
+
+
+def gacer_register_tenant(graph, params, batch, dtype="bf16"):
+    g, keep = graph_desc(graph, params, dtype)
+    rc = lib().gacer_register_tenant(C.byref(g), batch)
+    del keep
+    return _check(rc)
+
+
+def gacer_get_tenant_info(tenant):
+    info = gacer_tenant_info()
+    _check(lib().gacer_get_tenant_info(tenant, C.byref(info)))
+    return {f: getattr(info, f) for f, _ in gacer_tenant_info._fields_}
+
+
+def gacer_bind_io(tenant, input_dev_ptr, output_dev_ptr):
+    return _check(lib().gacer_bind_io(tenant, C.c_void_p(input_dev_ptr), C.c_void_p(output_dev_ptr)))
+
+
+def gacer_set_regulation(decomposition=None, pointers=None, n_tenants=None):
+    dp, pp, keep = regulation_desc(decomposition, pointers, n_tenants)
+    rc = lib().gacer_set_regulation(dp, pp)
+    del keep
+    return _check(rc)
+
+
+def gacer_query_op_clusters(tenant, n_ops):
+    out = np.zeros(n_ops, dtype=np.int32)
+    n = _check(lib().gacer_query_op_clusters(tenant, out.ctypes.data_as(IP), n_ops))
+    return out[:n].tolist()
+
+
+def gacer_set_mode(mode):
+    return _check(lib().gacer_set_mode(MODE[mode] if isinstance(mode, str) else mode))
+
+
+def gacer_run_round():
+    return _check(lib().gacer_run_round())
+
+
+def gacer_run_round_async(stream_ptr=0):
+    return _check(lib().gacer_run_round_async(C.c_void_p(stream_ptr)))
+
+
+def gacer_run_round_host(host_in_ptrs, host_out_ptrs):
+    n = len(host_in_ptrs)
+    ins = (C.c_void_p * n)(*host_in_ptrs)
+    outs = (C.c_void_p * n)(*host_out_ptrs)
+    return _check(lib().gacer_run_round_host(ins, outs))
+
+
+def gacer_get_stats():
+    s = gacer_round_stats()
+    _check(lib().gacer_get_stats(C.byref(s)))
+    return {f: getattr(s, f) for f, _ in gacer_round_stats._fields_}
+
+
+def gacer_get_trace(cap):
+    buf = np.zeros((cap, 6), dtype=np.int64)
+    n = _check(lib().gacer_get_trace(buf.ctypes.data_as(C.POINTER(C.c_int64)), cap))
+    return buf[:n]
+
+
+def gacer_last_error():
+    return lib().gacer_last_error().decode()

@@ -1,0 +1,156 @@
+"""C-ABI tests that need no GPU: the library loads, exports every symbol
+include/gacer.h declares, and its host logic (validation, lowering, Eq. 6/7
+plan compilation) behaves as the paper and the header state.  Uses the
+HOST-ONLY instance (gacer_init(-1)): no CUDA call is made."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads
+from gacer_testutil import read_golden
+from paper_2304_11745_b200 import gacer as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture()
+def host():
+    G.gacer_init(-1)
+    yield
+    G.gacer_shutdown()
+
+
+def test_exports_every_declared_symbol():
+    with open(os.path.join(ROOT, "include", "gacer.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(gacer_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 14
+    lib = G.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(G.EXPORTS)
+
+
+def chain_graph(n_ops, c=8, hw=4):
+    """conv followed by n_ops-1 ReLUs: an n_ops-long operator list."""
+    g = workloads.Graph("chain", c, hw, hw)
+    x = g.conv(0, c, c, 1)
+    for _ in range(n_ops - 1):
+        x = g.relu(x)
+    return g
+
+
+def register(g, B=2, dt="bf16", seed=0):
+    return G.gacer_register_tenant(g, workloads.make_params(g, seed, dt), B, dt)
+
+
+def test_eq6_eq7_cluster_compilation(host):
+    """Eq. 7 (l.747) and Eq. 6 (l.730-732) as compiled by gacer_set_regulation."""
+    lines = read_golden("eq6_clusters.txt")
+    ns, cuts = (t.strip() for t in lines[0].split("|"))
+    ns = [int(v) for v in ns.split(",")]
+    matrix_p = [[int(v) for v in c.split(",")] for c in cuts.split("/")]
+    for n in ns:
+        register(chain_graph(n))
+    G.gacer_set_regulation(None, matrix_p)
+    got = [G.gacer_query_op_clusters(t, n) for t, n in enumerate(ns)]
+    # expected: parse the golden listing back into op -> cluster
+    for k, ln in enumerate(lines[1:]):
+        segs = re.findall(r"\[([^\]]*)\]", ln)
+        for m, seg in enumerate(segs):
+            for i in re.findall(r"O_\{\d+,(\d+)\}", seg):
+                assert got[m][int(i) - 1] == k
+    st = G.gacer_get_stats()
+    assert st["n_clusters"] == 3
+
+
+def test_eq7_segments_golden(host):
+    for ln in read_golden("eq7_segments.txt"):
+        n, cuts, segs = (t.strip() for t in ln.split("|"))
+        register(chain_graph(int(n)))
+        G.gacer_set_regulation(None, [[int(c) for c in cuts.split(",")]])
+        got = G.gacer_query_op_clusters(0, int(n))
+        for k, seg in enumerate(segs.split(";")):
+            for i in seg.split(","):
+                assert got[int(i) - 1] == k
+
+
+def test_error_codes_graph(host):
+    g = chain_graph(3)
+    g.ops[1]["id"] = 1                       # duplicate id
+    with pytest.raises(G.GacerError) as e:
+        register(g)
+    assert e.value.name == "GACER_E_DUPLICATE_ID"
+    g = chain_graph(3)
+    g.ops[2]["preds"] = [42]
+    with pytest.raises(G.GacerError) as e:
+        register(g)
+    assert e.value.name == "GACER_E_UNKNOWN_PREDECESSOR"
+    g = chain_graph(3)
+    g.ops[0]["preds"] = [3]                  # 1 <- 3 <- 2 <- 1
+    with pytest.raises(G.GacerError) as e:
+        register(g)
+    assert e.value.name == "GACER_E_CYCLE"
+    g = chain_graph(3)
+    g.ops[0]["c_in"] = 16
+    with pytest.raises(G.GacerError) as e:
+        register(g)
+    assert e.value.name == "GACER_E_SHAPE"
+
+
+def test_error_codes_plan(host):
+    register(chain_graph(6))
+    register(chain_graph(4))
+    cases = [
+        (([(0, 1, "batch", [1, 2])], None), "GACER_E_CHUNK_SUM_MISMATCH"),     # Eq. 5: sum != B=2
+        (([(0, 1, "batch", None)], None), "GACER_E_MASKED_OP_MISSING_CHUNKS"),
+        (([(0, 1, "channel", [4, 3])], None), "GACER_E_CHUNK_SUM_MISMATCH"),   # C_out = 8
+        ((None, [[7], [1]]), "GACER_E_CUT_OUT_OF_RANGE"),
+        ((None, [[3, 2], [1, 1]]), "GACER_E_UNSORTED_CUTS"),
+        ((None, [[-1], [1]]), "GACER_E_CUT_OUT_OF_RANGE"),
+    ]
+    for (dec, ptr), name in cases:
+        with pytest.raises(G.GacerError) as e:
+            G.gacer_set_regulation(dec, ptr, n_tenants=2)
+        assert e.value.name == name, (dec, ptr, e.value)
+    # atomic: a failed call leaves the previous plan in force
+    G.gacer_set_regulation(None, [[2], [1]])
+    with pytest.raises(G.GacerError):
+        G.gacer_set_regulation(None, [[3, 2], [0, 0]])
+    assert G.gacer_query_op_clusters(0, 6) == [0, 0, 1, 1, 1, 1]
+    with pytest.raises(G.GacerError) as e:
+        G.gacer_run_round()
+    assert e.value.name == "GACER_E_STATE"
+
+
+def test_table3_plans_accepted(host):
+    """Table 3 (l.1074-1082): V16(32) || R18(32) with convs and the ReLUs after
+    them batch-decomposed per the listed list_B -- all are legal plans."""
+    v16, r18 = workloads.build_model("vgg16"), workloads.build_model("resnet18")
+    register(v16, 32)
+    register(r18, 32)
+    base = G.gacer_get_stats()["n_items"]
+    for ln in read_golden("table3_plans.txt"):
+        _, lv, lr = (t.strip() for t in ln.split("|"))
+        dec = []
+        for t, (g, lst) in enumerate(((v16, lv), (r18, lr))):
+            sizes = [int(v) for v in lst.split(",")]
+            if len(sizes) == 1:
+                continue
+            for i, op in enumerate(g.ops):
+                if op["kind"] == "conv" or (op["kind"] == "relu" and i > 0 and g.ops[i - 1]["kind"] == "conv"):
+                    dec.append((t, i + 1, "batch", sizes))
+        G.gacer_set_regulation(dec, None, n_tenants=2)
+        # chunks own whole tiles: the decomposition never adds or drops work
+        assert G.gacer_get_stats()["n_items"] == base
+
+
+def test_identity_plan_and_fusion_counts(host):
+    t = register(workloads.build_model("resnet50"), 8)
+    info = G.gacer_get_tenant_info(t)
+    assert info["n_orig_ops"] == 175 and info["n_fused_ops"] == 56
+    assert abs(info["flops"] - 65.43e9) / 65.43e9 < 1e-3
+    st = G.gacer_get_stats()
+    assert st["n_clusters"] == 1 and st["n_fused_ops"] == 56

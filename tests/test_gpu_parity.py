@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle.
+
+Gates (north_star / SURVEY §8(c) Q2): max-norm relative error
+max|g - o| / max|o| <= 2e-2 on the bf16 tensor-core path and <= 1e-4 on
+fp32.  The per-op gate additionally requires >= 99.9% of outputs to round to
+the same bf16 as the oracle (oracle fed the GPU's own bf16 input)."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import forward_graph
+from oracle import ops as oops
+
+pytestmark = pytest.mark.gpu
+
+
+def maxrel(y, r):
+    return float(np.max(np.abs(y - r)) / max(np.max(np.abs(r)), 1e-30))
+
+
+def bf16_rne(a):
+    return workloads.bf16_round(np.asarray(a, np.float32))
+
+
+def run_session(tenants, plan=None, mode="executor", **kw):
+    from paper_2304_11745_b200.runtime import Session
+    s = Session([(g, p, B, dt) for g, p, B, dt, _ in tenants], **kw)
+    try:
+        for t, tt in enumerate(tenants):
+            s.set_input(t, tt[4])
+        if plan is not None:
+            s.set_regulation(*plan)
+        s.set_mode(mode)
+        s.run()
+        return s.results(), s.stats()
+    finally:
+        s.close()
+
+
+def make_tenant(name, B, dt, seed, hw=None):
+    g = workloads.build_model(name, hw)
+    p = workloads.make_params(g, seed, dt)
+    x = workloads.make_input(g, B, seed, dt)
+    return g, p, B, dt, x
+
+
+def nhwc_to_nchw(y, B, H, W, C):
+    return y.reshape(B, H, W, C).transpose(0, 3, 1, 2)
+
+
+def test_d1_tiny_fp32(cuda_ok):
+    """BASELINE config 1: tiny CNN + MLP, fp32, B=2, gate 1e-4."""
+    ts = [make_tenant("tiny_cnn", 2, "fp32", 1001), make_tenant("tiny_mlp", 2, "fp32", 1002)]
+    outs, st = run_session(ts)
+    for (g, p, B, dt, x), y in zip(ts, outs):
+        assert maxrel(y, forward_graph(g, p, x)) <= 1e-4
+    assert st["kernel_launches"] == 1
+
+
+CONV_CASES = [
+    # cin, cout, k, stride, pad, hw, B
+    (8, 64, 7, 2, 3, 32, 2),      # stem-like
+    (64, 64, 3, 1, 1, 14, 2),     # 3x3
+    (256, 128, 1, 1, 0, 14, 3),   # 1x1, ragged M (588 rows)
+    (128, 256, 3, 2, 1, 15, 2),   # stride 2, odd size, 2 N-tiles
+    (96, 24, 1, 1, 0, 9, 2),      # MV2 narrow N = 24 (BN 32)
+    (512, 512, 3, 1, 1, 7, 8),    # deep K -> split-K
+    (3, 32, 3, 2, 1, 33, 2),      # 3-channel input padded to 8
+    (16, 48, (1, 7), 1, (0, 3), 12, 2),   # Inception 1x7
+    (16, 48, (7, 1), 1, (3, 0), 12, 2),   # Inception 7x1
+]
+
+
+@pytest.mark.parametrize("cin,cout,k,stride,pad,hw,B", CONV_CASES)
+def test_conv_op_parity(cuda_ok, cin, cout, k, stride, pad, hw, B):
+    """Per-op gate of the tcgen05 implicit-GEMM conv with fused BN + ReLU."""
+    g = workloads.Graph("conv_op", cin, hw, hw)
+    c = g.conv(0, cin, cout, k, stride, pad)
+    c = g.bn(c, cout)
+    g.relu(c)
+    params = workloads.make_params(g, 77 + cin, "bf16")
+    x = workloads.make_input(g, B, 78 + cout, "bf16")
+    outs, _ = run_session([(g, params, B, "bf16", x)])
+    kk = (k, k) if isinstance(k, int) else k
+    pp = (pad, pad) if isinstance(pad, int) else pad
+    ho = (hw + 2 * pp[0] - kk[0]) // stride + 1
+    wo = (hw + 2 * pp[1] - kk[1]) // stride + 1
+    y = nhwc_to_nchw(outs[0], B, ho, wo, cout)
+    bn = params[g.ops[1]["id"]]
+    ref = oops.conv2d(x, params[g.ops[0]["id"]]["w"], None, stride, pp)
+    ref = oops.relu(oops.batchnorm(ref, bn["gamma"], bn["beta"], bn["mean"], bn["var"], 1e-5))
+    assert maxrel(y, ref) <= 2e-2
+    exact = float(np.mean(bf16_rne(y) == bf16_rne(ref)))
+    assert exact >= 0.999, exact
+
+
+@pytest.mark.parametrize("kind", ["dw", "maxpool", "avgpool", "gap"])
+def test_cuda_core_op_parity(cuda_ok, kind):
+    B, C, hw = 3, 40, 13
+    g = workloads.Graph("cc_op", C, hw, hw)
+    if kind == "dw":
+        y = g.conv(0, C, C, 3, 2, 1, groups=C)
+        y = g.bn(y, C)
+        g.relu6(y)
+    elif kind == "maxpool":
+        g.maxpool(0, 3, 2, 1)
+    elif kind == "avgpool":
+        g.avgpool(0, 3, 1, 1)
+    else:
+        g.gap(0)
+    p = workloads.make_params(g, 5, "bf16")
+    x = workloads.make_input(g, B, 6, "bf16")
+    outs, _ = run_session([(g, p, B, "bf16", x)])
+    ref = forward_graph(g, p, x, return_all=True)[1][g.ops[-1]["id"]]
+    y = nhwc_to_nchw(outs[0], B, ref.shape[2], ref.shape[3], C)
+    assert maxrel(y, ref) <= 2e-2
+    if kind == "maxpool":
+        assert np.array_equal(y, ref)   # max of bf16 values is exact
+
+
+@pytest.mark.parametrize("name,B,hw", [("resnet50", 2, 224), ("mobilenet_v2", 2, 224),
+                                       ("vgg16", 1, 224), ("resnet18", 3, 64)])
+def test_tenant_parity(cuda_ok, name, B, hw):
+    t = make_tenant(name, B, "bf16", 2000 + B, hw)
+    outs, _ = run_session([t])
+    g, p, B, dt, x = t
+    assert maxrel(outs[0], forward_graph(g, p, x)) <= 2e-2
+
+
+@pytest.mark.parametrize("name,hw,B", [("inception_v3", 224, 1), ("alexnet", 224, 2),
+                                       ("resnet101", 64, 2)])
+def test_tenant_parity_d3_models(cuda_ok, name, hw, B):
+    t = make_tenant(name, B, "bf16", 3000 + B, hw)
+    outs, _ = run_session([t])
+    g, p, B, dt, x = t
+    assert maxrel(outs[0], forward_graph(g, p, x)) <= 2e-2
