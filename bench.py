@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""GACER on B200 -- benchmark of one regulated multi-tenant round.
+
+Workload (BASELINE.json configs[1]): ResNet-50 + VGG-16 + MobileNetV2,
+batch 8 each, 224x224, bf16, synthetic seeded inputs and random-init weights
+(workloads/).  A *step* is one round: every tenant's forward once, through
+the whole hot path (the persistent executor kernel).  Metric: aggregate
+tenant inferences/s = sum_t B_t / makespan (higher is better).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gacer|reference]
+
+N > 1 is launched by torchrun: one process per GPU, each running its own
+replica of the mix (tenant placement, no data-path collective; weak scaling).
+Timing: per-step CUDA events on the launching stream, L2 flushed (256 MB
+write) between steps outside the events, barrier + synchronize around the
+timed region, max over ranks.  --impl reference times the fp64 oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "aggregate tenant inferences/s per B200 + makespan/round vs sequential & multi-stream"
+UNIT = "inferences/s"
+CONFIG = "d2_r50_v16_mv2"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, dev):
+        self.dev, self.samples, self.reasons, self.stop_ev = dev, [], set(), threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        N = self.N
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, v in names.items():
+                    if r & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "note": "no NVML samples"}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "n_samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload
+def make_workload(cfg=CONFIG):
+    import workloads
+    from workloads.zoo import CONFIG_INDEX
+    ts = []
+    for i, (name, B, dt) in enumerate(workloads.config_tenants(cfg)):
+        g = workloads.build_model(name)
+        seed = workloads.tenant_seed(CONFIG_INDEX[cfg], i)
+        ts.append((name, g, workloads.make_params(g, seed, dt), B, dt,
+                   workloads.make_input(g, B, seed, dt)))
+    return ts
+
+
+def cpu_oracle_sample(ts, budget_s=30.0):
+    """Time the fp64 oracle (as it stands) on one image of each tenant of the
+    mix: a bounded sample of the workload.  Returns (images/s, cores, desc)."""
+    from oracle import forward_graph
+    from oracle import ops as oops
+    oops.build()
+    t0 = time.perf_counter()
+    n = 0
+    for name, g, p, B, dt, x in ts:
+        forward_graph(g, p, x[:1])
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt_s = time.perf_counter() - t0
+    desc = f"1 image of each of {n} tenant(s) of {CONFIG} (fp64 oracle, OpenMP)"
+    return n / dt_s, oops.num_threads(), desc, dt_s
+
+
+# ------------------------------------------------------------------ main arms
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    ts = make_workload()
+    steps = max(1, args.steps)
+    warm = 0
+    tot_img, tot_s = 0, 0.0
+    for i in range(warm + steps):
+        v, cores, desc, secs = cpu_oracle_sample(ts, budget_s=30.0)
+        if i >= warm:
+            tot_img += v * secs
+            tot_s += secs
+    value = tot_img / tot_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, random-init weights)",
+        "config": {"workload": CONFIG, "sample": "one image per tenant per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_mode(G, s, torch, stream, mode, steps, warmup, flush):
+    s.set_mode(mode)
+    for _ in range(warmup):
+        G.gacer_run_round_async(stream.cuda_stream)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        G.gacer_run_round_async(stream.cuda_stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def run_gacer(args, rank, world, dist):
+    import torch
+    from paper_2304_11745_b200 import gacer as G
+    from paper_2304_11745_b200.runtime import Session
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    ts = make_workload()
+    sess = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], device=dev)
+    for t, (*_, x) in enumerate(ts):
+        sess.set_input(t, x)
+    n_inf = sum(B for _, _, _, B, _, _ in ts)
+    stream = torch.cuda.Stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
+    torch.cuda.set_stream(stream)
+
+    st = G.gacer_get_stats()
+    # ---- main arm: GACER executor, identity plan
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        times = time_mode(G, sess, torch, stream, "executor", args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    total_ms = float(np.sum(times))
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * n_inf * args.steps / (total_ms / 1000.0)
+    launches_per_round = G.gacer_get_stats()["kernel_launches"]
+
+    # ---- same-kernel baselines (makespan per round), same timing protocol
+    base = {}
+    for mode in ("sequential", "multistream"):
+        tm = time_mode(G, sess, torch, stream, mode, args.steps, args.warmup, flush)
+        m = float(np.mean(tm))
+        base[mode] = {"ms_per_round": m, "inferences_per_s": n_inf / (m / 1000.0),
+                      "kernel_launches_per_round": G.gacer_get_stats()["kernel_launches"]}
+    sess.set_mode("executor")
+
+    # ---- e2e: through the public C ABI with HOST buffers (H2D + D2H inside)
+    host_in = [sess.host_input(t, x) for t, (*_, x) in enumerate(ts)]
+    host_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in sess.outputs]
+    for _ in range(args.warmup):
+        G.gacer_run_round_host([h.data_ptr() for h in host_in], [h.data_ptr() for h in host_out])
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        G.gacer_run_round_host([h.data_ptr() for h in host_in], [h.data_ptr() for h in host_out])
+        e2e_ms.append(G.gacer_get_stats()["last_round_ms"])
+    e2e_total = float(np.sum(e2e_ms))
+    if dist:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    h2d = int(sum(i["in_bytes"] for i in sess.info))
+    d2h = int(sum(i["out_bytes"] for i in sess.info))
+
+    if rank == 0:
+        peaks, src = load_peaks()
+        flops = st["tensor_flops"]
+        peak = peaks["bf16_tflops"]
+        achieved = flops / (ms_step / 1000.0) / 1e12
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(CONFIG)
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded inputs, random-init weights)",
+            "config": {"workload": CONFIG, "tenants": [f"{n}(B={B})" for n, _, _, B, _, _ in ts],
+                       "image": 224, "plan": "identity", "mode": "executor",
+                       "parallelism": f"replica-per-gpu x{world}",
+                       "l2": "flushed between steps (256 MB write, outside the events)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "gacer_executor",
+                         "algorithmic": f"{flops / 1e9:.1f} GFLOP conv+FC (2*MAC) per launch",
+                         "peak_source": f"{src} bf16_tflops (burst; kernel timed alone)"},
+            "e2e": {"value": world * n_inf * args.steps / (e2e_total / 1000.0), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_round * args.steps,
+            "clocks": clk.summary(),
+            "baselines": base,
+            "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
+            "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,
+            "makespan_ms": {"p10": float(np.percentile(times, 10)), "p50": float(np.median(times)),
+                            "p90": float(np.percentile(times, 90))},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, desc, secs = cpu_oracle_sample(ts, budget_s=30.0)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": desc}
+        print(json.dumps(line), flush=True)
+    sess.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="gacer", choices=["gacer", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        backend = "nccl" if args.impl == "gacer" else "gloo"
+        if args.impl == "gacer":
+            import torch
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist_mod.init_process_group(backend)
+        dist = dist_mod
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_gacer(args, rank, world, dist)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

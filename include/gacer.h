@@ -228,13 +228,15 @@ int gacer_run_round_async(void* stream);
 /* End-to-end round with HOST buffers: copies host_inputs[t] (layout as
  * gacer_bind_io, pinned memory recommended) to the bound device inputs, runs
  * the round, copies every output to host_outputs[t]; blocks.  Arrays are
- * indexed by tenant id. */
+ * indexed by tenant id.  gacer_get_stats().last_round_ms then covers the
+ * copies and the round (CUDA events on the library stream). */
 int gacer_run_round_host(const void* const* host_inputs, void* const* host_outputs);
 
 int gacer_get_stats(gacer_round_stats* out);
 
 /* Trace of the last executor round (options.trace = 1): up to `cap` records
- * of 6 int64 each: tenant, fused op, sm id, item index, t_start_ns, t_end_ns.
+ * of 8 int64 each, indexed by work item: tenant, global fused-op index, SM id,
+ * item index, cluster, chunk counter, t_start_ns, t_end_ns (%globaltimer).
  * Returns the number of records written. */
 int gacer_get_trace(int64_t* records, int32_t cap);
 

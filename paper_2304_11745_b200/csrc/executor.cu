@@ -745,9 +745,10 @@ extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor(ExecPar
       atomicAdd(p.chunk_done + it.chunk, 1u);
       atomicAdd(p.cluster_done + it.cluster, 1u);
       if (p.trace) {
-        int64_t* rec = p.trace + static_cast<size_t>(claimed) * 6;
+        int64_t* rec = p.trace + static_cast<size_t>(claimed) * 8;
         rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = claimed;
-        rec[4] = static_cast<int64_t>(t_start); rec[5] = static_cast<int64_t>(globaltimer());
+        rec[4] = it.cluster; rec[5] = it.chunk;
+        rec[6] = static_cast<int64_t>(t_start); rec[7] = static_cast<int64_t>(globaltimer());
       }
     }
   }

@@ -967,7 +967,7 @@ int upload_plan() {
   if (!S.d_exit && (rc = dev_upload<uint32_t>(&S.d_exit, nullptr, 1))) return rc;
   if (!S.d_error && (rc = dev_upload<int32_t>(&S.d_error, nullptr, 1))) return rc;
   if (S.d_trace) { cudaFree(S.d_trace); S.d_trace = nullptr; }
-  if (S.opts.trace) CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * 6 * sizeof(int64_t)));
+  if (S.opts.trace) CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * 8 * sizeof(int64_t)));
   S.epoch = 0;
   return 0;
 }
@@ -997,10 +997,10 @@ int check_ready() {
   return 0;
 }
 
-int enqueue_round(cudaStream_t st) {
+int enqueue_round(cudaStream_t st, bool record_events = true) {
   if (int rc = check_ready()) return rc;
   if (!st) st = S.stream;
-  CUDA_TRY(cudaEventRecord(S.ev0, st));
+  if (record_events) CUDA_TRY(cudaEventRecord(S.ev0, st));
   int launches = 0;
   if (S.mode == GACER_MODE_EXECUTOR) {
     if (S.epoch >= 0x7FFFFF00u / std::max<uint32_t>(1, 1 + static_cast<uint32_t>(S.plan.items.size()))) {
@@ -1052,7 +1052,7 @@ int enqueue_round(cudaStream_t st) {
       }
     }
   }
-  CUDA_TRY(cudaEventRecord(S.ev1, st));
+  if (record_events) CUDA_TRY(cudaEventRecord(S.ev1, st));
   S.last_launches = launches;
   return 0;
 }
@@ -1265,18 +1265,19 @@ int gacer_run_round(void) {
 int gacer_run_round_host(const void* const* host_inputs, void* const* host_outputs) {
   if (int rc = check_ready()) return rc;
   if (!host_inputs || !host_outputs) return set_err(GACER_E_INVALID_ARG, "NULL host arrays");
+  CUDA_TRY(cudaEventRecord(S.ev0, S.stream));  // the e2e time includes both copies
   for (size_t t = 0; t < S.tenants.size(); ++t) {
     const Tenant& T = S.tenants[t];
     const size_t bytes = static_cast<size_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
     CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(T.in_dev), host_inputs[t], bytes, cudaMemcpyHostToDevice, S.stream));
   }
-  if (int rc = enqueue_round(S.stream)) return rc;
+  if (int rc = enqueue_round(S.stream, false)) return rc;
   for (size_t t = 0; t < S.tenants.size(); ++t) {
     const Tenant& T = S.tenants[t];
     CUDA_TRY(cudaMemcpyAsync(host_outputs[t], T.out_dev, static_cast<size_t>(T.batch) * T.out_features * 4,
                              cudaMemcpyDeviceToHost, S.stream));
   }
-  CUDA_TRY(cudaStreamSynchronize(S.stream));
+  CUDA_TRY(cudaEventRecord(S.ev1, S.stream));
   return finish_round();
 }
 
@@ -1303,7 +1304,7 @@ int gacer_get_trace(int64_t* records, int32_t cap) {
   if (!S.inited || S.host_only || !S.d_trace) return set_err(GACER_E_STATE, "tracing not enabled");
   if (!records || cap < 0) return set_err(GACER_E_INVALID_ARG, "bad buffer");
   const size_t n = std::min<size_t>(cap, S.plan.items.size());
-  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return static_cast<int>(n);
 }
 

@@ -290,7 +290,7 @@ def gacer_get_stats():
 
 
 def gacer_get_trace(cap):
-    buf = np.zeros((cap, 6), dtype=np.int64)
+    buf = np.zeros((cap, 8), dtype=np.int64)
     n = _check(lib().gacer_get_trace(buf.ctypes.data_as(C.POINTER(C.c_int64)), cap))
     return buf[:n]
 
