@@ -166,56 +166,93 @@ __device__ __forceinline__ float apply_act(float v, int act) {
   return v;
 }
 
+// more PTX helpers: mbarrier arrive / tx, TMA, named barriers
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* tmap, uint64_t* bar, int c, int w,
+                                                   int h, int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // =====================================================================
-// shared memory layout
+// shared memory layout of the executor CTA
 // =====================================================================
 constexpr int A_STAGE_BYTES = BM * 128;
 constexpr int B_STAGE_BYTES = BN_MAX * 128;
 constexpr int SMEM_RING_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES);
+constexpr int TMEM_COLS = 2 * BN_MAX;   // double-buffered accumulators
+
+struct RingSlot {            // scheduler -> MMA / epilogue
+  Item it;
+  int32_t idx;               // item index (trace), -1 = STOP
+  int32_t pad;
+  uint64_t t0;
+};
 
 struct SmemCtl {
-  uint64_t mma_done[STAGES];
-  uint64_t acc_bar;
-  uint32_t tmem_base;
-  int32_t flag;
-  Item item;
+  uint64_t full[STAGES];     // TMA/gather -> MMA
+  uint64_t empty[STAGES];    // MMA -> producers
+  uint64_t tfull[2];         // MMA -> epilogue (accumulator ready)
+  uint64_t tempty[2];        // epilogue -> MMA (accumulator drained)
+  uint64_t rfull[ITEM_RING];
+  uint64_t rempty[ITEM_RING];
+  RingSlot ring[ITEM_RING];
+  Item cur;                  // scheduler -> producer warps
   int32_t claimed;
-  float red[NTHREADS * 8 / 8 + 8];
+  uint32_t tmem_base;
+  int32_t epi_flag;
+  int32_t pad;
+  uint64_t cur_t0;
+  float red[CC_THREADS * 8]; // GAP fixed-order reduction scratch
 };
-constexpr int SMEM_GEMM_BYTES = SMEM_RING_BYTES + 1024 /*align slack*/ + (int)sizeof(SmemCtl) + 64;
-constexpr int GAP_RED_FLOATS = NTHREADS * 8;   // per-thread 8-channel partials
+constexpr int SMEM_BYTES = SMEM_RING_BYTES + 1024 /*align slack*/ + (int)sizeof(SmemCtl);
 
-struct Ctx {               // per-CTA persistent state (uniform across threads)
-  uint8_t* ring;           // 1024-aligned
+struct Ctx {
+  uint8_t* ring;             // 1024-aligned stage buffers
   SmemCtl* ctl;
-  float* gap_red;          // NTHREADS*8 floats (aliases the ring; used only by CC items)
   uint32_t tmem;
-  uint32_t ring_pos;       // K-blocks issued so far (smem ring position)
-  uint32_t acc_uses;       // accumulator commits so far
 };
 
 // =====================================================================
-// GEMM tile (tcgen05)
+// epilogue math (shared by every mode): y = act(acc*scale + bias [+ skip])
 // =====================================================================
-struct ARowInfo {
-  const __nv_bfloat16* img;  // image base for the row's sample (conv) or row pointer (rows mode)
-  int hi0, wi0;
-  bool ok;
-};
-
-__device__ __forceinline__ void load_rows_tile(uint32_t stage_base, const __nv_bfloat16* src, int ld, int row0,
-                                               int nrows, int row_limit, int k, int k_limit, int chunk,
-                                               int rsub) {
-  const bool kok = k < k_limit;
-  for (int r = rsub; r < nrows; r += 32) {
-    const int row = row0 + r;
-    const bool ok = kok && row < row_limit;
-    const __nv_bfloat16* s = ok ? src + static_cast<size_t>(row) * ld + k : src;
-    const uint32_t dst = stage_base + r * 128 + ((chunk ^ (r & 7)) << 4);
-    cp_async16(dst, s, ok);
-  }
-}
-
 __device__ void epilogue_store8(const OpDev& op, int m, int n, const float* v) {
   // m: GEMM row, n: first of 8 GEMM columns
   if (!op.swap) {
@@ -278,174 +315,122 @@ __device__ void epilogue_store8(const OpDev& op, int m, int n, const float* v) {
   }
 }
 
-__device__ void gemm_item(const OpDev& op, const Item& it, Ctx& cx) {
-  const int tid = threadIdx.x;
-  const int bn = op.bn;
-  const int kb0 = (it.ks * op.nkb) / op.split_k;
-  const int kb1 = ((it.ks + 1) * op.nkb) / op.split_k;
-  const int nk = kb1 - kb0;
-  const int m0 = it.mt * BM, n0 = it.nt * bn;
-  const int chunk = tid & 7, rsub = tid >> 3;
-  const uint32_t ring_base = smem_u32(cx.ring);
-  const uint32_t idesc = make_idesc(bn);
+// =====================================================================
+// producer side of a GEMM item: fill the smem ring for its K-blocks
+// =====================================================================
+__device__ __forceinline__ void kb_range(const OpDev& op, int ks, int& kb0, int& nk) {
+  kb0 = (ks * op.nkb) / op.split_k;
+  nk = ((ks + 1) * op.nkb) / op.split_k - kb0;
+}
 
-  // per-thread A-row info (conv im2col): rows rsub + 32*i
-  ARowInfo ar[4];
-  const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
-  if (!op.swap) {
+__device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t& g) {
+  const int ptid = threadIdx.x;  // 0..NPROD-1
+  SmemCtl* ctl = cx.ctl;
+  int kb0, nk;
+  kb_range(op, it.ks, kb0, nk);
+  const uint32_t ring_base = smem_u32(cx.ring);
+  const uint32_t bbytes = static_cast<uint32_t>(op.bn) * 128u;
+  const int m0 = it.mt * BM, n0 = it.nt * op.bn;
+  if (op.a_mode != A_GATHER) {
+    if (ptid == 0) {
+      int w0 = 0, h0 = 0, img0 = 0;
+      if (op.a_mode == A_IM2COL) {
+        const int HoWo = op.Ho * op.Wo;
+        img0 = m0 / HoWo;
+        const int rem = m0 - img0 * HoWo;
+        const int ho = rem / op.Wo, wo = rem - (rem / op.Wo) * op.Wo;
+        w0 = wo * op.stride - op.pw;
+        h0 = ho * op.stride - op.ph;
+      }
+      for (int i = 0; i < nk; ++i) {
+        const uint32_t gi = g + i, stage = gi % STAGES;
+        if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
+        uint64_t* bar = &ctl->full[stage];
+        mbar_arrive_expect_tx(bar, A_STAGE_BYTES + bbytes);
+        const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
+        const uint32_t b_dst = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
+        const int k = (kb0 + i) * BK;
+        if (op.a_mode == A_IM2COL) {
+          const int tap = k / op.C;
+          const int c0 = k - tap * op.C;
+          const int r = tap / op.kw, s = tap - (tap / op.kw) * op.kw;
+          tma_load_im2col_4d(a_dst, op.tmap_a, bar, c0, w0, h0, img0, static_cast<uint16_t>(s),
+                             static_cast<uint16_t>(r));
+        } else {
+          tma_load_2d(a_dst, op.tmap_a, bar, k, m0);
+        }
+        tma_load_2d(b_dst, op.tmap_b, bar, k, n0);
+      }
+    }
+  } else {
+    // im2col gather with cp.async (C not a multiple of 64): 16-byte chunks of
+    // 8 channels of one tap; thread -> chunk j = ptid & 7, rows (ptid>>3)+16i
+    constexpr int ROWS = BM / (NPROD / 8);  // 8 rows per thread
+    constexpr int LAG = 3;                  // stages in flight per thread (< STAGES)
+    const int chunk = ptid & 7, rsub = ptid >> 3;
+    const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
+    const __nv_bfloat16* img[ROWS];
+    int hi0[ROWS], wi0[ROWS];
     const int HoWo = op.Ho * op.Wo;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int m = m0 + rsub + 32 * i;
-      ar[i].ok = m < op.M;
-      const int mm = ar[i].ok ? m : 0;
-      const int b = mm / HoWo;
-      const int rem = mm - b * HoWo;
-      const int ho = rem / op.Wo;
-      const int wo = rem - ho * op.Wo;
-      ar[i].img = in + static_cast<size_t>(b) * op.H * op.W * op.ldi;
-      ar[i].hi0 = ho * op.stride - op.ph;
-      ar[i].wi0 = wo * op.stride - op.pw;
+    for (int i = 0; i < ROWS; ++i) {
+      const int m = m0 + rsub + 16 * i;
+      const bool ok = m < op.M;
+      const int mm = ok ? m : 0;
+      const int b = mm / HoWo, rem = mm - b * HoWo, ho = rem / op.Wo, wo = rem - (rem / op.Wo) * op.Wo;
+      img[i] = in + static_cast<size_t>(b) * op.H * op.W * op.ldi;
+      hi0[i] = ok ? ho * op.stride - op.ph : -100000;
+      wi0[i] = wo * op.stride - op.pw;
     }
-  }
-
-  auto load_stage = [&](int kb, uint32_t stage) {
-    const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
-    const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
-    const int k = kb * BK + chunk * 8;
-    if (!op.swap) {
-      // A: im2col gather, one 16-byte chunk = 8 channels of one filter tap
+    for (int i = 0; i < nk; ++i) {
+      const uint32_t gi = g + i, stage = gi % STAGES;
+      if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
+      const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
+      const int k0 = (kb0 + i) * BK;
+      if (ptid == 0) {
+        mbar_expect_tx(&ctl->full[stage], bbytes);
+        tma_load_2d(ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES, op.tmap_b, &ctl->full[stage], k0,
+                    n0);
+      }
+      const int k = k0 + chunk * 8;
       const bool kok = k < op.K;
       const int tap = k / op.C;
       const int c = k - tap * op.C;
-      const int r = tap / op.kw;
-      const int s = tap - r * op.kw;
+      const int r = tap / op.kw, s = tap - (tap / op.kw) * op.kw;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = rsub + 32 * i;
-        const int hi = ar[i].hi0 + r, wi = ar[i].wi0 + s;
-        const bool ok = kok && ar[i].ok && hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
-        const __nv_bfloat16* src = ok ? ar[i].img + (static_cast<size_t>(hi) * op.W + wi) * op.ldi + c : in;
-        cp_async16(a_base + row * 128 + ((chunk ^ (row & 7)) << 4), src, ok);
+      for (int j = 0; j < ROWS; ++j) {
+        const int row = rsub + 16 * j;
+        const int hi = hi0[j] + r, wi = wi0[j] + s;
+        const bool ok = kok && hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
+        const __nv_bfloat16* src = ok ? img[j] + (static_cast<size_t>(hi) * op.W + wi) * op.ldi + c : in;
+        cp_async16(a_dst + row * 128 + ((chunk ^ (row & 7)) << 4), src, ok);
       }
-      // B: packed weights [Npad][Kpad], zero-padded
-      load_rows_tile(b_base, static_cast<const __nv_bfloat16*>(op.wt), op.ldw, n0, bn, op.tiles_n * bn, k,
-                     op.Kpad, chunk, rsub);
-    } else {
-      load_rows_tile(a_base, static_cast<const __nv_bfloat16*>(op.wt), op.ldw, m0, BM, op.tiles_m * BM, k,
-                     op.Kpad, chunk, rsub);
-      load_rows_tile(b_base, static_cast<const __nv_bfloat16*>(op.act_b), op.ldb, n0, bn, op.B, k, op.K, chunk,
-                     rsub);
+      cp_async_commit();
+      if (i >= LAG) {
+        cp_async_wait<LAG>();
+        fence_proxy_async_smem();
+        named_bar_sync(1, NPROD);
+        if (ptid == 0) mbar_arrive(&ctl->full[(g + i - LAG) % STAGES]);
+      }
     }
-  };
-  auto wait_free = [&](uint32_t g) {
-    if (g >= STAGES) mbar_wait(&cx.ctl->mma_done[g % STAGES], ((g / STAGES) + 1) & 1);
-  };
-
-  // ---- main loop: STAGES-1 K-blocks in flight
-#pragma unroll 1
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) {
-      wait_free(cx.ring_pos + s);
-      load_stage(kb0 + s, (cx.ring_pos + s) % STAGES);
-    }
-    cp_async_commit();
-  }
-#pragma unroll 1
-  for (int i = 0; i < nk; ++i) {
-    const int il = i + STAGES - 1;
-    if (il < nk) {
-      wait_free(cx.ring_pos + il);
-      load_stage(kb0 + il, (cx.ring_pos + il) % STAGES);
-    }
-    cp_async_commit();
-    cp_async_wait<STAGES - 1>();
+    cp_async_wait<0>();
     fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t stage = (cx.ring_pos + i) % STAGES;
-      const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
-      const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk) {
-        umma_bf16(cx.tmem, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
-                  (i > 0 || kk > 0) ? 1u : 0u);
-      }
-      umma_commit(&cx.ctl->mma_done[stage]);
-      if (i == nk - 1) umma_commit(&cx.ctl->acc_bar);
-    }
+    named_bar_sync(1, NPROD);
+    if (ptid == 0)
+      for (int i = (nk > LAG ? nk - LAG : 0); i < nk; ++i) mbar_arrive(&ctl->full[(g + i) % STAGES]);
   }
-  cx.ring_pos += nk;
-
-  // ---- accumulator ready
-  mbar_wait(&cx.ctl->acc_bar, cx.acc_uses & 1);
-  cx.acc_uses++;
-  tc_fence_after();
-
-  const int warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, h = warp >> 2;
-  const int row = q * 32 + lane;
-  const int half = bn >> 1;
-  const uint32_t tbase = cx.tmem + (static_cast<uint32_t>(q * 32) << 16);
-
-  if (op.split_k == 1) {
-    for (int c = 0; c < half; c += 8) {
-      float v[8];
-      tmem_ld8(tbase + h * half + c, v);
-      epilogue_store8(op, m0 + row, n0 + h * half + c, v);
-    }
-    tc_fence_before();
-  } else {
-    // write fp32 partial, last arriver reduces in fixed ks order
-    const int tile = it.mt * op.tiles_n + it.nt;
-    float* part = op.partial + (static_cast<size_t>(tile) * op.split_k) * (BM * bn);
-    float* mine = part + static_cast<size_t>(it.ks) * (BM * bn) + row * bn;
-    for (int c = 0; c < half; c += 8) {
-      float v[8];
-      tmem_ld8(tbase + h * half + c, v);
-      float* o = mine + h * half + c;
-      __stcg(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
-      __stcg(reinterpret_cast<float4*>(o + 4), make_float4(v[4], v[5], v[6], v[7]));
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      const uint32_t old = atomicAdd(op.tile_cnt + tile, 1u);
-      const int last = (old == static_cast<uint32_t>(op.split_k - 1));
-      if (last) op.tile_cnt[tile] = 0;  // all arrivals done: re-arm for the next round
-      cx.ctl->flag = last;
-      __threadfence();
-    }
-    __syncthreads();
-    if (cx.ctl->flag) {
-      for (int c = 0; c < half; c += 8) {
-        float acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-        for (int ks = 0; ks < op.split_k; ++ks) {
-          const float* p = part + static_cast<size_t>(ks) * (BM * bn) + row * bn + h * half + c;
-          const float4 a = __ldcg(reinterpret_cast<const float4*>(p));
-          const float4 b = __ldcg(reinterpret_cast<const float4*>(p + 4));
-          acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-          acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
-        }
-        epilogue_store8(op, m0 + row, n0 + h * half + c, acc);
-      }
-    }
-  }
+  g += nk;
 }
 
 // =====================================================================
 // fp32 SIMT GEMM (fp32 tenants): conv / linear-as-conv, fixed K order
 // =====================================================================
-__device__ void simt_item(const OpDev& op, const Item& it) {
+__device__ void simt_item(const OpDev& op, const Item& it, int tid, int nthr) {
   const float* in = static_cast<const float*>(op.in);
   const float* w = static_cast<const float*>(op.wt);
   const int m0 = it.mt * op.bm, n0 = it.nt * op.bn;
   const int HoWo = op.Ho * op.Wo;
-  for (int e = threadIdx.x; e < op.bm * op.bn; e += NTHREADS) {
+  for (int e = tid; e < op.bm * op.bn; e += nthr) {
     const int m = m0 + e / op.bn, n = n0 + e % op.bn;
     if (m >= op.M || n >= op.Cout) continue;
     const int b = m / HoWo, rem = m - b * HoWo, ho = rem / op.Wo, wo = rem - ho * op.Wo;
@@ -499,23 +484,22 @@ __device__ __forceinline__ void store8(void* base, size_t idx, const float* y, b
   }
 }
 
-// tile: bm output pixels x bn channels; G = bn/8 channel groups, each thread
-// handles pixel p = tid / G + j * (NTHREADS / G), group tid % G.
+// tile: bm output pixels x bn channels; G = bn/8 channel groups; thread tid
+// (of CC_THREADS) handles pixel tid / G + j * (CC_THREADS / G), group tid % G.
+// Runs on the producer warps (named barrier 1) or a standalone CTA.
 template <bool F32>
-__device__ void cc_item(const OpDev& op, const Item& it, Ctx& cx) {
-  const int tid = threadIdx.x;
+__device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
   const int G = op.bn >> 3;
   const int g = tid % G;
-  const int pstep = NTHREADS / G;
+  const int pstep = CC_THREADS / G;
   const int c = it.nt * op.bn + g * 8;
   if (op.kind == DK_GAP) {
-    // rows are samples; each (sample, 8 channels) is the mean over H*W pixels,
-    // summed in a fixed order: lane l sums pixels l, l+L, ..., then the L lane
-    // partials are added in lane order.
+    // rows are samples; (sample, 8 channels) = mean over H*W pixels, summed in
+    // a fixed order: lane l sums pixels l, l+L, ..., then the L lane partials
+    // are added in lane order.
     const int L = pstep;
     const int lane = tid / G;
     const int HW = op.H * op.W;
-    float* red = cx.gap_red;
     for (int b = it.mt * op.bm; b < min(op.B, (it.mt + 1) * op.bm); ++b) {
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (c < op.C) {
@@ -528,7 +512,7 @@ __device__ void cc_item(const OpDev& op, const Item& it, Ctx& cx) {
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) red[(lane * G + g) * 8 + j] = acc[j];
-      __syncthreads();
+      named_bar_sync(1, CC_THREADS);
       if (tid < G * 8) {
         const int gg = tid >> 3, jj = tid & 7;
         const int cc = it.nt * op.bn + gg * 8 + jj;
@@ -540,7 +524,7 @@ __device__ void cc_item(const OpDev& op, const Item& it, Ctx& cx) {
           else static_cast<__nv_bfloat16*>(op.out)[static_cast<size_t>(b) * op.ldo + cc] = __float2bfloat16_rn(y);
         }
       }
-      __syncthreads();
+      named_bar_sync(1, CC_THREADS);
     }
     return;
   }
@@ -636,40 +620,28 @@ __device__ void cc_item(const OpDev& op, const Item& it, Ctx& cx) {
   }
 }
 
-__device__ __forceinline__ void run_item(const OpDev& op, const Item& it, Ctx& cx) {
-  switch (op.kind) {
-    case DK_GEMM: gemm_item(op, it, cx); break;
-    case DK_SIMT_GEMM: simt_item(op, it); break;
-    default:
-      if (op.f32) cc_item<true>(op, it, cx);
-      else cc_item<false>(op, it, cx);
-  }
+__device__ __forceinline__ void run_cc(const OpDev& op, const Item& it, int tid, float* red) {
+  if (op.kind == DK_SIMT_GEMM) simt_item(op, it, tid, CC_THREADS);
+  else if (op.f32) cc_item<true>(op, it, tid, red);
+  else cc_item<false>(op, it, tid, red);
+}
+
+__device__ __forceinline__ Item decode_single(const OpDev& op, int op_idx, int b) {
+  Item it;
+  it.op = op_idx;
+  const int split = op.kind == DK_GEMM ? op.split_k : 1;
+  it.ks = b % split;
+  b /= split;
+  it.nt = b % op.tiles_n;
+  it.mt = b / op.tiles_n;
+  it.dep_begin = it.dep_count = 0;
+  it.chunk = -1;
+  it.cluster = 0;
+  return it;
 }
 
 // =====================================================================
-// CTA setup shared by the executor and the standalone GEMM kernel
-// =====================================================================
-__device__ __forceinline__ void cta_setup(Ctx& cx, uint8_t* smem_raw, uint32_t tmem_cols, bool need_tmem) {
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  cx.ring = base;
-  cx.ctl = reinterpret_cast<SmemCtl*>(base + SMEM_RING_BYTES);
-  cx.gap_red = reinterpret_cast<float*>(base);
-  cx.ring_pos = 0;
-  cx.acc_uses = 0;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&cx.ctl->mma_done[s], 1);
-    mbar_init(&cx.ctl->acc_bar, 1);
-    fence_mbar_init();
-  }
-  if (need_tmem && (threadIdx.x >> 5) == 0) tmem_alloc(&cx.ctl->tmem_base, tmem_cols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  cx.tmem = need_tmem ? cx.ctl->tmem_base : 0;
-}
-
-// =====================================================================
-// The persistent multi-tenant executor
+// the persistent multi-tenant executor
 // =====================================================================
 // Spin until *ctr >= target, with watchdog; returns false on abort.
 __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& p) {
@@ -677,7 +649,7 @@ __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& 
   const uint64_t t0 = globaltimer();
   uint32_t it = 0;
   while (ld_acquire(ctr) < target) {
-    __nanosleep(64);
+    __nanosleep(32);
     if ((++it & 255) == 0) {
       if (*reinterpret_cast<volatile int32_t*>(p.error)) return false;
       if (static_cast<int64_t>(globaltimer() - t0) > p.watchdog_ns) {
@@ -689,75 +661,245 @@ __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& 
   return true;
 }
 
-extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor(ExecParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  Ctx cx;
-  cta_setup(cx, smem_raw, 256, true);
-  SmemCtl* ctl = cx.ctl;
-  const int tid = threadIdx.x;
+// Scheduler (producer thread 0): claim the next item of the open cluster k.
+// Returns the item index, -2 when the round is done, -3 on abort.
+__device__ int claim_item(const ExecParams& p, int& k) {
   const int32_t* pref = p.cta_pref + static_cast<size_t>(blockIdx.x) * p.n_tenants;
-  int k = 0;  // open cluster (thread 0's view)
+  while (k < p.n_clusters) {
+    for (int j = 0; j < p.n_tenants; ++j) {
+      const int t = pref[j];
+      if (t < 0) break;
+      const int si = t * p.n_clusters + k;
+      const Seg sg = p.segs[si];
+      if (sg.size == 0) continue;
+      if (ld_relaxed(p.heads + si) >= static_cast<uint32_t>(sg.size)) continue;
+      const uint32_t idx = atomicAdd(p.heads + si, 1u);
+      if (idx < static_cast<uint32_t>(sg.size)) return p.queue[sg.begin + idx];
+    }
+    // nothing left to claim in cluster k: the synchronisation pointer --
+    // wait until every item of cluster k (all tenants) is done.
+    if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) return -3;
+    ++k;
+  }
+  return -2;
+}
 
+__device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, int idx, uint64_t t0,
+                                             const OpDev& op) {
+  // caller: all writes of the item are ordered before this thread (barrier)
+  __threadfence();
+  atomicAdd(p.chunk_done + it.chunk, 1u);
+  atomicAdd(p.cluster_done + it.cluster, 1u);
+  if (p.trace) {
+    int64_t* rec = p.trace + static_cast<size_t>(idx) * 8;
+    rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = idx;
+    rec[4] = it.cluster; rec[5] = it.chunk;
+    rec[6] = static_cast<int64_t>(t0); rec[7] = static_cast<int64_t>(globaltimer());
+  }
+}
+
+__device__ void producer_role(const ExecParams& p, Ctx& cx) {
+  const int ptid = threadIdx.x;
+  SmemCtl* ctl = cx.ctl;
+  uint32_t g = 0, islot = 0;
+  int k = 0;
+  int sidx = blockIdx.x;
   for (;;) {
-    if (tid == 0) {
-      int claimed = -2;  // -2 = round finished, -3 = abort
-      while (k < p.n_clusters) {
-        int got = -1;
-        for (int j = 0; j < p.n_tenants && got < 0; ++j) {
-          const int t = pref[j];
-          if (t < 0) break;
-          const int si = t * p.n_clusters + k;
-          const Seg sg = p.segs[si];
-          if (sg.size == 0) continue;
-          if (ld_relaxed(p.heads + si) >= static_cast<uint32_t>(sg.size)) continue;
-          const uint32_t idx = atomicAdd(p.heads + si, 1u);
-          if (idx < static_cast<uint32_t>(sg.size)) got = p.queue[sg.begin + idx];
+    if (ptid == 0) {
+      int claimed;
+      if (p.single_op >= 0) {
+        const OpDev& op = p.ops[p.single_op];
+        const int n = op.tiles_m * op.tiles_n * (op.kind == DK_GEMM ? op.split_k : 1);
+        claimed = sidx < n ? sidx : -2;
+        if (claimed >= 0) ctl->cur = decode_single(op, p.single_op, sidx);
+        sidx += gridDim.x;
+      } else {
+        claimed = claim_item(p, k);
+        if (claimed >= 0) {
+          const Item it = p.items[claimed];
+          ctl->cur = it;
+          for (int d = 0; d < it.dep_count; ++d) {
+            const Dep dp = p.deps[it.dep_begin + d];
+            if (!spin_ge(p.chunk_done + dp.counter, p.epoch * dp.target, p)) { claimed = -3; break; }
+          }
+          // acquire: producers' generic writes -> this CTA's generic and TMA reads
+          __threadfence();
+          fence_proxy_async_global();
         }
-        if (got >= 0) { claimed = got; break; }
-        // nothing left to claim in cluster k: the synchronisation pointer --
-        // wait until every item of cluster k (all tenants) is done.
-        if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) { claimed = -3; break; }
-        ++k;
       }
-      if (claimed >= 0) {
-        const Item it = p.items[claimed];
-        ctl->item = it;
-        // producer -> consumer dependencies (chunk counters)
-        for (int d = 0; d < it.dep_count; ++d) {
-          const Dep dp = p.deps[it.dep_begin + d];
-          if (!spin_ge(p.chunk_done + dp.counter, p.epoch * dp.target, p)) { claimed = -3; break; }
-        }
-        __threadfence();  // acquire side: invalidate stale L1 lines before the CTA reads inputs
+      ctl->cur_t0 = p.trace ? globaltimer() : 0;
+      const bool gemm = claimed >= 0 && p.ops[ctl->cur.op].kind == DK_GEMM;
+      if (claimed < 0 || gemm) {  // GEMM items and the STOP marker go to the MMA/epilogue ring
+        const uint32_t slot = islot % ITEM_RING;
+        if (islot >= ITEM_RING) mbar_wait(&ctl->rempty[slot], ((islot / ITEM_RING) + 1) & 1);
+        ctl->ring[slot].it = ctl->cur;
+        ctl->ring[slot].idx = claimed >= 0 ? claimed : -1;
+        ctl->ring[slot].t0 = ctl->cur_t0;
+        mbar_arrive(&ctl->rfull[slot]);
+        ++islot;
       }
       ctl->claimed = claimed;
     }
-    __syncthreads();
+    named_bar_sync(1, NPROD);
     const int claimed = ctl->claimed;
     if (claimed < 0) break;
-    const Item it = ctl->item;
+    const Item it = ctl->cur;
+    const uint64_t t0 = ctl->cur_t0;
     const OpDev& op = p.ops[it.op];
-    uint64_t t_start = 0;
-    if (p.trace && tid == 0) t_start = globaltimer();
-    run_item(op, it, cx);
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();  // release: the item's global writes before the counters
-      atomicAdd(p.chunk_done + it.chunk, 1u);
-      atomicAdd(p.cluster_done + it.cluster, 1u);
-      if (p.trace) {
-        int64_t* rec = p.trace + static_cast<size_t>(claimed) * 8;
-        rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = claimed;
-        rec[4] = it.cluster; rec[5] = it.chunk;
-        rec[6] = static_cast<int64_t>(t_start); rec[7] = static_cast<int64_t>(globaltimer());
+    if (op.kind == DK_GEMM) {
+      produce_gemm(op, it, cx, g);
+    } else {
+      run_cc(op, it, ptid, ctl->red);
+      named_bar_sync(1, NPROD);
+      if (ptid == 0 && p.single_op < 0) release_item(p, it, claimed, t0, op);
+    }
+    named_bar_sync(1, NPROD);  // ctl->cur may be overwritten after this
+  }
+}
+
+__device__ void mma_role(const ExecParams& p, Ctx& cx) {
+  SmemCtl* ctl = cx.ctl;
+  uint32_t g = 0, islot = 0, acc = 0;
+  const uint32_t ring_base = smem_u32(cx.ring);
+  for (;;) {
+    const uint32_t slot = islot % ITEM_RING;
+    mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
+    const int idx = ctl->ring[slot].idx;
+    const Item it = ctl->ring[slot].it;
+    mbar_arrive(&ctl->rempty[slot]);
+    ++islot;
+    if (idx < 0) break;
+    const OpDev& op = p.ops[it.op];
+    int kb0, nk;
+    kb_range(op, it.ks, kb0, nk);
+    const uint32_t abuf = acc & 1;
+    if (acc >= 2) mbar_wait(&ctl->tempty[abuf], ((acc / 2) + 1) & 1);
+    tc_fence_after();
+    const uint32_t d = cx.tmem + abuf * BN_MAX;
+    const uint32_t idesc = make_idesc(op.bn);
+    for (int i = 0; i < nk; ++i) {
+      const uint32_t stage = g % STAGES;
+      mbar_wait(&ctl->full[stage], (g / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
+      const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk)
+        umma_bf16(d, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
+                  (i > 0 || kk > 0) ? 1u : 0u);
+      umma_commit(&ctl->empty[stage]);
+      ++g;
+    }
+    umma_commit(&ctl->tfull[abuf]);
+    ++acc;
+  }
+}
+
+__device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
+  SmemCtl* ctl = cx.ctl;
+  const int etid = threadIdx.x - NPROD;  // 0..127
+  const int ew = etid >> 5, lane = etid & 31;  // warp 4+ew accesses TMEM lanes 32*ew..
+  uint32_t islot = 0, acc = 0;
+  for (;;) {
+    const uint32_t slot = islot % ITEM_RING;
+    mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
+    const int idx = ctl->ring[slot].idx;
+    const Item it = ctl->ring[slot].it;
+    const uint64_t t0 = ctl->ring[slot].t0;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl->rempty[slot]);
+    ++islot;
+    if (idx < 0) break;
+    const OpDev& op = p.ops[it.op];
+    const int bn = op.bn;
+    const uint32_t abuf = acc & 1;
+    mbar_wait(&ctl->tfull[abuf], (acc / 2) & 1);
+    tc_fence_after();
+    const int row = ew * 32 + lane;
+    const int m0 = it.mt * BM, n0 = it.nt * bn;
+    const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(ew * 32) << 16);
+    float* part = nullptr;
+    const int tile = it.mt * op.tiles_n + it.nt;
+    if (op.split_k == 1) {
+      for (int c = 0; c < bn; c += 16) {
+        float v[16];
+        tmem_ld16(taddr + c, v);
+        epilogue_store8(op, m0 + row, n0 + c, v);
+        epilogue_store8(op, m0 + row, n0 + c + 8, v + 8);
+      }
+    } else {
+      part = op.partial + static_cast<size_t>(tile) * op.split_k * (BM * bn);
+      float* mine = part + static_cast<size_t>(it.ks) * (BM * bn) + row * bn;
+      for (int c = 0; c < bn; c += 16) {
+        float v[16];
+        tmem_ld16(taddr + c, v);
+#pragma unroll
+        for (int q = 0; q < 16; q += 4)
+          __stcg(reinterpret_cast<float4*>(mine + c + q), make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
       }
     }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl->tempty[abuf]);
+    ++acc;
+    if (op.split_k > 1) {
+      named_bar_sync(2, NEPI);
+      if (etid == 0) {
+        __threadfence();
+        const uint32_t old = atomicAdd(op.tile_cnt + tile, 1u);
+        const int last = (old == static_cast<uint32_t>(op.split_k - 1));
+        if (last) op.tile_cnt[tile] = 0;  // all arrivals done: re-arm for the next round
+        ctl->epi_flag = last;
+        __threadfence();
+      }
+      named_bar_sync(2, NEPI);
+      if (ctl->epi_flag) {
+        for (int c = 0; c < bn; c += 8) {
+          float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int ks = 0; ks < op.split_k; ++ks) {  // fixed order: bit-identical in every mode
+            const float* q = part + static_cast<size_t>(ks) * (BM * bn) + row * bn + c;
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(q));
+            const float4 b = __ldcg(reinterpret_cast<const float4*>(q + 4));
+            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+          }
+          epilogue_store8(op, m0 + row, n0 + c, s);
+        }
+      }
+    }
+    fence_proxy_async_global();  // generic stores -> later TMA reads by consumers
+    named_bar_sync(2, NEPI);
+    if (etid == 0 && p.single_op < 0) release_item(p, it, idx, t0, op);
   }
+}
 
-  // teardown
+__device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Ctx cx;
+  cx.ring = base;
+  cx.ctl = reinterpret_cast<SmemCtl*>(base + SMEM_RING_BYTES);
+  SmemCtl* ctl = cx.ctl;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&ctl->full[s], 1); mbar_init(&ctl->empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&ctl->tfull[a], 1); mbar_init(&ctl->tempty[a], NEPI / 32); }
+    for (int r = 0; r < ITEM_RING; ++r) { mbar_init(&ctl->rfull[r], 1); mbar_init(&ctl->rempty[r], 1 + NEPI / 32); }
+    fence_mbar_init();
+  }
+  if (warp == MMA_WARP) tmem_alloc(&ctl->tmem_base, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
-  if ((tid >> 5) == 0) tmem_dealloc(cx.tmem, 256);
-  if (tid == 0) {
+  tc_fence_after();
+  cx.tmem = ctl->tmem_base;
+
+  if (warp < NPROD / 32) producer_role(p, cx);
+  else if (warp < (NPROD + NEPI) / 32) epilogue_role(p, cx);
+  else if ((tid & 31) == 0) mma_role(p, cx);
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) tmem_dealloc(cx.tmem, TMEM_COLS);
+  if (tid == 0 && p.single_op < 0) {
     __threadfence();
     const uint32_t old = atomicAdd(p.exit_count, 1u);
     if (old == gridDim.x - 1) {  // last CTA out re-arms the claim counters
@@ -768,61 +910,48 @@ extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor(ExecPar
   }
 }
 
-// =====================================================================
-// Standalone per-op kernels (baselines): same tile functions
-// =====================================================================
-extern "C" __global__ void __launch_bounds__(NTHREADS, 1) op_gemm_kernel(const OpDev* ops, int op_idx) {
+extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor(ExecParams p) {
   extern __shared__ uint8_t smem_raw[];
-  Ctx cx;
-  cta_setup(cx, smem_raw, 128, true);
-  const OpDev& op = ops[op_idx];
-  Item it;
-  int b = blockIdx.x;
-  it.op = op_idx;
-  it.ks = b % op.split_k;
-  b /= op.split_k;
-  it.nt = b % op.tiles_n;
-  it.mt = b / op.tiles_n;
-  gemm_item(op, it, cx);
-  tc_fence_before();
-  __syncthreads();
-  if ((threadIdx.x >> 5) == 0) tmem_dealloc(cx.tmem, 128);
+  executor_body(p, smem_raw);
 }
 
-extern "C" __global__ void __launch_bounds__(NTHREADS) op_cc_kernel(const OpDev* ops, int op_idx) {
-  __shared__ __align__(16) float red[GAP_RED_FLOATS];
-  Ctx cx;
-  cx.gap_red = red;
+// Standalone CUDA-core op kernel (baselines): one item per CTA, same tile function.
+extern "C" __global__ void __launch_bounds__(CC_THREADS) op_cc_kernel(const OpDev* ops, int op_idx) {
+  __shared__ __align__(16) float red[CC_THREADS * 8];
   const OpDev& op = ops[op_idx];
-  Item it;
-  it.op = op_idx;
-  it.ks = 0;
-  it.nt = blockIdx.x % op.tiles_n;
-  it.mt = blockIdx.x / op.tiles_n;
-  if (op.kind == DK_SIMT_GEMM) simt_item(op, it);
-  else if (op.f32) cc_item<true>(op, it, cx);
-  else cc_item<false>(op, it, cx);
+  const Item it = decode_single(op, op_idx, blockIdx.x);
+  run_cc(op, it, threadIdx.x, red);
 }
 
 // =====================================================================
 // host-side launchers (C++ linkage, used by host.cpp)
 // =====================================================================
-int executor_smem_bytes() { return SMEM_GEMM_BYTES; }
+int executor_smem_bytes() { return SMEM_BYTES; }
 
 cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(gacer_executor, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_GEMM_BYTES);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(op_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_GEMM_BYTES);
+  return cudaFuncSetAttribute(gacer_executor, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
 cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s) {
-  gacer_executor<<<grid, NTHREADS, SMEM_GEMM_BYTES, s>>>(p);
+  gacer_executor<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_op(const OpDev* ops_dev, int op_idx, int kind, int n_blocks, cudaStream_t s) {
-  if (kind == DK_GEMM) op_gemm_kernel<<<n_blocks, NTHREADS, SMEM_GEMM_BYTES, s>>>(ops_dev, op_idx);
-  else op_cc_kernel<<<n_blocks, NTHREADS, 0, s>>>(ops_dev, op_idx);
+// Standalone per-op launch (sequential / multi-stream baselines).  GEMM ops
+// run the executor kernel in single-op mode: persistent over the op's tiles,
+// the same warp-specialised pipeline and tile functions.
+cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, int kind, int n_items, int num_sms,
+                      cudaStream_t s) {
+  if (kind == DK_GEMM) {
+    ExecParams p = base;
+    p.ops = ops_dev;
+    p.single_op = op_idx;
+    p.trace = nullptr;
+    const int grid = n_items < num_sms ? n_items : num_sms;
+    gacer_executor<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
+  } else {
+    op_cc_kernel<<<n_items, CC_THREADS, 0, s>>>(ops_dev, op_idx);
+  }
   return cudaGetLastError();
 }
 

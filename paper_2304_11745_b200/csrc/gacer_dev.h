@@ -24,9 +24,18 @@ enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2 };
 constexpr int BM = 128;           // rows per tile (UMMA M)
 constexpr int BK = 64;            // bf16 elements per K-block = one 128-byte swizzle row
 constexpr int BN_MAX = 128;       // max UMMA N per tile
-constexpr int STAGES = 4;         // smem ring depth
-constexpr int NTHREADS = 256;     // threads per CTA (8 warps)
+constexpr int STAGES = 6;         // smem ring depth (A 16 KB + B 16 KB per stage)
+constexpr int ITEM_RING = 4;      // scheduler -> MMA/epilogue item queue depth
+// warp roles of the executor CTA
+constexpr int NPROD = 128;        // warps 0-3: scheduler (thread 0) + loads + CUDA-core items
+constexpr int NEPI = 128;         // warps 4-7: TMEM -> register epilogue (lane quarter = warp % 4)
+constexpr int MMA_WARP = 8;       // warp 8: single-thread tcgen05.mma issue
+constexpr int NTHREADS = NPROD + NEPI + 32;
+constexpr int CC_THREADS = NPROD; // threads that execute a CUDA-core item
 constexpr int CC_TASKS_PER_THREAD = 4;
+
+// operand A load mode of a GEMM op
+enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2 };
 
 struct OpDev {
   int32_t kind;            // DevKind
@@ -65,6 +74,10 @@ struct OpDev {
   const float* bias;       // [Cout] folded BN shift + conv bias
   float* partial;          // split-K workspace [tiles][split][BM*bn] fp32
   uint32_t* tile_cnt;      // split-K arrival counters [tiles]
+  const void* tmap_a;      // CUtensorMap (64 B aligned, device memory): im2col or tiled A
+  const void* tmap_b;      // CUtensorMap: tiled B (weights, or activations for swap-AB)
+  int32_t a_mode;          // AMode
+  int32_t pad4;
 };
 
 // One work item: one output tile (mt, nt) of one op, K-slice ks.
@@ -103,6 +116,8 @@ struct ExecParams {
   uint32_t epoch;           // round number since plan install, >= 1
   int32_t n_heads;
   int64_t watchdog_ns;
+  int32_t single_op;        // >= 0: standalone mode, run every tile of this op (strided over CTAs)
+  int32_t pad;
 };
 
 }  // namespace gacer

@@ -5,6 +5,8 @@
 // -- mask/list_B (§4.2 l.657-685, Eq. 5) and Matrix_P (§4.3 l.742-753,
 // Eq. 6/7) -- into per-(tenant, cluster) work queues, per-item dependency
 // lists and cluster totals that the persistent kernel enforces on-device.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,7 +27,8 @@ namespace gacer {
 int executor_smem_bytes();
 cudaError_t configure_kernels();
 cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s);
-cudaError_t launch_op(const OpDev* ops_dev, int op_idx, int kind, int n_blocks, cudaStream_t s);
+cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, int kind, int n_items, int num_sms,
+                      cudaStream_t s);
 }  // namespace gacer
 
 using namespace gacer;
@@ -99,6 +102,7 @@ struct FusedOp {
   uint32_t* d_tile_cnt = nullptr;
   double flops = 0, bytes = 0;
   bool rows_are_pixels = true;  // output pixel rows are the GEMM/tile M axis
+  int a_mode = A_GATHER;        // GEMM operand-A load path
 };
 
 struct Tenant {
@@ -153,9 +157,11 @@ struct State {
   Plan plan;
   int mode = GACER_MODE_EXECUTOR;
   bool sticky_cuda = false;
-  // device op table
+  // device op table + TMA descriptors (2 per op)
   OpDev* d_ops = nullptr;
   std::vector<OpDev> h_ops;
+  CUtensorMap* d_tmaps = nullptr;
+  size_t n_tmaps = 0;
   // device plan
   Item* d_items = nullptr;
   Dep* d_deps = nullptr;
@@ -619,6 +625,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           rows = static_cast<size_t>(F.tiles_n) * F.bn;
         }
         F.bm = BM;
+        F.a_mode = F.swap ? A_ROWS : (F.cread % 64 == 0 ? A_IM2COL : A_GATHER);
         // split-K: a function of the layer shape only (same in every mode/plan)
         const int tiles = F.tiles_m * F.tiles_n;
         int sk = 1;
@@ -658,7 +665,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
     if (F.kind != DK_GEMM && F.kind != DK_SIMT_GEMM) {
       F.bn = std::min(64, pow2ceil(roundup(F.Cout, 8)));
       const int G = F.bn / 8;
-      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : CC_TASKS_PER_THREAD * (NTHREADS / G);
+      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : CC_TASKS_PER_THREAD * (CC_THREADS / G);
       F.tiles_m = cdiv(F.M, F.bm);
       F.tiles_n = cdiv(F.Cout, F.bn);
       F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
@@ -759,14 +766,95 @@ OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
   return d;
 }
 
+// ---- TMA descriptors (driver entry points resolved through the runtime)
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
+
+int load_tma_encoders() {
+  if (g_encode_tiled && g_encode_im2col) return 0;
+  cudaDriverEntryPointQueryResult q;
+  void* f = nullptr;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+  g_encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q));
+  g_encode_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(f);
+  if (!g_encode_tiled || !g_encode_im2col) return set_err(GACER_E_CUDA, "cuTensorMapEncode* not available");
+  return 0;
+}
+
+// K-major bf16 matrix [rows][ld] (row stride ld elements), box {64, box_rows},
+// 128-byte swizzle = the UMMA SWIZZLE_128B K-major canonical layout.
+int encode_rows(CUtensorMap* m, const void* base, int cols, int rows, int ld, int box_rows) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return 0;
+}
+
+// NHWC bf16 activation as an im2col view: 128 output pixels x 64 channels of
+// one filter tap per load (pixelsPerColumn = BM, channelsPerPixel = BK).
+// Bounding box per CUTLASS fprop convention: lower = -pad, upper = pad - (k-1).
+int encode_im2col(CUtensorMap* m, const OpDev& d) {
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.C), static_cast<cuuint64_t>(d.W),
+                              static_cast<cuuint64_t>(d.H), static_cast<cuuint64_t>(d.B)};
+  const cuuint64_t st[3] = {static_cast<cuuint64_t>(d.ldi) * 2, static_cast<cuuint64_t>(d.ldi) * 2 * d.W,
+                            static_cast<cuuint64_t>(d.ldi) * 2 * d.W * d.H};
+  const int lower[2] = {-d.pw, -d.ph};
+  const int upper[2] = {d.pw - (d.kw - 1), d.ph - (d.kh - 1)};
+  const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(d.stride), static_cast<cuuint32_t>(d.stride), 1};
+  CUresult r = g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d.in), dims, st, lower, upper,
+                               BK, BM, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "cuTensorMapEncodeIm2col failed (%d)", static_cast<int>(r));
+  return 0;
+}
+
 int rebuild_op_table() {
   S.h_ops.clear();
+  std::vector<const FusedOp*> fops;
   for (size_t t = 0; t < S.tenants.size(); ++t) {
     Tenant& T = S.tenants[t];
     T.op_base = static_cast<int>(S.h_ops.size());
-    for (const FusedOp& F : T.fops) S.h_ops.push_back(make_opdev(T, static_cast<int>(t), F));
+    for (const FusedOp& F : T.fops) {
+      S.h_ops.push_back(make_opdev(T, static_cast<int>(t), F));
+      fops.push_back(&F);
+    }
   }
   if (S.host_only) return 0;
+  if (int rc = load_tma_encoders()) return rc;
+  const size_t n = S.h_ops.size();
+  if (S.n_tmaps < 2 * n) {
+    if (S.d_tmaps) cudaFree(S.d_tmaps);
+    S.d_tmaps = nullptr;
+    CUDA_TRY(cudaMalloc(&S.d_tmaps, 2 * n * sizeof(CUtensorMap)));  // cudaMalloc: 256-byte aligned
+    S.n_tmaps = 2 * n;
+  }
+  std::vector<CUtensorMap> maps(2 * n);
+  std::memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
+  for (size_t i = 0; i < n; ++i) {
+    OpDev& d = S.h_ops[i];
+    if (d.kind != DK_GEMM) continue;
+    const FusedOp& F = *fops[i];
+    d.a_mode = F.a_mode;
+    d.tmap_a = S.d_tmaps + 2 * i;
+    d.tmap_b = S.d_tmaps + 2 * i + 1;
+    if (!d.in || !d.out) continue;  // I/O not bound yet: re-encoded by gacer_bind_io
+    int rc = 0;
+    if (d.swap) {
+      rc = encode_rows(&maps[2 * i], d.wt, d.Kpad, d.tiles_m * BM, d.Kpad, BM);
+      if (!rc) rc = encode_rows(&maps[2 * i + 1], d.act_b, d.K, d.B, d.ldb, d.bn);
+    } else {
+      if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[2 * i], d);
+      if (!rc) rc = encode_rows(&maps[2 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
+    }
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaMemcpy(S.d_tmaps, maps.data(), 2 * n * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   return dev_upload(&S.d_ops, S.h_ops.data(), S.h_ops.size());
 }
 
@@ -1017,6 +1105,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     p.epoch = ++S.epoch;
     p.n_heads = p.n_tenants * p.n_clusters;
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
+    p.single_op = -1;
     CUDA_TRY(launch_executor(p, S.grid, st));
     launches = 1;
   } else {
@@ -1038,7 +1127,11 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
       for (size_t f = 0; f < T.fops.size(); ++f) {
         const FusedOp& F = T.fops[f];
         const int nb = F.tiles_m * F.tiles_n * (F.kind == DK_GEMM ? F.split_k : 1);
-        CUDA_TRY(launch_op(S.d_ops, T.op_base + static_cast<int>(f), F.kind, nb, ts));
+        ExecParams base;
+        std::memset(&base, 0, sizeof base);
+        base.error = S.d_error;
+        base.watchdog_ns = 2000000000LL;
+        CUDA_TRY(launch_op(base, S.d_ops, T.op_base + static_cast<int>(f), F.kind, nb, S.num_sms, ts));
         ++launches;
       }
     }
@@ -1123,6 +1216,7 @@ int gacer_shutdown(void) {
     for (Tenant& T : S.tenants) free_tenant(T);
     free_plan_device();
     if (S.d_ops) cudaFree(S.d_ops);
+    if (S.d_tmaps) cudaFree(S.d_tmaps);
     for (cudaStream_t s : S.tstreams) cudaStreamDestroy(s);
     if (S.stream) cudaStreamDestroy(S.stream);
     if (S.ev0) cudaEventDestroy(S.ev0);
