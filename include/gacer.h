@@ -242,6 +242,13 @@ int gacer_get_trace(int64_t* records, int32_t cap);
 
 const char* gacer_last_error(void);
 
+/* Diagnostics only (not on the method's path): when the process runs with
+ * GACER_DEBUG_TIMING=1, kernels record %globaltimer milestones per CTA
+ * ([op slot][cta][16] int64; executor rounds use slot 0).  Copies up to cap
+ * values to out (may be NULL), optionally zeroes the buffer.  Returns the
+ * count copied. */
+int gacer_debug_timing(int64_t* out, int64_t cap, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -131,6 +131,13 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ void dbg_mark(const ExecParams& p, int ev) {
+  if (p.dbg) {
+    int64_t* d = p.dbg + static_cast<size_t>(blockIdx.x) * DBG_EVENTS + ev;
+    if (*d == 0) *d = static_cast<int64_t>(globaltimer());   // first occurrence only
+  }
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -218,29 +225,31 @@ constexpr int A_STAGE_BYTES = BM * 128;
 constexpr int B_STAGE_BYTES = BN_MAX * 128;
 constexpr int SMEM_RING_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES);
 constexpr int TMEM_COLS = 2 * BN_MAX;   // double-buffered accumulators
+constexpr int RING_CONSUMERS = 1 + 1 + NEPI / 32;  // worker group, MMA thread, epilogue warps
 
-struct RingSlot {            // scheduler -> MMA / epilogue
+struct RingSlot {            // scheduler -> workers / MMA / epilogue
   Item it;
-  int32_t idx;               // item index (trace), -1 = STOP
-  int32_t pad;
-  uint64_t t0;
+  int32_t idx;               // item index, -1 = STOP
+  int32_t kind;              // op kind (DK_GEMM items go to MMA + epilogue)
+  uint64_t t0;               // claim time (trace)
 };
 
 struct SmemCtl {
   uint64_t full[STAGES];     // TMA/gather -> MMA
-  uint64_t empty[STAGES];    // MMA -> producers
+  uint64_t empty[STAGES];    // MMA -> workers
   uint64_t tfull[2];         // MMA -> epilogue (accumulator ready)
   uint64_t tempty[2];        // epilogue -> MMA (accumulator drained)
   uint64_t rfull[ITEM_RING];
   uint64_t rempty[ITEM_RING];
   RingSlot ring[ITEM_RING];
-  Item cur;                  // scheduler -> producer warps
-  int32_t claimed;
   uint32_t tmem_base;
   int32_t epi_flag;
+  int32_t n_segs_smem;
   int32_t pad;
-  uint64_t cur_t0;
   float red[CC_THREADS * 8]; // GAP fixed-order reduction scratch
+  float epi_scale[BN_MAX];   // epilogue: folded BN scale / bias of the tile's columns
+  float epi_bias[BN_MAX];
+  Seg segs[MAX_SMEM_SEGS];   // (tenant, cluster) queue segments, cached
 };
 constexpr int SMEM_BYTES = SMEM_RING_BYTES + 1024 /*align slack*/ + (int)sizeof(SmemCtl);
 
@@ -253,78 +262,66 @@ struct Ctx {
 // =====================================================================
 // epilogue math (shared by every mode): y = act(acc*scale + bias [+ skip])
 // =====================================================================
-__device__ void epilogue_store8(const OpDev& op, int m, int n, const float* v) {
-  // m: GEMM row, n: first of 8 GEMM columns
-  if (!op.swap) {
-    if (m >= op.M) return;
-    if (n + 8 <= op.Cout) {
-      float y[8];
-      const float4 s0 = *reinterpret_cast<const float4*>(op.scale + n);
-      const float4 s1 = *reinterpret_cast<const float4*>(op.scale + n + 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(op.bias + n);
-      const float4 b1 = *reinterpret_cast<const float4*>(op.bias + n + 4);
-      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+// m: GEMM row; n: first of 8 GEMM columns; sc/bi: the 8 columns' scale/bias
+// (non-swap); skip8: the 8 residual values (bf16) when op.has_skip.
+__device__ __forceinline__ void epilogue_store8(const OpDev& op, int m, int n, const float* v, const float* sc,
+                                                const float* bi, const uint4& skip8) {
+  if (m >= op.M) return;
+  float y[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) y[j] = fmaf(v[j], sc[j], bi[j]);
-      if (op.has_skip) {
-        const uint4 u = *reinterpret_cast<const uint4*>(
-            static_cast<const __nv_bfloat16*>(op.skip) + static_cast<size_t>(m) * op.lds + n);
-        float s[8];
-        bf16x8_to_f32(u, s);
+  for (int j = 0; j < 8; ++j) y[j] = fmaf(v[j], sc[j], bi[j]);
+  if (op.has_skip) {
+    float s[8];
+    bf16x8_to_f32(skip8, s);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) y[j] += s[j];
-      }
+    for (int j = 0; j < 8; ++j) y[j] += s[j];
+  }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) y[j] = apply_act(y[j], op.act);
-      if (op.out_f32) {
-        float* o = static_cast<float*>(op.out) + static_cast<size_t>(m) * op.ldo + n;
-        *reinterpret_cast<float4*>(o) = make_float4(y[0], y[1], y[2], y[3]);
-        *reinterpret_cast<float4*>(o + 4) = make_float4(y[4], y[5], y[6], y[7]);
-      } else {
-        uint4 u;
-        u.x = pack_bf16x2(y[0], y[1]);
-        u.y = pack_bf16x2(y[2], y[3]);
-        u.z = pack_bf16x2(y[4], y[5]);
-        u.w = pack_bf16x2(y[6], y[7]);
-        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(op.out) + static_cast<size_t>(m) * op.ldo + n) = u;
-      }
+  for (int j = 0; j < 8; ++j) y[j] = apply_act(y[j], op.act);
+  if (n + 8 <= op.Cout) {
+    if (op.out_f32) {
+      float* o = static_cast<float*>(op.out) + static_cast<size_t>(m) * op.ldo + n;
+      *reinterpret_cast<float4*>(o) = make_float4(y[0], y[1], y[2], y[3]);
+      *reinterpret_cast<float4*>(o + 4) = make_float4(y[4], y[5], y[6], y[7]);
     } else {
-      for (int j = 0; j < 8; ++j) {
-        const int nn = n + j;
-        if (nn >= op.Cout) break;
-        float y = fmaf(v[j], op.scale[nn], op.bias[nn]);
-        if (op.has_skip)
-          y += __bfloat162float(static_cast<const __nv_bfloat16*>(op.skip)[static_cast<size_t>(m) * op.lds + nn]);
-        y = apply_act(y, op.act);
-        if (op.out_f32) static_cast<float*>(op.out)[static_cast<size_t>(m) * op.ldo + nn] = y;
-        else static_cast<__nv_bfloat16*>(op.out)[static_cast<size_t>(m) * op.ldo + nn] = __float2bfloat16_rn(y);
-      }
+      uint4 u;
+      u.x = pack_bf16x2(y[0], y[1]);
+      u.y = pack_bf16x2(y[2], y[3]);
+      u.z = pack_bf16x2(y[4], y[5]);
+      u.w = pack_bf16x2(y[6], y[7]);
+      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(op.out) + static_cast<size_t>(m) * op.ldo + n) = u;
     }
   } else {
-    // swap-AB: GEMM row m = output feature, GEMM column n = sample
-    if (m >= op.Cout) return;
-    const float sc = op.scale[m], bi = op.bias[m];
-    for (int j = 0; j < 8; ++j) {
-      const int nn = n + j;
-      if (nn >= op.B) break;
-      const float y = apply_act(fmaf(v[j], sc, bi), op.act);
-      if (op.out_f32) static_cast<float*>(op.out)[static_cast<size_t>(nn) * op.ldo + m] = y;
-      else static_cast<__nv_bfloat16*>(op.out)[static_cast<size_t>(nn) * op.ldo + m] = __float2bfloat16_rn(y);
+    for (int j = 0; j < 8 && n + j < op.Cout; ++j) {
+      if (op.out_f32) static_cast<float*>(op.out)[static_cast<size_t>(m) * op.ldo + n + j] = y[j];
+      else static_cast<__nv_bfloat16*>(op.out)[static_cast<size_t>(m) * op.ldo + n + j] = __float2bfloat16_rn(y[j]);
     }
   }
 }
 
+// swap-AB (linear): GEMM row m = output feature, GEMM column n = sample
+__device__ __forceinline__ void epilogue_store8_swap(const OpDev& op, int m, int n, const float* v, float sc,
+                                                     float bi) {
+  if (m >= op.Cout) return;
+  for (int j = 0; j < 8; ++j) {
+    const int nn = n + j;
+    if (nn >= op.B) break;
+    const float y = apply_act(fmaf(v[j], sc, bi), op.act);
+    if (op.out_f32) static_cast<float*>(op.out)[static_cast<size_t>(nn) * op.ldo + m] = y;
+    else static_cast<__nv_bfloat16*>(op.out)[static_cast<size_t>(nn) * op.ldo + m] = __float2bfloat16_rn(y);
+  }
+}
+
 // =====================================================================
-// producer side of a GEMM item: fill the smem ring for its K-blocks
+// worker side of a GEMM item: fill the smem ring for its K-blocks
 // =====================================================================
 __device__ __forceinline__ void kb_range(const OpDev& op, int ks, int& kb0, int& nk) {
   kb0 = (ks * op.nkb) / op.split_k;
   nk = ((ks + 1) * op.nkb) / op.split_k - kb0;
 }
 
-__device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t& g) {
-  const int ptid = threadIdx.x;  // 0..NPROD-1
+__device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t& g, int wtid,
+                             const ExecParams& p) {
   SmemCtl* ctl = cx.ctl;
   int kb0, nk;
   kb_range(op, it.ks, kb0, nk);
@@ -332,7 +329,8 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
   const uint32_t bbytes = static_cast<uint32_t>(op.bn) * 128u;
   const int m0 = it.mt * BM, n0 = it.nt * op.bn;
   if (op.a_mode != A_GATHER) {
-    if (ptid == 0) {
+    if (wtid == 0) {
+      fence_proxy_async_global();   // acquired producer data -> this thread's TMA reads
       int w0 = 0, h0 = 0, img0 = 0;
       if (op.a_mode == A_IM2COL) {
         const int HoWo = op.Ho * op.Wo;
@@ -360,22 +358,25 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
           tma_load_2d(a_dst, op.tmap_a, bar, k, m0);
         }
         tma_load_2d(b_dst, op.tmap_b, bar, k, n0);
+        if (i == 0) dbg_mark(p, 2);
       }
     }
   } else {
     // im2col gather with cp.async (C not a multiple of 64): 16-byte chunks of
-    // 8 channels of one tap; thread -> chunk j = ptid & 7, rows (ptid>>3)+16i
-    constexpr int ROWS = BM / (NPROD / 8);  // 8 rows per thread
-    constexpr int LAG = 3;                  // stages in flight per thread (< STAGES)
-    const int chunk = ptid & 7, rsub = ptid >> 3;
+    // 8 channels of one tap; thread -> chunk j = wtid & 7, rows (wtid>>3) + 12i
+    constexpr int RSTEP = NWORK / 8;                  // 12
+    constexpr int ROWS = (BM + RSTEP - 1) / RSTEP;    // 11
+    constexpr int LAG = 3;                            // stages in flight per thread (< STAGES)
+    const int chunk = wtid & 7, rsub = wtid >> 3;
     const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
     const __nv_bfloat16* img[ROWS];
     int hi0[ROWS], wi0[ROWS];
     const int HoWo = op.Ho * op.Wo;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
-      const int m = m0 + rsub + 16 * i;
-      const bool ok = m < op.M;
+      const int row = rsub + RSTEP * i;
+      const int m = m0 + row;
+      const bool ok = m < op.M && row < BM;
       const int mm = ok ? m : 0;
       const int b = mm / HoWo, rem = mm - b * HoWo, ho = rem / op.Wo, wo = rem - (rem / op.Wo) * op.Wo;
       img[i] = in + static_cast<size_t>(b) * op.H * op.W * op.ldi;
@@ -387,7 +388,7 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
       const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
       const int k0 = (kb0 + i) * BK;
-      if (ptid == 0) {
+      if (wtid == 0) {
         mbar_expect_tx(&ctl->full[stage], bbytes);
         tma_load_2d(ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES, op.tmap_b, &ctl->full[stage], k0,
                     n0);
@@ -399,24 +400,26 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       const int r = tap / op.kw, s = tap - (tap / op.kw) * op.kw;
 #pragma unroll
       for (int j = 0; j < ROWS; ++j) {
-        const int row = rsub + 16 * j;
-        const int hi = hi0[j] + r, wi = wi0[j] + s;
-        const bool ok = kok && hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
-        const __nv_bfloat16* src = ok ? img[j] + (static_cast<size_t>(hi) * op.W + wi) * op.ldi + c : in;
-        cp_async16(a_dst + row * 128 + ((chunk ^ (row & 7)) << 4), src, ok);
+        const int row = rsub + RSTEP * j;
+        if (row < BM) {
+          const int hi = hi0[j] + r, wi = wi0[j] + s;
+          const bool ok = kok && hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
+          const __nv_bfloat16* src = ok ? img[j] + (static_cast<size_t>(hi) * op.W + wi) * op.ldi + c : in;
+          cp_async16(a_dst + row * 128 + ((chunk ^ (row & 7)) << 4), src, ok);
+        }
       }
       cp_async_commit();
       if (i >= LAG) {
         cp_async_wait<LAG>();
         fence_proxy_async_smem();
-        named_bar_sync(1, NPROD);
-        if (ptid == 0) mbar_arrive(&ctl->full[(g + i - LAG) % STAGES]);
+        named_bar_sync(1, NWORK);
+        if (wtid == 0) mbar_arrive(&ctl->full[(g + i - LAG) % STAGES]);
       }
     }
     cp_async_wait<0>();
     fence_proxy_async_smem();
-    named_bar_sync(1, NPROD);
-    if (ptid == 0)
+    named_bar_sync(1, NWORK);
+    if (wtid == 0)
       for (int i = (nk > LAG ? nk - LAG : 0); i < nk; ++i) mbar_arrive(&ctl->full[(g + i) % STAGES]);
   }
   g += nk;
@@ -484,9 +487,183 @@ __device__ __forceinline__ void store8(void* base, size_t idx, const float* y, b
   }
 }
 
+// One output pixel x 8 channels of a pool / depthwise / eltwise op.
+template <bool F32>
+__device__ __forceinline__ void cc_pixel(const OpDev& op, int m, int c, int HoWo) {
+  const int b = m / HoWo, rem = m - b * HoWo, ho = rem / op.Wo, wo = rem - ho * op.Wo;
+  const size_t img = static_cast<size_t>(b) * op.H * op.W;
+  float y[8];
+  if (op.kind == DK_ELTWISE) {
+    load8<F32>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
+    if (op.has_skip) {
+      float s[8];
+      load8<F32>(op.skip, static_cast<size_t>(m) * op.lds + c, s);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] += s[q];
+    }
+  } else if (op.kind == DK_MAXPOOL) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = -INFINITY;
+    for (int r = 0; r < op.kh; ++r) {
+      const int hi = ho * op.stride - op.ph + r;
+      if (hi < 0 || hi >= op.H) continue;
+      for (int s = 0; s < op.kw; ++s) {
+        const int wi = wo * op.stride - op.pw + s;
+        if (wi < 0 || wi >= op.W) continue;
+        float f[8];
+        load8<F32>(op.in, (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c, f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
+      }
+    }
+  } else if (op.kind == DK_AVGPOOL) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = 0.0f;
+    int cnt = 0;
+    for (int r = 0; r < op.kh; ++r) {
+      const int hi = ho * op.stride - op.ph + r;
+      for (int s = 0; s < op.kw; ++s) {
+        const int wi = wo * op.stride - op.pw + s;
+        if (hi < -op.ph || hi >= op.H + op.ph || wi < -op.pw || wi >= op.W + op.pw) continue;
+        const bool in_b = hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
+        if (op.cip || in_b) ++cnt;
+        if (!in_b) continue;
+        float f[8];
+        load8<F32>(op.in, (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c, f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] += f[q];
+      }
+    }
+    const float inv = static_cast<float>(cnt);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = y[q] / inv;
+  } else {  // DK_DW: depthwise conv, weights [kh*kw][C] fp32, fused BN scale/bias + act
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = 0.0f;
+    const float* wt = static_cast<const float*>(op.wt);
+    for (int r = 0; r < op.kh; ++r) {
+      const int hi = ho * op.stride - op.ph + r;
+      if (hi < 0 || hi >= op.H) continue;
+      for (int s = 0; s < op.kw; ++s) {
+        const int wi = wo * op.stride - op.pw + s;
+        if (wi < 0 || wi >= op.W) continue;
+        float f[8];
+        load8<F32>(op.in, (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c, f);
+        const float4 w0 = *reinterpret_cast<const float4*>(wt + (r * op.kw + s) * op.C + c);
+        const float4 w1 = *reinterpret_cast<const float4*>(wt + (r * op.kw + s) * op.C + c + 4);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = fmaf(f[q], wv[q], y[q]);
+      }
+    }
+    const float4 s0 = *reinterpret_cast<const float4*>(op.scale + c);
+    const float4 s1 = *reinterpret_cast<const float4*>(op.scale + c + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(op.bias + c);
+    const float4 b1 = *reinterpret_cast<const float4*>(op.bias + c + 4);
+    const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
+    if (op.has_skip) {
+      float s[8];
+      load8<F32>(op.skip, static_cast<size_t>(m) * op.lds + c, s);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] += s[q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) y[q] = apply_act(y[q], op.act);
+  store8<F32>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+}
+
+// Two output pixels (m0, m1; m1 = -1: none) x 8 channels of a bf16
+// max-pool / avg-pool / depthwise op with kh*kw <= 9.  Taps are loaded
+// unconditionally from a clamped address and masked, so the 2*kh*kw loads
+// are independent and in flight together; the reduction order over taps is
+// the same fixed (r, s) order as cc_pixel.
+__device__ void window2_bf16(const OpDev& op, int m0, int m1, int c, int HoWo) {
+  const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
+  const int T = op.kh * op.kw;
+  uint4 raw[2][9];
+  uint32_t valid[2] = {0, 0};
+  int cnt[2] = {0, 0};
+#pragma unroll
+  for (int px = 0; px < 2; ++px) {
+    const int m = px == 0 ? m0 : (m1 >= 0 ? m1 : m0);
+    const int b = m / HoWo, rem = m - b * HoWo, ho = rem / op.Wo, wo = rem - ho * op.Wo;
+    const size_t img = static_cast<size_t>(b) * op.H * op.W;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      if (t < T) {
+        const int r = t / op.kw, s = t - (t / op.kw) * op.kw;
+        const int hi = ho * op.stride - op.ph + r, wi = wo * op.stride - op.pw + s;
+        const bool ok = hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
+        const bool in_frame = hi >= -op.ph && hi < op.H + op.ph && wi >= -op.pw && wi < op.W + op.pw;
+        valid[px] |= (ok ? 1u : 0u) << t;
+        cnt[px] += (op.cip ? in_frame : ok) ? 1 : 0;
+        const int hc = ok ? hi : 0, wc = ok ? wi : 0;
+        raw[px][t] = *reinterpret_cast<const uint4*>(in + (img + static_cast<size_t>(hc) * op.W + wc) * op.ldi + c);
+      }
+    }
+  }
+  const float* wt = static_cast<const float*>(op.wt);
+#pragma unroll
+  for (int px = 0; px < 2; ++px) {
+    const int m = px == 0 ? m0 : m1;
+    if (m < 0) break;
+    float y[8];
+    const float init = op.kind == DK_MAXPOOL ? -INFINITY : 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = init;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      if (t < T && ((valid[px] >> t) & 1u)) {
+        float f[8];
+        bf16x8_to_f32(raw[px][t], f);
+        if (op.kind == DK_MAXPOOL) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
+        } else if (op.kind == DK_AVGPOOL) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) y[q] += f[q];
+        } else {
+          const float4 w0 = *reinterpret_cast<const float4*>(wt + t * op.C + c);
+          const float4 w1 = *reinterpret_cast<const float4*>(wt + t * op.C + c + 4);
+          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int q = 0; q < 8; ++q) y[q] = fmaf(f[q], wv[q], y[q]);
+        }
+      }
+    }
+    if (op.kind == DK_AVGPOOL) {
+      const float inv = static_cast<float>(cnt[px]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = y[q] / inv;
+    } else if (op.kind == DK_DW) {
+      const float4 s0 = *reinterpret_cast<const float4*>(op.scale + c);
+      const float4 s1 = *reinterpret_cast<const float4*>(op.scale + c + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(op.bias + c);
+      const float4 b1 = *reinterpret_cast<const float4*>(op.bias + c + 4);
+      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
+      if (op.has_skip) {
+        float sk[8];
+        load8<false>(op.skip, static_cast<size_t>(m) * op.lds + c, sk);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] += sk[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = apply_act(y[q], op.act);
+    store8<false>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+  }
+}
+
 // tile: bm output pixels x bn channels; G = bn/8 channel groups; thread tid
-// (of CC_THREADS) handles pixel tid / G + j * (CC_THREADS / G), group tid % G.
-// Runs on the producer warps (named barrier 1) or a standalone CTA.
+// (of CC_THREADS) handles pixels tid / G + j * (CC_THREADS / G), group tid % G.
+// Runs on the worker warps (named barrier 1) or a standalone CTA.
 template <bool F32>
 __device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
   const int G = op.bn >> 3;
@@ -530,93 +707,21 @@ __device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
   }
   if (c >= op.Cout) return;
   const int HoWo = op.Ho * op.Wo;
-  for (int j = 0; j < CC_TASKS_PER_THREAD; ++j) {
-    const int m = it.mt * op.bm + tid / G + j * pstep;
-    if (m >= op.M) break;
-    const int b = m / HoWo, rem = m - b * HoWo, ho = rem / op.Wo, wo = rem - ho * op.Wo;
-    const size_t img = static_cast<size_t>(b) * op.H * op.W;
-    float y[8];
-    if (op.kind == DK_ELTWISE) {
-      load8<F32>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
-      if (op.has_skip) {
-        float s[8];
-        load8<F32>(op.skip, static_cast<size_t>(m) * op.lds + c, s);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) y[q] += s[q];
-      }
-    } else if (op.kind == DK_MAXPOOL) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = -INFINITY;
-      for (int r = 0; r < op.kh; ++r) {
-        const int hi = ho * op.stride - op.ph + r;
-        if (hi < 0 || hi >= op.H) continue;
-        for (int s = 0; s < op.kw; ++s) {
-          const int wi = wo * op.stride - op.pw + s;
-          if (wi < 0 || wi >= op.W) continue;
-          float f[8];
-          load8<F32>(op.in, (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c, f);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
-        }
-      }
-    } else if (op.kind == DK_AVGPOOL) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = 0.0f;
-      int cnt = 0;
-      for (int r = 0; r < op.kh; ++r) {
-        const int hi = ho * op.stride - op.ph + r;
-        for (int s = 0; s < op.kw; ++s) {
-          const int wi = wo * op.stride - op.pw + s;
-          if (hi < -op.ph || hi >= op.H + op.ph || wi < -op.pw || wi >= op.W + op.pw) continue;
-          const bool in_b = hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
-          if (op.cip || in_b) ++cnt;
-          if (!in_b) continue;
-          float f[8];
-          load8<F32>(op.in, (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c, f);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] += f[q];
-        }
-      }
-      const float inv = static_cast<float>(cnt);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = y[q] / inv;
-    } else {  // DK_DW: depthwise conv, weights [kh*kw][C] fp32, fused BN scale/bias + act
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = 0.0f;
-      const float* wt = static_cast<const float*>(op.wt);
-      for (int r = 0; r < op.kh; ++r) {
-        const int hi = ho * op.stride - op.ph + r;
-        if (hi < 0 || hi >= op.H) continue;
-        for (int s = 0; s < op.kw; ++s) {
-          const int wi = wo * op.stride - op.pw + s;
-          if (wi < 0 || wi >= op.W) continue;
-          float f[8];
-          load8<F32>(op.in, (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c, f);
-          const float4 w0 = *reinterpret_cast<const float4*>(wt + (r * op.kw + s) * op.C + c);
-          const float4 w1 = *reinterpret_cast<const float4*>(wt + (r * op.kw + s) * op.C + c + 4);
-          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] = fmaf(f[q], wv[q], y[q]);
-        }
-      }
-      const float4 s0 = *reinterpret_cast<const float4*>(op.scale + c);
-      const float4 s1 = *reinterpret_cast<const float4*>(op.scale + c + 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(op.bias + c);
-      const float4 b1 = *reinterpret_cast<const float4*>(op.bias + c + 4);
-      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
-      if (op.has_skip) {
-        float s[8];
-        load8<F32>(op.skip, static_cast<size_t>(m) * op.lds + c, s);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) y[q] += s[q];
-      }
+  const int mb = it.mt * op.bm + tid / G;
+  if (!F32 && op.kind != DK_ELTWISE && op.kh * op.kw <= 9) {
+    // latency-bound window ops: two output pixels per step, all their tap
+    // loads issued back to back (branch-free, predicated), then reduced
+    for (int j = 0; j < CC_TASKS_PER_THREAD; j += 2) {
+      const int m0 = mb + j * pstep, m1 = m0 + pstep;
+      if (m0 >= op.M) break;
+      window2_bf16(op, m0, m1 < op.M ? m1 : -1, c, HoWo);
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) y[q] = apply_act(y[q], op.act);
-    store8<F32>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+    return;
+  }
+  for (int j = 0; j < CC_TASKS_PER_THREAD; ++j) {
+    const int m = mb + j * pstep;
+    if (m >= op.M) break;
+    cc_pixel<F32>(op, m, c, HoWo);
   }
 }
 
@@ -637,20 +742,25 @@ __device__ __forceinline__ Item decode_single(const OpDev& op, int op_idx, int b
   it.dep_begin = it.dep_count = 0;
   it.chunk = -1;
   it.cluster = 0;
+  it.prio = 0;
+  it.idx = -1;
   return it;
 }
 
 // =====================================================================
-// the persistent multi-tenant executor
+// scheduler: dependency-aware, rank-ordered claiming
 // =====================================================================
 // Spin until *ctr >= target, with watchdog; returns false on abort.
 __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& p) {
-  if (ld_acquire(ctr) >= target) return true;
+  // relaxed polling (an acquire load invalidates the SM's L1 on every poll,
+  // evicting the co-resident warps' working set); one fence on success
+  if (ld_relaxed(ctr) >= target) { __threadfence(); return true; }
   const uint64_t t0 = globaltimer();
-  uint32_t it = 0;
-  while (ld_acquire(ctr) < target) {
-    __nanosleep(32);
-    if ((++it & 255) == 0) {
+  uint32_t it = 0, ns = 32;
+  while (ld_relaxed(ctr) < target) {
+    __nanosleep(ns);              // exponential backoff: 148 CTAs poll a few hot lines
+    ns = ns < 512 ? ns * 2 : 512;
+    if ((++it & 63) == 0) {
       if (*reinterpret_cast<volatile int32_t*>(p.error)) return false;
       if (static_cast<int64_t>(globaltimer() - t0) > p.watchdog_ns) {
         atomicExch(p.error, 1);
@@ -658,102 +768,182 @@ __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& 
       }
     }
   }
+  __threadfence();
   return true;
 }
 
-// Scheduler (producer thread 0): claim the next item of the open cluster k.
-// Returns the item index, -2 when the round is done, -3 on abort.
-__device__ int claim_item(const ExecParams& p, int& k) {
+// Non-blocking readiness test of an item's producer-chunk dependencies
+// (relaxed loads; the caller fences once after claiming).
+__device__ __forceinline__ bool deps_ready(const ExecParams& p, const Item& it) {
+  if (it.dep_count <= INLINE_DEPS) {
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < INLINE_DEPS; ++d)
+      if (d < it.dep_count) ok &= ld_relaxed(p.chunk_done + it.dc[d]) >= p.epoch * it.dt[d];
+    return ok;
+  }
+  for (int d = 0; d < it.dep_count; ++d) {
+    const Dep dp = p.deps[it.dep_begin + d];
+    if (ld_relaxed(p.chunk_done + dp.counter) < p.epoch * dp.target) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ Seg get_seg(const ExecParams& p, const SmemCtl* ctl, int si) {
+  return si < ctl->n_segs_smem ? ctl->segs[si] : p.segs[si];
+}
+
+// Claim the next item of the open cluster k.  Greedy, dependency-aware issue
+// (§3, l.438-444: an operator that cannot be deployed now "is moved
+// to the next cycle"): among the head items of the tenant queues this CTA may
+// serve, claim the READY one (producers complete) with the highest upward
+// rank (longest estimated remaining chain, computed by the plan compiler).
+// The critical tenant's chain advances at full width while the others fill
+// its residue (l.447-453).  Unready heads are never claimed, which keeps the
+// wait-for graph acyclic.  Returns the item position, -2 when the round is
+// done, -3 on abort.
+__device__ int claim_item(const ExecParams& p, const SmemCtl* ctl, int& k, Item& out) {
   const int32_t* pref = p.cta_pref + static_cast<size_t>(blockIdx.x) * p.n_tenants;
+  uint64_t t0 = 0;
+  uint32_t spins = 0;
   while (k < p.n_clusters) {
+    bool unclaimed = false;
+    int best_si = -1;
+    uint32_t best_prio = 0;
     for (int j = 0; j < p.n_tenants; ++j) {
       const int t = pref[j];
       if (t < 0) break;
       const int si = t * p.n_clusters + k;
-      const Seg sg = p.segs[si];
+      const Seg sg = get_seg(p, ctl, si);
       if (sg.size == 0) continue;
-      if (ld_relaxed(p.heads + si) >= static_cast<uint32_t>(sg.size)) continue;
-      const uint32_t idx = atomicAdd(p.heads + si, 1u);
-      if (idx < static_cast<uint32_t>(sg.size)) return p.queue[sg.begin + idx];
+      const uint32_t h = ld_relaxed(p.heads + si);
+      if (h >= static_cast<uint32_t>(sg.size)) continue;
+      unclaimed = true;
+      const uint32_t prio = p.items[sg.begin + h].prio;
+      if (best_si >= 0 && prio <= best_prio) continue;
+      if (!deps_ready(p, p.items[sg.begin + h])) continue;
+      best_si = si;
+      best_prio = prio;
     }
-    // nothing left to claim in cluster k: the synchronisation pointer --
-    // wait until every item of cluster k (all tenants) is done.
-    if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) return -3;
-    ++k;
+    if (best_si >= 0) {
+      const Seg sg = get_seg(p, ctl, best_si);
+      const uint32_t idx = atomicAdd(p.heads + best_si, 1u);
+      if (idx < static_cast<uint32_t>(sg.size)) {
+        out = p.items[sg.begin + idx];
+        // the claimed item may be a later one than the one checked (race):
+        // its dependencies were claimed earlier, so this wait terminates
+        if (!deps_ready(p, out)) {
+          if (out.dep_count <= INLINE_DEPS) {
+            for (int d = 0; d < out.dep_count; ++d)
+              if (!spin_ge(p.chunk_done + out.dc[d], p.epoch * out.dt[d], p)) return -3;
+          } else {
+            for (int d = 0; d < out.dep_count; ++d) {
+              const Dep dp = p.deps[out.dep_begin + d];
+              if (!spin_ge(p.chunk_done + dp.counter, p.epoch * dp.target, p)) return -3;
+            }
+          }
+        }
+        return sg.begin + static_cast<int>(idx);
+      }
+      continue;  // lost the race for the last item of that queue: rescan
+    }
+    if (!unclaimed) {
+      // every item of cluster k is claimed: the synchronisation pointer --
+      // wait until every item of cluster k (all tenants) is done.
+      if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) return -3;
+      ++k;
+      spins = 0;
+      continue;
+    }
+    // unclaimed work exists but none of it is ready yet: back off, rescan
+    __nanosleep(spins < 4 ? 64u : (spins < 8 ? 256u : 512u));
+    if (spins++ == 0) t0 = globaltimer();
+    if ((spins & 31) == 0) {
+      if (*reinterpret_cast<volatile int32_t*>(p.error)) return -3;
+      if (static_cast<int64_t>(globaltimer() - t0) > p.watchdog_ns) {
+        atomicExch(p.error, 1);
+        return -3;
+      }
+    }
   }
   return -2;
 }
 
-__device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, int idx, uint64_t t0,
-                                             const OpDev& op) {
+__device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, uint64_t t0, const OpDev& op) {
   // caller: all writes of the item are ordered before this thread (barrier)
   __threadfence();
   atomicAdd(p.chunk_done + it.chunk, 1u);
   atomicAdd(p.cluster_done + it.cluster, 1u);
   if (p.trace) {
-    int64_t* rec = p.trace + static_cast<size_t>(idx) * 8;
-    rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = idx;
+    int64_t* rec = p.trace + static_cast<size_t>(it.idx) * 8;
+    rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = it.idx;
     rec[4] = it.cluster; rec[5] = it.chunk;
     rec[6] = static_cast<int64_t>(t0); rec[7] = static_cast<int64_t>(globaltimer());
   }
 }
 
-__device__ void producer_role(const ExecParams& p, Ctx& cx) {
-  const int ptid = threadIdx.x;
+__device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = cx.ctl;
-  uint32_t g = 0, islot = 0;
+  uint32_t islot = 0;
   int k = 0;
   int sidx = blockIdx.x;
   for (;;) {
-    if (ptid == 0) {
-      int claimed;
-      if (p.single_op >= 0) {
-        const OpDev& op = p.ops[p.single_op];
-        const int n = op.tiles_m * op.tiles_n * (op.kind == DK_GEMM ? op.split_k : 1);
-        claimed = sidx < n ? sidx : -2;
-        if (claimed >= 0) ctl->cur = decode_single(op, p.single_op, sidx);
-        sidx += gridDim.x;
-      } else {
-        claimed = claim_item(p, k);
-        if (claimed >= 0) {
-          const Item it = p.items[claimed];
-          ctl->cur = it;
-          for (int d = 0; d < it.dep_count; ++d) {
-            const Dep dp = p.deps[it.dep_begin + d];
-            if (!spin_ge(p.chunk_done + dp.counter, p.epoch * dp.target, p)) { claimed = -3; break; }
-          }
-          // acquire: producers' generic writes -> this CTA's generic and TMA reads
-          __threadfence();
-          fence_proxy_async_global();
-        }
-      }
-      ctl->cur_t0 = p.trace ? globaltimer() : 0;
-      const bool gemm = claimed >= 0 && p.ops[ctl->cur.op].kind == DK_GEMM;
-      if (claimed < 0 || gemm) {  // GEMM items and the STOP marker go to the MMA/epilogue ring
-        const uint32_t slot = islot % ITEM_RING;
-        if (islot >= ITEM_RING) mbar_wait(&ctl->rempty[slot], ((islot / ITEM_RING) + 1) & 1);
-        ctl->ring[slot].it = ctl->cur;
-        ctl->ring[slot].idx = claimed >= 0 ? claimed : -1;
-        ctl->ring[slot].t0 = ctl->cur_t0;
-        mbar_arrive(&ctl->rfull[slot]);
-        ++islot;
-      }
-      ctl->claimed = claimed;
+    // at most LOOKAHEAD claimed-but-unconsumed items per CTA
+    if (islot >= LOOKAHEAD) {
+      const uint32_t old = islot - LOOKAHEAD;
+      mbar_wait(&ctl->rempty[old % ITEM_RING], (old / ITEM_RING) & 1);
     }
-    named_bar_sync(1, NPROD);
-    const int claimed = ctl->claimed;
-    if (claimed < 0) break;
-    const Item it = ctl->cur;
-    const uint64_t t0 = ctl->cur_t0;
-    const OpDev& op = p.ops[it.op];
-    if (op.kind == DK_GEMM) {
-      produce_gemm(op, it, cx, g);
+    Item it;
+    int claimed;
+    if (p.single_op >= 0) {
+      const OpDev& op = p.ops[p.single_op];
+      const int n = op.tiles_m * op.tiles_n * (op.kind == DK_GEMM ? op.split_k : 1);
+      claimed = sidx < n ? sidx : -2;
+      if (claimed >= 0) it = decode_single(op, p.single_op, sidx);
+      sidx += gridDim.x;
     } else {
-      run_cc(op, it, ptid, ctl->red);
-      named_bar_sync(1, NPROD);
-      if (ptid == 0 && p.single_op < 0) release_item(p, it, claimed, t0, op);
+      claimed = claim_item(p, ctl, k, it);
+      if (claimed >= 0) __threadfence();  // acquire side: drop stale L1 lines before the CTA reads inputs
     }
-    named_bar_sync(1, NPROD);  // ctl->cur may be overwritten after this
+    dbg_mark(p, 1);
+    const uint32_t slot = islot % ITEM_RING;
+    // (slot reuse is implied by the LOOKAHEAD wait since LOOKAHEAD <= ITEM_RING)
+    RingSlot& rs = ctl->ring[slot];
+    rs.it = it;
+    rs.idx = claimed >= 0 ? claimed : -1;
+    rs.kind = claimed >= 0 ? p.ops[it.op].kind : 0;
+    rs.t0 = p.trace ? globaltimer() : 0;
+    mbar_arrive(&ctl->rfull[slot]);
+    ++islot;
+    if (claimed < 0) break;
+  }
+}
+
+__device__ void worker_role(const ExecParams& p, Ctx& cx) {
+  SmemCtl* ctl = cx.ctl;
+  const int wtid = threadIdx.x - WORK_WARP0 * 32;  // 0..NWORK-1
+  uint32_t g = 0, islot = 0;
+  for (;;) {
+    const uint32_t slot = islot % ITEM_RING;
+    mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
+    const RingSlot rs = ctl->ring[slot];
+    ++islot;
+    if (rs.idx < 0) {
+      named_bar_sync(1, NWORK);
+      if (wtid == 0) mbar_arrive(&ctl->rempty[slot]);
+      break;
+    }
+    const OpDev& op = p.ops[rs.it.op];
+    if (rs.kind == DK_GEMM) {
+      produce_gemm(op, rs.it, cx, g, wtid, p);
+      if (wtid == 0) dbg_mark(p, 3);
+      named_bar_sync(1, NWORK);
+    } else {
+      run_cc(op, rs.it, wtid, ctl->red);
+      named_bar_sync(1, NWORK);
+      if (wtid == 0 && p.single_op < 0) release_item(p, rs.it, rs.t0, op);
+    }
+    if (wtid == 0) mbar_arrive(&ctl->rempty[slot]);
   }
 }
 
@@ -765,10 +955,12 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     const uint32_t slot = islot % ITEM_RING;
     mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
     const int idx = ctl->ring[slot].idx;
+    const int kind = ctl->ring[slot].kind;
     const Item it = ctl->ring[slot].it;
     mbar_arrive(&ctl->rempty[slot]);
     ++islot;
     if (idx < 0) break;
+    if (kind != DK_GEMM) continue;
     const OpDev& op = p.ops[it.op];
     int kb0, nk;
     kb_range(op, it.ks, kb0, nk);
@@ -780,6 +972,7 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     for (int i = 0; i < nk; ++i) {
       const uint32_t stage = g % STAGES;
       mbar_wait(&ctl->full[stage], (g / STAGES) & 1);
+      if (i == 0) dbg_mark(p, 4);
       tc_fence_after();
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
@@ -791,58 +984,105 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
       ++g;
     }
     umma_commit(&ctl->tfull[abuf]);
+    dbg_mark(p, 5);
     ++acc;
   }
 }
 
 __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = cx.ctl;
-  const int etid = threadIdx.x - NPROD;  // 0..127
-  const int ew = etid >> 5, lane = etid & 31;  // warp 4+ew accesses TMEM lanes 32*ew..
+  const int etid = threadIdx.x - EPI_WARP0 * 32;  // 0..127
+  const int ew = etid >> 5, lane = etid & 31;     // warp 4+ew accesses TMEM lanes 32*ew..
   uint32_t islot = 0, acc = 0;
   for (;;) {
     const uint32_t slot = islot % ITEM_RING;
     mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
     const int idx = ctl->ring[slot].idx;
+    const int kind = ctl->ring[slot].kind;
     const Item it = ctl->ring[slot].it;
     const uint64_t t0 = ctl->ring[slot].t0;
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->rempty[slot]);
     ++islot;
     if (idx < 0) break;
+    if (kind != DK_GEMM) continue;
     const OpDev& op = p.ops[it.op];
     const int bn = op.bn;
-    const uint32_t abuf = acc & 1;
-    mbar_wait(&ctl->tfull[abuf], (acc / 2) & 1);
-    tc_fence_after();
     const int row = ew * 32 + lane;
     const int m0 = it.mt * BM, n0 = it.nt * bn;
+    const int m = m0 + row;
+    const int split = op.split_k;
+    const bool swap = op.swap;
+    // ---- global reads the epilogue needs are issued before the accumulator
+    //      is waited on (hides their latency behind the MMA)
+    float sc_row = 1.0f, bi_row = 0.0f;
+    if (swap) {
+      if (m < op.Cout) { sc_row = op.scale[m]; bi_row = op.bias[m]; }
+    } else if (etid < bn) {
+      ctl->epi_scale[etid] = op.scale[n0 + etid];
+      ctl->epi_bias[etid] = op.bias[n0 + etid];
+    }
+    const bool do_skip = op.has_skip && split == 1 && m < op.M;
+    const __nv_bfloat16* skrow =
+        do_skip ? static_cast<const __nv_bfloat16*>(op.skip) + static_cast<size_t>(m) * op.lds + n0 : nullptr;
+    const int cout_left = op.Cout - n0;
+    uint4 skA[4], skB[4];  // residual values of the current / next 32 columns
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      skA[q] = (do_skip && q * 8 < bn && q * 8 < cout_left) ? *reinterpret_cast<const uint4*>(skrow + q * 8)
+                                                             : make_uint4(0, 0, 0, 0);
+    named_bar_sync(2, NEPI);  // epi_scale / epi_bias visible
+    const uint32_t abuf = acc & 1;
+    mbar_wait(&ctl->tfull[abuf], (acc / 2) & 1);
+    if (etid == 0) dbg_mark(p, 6);
+    tc_fence_after();
     const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(ew * 32) << 16);
     float* part = nullptr;
     const int tile = it.mt * op.tiles_n + it.nt;
-    if (op.split_k == 1) {
-      for (int c = 0; c < bn; c += 16) {
-        float v[16];
-        tmem_ld16(taddr + c, v);
-        epilogue_store8(op, m0 + row, n0 + c, v);
-        epilogue_store8(op, m0 + row, n0 + c + 8, v + 8);
+    if (split == 1) {
+      for (int c = 0; c < bn; c += 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int cc = c + 32 + q * 8;
+          skB[q] = (do_skip && cc < bn && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc)
+                                                         : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int h = 0; h < 32; h += 16) {
+          if (c + h < bn) {
+            float v[16];
+            tmem_ld16(taddr + c + h, v);
+            if (swap) {
+              epilogue_store8_swap(op, m, n0 + c + h, v, sc_row, bi_row);
+              epilogue_store8_swap(op, m, n0 + c + h + 8, v + 8, sc_row, bi_row);
+            } else {
+              epilogue_store8(op, m, n0 + c + h, v, ctl->epi_scale + c + h, ctl->epi_bias + c + h, skA[h / 8]);
+              epilogue_store8(op, m, n0 + c + h + 8, v + 8, ctl->epi_scale + c + h + 8, ctl->epi_bias + c + h + 8,
+                              skA[h / 8 + 1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) skA[q] = skB[q];
       }
     } else {
-      part = op.partial + static_cast<size_t>(tile) * op.split_k * (BM * bn);
-      float* mine = part + static_cast<size_t>(it.ks) * (BM * bn) + row * bn;
+      // partial layout [tile][ks][bn/4][BM] float4: a warp's 32 rows of one
+      // float4 column are 512 contiguous bytes (coalesced write and read)
+      part = op.partial + static_cast<size_t>(tile) * split * (BM * bn);
+      float4* mine = reinterpret_cast<float4*>(part + static_cast<size_t>(it.ks) * (BM * bn)) + row;
       for (int c = 0; c < bn; c += 16) {
         float v[16];
         tmem_ld16(taddr + c, v);
 #pragma unroll
         for (int q = 0; q < 16; q += 4)
-          __stcg(reinterpret_cast<float4*>(mine + c + q), make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+          __stcg(mine + ((c + q) >> 2) * BM, make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
       }
     }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->tempty[abuf]);
     ++acc;
-    if (op.split_k > 1) {
+    if (split > 1) {
       named_bar_sync(2, NEPI);
       if (etid == 0) {
         __threadfence();
@@ -854,22 +1094,40 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       }
       named_bar_sync(2, NEPI);
       if (ctl->epi_flag) {
+        // fixed ks order (bit-identical in every mode); all partial loads of an
+        // 8-column chunk are in flight together
         for (int c = 0; c < bn; c += 8) {
-          float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int ks = 0; ks < op.split_k; ++ks) {  // fixed order: bit-identical in every mode
-            const float* q = part + static_cast<size_t>(ks) * (BM * bn) + row * bn + c;
-            const float4 a = __ldcg(reinterpret_cast<const float4*>(q));
-            const float4 b = __ldcg(reinterpret_cast<const float4*>(q + 4));
-            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
-            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+          float4 ld[MAX_SPLIT][2];
+#pragma unroll
+          for (int ks = 0; ks < MAX_SPLIT; ++ks)
+            if (ks < split) {
+              const float4* q = reinterpret_cast<const float4*>(part + static_cast<size_t>(ks) * (BM * bn)) + row;
+              ld[ks][0] = __ldcg(q + (c >> 2) * BM);
+              ld[ks][1] = __ldcg(q + ((c >> 2) + 1) * BM);
+            }
+          float s8[8] = {ld[0][0].x, ld[0][0].y, ld[0][0].z, ld[0][0].w, ld[0][1].x, ld[0][1].y, ld[0][1].z, ld[0][1].w};
+#pragma unroll
+          for (int ks = 1; ks < MAX_SPLIT; ++ks)
+            if (ks < split) {
+              s8[0] += ld[ks][0].x; s8[1] += ld[ks][0].y; s8[2] += ld[ks][0].z; s8[3] += ld[ks][0].w;
+              s8[4] += ld[ks][1].x; s8[5] += ld[ks][1].y; s8[6] += ld[ks][1].z; s8[7] += ld[ks][1].w;
+            }
+          if (swap) {
+            epilogue_store8_swap(op, m, n0 + c, s8, sc_row, bi_row);
+          } else {
+            uint4 k8 = make_uint4(0, 0, 0, 0);
+            if (op.has_skip && m < op.M && c < cout_left)
+              k8 = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(op.skip) +
+                                                   static_cast<size_t>(m) * op.lds + n0 + c);
+            epilogue_store8(op, m, n0 + c, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8);
           }
-          epilogue_store8(op, m0 + row, n0 + c, s);
         }
       }
     }
     fence_proxy_async_global();  // generic stores -> later TMA reads by consumers
-    named_bar_sync(2, NEPI);
-    if (etid == 0 && p.single_op < 0) release_item(p, it, idx, t0, op);
+    named_bar_sync(2, NEPI);     // also: epi_scale/bias free for the next item
+    if (etid == 0) dbg_mark(p, 7);
+    if (etid == 0 && p.single_op < 0) release_item(p, it, t0, op);
   }
 }
 
@@ -883,21 +1141,37 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&ctl->full[s], 1); mbar_init(&ctl->empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&ctl->tfull[a], 1); mbar_init(&ctl->tempty[a], NEPI / 32); }
-    for (int r = 0; r < ITEM_RING; ++r) { mbar_init(&ctl->rfull[r], 1); mbar_init(&ctl->rempty[r], 1 + NEPI / 32); }
+    for (int r = 0; r < ITEM_RING; ++r) { mbar_init(&ctl->rfull[r], 1); mbar_init(&ctl->rempty[r], RING_CONSUMERS); }
     fence_mbar_init();
+  }
+  if (p.single_op < 0) {  // cache the queue segments
+    const int ns = p.n_tenants * p.n_clusters;
+    const int nc = ns < MAX_SMEM_SEGS ? ns : MAX_SMEM_SEGS;
+    for (int i = tid; i < nc; i += NTHREADS) ctl->segs[i] = p.segs[i];
+    if (tid == 0) ctl->n_segs_smem = nc;
+  } else if (tid == 0) {
+    ctl->n_segs_smem = 0;
   }
   if (warp == MMA_WARP) tmem_alloc(&ctl->tmem_base, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   cx.tmem = ctl->tmem_base;
+  if (tid == 0) dbg_mark(p, 0);
 
-  if (warp < NPROD / 32) producer_role(p, cx);
-  else if (warp < (NPROD + NEPI) / 32) epilogue_role(p, cx);
-  else if ((tid & 31) == 0) mma_role(p, cx);
+  if (warp == SCHED_WARP) {
+    if (tid == 0) scheduler_role(p, cx);
+  } else if (warp == MMA_WARP) {
+    if ((tid & 31) == 0) mma_role(p, cx);
+  } else if (warp < EPI_WARP0) {
+    worker_role(p, cx);
+  } else {
+    epilogue_role(p, cx);
+  }
 
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) dbg_mark(p, 11);
   if (warp == MMA_WARP) tmem_dealloc(cx.tmem, TMEM_COLS);
   if (tid == 0 && p.single_op < 0) {
     __threadfence();
@@ -945,6 +1219,7 @@ cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, 
   if (kind == DK_GEMM) {
     ExecParams p = base;
     p.ops = ops_dev;
+    if (p.dbg) p.dbg += static_cast<size_t>(op_idx) * 148 * DBG_EVENTS;
     p.single_op = op_idx;
     p.trace = nullptr;
     const int grid = n_items < num_sms ? n_items : num_sms;

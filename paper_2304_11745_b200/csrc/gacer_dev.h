@@ -26,13 +26,20 @@ constexpr int BK = 64;            // bf16 elements per K-block = one 128-byte sw
 constexpr int BN_MAX = 128;       // max UMMA N per tile
 constexpr int STAGES = 6;         // smem ring depth (A 16 KB + B 16 KB per stage)
 constexpr int ITEM_RING = 4;      // scheduler -> MMA/epilogue item queue depth
-// warp roles of the executor CTA
-constexpr int NPROD = 128;        // warps 0-3: scheduler (thread 0) + loads + CUDA-core items
-constexpr int NEPI = 128;         // warps 4-7: TMEM -> register epilogue (lane quarter = warp % 4)
-constexpr int MMA_WARP = 8;       // warp 8: single-thread tcgen05.mma issue
-constexpr int NTHREADS = NPROD + NEPI + 32;
-constexpr int CC_THREADS = NPROD; // threads that execute a CUDA-core item
+// warp roles of the executor CTA (16 warps; 4 per SM sub-partition, <= 128 registers)
+constexpr int SCHED_WARP = 0;     // warp 0: scheduler (lane 0) -- claims ready items into the item ring
+constexpr int MMA_WARP = 1;       // warp 1: single-thread tcgen05.mma issue
+constexpr int WORK_WARP0 = 2;     // warps 2-11: TMA / gather loads of GEMM items, CUDA-core items
+constexpr int NWORK = 320;
+constexpr int EPI_WARP0 = 12;     // warps 12-15: TMEM -> register epilogue (lane quarter = warp % 4)
+constexpr int NEPI = 128;
+constexpr int NTHREADS = 512;
+constexpr int CC_THREADS = NWORK; // threads that execute a CUDA-core item
 constexpr int CC_TASKS_PER_THREAD = 4;
+constexpr int MAX_SPLIT = 4;      // split-K factor cap (fixed per layer shape)
+constexpr int LOOKAHEAD = 1;      // claimed items not yet picked up by every role (per CTA)
+constexpr int INLINE_DEPS = 4;    // dependencies stored inside the Item
+constexpr int MAX_SMEM_SEGS = 256;
 
 // operand A load mode of a GEMM op
 enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2 };
@@ -80,13 +87,19 @@ struct OpDev {
   int32_t pad4;
 };
 
-// One work item: one output tile (mt, nt) of one op, K-slice ks.
+// One work item: one output tile (mt, nt) of one op, K-slice ks.  Items are
+// stored in queue order (grouped by (tenant, cluster) segment).
 struct Item {
   int32_t op;
   int32_t mt, nt, ks;
-  int32_t dep_begin, dep_count;
   int32_t chunk;           // global chunk counter id (released on completion)
   int32_t cluster;
+  uint32_t prio;           // upward rank: estimated remaining critical path (ns) of its tenant
+  int32_t idx;             // position in the item array (trace / diagnostics)
+  int32_t dep_count;       // <= INLINE_DEPS: dc/dt hold them, else dep list at dep_begin
+  int32_t dep_begin;
+  int32_t dc[INLINE_DEPS]; // producer chunk counters
+  uint32_t dt[INLINE_DEPS];// their per-round targets
 };
 
 struct Dep {
@@ -100,9 +113,8 @@ struct Seg {                // queue segment for (tenant, cluster)
 
 struct ExecParams {
   const OpDev* ops;
-  const Item* items;
-  const Dep* deps;
-  const int32_t* queue;     // item ids, grouped by segment
+  const Item* items;        // queue order, grouped by segment
+  const Dep* deps;          // overflow dependency lists (dep_count > INLINE_DEPS)
   const Seg* segs;          // [n_tenants * n_clusters]
   const int32_t* cta_pref;  // [num_ctas * n_tenants] tenant preference (-1 = none)
   uint32_t* heads;          // [n_tenants * n_clusters] claim counters (reset by last CTA)
@@ -111,13 +123,15 @@ struct ExecParams {
   const uint32_t* cluster_total; // [n_clusters] items per round
   uint32_t* exit_count;
   int32_t* error;           // device error flag (deadlock watchdog)
-  int64_t* trace;           // optional [n_items * 6]
+  int64_t* trace;           // optional [n_items * 8]
   int32_t n_tenants, n_clusters;
   uint32_t epoch;           // round number since plan install, >= 1
   int32_t n_heads;
   int64_t watchdog_ns;
   int32_t single_op;        // >= 0: standalone mode, run every tile of this op (strided over CTAs)
   int32_t pad;
+  int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
 };
+constexpr int DBG_EVENTS = 16;
 
 }  // namespace gacer

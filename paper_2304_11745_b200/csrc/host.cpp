@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -175,6 +176,8 @@ struct State {
   uint32_t* d_exit = nullptr;
   int32_t* d_error = nullptr;
   int64_t* d_trace = nullptr;
+  int64_t* d_dbg = nullptr;     // GACER_DEBUG_TIMING=1: per-CTA milestones
+  size_t n_dbg = 0;
   uint32_t epoch = 0;
   int grid = 0;
   double last_ms = 0;
@@ -629,7 +632,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         // split-K: a function of the layer shape only (same in every mode/plan)
         const int tiles = F.tiles_m * F.tiles_n;
         int sk = 1;
-        while (sk < 16 && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 4) sk *= 2;
+        while (sk < MAX_SPLIT && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 4) sk *= 2;
         F.split_k = sk;
         F.w_bf16.assign(rows * F.Kpad, 0);
         for (int co = 0; co < F.Cout; ++co)
@@ -933,6 +936,44 @@ int compile_plan(Plan& P) {
   }
   P.n_chunk_counters = counter;
 
+  // upward rank of every fused op (HEFT-style): estimated time of the op on
+  // the whole GPU + the longest rank among its consumers.  The device
+  // scheduler claims the ready head item with the highest rank first.
+  std::vector<std::vector<uint32_t>> rank(nt);
+  for (int t = 0; t < nt; ++t) {
+    const Tenant& T = S.tenants[t];
+    const size_t nf = T.fops.size();
+    std::vector<double> est(nf), rk(nf, 0.0);
+    for (size_t f = 0; f < nf; ++f) {
+      const FusedOp& F = T.fops[f];
+      const int split = (F.kind == DK_GEMM) ? F.split_k : 1;
+      const double items = static_cast<double>(F.tiles_m) * F.tiles_n * split;
+      const double waves = std::ceil(items / kSplitSms);
+      double item_ns;
+      if (F.kind == DK_GEMM) {
+        const double kblocks = static_cast<double>(F.nkb) / split;
+        item_ns = kblocks * BK * BM * F.bn * 2.0 / 8192.0 / 1.9 + 1000.0;  // ~8192 FLOP/cycle/SM at 1.9 GHz
+      } else {
+        item_ns = F.bytes / std::max(1.0, items) / 40.0 + 1000.0;          // ~40 B/ns per SM
+      }
+      est[f] = waves * item_ns;
+    }
+    for (size_t f = nf; f-- > 0;) {
+      double best = 0.0;
+      for (size_t g2 = f + 1; g2 < nf; ++g2) {
+        const FusedOp& G2 = T.fops[g2];
+        bool consumes = false;
+        for (int tin : {G2.in_t, G2.skip_t})
+          if (tin >= 0)
+            for (int w : T.tensors[tin].writers) consumes |= (w == static_cast<int>(f));
+        if (consumes) best = std::max(best, rk[g2]);
+      }
+      rk[f] = est[f] + best;
+    }
+    rank[t].resize(nf);
+    for (size_t f = 0; f < nf; ++f) rank[t][f] = static_cast<uint32_t>(std::min(rk[f], 4.0e9));
+  }
+
   // items, grouped by (tenant, cluster) segment, in issue order
   std::vector<std::vector<std::vector<int32_t>>> seg_items(nt, std::vector<std::vector<int32_t>>(P.n_clusters));
   for (int t = 0; t < nt; ++t) {
@@ -979,16 +1020,23 @@ int compile_plan(Plan& P) {
                 }
               }
             }
-            const int dep_begin = static_cast<int>(P.deps.size());
-            P.deps.insert(P.deps.end(), dl.begin(), dl.end());
+            int dep_begin = 0;
+            if (dl.size() > static_cast<size_t>(INLINE_DEPS)) {
+              dep_begin = static_cast<int>(P.deps.size());
+              P.deps.insert(P.deps.end(), dl.begin(), dl.end());
+            }
             for (int ks = 0; ks < split; ++ks) {
               Item it;
+              std::memset(&it, 0, sizeof it);
               it.op = T.op_base + static_cast<int>(f);
               it.mt = mt; it.nt = ntile; it.ks = ks;
               it.dep_begin = dep_begin;
               it.dep_count = static_cast<int>(dl.size());
+              if (dl.size() <= static_cast<size_t>(INLINE_DEPS))
+                for (size_t d = 0; d < dl.size(); ++d) { it.dc[d] = dl[d].counter; it.dt[d] = dl[d].target; }
               it.chunk = r.counter;
               it.cluster = k;
+              it.prio = rank[t][f];
               seg_items[t][k].push_back(static_cast<int32_t>(P.items.size()));
               P.items.push_back(it);
               P.cluster_total[k] += 1;
@@ -997,14 +1045,21 @@ int compile_plan(Plan& P) {
       }
     }
   }
+  // store the items in queue order: segment (tenant, cluster) after segment
   P.segs.assign(static_cast<size_t>(nt) * P.n_clusters, Seg{0, 0});
+  std::vector<Item> ordered;
+  ordered.reserve(P.items.size());
   for (int t = 0; t < nt; ++t)
     for (int k = 0; k < P.n_clusters; ++k) {
       Seg& sg = P.segs[static_cast<size_t>(t) * P.n_clusters + k];
-      sg.begin = static_cast<int>(P.queue.size());
+      sg.begin = static_cast<int>(ordered.size());
       sg.size = static_cast<int>(seg_items[t][k].size());
-      P.queue.insert(P.queue.end(), seg_items[t][k].begin(), seg_items[t][k].end());
+      for (int32_t i : seg_items[t][k]) {
+        ordered.push_back(P.items[i]);
+        ordered.back().idx = static_cast<int32_t>(ordered.size() - 1);
+      }
     }
+  P.items = std::move(ordered);
   return 0;
 }
 
@@ -1045,7 +1100,6 @@ int upload_plan() {
   int rc;
   if ((rc = dev_upload(&S.d_items, P.items.data(), P.items.size()))) return rc;
   if ((rc = dev_upload(&S.d_deps, P.deps.data(), std::max<size_t>(1, P.deps.size())))) return rc;
-  if ((rc = dev_upload(&S.d_queue, P.queue.data(), std::max<size_t>(1, P.queue.size())))) return rc;
   if ((rc = dev_upload(&S.d_segs, P.segs.data(), P.segs.size()))) return rc;
   if ((rc = dev_upload(&S.d_pref, pref.data(), pref.size()))) return rc;
   if ((rc = dev_upload<uint32_t>(&S.d_heads, nullptr, nheads))) return rc;
@@ -1096,7 +1150,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     }
     ExecParams p;
     std::memset(&p, 0, sizeof p);
-    p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.queue = S.d_queue; p.segs = S.d_segs;
+    p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.segs = S.d_segs;
     p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
     p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
     p.error = S.d_error; p.trace = S.d_trace;
@@ -1106,6 +1160,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     p.n_heads = p.n_tenants * p.n_clusters;
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
+    p.dbg = S.d_dbg;
     CUDA_TRY(launch_executor(p, S.grid, st));
     launches = 1;
   } else {
@@ -1131,6 +1186,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
         std::memset(&base, 0, sizeof base);
         base.error = S.d_error;
         base.watchdog_ns = 2000000000LL;
+        base.dbg = S.d_dbg;
         CUDA_TRY(launch_op(base, S.d_ops, T.op_base + static_cast<int>(f), F.kind, nb, S.num_sms, ts));
         ++launches;
       }
@@ -1202,6 +1258,11 @@ int gacer_init(int cuda_device, const gacer_options* opts) {
       return set_err(GACER_E_CUDA, "device %d is sm_%d0, this library is built for sm_100a", cuda_device, major);
     }
     CUDA_TRY(configure_kernels());
+    if (const char* e = getenv("GACER_DEBUG_TIMING"); e && e[0] == '1') {
+      S.n_dbg = static_cast<size_t>(512) * 148 * DBG_EVENTS;   // up to 512 ops x 148 CTAs
+      CUDA_TRY(cudaMalloc(&S.d_dbg, S.n_dbg * sizeof(int64_t)));
+      CUDA_TRY(cudaMemset(S.d_dbg, 0, S.n_dbg * sizeof(int64_t)));
+    }
     CUDA_TRY(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreate(&S.ev0));
     CUDA_TRY(cudaEventCreate(&S.ev1));
@@ -1403,5 +1464,15 @@ int gacer_get_trace(int64_t* records, int32_t cap) {
 }
 
 const char* gacer_last_error(void) { return g_err.c_str(); }
+
+// Diagnostics (not part of the method): GACER_DEBUG_TIMING=1 milestones.
+int gacer_debug_timing(int64_t* out, int64_t cap, int reset) {
+  if (!S.inited || !S.d_dbg) return set_err(GACER_E_STATE, "GACER_DEBUG_TIMING not enabled");
+  const size_t n = std::min<size_t>(static_cast<size_t>(cap), S.n_dbg);
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (out) CUDA_TRY(cudaMemcpy(out, S.d_dbg, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (reset) CUDA_TRY(cudaMemset(S.d_dbg, 0, S.n_dbg * sizeof(int64_t)));
+  return static_cast<int>(n);
+}
 
 }  // extern "C"

@@ -102,6 +102,7 @@ EXPORTS = {
     "gacer_get_stats": ([C.POINTER(gacer_round_stats)], C.c_int),
     "gacer_get_trace": ([C.POINTER(C.c_int64), C.c_int32], C.c_int),
     "gacer_last_error": ([], C.c_char_p),
+    "gacer_debug_timing": ([C.POINTER(C.c_int64), C.c_int64, C.c_int], C.c_int),
 }
 
 _lib = None
@@ -297,3 +298,9 @@ def gacer_get_trace(cap):
 
 def gacer_last_error():
     return lib().gacer_last_error().decode()
+
+
+def gacer_debug_timing(n_ops=1, reset=True, n_ctas=148, events=16):
+    buf = np.zeros((n_ops, n_ctas, events), dtype=np.int64)
+    _check(lib().gacer_debug_timing(buf.ctypes.data_as(C.POINTER(C.c_int64)), buf.size, int(reset)))
+    return buf
