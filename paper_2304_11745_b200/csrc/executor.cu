@@ -262,9 +262,26 @@ struct Ctx {
 // =====================================================================
 // epilogue math (shared by every mode): y = act(acc*scale + bias [+ skip])
 // =====================================================================
+// The OpDev fields the epilogue uses, copied once per item into registers
+// (reading them through a reference to global memory re-loads them after
+// every store, since the compiler cannot prove the stores do not alias).
+struct EpiOp {
+  void* out;
+  const float* scale;
+  const float* bias;
+  int32_t M, Cout, B, ldo, act, out_f32, has_skip, swap;
+};
+__device__ __forceinline__ EpiOp make_epi(const OpDev& op) {
+  EpiOp e;
+  e.out = op.out; e.scale = op.scale; e.bias = op.bias;
+  e.M = op.M; e.Cout = op.Cout; e.B = op.B; e.ldo = op.ldo; e.act = op.act;
+  e.out_f32 = op.out_f32; e.has_skip = op.has_skip; e.swap = op.swap;
+  return e;
+}
+
 // m: GEMM row; n: first of 8 GEMM columns; sc/bi: the 8 columns' scale/bias
 // (non-swap); skip8: the 8 residual values (bf16) when op.has_skip.
-__device__ __forceinline__ void epilogue_store8(const OpDev& op, int m, int n, const float* v, const float* sc,
+__device__ __forceinline__ void epilogue_store8(const EpiOp& op, int m, int n, const float* v, const float* sc,
                                                 const float* bi, const uint4& skip8) {
   if (m >= op.M) return;
   float y[8];
@@ -300,7 +317,7 @@ __device__ __forceinline__ void epilogue_store8(const OpDev& op, int m, int n, c
 }
 
 // swap-AB (linear): GEMM row m = output feature, GEMM column n = sample
-__device__ __forceinline__ void epilogue_store8_swap(const OpDev& op, int m, int n, const float* v, float sc,
+__device__ __forceinline__ void epilogue_store8_swap(const EpiOp& op, int m, int n, const float* v, float sc,
                                                      float bi) {
   if (m >= op.Cout) return;
   for (int j = 0; j < 8; ++j) {
@@ -1006,25 +1023,32 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     ++islot;
     if (idx < 0) break;
     if (kind != DK_GEMM) continue;
-    const OpDev& op = p.ops[it.op];
-    const int bn = op.bn;
+    const OpDev& opg = p.ops[it.op];
+    const EpiOp op = make_epi(opg);
+    const int bn = opg.bn;
     const int row = ew * 32 + lane;
     const int m0 = it.mt * BM, n0 = it.nt * bn;
     const int m = m0 + row;
-    const int split = op.split_k;
+    const int split = opg.split_k;
     const bool swap = op.swap;
+    const int tiles_n = opg.tiles_n;
+    const __nv_bfloat16* skip_base = static_cast<const __nv_bfloat16*>(opg.skip);
+    const int lds = opg.lds;
+    float* const partial_base = opg.partial;
+    uint32_t* const tile_cnt = opg.tile_cnt;
     // ---- global reads the epilogue needs are issued before the accumulator
     //      is waited on (hides their latency behind the MMA)
     float sc_row = 1.0f, bi_row = 0.0f;
     if (swap) {
       if (m < op.Cout) { sc_row = op.scale[m]; bi_row = op.bias[m]; }
-    } else if (etid < bn) {
-      ctl->epi_scale[etid] = op.scale[n0 + etid];
-      ctl->epi_bias[etid] = op.bias[n0 + etid];
+    } else {
+      for (int j = etid; j < bn; j += NEPI) {
+        ctl->epi_scale[j] = op.scale[n0 + j];
+        ctl->epi_bias[j] = op.bias[n0 + j];
+      }
     }
     const bool do_skip = op.has_skip && split == 1 && m < op.M;
-    const __nv_bfloat16* skrow =
-        do_skip ? static_cast<const __nv_bfloat16*>(op.skip) + static_cast<size_t>(m) * op.lds + n0 : nullptr;
+    const __nv_bfloat16* skrow = do_skip ? skip_base + static_cast<size_t>(m) * lds + n0 : nullptr;
     const int cout_left = op.Cout - n0;
     uint4 skA[4], skB[4];  // residual values of the current / next 32 columns
 #pragma unroll
@@ -1038,7 +1062,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     tc_fence_after();
     const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(ew * 32) << 16);
     float* part = nullptr;
-    const int tile = it.mt * op.tiles_n + it.nt;
+    const int tile = it.mt * tiles_n + it.nt;
     if (split == 1) {
       for (int c = 0; c < bn; c += 32) {
 #pragma unroll
@@ -1068,7 +1092,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     } else {
       // partial layout [tile][ks][bn/4][BM] float4: a warp's 32 rows of one
       // float4 column are 512 contiguous bytes (coalesced write and read)
-      part = op.partial + static_cast<size_t>(tile) * split * (BM * bn);
+      part = partial_base + static_cast<size_t>(tile) * split * (BM * bn);
       float4* mine = reinterpret_cast<float4*>(part + static_cast<size_t>(it.ks) * (BM * bn)) + row;
       for (int c = 0; c < bn; c += 16) {
         float v[16];
@@ -1086,9 +1110,9 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       named_bar_sync(2, NEPI);
       if (etid == 0) {
         __threadfence();
-        const uint32_t old = atomicAdd(op.tile_cnt + tile, 1u);
-        const int last = (old == static_cast<uint32_t>(op.split_k - 1));
-        if (last) op.tile_cnt[tile] = 0;  // all arrivals done: re-arm for the next round
+        const uint32_t old = atomicAdd(tile_cnt + tile, 1u);
+        const int last = (old == static_cast<uint32_t>(split - 1));
+        if (last) tile_cnt[tile] = 0;  // all arrivals done: re-arm for the next round
         ctl->epi_flag = last;
         __threadfence();
       }
@@ -1117,8 +1141,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
           } else {
             uint4 k8 = make_uint4(0, 0, 0, 0);
             if (op.has_skip && m < op.M && c < cout_left)
-              k8 = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(op.skip) +
-                                                   static_cast<size_t>(m) * op.lds + n0 + c);
+              k8 = *reinterpret_cast<const uint4*>(skip_base + static_cast<size_t>(m) * lds + n0 + c);
             epilogue_store8(op, m, n0 + c, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8);
           }
         }
@@ -1127,7 +1150,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     fence_proxy_async_global();  // generic stores -> later TMA reads by consumers
     named_bar_sync(2, NEPI);     // also: epi_scale/bias free for the next item
     if (etid == 0) dbg_mark(p, 7);
-    if (etid == 0 && p.single_op < 0) release_item(p, it, t0, op);
+    if (etid == 0 && p.single_op < 0) release_item(p, it, t0, opg);
   }
 }
 

@@ -23,8 +23,8 @@ enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2 };
 // GEMM tile geometry
 constexpr int BM = 128;           // rows per tile (UMMA M)
 constexpr int BK = 64;            // bf16 elements per K-block = one 128-byte swizzle row
-constexpr int BN_MAX = 128;       // max UMMA N per tile
-constexpr int STAGES = 6;         // smem ring depth (A 16 KB + B 16 KB per stage)
+constexpr int BN_MAX = 256;       // max UMMA N per tile
+constexpr int STAGES = 4;         // smem ring depth (A 16 KB + B 32 KB per stage)
 constexpr int ITEM_RING = 4;      // scheduler -> MMA/epilogue item queue depth
 // warp roles of the executor CTA (16 warps; 4 per SM sub-partition, <= 128 registers)
 constexpr int SCHED_WARP = 0;     // warp 0: scheduler (lane 0) -- claims ready items into the item ring

@@ -623,7 +623,11 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         } else {
           F.M = B * F.Ho * F.Wo; F.N = F.Cout;
           F.tiles_m = cdiv(F.M, BM);
-          F.bn = F.Cout >= BN_MAX ? BN_MAX : roundup(F.Cout, 16);
+          // 128x256 tiles (less L2 operand traffic per FLOP) when they still
+          // give every SM a tile; else N <= 128.  A function of the layer
+          // shape only, identical in every mode.
+          if (F.Cout >= 256 && F.tiles_m * cdiv(F.Cout, 256) >= kSplitSms) F.bn = 256;
+          else F.bn = F.Cout >= 128 ? 128 : roundup(F.Cout, 16);
           F.tiles_n = cdiv(F.Cout, F.bn);
           rows = static_cast<size_t>(F.tiles_n) * F.bn;
         }

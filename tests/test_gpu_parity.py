@@ -68,6 +68,8 @@ CONV_CASES = [
     (3, 32, 3, 2, 1, 33, 2),      # 3-channel input padded to 8
     (16, 48, (1, 7), 1, (0, 3), 12, 2),   # Inception 1x7
     (16, 48, (7, 1), 1, (3, 0), 12, 2),   # Inception 7x1
+    (64, 256, 1, 1, 0, 56, 7),    # 172 M-tiles -> 128x256 tiles
+    (64, 320, 3, 1, 1, 56, 7),    # 128x256 tiles + a ragged N-tile, im2col
 ]
 
 
