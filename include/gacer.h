@@ -216,6 +216,15 @@ int gacer_set_regulation(const gacer_decomposition* decomposition,
  * (out[i] for op i+1), i.e. Eq. 6/7 as compiled.  n = capacity of out. */
 int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n);
 
+/* SM partition of the executor (the paper's resource share W, §4.1
+ * l.597-601): shares[t] > 0 is tenant t's relative share of the executor's
+ * CTAs; each CTA serves its tenant's ready items first and (in the
+ * work-conserving partition) other tenants' items when its own has none
+ * ready.  n = 0 / shares = NULL restores the automatic shares (each tenant's
+ * SM need: estimated work / chain latency).  Part of the regulation state;
+ * reset by gacer_register_tenant. */
+int gacer_set_sm_shares(const float* shares, int32_t n);
+
 int gacer_set_mode(int mode);               /* gacer_mode */
 
 /* One round: every tenant's forward once on its bound input.

@@ -678,6 +678,133 @@ __device__ void window2_bf16(const OpDev& op, int m0, int m1, int c, int HoWo) {
   }
 }
 
+// Row-run window op (bf16 max-pool / avg-pool / depthwise conv, KHxKW taps,
+// stride S): thread (run r, channel group g) computes RUN consecutive output
+// pixels of one channel group, sliding the KHxKW window of raw bf16x8 input
+// vectors along the output row (stride 1 reuses KW-1 of KW columns).  The
+// item's depthwise weights and folded scale/bias are staged in shared memory
+// (wsm) once.  Per output the taps are reduced in the same fixed (r, s)
+// order, each with an IEEE fma, as cc_pixel: results are bit-identical.
+constexpr int RUN = 4;
+template <int KH, int KW, int S>
+__device__ void window_run_bf16(const OpDev& op, const Item& it, int tid, int G, float* wsm) {
+  const int g = tid % G;
+  const int cl = g * 8;                      // channel offset inside the item
+  const int c = it.nt * op.bn + cl;
+  const int bnc = op.bn;
+  const bool dw = op.kind == DK_DW;
+  if (dw) {  // stage weights [tap][bn] and scale/bias [bn] (fp32)
+    const float* wt = static_cast<const float*>(op.wt);
+    const int c0 = it.nt * op.bn;
+    const int nld = KH * KW * bnc;
+    for (int i = tid; i < nld; i += CC_THREADS) {
+      const int t = i / bnc, cc = i - t * bnc;
+      wsm[i] = (c0 + cc < op.Cout) ? wt[t * op.C + c0 + cc] : 0.0f;
+    }
+    for (int i = tid; i < bnc; i += CC_THREADS) {
+      const bool ok = c0 + i < op.Cout;
+      wsm[nld + i] = ok ? op.scale[c0 + i] : 0.0f;
+      wsm[nld + bnc + i] = ok ? op.bias[c0 + i] : 0.0f;
+    }
+  }
+  named_bar_sync(1, CC_THREADS);
+  if (c >= op.Cout) return;
+  const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
+  const int HoWo = op.Ho * op.Wo;
+  const int m_begin = it.mt * op.bm + (tid / G) * RUN;
+  uint4 raw[KH][KW];
+  uint32_t valid = 0;                        // bit r*KW+s
+  int ho = -1, wo = 0, b = 0;
+  for (int j = 0; j < RUN; ++j) {
+    const int m = m_begin + j;
+    if (m >= op.M) break;
+    bool fresh = true;
+    if (ho >= 0 && wo + 1 < op.Wo) {         // same row: slide by S columns
+      ++wo;
+      fresh = false;
+    } else {
+      b = m / HoWo;
+      const int rem = m - b * HoWo;
+      ho = rem / op.Wo;
+      wo = rem - ho * op.Wo;
+    }
+    const size_t img = static_cast<size_t>(b) * op.H * op.W;
+#pragma unroll
+    for (int r = 0; r < KH; ++r) {
+      const int hi = ho * S - op.ph + r;
+      const bool hok = hi >= 0 && hi < op.H;
+#pragma unroll
+      for (int s = 0; s < KW; ++s) {
+        if (!fresh && s + S < KW) {          // reuse a column of the previous window
+          raw[r][s] = raw[r][s + S];
+          const uint32_t bit = (valid >> (r * KW + s + S)) & 1u;
+          valid = (valid & ~(1u << (r * KW + s))) | (bit << (r * KW + s));
+        } else {
+          const int wi = wo * S - op.pw + s;
+          const bool ok = hok && wi >= 0 && wi < op.W;
+          raw[r][s] = ok ? *reinterpret_cast<const uint4*>(in + (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c)
+                         : make_uint4(0, 0, 0, 0);
+          valid = (valid & ~(1u << (r * KW + s))) | ((ok ? 1u : 0u) << (r * KW + s));
+        }
+      }
+    }
+    float y[8];
+    const float init = op.kind == DK_MAXPOOL ? -INFINITY : 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = init;
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < KH; ++r)
+#pragma unroll
+      for (int s = 0; s < KW; ++s) {
+        const bool ok = (valid >> (r * KW + s)) & 1u;
+        if (op.kind == DK_AVGPOOL) {
+          const int hi = ho * S - op.ph + r, wi = wo * S - op.pw + s;
+          const bool in_frame = hi >= -op.ph && hi < op.H + op.ph && wi >= -op.pw && wi < op.W + op.pw;
+          cnt += (op.cip ? in_frame : ok) ? 1 : 0;
+        }
+        if (!ok) continue;
+        float f[8];
+        bf16x8_to_f32(raw[r][s], f);
+        if (op.kind == DK_MAXPOOL) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
+        } else if (op.kind == DK_AVGPOOL) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) y[q] += f[q];
+        } else {
+          const float* w = wsm + (r * KW + s) * bnc + cl;
+          const float4 w0 = *reinterpret_cast<const float4*>(w);
+          const float4 w1 = *reinterpret_cast<const float4*>(w + 4);
+          float2 a;
+          a = __ffma2_rn(make_float2(f[0], f[1]), make_float2(w0.x, w0.y), make_float2(y[0], y[1])); y[0] = a.x; y[1] = a.y;
+          a = __ffma2_rn(make_float2(f[2], f[3]), make_float2(w0.z, w0.w), make_float2(y[2], y[3])); y[2] = a.x; y[3] = a.y;
+          a = __ffma2_rn(make_float2(f[4], f[5]), make_float2(w1.x, w1.y), make_float2(y[4], y[5])); y[4] = a.x; y[5] = a.y;
+          a = __ffma2_rn(make_float2(f[6], f[7]), make_float2(w1.z, w1.w), make_float2(y[6], y[7])); y[6] = a.x; y[7] = a.y;
+        }
+      }
+    if (op.kind == DK_AVGPOOL) {
+      const float inv = static_cast<float>(cnt);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = y[q] / inv;
+    } else if (dw) {
+      const float* sc = wsm + KH * KW * bnc + cl;
+      const float* bi = sc + bnc;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
+      if (op.has_skip) {
+        float sk[8];
+        load8<false>(op.skip, static_cast<size_t>(m) * op.lds + c, sk);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] += sk[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = apply_act(y[q], op.act);
+    store8<false>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+  }
+}
+
 // tile: bm output pixels x bn channels; G = bn/8 channel groups; thread tid
 // (of CC_THREADS) handles pixels tid / G + j * (CC_THREADS / G), group tid % G.
 // Runs on the worker warps (named barrier 1) or a standalone CTA.
@@ -722,9 +849,18 @@ __device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
     }
     return;
   }
-  if (c >= op.Cout) return;
   const int HoWo = op.Ho * op.Wo;
   const int mb = it.mt * op.bm + tid / G;
+  if (!F32 && op.kind != DK_ELTWISE && op.kh == 3 && op.kw == 3 && (op.stride == 1 || op.stride == 2)) {
+    if (op.stride == 1) window_run_bf16<3, 3, 1>(op, it, tid, G, red);
+    else window_run_bf16<3, 3, 2>(op, it, tid, G, red);
+    return;
+  }
+  if (!F32 && op.kind != DK_ELTWISE && op.kh == 2 && op.kw == 2 && op.stride == 2) {
+    window_run_bf16<2, 2, 2>(op, it, tid, G, red);
+    return;
+  }
+  if (c >= op.Cout) return;
   if (!F32 && op.kind != DK_ELTWISE && op.kh * op.kw <= 9) {
     // latency-bound window ops: two output pixels per step, all their tap
     // loads issued back to back (branch-free, predicated), then reduced
@@ -810,80 +946,43 @@ __device__ __forceinline__ Seg get_seg(const ExecParams& p, const SmemCtl* ctl, 
   return si < ctl->n_segs_smem ? ctl->segs[si] : p.segs[si];
 }
 
-// Claim the next item of the open cluster k.  Greedy, dependency-aware issue
-// (§3, l.438-444: an operator that cannot be deployed now "is moved
-// to the next cycle"): among the head items of the tenant queues this CTA may
-// serve, claim the READY one (producers complete) with the highest upward
-// rank (longest estimated remaining chain, computed by the plan compiler).
-// The critical tenant's chain advances at full width while the others fill
-// its residue (l.447-453).  Unready heads are never claimed, which keeps the
-// wait-for graph acyclic.  Returns the item position, -2 when the round is
-// done, -3 on abort.
-__device__ int claim_item(const ExecParams& p, const SmemCtl* ctl, int& k, Item& out) {
+// Find the best claimable item of the open cluster k without claiming it.
+// Greedy, dependency-aware issue (§3, l.438-444: an operator that
+// cannot be deployed now "is moved to the next cycle"): among the head items
+// of the tenant queues this CTA may serve, pick the READY one (producers
+// complete) with the highest upward rank (longest estimated remaining chain,
+// computed by the plan compiler).  The critical tenant's chain advances while
+// the others fill its residue (l.447-453).  Unready heads are never claimed,
+// which keeps the wait-for graph acyclic.
+// Returns 1 (candidate in si/h/cand), 0 (unclaimed work, none ready),
+// 2 (every item of cluster k claimed).
+__device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& best_si, uint32_t& best_h,
+                          Item& cand) {
   const int32_t* pref = p.cta_pref + static_cast<size_t>(blockIdx.x) * p.n_tenants;
-  uint64_t t0 = 0;
-  uint32_t spins = 0;
-  while (k < p.n_clusters) {
-    bool unclaimed = false;
-    int best_si = -1;
-    uint32_t best_prio = 0;
-    for (int j = 0; j < p.n_tenants; ++j) {
-      const int t = pref[j];
-      if (t < 0) break;
-      const int si = t * p.n_clusters + k;
-      const Seg sg = get_seg(p, ctl, si);
-      if (sg.size == 0) continue;
-      const uint32_t h = ld_relaxed(p.heads + si);
-      if (h >= static_cast<uint32_t>(sg.size)) continue;
-      unclaimed = true;
-      const uint32_t prio = p.items[sg.begin + h].prio;
-      if (best_si >= 0 && prio <= best_prio) continue;
-      if (!deps_ready(p, p.items[sg.begin + h])) continue;
-      best_si = si;
-      best_prio = prio;
-    }
-    if (best_si >= 0) {
-      const Seg sg = get_seg(p, ctl, best_si);
-      const uint32_t idx = atomicAdd(p.heads + best_si, 1u);
-      if (idx < static_cast<uint32_t>(sg.size)) {
-        out = p.items[sg.begin + idx];
-        // the claimed item may be a later one than the one checked (race):
-        // its dependencies were claimed earlier, so this wait terminates
-        if (!deps_ready(p, out)) {
-          if (out.dep_count <= INLINE_DEPS) {
-            for (int d = 0; d < out.dep_count; ++d)
-              if (!spin_ge(p.chunk_done + out.dc[d], p.epoch * out.dt[d], p)) return -3;
-          } else {
-            for (int d = 0; d < out.dep_count; ++d) {
-              const Dep dp = p.deps[out.dep_begin + d];
-              if (!spin_ge(p.chunk_done + dp.counter, p.epoch * dp.target, p)) return -3;
-            }
-          }
-        }
-        return sg.begin + static_cast<int>(idx);
-      }
-      continue;  // lost the race for the last item of that queue: rescan
-    }
-    if (!unclaimed) {
-      // every item of cluster k is claimed: the synchronisation pointer --
-      // wait until every item of cluster k (all tenants) is done.
-      if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) return -3;
-      ++k;
-      spins = 0;
-      continue;
-    }
-    // unclaimed work exists but none of it is ready yet: back off, rescan
-    __nanosleep(spins < 4 ? 64u : (spins < 8 ? 256u : 512u));
-    if (spins++ == 0) t0 = globaltimer();
-    if ((spins & 31) == 0) {
-      if (*reinterpret_cast<volatile int32_t*>(p.error)) return -3;
-      if (static_cast<int64_t>(globaltimer() - t0) > p.watchdog_ns) {
-        atomicExch(p.error, 1);
-        return -3;
-      }
-    }
+  bool unclaimed = false;
+  best_si = -1;
+  uint32_t best_prio = 0;
+  for (int j = 0; j < p.n_tenants; ++j) {
+    const int t = pref[j];
+    if (t < 0) break;
+    const int si = t * p.n_clusters + k;
+    const Seg sg = get_seg(p, ctl, si);
+    if (sg.size == 0) continue;
+    const uint32_t h = ld_relaxed(p.heads + si);
+    if (h >= static_cast<uint32_t>(sg.size)) continue;
+    unclaimed = true;
+    const Item* ip = p.items + sg.begin + h;
+    const uint32_t prio = ip->prio;
+    if (best_si >= 0 && prio <= best_prio) continue;
+    const Item c = *ip;
+    if (!deps_ready(p, c)) continue;
+    best_si = si;
+    best_h = h;
+    best_prio = prio;
+    cand = c;
+    if (j == 0) return 1;  // the CTA's own tenant (SM partition) comes first
   }
-  return -2;
+  return best_si >= 0 ? 1 : (unclaimed ? 0 : 2);
 }
 
 __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, uint64_t t0, const OpDev& op) {
@@ -899,32 +998,100 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
   }
 }
 
+// Wait (blocking) until the item's dependencies are complete; false on abort.
+__device__ bool wait_deps(const ExecParams& p, const Item& it) {
+  if (it.dep_count <= INLINE_DEPS) {
+    for (int d = 0; d < it.dep_count; ++d)
+      if (!spin_ge(p.chunk_done + it.dc[d], p.epoch * it.dt[d], p)) return false;
+  } else {
+    for (int d = 0; d < it.dep_count; ++d) {
+      const Dep dp = p.deps[it.dep_begin + d];
+      if (!spin_ge(p.chunk_done + dp.counter, p.epoch * dp.target, p)) return false;
+    }
+  }
+  return true;
+}
+
+// The scheduler (warp 0, lane 0).  It finds the best ready candidate BEFORE
+// waiting for room in the CTA's item ring (the scan latency overlaps the
+// items in flight), then claims it.  In-flight depth: items continuing the
+// same large op may be claimed up to LOOKAHEAD deep (hides claim latency);
+// any other item only when the ring is drained to depth 1, so a
+// latency-critical item of a small op never queues behind several long tiles
+// of a big op (head-of-line blocking inside the CTA).
 __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = cx.ctl;
-  uint32_t islot = 0;
+  uint32_t islot = 0, consumed = 0;
   int k = 0;
   int sidx = blockIdx.x;
+  int last_op = -1;
+  const int big = 4 * static_cast<int>(gridDim.x);
   for (;;) {
-    // at most LOOKAHEAD claimed-but-unconsumed items per CTA
-    if (islot >= LOOKAHEAD) {
-      const uint32_t old = islot - LOOKAHEAD;
-      mbar_wait(&ctl->rempty[old % ITEM_RING], (old / ITEM_RING) & 1);
-    }
     Item it;
-    int claimed;
+    int claimed = -1;
     if (p.single_op >= 0) {
+      while (islot - consumed >= 2) {
+        mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
+        ++consumed;
+      }
       const OpDev& op = p.ops[p.single_op];
       const int n = op.tiles_m * op.tiles_n * (op.kind == DK_GEMM ? op.split_k : 1);
       claimed = sidx < n ? sidx : -2;
       if (claimed >= 0) it = decode_single(op, p.single_op, sidx);
       sidx += gridDim.x;
     } else {
-      claimed = claim_item(p, ctl, k, it);
-      if (claimed >= 0) __threadfence();  // acquire side: drop stale L1 lines before the CTA reads inputs
+      uint64_t t0 = 0;
+      uint32_t spins = 0;
+      while (claimed == -1) {
+        if (k >= p.n_clusters) { claimed = -2; break; }
+        int si;
+        uint32_t h;
+        Item cand;
+        const int st = scan_ready(p, ctl, k, si, h, cand);
+        if (st == 2) {
+          // every item of cluster k is claimed: the synchronisation pointer --
+          // wait until every item of cluster k (all tenants) is done.
+          if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) { claimed = -3; break; }
+          ++k;
+          spins = 0;
+          continue;
+        }
+        if (st == 0) {  // unclaimed work exists but none of it is ready: back off, rescan
+          __nanosleep(spins < 4 ? 64u : (spins < 8 ? 256u : 512u));
+          if (spins++ == 0) t0 = globaltimer();
+          if ((spins & 31) == 0) {
+            if (*reinterpret_cast<volatile int32_t*>(p.error)) { claimed = -3; break; }
+            if (static_cast<int64_t>(globaltimer() - t0) > p.watchdog_ns) {
+              atomicExch(p.error, 1);
+              claimed = -3;
+              break;
+            }
+          }
+          continue;
+        }
+        const uint32_t allowed = (cand.op == last_op && cand.op_left > big) ? LOOKAHEAD : 1;
+        while (islot - consumed >= allowed) {
+          mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
+          ++consumed;
+        }
+        const Seg sg = get_seg(p, ctl, si);
+        const uint32_t idx = atomicAdd(p.heads + si, 1u);
+        if (idx >= static_cast<uint32_t>(sg.size)) continue;  // lost the race for the last item
+        if (idx == h) {
+          it = cand;
+        } else {
+          // claimed a later item than the one checked: its dependencies are
+          // items claimed before it, so this wait terminates
+          it = p.items[sg.begin + idx];
+          if (!wait_deps(p, it)) { claimed = -3; break; }
+        }
+        claimed = sg.begin + static_cast<int>(idx);
+        last_op = it.op;
+      }
+      if (claimed >= 0) __threadfence();  // acquire side (pairs with the producers' release)
     }
     dbg_mark(p, 1);
-    const uint32_t slot = islot % ITEM_RING;
-    // (slot reuse is implied by the LOOKAHEAD wait since LOOKAHEAD <= ITEM_RING)
+    const uint32_t slot = islot % ITEM_RING;  // free: islot - consumed < LOOKAHEAD < ITEM_RING
     RingSlot& rs = ctl->ring[slot];
     rs.it = it;
     rs.idx = claimed >= 0 ? claimed : -1;

@@ -37,7 +37,7 @@ constexpr int NTHREADS = 512;
 constexpr int CC_THREADS = NWORK; // threads that execute a CUDA-core item
 constexpr int CC_TASKS_PER_THREAD = 4;
 constexpr int MAX_SPLIT = 4;      // split-K factor cap (fixed per layer shape)
-constexpr int LOOKAHEAD = 1;      // claimed items not yet picked up by every role (per CTA)
+constexpr int LOOKAHEAD = 3;      // max claimed items not yet picked up by every role (per CTA)
 constexpr int INLINE_DEPS = 4;    // dependencies stored inside the Item
 constexpr int MAX_SMEM_SEGS = 256;
 
@@ -96,6 +96,7 @@ struct Item {
   int32_t cluster;
   uint32_t prio;           // upward rank: estimated remaining critical path (ns) of its tenant
   int32_t idx;             // position in the item array (trace / diagnostics)
+  int32_t op_left;         // items of the same op after this one in its queue segment
   int32_t dep_count;       // <= INLINE_DEPS: dc/dt hold them, else dep list at dep_begin
   int32_t dep_begin;
   int32_t dc[INLINE_DEPS]; // producer chunk counters

@@ -143,6 +143,7 @@ struct Plan {
   std::vector<uint32_t> cluster_total;
   int n_chunk_counters = 0;
   std::vector<std::vector<int>> fop_cluster;        // [tenant][fused op]
+  std::vector<double> auto_share;                   // per tenant: SM need (work / chain latency)
 };
 
 struct State {
@@ -155,6 +156,7 @@ struct State {
   std::vector<cudaStream_t> tstreams;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<Tenant> tenants;
+  std::vector<double> user_share;   // gacer_set_sm_shares (empty = automatic)
   Plan plan;
   int mode = GACER_MODE_EXECUTOR;
   bool sticky_cuda = false;
@@ -606,12 +608,22 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
               for (int c = 0; c < F.Cin; ++c)
                 F.w_f32[static_cast<size_t>(co) * F.K + (r * F.kw + s) * F.cread + c] = wval(co, c, r, s);
       } else {
-        F.cread = roundup(F.Cin, 8);
-        if (F.in_t == 0 && F.cread > X.ldc) return set_err(GACER_E_UNSUPPORTED_OP, "input padding");
+        F.swap = lin && X.ldc == X.C && F.skip_t < 0;
+        // operand A: TMA im2col loads 64 channels of one tap per K-block and
+        // zero-fills channels >= Cin, so the per-tap K stride is Cin rounded
+        // up to 64; used when that padding wastes at most 1.5x (always for
+        // 1x1), else the cp.async gather with a stride of Cin rounded to 8.
+        {
+          const int c8 = roundup(F.Cin, 8), c64 = roundup(F.Cin, 64);
+          const bool tma = c64 == c8 || F.kh * F.kw == 1 || 2 * c64 <= 3 * c8;
+          F.a_mode = F.swap ? A_ROWS : (tma ? A_IM2COL : A_GATHER);
+          F.cread = (F.a_mode == A_IM2COL) ? c64 : c8;
+        }
+        if (F.in_t == 0 && F.a_mode == A_GATHER && F.cread > X.ldc)
+          return set_err(GACER_E_UNSUPPORTED_OP, "input padding");
         F.K = F.kh * F.kw * F.cread;
         F.Kpad = roundup(F.K, BK);
         F.nkb = F.Kpad / BK;
-        F.swap = lin && X.ldc == X.C && F.skip_t < 0;
         size_t rows;
         if (F.swap) {
           F.rows_are_pixels = false;
@@ -632,7 +644,6 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           rows = static_cast<size_t>(F.tiles_n) * F.bn;
         }
         F.bm = BM;
-        F.a_mode = F.swap ? A_ROWS : (F.cread % 64 == 0 ? A_IM2COL : A_GATHER);
         // split-K: a function of the layer shape only (same in every mode/plan)
         const int tiles = F.tiles_m * F.tiles_n;
         int sk = 1;
@@ -672,7 +683,10 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
     if (F.kind != DK_GEMM && F.kind != DK_SIMT_GEMM) {
       F.bn = std::min(64, pow2ceil(roundup(F.Cout, 8)));
       const int G = F.bn / 8;
-      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : CC_TASKS_PER_THREAD * (CC_THREADS / G);
+      const bool run = F.kind != DK_GAP && F.kind != DK_ELTWISE && !f32 &&
+                       ((F.kh == 3 && F.kw == 3 && (F.stride == 1 || F.stride == 2)) ||
+                        (F.kh == 2 && F.kw == 2 && F.stride == 2));
+      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : (run ? 4 /*RUN*/ : CC_TASKS_PER_THREAD) * (CC_THREADS / G);
       F.tiles_m = cdiv(F.M, F.bm);
       F.tiles_n = cdiv(F.Cout, F.bn);
       F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
@@ -806,8 +820,10 @@ int encode_rows(CUtensorMap* m, const void* base, int cols, int rows, int ld, in
 // NHWC bf16 activation as an im2col view: 128 output pixels x 64 channels of
 // one filter tap per load (pixelsPerColumn = BM, channelsPerPixel = BK).
 // Bounding box per CUTLASS fprop convention: lower = -pad, upper = pad - (k-1).
-int encode_im2col(CUtensorMap* m, const OpDev& d) {
-  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.C), static_cast<cuuint64_t>(d.W),
+int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c) {
+  // globalDim[0] is the tensor's real channel count: channels [Cin, cread)
+  // of a 64-channel box are out of bounds and zero-filled by the TMA
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(real_c), static_cast<cuuint64_t>(d.W),
                               static_cast<cuuint64_t>(d.H), static_cast<cuuint64_t>(d.B)};
   const cuuint64_t st[3] = {static_cast<cuuint64_t>(d.ldi) * 2, static_cast<cuuint64_t>(d.ldi) * 2 * d.W,
                             static_cast<cuuint64_t>(d.ldi) * 2 * d.W * d.H};
@@ -856,7 +872,7 @@ int rebuild_op_table() {
       rc = encode_rows(&maps[2 * i], d.wt, d.Kpad, d.tiles_m * BM, d.Kpad, BM);
       if (!rc) rc = encode_rows(&maps[2 * i + 1], d.act_b, d.K, d.B, d.ldb, d.bn);
     } else {
-      if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[2 * i], d);
+      if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[2 * i], d, F.Cin);
       if (!rc) rc = encode_rows(&maps[2 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
     }
     if (rc) return rc;
@@ -940,27 +956,38 @@ int compile_plan(Plan& P) {
   }
   P.n_chunk_counters = counter;
 
-  // upward rank of every fused op (HEFT-style): estimated time of the op on
-  // the whole GPU + the longest rank among its consumers.  The device
+  // upward rank of every fused op (HEFT-style list scheduling): estimated
+  // latency of the op + the longest rank among its consumers.  The device
   // scheduler claims the ready head item with the highest rank first.
   std::vector<std::vector<uint32_t>> rank(nt);
+  P.auto_share.assign(nt, 1.0);
   for (int t = 0; t < nt; ++t) {
     const Tenant& T = S.tenants[t];
     const size_t nf = T.fops.size();
-    std::vector<double> est(nf), rk(nf, 0.0);
+    std::vector<double> est(nf), rk(nf, 0.0), wk(nf, 0.0);
     for (size_t f = 0; f < nf; ++f) {
       const FusedOp& F = T.fops[f];
       const int split = (F.kind == DK_GEMM) ? F.split_k : 1;
       const double items = static_cast<double>(F.tiles_m) * F.tiles_n * split;
       const double waves = std::ceil(items / kSplitSms);
+      // per-item time at the executor's measured rates (~2.7 TFLOP/s of
+      // tensor work and ~10 GB/s of CUDA-core traffic per SM), and a per-op
+      // latency floor (dependency notice + claim + first load + epilogue):
+      // a chain of many small ops is long even when its work is tiny.
       double item_ns;
       if (F.kind == DK_GEMM) {
         const double kblocks = static_cast<double>(F.nkb) / split;
-        item_ns = kblocks * BK * BM * F.bn * 2.0 / 8192.0 / 1.9 + 1000.0;  // ~8192 FLOP/cycle/SM at 1.9 GHz
+        item_ns = kblocks * BK * BM * F.bn * 2.0 / 2700.0 + 1500.0;
       } else {
-        item_ns = F.bytes / std::max(1.0, items) / 40.0 + 1000.0;          // ~40 B/ns per SM
+        item_ns = F.bytes / std::max(1.0, items) / 10.0 + 2000.0;
       }
-      est[f] = waves * item_ns;
+      // Rank = remaining chain LATENCY: per op a latency floor plus one item
+      // (not the op's whole work).  Narrow ops of long chains (latency-bound)
+      // then outrank the wide ops of a throughput-bound tenant, which absorb
+      // the delay by filling whatever SMs the chains leave free.
+      wk[f] = items * item_ns / kSplitSms;  // work, as full-GPU time
+      (void)waves;
+      est[f] = 10000.0 + item_ns;
     }
     for (size_t f = nf; f-- > 0;) {
       double best = 0.0;
@@ -976,6 +1003,14 @@ int compile_plan(Plan& P) {
     }
     rank[t].resize(nf);
     for (size_t f = 0; f < nf; ++f) rank[t][f] = static_cast<uint32_t>(std::min(rk[f], 4.0e9));
+    // SM need of the tenant (the paper's resource share W, §4.1 l.597-601):
+    // the fraction of the GPU that sustains its work at its chain latency
+    double work_ns = 0.0, chain_ns = 0.0;
+    for (size_t f = 0; f < nf; ++f) {
+      work_ns += wk[f];
+      chain_ns = std::max(chain_ns, rk[f]);
+    }
+    P.auto_share[t] = std::min(1.0, work_ns / std::max(1.0, chain_ns));
   }
 
   // items, grouped by (tenant, cluster) segment, in issue order
@@ -1062,18 +1097,30 @@ int compile_plan(Plan& P) {
         ordered.push_back(P.items[i]);
         ordered.back().idx = static_cast<int32_t>(ordered.size() - 1);
       }
+      int run = 0;  // op_left: items of the same op that follow in the segment
+      for (int i = static_cast<int>(ordered.size()) - 1; i >= sg.begin; --i) {
+        run = (i + 1 < static_cast<int>(ordered.size()) && i + 1 < sg.begin + sg.size &&
+               ordered[i + 1].op == ordered[i].op) ? run + 1 : 0;
+        ordered[i].op_left = run;
+      }
     }
   P.items = std::move(ordered);
   return 0;
 }
 
-// SM partition: CTA c prefers tenant own[c] (shares proportional to tenant
-// FLOPs, at least one CTA each -- the resource share W of §4.1 l.597-601).
+// SM partition: CTA c prefers tenant own[c]; tenant shares are the plan's
+// (gacer_set_sm_shares) or, by default, each tenant's SM need -- work divided
+// by chain latency, the resource share W of §4.1 l.597-601 -- normalised;
+// every tenant gets at least one CTA.
 std::vector<int32_t> make_pref(int grid) {
   const int nt = static_cast<int>(S.tenants.size());
   std::vector<double> w(nt);
   double tot = 0;
-  for (int t = 0; t < nt; ++t) { w[t] = std::max(1.0, S.tenants[t].flops); tot += w[t]; }
+  for (int t = 0; t < nt; ++t) {
+    w[t] = (static_cast<int>(S.user_share.size()) == nt) ? S.user_share[t] : S.plan.auto_share[t];
+    w[t] = std::max(w[t], 1e-6);
+    tot += w[t];
+  }
   std::vector<int> own(grid);
   std::vector<double> got(nt, 0.0);
   for (int c = 0; c < grid; ++c) {  // largest deficit first (weighted round robin)
@@ -1086,6 +1133,13 @@ std::vector<int32_t> make_pref(int grid) {
     own[c] = best;
     got[best] += 1.0;
   }
+  for (int t = 0; t < nt && nt <= grid; ++t)  // at least one CTA per tenant
+    if (got[t] < 1.0) {
+      int donor = 0;
+      for (int u = 1; u < nt; ++u) if (got[u] > got[donor]) donor = u;
+      for (int c = grid - 1; c >= 0; --c)
+        if (own[c] == donor) { own[c] = t; got[t] += 1; got[donor] -= 1; break; }
+    }
   std::vector<int32_t> pref(static_cast<size_t>(grid) * nt, -1);
   for (int c = 0; c < grid; ++c) {
     pref[static_cast<size_t>(c) * nt] = own[c];
@@ -1305,6 +1359,7 @@ int gacer_register_tenant(const gacer_graph* graph, int32_t batch) {
   if (int rc = rebuild_op_table()) return rc;
   // registration resets the plan to the identity plan
   S.plan = Plan();
+  S.user_share.clear();
   if (int rc = compile_plan(S.plan)) return rc;
   if (int rc = upload_plan()) return rc;
   return id;
@@ -1405,6 +1460,23 @@ int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n) {
   const int m = std::min(n, T.n_orig);
   for (int i = 0; i < m; ++i) out[i] = cluster_of_orig(S.plan, tenant, i);
   return m;
+}
+
+int gacer_set_sm_shares(const float* shares, int32_t n) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (n == 0 || !shares) {
+    S.user_share.clear();
+  } else {
+    if (n != static_cast<int32_t>(S.tenants.size()))
+      return set_err(GACER_E_INVALID_ARG, "%d shares for %zu tenants", n, S.tenants.size());
+    std::vector<double> v(n);
+    for (int i = 0; i < n; ++i) {
+      if (!(shares[i] > 0.0f)) return set_err(GACER_E_INVALID_ARG, "share %d must be > 0", i);
+      v[i] = shares[i];
+    }
+    S.user_share = v;
+  }
+  return upload_plan();
 }
 
 int gacer_set_mode(int mode) {

@@ -1,0 +1,70 @@
+"""Sweep regulation plans (SM shares, partition mode, sync pointers, batch
+chunking) on the D2 mix and report the executor makespan of each."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2304_11745_b200 import gacer as G  # noqa: E402
+from paper_2304_11745_b200.runtime import Session  # noqa: E402
+
+
+def time_round(s, reps=10):
+    stream = torch.cuda.Stream()
+    for _ in range(3):
+        G.gacer_run_round_async(stream.cuda_stream)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        G.gacer_run_round_async(stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def equal_cuts(n_ops, k):
+    return [round(n_ops * (j + 1) / (k + 1)) for j in range(k)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/plan_sweep.json")
+    a = ap.parse_args()
+    ts = bench.make_workload()
+    res = []
+    for partition in ("work_conserving", "strict"):
+        s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], partition=partition)
+        for t, (*_, x) in enumerate(ts):
+            s.set_input(t, x)
+        nops = [len(g.ops) for _, g, *_ in ts]
+        plans = [("identity", None, None, None)]
+        for sh in ([0.2, 0.7, 0.1], [0.3, 0.6, 0.1], [0.25, 0.5, 0.25], [0.35, 0.45, 0.2]):
+            plans.append((f"shares{sh}", None, None, sh))
+        for k in (1, 2, 3, 4, 6):
+            plans.append((f"ptr{k}", None, [equal_cuts(n, k) for n in nops], None))
+        vgg = ts[1][1]
+        vdec = [(1, i + 1, "batch", [4, 4]) for i, op in enumerate(vgg.ops) if op["kind"] == "conv"]
+        plans.append(("vgg_conv_b44", vdec, None, None))
+        plans.append(("vgg_conv_b44+ptr2", vdec, [equal_cuts(n, 2) for n in nops], None))
+        for name, dec, ptr, sh in plans:
+            s.set_regulation(dec, ptr)
+            G.gacer_set_sm_shares(sh)
+            ms = time_round(s)
+            res.append({"partition": partition, "plan": name, "ms": ms})
+            print(json.dumps(res[-1]), flush=True)
+        s.close()
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    json.dump(res, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -68,6 +68,8 @@ CONV_CASES = [
     (3, 32, 3, 2, 1, 33, 2),      # 3-channel input padded to 8
     (16, 48, (1, 7), 1, (0, 3), 12, 2),   # Inception 1x7
     (16, 48, (7, 1), 1, (3, 0), 12, 2),   # Inception 7x1
+    (24, 144, 1, 1, 0, 28, 2),    # C = 24: TMA im2col, channels 24..63 zero-filled
+    (160, 192, (7, 1), 1, (3, 0), 12, 2),  # C = 160 -> 192-channel tap stride, 7x1
     (64, 256, 1, 1, 0, 56, 7),    # 172 M-tiles -> 128x256 tiles
     (64, 320, 3, 1, 1, 56, 7),    # 128x256 tiles + a ragged N-tile, im2col
 ]
@@ -96,16 +98,18 @@ def test_conv_op_parity(cuda_ok, cin, cout, k, stride, pad, hw, B):
     assert exact >= 0.999, exact
 
 
-@pytest.mark.parametrize("kind", ["dw", "maxpool", "avgpool", "gap"])
+@pytest.mark.parametrize("kind", ["dw", "dw_s1", "maxpool", "maxpool2", "avgpool", "gap"])
 def test_cuda_core_op_parity(cuda_ok, kind):
     B, C, hw = 3, 40, 13
     g = workloads.Graph("cc_op", C, hw, hw)
-    if kind == "dw":
-        y = g.conv(0, C, C, 3, 2, 1, groups=C)
+    if kind in ("dw", "dw_s1"):
+        y = g.conv(0, C, C, 3, 2 if kind == "dw" else 1, 1, groups=C)
         y = g.bn(y, C)
         g.relu6(y)
     elif kind == "maxpool":
         g.maxpool(0, 3, 2, 1)
+    elif kind == "maxpool2":
+        g.maxpool(0, 2, 2, 0)
     elif kind == "avgpool":
         g.avgpool(0, 3, 1, 1)
     else:
@@ -116,7 +120,7 @@ def test_cuda_core_op_parity(cuda_ok, kind):
     ref = forward_graph(g, p, x, return_all=True)[1][g.ops[-1]["id"]]
     y = nhwc_to_nchw(outs[0], B, ref.shape[2], ref.shape[3], C)
     assert maxrel(y, ref) <= 2e-2
-    if kind == "maxpool":
+    if kind.startswith("maxpool"):
         assert np.array_equal(y, ref)   # max of bf16 values is exact
 
 
