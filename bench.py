@@ -100,16 +100,45 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
-def make_workload(cfg=CONFIG):
+def make_workload(cfg=CONFIG, rank=0):
+    """The config's tenants with seeded random-init weights; each rank (GPU
+    replica) draws its own input batch."""
     import workloads
     from workloads.zoo import CONFIG_INDEX
+    from paper_2304_11745_b200.placement import replica_seed
     ts = []
     for i, (name, B, dt) in enumerate(workloads.config_tenants(cfg)):
         g = workloads.build_model(name)
         seed = workloads.tenant_seed(CONFIG_INDEX[cfg], i)
         ts.append((name, g, workloads.make_params(g, seed, dt), B, dt,
-                   workloads.make_input(g, B, seed, dt)))
+                   workloads.make_input(g, B, replica_seed(seed, rank), dt)))
     return ts
+
+
+def sweep_plans(ts):
+    """Regulation plans tried by the bench: the identity
+    plan, SM-share variants (the paper's resource share W), equal-op-count
+    sync pointers (Matrix_P, Eq. 7) and VGG batch chunking (Eq. 5, cf. the
+    paper's Table 3 case 2)."""
+    nops = [len(g.ops) for _, g, *_ in ts]
+    names = [n for n, *_ in ts]
+
+    def cuts(n, k):
+        return [round(n * (j + 1) / (k + 1)) for j in range(k)]
+    plans = [("identity", None, None, None)]
+    if len(ts) == 3:
+        plans += [("shares[.35,.45,.2]", None, None, [0.35, 0.45, 0.2]),
+                  ("shares[.25,.5,.25]", None, None, [0.25, 0.5, 0.25])]
+    plans += [(f"pointers{k}", None, [cuts(n, k) for n in nops], None) for k in (2, 4)]
+    if "vgg16" in names:
+        t = names.index("vgg16")
+        g = ts[t][1]
+        B = ts[t][3]
+        half = [B // 2, B - B // 2]
+        dec = [(t, i + 1, "batch", half) for i, op in enumerate(g.ops) if op["kind"] == "conv"]
+        plans.append(("vgg_conv_batch_split", dec, None, None))
+        plans.append(("vgg_conv_batch_split+pointers2", dec, [cuts(n, 2) for n in nops], None))
+    return plans
 
 
 def cpu_oracle_sample(ts, budget_s=30.0):
@@ -126,31 +155,44 @@ def cpu_oracle_sample(ts, budget_s=30.0):
         if time.perf_counter() - t0 > budget_s:
             break
     dt_s = time.perf_counter() - t0
-    desc = f"1 image of each of {n} tenant(s) of {CONFIG} (fp64 oracle, OpenMP)"
+    desc = f"1 image of each of {n} tenant(s) of the mix (fp64 oracle, OpenMP)"
     return n / dt_s, oops.num_threads(), desc, dt_s
 
 
 # ------------------------------------------------------------------ main arms
 def run_reference(args, rank):
+    """The reference arm of this tier: the fp64 oracle as it stands, timed on
+    the host cores.  Each step is a bounded sample of the workload: one image
+    of one tenant, rotating over the mix's tenants (the whole K+W run stays
+    within a few minutes).  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
-    ts = make_workload()
-    steps = max(1, args.steps)
-    warm = 0
-    tot_img, tot_s = 0, 0.0
-    for i in range(warm + steps):
-        v, cores, desc, secs = cpu_oracle_sample(ts, budget_s=30.0)
-        if i >= warm:
-            tot_img += v * secs
-            tot_s += secs
-    value = tot_img / tot_s
+    from oracle import forward_graph
+    from oracle import ops as oops
+    oops.build()
+    ts = make_workload(args.config)
+    for i in range(args.warmup):
+        _, g, p, B, dt, x = ts[i % len(ts)]
+        if g.name == "mobilenet_v2":
+            forward_graph(g, p, x[:1])
+    tot_s, n_img = 0.0, 0
+    for i in range(args.steps):
+        _, g, p, B, dt, x = ts[i % len(ts)]
+        t0 = time.perf_counter()
+        forward_graph(g, p, x[:1])
+        tot_s += time.perf_counter() - t0
+        n_img += 1
+    value = n_img / tot_s
+    desc = (f"{args.steps} steps x 1 image, tenants of {args.config} in rotation "
+            f"(fp64 oracle, OpenMP)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, random-init weights)",
-        "config": {"workload": CONFIG, "sample": "one image per tenant per step"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "config": {"workload": args.config, "sample": "one image per step, tenants in rotation"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oops.num_threads(), "kind": "oracle",
+                         "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -174,11 +216,12 @@ def time_mode(G, s, torch, stream, mode, steps, warmup, flush):
 def run_gacer(args, rank, world, dist):
     import torch
     from paper_2304_11745_b200 import gacer as G
+    from paper_2304_11745_b200.placement import max_over_ranks
     from paper_2304_11745_b200.runtime import Session
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    ts = make_workload()
+    ts = make_workload(args.config, rank)
     sess = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], device=dev)
     for t, (*_, x) in enumerate(ts):
         sess.set_input(t, x)
@@ -186,9 +229,22 @@ def run_gacer(args, rank, world, dist):
     stream = torch.cuda.Stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
     torch.cuda.set_stream(stream)
-
     st = G.gacer_get_stats()
-    # ---- main arm: GACER executor, identity plan
+
+    # ---- regulation plan: identity, or the best of a short sweep (each rank
+    #      picks on its own measurements; the result is identical math)
+    plans = sweep_plans(ts) if args.plan == "sweep" else [("identity", None, None, None)]
+    plan_ms = {}
+    for name, dec, ptr, sh in plans:
+        sess.set_regulation(dec, ptr)
+        G.gacer_set_sm_shares(sh)
+        plan_ms[name] = float(np.median(time_mode(G, sess, torch, stream, "executor", 5, 2, flush)))
+    best = min(plan_ms, key=plan_ms.get)
+    name, dec, ptr, sh = next(pl for pl in plans if pl[0] == best)
+    sess.set_regulation(dec, ptr)
+    G.gacer_set_sm_shares(sh)
+
+    # ---- main arm: the GACER executor under the chosen plan
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -197,11 +253,7 @@ def run_gacer(args, rank, world, dist):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    total_ms = float(np.sum(times))
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(float(np.sum(times)), dist, f"cuda:{dev}")
     ms_step = total_ms / args.steps
     value = world * n_inf * args.steps / (total_ms / 1000.0)
     launches_per_round = G.gacer_get_stats()["kernel_launches"]
@@ -210,12 +262,13 @@ def run_gacer(args, rank, world, dist):
     base = {}
     for mode in ("sequential", "multistream"):
         tm = time_mode(G, sess, torch, stream, mode, args.steps, args.warmup, flush)
-        m = float(np.mean(tm))
-        base[mode] = {"ms_per_round": m, "inferences_per_s": n_inf / (m / 1000.0),
+        m = max_over_ranks(float(np.mean(tm)), dist, f"cuda:{dev}")
+        base[mode] = {"ms_per_round": m, "inferences_per_s": world * n_inf / (m / 1000.0),
                       "kernel_launches_per_round": G.gacer_get_stats()["kernel_launches"]}
     sess.set_mode("executor")
 
-    # ---- e2e: through the public C ABI with HOST buffers (H2D + D2H inside)
+    # ---- e2e: through the public C ABI with HOST buffers (H2D + D2H inside
+    #      the timed region, CUDA events on the library stream)
     host_in = [sess.host_input(t, x) for t, (*_, x) in enumerate(ts)]
     host_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in sess.outputs]
     for _ in range(args.warmup):
@@ -226,11 +279,7 @@ def run_gacer(args, rank, world, dist):
         torch.cuda.synchronize()
         G.gacer_run_round_host([h.data_ptr() for h in host_in], [h.data_ptr() for h in host_out])
         e2e_ms.append(G.gacer_get_stats()["last_round_ms"])
-    e2e_total = float(np.sum(e2e_ms))
-    if dist:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
+    e2e_total = max_over_ranks(float(np.sum(e2e_ms)), dist, f"cuda:{dev}")
     h2d = int(sum(i["in_bytes"] for i in sess.info))
     d2h = int(sum(i["out_bytes"] for i in sess.info))
 
@@ -242,15 +291,15 @@ def run_gacer(args, rank, world, dist):
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get(CONFIG)
+                traffic = json.load(f).get(args.config)
         except Exception:
             pass
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded inputs, random-init weights)",
-            "config": {"workload": CONFIG, "tenants": [f"{n}(B={B})" for n, _, _, B, _, _ in ts],
-                       "image": 224, "plan": "identity", "mode": "executor",
+            "config": {"workload": args.config, "tenants": [f"{n}(B={B})" for n, _, _, B, _, _ in ts],
+                       "image": 224, "plan": best, "mode": "executor",
                        "parallelism": f"replica-per-gpu x{world}",
                        "l2": "flushed between steps (256 MB write, outside the events)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -262,6 +311,7 @@ def run_gacer(args, rank, world, dist):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_round * args.steps,
             "clocks": clk.summary(),
+            "plans_ms": plan_ms,
             "baselines": base,
             "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
             "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,
@@ -283,6 +333,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gacer", choices=["gacer", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default=CONFIG, choices=["d2_r50_v16_mv2", "d3_five"])
+    ap.add_argument("--plan", default="sweep", choices=["identity", "sweep"])
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
