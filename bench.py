@@ -137,7 +137,21 @@ def sweep_plans(ts):
         half = [B // 2, B - B // 2]
         dec = [(t, i + 1, "batch", half) for i, op in enumerate(g.ops) if op["kind"] == "conv"]
         plans.append(("vgg_conv_batch_split", dec, None, None))
-        plans.append(("vgg_conv_batch_split+pointers2", dec, [cuts(n, 2) for n in nops], None))
+
+    # Eq. 5 on every decomposable op of every tenant: consecutive layers then
+    # pipeline chunk by chunk through the chunk-granular dependencies
+    def all_batch(nchunks):
+        dec = []
+        for t, (_, g, _, B, _, _) in enumerate(ts):
+            k = min(nchunks, B)
+            sizes = [B // k + (1 if j < B % k else 0) for j in range(k)]
+            for i, op in enumerate(g.ops):
+                if op["kind"] in ("conv", "linear", "maxpool", "avgpool", "gap", "add", "relu", "relu6", "bn"):
+                    dec.append((t, i + 1, "batch", sizes))
+        return dec
+    for k in (2, 4, 8):
+        plans.append((f"all_ops_batch_split{k}", all_batch(k), None, None))
+    plans.append(("all_ops_batch_split4+pointers2", all_batch(4), [cuts(n, 2) for n in nops], None))
     return plans
 
 

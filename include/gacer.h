@@ -147,7 +147,10 @@ typedef enum {
 
 typedef enum {
   GACER_PARTITION_WORK_CONSERVING = 0, /* each CTA prefers one tenant, steals from the others */
-  GACER_PARTITION_STRICT = 1           /* each CTA serves only its tenant (SM share per tenant) */
+  GACER_PARTITION_STRICT = 1,          /* each CTA serves only its tenant (SM share per tenant) */
+  GACER_PARTITION_HYBRID = 2           /* like WORK_CONSERVING, except that CTAs of the other tenants
+                                          never take the bulk tenant's (largest share) items: its long
+                                          tiles cannot delay the latency-bound chains */
 } gacer_partition;
 
 typedef struct {
@@ -244,9 +247,10 @@ int gacer_run_round_host(const void* const* host_inputs, void* const* host_outpu
 int gacer_get_stats(gacer_round_stats* out);
 
 /* Trace of the last executor round (options.trace = 1): up to `cap` records
- * of 8 int64 each, indexed by work item: tenant, global fused-op index, SM id,
- * item index, cluster, chunk counter, t_start_ns, t_end_ns (%globaltimer).
- * Returns the number of records written. */
+ * of 10 int64 each, indexed by work item: tenant, global fused-op index, SM
+ * id, item index, cluster, chunk counter, t_claim_ns, t_release_ns,
+ * t_mma_start_ns, t_epilogue_start_ns (%globaltimer; the last two are 0 for
+ * CUDA-core items).  Returns the number of records written. */
 int gacer_get_trace(int64_t* records, int32_t cap);
 
 const char* gacer_last_error(void);

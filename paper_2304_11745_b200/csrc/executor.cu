@@ -105,6 +105,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld of 16 columns without waiting (batch several, then tmem_wait)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
 // UMMA shared-memory descriptor, K-major, SWIZZLE_128B canonical layout:
 // 8-row x 128-byte atoms (row r, 16B chunk j stored at chunk j ^ (r & 7)),
 // atoms stacked every 1024 bytes (SBO).  Bits: [0,14) start>>4, [16,30)
@@ -131,10 +141,11 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__shared__ uint32_t g_dbg_seen;   // per-CTA: milestones already recorded (no global load per probe)
 __device__ __forceinline__ void dbg_mark(const ExecParams& p, int ev) {
-  if (p.dbg) {
-    int64_t* d = p.dbg + static_cast<size_t>(blockIdx.x) * DBG_EVENTS + ev;
-    if (*d == 0) *d = static_cast<int64_t>(globaltimer());   // first occurrence only
+  if (p.dbg && !(g_dbg_seen & (1u << ev))) {   // first occurrence only
+    atomicOr(&g_dbg_seen, 1u << ev);
+    p.dbg[static_cast<size_t>(blockIdx.x) * DBG_EVENTS + ev] = static_cast<int64_t>(globaltimer());
   }
 }
 
@@ -200,6 +211,14 @@ __device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* tma
       "l"(tmap), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(tmap),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -242,6 +261,9 @@ struct SmemCtl {
   uint64_t rfull[ITEM_RING];
   uint64_t rempty[ITEM_RING];
   RingSlot ring[ITEM_RING];
+  uint64_t lfull[ITEM_RING];   // epilogue -> releaser (completed GEMM items)
+  uint64_t lempty[ITEM_RING];
+  RingSlot rel[ITEM_RING];
   uint32_t tmem_base;
   int32_t epi_flag;
   int32_t n_segs_smem;
@@ -251,10 +273,13 @@ struct SmemCtl {
   float epi_bias[BN_MAX];
   Seg segs[MAX_SMEM_SEGS];   // (tenant, cluster) queue segments, cached
 };
-constexpr int SMEM_BYTES = SMEM_RING_BYTES + 1024 /*align slack*/ + (int)sizeof(SmemCtl);
+constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 rows x 128 B per warp (SW128)
+constexpr int SMEM_STAGE_BYTES = (NEPI / 32) * STAGE_WARP_BYTES;
+constexpr int SMEM_BYTES = SMEM_RING_BYTES + SMEM_STAGE_BYTES + 1024 /*align slack*/ + (int)sizeof(SmemCtl);
 
 struct Ctx {
   uint8_t* ring;             // 1024-aligned stage buffers
+  uint8_t* stage;            // 1024-aligned epilogue staging (SWIZZLE_128B rows)
   SmemCtl* ctl;
   uint32_t tmem;
 };
@@ -269,14 +294,55 @@ struct EpiOp {
   void* out;
   const float* scale;
   const float* bias;
-  int32_t M, Cout, B, ldo, act, out_f32, has_skip, swap;
+  const void* tmap_c;
+  int32_t M, Cout, B, ldo, act, out_f32, has_skip, swap, c_tma;
 };
 __device__ __forceinline__ EpiOp make_epi(const OpDev& op) {
   EpiOp e;
-  e.out = op.out; e.scale = op.scale; e.bias = op.bias;
+  e.out = op.out; e.scale = op.scale; e.bias = op.bias; e.tmap_c = op.tmap_c;
   e.M = op.M; e.Cout = op.Cout; e.B = op.B; e.ldo = op.ldo; e.act = op.act;
-  e.out_f32 = op.out_f32; e.has_skip = op.has_skip; e.swap = op.swap;
+  e.out_f32 = op.out_f32; e.has_skip = op.has_skip; e.swap = op.swap; e.c_tma = op.c_tma;
   return e;
+}
+
+// y = act(v*scale + bias [+ skip]) for 8 columns (no store)
+__device__ __forceinline__ void epi_math8(const EpiOp& op, const float* v, const float* sc, const float* bi,
+                                          const uint4& skip8, float* y) {
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {   // packed FFMA2: two IEEE fmas, same results as fmaf
+    const float2 r = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc[j], sc[j + 1]),
+                                make_float2(bi[j], bi[j + 1]));
+    y[j] = r.x;
+    y[j + 1] = r.y;
+  }
+  if (op.has_skip) {
+    float s[8];
+    bf16x8_to_f32(skip8, s);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] += s[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) y[j] = apply_act(y[j], op.act);
+}
+
+// Write 8 results of `row` at column offset `col` (within the staged chunk)
+// into the warp's 32x128B staging block with the 128-byte swizzle (16-byte
+// chunk j of row r at j ^ (r & 7)), the layout the TMA store reads.
+__device__ __forceinline__ void stage8(uint8_t* wbuf, int row, int col, const float* y, bool f32) {
+  const int sw = row & 7;
+  if (f32) {
+    const int j0 = (col * 4) >> 4;
+    *reinterpret_cast<float4*>(wbuf + row * 128 + ((j0 ^ sw) << 4)) = make_float4(y[0], y[1], y[2], y[3]);
+    *reinterpret_cast<float4*>(wbuf + row * 128 + (((j0 + 1) ^ sw) << 4)) = make_float4(y[4], y[5], y[6], y[7]);
+  } else {
+    const int j = (col * 2) >> 4;
+    uint4 u;
+    u.x = pack_bf16x2(y[0], y[1]);
+    u.y = pack_bf16x2(y[2], y[3]);
+    u.z = pack_bf16x2(y[4], y[5]);
+    u.w = pack_bf16x2(y[6], y[7]);
+    *reinterpret_cast<uint4*>(wbuf + row * 128 + ((j ^ sw) << 4)) = u;
+  }
 }
 
 // m: GEMM row; n: first of 8 GEMM columns; sc/bi: the 8 columns' scale/bias
@@ -685,7 +751,7 @@ __device__ void window2_bf16(const OpDev& op, int m0, int m1, int c, int HoWo) {
 // item's depthwise weights and folded scale/bias are staged in shared memory
 // (wsm) once.  Per output the taps are reduced in the same fixed (r, s)
 // order, each with an IEEE fma, as cc_pixel: results are bit-identical.
-constexpr int RUN = 4;
+constexpr int RUN = CC_RUN;
 template <int KH, int KW, int S>
 __device__ void window_run_bf16(const OpDev& op, const Item& it, int tid, int G, float* wsm) {
   const int g = tid % G;
@@ -988,10 +1054,12 @@ __device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& b
 __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, uint64_t t0, const OpDev& op) {
   // caller: all writes of the item are ordered before this thread (barrier)
   __threadfence();
+  dbg_mark(p, 8);
   atomicAdd(p.chunk_done + it.chunk, 1u);
   atomicAdd(p.cluster_done + it.cluster, 1u);
+  dbg_mark(p, 9);
   if (p.trace) {
-    int64_t* rec = p.trace + static_cast<size_t>(it.idx) * 8;
+    int64_t* rec = p.trace + static_cast<size_t>(it.idx) * 10;
     rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = it.idx;
     rec[4] = it.cluster; rec[5] = it.chunk;
     rec[6] = static_cast<int64_t>(t0); rec[7] = static_cast<int64_t>(globaltimer());
@@ -1052,6 +1120,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
           // every item of cluster k is claimed: the synchronisation pointer --
           // wait until every item of cluster k (all tenants) is done.
           if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) { claimed = -3; break; }
+          dbg_mark(p, 10);
           ++k;
           spins = 0;
           continue;
@@ -1069,7 +1138,10 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
           }
           continue;
         }
-        const uint32_t allowed = (cand.op == last_op && cand.op_left > big) ? LOOKAHEAD : 1;
+        const int G1 = static_cast<int>(gridDim.x);
+        const uint32_t allowed =
+            (cand.op != last_op) ? 1u : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
+                                                            : (cand.op_left > G1 ? 2u : 1u));
         while (islot - consumed >= allowed) {
           mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
           ++consumed;
@@ -1123,6 +1195,8 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
       if (wtid == 0) dbg_mark(p, 3);
       named_bar_sync(1, NWORK);
     } else {
+      if (wtid == 0 && p.trace && p.single_op < 0)
+        p.trace[static_cast<size_t>(rs.it.idx) * 10 + 8] = static_cast<int64_t>(globaltimer());
       run_cc(op, rs.it, wtid, ctl->red);
       named_bar_sync(1, NWORK);
       if (wtid == 0 && p.single_op < 0) release_item(p, rs.it, rs.t0, op);
@@ -1153,10 +1227,15 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     tc_fence_after();
     const uint32_t d = cx.tmem + abuf * BN_MAX;
     const uint32_t idesc = make_idesc(op.bn);
+    bool stamped = false;
     for (int i = 0; i < nk; ++i) {
       const uint32_t stage = g % STAGES;
       mbar_wait(&ctl->full[stage], (g / STAGES) & 1);
       if (i == 0) dbg_mark(p, 4);
+      if (p.trace && !stamped && p.single_op < 0) {
+        p.trace[static_cast<size_t>(it.idx) * 10 + 8] = static_cast<int64_t>(globaltimer());
+        stamped = true;
+      }
       tc_fence_after();
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
@@ -1173,11 +1252,20 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
   }
 }
 
+// Epilogue: 8 warps; warp e reads TMEM lane quarter e % 4 (tile rows
+// 32*(e%4)..) and the column half e / 4 (when bn is a multiple of 32, else
+// the first four warps take every column).  Per 32 columns: two tcgen05.ld
+// x16 behind one wait, fused scale/bias(/residual)/act with FFMA2, a
+// 64-byte-swizzled 32x64B smem chunk, and a TMA tensor store of that chunk
+// (coalesced; rows >= M and columns >= Cout clipped by the tensor map).
 __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = cx.ctl;
-  const int etid = threadIdx.x - EPI_WARP0 * 32;  // 0..127
-  const int ew = etid >> 5, lane = etid & 31;     // warp 4+ew accesses TMEM lanes 32*ew..
-  uint32_t islot = 0, acc = 0;
+  const int etid = threadIdx.x - EPI_WARP0 * 32;  // 0..NEPI-1
+  const int ew = etid >> 5, lane = etid & 31;
+  const int q = ew & 3, hcol = ew >> 2;
+  uint8_t* wbuf = cx.stage + ew * STAGE_WARP_BYTES;
+  const uint32_t wbuf_s = smem_u32(wbuf);
+  uint32_t islot = 0, acc = 0, nrel = 0;
   for (;;) {
     const uint32_t slot = islot % ITEM_RING;
     mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
@@ -1193,18 +1281,20 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     const OpDev& opg = p.ops[it.op];
     const EpiOp op = make_epi(opg);
     const int bn = opg.bn;
-    const int row = ew * 32 + lane;
-    const int m0 = it.mt * BM, n0 = it.nt * bn;
-    const int m = m0 + row;
     const int split = opg.split_k;
     const bool swap = op.swap;
-    const int tiles_n = opg.tiles_n;
-    const __nv_bfloat16* skip_base = static_cast<const __nv_bfloat16*>(opg.skip);
-    const int lds = opg.lds;
-    float* const partial_base = opg.partial;
-    uint32_t* const tile_cnt = opg.tile_cnt;
-    // ---- global reads the epilogue needs are issued before the accumulator
-    //      is waited on (hides their latency behind the MMA)
+    const int row = q * 32 + lane;
+    const int m0 = it.mt * BM, n0 = it.nt * bn;
+    const int m = m0 + row;
+    const int tile = it.mt * opg.tiles_n + it.nt;
+    const int cout_left = op.Cout - n0;
+    // this warp's tile columns: halves split at a multiple of 32, so a staged
+    // 32-column box never reaches into the other warp's columns (boxes past
+    // bn only cover columns >= Cout, which the tensor map clips)
+    const int c_split = (NEPI / 128 > 1) ? 32 * ((bn + 63) / 64) : bn;
+    const int c_lo = hcol ? (c_split < bn ? c_split : bn) : 0;
+    const int c_hi = hcol ? bn : (c_split < bn ? c_split : bn);
+    // ---- global reads issued before the accumulator is waited on
     float sc_row = 1.0f, bi_row = 0.0f;
     if (swap) {
       if (m < op.Cout) { sc_row = op.scale[m]; bi_row = op.bias[m]; }
@@ -1214,61 +1304,101 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
         ctl->epi_bias[j] = op.bias[n0 + j];
       }
     }
-    const bool do_skip = op.has_skip && split == 1 && m < op.M;
-    const __nv_bfloat16* skrow = do_skip ? skip_base + static_cast<size_t>(m) * lds + n0 : nullptr;
-    const int cout_left = op.Cout - n0;
+    const bool do_skip = op.has_skip && split == 1 && m < op.M && !swap;
+    const __nv_bfloat16* skrow =
+        do_skip ? static_cast<const __nv_bfloat16*>(opg.skip) + static_cast<size_t>(m) * opg.lds + n0 : nullptr;
     uint4 skA[4], skB[4];  // residual values of the current / next 32 columns
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      skA[q] = (do_skip && q * 8 < bn && q * 8 < cout_left) ? *reinterpret_cast<const uint4*>(skrow + q * 8)
-                                                             : make_uint4(0, 0, 0, 0);
+    for (int u = 0; u < 4; ++u) {
+      const int cc = c_lo + u * 8;
+      skA[u] = (do_skip && cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc)
+                                                       : make_uint4(0, 0, 0, 0);
+    }
     named_bar_sync(2, NEPI);  // epi_scale / epi_bias visible
+    if (etid == 0) dbg_mark(p, 12);
     const uint32_t abuf = acc & 1;
     mbar_wait(&ctl->tfull[abuf], (acc / 2) & 1);
     if (etid == 0) dbg_mark(p, 6);
+    if (etid == 0 && p.trace && p.single_op < 0)
+      p.trace[static_cast<size_t>(it.idx) * 10 + 9] = static_cast<int64_t>(globaltimer());
     tc_fence_after();
-    const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(ew * 32) << 16);
-    float* part = nullptr;
-    const int tile = it.mt * tiles_n + it.nt;
+    const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(q * 32) << 16);
+    float* part = opg.partial + static_cast<size_t>(tile) * split * (BM * bn);
+    const bool staged = op.c_tma && !swap;
+    const int CW = op.out_f32 ? 32 : 64;          // columns per 128-byte staged row
     if (split == 1) {
-      for (int c = 0; c < bn; c += 32) {
+      for (int c = c_lo; c < c_hi; c += 32) {
+        uint32_t r[32];
+        tmem_ld16_nw(taddr + c, r);
+        if (c + 16 < c_hi) tmem_ld16_nw(taddr + c + 16, r + 16);
+        tmem_wait();
+        if (etid == 0) dbg_mark(p, 16);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int cc = c + 32 + q * 8;
-          skB[q] = (do_skip && cc < bn && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc)
-                                                         : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) {
+          const int cc = c + 32 + u * 8;
+          skB[u] = (do_skip && cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc)
+                                                           : make_uint4(0, 0, 0, 0);
         }
+        const float* v = reinterpret_cast<const float*>(r);
+        if (swap) {
 #pragma unroll
-        for (int h = 0; h < 32; h += 16) {
-          if (c + h < bn) {
-            float v[16];
-            tmem_ld16(taddr + c + h, v);
-            if (swap) {
-              epilogue_store8_swap(op, m, n0 + c + h, v, sc_row, bi_row);
-              epilogue_store8_swap(op, m, n0 + c + h + 8, v + 8, sc_row, bi_row);
-            } else {
-              epilogue_store8(op, m, n0 + c + h, v, ctl->epi_scale + c + h, ctl->epi_bias + c + h, skA[h / 8]);
-              epilogue_store8(op, m, n0 + c + h + 8, v + 8, ctl->epi_scale + c + h + 8, ctl->epi_bias + c + h + 8,
-                              skA[h / 8 + 1]);
+          for (int u = 0; u < 32; u += 8)
+            if (c + u < c_hi) epilogue_store8_swap(op, m, n0 + c + u, v + u, sc_row, bi_row);
+        } else if (staged) {
+          const int cin = (c - c_lo) % CW;       // column offset inside the staged chunk
+          if (cin == 0 && c > c_lo) {            // a new chunk: wait until the last store read the buffer
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int sub = 0; sub < 32; sub += 16) {
+            if (c + sub < c_hi) {
+              float y[8];
+              epi_math8(op, v + sub, ctl->epi_scale + c + sub, ctl->epi_bias + c + sub, skA[sub / 8], y);
+              stage8(wbuf, lane, cin + sub, y, op.out_f32);
+              epi_math8(op, v + sub + 8, ctl->epi_scale + c + sub + 8, ctl->epi_bias + c + sub + 8, skA[sub / 8 + 1], y);
+              stage8(wbuf, lane, cin + sub + 8, y, op.out_f32);
             }
           }
+          if (cin + 32 == CW || c + 32 >= c_hi) {  // chunk complete: TMA-store it
+            if (etid == 0) dbg_mark(p, 17);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(op.tmap_c, wbuf_s, n0 + c - cin, m0 + q * 32);
+              bulk_commit();
+            }
+            if (etid == 0) dbg_mark(p, 18);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 32; u += 8)
+            if (c + u < c_hi) epilogue_store8(op, m, n0 + c + u, v + u, ctl->epi_scale + c + u, ctl->epi_bias + c + u, skA[u / 8]);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) skA[q] = skB[q];
+        for (int u = 0; u < 4; ++u) skA[u] = skB[u];
+      }
+      if (staged) {
+        if (etid == 0) dbg_mark(p, 14);
+        if (lane == 0) bulk_wait0();        // stores complete before the item is released
+        __syncwarp();
       }
     } else {
       // partial layout [tile][ks][bn/4][BM] float4: a warp's 32 rows of one
       // float4 column are 512 contiguous bytes (coalesced write and read)
-      part = partial_base + static_cast<size_t>(tile) * split * (BM * bn);
       float4* mine = reinterpret_cast<float4*>(part + static_cast<size_t>(it.ks) * (BM * bn)) + row;
-      for (int c = 0; c < bn; c += 16) {
-        float v[16];
-        tmem_ld16(taddr + c, v);
+      for (int c = c_lo; c < c_hi; c += 32) {
+        uint32_t r[32];
+        tmem_ld16_nw(taddr + c, r);
+        if (c + 16 < c_hi) tmem_ld16_nw(taddr + c + 16, r + 16);
+        tmem_wait();
+        const float* v = reinterpret_cast<const float*>(r);
 #pragma unroll
-        for (int q = 0; q < 16; q += 4)
-          __stcg(mine + ((c + q) >> 2) * BM, make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+        for (int u = 0; u < 32; u += 4)
+          if (c + u < c_hi) __stcg(mine + ((c + u) >> 2) * BM, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]));
       }
     }
+    if (etid == 0) dbg_mark(p, 13);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->tempty[abuf]);
@@ -1277,24 +1407,35 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       named_bar_sync(2, NEPI);
       if (etid == 0) {
         __threadfence();
-        const uint32_t old = atomicAdd(tile_cnt + tile, 1u);
+        const uint32_t old = atomicAdd(opg.tile_cnt + tile, 1u);
         const int last = (old == static_cast<uint32_t>(split - 1));
-        if (last) tile_cnt[tile] = 0;  // all arrivals done: re-arm for the next round
+        if (last) opg.tile_cnt[tile] = 0;  // all arrivals done: re-arm for the next round
         ctl->epi_flag = last;
         __threadfence();
       }
       named_bar_sync(2, NEPI);
       if (ctl->epi_flag) {
-        // fixed ks order (bit-identical in every mode); all partial loads of an
-        // 8-column chunk are in flight together
-        for (int c = 0; c < bn; c += 8) {
+        // fixed ks order (bit-identical in every mode); the partial loads of
+        // an 8-column chunk are in flight together
+        const __nv_bfloat16* skb = static_cast<const __nv_bfloat16*>(opg.skip);
+        for (int c = c_lo; c < c_hi; c += 8) {
+          if (staged && c > c_lo && ((c - c_lo) % CW) == 0) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(op.tmap_c, wbuf_s, n0 + c - CW, m0 + q * 32);
+              bulk_commit();
+              bulk_wait_read0();
+            }
+            __syncwarp();
+          }
           float4 ld[MAX_SPLIT][2];
 #pragma unroll
           for (int ks = 0; ks < MAX_SPLIT; ++ks)
             if (ks < split) {
-              const float4* q = reinterpret_cast<const float4*>(part + static_cast<size_t>(ks) * (BM * bn)) + row;
-              ld[ks][0] = __ldcg(q + (c >> 2) * BM);
-              ld[ks][1] = __ldcg(q + ((c >> 2) + 1) * BM);
+              const float4* qp = reinterpret_cast<const float4*>(part + static_cast<size_t>(ks) * (BM * bn)) + row;
+              ld[ks][0] = __ldcg(qp + (c >> 2) * BM);
+              ld[ks][1] = __ldcg(qp + ((c >> 2) + 1) * BM);
             }
           float s8[8] = {ld[0][0].x, ld[0][0].y, ld[0][0].z, ld[0][0].w, ld[0][1].x, ld[0][1].y, ld[0][1].z, ld[0][1].w};
 #pragma unroll
@@ -1308,16 +1449,68 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
           } else {
             uint4 k8 = make_uint4(0, 0, 0, 0);
             if (op.has_skip && m < op.M && c < cout_left)
-              k8 = *reinterpret_cast<const uint4*>(skip_base + static_cast<size_t>(m) * lds + n0 + c);
-            epilogue_store8(op, m, n0 + c, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8);
+              k8 = *reinterpret_cast<const uint4*>(skb + static_cast<size_t>(m) * opg.lds + n0 + c);
+            if (staged) {
+              float y[8];
+              epi_math8(op, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8, y);
+              stage8(wbuf, lane, (c - c_lo) % CW, y, op.out_f32);
+            } else {
+              epilogue_store8(op, m, n0 + c, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8);
+            }
           }
+        }
+        if (staged && c_hi > c_lo) {
+          const int last = c_lo + ((c_hi - c_lo - 1) / CW) * CW;
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(op.tmap_c, wbuf_s, n0 + last, m0 + q * 32);
+            bulk_commit();
+            bulk_wait0();
+          }
+          __syncwarp();
         }
       }
     }
     fence_proxy_async_global();  // generic stores -> later TMA reads by consumers
+    if (etid == 0) dbg_mark(p, 15);
     named_bar_sync(2, NEPI);     // also: epi_scale/bias free for the next item
     if (etid == 0) dbg_mark(p, 7);
-    if (etid == 0 && p.single_op < 0) release_item(p, it, t0, opg);
+    if (etid == 0 && p.single_op < 0) {   // hand the release to the releaser lane
+      const uint32_t ls = nrel % ITEM_RING;
+      if (nrel >= ITEM_RING) mbar_wait(&ctl->lempty[ls], ((nrel / ITEM_RING) + 1) & 1);
+      ctl->rel[ls].it = it;
+      ctl->rel[ls].t0 = t0;
+      ctl->rel[ls].idx = idx;
+      mbar_arrive(&ctl->lfull[ls]);
+      ++nrel;
+    }
+  }
+  if (etid == 0 && p.single_op < 0) {     // STOP for the releaser
+    const uint32_t ls = nrel % ITEM_RING;
+    if (nrel >= ITEM_RING) mbar_wait(&ctl->lempty[ls], ((nrel / ITEM_RING) + 1) & 1);
+    ctl->rel[ls].idx = -1;
+    mbar_arrive(&ctl->lfull[ls]);
+  }
+}
+
+// Releaser (warp 1, lane 1): publishes completed GEMM items -- fence, then
+// the chunk and cluster counters -- off the epilogue warps' critical path.
+// Ordering: the epilogue's stores (TMA stores waited to completion, generic
+// stores) precede its named barrier and mbarrier arrive (release.cta); this
+// lane's wait is an acquire, and __threadfence() makes the chain cumulative
+// at GPU scope before the counter atomics.
+__device__ void releaser_role(const ExecParams& p, Ctx& cx) {
+  SmemCtl* ctl = cx.ctl;
+  uint32_t n = 0;
+  for (;;) {
+    const uint32_t ls = n % ITEM_RING;
+    mbar_wait(&ctl->lfull[ls], (n / ITEM_RING) & 1);
+    const RingSlot r = ctl->rel[ls];
+    mbar_arrive(&ctl->lempty[ls]);
+    ++n;
+    if (r.idx < 0) break;
+    release_item(p, r.it, r.t0, p.ops[r.it.op]);
   }
 }
 
@@ -1325,13 +1518,16 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Ctx cx;
   cx.ring = base;
-  cx.ctl = reinterpret_cast<SmemCtl*>(base + SMEM_RING_BYTES);
+  cx.stage = base + SMEM_RING_BYTES;
+  cx.ctl = reinterpret_cast<SmemCtl*>(base + SMEM_RING_BYTES + SMEM_STAGE_BYTES);
   SmemCtl* ctl = cx.ctl;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) {
+    g_dbg_seen = 0;
     for (int s = 0; s < STAGES; ++s) { mbar_init(&ctl->full[s], 1); mbar_init(&ctl->empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&ctl->tfull[a], 1); mbar_init(&ctl->tempty[a], NEPI / 32); }
     for (int r = 0; r < ITEM_RING; ++r) { mbar_init(&ctl->rfull[r], 1); mbar_init(&ctl->rempty[r], RING_CONSUMERS); }
+    for (int r = 0; r < ITEM_RING; ++r) { mbar_init(&ctl->lfull[r], 1); mbar_init(&ctl->lempty[r], 1); }
     fence_mbar_init();
   }
   if (p.single_op < 0) {  // cache the queue segments
@@ -1353,6 +1549,7 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
     if (tid == 0) scheduler_role(p, cx);
   } else if (warp == MMA_WARP) {
     if ((tid & 31) == 0) mma_role(p, cx);
+    else if ((tid & 31) == 1 && p.single_op < 0) releaser_role(p, cx);
   } else if (warp < EPI_WARP0) {
     worker_role(p, cx);
   } else {

@@ -29,12 +29,13 @@ constexpr int ITEM_RING = 4;      // scheduler -> MMA/epilogue item queue depth
 // warp roles of the executor CTA (16 warps; 4 per SM sub-partition, <= 128 registers)
 constexpr int SCHED_WARP = 0;     // warp 0: scheduler (lane 0) -- claims ready items into the item ring
 constexpr int MMA_WARP = 1;       // warp 1: single-thread tcgen05.mma issue
-constexpr int WORK_WARP0 = 2;     // warps 2-11: TMA / gather loads of GEMM items, CUDA-core items
-constexpr int NWORK = 320;
-constexpr int EPI_WARP0 = 12;     // warps 12-15: TMEM -> register epilogue (lane quarter = warp % 4)
-constexpr int NEPI = 128;
-constexpr int NTHREADS = 512;
+constexpr int WORK_WARP0 = 2;     // warps 2-7: TMA / gather loads of GEMM items, CUDA-core items
+constexpr int NWORK = 192;
+constexpr int EPI_WARP0 = 8;      // warps 8-11: TMEM -> register epilogue; warp w reads TMEM lane
+constexpr int NEPI = 128;         //   quarter w % 4 (NEPI = 256 would also split the columns in halves)
+constexpr int NTHREADS = 384;
 constexpr int CC_THREADS = NWORK; // threads that execute a CUDA-core item
+constexpr int CC_RUN = 8;         // consecutive output pixels per thread in the row-run window kernel
 constexpr int CC_TASKS_PER_THREAD = 4;
 constexpr int MAX_SPLIT = 4;      // split-K factor cap (fixed per layer shape)
 constexpr int LOOKAHEAD = 3;      // max claimed items not yet picked up by every role (per CTA)
@@ -84,7 +85,8 @@ struct OpDev {
   const void* tmap_a;      // CUtensorMap (64 B aligned, device memory): im2col or tiled A
   const void* tmap_b;      // CUtensorMap: tiled B (weights, or activations for swap-AB)
   int32_t a_mode;          // AMode
-  int32_t pad4;
+  int32_t c_tma;           // 1: epilogue stores through smem staging + TMA tensor store (tmap_c)
+  const void* tmap_c;      // CUtensorMap of the output [M rows][Cout] (row stride ldo)
 };
 
 // One work item: one output tile (mt, nt) of one op, K-slice ks.  Items are
@@ -133,6 +135,6 @@ struct ExecParams {
   int32_t pad;
   int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
 };
-constexpr int DBG_EVENTS = 16;
+constexpr int DBG_EVENTS = 24;
 
 }  // namespace gacer

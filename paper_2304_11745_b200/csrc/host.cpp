@@ -647,7 +647,9 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         // split-K: a function of the layer shape only (same in every mode/plan)
         const int tiles = F.tiles_m * F.tiles_n;
         int sk = 1;
-        while (sk < MAX_SPLIT && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 4) sk *= 2;
+        // (each split keeps >= 8 K-blocks: below that the fixed-order
+        //  reduction of the partials costs more than the MMA it parallelises)
+        while (sk < MAX_SPLIT && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 8) sk *= 2;
         F.split_k = sk;
         F.w_bf16.assign(rows * F.Kpad, 0);
         for (int co = 0; co < F.Cout; ++co)
@@ -686,7 +688,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
       const bool run = F.kind != DK_GAP && F.kind != DK_ELTWISE && !f32 &&
                        ((F.kh == 3 && F.kw == 3 && (F.stride == 1 || F.stride == 2)) ||
                         (F.kh == 2 && F.kw == 2 && F.stride == 2));
-      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : (run ? 4 /*RUN*/ : CC_TASKS_PER_THREAD) * (CC_THREADS / G);
+      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : (run ? CC_RUN : CC_TASKS_PER_THREAD) * (CC_THREADS / G);
       F.tiles_m = cdiv(F.M, F.bm);
       F.tiles_n = cdiv(F.Cout, F.bn);
       F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
@@ -851,33 +853,52 @@ int rebuild_op_table() {
   if (S.host_only) return 0;
   if (int rc = load_tma_encoders()) return rc;
   const size_t n = S.h_ops.size();
-  if (S.n_tmaps < 2 * n) {
+  if (S.n_tmaps < 3 * n) {
     if (S.d_tmaps) cudaFree(S.d_tmaps);
     S.d_tmaps = nullptr;
-    CUDA_TRY(cudaMalloc(&S.d_tmaps, 2 * n * sizeof(CUtensorMap)));  // cudaMalloc: 256-byte aligned
-    S.n_tmaps = 2 * n;
+    CUDA_TRY(cudaMalloc(&S.d_tmaps, 3 * n * sizeof(CUtensorMap)));  // cudaMalloc: 256-byte aligned
+    S.n_tmaps = 3 * n;
   }
-  std::vector<CUtensorMap> maps(2 * n);
+  std::vector<CUtensorMap> maps(3 * n);
   std::memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
   for (size_t i = 0; i < n; ++i) {
     OpDev& d = S.h_ops[i];
     if (d.kind != DK_GEMM) continue;
     const FusedOp& F = *fops[i];
     d.a_mode = F.a_mode;
-    d.tmap_a = S.d_tmaps + 2 * i;
-    d.tmap_b = S.d_tmaps + 2 * i + 1;
+    d.tmap_a = S.d_tmaps + 3 * i;
+    d.tmap_b = S.d_tmaps + 3 * i + 1;
+    d.tmap_c = S.d_tmaps + 3 * i + 2;
+    d.c_tma = 0;
     if (!d.in || !d.out) continue;  // I/O not bound yet: re-encoded by gacer_bind_io
     int rc = 0;
     if (d.swap) {
-      rc = encode_rows(&maps[2 * i], d.wt, d.Kpad, d.tiles_m * BM, d.Kpad, BM);
-      if (!rc) rc = encode_rows(&maps[2 * i + 1], d.act_b, d.K, d.B, d.ldb, d.bn);
+      rc = encode_rows(&maps[3 * i], d.wt, d.Kpad, d.tiles_m * BM, d.Kpad, BM);
+      if (!rc) rc = encode_rows(&maps[3 * i + 1], d.act_b, d.K, d.B, d.ldb, d.bn);
     } else {
-      if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[2 * i], d, F.Cin);
-      if (!rc) rc = encode_rows(&maps[2 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
+      if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[3 * i], d, F.Cin);
+      if (!rc) rc = encode_rows(&maps[3 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
+      // output [M][Cout] (row stride ldo) for the TMA-store epilogue
+      const int esz = d.out_f32 ? 4 : 2;
+      const bool ok = (static_cast<long long>(d.ldo) * esz) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
+      if (!rc && ok) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Cout), static_cast<cuuint64_t>(d.M)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ldo) * esz};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32u};  // 32 rows x 128 B
+        const cuuint32_t es[2] = {1, 1};
+        CUresult r = g_encode_tiled(&maps[3 * i + 2],
+                                    d.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                    d.out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "cuTensorMapEncodeTiled (output) failed (%d)", static_cast<int>(r));
+        d.c_tma = 1;
+      }
     }
     if (rc) return rc;
   }
-  CUDA_TRY(cudaMemcpy(S.d_tmaps, maps.data(), 2 * n * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(S.d_tmaps, maps.data(), 3 * n * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   return dev_upload(&S.d_ops, S.h_ops.data(), S.h_ops.size());
 }
 
@@ -1140,11 +1161,18 @@ std::vector<int32_t> make_pref(int grid) {
       for (int c = grid - 1; c >= 0; --c)
         if (own[c] == donor) { own[c] = t; got[t] += 1; got[donor] -= 1; break; }
     }
+  int bulk = 0;
+  for (int t = 1; t < nt; ++t) if (w[t] > w[bulk]) bulk = t;
   std::vector<int32_t> pref(static_cast<size_t>(grid) * nt, -1);
   for (int c = 0; c < grid; ++c) {
     pref[static_cast<size_t>(c) * nt] = own[c];
     if (S.opts.partition == GACER_PARTITION_STRICT) continue;
-    for (int j = 1; j < nt; ++j) pref[static_cast<size_t>(c) * nt + j] = (own[c] + j) % nt;
+    int j = 1;
+    for (int d = 1; d < nt; ++d) {
+      const int t = (own[c] + d) % nt;
+      if (S.opts.partition == GACER_PARTITION_HYBRID && own[c] != bulk && t == bulk) continue;
+      pref[static_cast<size_t>(c) * nt + j++] = t;
+    }
   }
   return pref;
 }
@@ -1167,7 +1195,10 @@ int upload_plan() {
   if (!S.d_exit && (rc = dev_upload<uint32_t>(&S.d_exit, nullptr, 1))) return rc;
   if (!S.d_error && (rc = dev_upload<int32_t>(&S.d_error, nullptr, 1))) return rc;
   if (S.d_trace) { cudaFree(S.d_trace); S.d_trace = nullptr; }
-  if (S.opts.trace) CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * 8 * sizeof(int64_t)));
+  if (S.opts.trace) {
+    CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * 10 * sizeof(int64_t)));
+    CUDA_TRY(cudaMemset(S.d_trace, 0, P.items.size() * 10 * sizeof(int64_t)));
+  }
   S.epoch = 0;
   return 0;
 }
@@ -1535,7 +1566,7 @@ int gacer_get_trace(int64_t* records, int32_t cap) {
   if (!S.inited || S.host_only || !S.d_trace) return set_err(GACER_E_STATE, "tracing not enabled");
   if (!records || cap < 0) return set_err(GACER_E_INVALID_ARG, "bad buffer");
   const size_t n = std::min<size_t>(cap, S.plan.items.size());
-  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * 10 * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return static_cast<int>(n);
 }
 

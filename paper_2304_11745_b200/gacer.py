@@ -17,7 +17,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgacer.so")
+# GACER_LIB selects an alternative build of the same library (A/B timing of
+# kernel variants on one box); default: the in-tree build.
+LIB_PATH = os.environ.get("GACER_LIB") or os.path.join(_HERE, "libgacer.so")
 
 # ---------------------------------------------------------------- constants
 OK = 0
@@ -35,7 +37,7 @@ OP = {"conv": 1, "linear": 2, "maxpool": 3, "avgpool": 4, "gap": 5, "add": 6, "c
 DTYPE = {"bf16": 1, "fp32": 2}
 AXIS = {"none": 0, "batch": 1, "channel": 2}
 MODE = {"executor": 0, "sequential": 1, "multistream": 2}
-PARTITION = {"work_conserving": 0, "strict": 1}
+PARTITION = {"work_conserving": 0, "strict": 1, "hybrid": 2}
 FLAG_BIAS, FLAG_CIP = 1, 2
 
 FP = C.POINTER(C.c_float)
@@ -299,7 +301,7 @@ def gacer_get_stats():
 
 
 def gacer_get_trace(cap):
-    buf = np.zeros((cap, 8), dtype=np.int64)
+    buf = np.zeros((cap, 10), dtype=np.int64)
     n = _check(lib().gacer_get_trace(buf.ctypes.data_as(C.POINTER(C.c_int64)), cap))
     return buf[:n]
 
@@ -308,7 +310,7 @@ def gacer_last_error():
     return lib().gacer_last_error().decode()
 
 
-def gacer_debug_timing(n_ops=1, reset=True, n_ctas=148, events=16):
+def gacer_debug_timing(n_ops=1, reset=True, n_ctas=148, events=24):
     buf = np.zeros((n_ops, n_ctas, events), dtype=np.int64)
     _check(lib().gacer_debug_timing(buf.ctypes.data_as(C.POINTER(C.c_int64)), buf.size, int(reset)))
     return buf

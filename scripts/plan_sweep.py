@@ -41,25 +41,37 @@ def main():
     a = ap.parse_args()
     ts = bench.make_workload()
     res = []
-    for partition in ("work_conserving", "strict"):
+    for partition in ("work_conserving",):
         s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], partition=partition)
         for t, (*_, x) in enumerate(ts):
             s.set_input(t, x)
         nops = [len(g.ops) for _, g, *_ in ts]
+
+        def all_batch(tenants, sizes):
+            dec = []
+            for t in tenants:
+                g = ts[t][1]
+                for i, op in enumerate(g.ops):
+                    if op["kind"] in ("conv", "linear", "maxpool", "avgpool", "gap", "add", "relu", "relu6"):
+                        dec.append((t, i + 1, "batch", sizes))
+            return dec
         plans = [("identity", None, None, None)]
-        for sh in ([0.2, 0.7, 0.1], [0.3, 0.6, 0.1], [0.25, 0.5, 0.25], [0.35, 0.45, 0.2]):
-            plans.append((f"shares{sh}", None, None, sh))
-        for k in (1, 2, 3, 4, 6):
-            plans.append((f"ptr{k}", None, [equal_cuts(n, k) for n in nops], None))
-        vgg = ts[1][1]
-        vdec = [(1, i + 1, "batch", [4, 4]) for i, op in enumerate(vgg.ops) if op["kind"] == "conv"]
-        plans.append(("vgg_conv_b44", vdec, None, None))
-        plans.append(("vgg_conv_b44+ptr2", vdec, [equal_cuts(n, 2) for n in nops], None))
+        plans.append(("shares[.35,.45,.2]", None, None, [0.35, 0.45, 0.2]))
+        for sizes in ([4, 4], [2, 2, 2, 2], [1] * 8):
+            nm = "".join(str(v) for v in sizes)
+            plans.append((f"all_b{nm}", all_batch([0, 1, 2], sizes), None, None))
+            plans.append((f"r50mv2_b{nm}", all_batch([0, 2], sizes), None, None))
+            plans.append((f"all_b{nm}+shares", all_batch([0, 1, 2], sizes), None, [0.35, 0.45, 0.2]))
+        plans.append(("all_b2222+ptr2", all_batch([0, 1, 2], [2, 2, 2, 2]), [equal_cuts(n, 2) for n in nops], None))
         for name, dec, ptr, sh in plans:
-            s.set_regulation(dec, ptr)
+            try:
+                s.set_regulation(dec, ptr)
+            except G.GacerError as e:
+                print(json.dumps({"plan": name, "error": str(e)}), flush=True)
+                continue
             G.gacer_set_sm_shares(sh)
             ms = time_round(s)
-            res.append({"partition": partition, "plan": name, "ms": ms})
+            res.append({"partition": partition, "plan": name, "ms": ms, "items": s.stats()["n_items"]})
             print(json.dumps(res[-1]), flush=True)
         s.close()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
