@@ -146,9 +146,12 @@ typedef enum {
 } gacer_mode;
 
 typedef enum {
-  GACER_PARTITION_WORK_CONSERVING = 0, /* each CTA prefers one tenant, steals from the others */
-  GACER_PARTITION_STRICT = 1,          /* each CTA serves only its tenant (SM share per tenant) */
-  GACER_PARTITION_HYBRID = 2           /* like WORK_CONSERVING, except that CTAs of the other tenants
+  GACER_PARTITION_PRIORITY = 0,        /* default.  No tenant ownership: every CTA claims the ready item
+                                          of highest upward rank over all tenants (global list
+                                          scheduling, HEFT-style); the SM shares only order ties */
+  GACER_PARTITION_WORK_CONSERVING = 1, /* each CTA prefers one tenant (SM share), steals from the others */
+  GACER_PARTITION_STRICT = 2,          /* each CTA serves only its tenant (SM share per tenant) */
+  GACER_PARTITION_HYBRID = 3           /* like WORK_CONSERVING, except that CTAs of the other tenants
                                           never take the bulk tenant's (largest share) items: its long
                                           tiles cannot delay the latency-bound chains */
 } gacer_partition;

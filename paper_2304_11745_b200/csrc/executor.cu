@@ -1046,7 +1046,7 @@ __device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& b
     best_h = h;
     best_prio = prio;
     cand = c;
-    if (j == 0) return 1;  // the CTA's own tenant (SM partition) comes first
+    if (j == 0 && p.own_first) return 1;  // the CTA's own tenant (SM partition) comes first
   }
   return best_si >= 0 ? 1 : (unclaimed ? 0 : 2);
 }

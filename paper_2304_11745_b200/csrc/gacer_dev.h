@@ -132,7 +132,7 @@ struct ExecParams {
   int32_t n_heads;
   int64_t watchdog_ns;
   int32_t single_op;        // >= 0: standalone mode, run every tile of this op (strided over CTAs)
-  int32_t pad;
+  int32_t own_first;        // 1: the CTA's own tenant (pref[0]) wins over higher-ranked items
   int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
 };
 constexpr int DBG_EVENTS = 24;

@@ -1249,6 +1249,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     p.n_heads = p.n_tenants * p.n_clusters;
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
+    p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
     p.dbg = S.d_dbg;
     CUDA_TRY(launch_executor(p, S.grid, st));
     launches = 1;
@@ -1334,6 +1335,11 @@ int gacer_init(int cuda_device, const gacer_options* opts) {
   if (S.inited) gacer_shutdown();
   S = State();
   if (opts) S.opts = *opts;
+  if (S.opts.partition < GACER_PARTITION_PRIORITY || S.opts.partition > GACER_PARTITION_HYBRID) {
+    const int bad = S.opts.partition;
+    S = State();
+    return set_err(GACER_E_INVALID_ARG, "unknown partition mode %d", bad);
+  }
   S.host_only = cuda_device < 0;
   S.device = cuda_device;
   S.inited = true;

@@ -37,7 +37,7 @@ OP = {"conv": 1, "linear": 2, "maxpool": 3, "avgpool": 4, "gap": 5, "add": 6, "c
 DTYPE = {"bf16": 1, "fp32": 2}
 AXIS = {"none": 0, "batch": 1, "channel": 2}
 MODE = {"executor": 0, "sequential": 1, "multistream": 2}
-PARTITION = {"work_conserving": 0, "strict": 1, "hybrid": 2}
+PARTITION = {"priority": 0, "work_conserving": 1, "strict": 2, "hybrid": 3}
 FLAG_BIAS, FLAG_CIP = 1, 2
 
 FP = C.POINTER(C.c_float)
@@ -228,7 +228,7 @@ def regulation_desc(decomposition=None, pointers=None, n_tenants=None):
 
 
 # ---------------------------------------------------------------- calls
-def gacer_init(device=0, num_ctas=0, partition="work_conserving", watchdog_ms=0, trace=False):
+def gacer_init(device=0, num_ctas=0, partition="priority", watchdog_ms=0, trace=False):
     o = gacer_options(num_ctas=num_ctas, partition=PARTITION[partition], watchdog_ms=watchdog_ms,
                       trace=int(trace))
     return _check(lib().gacer_init(device, C.byref(o)))

@@ -26,7 +26,7 @@ def nchw_to_nhwc_padded(x: np.ndarray, c_pad: int, dtype: torch.dtype) -> torch.
 class Session:
     """One GACER instance on one GPU with its registered tenants."""
 
-    def __init__(self, tenants, device=0, num_ctas=0, partition="work_conserving",
+    def __init__(self, tenants, device=0, num_ctas=0, partition="priority",
                  watchdog_ms=0, trace=False):
         """tenants: list of (graph, params, batch, dtype)."""
         self.device = device

@@ -13,7 +13,7 @@ from paper_2304_11745_b200.runtime import Session  # noqa: E402
 
 plan = sys.argv[1] if len(sys.argv) > 1 else "identity"
 ts = bench.make_workload()
-s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], trace=True)
+s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], trace=True, partition=os.environ.get("GACER_PARTITION", "priority"))
 for t, (*_, x) in enumerate(ts):
     s.set_input(t, x)
 for nm, dec, ptr, sh in bench.sweep_plans(ts):

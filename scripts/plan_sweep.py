@@ -41,28 +41,12 @@ def main():
     a = ap.parse_args()
     ts = bench.make_workload()
     res = []
-    for partition in ("work_conserving",):
+    parts = os.environ.get("PARTITIONS", "priority,work_conserving,hybrid").split(",")
+    for partition in parts:
         s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], partition=partition)
         for t, (*_, x) in enumerate(ts):
             s.set_input(t, x)
-        nops = [len(g.ops) for _, g, *_ in ts]
-
-        def all_batch(tenants, sizes):
-            dec = []
-            for t in tenants:
-                g = ts[t][1]
-                for i, op in enumerate(g.ops):
-                    if op["kind"] in ("conv", "linear", "maxpool", "avgpool", "gap", "add", "relu", "relu6"):
-                        dec.append((t, i + 1, "batch", sizes))
-            return dec
-        plans = [("identity", None, None, None)]
-        plans.append(("shares[.35,.45,.2]", None, None, [0.35, 0.45, 0.2]))
-        for sizes in ([4, 4], [2, 2, 2, 2], [1] * 8):
-            nm = "".join(str(v) for v in sizes)
-            plans.append((f"all_b{nm}", all_batch([0, 1, 2], sizes), None, None))
-            plans.append((f"r50mv2_b{nm}", all_batch([0, 2], sizes), None, None))
-            plans.append((f"all_b{nm}+shares", all_batch([0, 1, 2], sizes), None, [0.35, 0.45, 0.2]))
-        plans.append(("all_b2222+ptr2", all_batch([0, 1, 2], [2, 2, 2, 2]), [equal_cuts(n, 2) for n in nops], None))
+        plans = bench.sweep_plans(ts)
         for name, dec, ptr, sh in plans:
             try:
                 s.set_regulation(dec, ptr)

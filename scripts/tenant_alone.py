@@ -14,7 +14,7 @@ ts = bench.make_workload()
 stream = torch.cuda.Stream()
 for sel in ([0], [1], [2], [0, 2], [0, 1, 2]):
     sub = [ts[i] for i in sel]
-    s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in sub])
+    s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in sub], partition=os.environ.get("GACER_PARTITION", "priority"))
     for t, (*_, x) in enumerate(sub):
         s.set_input(t, x)
     row = [",".join(ts[i][0] for i in sel)]

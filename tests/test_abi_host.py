@@ -154,3 +154,15 @@ def test_identity_plan_and_fusion_counts(host):
     assert abs(info["flops"] - 65.43e9) / 65.43e9 < 1e-3
     st = G.gacer_get_stats()
     assert st["n_clusters"] == 1 and st["n_fused_ops"] == 56
+
+
+def test_partition_modes_validated():
+    """Every gacer_partition value opens an instance; others are rejected."""
+    import ctypes
+    for name in G.PARTITION:
+        G.gacer_init(-1, partition=name)
+        G.gacer_shutdown()
+    for bad in (-1, 4, 99):
+        o = G.gacer_options(num_ctas=0, partition=bad, watchdog_ms=0, trace=0)
+        assert G.lib().gacer_init(-1, ctypes.byref(o)) == -1  # GACER_E_INVALID_ARG
+    assert G.PARTITION["priority"] == 0   # the default (zeroed options)

@@ -3,7 +3,7 @@ different regulation plans of the same tenant mix").
 
 The D2 mix (ResNet-50 + VGG-16 + MobileNetV2, B=8, 224^2, bf16) runs under
 the identity plan, seeded random spatial plans (batch and channel chunks),
-random sync pointers, strict and work-conserving SM partitions, several grid
+random sync pointers, priority / strict / work-conserving / hybrid SM partitions, several grid
 sizes, and the sequential / multi-stream baselines: every output must be
 byte-identical.  The device trace must respect the cluster barrier
 (Eq. 6, l.725: clusters are deployed in order) and chain order."""
@@ -77,7 +77,8 @@ def run(ts, plan=None, mode="executor", **kw):
 def test_bitwise_across_plans_and_modes(cuda_ok, d2):
     ref, _ = run(d2)
     variants = [dict(mode="sequential"), dict(mode="multistream"),
-                dict(partition="strict"), dict(num_ctas=37), dict(num_ctas=296)]
+                dict(partition="strict"), dict(partition="work_conserving"), dict(partition="hybrid"),
+                dict(num_ctas=37), dict(num_ctas=296)]
     rng = np.random.default_rng(12345)
     for k in range(6):
         variants.append(dict(plan=random_plan(d2, rng, n_pointers=k % 4)))
