@@ -161,6 +161,10 @@ typedef struct {
   int32_t partition;          /* gacer_partition */
   int32_t watchdog_ms;        /* device spin budget before GACER_E_DEADLOCK; 0 = 2000 */
   int32_t trace;              /* 1 = record per-item (tenant, op, sm, t0, t1) */
+  int32_t coarse_deps;        /* 1 = an item waits for whole producer chunks (the paper's
+                                 op-level dependency); 0 (default) = only for the producer
+                                 M-tiles its input window reads (tile wavefront).  Results
+                                 are bit-identical either way. */
 } gacer_options;
 
 typedef struct {

@@ -114,6 +114,23 @@ __device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+// tcgen05.ld of 32 columns without waiting
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// keep the uses of r after the preceding tcgen05.wait::ld (the registers are
+// written asynchronously; the empty asm orders every use after the wait)
+__device__ __forceinline__ void tmem_pin32(uint32_t* r) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));
+}
 
 // UMMA shared-memory descriptor, K-major, SWIZZLE_128B canonical layout:
 // 8-row x 128-byte atoms (row r, 16B chunk j stored at chunk j ^ (r & 7)),
@@ -147,6 +164,18 @@ __device__ __forceinline__ void dbg_mark(const ExecParams& p, int ev) {
     atomicOr(&g_dbg_seen, 1u << ev);
     p.dbg[static_cast<size_t>(blockIdx.x) * DBG_EVENTS + ev] = static_cast<int64_t>(globaltimer());
   }
+}
+
+// per-k-block timeline of CTA 0 (GACER_DEBUG_TIMING): [0,256) MMA saw stage
+// full, [256,512) producer issued the stage, [512,768) epilogue (tfull, done)
+constexpr size_t KDBG_OFF = static_cast<size_t>(400) * 148 * DBG_EVENTS;
+__device__ __forceinline__ void kdbg(const ExecParams& p, int slot, uint32_t i) {
+  if (p.dbg && blockIdx.x == 0 && i < 256) p.dbg[KDBG_OFF + slot * 256 + i] = static_cast<int64_t>(globaltimer());
+}
+
+// epilogue clock64 stamps of CTA 0's first 8 GEMM items (GACER_DEBUG_TIMING)
+__device__ __forceinline__ void edbg(const ExecParams& p, int point, uint32_t acc) {
+  if (p.dbg && blockIdx.x == 0 && acc < 8) p.dbg[KDBG_OFF + 768 + acc * 16 + point] = static_cast<int64_t>(clock64());
 }
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -268,14 +297,19 @@ struct SmemCtl {
   int32_t epi_flag;
   int32_t n_segs_smem;
   int32_t pad;
-  float red[CC_THREADS * 8]; // GAP fixed-order reduction scratch
+  __align__(16) float red[CC_THREADS * 8]; // GAP fixed-order reduction scratch / dw weights (float4 reads)
   float epi_scale[BN_MAX];   // epilogue: folded BN scale / bias of the tile's columns
   float epi_bias[BN_MAX];
   Seg segs[MAX_SMEM_SEGS];   // (tenant, cluster) queue segments, cached
+  OpDev wop;                 // the worker group's current op (staged once per item)
 };
 constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 rows x 128 B per warp (SW128)
 constexpr int SMEM_STAGE_BYTES = (NEPI / 32) * STAGE_WARP_BYTES;
-constexpr int SMEM_BYTES = SMEM_RING_BYTES + SMEM_STAGE_BYTES + 1024 /*align slack*/ + (int)sizeof(SmemCtl);
+constexpr int SMEM_BYTES = SMEM_RING_BYTES + SMEM_STAGE_BYTES + 1024 /*align slack*/;
+// The control block is a static __shared__ object (not carved from the
+// dynamic buffer) so every access compiles to LDS/STS instead of generic
+// loads/stores.
+__shared__ __align__(128) SmemCtl g_ctl;
 
 struct Ctx {
   uint8_t* ring;             // 1024-aligned stage buffers
@@ -328,20 +362,22 @@ __device__ __forceinline__ void epi_math8(const EpiOp& op, const float* v, const
 // Write 8 results of `row` at column offset `col` (within the staged chunk)
 // into the warp's 32x128B staging block with the 128-byte swizzle (16-byte
 // chunk j of row r at j ^ (r & 7)), the layout the TMA store reads.
-__device__ __forceinline__ void stage8(uint8_t* wbuf, int row, int col, const float* y, bool f32) {
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void stage8(uint32_t wbuf, int row, int col, const float* y, bool f32) {
   const int sw = row & 7;
+  const uint32_t rb = wbuf + row * 128;
   if (f32) {
     const int j0 = (col * 4) >> 4;
-    *reinterpret_cast<float4*>(wbuf + row * 128 + ((j0 ^ sw) << 4)) = make_float4(y[0], y[1], y[2], y[3]);
-    *reinterpret_cast<float4*>(wbuf + row * 128 + (((j0 + 1) ^ sw) << 4)) = make_float4(y[4], y[5], y[6], y[7]);
+    sts128(rb + ((j0 ^ sw) << 4), __float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]),
+           __float_as_uint(y[3]));
+    sts128(rb + (((j0 + 1) ^ sw) << 4), __float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]),
+           __float_as_uint(y[7]));
   } else {
     const int j = (col * 2) >> 4;
-    uint4 u;
-    u.x = pack_bf16x2(y[0], y[1]);
-    u.y = pack_bf16x2(y[2], y[3]);
-    u.z = pack_bf16x2(y[4], y[5]);
-    u.w = pack_bf16x2(y[6], y[7]);
-    *reinterpret_cast<uint4*>(wbuf + row * 128 + ((j ^ sw) << 4)) = u;
+    sts128(rb + ((j ^ sw) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]),
+           pack_bf16x2(y[6], y[7]));
   }
 }
 
@@ -382,6 +418,93 @@ __device__ __forceinline__ void epilogue_store8(const EpiOp& op, int m, int n, c
   }
 }
 
+// Staged bf16 epilogue of one warp's 32 accumulator rows (split-K 1, not
+// swap-AB): the TMEM load of the next 32 columns is in flight while the
+// current 32 are converted -- y = clamp(acc*scale + bias [+ skip], lo, hi)
+// with FFMA2 (lo/hi encode the activation: none = (-inf, inf), ReLU =
+// (0, inf), ReLU6 = (0, 6); same IEEE ops as apply_act), RNE to bf16 --
+// written 128B-swizzled to the warp's staging rows and TMA-stored per 64
+// columns.  One instantiation (runtime act/skip): several inlined variants
+// overflow the 168-register budget.
+__device__ __forceinline__ void epi_chunk_bf16(const uint32_t* r, int c, int c_lo, int c_hi, const float* esc,
+                                               const float* ebi, bool skip, const uint4* sk, float lo, float hi,
+                                               uint32_t wbuf_s, int lane, const void* tmap_c, int n0, int row0) {
+  const int cin = (c - c_lo) & 63;         // column offset inside the staged 64-column chunk
+  if (cin == 0 && c > c_lo) {              // new chunk: the previous store must have read the buffer
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+  }
+#pragma unroll
+  for (int g8 = 0; g8 < 4; ++g8) {
+    const int cc = c + g8 * 8;
+    float y[8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[g8 * 8 + j]), __uint_as_float(r[g8 * 8 + j + 1])),
+                                  make_float2(esc[cc + j], esc[cc + j + 1]), make_float2(ebi[cc + j], ebi[cc + j + 1]));
+      y[j] = o.x;
+      y[j + 1] = o.y;
+    }
+    if (skip) {
+      float sv[8];
+      bf16x8_to_f32(sk[g8], sv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[j] += sv[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
+    const int jj = ((cin + g8 * 8) * 2) >> 4;   // 16-byte chunk in the 128-byte row
+    sts128(wbuf_s + lane * 128 + ((jj ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+           pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+  }
+  if (cin == 32 || c + 32 >= c_hi) {       // chunk complete: TMA-store it
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmap_c, wbuf_s, n0 + c - cin, row0);
+      bulk_commit();
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_load_skip(uint4* dst, const __nv_bfloat16* skrow, int c, int c_hi, int cout_left) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int cc = c + u * 8;
+    dst[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+__device__ __forceinline__ void epi_staged_bf16(uint32_t taddr, int c_lo, int c_hi, int cout_left, const float* esc,
+                                                const float* ebi, const __nv_bfloat16* skrow, int act,
+                                                uint32_t wbuf_s, int lane, const void* tmap_c, int n0, int row0) {
+  const float lo = act == ACT_NONE ? -INFINITY : 0.0f;
+  const float hi = act == ACT_RELU6 ? 6.0f : INFINITY;
+  const bool skip = skrow != nullptr;
+  uint32_t ra[32], rb[32];
+  uint4 ska[4], skb[4];
+  tmem_ld32_nw(taddr + c_lo, ra);
+  if (skip) epi_load_skip(ska, skrow, c_lo, c_hi, cout_left);
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 64) {
+    tmem_wait();
+    tmem_pin32(ra);
+    if (c + 32 < c_hi) {
+      tmem_ld32_nw(taddr + c + 32, rb);
+      if (skip) epi_load_skip(skb, skrow, c + 32, c_hi, cout_left);
+    }
+    epi_chunk_bf16(ra, c, c_lo, c_hi, esc, ebi, skip, ska, lo, hi, wbuf_s, lane, tmap_c, n0, row0);
+    if (c + 32 >= c_hi) break;
+    tmem_wait();
+    tmem_pin32(rb);
+    if (c + 64 < c_hi) {
+      tmem_ld32_nw(taddr + c + 64, ra);
+      if (skip) epi_load_skip(ska, skrow, c + 64, c_hi, cout_left);
+    }
+    epi_chunk_bf16(rb, c + 32, c_lo, c_hi, esc, ebi, skip, skb, lo, hi, wbuf_s, lane, tmap_c, n0, row0);
+  }
+}
+
 // swap-AB (linear): GEMM row m = output feature, GEMM column n = sample
 __device__ __forceinline__ void epilogue_store8_swap(const EpiOp& op, int m, int n, const float* v, float sc,
                                                      float bi) {
@@ -405,44 +528,59 @@ __device__ __forceinline__ void kb_range(const OpDev& op, int ks, int& kb0, int&
 
 __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t& g, int wtid,
                              const ExecParams& p) {
-  SmemCtl* ctl = cx.ctl;
+  SmemCtl* ctl = &g_ctl;
   int kb0, nk;
   kb_range(op, it.ks, kb0, nk);
   const uint32_t ring_base = smem_u32(cx.ring);
   const uint32_t bbytes = static_cast<uint32_t>(op.bn) * 128u;
   const int m0 = it.mt * BM, n0 = it.nt * op.bn;
   if (op.a_mode != A_GATHER) {
-    if (wtid == 0) {
+    // NPROD producer threads (lane 0 of worker warps 0..NPROD-1), producer j
+    // filling the stages gi = j (mod NPROD): one thread's TMA loads complete
+    // at only ~27-35 B/clk (measured, scripts/micro/tma_rate.cu), far below
+    // what the MMA consumes, so the issue is spread over several threads.
+    const int pj = wtid >> 5;
+    if ((wtid & 31) == 0 && pj < NPROD) {
+      // every OpDev field the loop needs is loaded once into registers: the
+      // SM's L1 is invalidated by the gpu-scope fences of the other roles,
+      // so a global re-load per K-block would cost an L2 round trip each
+      const int a_mode = op.a_mode, C = op.C, kw = op.kw;
+      const void* tmap_a = op.tmap_a;
+      const void* tmap_b = op.tmap_b;
       fence_proxy_async_global();   // acquired producer data -> this thread's TMA reads
       int w0 = 0, h0 = 0, img0 = 0;
-      if (op.a_mode == A_IM2COL) {
-        const int HoWo = op.Ho * op.Wo;
+      if (a_mode == A_IM2COL) {
+        const int HoWo = op.Ho * op.Wo, Wo = op.Wo;
         img0 = m0 / HoWo;
         const int rem = m0 - img0 * HoWo;
-        const int ho = rem / op.Wo, wo = rem - (rem / op.Wo) * op.Wo;
+        const int ho = rem / Wo, wo = rem - (rem / Wo) * Wo;
         w0 = wo * op.stride - op.pw;
         h0 = ho * op.stride - op.ph;
       }
-      for (int i = 0; i < nk; ++i) {
+      const uint32_t tx = A_STAGE_BYTES + bbytes;
+      const int i0 = static_cast<int>((static_cast<uint32_t>(pj) - g) % NPROD);
+#pragma unroll 1
+      for (int i = i0; i < nk; i += NPROD) {
         const uint32_t gi = g + i, stage = gi % STAGES;
         if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
         uint64_t* bar = &ctl->full[stage];
-        mbar_arrive_expect_tx(bar, A_STAGE_BYTES + bbytes);
+        mbar_arrive_expect_tx(bar, tx);
         const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
         const uint32_t b_dst = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
         const int k = (kb0 + i) * BK;
-        if (op.a_mode == A_IM2COL) {
-          const int tap = k / op.C;
-          const int c0 = k - tap * op.C;
-          const int r = tap / op.kw, s = tap - (tap / op.kw) * op.kw;
-          tma_load_im2col_4d(a_dst, op.tmap_a, bar, c0, w0, h0, img0, static_cast<uint16_t>(s),
+        if (a_mode == A_IM2COL) {
+          const int tap = k / C;
+          const int c0 = k - tap * C;
+          const int r = tap / kw, sx = tap - r * kw;
+          tma_load_im2col_4d(a_dst, tmap_a, bar, c0, w0, h0, img0, static_cast<uint16_t>(sx),
                              static_cast<uint16_t>(r));
         } else {
-          tma_load_2d(a_dst, op.tmap_a, bar, k, m0);
+          tma_load_2d(a_dst, tmap_a, bar, k, m0);
         }
-        tma_load_2d(b_dst, op.tmap_b, bar, k, n0);
-        if (i == 0) dbg_mark(p, 2);
+        tma_load_2d(b_dst, tmap_b, bar, k, n0);
+        kdbg(p, 1, gi);
       }
+      if (pj == 0) dbg_mark(p, 2);
     }
   } else {
     // im2col gather with cp.async (C not a multiple of 64): 16-byte chunks of
@@ -466,6 +604,7 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       hi0[i] = ok ? ho * op.stride - op.ph : -100000;
       wi0[i] = wo * op.stride - op.pw;
     }
+#pragma unroll 1
     for (int i = 0; i < nk; ++i) {
       const uint32_t gi = g + i, stage = gi % STAGES;
       if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
@@ -659,215 +798,161 @@ __device__ __forceinline__ void cc_pixel(const OpDev& op, int m, int c, int HoWo
   store8<F32>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
 }
 
-// Two output pixels (m0, m1; m1 = -1: none) x 8 channels of a bf16
-// max-pool / avg-pool / depthwise op with kh*kw <= 9.  Taps are loaded
-// unconditionally from a clamped address and masked, so the 2*kh*kw loads
-// are independent and in flight together; the reduction order over taps is
-// the same fixed (r, s) order as cc_pixel.
-__device__ void window2_bf16(const OpDev& op, int m0, int m1, int c, int HoWo) {
-  const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
-  const int T = op.kh * op.kw;
-  uint4 raw[2][9];
-  uint32_t valid[2] = {0, 0};
-  int cnt[2] = {0, 0};
-#pragma unroll
-  for (int px = 0; px < 2; ++px) {
-    const int m = px == 0 ? m0 : (m1 >= 0 ? m1 : m0);
-    const int b = m / HoWo, rem = m - b * HoWo, ho = rem / op.Wo, wo = rem - ho * op.Wo;
-    const size_t img = static_cast<size_t>(b) * op.H * op.W;
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      if (t < T) {
-        const int r = t / op.kw, s = t - (t / op.kw) * op.kw;
-        const int hi = ho * op.stride - op.ph + r, wi = wo * op.stride - op.pw + s;
-        const bool ok = hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
-        const bool in_frame = hi >= -op.ph && hi < op.H + op.ph && wi >= -op.pw && wi < op.W + op.pw;
-        valid[px] |= (ok ? 1u : 0u) << t;
-        cnt[px] += (op.cip ? in_frame : ok) ? 1 : 0;
-        const int hc = ok ? hi : 0, wc = ok ? wi : 0;
-        raw[px][t] = *reinterpret_cast<const uint4*>(in + (img + static_cast<size_t>(hc) * op.W + wc) * op.ldi + c);
-      }
-    }
-  }
-  const float* wt = static_cast<const float*>(op.wt);
-#pragma unroll
-  for (int px = 0; px < 2; ++px) {
-    const int m = px == 0 ? m0 : m1;
-    if (m < 0) break;
-    float y[8];
-    const float init = op.kind == DK_MAXPOOL ? -INFINITY : 0.0f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) y[q] = init;
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      if (t < T && ((valid[px] >> t) & 1u)) {
-        float f[8];
-        bf16x8_to_f32(raw[px][t], f);
-        if (op.kind == DK_MAXPOOL) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
-        } else if (op.kind == DK_AVGPOOL) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] += f[q];
-        } else {
-          const float4 w0 = *reinterpret_cast<const float4*>(wt + t * op.C + c);
-          const float4 w1 = *reinterpret_cast<const float4*>(wt + t * op.C + c + 4);
-          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] = fmaf(f[q], wv[q], y[q]);
-        }
-      }
-    }
-    if (op.kind == DK_AVGPOOL) {
-      const float inv = static_cast<float>(cnt[px]);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = y[q] / inv;
-    } else if (op.kind == DK_DW) {
-      const float4 s0 = *reinterpret_cast<const float4*>(op.scale + c);
-      const float4 s1 = *reinterpret_cast<const float4*>(op.scale + c + 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(op.bias + c);
-      const float4 b1 = *reinterpret_cast<const float4*>(op.bias + c + 4);
-      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
-      if (op.has_skip) {
-        float sk[8];
-        load8<false>(op.skip, static_cast<size_t>(m) * op.lds + c, sk);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) y[q] += sk[q];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) y[q] = apply_act(y[q], op.act);
-    store8<false>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
-  }
+// Shared-memory window op (bf16 depthwise conv / max-pool / avg-pool, any
+// kernel <= 3x3 taps... any kh*kw <= 9): the item is bm output pixels (whole
+// output rows, chosen on the host) x bn channels.  Per image segment of the
+// item, every input row the segment's windows touch is copied into shared
+// memory with cp.async at once (coalesced 16-byte chunks, ~all of it in
+// flight: the op is latency/bandwidth bound, not compute bound), then each
+// thread computes (pixel, 8 channels) outputs from shared memory.  Per output
+// the taps are reduced in the same fixed (r, s) order with IEEE fma as
+// cc_pixel, so results are bit-identical to the other window paths.
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
 }
-
-// Row-run window op (bf16 max-pool / avg-pool / depthwise conv, KHxKW taps,
-// stride S): thread (run r, channel group g) computes RUN consecutive output
-// pixels of one channel group, sliding the KHxKW window of raw bf16x8 input
-// vectors along the output row (stride 1 reuses KW-1 of KW columns).  The
-// item's depthwise weights and folded scale/bias are staged in shared memory
-// (wsm) once.  Per output the taps are reduced in the same fixed (r, s)
-// order, each with an IEEE fma, as cc_pixel: results are bit-identical.
-constexpr int RUN = CC_RUN;
-template <int KH, int KW, int S>
-__device__ void window_run_bf16(const OpDev& op, const Item& it, int tid, int G, float* wsm) {
-  const int g = tid % G;
-  const int cl = g * 8;                      // channel offset inside the item
-  const int c = it.nt * op.bn + cl;
-  const int bnc = op.bn;
-  const bool dw = op.kind == DK_DW;
-  if (dw) {  // stage weights [tap][bn] and scale/bias [bn] (fp32)
-    const float* wt = static_cast<const float*>(op.wt);
-    const int c0 = it.nt * op.bn;
-    const int nld = KH * KW * bnc;
-    for (int i = tid; i < nld; i += CC_THREADS) {
-      const int t = i / bnc, cc = i - t * bnc;
-      wsm[i] = (c0 + cc < op.Cout) ? wt[t * op.C + c0 + cc] : 0.0f;
-    }
-    for (int i = tid; i < bnc; i += CC_THREADS) {
-      const bool ok = c0 + i < op.Cout;
-      wsm[nld + i] = ok ? op.scale[c0 + i] : 0.0f;
-      wsm[nld + bnc + i] = ok ? op.bias[c0 + i] : 0.0f;
-    }
-  }
-  named_bar_sync(1, CC_THREADS);
-  if (c >= op.Cout) return;
-  const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
-  const int HoWo = op.Ho * op.Wo;
-  const int m_begin = it.mt * op.bm + (tid / G) * RUN;
-  uint4 raw[KH][KW];
-  uint32_t valid = 0;                        // bit r*KW+s
-  int ho = -1, wo = 0, b = 0;
-  for (int j = 0; j < RUN; ++j) {
-    const int m = m_begin + j;
-    if (m >= op.M) break;
-    bool fresh = true;
-    if (ho >= 0 && wo + 1 < op.Wo) {         // same row: slide by S columns
-      ++wo;
-      fresh = false;
-    } else {
-      b = m / HoWo;
-      const int rem = m - b * HoWo;
-      ho = rem / op.Wo;
-      wo = rem - ho * op.Wo;
-    }
-    const size_t img = static_cast<size_t>(b) * op.H * op.W;
-#pragma unroll
-    for (int r = 0; r < KH; ++r) {
-      const int hi = ho * S - op.ph + r;
-      const bool hok = hi >= 0 && hi < op.H;
-#pragma unroll
-      for (int s = 0; s < KW; ++s) {
-        if (!fresh && s + S < KW) {          // reuse a column of the previous window
-          raw[r][s] = raw[r][s + S];
-          const uint32_t bit = (valid >> (r * KW + s + S)) & 1u;
-          valid = (valid & ~(1u << (r * KW + s))) | (bit << (r * KW + s));
-        } else {
-          const int wi = wo * S - op.pw + s;
-          const bool ok = hok && wi >= 0 && wi < op.W;
-          raw[r][s] = ok ? *reinterpret_cast<const uint4*>(in + (img + static_cast<size_t>(hi) * op.W + wi) * op.ldi + c)
-                         : make_uint4(0, 0, 0, 0);
-          valid = (valid & ~(1u << (r * KW + s))) | ((ok ? 1u : 0u) << (r * KW + s));
-        }
-      }
-    }
-    float y[8];
-    const float init = op.kind == DK_MAXPOOL ? -INFINITY : 0.0f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) y[q] = init;
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32f(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(a), "f"(v) : "memory");
+}
+// Outputs of one staged image segment: task (pixel, 8-channel group).  KH,
+// KW, S > 0: compile-time window (taps unrolled, the tap loads of a pixel
+// issued together); 0: runtime window.  Same fixed (r, s) reduction order.
+template <int KH_, int KW_, int S_>
+__device__ __forceinline__ void window_segment(const OpDev& op, int tid, int nthr, uint32_t sbuf, uint32_t wsm,
+                                               int img, int m, int seg_end, int h_lo, int c0, int bnc) {
+  const int KH = KH_ ? KH_ : op.kh, KW = KW_ ? KW_ : op.kw, S = S_ ? S_ : op.stride;
+  constexpr int TMAX = KH_ ? KH_ * KW_ : 9;
+  const int PH = op.ph, PW = op.pw, H = op.H, W = op.W, Wo = op.Wo;
+  const int HoWo = op.Ho * Wo;
+  const int kind = op.kind;
+  const int G8 = bnc >> 3;
+  const int tasks = (seg_end - m) * G8;
+  // nthr % G8 == 0: a thread keeps its channel group (no division per task)
+  const bool fixed_cg = (nthr % G8) == 0;
+  for (int i = tid; i < tasks; i += nthr) {
+    const int cg = fixed_cg ? (tid % G8) : (i % G8);
+    const int px = m + i / G8;
+    const int rem = px - img * HoWo, ho = rem / Wo, wo = rem - ho * Wo;
+    const int hb = ho * S - PH, wb = wo * S - PW;
+    uint4 raw[TMAX];
+    uint32_t valid = 0;
     int cnt = 0;
 #pragma unroll
-    for (int r = 0; r < KH; ++r)
-#pragma unroll
-      for (int s = 0; s < KW; ++s) {
-        const bool ok = (valid >> (r * KW + s)) & 1u;
-        if (op.kind == DK_AVGPOOL) {
-          const int hi = ho * S - op.ph + r, wi = wo * S - op.pw + s;
-          const bool in_frame = hi >= -op.ph && hi < op.H + op.ph && wi >= -op.pw && wi < op.W + op.pw;
-          cnt += (op.cip ? in_frame : ok) ? 1 : 0;
-        }
-        if (!ok) continue;
-        float f[8];
-        bf16x8_to_f32(raw[r][s], f);
-        if (op.kind == DK_MAXPOOL) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
-        } else if (op.kind == DK_AVGPOOL) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) y[q] += f[q];
-        } else {
-          const float* w = wsm + (r * KW + s) * bnc + cl;
-          const float4 w0 = *reinterpret_cast<const float4*>(w);
-          const float4 w1 = *reinterpret_cast<const float4*>(w + 4);
-          float2 a;
-          a = __ffma2_rn(make_float2(f[0], f[1]), make_float2(w0.x, w0.y), make_float2(y[0], y[1])); y[0] = a.x; y[1] = a.y;
-          a = __ffma2_rn(make_float2(f[2], f[3]), make_float2(w0.z, w0.w), make_float2(y[2], y[3])); y[2] = a.x; y[3] = a.y;
-          a = __ffma2_rn(make_float2(f[4], f[5]), make_float2(w1.x, w1.y), make_float2(y[4], y[5])); y[4] = a.x; y[5] = a.y;
-          a = __ffma2_rn(make_float2(f[6], f[7]), make_float2(w1.z, w1.w), make_float2(y[6], y[7])); y[6] = a.x; y[7] = a.y;
-        }
+    for (int t = 0; t < TMAX; ++t) {
+      if (KH_ == 0 && t >= KH * KW) break;
+      const int r = t / KW, s2 = t - (t / KW) * KW;
+      const int hi = hb + r, wi = wb + s2;
+      const bool ok = hi >= 0 && hi < H && wi >= 0 && wi < W;
+      if (kind == DK_AVGPOOL) {
+        const bool in_frame = hi >= -PH && hi < H + PH && wi >= -PW && wi < W + PW;
+        cnt += (op.cip ? in_frame : ok) ? 1 : 0;
       }
-    if (op.kind == DK_AVGPOOL) {
+      valid |= (ok ? 1u : 0u) << t;
+      const int hc = ok ? hi - h_lo : 0, wc = ok ? wi : 0;
+      raw[t] = lds128(sbuf + ((hc * W + wc) * bnc + cg * 8) * 2);
+    }
+    float y[8];
+    const float init = kind == DK_MAXPOOL ? -INFINITY : 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = init;
+#pragma unroll
+    for (int t = 0; t < TMAX; ++t) {
+      if (KH_ == 0 && t >= KH * KW) break;
+      if (!((valid >> t) & 1u)) continue;
+      float f[8];
+      bf16x8_to_f32(raw[t], f);
+      if (kind == DK_MAXPOOL) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = fmaxf(y[q], f[q]);
+      } else if (kind == DK_AVGPOOL) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] += f[q];
+      } else {
+        const uint32_t wa = wsm + 4 * (t * bnc + cg * 8);
+        const float4 w0 = lds128f(wa), w1 = lds128f(wa + 16);
+        y[0] = fmaf(f[0], w0.x, y[0]); y[1] = fmaf(f[1], w0.y, y[1]);
+        y[2] = fmaf(f[2], w0.z, y[2]); y[3] = fmaf(f[3], w0.w, y[3]);
+        y[4] = fmaf(f[4], w1.x, y[4]); y[5] = fmaf(f[5], w1.y, y[5]);
+        y[6] = fmaf(f[6], w1.z, y[6]); y[7] = fmaf(f[7], w1.w, y[7]);
+      }
+    }
+    if (kind == DK_AVGPOOL) {
       const float inv = static_cast<float>(cnt);
 #pragma unroll
       for (int q = 0; q < 8; ++q) y[q] = y[q] / inv;
-    } else if (dw) {
-      const float* sc = wsm + KH * KW * bnc + cl;
-      const float* bi = sc + bnc;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
+    } else if (kind == DK_DW) {
+      const uint32_t sa = wsm + 4 * (KH * KW * bnc + cg * 8), ba = sa + 4 * bnc;
+      const float4 s0 = lds128f(sa), s1 = lds128f(sa + 16), b0 = lds128f(ba), b1 = lds128f(ba + 16);
+      y[0] = fmaf(y[0], s0.x, b0.x); y[1] = fmaf(y[1], s0.y, b0.y);
+      y[2] = fmaf(y[2], s0.z, b0.z); y[3] = fmaf(y[3], s0.w, b0.w);
+      y[4] = fmaf(y[4], s1.x, b1.x); y[5] = fmaf(y[5], s1.y, b1.y);
+      y[6] = fmaf(y[6], s1.z, b1.z); y[7] = fmaf(y[7], s1.w, b1.w);
       if (op.has_skip) {
         float sk[8];
-        load8<false>(op.skip, static_cast<size_t>(m) * op.lds + c, sk);
+        load8<false>(op.skip, static_cast<size_t>(px) * op.lds + c0 + cg * 8, sk);
 #pragma unroll
         for (int q = 0; q < 8; ++q) y[q] += sk[q];
       }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) y[q] = apply_act(y[q], op.act);
-    store8<false>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+    store8<false>(op.out, static_cast<size_t>(px) * op.ldo + c0 + cg * 8, y, op.out_f32);
+  }
+}
+
+__device__ void window_smem(const OpDev& op, const Item& it, int tid, int nthr, uint32_t sbuf, int bar_id) {
+  const int c0 = it.nt * op.bn;
+  const int bnc = min(op.bn, op.Cout - c0);          // channels of this item (multiple of 8)
+  const int G8 = bnc >> 3;
+  const int HoWo = op.Ho * op.Wo;
+  const int KH = op.kh, KW = op.kw, S = op.stride, PH = op.ph, H = op.H, W = op.W;
+  const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
+  const uint32_t wsm = sbuf + WIN_IN_BYTES;           // dw weights [tap][bnc], scale[bnc], bias[bnc]
+  if (op.kind == DK_DW) {
+    const float* wt = static_cast<const float*>(op.wt);
+    const int T = KH * KW;
+    for (int i = tid; i < T * bnc; i += nthr) {
+      const int t = i / bnc, cc = i - t * bnc;
+      sts32f(wsm + 4 * i, wt[t * op.C + c0 + cc]);
+    }
+    for (int i = tid; i < bnc; i += nthr) {
+      sts32f(wsm + 4 * (T * bnc + i), op.scale[c0 + i]);
+      sts32f(wsm + 4 * (T * bnc + bnc + i), op.bias[c0 + i]);
+    }
+  }
+  const int m_end = min(op.M, (it.mt + 1) * op.bm);
+  for (int m = it.mt * op.bm; m < m_end;) {
+    const int img = m / HoWo;
+    const int seg_end = min(m_end, (img + 1) * HoWo);
+    const int ho_a = (m - img * HoWo) / op.Wo, ho_b = (seg_end - 1 - img * HoWo) / op.Wo;
+    const int h_lo = max(0, ho_a * S - PH), h_hi = min(H - 1, ho_b * S - PH + KH - 1);
+    const int nrows = h_hi - h_lo + 1;
+    // ---- stage input rows [h_lo, h_hi] x W x bnc channels (row-major, channel-minor)
+    const int chunks = nrows * W * G8;
+    const __nv_bfloat16* src0 = in + (static_cast<size_t>(img) * H + h_lo) * W * op.ldi + c0;
+    for (int i = tid; i < chunks; i += nthr) {
+      const int cg = i % G8, pw_ = i / G8;          // pw_ = row * W + w
+      cp_async16(sbuf + (pw_ * bnc + cg * 8) * 2, src0 + static_cast<size_t>(pw_) * op.ldi + cg * 8, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    named_bar_sync(bar_id, nthr);
+    if (KH == 3 && KW == 3 && S == 1)
+      window_segment<3, 3, 1>(op, tid, nthr, sbuf, wsm, img, m, seg_end, h_lo, c0, bnc);
+    else if (KH == 3 && KW == 3 && S == 2)
+      window_segment<3, 3, 2>(op, tid, nthr, sbuf, wsm, img, m, seg_end, h_lo, c0, bnc);
+    else if (KH == 2 && KW == 2 && S == 2)
+      window_segment<2, 2, 2>(op, tid, nthr, sbuf, wsm, img, m, seg_end, h_lo, c0, bnc);
+    else
+      window_segment<0, 0, 0>(op, tid, nthr, sbuf, wsm, img, m, seg_end, h_lo, c0, bnc);
+    named_bar_sync(bar_id, nthr);   // smem free for the next segment
+    m = seg_end;
   }
 }
 
@@ -917,26 +1002,8 @@ __device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
   }
   const int HoWo = op.Ho * op.Wo;
   const int mb = it.mt * op.bm + tid / G;
-  if (!F32 && op.kind != DK_ELTWISE && op.kh == 3 && op.kw == 3 && (op.stride == 1 || op.stride == 2)) {
-    if (op.stride == 1) window_run_bf16<3, 3, 1>(op, it, tid, G, red);
-    else window_run_bf16<3, 3, 2>(op, it, tid, G, red);
-    return;
-  }
-  if (!F32 && op.kind != DK_ELTWISE && op.kh == 2 && op.kw == 2 && op.stride == 2) {
-    window_run_bf16<2, 2, 2>(op, it, tid, G, red);
-    return;
-  }
   if (c >= op.Cout) return;
-  if (!F32 && op.kind != DK_ELTWISE && op.kh * op.kw <= 9) {
-    // latency-bound window ops: two output pixels per step, all their tap
-    // loads issued back to back (branch-free, predicated), then reduced
-    for (int j = 0; j < CC_TASKS_PER_THREAD; j += 2) {
-      const int m0 = mb + j * pstep, m1 = m0 + pstep;
-      if (m0 >= op.M) break;
-      window2_bf16(op, m0, m1 < op.M ? m1 : -1, c, HoWo);
-    }
-    return;
-  }
+  // (bf16 window ops normally run as staged items, window_smem)
   for (int j = 0; j < CC_TASKS_PER_THREAD; ++j) {
     const int m = mb + j * pstep;
     if (m >= op.M) break;
@@ -1059,7 +1126,7 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
   atomicAdd(p.cluster_done + it.cluster, 1u);
   dbg_mark(p, 9);
   if (p.trace) {
-    int64_t* rec = p.trace + static_cast<size_t>(it.idx) * 10;
+    int64_t* rec = p.trace + static_cast<size_t>(it.idx) * TRACE_FIELDS;
     rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = it.idx;
     rec[4] = it.cluster; rec[5] = it.chunk;
     rec[6] = static_cast<int64_t>(t0); rec[7] = static_cast<int64_t>(globaltimer());
@@ -1088,7 +1155,7 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 // latency-critical item of a small op never queues behind several long tiles
 // of a big op (head-of-line blocking inside the CTA).
 __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
-  SmemCtl* ctl = cx.ctl;
+  SmemCtl* ctl = &g_ctl;
   uint32_t islot = 0, consumed = 0;
   int k = 0;
   int sidx = blockIdx.x;
@@ -1176,7 +1243,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
 }
 
 __device__ void worker_role(const ExecParams& p, Ctx& cx) {
-  SmemCtl* ctl = cx.ctl;
+  SmemCtl* ctl = &g_ctl;
   const int wtid = threadIdx.x - WORK_WARP0 * 32;  // 0..NWORK-1
   uint32_t g = 0, islot = 0;
   for (;;) {
@@ -1189,15 +1256,31 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
       if (wtid == 0) mbar_arrive(&ctl->rempty[slot]);
       break;
     }
-    const OpDev& op = p.ops[rs.it.op];
+    {  // stage the item's op descriptor in shared memory: the tile functions
+       // read its fields many times, and global re-loads would each be an L2
+       // round trip (L1 is invalidated by the other roles' gpu-scope fences)
+      constexpr int WORDS = static_cast<int>(sizeof(OpDev) / 4);
+      static_assert(WORDS <= NWORK, "OpDev staging");
+      if (wtid < WORDS)
+        reinterpret_cast<uint32_t*>(&ctl->wop)[wtid] = reinterpret_cast<const uint32_t*>(p.ops + rs.it.op)[wtid];
+      named_bar_sync(1, NWORK);
+    }
+    const OpDev& op = ctl->wop;
     if (rs.kind == DK_GEMM) {
       produce_gemm(op, rs.it, cx, g, wtid, p);
       if (wtid == 0) dbg_mark(p, 3);
       named_bar_sync(1, NWORK);
     } else {
       if (wtid == 0 && p.trace && p.single_op < 0)
-        p.trace[static_cast<size_t>(rs.it.idx) * 10 + 8] = static_cast<int64_t>(globaltimer());
-      run_cc(op, rs.it, wtid, ctl->red);
+        p.trace[static_cast<size_t>(rs.it.idx) * TRACE_FIELDS + 8] = static_cast<int64_t>(globaltimer());
+      if (op.win) {
+        // the staged window op borrows the GEMM smem ring: wait until the MMA
+        // has consumed every stage produced so far (MMAs complete in order)
+        if (g > 0) mbar_wait(&ctl->empty[(g - 1) % STAGES], ((g - 1) / STAGES) & 1);
+        window_smem(op, rs.it, wtid, NWORK, smem_u32(cx.ring), 1);
+      } else {
+        run_cc(op, rs.it, wtid, ctl->red);
+      }
       named_bar_sync(1, NWORK);
       if (wtid == 0 && p.single_op < 0) release_item(p, rs.it, rs.t0, op);
     }
@@ -1206,7 +1289,7 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
 }
 
 __device__ void mma_role(const ExecParams& p, Ctx& cx) {
-  SmemCtl* ctl = cx.ctl;
+  SmemCtl* ctl = &g_ctl;
   uint32_t g = 0, islot = 0, acc = 0;
   const uint32_t ring_base = smem_u32(cx.ring);
   for (;;) {
@@ -1228,17 +1311,20 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     const uint32_t d = cx.tmem + abuf * BN_MAX;
     const uint32_t idesc = make_idesc(op.bn);
     bool stamped = false;
+#pragma unroll 1
     for (int i = 0; i < nk; ++i) {
       const uint32_t stage = g % STAGES;
       mbar_wait(&ctl->full[stage], (g / STAGES) & 1);
+      kdbg(p, 0, g);
       if (i == 0) dbg_mark(p, 4);
       if (p.trace && !stamped && p.single_op < 0) {
-        p.trace[static_cast<size_t>(it.idx) * 10 + 8] = static_cast<int64_t>(globaltimer());
+        p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 8] = static_cast<int64_t>(globaltimer());
         stamped = true;
       }
       tc_fence_after();
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
+      if (!(p.dbg && (p.dbg_spin & 1)))   // diagnostics: odd dbg_spin skips the MMAs
 #pragma unroll
       for (int kk = 0; kk < BK / 16; ++kk)
         umma_bf16(d, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
@@ -1259,7 +1345,7 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
 // 64-byte-swizzled 32x64B smem chunk, and a TMA tensor store of that chunk
 // (coalesced; rows >= M and columns >= Cout clipped by the tensor map).
 __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
-  SmemCtl* ctl = cx.ctl;
+  SmemCtl* ctl = &g_ctl;
   const int etid = threadIdx.x - EPI_WARP0 * 32;  // 0..NEPI-1
   const int ew = etid >> 5, lane = etid & 31;
   const int q = ew & 3, hcol = ew >> 2;
@@ -1275,6 +1361,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     const uint64_t t0 = ctl->ring[slot].t0;
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->rempty[slot]);
+    if (etid == 0 && idx >= 0 && kind == DK_GEMM) edbg(p, 0, acc);
     ++islot;
     if (idx < 0) break;
     if (kind != DK_GEMM) continue;
@@ -1315,24 +1402,36 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
                                                        : make_uint4(0, 0, 0, 0);
     }
     named_bar_sync(2, NEPI);  // epi_scale / epi_bias visible
-    if (etid == 0) dbg_mark(p, 12);
+    if (etid == 0) { dbg_mark(p, 12); edbg(p, 1, acc); }
     const uint32_t abuf = acc & 1;
     mbar_wait(&ctl->tfull[abuf], (acc / 2) & 1);
-    if (etid == 0) dbg_mark(p, 6);
+    if (etid == 0) { dbg_mark(p, 6); kdbg(p, 2, 2 * acc); edbg(p, 2, acc); }
     if (etid == 0 && p.trace && p.single_op < 0)
-      p.trace[static_cast<size_t>(it.idx) * 10 + 9] = static_cast<int64_t>(globaltimer());
+      p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 9] = static_cast<int64_t>(globaltimer());
     tc_fence_after();
+    if (p.dbg && p.dbg_spin) {   // diagnostic: delay the TMEM read after tfull
+      const long long ts = clock64();
+      while (clock64() - ts < p.dbg_spin) {}
+    }
+    if (etid == 0) edbg(p, 11, acc);
     const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(q * 32) << 16);
     float* part = opg.partial + static_cast<size_t>(tile) * split * (BM * bn);
     const bool staged = op.c_tma && !swap;
     const int CW = op.out_f32 ? 32 : 64;          // columns per 128-byte staged row
-    if (split == 1) {
+    if (split == 1 && staged && !op.out_f32) {
+      const __nv_bfloat16* skr = do_skip ? skrow : nullptr;
+      epi_staged_bf16(taddr, c_lo, c_hi, cout_left, ctl->epi_scale, ctl->epi_bias, skr, op.act, wbuf_s, lane,
+                      op.tmap_c, n0, m0 + q * 32);
+      if (lane == 0) bulk_wait0();        // stores complete before the item is released
+      __syncwarp();
+    } else if (split == 1) {
       for (int c = c_lo; c < c_hi; c += 32) {
         uint32_t r[32];
+        if (etid == 0 && c == c_lo) edbg(p, 12, acc);
         tmem_ld16_nw(taddr + c, r);
         if (c + 16 < c_hi) tmem_ld16_nw(taddr + c + 16, r + 16);
         tmem_wait();
-        if (etid == 0) dbg_mark(p, 16);
+        if (etid == 0) { dbg_mark(p, 16); edbg(p, 3, acc); }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int cc = c + 32 + u * 8;
@@ -1355,20 +1454,20 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
             if (c + sub < c_hi) {
               float y[8];
               epi_math8(op, v + sub, ctl->epi_scale + c + sub, ctl->epi_bias + c + sub, skA[sub / 8], y);
-              stage8(wbuf, lane, cin + sub, y, op.out_f32);
+              stage8(wbuf_s, lane, cin + sub, y, op.out_f32);
               epi_math8(op, v + sub + 8, ctl->epi_scale + c + sub + 8, ctl->epi_bias + c + sub + 8, skA[sub / 8 + 1], y);
-              stage8(wbuf, lane, cin + sub + 8, y, op.out_f32);
+              stage8(wbuf_s, lane, cin + sub + 8, y, op.out_f32);
             }
           }
           if (cin + 32 == CW || c + 32 >= c_hi) {  // chunk complete: TMA-store it
-            if (etid == 0) dbg_mark(p, 17);
+            if (etid == 0) { dbg_mark(p, 17); edbg(p, 4, acc); }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
               tma_store_2d(op.tmap_c, wbuf_s, n0 + c - cin, m0 + q * 32);
               bulk_commit();
             }
-            if (etid == 0) dbg_mark(p, 18);
+            if (etid == 0) { dbg_mark(p, 18); edbg(p, 5, acc); }
           }
         } else {
 #pragma unroll
@@ -1379,9 +1478,10 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
         for (int u = 0; u < 4; ++u) skA[u] = skB[u];
       }
       if (staged) {
-        if (etid == 0) dbg_mark(p, 14);
+        if (etid == 0) { dbg_mark(p, 14); edbg(p, 6, acc); }
         if (lane == 0) bulk_wait0();        // stores complete before the item is released
         __syncwarp();
+        if (etid == 0) edbg(p, 8, acc);
       }
     } else {
       // partial layout [tile][ks][bn/4][BM] float4: a warp's 32 rows of one
@@ -1398,7 +1498,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
           if (c + u < c_hi) __stcg(mine + ((c + u) >> 2) * BM, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]));
       }
     }
-    if (etid == 0) dbg_mark(p, 13);
+    if (etid == 0) { dbg_mark(p, 13); edbg(p, 7, acc - 0); }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->tempty[abuf]);
@@ -1453,7 +1553,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
             if (staged) {
               float y[8];
               epi_math8(op, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8, y);
-              stage8(wbuf, lane, (c - c_lo) % CW, y, op.out_f32);
+              stage8(wbuf_s, lane, (c - c_lo) % CW, y, op.out_f32);
             } else {
               epilogue_store8(op, m, n0 + c, s8, ctl->epi_scale + c, ctl->epi_bias + c, k8);
             }
@@ -1473,9 +1573,11 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       }
     }
     fence_proxy_async_global();  // generic stores -> later TMA reads by consumers
-    if (etid == 0) dbg_mark(p, 15);
+    if (etid == 0) { dbg_mark(p, 15); kdbg(p, 2, 2 * acc - 1); edbg(p, 9, acc - 1); }
     named_bar_sync(2, NEPI);     // also: epi_scale/bias free for the next item
-    if (etid == 0) dbg_mark(p, 7);
+    if (etid == 0) { dbg_mark(p, 7); edbg(p, 10, acc - 1); }
+    if (etid == 0 && p.trace && p.single_op < 0)
+      p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 10] = static_cast<int64_t>(globaltimer());
     if (etid == 0 && p.single_op < 0) {   // hand the release to the releaser lane
       const uint32_t ls = nrel % ITEM_RING;
       if (nrel >= ITEM_RING) mbar_wait(&ctl->lempty[ls], ((nrel / ITEM_RING) + 1) & 1);
@@ -1501,7 +1603,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
 // lane's wait is an acquire, and __threadfence() makes the chain cumulative
 // at GPU scope before the counter atomics.
 __device__ void releaser_role(const ExecParams& p, Ctx& cx) {
-  SmemCtl* ctl = cx.ctl;
+  SmemCtl* ctl = &g_ctl;
   uint32_t n = 0;
   for (;;) {
     const uint32_t ls = n % ITEM_RING;
@@ -1519,8 +1621,8 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
   Ctx cx;
   cx.ring = base;
   cx.stage = base + SMEM_RING_BYTES;
-  cx.ctl = reinterpret_cast<SmemCtl*>(base + SMEM_RING_BYTES + SMEM_STAGE_BYTES);
-  SmemCtl* ctl = cx.ctl;
+  cx.ctl = &g_ctl;
+  SmemCtl* ctl = &g_ctl;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) {
     g_dbg_seen = 0;
@@ -1579,9 +1681,11 @@ extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor(ExecPar
 // Standalone CUDA-core op kernel (baselines): one item per CTA, same tile function.
 extern "C" __global__ void __launch_bounds__(CC_THREADS) op_cc_kernel(const OpDev* ops, int op_idx) {
   __shared__ __align__(16) float red[CC_THREADS * 8];
+  extern __shared__ __align__(1024) uint8_t win_buf[];
   const OpDev& op = ops[op_idx];
   const Item it = decode_single(op, op_idx, blockIdx.x);
-  run_cc(op, it, threadIdx.x, red);
+  if (op.win) window_smem(op, it, threadIdx.x, CC_THREADS, smem_u32(win_buf), 1);
+  else run_cc(op, it, threadIdx.x, red);
 }
 
 // =====================================================================
@@ -1590,7 +1694,10 @@ extern "C" __global__ void __launch_bounds__(CC_THREADS) op_cc_kernel(const OpDe
 int executor_smem_bytes() { return SMEM_BYTES; }
 
 cudaError_t configure_kernels() {
-  return cudaFuncSetAttribute(gacer_executor, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  static_assert(WIN_SMEM_BYTES <= SMEM_RING_BYTES, "window staging must fit in the GEMM ring");
+  cudaError_t e = cudaFuncSetAttribute(gacer_executor, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(op_cc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIN_SMEM_BYTES);
 }
 
 cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s) {
@@ -1612,7 +1719,7 @@ cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, 
     const int grid = n_items < num_sms ? n_items : num_sms;
     gacer_executor<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
   } else {
-    op_cc_kernel<<<n_items, CC_THREADS, 0, s>>>(ops_dev, op_idx);
+    op_cc_kernel<<<n_items, CC_THREADS, WIN_SMEM_BYTES, s>>>(ops_dev, op_idx);
   }
   return cudaGetLastError();
 }

@@ -25,6 +25,7 @@ constexpr int BM = 128;           // rows per tile (UMMA M)
 constexpr int BK = 64;            // bf16 elements per K-block = one 128-byte swizzle row
 constexpr int BN_MAX = 256;       // max UMMA N per tile
 constexpr int STAGES = 4;         // smem ring depth (A 16 KB + B 32 KB per stage)
+constexpr int NPROD = 4;          // TMA-issuing producer threads per CTA (lane 0 of worker warps 0..3)
 constexpr int ITEM_RING = 4;      // scheduler -> MMA/epilogue item queue depth
 // warp roles of the executor CTA (16 warps; 4 per SM sub-partition, <= 128 registers)
 constexpr int SCHED_WARP = 0;     // warp 0: scheduler (lane 0) -- claims ready items into the item ring
@@ -41,6 +42,8 @@ constexpr int MAX_SPLIT = 4;      // split-K factor cap (fixed per layer shape)
 constexpr int LOOKAHEAD = 3;      // max claimed items not yet picked up by every role (per CTA)
 constexpr int INLINE_DEPS = 4;    // dependencies stored inside the Item
 constexpr int MAX_SMEM_SEGS = 256;
+constexpr int WIN_IN_BYTES = 96 * 1024;   // window_smem: staged input rows of one image segment
+constexpr int WIN_SMEM_BYTES = WIN_IN_BYTES + (9 + 2) * 64 * 4 + 1024;  // + dw weights/scale/bias (kh*kw <= 9)
 
 // operand A load mode of a GEMM op
 enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2 };
@@ -65,7 +68,7 @@ struct OpDev {
   const void* skip;
   int32_t lds, pad0;
 
-  int32_t kh, kw, stride, ph, pw, pad1;
+  int32_t kh, kw, stride, ph, pw, win; // win: 1 = window op staged through shared memory (window_smem)
 
   // GEMM view
   int32_t M, N, K;         // conv: M = B*Ho*Wo, N = Cout, K = kh*kw*C;  swap: M = Cout, N = B, K = C_flat
@@ -134,7 +137,11 @@ struct ExecParams {
   int32_t single_op;        // >= 0: standalone mode, run every tile of this op (strided over CTAs)
   int32_t own_first;        // 1: the CTA's own tenant (pref[0]) wins over higher-ranked items
   int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
+  int64_t dbg_spin;         // diagnostics: epilogue delay (clocks) between tfull and the TMEM read
 };
 constexpr int DBG_EVENTS = 24;
+// trace record per item: tenant, op, smid, idx, cluster, chunk, t_claim,
+// t_release, t_start, t_acc_ready (GEMM), t_epilogue_done (GEMM), reserved
+constexpr int TRACE_FIELDS = 12;
 
 }  // namespace gacer

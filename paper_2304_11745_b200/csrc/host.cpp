@@ -89,6 +89,7 @@ struct FusedOp {
   int Cin = 0, H = 0, W = 0, Cout = 0, Ho = 0, Wo = 0;
   int kh = 1, kw = 1, stride = 1, ph = 0, pw = 0;
   int cread = 0;  // channels read per tap (K = kh*kw*cread)
+  bool win = false;  // window op staged through shared memory
   int M = 0, N = 0, K = 0, Kpad = 0, tiles_m = 1, tiles_n = 1, bm = 0, bn = 0, split_k = 1, nkb = 0;
   bool cip = true;
   // packed params (host)
@@ -618,6 +619,12 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           const bool tma = c64 == c8 || F.kh * F.kw == 1 || 2 * c64 <= 3 * c8;
           F.a_mode = F.swap ? A_ROWS : (tma ? A_IM2COL : A_GATHER);
           F.cread = (F.a_mode == A_IM2COL) ? c64 : c8;
+          // 1x1 stride-1 conv over a dense NHWC tensor is a plain GEMM: tiled TMA rows
+          if (!F.swap && F.kh * F.kw == 1 && F.stride == 1 && o.pad_h == 0 && o.pad_w == 0 && c64 == c8 &&
+              !getenv("GACER_IM2COL_1X1")) {
+            F.a_mode = A_ROWS;
+            F.cread = c64;
+          }
         }
         if (F.in_t == 0 && F.a_mode == A_GATHER && F.cread > X.ldc)
           return set_err(GACER_E_UNSUPPORTED_OP, "input padding");
@@ -685,12 +692,25 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
     if (F.kind != DK_GEMM && F.kind != DK_SIMT_GEMM) {
       F.bn = std::min(64, pow2ceil(roundup(F.Cout, 8)));
       const int G = F.bn / 8;
-      const bool run = F.kind != DK_GAP && F.kind != DK_ELTWISE && !f32 &&
-                       ((F.kh == 3 && F.kw == 3 && (F.stride == 1 || F.stride == 2)) ||
-                        (F.kh == 2 && F.kw == 2 && F.stride == 2));
-      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : (run ? CC_RUN : CC_TASKS_PER_THREAD) * (CC_THREADS / G);
-      F.tiles_m = cdiv(F.M, F.bm);
+      F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : CC_TASKS_PER_THREAD * (CC_THREADS / G);
       F.tiles_n = cdiv(F.Cout, F.bn);
+      // bf16 window ops (depthwise / max / avg pool, <= 9 taps): items of R
+      // whole output rows whose input rows are staged in shared memory
+      // (window_smem); R from the staging budget and >= ~2 items per SM
+      F.win = false;
+      if (!f32 && (F.kind == DK_DW || F.kind == DK_MAXPOOL || F.kind == DK_AVGPOOL) && F.kh * F.kw <= 9) {
+        const long long row_bytes = static_cast<long long>(F.W) * F.bn * 2;
+        const long long rows_fit = WIN_IN_BYTES / row_bytes;   // input rows that fit
+        if (rows_fit >= F.kh) {
+          const int r_max = static_cast<int>((rows_fit - F.kh) / F.stride + 1);
+          const long long out_rows = static_cast<long long>(B) * F.Ho;
+          const int r_par = static_cast<int>(std::max<long long>(1, out_rows * F.tiles_n / (2 * kSplitSms)));
+          const int R = std::max(1, std::min(r_max, r_par));
+          F.bm = R * F.Wo;
+          F.win = true;
+        }
+      }
+      F.tiles_m = cdiv(F.M, F.bm);
       F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
       F.bias.resize(roundup(F.Cout, 8) + 8, 0.0f);
     }
@@ -778,6 +798,7 @@ OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
   d.Ho = F.Ho; d.Wo = F.Wo; d.Cout = F.Cout; d.ldo = Y.ldc;
   if (F.skip_t >= 0) { d.skip = tensor_addr(T, F.skip_t); d.lds = T.tensors[F.skip_t].ldc; }
   d.kh = F.kh; d.kw = F.kw; d.stride = F.stride; d.ph = F.ph; d.pw = F.pw;
+  d.win = F.win ? 1 : 0;
   d.M = F.M; d.N = F.N; d.K = F.K; d.Kpad = F.Kpad;
   d.tiles_m = F.tiles_m; d.tiles_n = F.tiles_n; d.bm = F.bm; d.bn = F.bn;
   d.split_k = F.split_k; d.nkb = F.nkb;
@@ -877,6 +898,7 @@ int rebuild_op_table() {
       if (!rc) rc = encode_rows(&maps[3 * i + 1], d.act_b, d.K, d.B, d.ldb, d.bn);
     } else {
       if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[3 * i], d, F.Cin);
+      else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[3 * i], d.in, d.K, d.M, d.ldi, BM);
       if (!rc) rc = encode_rows(&maps[3 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
       // output [M][Cout] (row stride ldo) for the TMA-store epilogue
       const int esz = d.out_f32 ? 4 : 2;
@@ -909,6 +931,14 @@ struct ChunkRange {
   int m0, m1, n0, n1;  // tile ranges
   int counter;
   uint32_t n_items;
+  // Completion counters at M-tile granularity (ops whose M axis is output
+  // pixels or samples): mc[mt - m0] counts the items of M-tile mt in this
+  // chunk (target mc_items).  A consumer waits only for the producer tiles
+  // its input window reads, so consecutive ops of a chain overlap (a
+  // wavefront) instead of meeting at whole-op barriers.  Chunk semantics
+  // (Eq. 5) are unchanged: this only refines the dependency bookkeeping.
+  std::vector<int> mc;
+  uint32_t mc_items = 0;
 };
 
 int cluster_of_orig(const Plan& P, int t, int orig0) {  // orig0: 0-based op index
@@ -971,7 +1001,14 @@ int compile_plan(Plan& P) {
       }
       for (ChunkRange& r : ranges) {
         r.n_items = static_cast<uint32_t>(std::max(0, r.m1 - r.m0) * std::max(0, r.n1 - r.n0) * split);
-        r.counter = r.n_items ? counter++ : -1;
+        r.counter = -1;
+        if (!r.n_items) continue;
+        if (F.rows_are_pixels && !S.opts.coarse_deps) {
+          r.mc_items = static_cast<uint32_t>((r.n1 - r.n0) * split);
+          for (int mt = r.m0; mt < r.m1; ++mt) r.mc.push_back(counter++);
+        } else {
+          r.counter = counter++;
+        }
       }
     }
   }
@@ -1008,7 +1045,11 @@ int compile_plan(Plan& P) {
       // the delay by filling whatever SMs the chains leave free.
       wk[f] = items * item_ns / kSplitSms;  // work, as full-GPU time
       (void)waves;
-      est[f] = 10000.0 + item_ns;
+      // HEFT upward rank: the op's duration with the whole GPU (its work
+      // spread over every SM, but never below one item) plus a per-op
+      // latency floor.  A chain of few but wide ops (VGG-16) is then ranked
+      // by its real length instead of its op count.
+      est[f] = 10000.0 + std::max(item_ns, wk[f]);
     }
     for (size_t f = nf; f-- > 0;) {
       double best = 0.0;
@@ -1046,37 +1087,65 @@ int compile_plan(Plan& P) {
         if (!r.n_items) continue;
         for (int mt = r.m0; mt < r.m1; ++mt)
           for (int ntile = r.n0; ntile < r.n1; ++ntile) {
-            // samples this tile needs
-            int s_lo, s_hi;
+            // input rows this tile reads, as a flattened row range of each
+            // input tensor: pixels (b*H + h)*W + w, or samples for [B][C] rows
+            long long s_lo, s_hi;   // samples
+            long long px_lo = -1, px_hi = -1;  // input pixels of in_t (-1: whole samples)
             if (F.rows_are_pixels) {
               const long long R = (F.kind == DK_GAP) ? 1 : static_cast<long long>(F.Ho) * F.Wo;
               const long long r0 = static_cast<long long>(mt) * F.bm;
               const long long r1 = std::min<long long>(F.M, r0 + F.bm);
-              s_lo = static_cast<int>(r0 / R);
-              s_hi = static_cast<int>((r1 - 1) / R);
+              s_lo = r0 / R;
+              s_hi = (r1 - 1) / R;
+              if (F.kind != DK_GAP) {
+                const long long HW = static_cast<long long>(F.H) * F.W;
+                const long long ho0 = (r0 % R) / F.Wo, ho1 = ((r1 - 1) % R) / F.Wo;
+                const long long h_lo = std::max<long long>(0, ho0 * F.stride - F.ph);
+                const long long h_hi = std::min<long long>(F.H - 1, ho1 * F.stride - F.ph + F.kh - 1);
+                px_lo = s_lo * HW + h_lo * F.W;
+                px_hi = s_hi * HW + h_hi * F.W + F.W - 1;
+              }
             } else {
-              s_lo = ntile * F.bn;
-              s_hi = std::min(T.batch, (ntile + 1) * F.bn) - 1;
+              s_lo = static_cast<long long>(ntile) * F.bn;
+              s_hi = std::min<long long>(T.batch, static_cast<long long>(ntile + 1) * F.bn) - 1;
             }
             std::set<int> dset;
             std::vector<Dep> dl;
             for (int tin : {F.in_t, F.skip_t}) {
               if (tin < 0) continue;
+              const Tensor& X = T.tensors[tin];
+              const long long XHW = static_cast<long long>(X.H) * X.W;
+              // flattened row range [lo, hi] of tensor tin this tile reads
+              long long lo = s_lo * XHW, hi = (s_hi + 1) * XHW - 1;
+              if (tin == F.skip_t && F.rows_are_pixels && F.kind != DK_GAP) {
+                lo = static_cast<long long>(mt) * F.bm;   // residual: same pixels as the output
+                hi = std::min<long long>(F.M, lo + F.bm) - 1;
+              } else if (px_lo >= 0) {
+                lo = px_lo;
+                hi = px_hi;
+              }
               for (int w : T.tensors[tin].writers) {
                 const FusedOp& Wf = T.fops[w];
                 int wm0 = 0, wm1 = Wf.tiles_m, wn0 = 0, wn1 = Wf.tiles_n;
                 if (Wf.rows_are_pixels) {
-                  const long long R = (Wf.kind == DK_GAP) ? 1 : static_cast<long long>(Wf.Ho) * Wf.Wo;
-                  wm0 = static_cast<int>((s_lo * R) / Wf.bm);
-                  wm1 = static_cast<int>(((s_hi + 1) * R - 1) / Wf.bm) + 1;
+                  // producer rows are tin's pixels (or samples for GAP, XHW == 1)
+                  wm0 = static_cast<int>(lo / Wf.bm);
+                  wm1 = static_cast<int>(hi / Wf.bm) + 1;
                 } else {
-                  wn0 = s_lo / Wf.bn;
-                  wn1 = s_hi / Wf.bn + 1;
+                  wn0 = static_cast<int>((lo / XHW) / Wf.bn);
+                  wn1 = static_cast<int>((hi / XHW) / Wf.bn) + 1;
                 }
                 for (const ChunkRange& q : cr[t][w]) {
                   if (!q.n_items) continue;
                   if (q.m1 <= wm0 || q.m0 >= wm1 || q.n1 <= wn0 || q.n0 >= wn1) continue;
-                  if (dset.insert(q.counter).second) dl.push_back({q.counter, q.n_items});
+                  if (q.mc.empty()) {
+                    if (dset.insert(q.counter).second) dl.push_back({q.counter, q.n_items});
+                  } else {
+                    for (int pm = std::max(q.m0, wm0); pm < std::min(q.m1, wm1); ++pm) {
+                      const int c = q.mc[pm - q.m0];
+                      if (dset.insert(c).second) dl.push_back({c, q.mc_items});
+                    }
+                  }
                 }
               }
             }
@@ -1094,7 +1163,7 @@ int compile_plan(Plan& P) {
               it.dep_count = static_cast<int>(dl.size());
               if (dl.size() <= static_cast<size_t>(INLINE_DEPS))
                 for (size_t d = 0; d < dl.size(); ++d) { it.dc[d] = dl[d].counter; it.dt[d] = dl[d].target; }
-              it.chunk = r.counter;
+              it.chunk = r.mc.empty() ? r.counter : r.mc[mt - r.m0];
               it.cluster = k;
               it.prio = rank[t][f];
               seg_items[t][k].push_back(static_cast<int32_t>(P.items.size()));
@@ -1196,8 +1265,8 @@ int upload_plan() {
   if (!S.d_error && (rc = dev_upload<int32_t>(&S.d_error, nullptr, 1))) return rc;
   if (S.d_trace) { cudaFree(S.d_trace); S.d_trace = nullptr; }
   if (S.opts.trace) {
-    CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * 10 * sizeof(int64_t)));
-    CUDA_TRY(cudaMemset(S.d_trace, 0, P.items.size() * 10 * sizeof(int64_t)));
+    CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * TRACE_FIELDS * sizeof(int64_t)));
+    CUDA_TRY(cudaMemset(S.d_trace, 0, P.items.size() * TRACE_FIELDS * sizeof(int64_t)));
   }
   S.epoch = 0;
   return 0;
@@ -1251,6 +1320,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     p.single_op = -1;
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
     p.dbg = S.d_dbg;
+    if (const char* e = getenv("GACER_DBG_SPIN")) p.dbg_spin = atoll(e);
     CUDA_TRY(launch_executor(p, S.grid, st));
     launches = 1;
   } else {
@@ -1277,6 +1347,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
         base.error = S.d_error;
         base.watchdog_ns = 2000000000LL;
         base.dbg = S.d_dbg;
+        if (const char* e = getenv("GACER_DBG_SPIN")) base.dbg_spin = atoll(e);
         CUDA_TRY(launch_op(base, S.d_ops, T.op_base + static_cast<int>(f), F.kind, nb, S.num_sms, ts));
         ++launches;
       }
@@ -1572,7 +1643,7 @@ int gacer_get_trace(int64_t* records, int32_t cap) {
   if (!S.inited || S.host_only || !S.d_trace) return set_err(GACER_E_STATE, "tracing not enabled");
   if (!records || cap < 0) return set_err(GACER_E_INVALID_ARG, "bad buffer");
   const size_t n = std::min<size_t>(cap, S.plan.items.size());
-  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * 10 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(records, S.d_trace, n * TRACE_FIELDS * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return static_cast<int>(n);
 }
 

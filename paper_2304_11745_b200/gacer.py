@@ -73,7 +73,7 @@ class gacer_sync_pointers(C.Structure):
 
 class gacer_options(C.Structure):
     _fields_ = [("num_ctas", C.c_int32), ("partition", C.c_int32), ("watchdog_ms", C.c_int32),
-                ("trace", C.c_int32)]
+                ("trace", C.c_int32), ("coarse_deps", C.c_int32)]
 
 
 class gacer_round_stats(C.Structure):
@@ -228,9 +228,9 @@ def regulation_desc(decomposition=None, pointers=None, n_tenants=None):
 
 
 # ---------------------------------------------------------------- calls
-def gacer_init(device=0, num_ctas=0, partition="priority", watchdog_ms=0, trace=False):
+def gacer_init(device=0, num_ctas=0, partition="priority", watchdog_ms=0, trace=False, coarse_deps=False):
     o = gacer_options(num_ctas=num_ctas, partition=PARTITION[partition], watchdog_ms=watchdog_ms,
-                      trace=int(trace))
+                      trace=int(trace), coarse_deps=int(coarse_deps))
     return _check(lib().gacer_init(device, C.byref(o)))
 
 
@@ -301,7 +301,7 @@ def gacer_get_stats():
 
 
 def gacer_get_trace(cap):
-    buf = np.zeros((cap, 10), dtype=np.int64)
+    buf = np.zeros((cap, 12), dtype=np.int64)
     n = _check(lib().gacer_get_trace(buf.ctypes.data_as(C.POINTER(C.c_int64)), cap))
     return buf[:n]
 

@@ -27,11 +27,12 @@ class Session:
     """One GACER instance on one GPU with its registered tenants."""
 
     def __init__(self, tenants, device=0, num_ctas=0, partition="priority",
-                 watchdog_ms=0, trace=False):
+                 watchdog_ms=0, trace=False, coarse_deps=False):
         """tenants: list of (graph, params, batch, dtype)."""
         self.device = device
         torch.cuda.set_device(device)
-        G.gacer_init(device, num_ctas=num_ctas, partition=partition, watchdog_ms=watchdog_ms, trace=trace)
+        G.gacer_init(device, num_ctas=num_ctas, partition=partition, watchdog_ms=watchdog_ms, trace=trace,
+                     coarse_deps=coarse_deps)
         self.tenants = []
         self.inputs, self.outputs, self.info = [], [], []
         for graph, params, batch, dtype in tenants:

@@ -78,7 +78,8 @@ def test_bitwise_across_plans_and_modes(cuda_ok, d2):
     ref, _ = run(d2)
     variants = [dict(mode="sequential"), dict(mode="multistream"),
                 dict(partition="strict"), dict(partition="work_conserving"), dict(partition="hybrid"),
-                dict(num_ctas=37), dict(num_ctas=296)]
+                dict(num_ctas=37), dict(num_ctas=296), dict(coarse_deps=True),
+                dict(coarse_deps=True, partition="strict")]
     rng = np.random.default_rng(12345)
     for k in range(6):
         variants.append(dict(plan=random_plan(d2, rng, n_pointers=k % 4)))
@@ -98,13 +99,22 @@ def test_trace_respects_clusters_and_chain(cuda_ok, d2):
     for k in range(int(cl.max())):
         if np.any(cl == k) and np.any(cl == k + 1):
             assert t0[cl == k + 1].min() >= t1[cl == k].max(), k
-    # identity plan: VGG-16 is a chain, so every item of fused op f+1 starts
-    # after every item of fused op f has ended
-    _, tr = run(d2, trace=True)
+    # identity plan with op-level dependencies (coarse_deps): VGG-16 is a
+    # chain, so every item of fused op f+1 starts after every item of fused
+    # op f has ended
+    _, tr = run(d2, trace=True, coarse_deps=True)
     vgg = tr[tr[:, 0] == 1]
     ops = np.unique(vgg[:, 1])
     for a, b in zip(ops, ops[1:]):
         assert vgg[vgg[:, 1] == b, 6].min() >= vgg[vgg[:, 1] == a, 7].max()
+    # tile-level dependencies (default): consecutive ops may overlap, but no
+    # item of op f+1 starts before some item of op f has ended, and op f+1
+    # cannot finish before op f
+    _, tr = run(d2, trace=True)
+    vgg = tr[tr[:, 0] == 1]
+    for a, b in zip(ops, ops[1:]):
+        assert vgg[vgg[:, 1] == b, 6].min() >= vgg[vgg[:, 1] == a, 7].min()
+        assert vgg[vgg[:, 1] == b, 7].max() >= vgg[vgg[:, 1] == a, 7].max()
 
 
 def test_full_size_sampled_parity(cuda_ok, d2):
