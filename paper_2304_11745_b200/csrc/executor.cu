@@ -178,6 +178,14 @@ __device__ __forceinline__ void edbg(const ExecParams& p, int point, uint32_t ac
   if (p.dbg && blockIdx.x == 0 && acc < 8) p.dbg[KDBG_OFF + 768 + acc * 16 + point] = static_cast<int64_t>(clock64());
 }
 
+// gpu-scope fences.  __threadfence() is fence.sc.gpu: MEMBAR.SC.GPU plus an
+// L1 invalidation (CCTL.IVALL) of the whole SM.  A release needs only
+// MEMBAR.ALL.GPU and an acquire only the invalidation, so each side uses its
+// own fence: completions no longer flush the co-resident warps' L1 working
+// set (spills, op fields, residual rows).
+__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.release.gpu;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;\n" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -304,7 +312,10 @@ struct SmemCtl {
   OpDev wop;                 // the worker group's current op (staged once per item)
 };
 constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 rows x 128 B per warp (SW128)
-constexpr int SMEM_STAGE_BYTES = (NEPI / 32) * STAGE_WARP_BYTES;
+// TMA-store staging only with 4 epilogue warps: 8 warps' staging rows do not
+// fit beside the ring; they store their rows directly (16 B per thread)
+constexpr bool EPI_STAGED = NEPI == 128;
+constexpr int SMEM_STAGE_BYTES = EPI_STAGED ? (NEPI / 32) * STAGE_WARP_BYTES : 0;
 constexpr int SMEM_BYTES = SMEM_RING_BYTES + SMEM_STAGE_BYTES + 1024 /*align slack*/;
 // The control block is a static __shared__ object (not carved from the
 // dynamic buffer) so every access compiles to LDS/STS instead of generic
@@ -346,6 +357,30 @@ __device__ __forceinline__ void epi_math8(const EpiOp& op, const float* v, const
   for (int j = 0; j < 8; j += 2) {   // packed FFMA2: two IEEE fmas, same results as fmaf
     const float2 r = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc[j], sc[j + 1]),
                                 make_float2(bi[j], bi[j + 1]));
+    y[j] = r.x;
+    y[j + 1] = r.y;
+  }
+  if (op.has_skip) {
+    float s[8];
+    bf16x8_to_f32(skip8, s);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] += s[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) y[j] = apply_act(y[j], op.act);
+}
+
+// y = act(v*scale + bias [+ skip]) for 8 columns whose scale/bias live in
+// lanes j0..j0+7 of (sc_l, bi_l): broadcast by warp shuffles instead of
+// shared-memory loads (the smem port is saturated by the TMA fills and the
+// tensor-core operand reads of the next tile).  Same IEEE ops as epi_math8.
+__device__ __forceinline__ void epi_math8_shfl(const EpiOp& op, const float* v, float sc_l, float bi_l, int j0,
+                                               const uint4& skip8, float* y) {
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float s0 = __shfl_sync(0xffffffffu, sc_l, j0 + j), s1 = __shfl_sync(0xffffffffu, sc_l, j0 + j + 1);
+    const float b0 = __shfl_sync(0xffffffffu, bi_l, j0 + j), b1 = __shfl_sync(0xffffffffu, bi_l, j0 + j + 1);
+    const float2 r = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(s0, s1), make_float2(b0, b1));
     y[j] = r.x;
     y[j + 1] = r.y;
   }
@@ -415,93 +450,6 @@ __device__ __forceinline__ void epilogue_store8(const EpiOp& op, int m, int n, c
       if (op.out_f32) static_cast<float*>(op.out)[static_cast<size_t>(m) * op.ldo + n + j] = y[j];
       else static_cast<__nv_bfloat16*>(op.out)[static_cast<size_t>(m) * op.ldo + n + j] = __float2bfloat16_rn(y[j]);
     }
-  }
-}
-
-// Staged bf16 epilogue of one warp's 32 accumulator rows (split-K 1, not
-// swap-AB): the TMEM load of the next 32 columns is in flight while the
-// current 32 are converted -- y = clamp(acc*scale + bias [+ skip], lo, hi)
-// with FFMA2 (lo/hi encode the activation: none = (-inf, inf), ReLU =
-// (0, inf), ReLU6 = (0, 6); same IEEE ops as apply_act), RNE to bf16 --
-// written 128B-swizzled to the warp's staging rows and TMA-stored per 64
-// columns.  One instantiation (runtime act/skip): several inlined variants
-// overflow the 168-register budget.
-__device__ __forceinline__ void epi_chunk_bf16(const uint32_t* r, int c, int c_lo, int c_hi, const float* esc,
-                                               const float* ebi, bool skip, const uint4* sk, float lo, float hi,
-                                               uint32_t wbuf_s, int lane, const void* tmap_c, int n0, int row0) {
-  const int cin = (c - c_lo) & 63;         // column offset inside the staged 64-column chunk
-  if (cin == 0 && c > c_lo) {              // new chunk: the previous store must have read the buffer
-    if (lane == 0) bulk_wait_read0();
-    __syncwarp();
-  }
-#pragma unroll
-  for (int g8 = 0; g8 < 4; ++g8) {
-    const int cc = c + g8 * 8;
-    float y[8];
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[g8 * 8 + j]), __uint_as_float(r[g8 * 8 + j + 1])),
-                                  make_float2(esc[cc + j], esc[cc + j + 1]), make_float2(ebi[cc + j], ebi[cc + j + 1]));
-      y[j] = o.x;
-      y[j + 1] = o.y;
-    }
-    if (skip) {
-      float sv[8];
-      bf16x8_to_f32(sk[g8], sv);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) y[j] += sv[j];
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
-    const int jj = ((cin + g8 * 8) * 2) >> 4;   // 16-byte chunk in the 128-byte row
-    sts128(wbuf_s + lane * 128 + ((jj ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
-           pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
-  }
-  if (cin == 32 || c + 32 >= c_hi) {       // chunk complete: TMA-store it
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(tmap_c, wbuf_s, n0 + c - cin, row0);
-      bulk_commit();
-    }
-  }
-}
-
-__device__ __forceinline__ void epi_load_skip(uint4* dst, const __nv_bfloat16* skrow, int c, int c_hi, int cout_left) {
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int cc = c + u * 8;
-    dst[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
-  }
-}
-
-__device__ __forceinline__ void epi_staged_bf16(uint32_t taddr, int c_lo, int c_hi, int cout_left, const float* esc,
-                                                const float* ebi, const __nv_bfloat16* skrow, int act,
-                                                uint32_t wbuf_s, int lane, const void* tmap_c, int n0, int row0) {
-  const float lo = act == ACT_NONE ? -INFINITY : 0.0f;
-  const float hi = act == ACT_RELU6 ? 6.0f : INFINITY;
-  const bool skip = skrow != nullptr;
-  uint32_t ra[32], rb[32];
-  uint4 ska[4], skb[4];
-  tmem_ld32_nw(taddr + c_lo, ra);
-  if (skip) epi_load_skip(ska, skrow, c_lo, c_hi, cout_left);
-#pragma unroll 1
-  for (int c = c_lo; c < c_hi; c += 64) {
-    tmem_wait();
-    tmem_pin32(ra);
-    if (c + 32 < c_hi) {
-      tmem_ld32_nw(taddr + c + 32, rb);
-      if (skip) epi_load_skip(skb, skrow, c + 32, c_hi, cout_left);
-    }
-    epi_chunk_bf16(ra, c, c_lo, c_hi, esc, ebi, skip, ska, lo, hi, wbuf_s, lane, tmap_c, n0, row0);
-    if (c + 32 >= c_hi) break;
-    tmem_wait();
-    tmem_pin32(rb);
-    if (c + 64 < c_hi) {
-      tmem_ld32_nw(taddr + c + 64, ra);
-      if (skip) epi_load_skip(ska, skrow, c + 64, c_hi, cout_left);
-    }
-    epi_chunk_bf16(rb, c + 32, c_lo, c_hi, esc, ebi, skip, skb, lo, hi, wbuf_s, lane, tmap_c, n0, row0);
   }
 }
 
@@ -1040,7 +988,7 @@ __device__ __forceinline__ Item decode_single(const OpDev& op, int op_idx, int b
 __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& p) {
   // relaxed polling (an acquire load invalidates the SM's L1 on every poll,
   // evicting the co-resident warps' working set); one fence on success
-  if (ld_relaxed(ctr) >= target) { __threadfence(); return true; }
+  if (ld_relaxed(ctr) >= target) { fence_acquire_gpu(); return true; }
   const uint64_t t0 = globaltimer();
   uint32_t it = 0, ns = 32;
   while (ld_relaxed(ctr) < target) {
@@ -1054,7 +1002,7 @@ __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& 
       }
     }
   }
-  __threadfence();
+  fence_acquire_gpu();
   return true;
 }
 
@@ -1119,8 +1067,9 @@ __device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& b
 }
 
 __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, uint64_t t0, const OpDev& op) {
-  // caller: all writes of the item are ordered before this thread (barrier)
-  __threadfence();
+  // caller: all writes of the item are ordered before this thread (barrier);
+  // the release fence makes them visible at gpu scope before the counters
+  fence_release_gpu();
   dbg_mark(p, 8);
   atomicAdd(p.chunk_done + it.chunk, 1u);
   atomicAdd(p.cluster_done + it.cluster, 1u);
@@ -1227,7 +1176,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         claimed = sg.begin + static_cast<int>(idx);
         last_op = it.op;
       }
-      if (claimed >= 0) __threadfence();  // acquire side (pairs with the producers' release)
+      if (claimed >= 0) fence_acquire_gpu();  // acquire side (pairs with the producers' release)
     }
     dbg_mark(p, 1);
     const uint32_t slot = islot % ITEM_RING;  // free: islot - consumed < LOOKAHEAD < ITEM_RING
@@ -1416,12 +1365,72 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     if (etid == 0) edbg(p, 11, acc);
     const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(q * 32) << 16);
     float* part = opg.partial + static_cast<size_t>(tile) * split * (BM * bn);
-    const bool staged = op.c_tma && !swap;
+    const bool staged = EPI_STAGED && op.c_tma && !swap;
     const int CW = op.out_f32 ? 32 : 64;          // columns per 128-byte staged row
     if (split == 1 && staged && !op.out_f32) {
-      const __nv_bfloat16* skr = do_skip ? skrow : nullptr;
-      epi_staged_bf16(taddr, c_lo, c_hi, cout_left, ctl->epi_scale, ctl->epi_bias, skr, op.act, wbuf_s, lane,
-                      op.tmap_c, n0, m0 + q * 32);
+      // lean staged bf16 path: branch-free activation clamp, 64-column
+      // staging chunks (a compile-time constant), scale/bias by shuffle
+      const float lo = op.act == ACT_NONE ? -INFINITY : 0.0f;
+      const float hi = op.act == ACT_RELU6 ? 6.0f : INFINITY;
+      const bool skip = do_skip;
+      const int row0 = m0 + q * 32;
+      for (int c = c_lo; c < c_hi; c += 32) {
+        uint32_t r[32];
+        tmem_ld16_nw(taddr + c, r);
+        tmem_ld16_nw(taddr + c + 16, r + 16);   // c + 32 <= BN_MAX: columns past c_hi are never stored
+        const float sc_l = ctl->epi_scale[c + lane], bi_l = ctl->epi_bias[c + lane];
+        if (skip) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cc = c + 32 + u * 8;
+            skB[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
+          }
+        }
+        const int cin = (c - c_lo) & 63;
+        if (cin == 0 && c > c_lo) {            // a new chunk: wait until the last store read the buffer
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
+        tmem_wait();
+#pragma unroll
+        for (int g8 = 0; g8 < 4; ++g8) {
+          float y[8];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const int jj = g8 * 8 + j;
+            const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1])),
+                                        make_float2(__shfl_sync(0xffffffffu, sc_l, jj), __shfl_sync(0xffffffffu, sc_l, jj + 1)),
+                                        make_float2(__shfl_sync(0xffffffffu, bi_l, jj), __shfl_sync(0xffffffffu, bi_l, jj + 1)));
+            y[j] = o.x;
+            y[j + 1] = o.y;
+          }
+          if (skip) {
+            float sv[8];
+            bf16x8_to_f32(skA[g8], sv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] += sv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
+          const uint32_t ch = static_cast<uint32_t>((cin + g8 * 8) >> 3);   // 16-byte chunk of the 128-byte row
+          sts128(wbuf_s + lane * 128 + ((ch ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+                 pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+        }
+        if (cin == 32 || c + 32 >= c_hi) {     // 64-column chunk complete: TMA-store it
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(op.tmap_c, wbuf_s, n0 + c - cin, row0);
+            bulk_commit();
+          }
+        }
+        if (skip) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) skA[u] = skB[u];
+        }
+      }
+      if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
+        p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
       if (lane == 0) bulk_wait0();        // stores complete before the item is released
       __syncwarp();
     } else if (split == 1) {
@@ -1449,13 +1458,14 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
           }
+          const float sc_l = ctl->epi_scale[c + lane], bi_l = ctl->epi_bias[c + lane];  // one LDS per lane
 #pragma unroll
           for (int sub = 0; sub < 32; sub += 16) {
             if (c + sub < c_hi) {
               float y[8];
-              epi_math8(op, v + sub, ctl->epi_scale + c + sub, ctl->epi_bias + c + sub, skA[sub / 8], y);
+              epi_math8_shfl(op, v + sub, sc_l, bi_l, sub, skA[sub / 8], y);
               stage8(wbuf_s, lane, cin + sub, y, op.out_f32);
-              epi_math8(op, v + sub + 8, ctl->epi_scale + c + sub + 8, ctl->epi_bias + c + sub + 8, skA[sub / 8 + 1], y);
+              epi_math8_shfl(op, v + sub + 8, sc_l, bi_l, sub + 8, skA[sub / 8 + 1], y);
               stage8(wbuf_s, lane, cin + sub + 8, y, op.out_f32);
             }
           }
@@ -1477,6 +1487,8 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) skA[u] = skB[u];
       }
+      if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
+        p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
       if (staged) {
         if (etid == 0) { dbg_mark(p, 14); edbg(p, 6, acc); }
         if (lane == 0) bulk_wait0();        // stores complete before the item is released
@@ -1600,7 +1612,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
 // the chunk and cluster counters -- off the epilogue warps' critical path.
 // Ordering: the epilogue's stores (TMA stores waited to completion, generic
 // stores) precede its named barrier and mbarrier arrive (release.cta); this
-// lane's wait is an acquire, and __threadfence() makes the chain cumulative
+// lane's wait is an acquire, and the (cumulative) fence.release.gpu orders the chain
 // at GPU scope before the counter atomics.
 __device__ void releaser_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = &g_ctl;

@@ -33,7 +33,7 @@ constexpr int MMA_WARP = 1;       // warp 1: single-thread tcgen05.mma issue
 constexpr int WORK_WARP0 = 2;     // warps 2-7: TMA / gather loads of GEMM items, CUDA-core items
 constexpr int NWORK = 192;
 constexpr int EPI_WARP0 = 8;      // warps 8-11: TMEM -> register epilogue; warp w reads TMEM lane
-constexpr int NEPI = 128;         //   quarter w % 4 (NEPI = 256 would also split the columns in halves)
+constexpr int NEPI = 128;         //   quarter w % 4 (8 warps splitting the columns measured no faster)
 constexpr int NTHREADS = 384;
 constexpr int CC_THREADS = NWORK; // threads that execute a CUDA-core item
 constexpr int CC_RUN = 8;         // consecutive output pixels per thread in the row-run window kernel

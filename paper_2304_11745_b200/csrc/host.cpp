@@ -904,7 +904,7 @@ int rebuild_op_table() {
       const int esz = d.out_f32 ? 4 : 2;
       const bool ok = (static_cast<long long>(d.ldo) * esz) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
-      if (!rc && ok) {
+      if (!rc && ok && !getenv("GACER_NO_TMA_STORE")) {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Cout), static_cast<cuuint64_t>(d.M)};
         const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ldo) * esz};
         const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32u};  // 32 rows x 128 B

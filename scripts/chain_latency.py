@@ -31,10 +31,11 @@ for op in np.unique(tr[:, 1]):
     acc = (sel[:, 9] - t0) / 1e3
     rel = (sel[:, 7] - t0) / 1e3
     edone = (sel[:, 10] - t0) / 1e3
+    eloop = (sel[:, 11] - t0) / 1e3
     gemm = np.all(sel[:, 9] > 0)
     print(f"op {int(op):3d} items {len(sel):4d} claim[{c.min():7.1f},{c.max():7.1f}] "
           f"start-claim med {np.median(st_ - c):5.2f} "
-          + (f"acc-start {np.median(acc - st_):5.2f} epi {np.median(edone - acc):5.2f} rel {np.median(rel - edone):5.2f} " if gemm else
+          + (f"acc-start {np.median(acc - st_):5.2f} epi {np.median(edone - acc):5.2f} (loop {np.median(eloop - acc):5.2f}) rel {np.median(rel - edone):5.2f} " if gemm else
              f"rel-start med {np.median(rel - st_):5.2f}                       ")
           + f"end {rel.max():7.1f} (first claim - prev end {c.min() - prev_end:6.2f})")
     prev_end = rel.max()
