@@ -129,6 +129,13 @@ def sweep_plans(ts):
     if len(ts) == 3:
         plans += [("shares[.35,.45,.2]", None, None, [0.35, 0.45, 0.2]),
                   ("shares[.25,.5,.25]", None, None, [0.25, 0.5, 0.25])]
+    # SM partition policies (the paper's resource share W per tenant): each
+    # CTA serves its own tenant first, then steals (work-conserving / hybrid)
+    plans += [("work_conserving", None, None, None, "work_conserving"),
+              ("hybrid", None, None, None, "hybrid")]
+    if len(ts) == 3:
+        plans += [(f"{pol}+shares[{a},{b},{a}]", None, None, [a, b, a], pol)
+                  for pol in ("work_conserving", "hybrid") for a, b in ((0.3, 0.4), (0.35, 0.3))]
     plans += [(f"pointers{k}", None, [cuts(n, k) for n in nops], None) for k in (2, 4)]
     if "vgg16" in names:
         t = names.index("vgg16")
@@ -248,14 +255,17 @@ def run_gacer(args, rank, world, dist):
     # ---- regulation plan: identity, or the best of a short sweep (each rank
     #      picks on its own measurements; the result is identical math)
     plans = sweep_plans(ts) if args.plan == "sweep" else [("identity", None, None, None)]
+    plans = [pl if len(pl) == 5 else (*pl, "priority") for pl in plans]
     plan_ms = {}
-    for name, dec, ptr, sh in plans:
+    for name, dec, ptr, sh, part in plans:
         sess.set_regulation(dec, ptr)
+        G.gacer_set_partition(part)
         G.gacer_set_sm_shares(sh)
         plan_ms[name] = float(np.median(time_mode(G, sess, torch, stream, "executor", 5, 2, flush)))
     best = min(plan_ms, key=plan_ms.get)
-    name, dec, ptr, sh = next(pl for pl in plans if pl[0] == best)
+    name, dec, ptr, sh, part = next(pl for pl in plans if pl[0] == best)
     sess.set_regulation(dec, ptr)
+    G.gacer_set_partition(part)
     G.gacer_set_sm_shares(sh)
 
     # ---- main arm: the GACER executor under the chosen plan

@@ -235,6 +235,12 @@ int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n);
  * reset by gacer_register_tenant. */
 int gacer_set_sm_shares(const float* shares, int32_t n);
 
+/* Switch the SM-partition policy (gacer_partition) of the executor; the
+ * initial value comes from gacer_options.partition.  Together with the
+ * shares it forms the spatial part of the regulation: bench.py sweeps both.
+ * GACER_E_INVALID_ARG for an unknown policy (the previous one stays). */
+int gacer_set_partition(int32_t partition);
+
 int gacer_set_mode(int mode);               /* gacer_mode */
 
 /* One round: every tenant's forward once on its bound input.

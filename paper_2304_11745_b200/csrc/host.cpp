@@ -1587,6 +1587,14 @@ int gacer_set_sm_shares(const float* shares, int32_t n) {
   return upload_plan();
 }
 
+int gacer_set_partition(int32_t partition) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (partition < GACER_PARTITION_PRIORITY || partition > GACER_PARTITION_HYBRID)
+    return set_err(GACER_E_INVALID_ARG, "unknown partition mode %d", partition);
+  S.opts.partition = partition;
+  return upload_plan();
+}
+
 int gacer_set_mode(int mode) {
   if (mode != GACER_MODE_EXECUTOR && mode != GACER_MODE_SEQUENTIAL && mode != GACER_MODE_MULTISTREAM)
     return set_err(GACER_E_INVALID_ARG, "bad mode %d", mode);

@@ -98,6 +98,7 @@ EXPORTS = {
     "gacer_set_regulation": ([C.POINTER(gacer_decomposition), C.POINTER(gacer_sync_pointers)], C.c_int),
     "gacer_query_op_clusters": ([C.c_int, IP, C.c_int32], C.c_int),
     "gacer_set_sm_shares": ([C.POINTER(C.c_float), C.c_int32], C.c_int),
+    "gacer_set_partition": ([C.c_int32], C.c_int),
     "gacer_set_mode": ([C.c_int], C.c_int),
     "gacer_run_round": ([], C.c_int),
     "gacer_run_round_async": ([C.c_void_p], C.c_int),
@@ -266,6 +267,10 @@ def gacer_query_op_clusters(tenant, n_ops):
     out = np.zeros(n_ops, dtype=np.int32)
     n = _check(lib().gacer_query_op_clusters(tenant, out.ctypes.data_as(IP), n_ops))
     return out[:n].tolist()
+
+
+def gacer_set_partition(partition="priority"):
+    return _check(lib().gacer_set_partition(PARTITION[partition] if isinstance(partition, str) else int(partition)))
 
 
 def gacer_set_sm_shares(shares=None):

@@ -16,7 +16,7 @@ ts = bench.make_workload()
 s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], trace=True, partition=os.environ.get("GACER_PARTITION", "priority"))
 for t, (*_, x) in enumerate(ts):
     s.set_input(t, x)
-for nm, dec, ptr, sh in bench.sweep_plans(ts):
+for nm, dec, ptr, sh, *_rest in bench.sweep_plans(ts):
     if nm == plan:
         s.set_regulation(dec, ptr)
         G.gacer_set_sm_shares(sh)

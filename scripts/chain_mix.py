@@ -21,7 +21,7 @@ def traced(idx):
     for j, i in enumerate(idx):
         s.set_input(j, ts[i][5])
     if len(idx) == len(ts):
-        for nm, dec, ptr, sh in bench.sweep_plans(ts):
+        for nm, dec, ptr, sh, *_rest in bench.sweep_plans(ts):
             if nm == plan_name:
                 s.set_regulation(dec, ptr)
                 G.gacer_set_sm_shares(sh)

@@ -47,7 +47,9 @@ def main():
         for t, (*_, x) in enumerate(ts):
             s.set_input(t, x)
         plans = bench.sweep_plans(ts)
-        for name, dec, ptr, sh in plans:
+        for name, dec, ptr, sh, *pol in plans:
+            if pol and pol[0] != partition:
+                continue   # the partition is swept by the outer loop
             try:
                 s.set_regulation(dec, ptr)
             except G.GacerError as e:

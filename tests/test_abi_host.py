@@ -166,3 +166,11 @@ def test_partition_modes_validated():
         o = G.gacer_options(num_ctas=0, partition=bad, watchdog_ms=0, trace=0)
         assert G.lib().gacer_init(-1, ctypes.byref(o)) == -1  # GACER_E_INVALID_ARG
     assert G.PARTITION["priority"] == 0   # the default (zeroed options)
+    G.gacer_init(-1)
+    try:
+        for name in G.PARTITION:            # switchable at run time (part of the regulation)
+            G.gacer_set_partition(name)
+        for bad in (-1, 4, 99):
+            assert G.lib().gacer_set_partition(bad) == -1
+    finally:
+        G.gacer_shutdown()
