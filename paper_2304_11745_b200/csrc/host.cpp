@@ -645,7 +645,14 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           // 128x256 tiles (less L2 operand traffic per FLOP) when they still
           // give every SM a tile; else N <= 128.  A function of the layer
           // shape only, identical in every mode.
-          if (F.Cout >= 256 && F.tiles_m * cdiv(F.Cout, 256) >= kSplitSms) F.bn = 256;
+          // Also for every throughput-dominant layer (>= 2 GFLOP): a 128x256
+          // tile moves (128+256)/(128*256) smem/L2 bytes per MAC against
+          // (128+128)/(128*128) for 128x128 -- the mainloop is bound by the
+          // shared-memory port (TMA fill + tensor-core operand reads,
+          // scripts/micro/tma_rate2.cu), so the wide tile needs ~30% less
+          // SM time per FLOP; in a multi-tenant round the other tenants'
+          // items fill the SMs a layer no longer covers by itself.
+          if (F.Cout >= 256 && (F.tiles_m * cdiv(F.Cout, 256) >= kSplitSms || F.flops >= 2.0e9)) F.bn = 256;
           else F.bn = F.Cout >= 128 ? 128 : roundup(F.Cout, 16);
           F.tiles_n = cdiv(F.Cout, F.bn);
           rows = static_cast<size_t>(F.tiles_n) * F.bn;
