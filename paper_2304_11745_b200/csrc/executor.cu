@@ -173,6 +173,11 @@ __device__ __forceinline__ void kdbg(const ExecParams& p, int slot, uint32_t i) 
   if (p.dbg && blockIdx.x == 0 && i < 256) p.dbg[KDBG_OFF + slot * 256 + i] = static_cast<int64_t>(globaltimer());
 }
 
+// scheduler stamps of CTA 0's first 24 claims (GACER_DEBUG_TIMING): globaltimer
+__device__ __forceinline__ void sdbg(const ExecParams& p, uint32_t n, int j, int64_t v) {
+  if (p.dbg && blockIdx.x == 0 && n < 24) p.dbg[KDBG_OFF + 1024 + n * 8 + j] = v;
+}
+
 // epilogue clock64 stamps of CTA 0's first 8 GEMM items (GACER_DEBUG_TIMING)
 __device__ __forceinline__ void edbg(const ExecParams& p, int point, uint32_t acc) {
   if (p.dbg && blockIdx.x == 0 && acc < 8) p.dbg[KDBG_OFF + 768 + acc * 16 + point] = static_cast<int64_t>(clock64());
@@ -1016,11 +1021,24 @@ __device__ __forceinline__ bool deps_ready(const ExecParams& p, const Item& it) 
       if (d < it.dep_count) ok &= ld_relaxed(p.chunk_done + it.dc[d]) >= p.epoch * it.dt[d];
     return ok;
   }
-  for (int d = 0; d < it.dep_count; ++d) {
-    const Dep dp = p.deps[it.dep_begin + d];
-    if (ld_relaxed(p.chunk_done + dp.counter) < p.epoch * dp.target) return false;
+  // overflow list (tile-level dependencies of wide windows): the Dep entries
+  // and then their counters are loaded in groups of 8 independent loads --
+  // two L2 round trips per group instead of two per dependency
+  bool ok = true;
+  for (int d0 = 0; d0 < it.dep_count && ok; d0 += 8) {
+    Dep dp[8];
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (d0 + j < it.dep_count) dp[j] = p.deps[it.dep_begin + d0 + j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (d0 + j < it.dep_count) v[j] = ld_relaxed(p.chunk_done + dp[j].counter);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (d0 + j < it.dep_count) ok &= v[j] >= p.epoch * dp[j].target;
   }
-  return true;
+  return ok;
 }
 
 __device__ __forceinline__ Seg get_seg(const ExecParams& p, const SmemCtl* ctl, int si) {
@@ -1084,6 +1102,7 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
 
 // Wait (blocking) until the item's dependencies are complete; false on abort.
 __device__ bool wait_deps(const ExecParams& p, const Item& it) {
+  if (deps_ready(p, it)) { fence_acquire_gpu(); return true; }   // usual case: one parallel check
   if (it.dep_count <= INLINE_DEPS) {
     for (int d = 0; d < it.dep_count; ++d)
       if (!spin_ge(p.chunk_done + it.dc[d], p.epoch * it.dt[d], p)) return false;
@@ -1111,7 +1130,9 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   int last_op = -1;
   const int big = 4 * static_cast<int>(gridDim.x);
   for (;;) {
-    Item it;
+    Item its[2];
+    int32_t idxs[2];
+    int n_claimed = 0;
     int claimed = -1;
     if (p.single_op >= 0) {
       while (islot - consumed >= 2) {
@@ -1121,7 +1142,12 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
       const OpDev& op = p.ops[p.single_op];
       const int n = op.tiles_m * op.tiles_n * (op.kind == DK_GEMM ? op.split_k : 1);
       claimed = sidx < n ? sidx : -2;
-      if (claimed >= 0) it = decode_single(op, p.single_op, sidx);
+      if (claimed >= 0) {
+        its[0] = decode_single(op, p.single_op, sidx);
+        its[0].kind = op.kind;
+        idxs[0] = claimed;
+        n_claimed = 1;
+      }
       sidx += gridDim.x;
     } else {
       uint64_t t0 = 0;
@@ -1131,7 +1157,9 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         int si;
         uint32_t h;
         Item cand;
+        sdbg(p, islot, 0, static_cast<int64_t>(globaltimer()));
         const int st = scan_ready(p, ctl, k, si, h, cand);
+        sdbg(p, islot, 1, static_cast<int64_t>(globaltimer()));
         if (st == 2) {
           // every item of cluster k is claimed: the synchronisation pointer --
           // wait until every item of cluster k (all tenants) is done.
@@ -1158,35 +1186,51 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         const uint32_t allowed =
             (cand.op != last_op) ? 1u : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
                                                             : (cand.op_left > G1 ? 2u : 1u));
+        sdbg(p, islot, 5, static_cast<int64_t>(allowed) * 1000 + (islot - consumed));
         while (islot - consumed >= allowed) {
           mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
           ++consumed;
         }
+        sdbg(p, islot, 2, static_cast<int64_t>(globaltimer()));
         const Seg sg = get_seg(p, ctl, si);
-        const uint32_t idx = atomicAdd(p.heads + si, 1u);
-        if (idx >= static_cast<uint32_t>(sg.size)) continue;  // lost the race for the last item
-        if (idx == h) {
-          it = cand;
-        } else {
-          // claimed a later item than the one checked: its dependencies are
-          // items claimed before it, so this wait terminates
-          it = p.items[sg.begin + idx];
-          if (!wait_deps(p, it)) { claimed = -3; break; }
+        const uint32_t want = 1;
+        const uint32_t idx = atomicAdd(p.heads + si, want);
+        sdbg(p, islot, 3, static_cast<int64_t>(globaltimer()));
+        if (idx >= static_cast<uint32_t>(sg.size)) continue;  // lost the race for the last item(s)
+        const uint32_t got = min(want, static_cast<uint32_t>(sg.size) - idx);
+        bool abort = false;
+        for (uint32_t j = 0; j < got; ++j) {
+          if (idx == h && j == 0) {
+            its[j] = cand;
+          } else {
+            // a later item than the one checked: its dependencies are items
+            // claimed before it, so this wait terminates
+            its[j] = p.items[sg.begin + idx + j];
+            if (!wait_deps(p, its[j])) { abort = true; break; }
+          }
+          idxs[j] = sg.begin + static_cast<int>(idx + j);
         }
-        claimed = sg.begin + static_cast<int>(idx);
-        last_op = it.op;
+        if (abort) { claimed = -3; break; }
+        n_claimed = static_cast<int>(got);
+        claimed = idxs[0];
+        last_op = its[got - 1].op;
       }
       if (claimed >= 0) fence_acquire_gpu();  // acquire side (pairs with the producers' release)
     }
     dbg_mark(p, 1);
-    const uint32_t slot = islot % ITEM_RING;  // free: islot - consumed < LOOKAHEAD < ITEM_RING
-    RingSlot& rs = ctl->ring[slot];
-    rs.it = it;
-    rs.idx = claimed >= 0 ? claimed : -1;
-    rs.kind = claimed >= 0 ? p.ops[it.op].kind : 0;
-    rs.t0 = p.trace ? globaltimer() : 0;
-    mbar_arrive(&ctl->rfull[slot]);
-    ++islot;
+    sdbg(p, islot, 4, static_cast<int64_t>(globaltimer()));
+    sdbg(p, islot, 6, claimed >= 0 ? its[0].op : -1);
+    if (claimed < 0) n_claimed = 0;
+    for (int j = 0; j < (n_claimed > 0 ? n_claimed : 1); ++j) {
+      const uint32_t slot = islot % ITEM_RING;  // free: islot - consumed < LOOKAHEAD < ITEM_RING
+      RingSlot& rs = ctl->ring[slot];
+      if (n_claimed > 0) rs.it = its[j];
+      rs.idx = n_claimed > 0 ? idxs[j] : -1;
+      rs.kind = n_claimed > 0 ? its[j].kind : 0;
+      rs.t0 = p.trace ? globaltimer() : 0;
+      mbar_arrive(&ctl->rfull[slot]);
+      ++islot;
+    }
     if (claimed < 0) break;
   }
 }
@@ -1195,6 +1239,7 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = &g_ctl;
   const int wtid = threadIdx.x - WORK_WARP0 * 32;  // 0..NWORK-1
   uint32_t g = 0, islot = 0;
+  int wop_cached = -1;   // op whose descriptor ctl->wop holds (uniform across the worker group)
   for (;;) {
     const uint32_t slot = islot % ITEM_RING;
     mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
@@ -1205,14 +1250,16 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
       if (wtid == 0) mbar_arrive(&ctl->rempty[slot]);
       break;
     }
-    {  // stage the item's op descriptor in shared memory: the tile functions
-       // read its fields many times, and global re-loads would each be an L2
-       // round trip (L1 is invalidated by the other roles' gpu-scope fences)
+    if (rs.it.op != wop_cached) {  // stage the item's op descriptor in shared memory
+       // (once per op run): the tile functions read its fields many times,
+       // and global re-loads would each be an L2 round trip (L1 is
+       // invalidated by the scheduler's acquire fences)
       constexpr int WORDS = static_cast<int>(sizeof(OpDev) / 4);
       static_assert(WORDS <= NWORK, "OpDev staging");
       if (wtid < WORDS)
         reinterpret_cast<uint32_t*>(&ctl->wop)[wtid] = reinterpret_cast<const uint32_t*>(p.ops + rs.it.op)[wtid];
       named_bar_sync(1, NWORK);
+      wop_cached = rs.it.op;
     }
     const OpDev& op = ctl->wop;
     if (rs.kind == DK_GEMM) {

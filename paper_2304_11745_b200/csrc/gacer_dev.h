@@ -102,6 +102,7 @@ struct Item {
   uint32_t prio;           // upward rank: estimated remaining critical path (ns) of its tenant
   int32_t idx;             // position in the item array (trace / diagnostics)
   int32_t op_left;         // items of the same op after this one in its queue segment
+  int32_t kind;            // DevKind of the op (saves the scheduler a global load per claim)
   int32_t dep_count;       // <= INLINE_DEPS: dc/dt hold them, else dep list at dep_begin
   int32_t dep_begin;
   int32_t dc[INLINE_DEPS]; // producer chunk counters

@@ -1173,6 +1173,7 @@ int compile_plan(Plan& P) {
               it.chunk = r.mc.empty() ? r.counter : r.mc[mt - r.m0];
               it.cluster = k;
               it.prio = rank[t][f];
+              it.kind = F.kind;
               seg_items[t][k].push_back(static_cast<int32_t>(P.items.size()));
               P.items.push_back(it);
               P.cluster_total[k] += 1;

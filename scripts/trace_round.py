@@ -19,9 +19,13 @@ from paper_2304_11745_b200.runtime import Session  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--out", default="gpurun_out/trace_summary.json")
+ap.add_argument("--partition", default="priority")
+ap.add_argument("--shares", default="", help="comma-separated SM shares per tenant")
 a = ap.parse_args()
 ts = bench.make_workload()
-s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], trace=True)
+s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts], trace=True, partition=a.partition)
+if a.shares:
+    G.gacer_set_sm_shares([float(v) for v in a.shares.split(",")])
 for t, (*_, x) in enumerate(ts):
     s.set_input(t, x)
 for _ in range(a.rounds):
