@@ -1273,6 +1273,8 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
         // the staged window op borrows the GEMM smem ring: wait until the MMA
         // has consumed every stage produced so far (MMAs complete in order)
         if (g > 0) mbar_wait(&ctl->empty[(g - 1) % STAGES], ((g - 1) / STAGES) & 1);
+        if (wtid == 0 && p.trace && p.single_op < 0)   // ring drained (diagnostics)
+          p.trace[static_cast<size_t>(rs.it.idx) * TRACE_FIELDS + 9] = static_cast<int64_t>(globaltimer());
         window_smem(op, rs.it, wtid, NWORK, smem_u32(cx.ring), 1);
       } else {
         run_cc(op, rs.it, wtid, ctl->red);
