@@ -286,6 +286,7 @@ constexpr int A_STAGE_BYTES = BM * 128;
 constexpr int B_STAGE_BYTES = BN_MAX * 128;
 constexpr int SMEM_RING_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES);
 constexpr int TMEM_COLS = 2 * BN_MAX;   // double-buffered accumulators
+constexpr int A2_OFF = 16384;            // M-pair tiles: second A block inside the stage's B region
 constexpr int RING_CONSUMERS = 1 + 1 + NEPI / 32;  // worker group, MMA thread, epilogue warps
 
 struct RingSlot {            // scheduler -> workers / MMA / epilogue
@@ -486,7 +487,8 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
   kb_range(op, it.ks, kb0, nk);
   const uint32_t ring_base = smem_u32(cx.ring);
   const uint32_t bbytes = static_cast<uint32_t>(op.bn) * 128u;
-  const int m0 = it.mt * BM, n0 = it.nt * op.bn;
+  const int mrep = op.mrep;
+  const int m0 = it.mt * BM * mrep, n0 = it.nt * op.bn;
   if (op.a_mode != A_GATHER) {
     // NPROD producer threads (lane 0 of worker warps 0..NPROD-1), producer j
     // filling the stages gi = j (mod NPROD): one thread's TMA loads complete
@@ -501,16 +503,22 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       const void* tmap_a = op.tmap_a;
       const void* tmap_b = op.tmap_b;
       fence_proxy_async_global();   // acquired producer data -> this thread's TMA reads
-      int w0 = 0, h0 = 0, img0 = 0;
+      // im2col start (top-left input tap) of each 128-row half of the tile
+      int w0[2] = {0, 0}, h0[2] = {0, 0}, img0[2] = {0, 0};
       if (a_mode == A_IM2COL) {
         const int HoWo = op.Ho * op.Wo, Wo = op.Wo;
-        img0 = m0 / HoWo;
-        const int rem = m0 - img0 * HoWo;
-        const int ho = rem / Wo, wo = rem - (rem / Wo) * Wo;
-        w0 = wo * op.stride - op.pw;
-        h0 = ho * op.stride - op.ph;
+        for (int hf = 0; hf < mrep; ++hf) {
+          const int mm = m0 + hf * BM;
+          img0[hf] = mm / HoWo;
+          const int rem = mm - img0[hf] * HoWo;
+          const int ho = rem / Wo, wo = rem - (rem / Wo) * Wo;
+          w0[hf] = wo * op.stride - op.pw;
+          h0[hf] = ho * op.stride - op.ph;
+        }
       }
-      const uint32_t tx = A_STAGE_BYTES + bbytes;
+      // M-pair tiles: the second 128-row A block lands in the stage's B region
+      // after the (<= 16 KB, bn <= 128) B block
+      const uint32_t tx = A_STAGE_BYTES * mrep + bbytes;
       const int i0 = static_cast<int>((static_cast<uint32_t>(pj) - g) % NPROD);
 #pragma unroll 1
       for (int i = i0; i < nk; i += NPROD) {
@@ -525,10 +533,14 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
           const int tap = k / C;
           const int c0 = k - tap * C;
           const int r = tap / kw, sx = tap - r * kw;
-          tma_load_im2col_4d(a_dst, tmap_a, bar, c0, w0, h0, img0, static_cast<uint16_t>(sx),
+          tma_load_im2col_4d(a_dst, tmap_a, bar, c0, w0[0], h0[0], img0[0], static_cast<uint16_t>(sx),
                              static_cast<uint16_t>(r));
+          if (mrep > 1)
+            tma_load_im2col_4d(b_dst + A2_OFF, tmap_a, bar, c0, w0[1], h0[1], img0[1], static_cast<uint16_t>(sx),
+                               static_cast<uint16_t>(r));
         } else {
           tma_load_2d(a_dst, tmap_a, bar, k, m0);
+          if (mrep > 1) tma_load_2d(b_dst + A2_OFF, tmap_a, bar, k, m0 + BM);
         }
         tma_load_2d(b_dst, tmap_b, bar, k, n0);
         kdbg(p, 1, gi);
@@ -1308,6 +1320,8 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     tc_fence_after();
     const uint32_t d = cx.tmem + abuf * BN_MAX;
     const uint32_t idesc = make_idesc(op.bn);
+    const int mrep = op.mrep;
+    const uint32_t d2 = d + static_cast<uint32_t>(op.bn);   // second accumulator (M-pair tiles)
     bool stamped = false;
 #pragma unroll 1
     for (int i = 0; i < nk; ++i) {
@@ -1322,11 +1336,18 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
       tc_fence_after();
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
-      if (!(p.dbg && (p.dbg_spin & 1)))   // diagnostics: odd dbg_spin skips the MMAs
+      if (!(p.dbg && (p.dbg_spin & 1))) {  // diagnostics: odd dbg_spin skips the MMAs
 #pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk)
-        umma_bf16(d, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
-                  (i > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BK / 16; ++kk)
+          umma_bf16(d, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
+                    (i > 0 || kk > 0) ? 1u : 0u);
+        if (mrep > 1) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(d2, make_sdesc(b_base + A2_OFF + kk * 32), make_sdesc(b_base + kk * 32), idesc,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
       umma_commit(&ctl->empty[stage]);
       ++g;
     }
@@ -1369,8 +1390,10 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     const int split = opg.split_k;
     const bool swap = op.swap;
     const int row = q * 32 + lane;
-    const int m0 = it.mt * BM, n0 = it.nt * bn;
-    const int m = m0 + row;
+    const int mrep = opg.mrep;
+    const int m0t = it.mt * BM * mrep, n0 = it.nt * bn;
+    int m0 = m0t;                 // first row of the current 128-row half
+    int m = m0 + row;
     const int tile = it.mt * opg.tiles_n + it.nt;
     const int cout_left = op.Cout - n0;
     // this warp's tile columns: halves split at a multiple of 32, so a staged
@@ -1389,7 +1412,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
         ctl->epi_bias[j] = op.bias[n0 + j];
       }
     }
-    const bool do_skip = op.has_skip && split == 1 && m < op.M && !swap;
+    bool do_skip = op.has_skip && split == 1 && m < op.M && !swap;
     const __nv_bfloat16* skrow =
         do_skip ? static_cast<const __nv_bfloat16*>(opg.skip) + static_cast<size_t>(m) * opg.lds + n0 : nullptr;
     uint4 skA[4], skB[4];  // residual values of the current / next 32 columns
@@ -1412,10 +1435,24 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       while (clock64() - ts < p.dbg_spin) {}
     }
     if (etid == 0) edbg(p, 11, acc);
-    const uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(q * 32) << 16);
+    uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(q * 32) << 16);
     float* part = opg.partial + static_cast<size_t>(tile) * split * (BM * bn);
     const bool staged = EPI_STAGED && op.c_tma && !swap;
     const int CW = op.out_f32 ? 32 : 64;          // columns per 128-byte staged row
+    for (int hf = 0; hf < mrep; ++hf) {         // M-pair tiles: two 128-row accumulators
+    if (hf > 0) {
+      m0 = m0t + hf * BM;
+      m = m0 + row;
+      taddr += static_cast<uint32_t>(bn);         // the second accumulator follows the first's bn columns
+      do_skip = op.has_skip && m < op.M;
+      skrow = do_skip ? static_cast<const __nv_bfloat16*>(opg.skip) + static_cast<size_t>(m) * opg.lds + n0 : nullptr;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int cc = c_lo + u * 8;
+        skA[u] = (do_skip && cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc)
+                                                         : make_uint4(0, 0, 0, 0);
+      }
+    }
     if (split == 1 && staged && !op.out_f32) {
       // lean staged bf16 path: branch-free activation clamp, 64-column
       // staging chunks (a compile-time constant), scale/bias by shuffle
@@ -1559,6 +1596,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
           if (c + u < c_hi) __stcg(mine + ((c + u) >> 2) * BM, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]));
       }
     }
+    }  // halves
     if (etid == 0) { dbg_mark(p, 13); edbg(p, 7, acc - 0); }
     tc_fence_before();
     __syncwarp();

@@ -66,7 +66,7 @@ struct OpDev {
   int32_t Ho, Wo, Cout, ldo;
   // residual operand (same shape/layout as out), row stride lds
   const void* skip;
-  int32_t lds, pad0;
+  int32_t lds, mrep;       // mrep: 128-row accumulators per GEMM tile (2: M-pair tile of 256 rows)
 
   int32_t kh, kw, stride, ph, pw, win; // win: 1 = window op staged through shared memory (window_smem)
 

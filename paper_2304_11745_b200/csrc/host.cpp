@@ -47,6 +47,11 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+// diagnostic switches: set and non-empty
+static bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && v[0] != '0';
+}
 constexpr int kSplitSms = 148;  // split-K is a function of the layer shape only (bit-identity, H4)
 
 int roundup(int a, int b) { return (a + b - 1) / b * b; }
@@ -90,6 +95,7 @@ struct FusedOp {
   int kh = 1, kw = 1, stride = 1, ph = 0, pw = 0;
   int cread = 0;  // channels read per tap (K = kh*kw*cread)
   bool win = false;  // window op staged through shared memory
+  int mrep = 1;      // GEMM: 128-row accumulators per tile (2 = M-pair tile, bm = 256)
   int M = 0, N = 0, K = 0, Kpad = 0, tiles_m = 1, tiles_n = 1, bm = 0, bn = 0, split_k = 1, nkb = 0;
   bool cip = true;
   // packed params (host)
@@ -619,9 +625,26 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           const bool tma = c64 == c8 || F.kh * F.kw == 1 || 2 * c64 <= 3 * c8;
           F.a_mode = F.swap ? A_ROWS : (tma ? A_IM2COL : A_GATHER);
           F.cread = (F.a_mode == A_IM2COL) ? c64 : c8;
+          // M-pair tiles (two 128-row accumulators sharing each B stage) for
+          // narrow (Cout <= 128), very wide layers (>= 2 tiles per SM even
+          // in pairs): half the items, so the per-item scheduling, epilogue
+          // prologue and release costs are amortised over twice the work.
+          // They need TMA operand loads: a small-Cin layer switches from the
+          // gather to im2col with a 64-channel K stride (zero-filled).
+          const long long m_rows = static_cast<long long>(B) * F.Ho * F.Wo;
+          const int bn_est = F.Cout >= 128 ? 128 : roundup(F.Cout, 16);
+          F.mrep = 1;
+          // (a gather layer only if the im2col K stays short: a 7x7 stem
+          //  would grow from 7 to 49 K-blocks)
+          const bool short_k = F.a_mode != A_GATHER || F.kh * F.kw <= 16;
+          if (!F.swap && F.Cout <= 128 && F.Cin <= 64 && short_k &&
+              cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= 2 * kSplitSms && !env_flag("GACER_NO_MPAIR")) {
+            F.mrep = 2;
+            if (F.a_mode == A_GATHER) { F.a_mode = A_IM2COL; F.cread = c64; }
+          }
           // 1x1 stride-1 conv over a dense NHWC tensor is a plain GEMM: tiled TMA rows
           if (!F.swap && F.kh * F.kw == 1 && F.stride == 1 && o.pad_h == 0 && o.pad_w == 0 && c64 == c8 &&
-              !getenv("GACER_IM2COL_1X1")) {
+              !env_flag("GACER_IM2COL_1X1")) {
             F.a_mode = A_ROWS;
             F.cread = c64;
           }
@@ -641,7 +664,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           rows = static_cast<size_t>(F.tiles_m) * BM;
         } else {
           F.M = B * F.Ho * F.Wo; F.N = F.Cout;
-          F.tiles_m = cdiv(F.M, BM);
+          F.tiles_m = cdiv(F.M, BM * F.mrep);
           // 128x256 tiles (less L2 operand traffic per FLOP) when they still
           // give every SM a tile; else N <= 128.  A function of the layer
           // shape only, identical in every mode.
@@ -657,13 +680,14 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           F.tiles_n = cdiv(F.Cout, F.bn);
           rows = static_cast<size_t>(F.tiles_n) * F.bn;
         }
-        F.bm = BM;
+        F.bm = BM * F.mrep;
         // split-K: a function of the layer shape only (same in every mode/plan)
         const int tiles = F.tiles_m * F.tiles_n;
         int sk = 1;
         // (each split keeps >= 8 K-blocks: below that the fixed-order
         //  reduction of the partials costs more than the MMA it parallelises)
         while (sk < MAX_SPLIT && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 8) sk *= 2;
+        if (F.mrep > 1) sk = 1;
         F.split_k = sk;
         F.w_bf16.assign(rows * F.Kpad, 0);
         for (int co = 0; co < F.Cout; ++co)
@@ -806,6 +830,7 @@ OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
   if (F.skip_t >= 0) { d.skip = tensor_addr(T, F.skip_t); d.lds = T.tensors[F.skip_t].ldc; }
   d.kh = F.kh; d.kw = F.kw; d.stride = F.stride; d.ph = F.ph; d.pw = F.pw;
   d.win = F.win ? 1 : 0;
+  d.mrep = F.mrep;
   d.M = F.M; d.N = F.N; d.K = F.K; d.Kpad = F.Kpad;
   d.tiles_m = F.tiles_m; d.tiles_n = F.tiles_n; d.bm = F.bm; d.bn = F.bn;
   d.split_k = F.split_k; d.nkb = F.nkb;
@@ -911,7 +936,7 @@ int rebuild_op_table() {
       const int esz = d.out_f32 ? 4 : 2;
       const bool ok = (static_cast<long long>(d.ldo) * esz) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
-      if (!rc && ok && !getenv("GACER_NO_TMA_STORE")) {
+      if (!rc && ok && !env_flag("GACER_NO_TMA_STORE")) {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Cout), static_cast<cuuint64_t>(d.M)};
         const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ldo) * esz};
         const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32u};  // 32 rows x 128 B
