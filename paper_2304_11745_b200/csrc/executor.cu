@@ -1453,7 +1453,66 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
                                                          : make_uint4(0, 0, 0, 0);
       }
     }
-    if (split == 1 && staged && !op.out_f32) {
+    if (split == 1 && !staged && !op.out_f32 && !swap) {
+      // lean direct bf16 path: same math as the staged path below, each
+      // thread storing its row's 8-column groups with 16-byte global stores
+      // (no staging buffer, no TMA-store waits)
+      const float lo = op.act == ACT_NONE ? -INFINITY : 0.0f;
+      const float hi = op.act == ACT_RELU6 ? 6.0f : INFINITY;
+      const bool skip = do_skip;
+      __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(op.out) + static_cast<size_t>(m) * op.ldo + n0;
+      const bool row_ok = m < op.M;
+      for (int c = c_lo; c < c_hi; c += 32) {
+        uint32_t r[32];
+        tmem_ld16_nw(taddr + c, r);
+        tmem_ld16_nw(taddr + c + 16, r + 16);
+        const float sc_l = ctl->epi_scale[c + lane], bi_l = ctl->epi_bias[c + lane];
+        if (skip) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cc = c + 32 + u * 8;
+            skB[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
+          }
+        }
+        tmem_wait();
+#pragma unroll
+        for (int g8 = 0; g8 < 4; ++g8) {
+          float y[8];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const int jj = g8 * 8 + j;
+            const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1])),
+                                        make_float2(__shfl_sync(0xffffffffu, sc_l, jj), __shfl_sync(0xffffffffu, sc_l, jj + 1)),
+                                        make_float2(__shfl_sync(0xffffffffu, bi_l, jj), __shfl_sync(0xffffffffu, bi_l, jj + 1)));
+            y[j] = o.x;
+            y[j + 1] = o.y;
+          }
+          if (skip) {
+            float sv[8];
+            bf16x8_to_f32(skA[g8], sv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] += sv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
+          const int cc = c + g8 * 8;
+          if (row_ok && cc < cout_left) {
+            if (cc + 8 <= cout_left) {
+              *reinterpret_cast<uint4*>(orow + cc) = make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+                                                                pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+            } else {
+              for (int j = 0; j < 8 && cc + j < cout_left; ++j) orow[cc + j] = __float2bfloat16_rn(y[j]);
+            }
+          }
+        }
+        if (skip) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) skA[u] = skB[u];
+        }
+      }
+      if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
+        p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
+    } else if (split == 1 && staged && !op.out_f32) {
       // lean staged bf16 path: branch-free activation clamp, 64-column
       // staging chunks (a compile-time constant), scale/bias by shuffle
       const float lo = op.act == ACT_NONE ? -INFINITY : 0.0f;
