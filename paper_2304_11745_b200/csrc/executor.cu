@@ -260,6 +260,7 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
@@ -321,7 +322,11 @@ constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 row
 // TMA-store staging only with 4 epilogue warps: 8 warps' staging rows do not
 // fit beside the ring; they store their rows directly (16 B per thread)
 constexpr bool EPI_STAGED = NEPI == 128;
-constexpr int SMEM_STAGE_BYTES = EPI_STAGED ? (NEPI / 32) * STAGE_WARP_BYTES : 0;
+#ifndef GACER_EPI_DB
+#define GACER_EPI_DB 0
+#endif
+constexpr bool EPI_DB = GACER_EPI_DB != 0;              // double-buffered staging (needs the smem of a ring stage)
+constexpr int SMEM_STAGE_BYTES = EPI_STAGED ? (NEPI / 32) * STAGE_WARP_BYTES * (EPI_DB ? 2 : 1) : 0;
 constexpr int SMEM_BYTES = SMEM_RING_BYTES + SMEM_STAGE_BYTES + 1024 /*align slack*/;
 // The control block is a static __shared__ object (not carved from the
 // dynamic buffer) so every access compiles to LDS/STS instead of generic
@@ -1532,8 +1537,14 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
           }
         }
         const int cin = (c - c_lo) & 63;
-        if (cin == 0 && c > c_lo) {            // a new chunk: wait until the last store read the buffer
-          if (lane == 0) bulk_wait_read0();
+        // staging buffer of this 64-column chunk (EPI_DB: two per warp, the
+        // store of one chunk overlaps the conversion of the next)
+        const uint32_t sbuf = wbuf_s + (EPI_DB ? (((c - c_lo) >> 6) & 1) * STAGE_WARP_BYTES : 0);
+        if (cin == 0 && c > c_lo) {            // a new chunk: its buffer's previous store must have been read
+          if (lane == 0) {
+            if (EPI_DB) bulk_wait_read1();
+            else bulk_wait_read0();
+          }
           __syncwarp();
         }
         tmem_wait();
@@ -1558,14 +1569,14 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
           const uint32_t ch = static_cast<uint32_t>((cin + g8 * 8) >> 3);   // 16-byte chunk of the 128-byte row
-          sts128(wbuf_s + lane * 128 + ((ch ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+          sts128(sbuf + lane * 128 + ((ch ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
                  pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
         }
         if (cin == 32 || c + 32 >= c_hi) {     // 64-column chunk complete: TMA-store it
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(op.tmap_c, wbuf_s, n0 + c - cin, row0);
+            tma_store_2d(op.tmap_c, sbuf, n0 + c - cin, row0);
             bulk_commit();
           }
         }

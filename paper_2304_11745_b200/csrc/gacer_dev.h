@@ -24,8 +24,15 @@ enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2 };
 constexpr int BM = 128;           // rows per tile (UMMA M)
 constexpr int BK = 64;            // bf16 elements per K-block = one 128-byte swizzle row
 constexpr int BN_MAX = 256;       // max UMMA N per tile
-constexpr int STAGES = 4;         // smem ring depth (A 16 KB + B 32 KB per stage)
-constexpr int NPROD = 4;          // TMA-issuing producer threads per CTA (lane 0 of worker warps 0..3)
+#ifndef GACER_STAGES
+#define GACER_STAGES 4
+#endif
+constexpr int STAGES = GACER_STAGES;  // smem ring depth (A 16 KB + B 32 KB per stage)
+// TMA-issuing producer threads per CTA (lane 0 of worker warps 0..NPROD-1).
+// Producer j owns the stages s = j (mod NPROD); NPROD == STAGES so that no two
+// producers ever wait on the same stage barrier (a parity wait cannot tell
+// phase u from phase u - 2).
+constexpr int NPROD = STAGES;
 constexpr int ITEM_RING = 4;      // scheduler -> MMA/epilogue item queue depth
 // warp roles of the executor CTA (16 warps; 4 per SM sub-partition, <= 128 registers)
 constexpr int SCHED_WARP = 0;     // warp 0: scheduler (lane 0) -- claims ready items into the item ring
