@@ -282,6 +282,24 @@ def run_gacer(args, rank, world, dist):
     value = world * n_inf * args.steps / (total_ms / 1000.0)
     launches_per_round = G.gacer_get_stats()["kernel_launches"]
 
+    # ---- temporal-regulation overhead: the same pointer
+    #      plan with device-side cluster barriers vs the paper's CPU-side
+    #      pointers (one launch per cluster, host sync in between, T_SW)
+    t_sw = {}
+    if args.plan == "sweep":
+        nops = [len(g.ops) for _, g, *_ in ts]
+        for kp in (2, 4):
+            sess.set_regulation(None, [[round(n * (j + 1) / (kp + 1)) for j in range(kp)] for n in nops])
+            G.gacer_set_sm_shares(None)
+            G.gacer_set_partition("priority")
+            dev_ms = float(np.median(time_mode(G, sess, torch, stream, "executor", 5, 2, flush)))
+            host_ms = float(np.median(time_mode(G, sess, torch, stream, "executor_hostsync", 5, 2, flush)))
+            t_sw[f"pointers{kp}"] = {"device_ms": dev_ms, "host_sync_ms": host_ms}
+        sess.set_regulation(dec, ptr)
+        G.gacer_set_partition(part)
+        G.gacer_set_sm_shares(sh)
+        sess.set_mode("executor")
+
     # ---- same-kernel baselines (makespan per round), same timing protocol
     base = {}
     for mode in ("sequential", "multistream"):
@@ -336,6 +354,7 @@ def run_gacer(args, rank, world, dist):
             "gpu_launches": launches_per_round * args.steps,
             "clocks": clk.summary(),
             "plans_ms": plan_ms,
+            "pointer_sync_ms": t_sw,
             "baselines": base,
             "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
             "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,

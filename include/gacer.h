@@ -142,7 +142,10 @@ typedef struct {
 typedef enum {
   GACER_MODE_EXECUTOR = 0,    /* one persistent multi-tenant kernel per round */
   GACER_MODE_SEQUENTIAL = 1,  /* "CuDNN-Seq": one kernel per fused op, one stream, tenant after tenant */
-  GACER_MODE_MULTISTREAM = 2  /* "Stream-Parallel": one kernel per fused op, one stream per tenant */
+  GACER_MODE_MULTISTREAM = 2, /* "Stream-Parallel": one kernel per fused op, one stream per tenant */
+  GACER_MODE_EXECUTOR_HOSTSYNC = 3 /* the executor with the paper's CPU-side pointers: one launch per
+                                      cluster (pointer segment), the host synchronising with the GPU
+                                      between them (T_SW of Eq. 8); same results, measurement only */
 } gacer_mode;
 
 typedef enum {

@@ -1142,7 +1142,7 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = &g_ctl;
   uint32_t islot = 0, consumed = 0;
-  int k = 0;
+  int k = p.k_first;
   int sidx = blockIdx.x;
   int last_op = -1;
   const int big = 4 * static_cast<int>(gridDim.x);
@@ -1170,7 +1170,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
       uint64_t t0 = 0;
       uint32_t spins = 0;
       while (claimed == -1) {
-        if (k >= p.n_clusters) { claimed = -2; break; }
+        if (k > p.k_last) { claimed = -2; break; }
         int si;
         uint32_t h;
         Item cand;

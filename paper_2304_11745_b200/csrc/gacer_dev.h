@@ -139,6 +139,7 @@ struct ExecParams {
   int32_t* error;           // device error flag (deadlock watchdog)
   int64_t* trace;           // optional [n_items * 8]
   int32_t n_tenants, n_clusters;
+  int32_t k_first, k_last;  // clusters served by this launch (host-synchronised pointers: one each)
   uint32_t epoch;           // round number since plan install, >= 1
   int32_t n_heads;
   int64_t watchdog_ns;

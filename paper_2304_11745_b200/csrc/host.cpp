@@ -1354,8 +1354,37 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
     p.dbg = S.d_dbg;
     if (const char* e = getenv("GACER_DBG_SPIN")) p.dbg_spin = atoll(e);
+    p.k_first = 0;
+    p.k_last = p.n_clusters - 1;
     CUDA_TRY(launch_executor(p, S.grid, st));
     launches = 1;
+  } else if (S.mode == GACER_MODE_EXECUTOR_HOSTSYNC) {
+    // the paper's pointer mechanics (Fig. 6, Eq. 8): each cluster is issued
+    // separately and the CPU waits for the GPU at every pointer before it
+    // issues the next cluster -- the GPU idles for T_SW per pointer
+    if (S.epoch >= 0x7FFFFF00u / std::max<uint32_t>(1, 1 + static_cast<uint32_t>(S.plan.items.size()))) {
+      if (int rc = reset_device_counters()) return rc;
+    }
+    ExecParams p;
+    std::memset(&p, 0, sizeof p);
+    p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.segs = S.d_segs;
+    p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
+    p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
+    p.error = S.d_error; p.trace = S.d_trace;
+    p.n_tenants = static_cast<int>(S.tenants.size());
+    p.n_clusters = S.plan.n_clusters;
+    p.epoch = ++S.epoch;
+    p.n_heads = p.n_tenants * p.n_clusters;
+    p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
+    p.single_op = -1;
+    p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
+    for (int k = 0; k < p.n_clusters; ++k) {
+      if (S.plan.cluster_total[k] == 0) continue;   // empty segment: nothing to issue
+      p.k_first = p.k_last = k;
+      CUDA_TRY(launch_executor(p, S.grid, st));
+      ++launches;
+      if (k + 1 < p.n_clusters) CUDA_TRY(cudaStreamSynchronize(st));   // the CPU-side pointer
+    }
   } else {
     const bool ms = S.mode == GACER_MODE_MULTISTREAM;
     if (ms) {
@@ -1629,7 +1658,8 @@ int gacer_set_partition(int32_t partition) {
 }
 
 int gacer_set_mode(int mode) {
-  if (mode != GACER_MODE_EXECUTOR && mode != GACER_MODE_SEQUENTIAL && mode != GACER_MODE_MULTISTREAM)
+  if (mode != GACER_MODE_EXECUTOR && mode != GACER_MODE_SEQUENTIAL && mode != GACER_MODE_MULTISTREAM &&
+      mode != GACER_MODE_EXECUTOR_HOSTSYNC)
     return set_err(GACER_E_INVALID_ARG, "bad mode %d", mode);
   S.mode = mode;
   return GACER_OK;

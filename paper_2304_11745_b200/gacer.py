@@ -36,7 +36,7 @@ OP = {"conv": 1, "linear": 2, "maxpool": 3, "avgpool": 4, "gap": 5, "add": 6, "c
       "bn": 8, "relu": 9, "relu6": 10, "flatten": 11, "dropout": 12}
 DTYPE = {"bf16": 1, "fp32": 2}
 AXIS = {"none": 0, "batch": 1, "channel": 2}
-MODE = {"executor": 0, "sequential": 1, "multistream": 2}
+MODE = {"executor": 0, "sequential": 1, "multistream": 2, "executor_hostsync": 3}
 PARTITION = {"priority": 0, "work_conserving": 1, "strict": 2, "hybrid": 3}
 FLAG_BIAS, FLAG_CIP = 1, 2
 

@@ -84,6 +84,8 @@ def test_bitwise_across_plans_and_modes(cuda_ok, d2):
     for k in range(6):
         variants.append(dict(plan=random_plan(d2, rng, n_pointers=k % 4)))
     variants.append(dict(plan=random_plan(d2, rng, 3), partition="strict", num_ctas=100))
+    # the paper's CPU-side pointers: one launch per cluster, host sync between
+    variants.append(dict(plan=random_plan(d2, rng, 3), mode="executor_hostsync"))
     for v in variants:
         out, _ = run(d2, **v)
         for t, (a, b) in enumerate(zip(ref, out)):
