@@ -264,6 +264,29 @@ def run_gacer(args, rank, world, dist):
         plan_ms[name] = float(np.median(time_mode(G, sess, torch, stream, "executor", 5, 2, flush)))
     best = min(plan_ms, key=plan_ms.get)
     name, dec, ptr, sh, part = next(pl for pl in plans if pl[0] == best)
+    search = None
+    if args.plan == "sweep" and not args.no_search:
+        # Algorithm 1 (§4.4): measured coordinate descent over
+        # Matrix_P and batch decompositions under the chosen SM partition
+        from paper_2304_11745_b200 import planner as PL
+        G.gacer_set_partition(part)
+        G.gacer_set_sm_shares(sh)
+        graphs = [g for _, g, *_ in ts]
+        n_ops = [len(g.ops) for g in graphs]
+        ev = PL.measured_objective(G, sess, graphs, [B for _, _, _, B, _, _ in ts], torch, stream, flush,
+                                   rounds=5, warmup=2)
+        res = PL.granularity_aware_search(ev, n_ops, PL.SearchConfig(max_pointers=2, stride=max(1, min(n_ops) // 6),
+                                                                     max_evals=args.search_evals))
+        s_dec = ev.plan_decomposition(res.decomposition)
+        s_ptr = [list(p_) for p_ in res.pointers] if any(res.pointers) else None
+        search = {"evals": res.evals, "ms": res.R, "pointers": [list(p_) for p_ in res.pointers],
+                  "batch_chunks": [c for _, c in res.decomposition], "ms_per_pointer_count": res.records}
+        sname = f"gacer_search[{part}]"
+        plans.append((sname, s_dec, s_ptr, sh, part))
+        plan_ms[sname] = res.R
+        if res.R < plan_ms[best]:
+            best = sname
+            name, dec, ptr, sh, part = plans[-1]
     sess.set_regulation(dec, ptr)
     G.gacer_set_partition(part)
     G.gacer_set_sm_shares(sh)
@@ -355,6 +378,7 @@ def run_gacer(args, rank, world, dist):
             "clocks": clk.summary(),
             "plans_ms": plan_ms,
             "pointer_sync_ms": t_sw,
+            "search": search,
             "baselines": base,
             "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
             "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,
@@ -378,6 +402,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default=CONFIG, choices=["d2_r50_v16_mv2", "d3_five"])
     ap.add_argument("--plan", default="sweep", choices=["identity", "sweep"])
+    ap.add_argument("--no-search", action="store_true", help="skip the Algorithm 1 plan search")
+    ap.add_argument("--search-evals", type=int, default=30)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
