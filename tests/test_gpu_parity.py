@@ -134,7 +134,7 @@ def test_tenant_parity(cuda_ok, name, B, hw):
 
 
 @pytest.mark.parametrize("name,hw,B", [("inception_v3", 224, 1), ("alexnet", 224, 2),
-                                       ("resnet101", 64, 2)])
+                                       ("resnet101", 64, 2), ("resnet34", 64, 2)])
 def test_tenant_parity_d3_models(cuda_ok, name, hw, B):
     t = make_tenant(name, B, "bf16", 3000 + B, hw)
     outs, _ = run_session([t])

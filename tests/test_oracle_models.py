@@ -41,6 +41,7 @@ def load_into_torch(graph, params, tmodel):
 
 TV = {
     "resnet18": lambda: torchvision.models.resnet18(),
+    "resnet34": lambda: torchvision.models.resnet34(),
     "resnet50": lambda: torchvision.models.resnet50(),
     "resnet101": lambda: torchvision.models.resnet101(),
     "mobilenet_v2": lambda: torchvision.models.mobilenet_v2(),
@@ -52,7 +53,7 @@ TV = {
 
 CASES = [("resnet18", 64, 2), ("resnet50", 64, 2), ("mobilenet_v2", 64, 2),
          ("alexnet", 224, 1), ("vgg16", 224, 1), ("inception_v3", 224, 1),
-         ("resnet101", 64, 1)]
+         ("resnet101", 64, 1), ("resnet34", 64, 1)]
 
 
 @pytest.mark.parametrize("name,hw,batch", CASES)

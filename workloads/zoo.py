@@ -155,6 +155,10 @@ def resnet18():
     return _resnet("resnet18", "basic", (2, 2, 2, 2))
 
 
+def resnet34():
+    return _resnet("resnet34", "basic", (3, 4, 6, 3))
+
+
 def resnet50():
     return _resnet("resnet50", "bottleneck", (3, 4, 6, 3))
 
@@ -318,6 +322,7 @@ MODELS = {
     "tiny_cnn": tiny_cnn,
     "tiny_mlp": tiny_mlp,
     "resnet18": resnet18,
+    "resnet34": resnet34,
     "resnet50": resnet50,
     "resnet101": resnet101,
     "vgg16": vgg16,
