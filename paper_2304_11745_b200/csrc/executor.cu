@@ -323,7 +323,7 @@ constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 row
 // fit beside the ring; they store their rows directly (16 B per thread)
 constexpr bool EPI_STAGED = NEPI == 128;
 #ifndef GACER_EPI_DB
-#define GACER_EPI_DB 0
+#define GACER_EPI_DB 1
 #endif
 constexpr bool EPI_DB = GACER_EPI_DB != 0;              // double-buffered staging (needs the smem of a ring stage)
 constexpr int SMEM_STAGE_BYTES = EPI_STAGED ? (NEPI / 32) * STAGE_WARP_BYTES * (EPI_DB ? 2 : 1) : 0;
@@ -524,7 +524,8 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       // M-pair tiles: the second 128-row A block lands in the stage's B region
       // after the (<= 16 KB, bn <= 128) B block
       const uint32_t tx = A_STAGE_BYTES * mrep + bbytes;
-      const int i0 = static_cast<int>((static_cast<uint32_t>(pj) - g) % NPROD);
+      // first K-block of this item whose stage (g + i) % NPROD belongs to producer pj
+      const int i0 = (pj - static_cast<int>(g % NPROD) + NPROD) % NPROD;
 #pragma unroll 1
       for (int i = i0; i < nk; i += NPROD) {
         const uint32_t gi = g + i, stage = gi % STAGES;
@@ -557,7 +558,7 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
     // 8 channels of one tap; thread -> chunk j = wtid & 7, rows (wtid>>3) + 12i
     constexpr int RSTEP = NWORK / 8;                  // 12
     constexpr int ROWS = (BM + RSTEP - 1) / RSTEP;    // 11
-    constexpr int LAG = 3;                            // stages in flight per thread (< STAGES)
+    constexpr int LAG = STAGES - 1;                   // stages in flight per thread (< STAGES)
     const int chunk = wtid & 7, rsub = wtid >> 3;
     const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
     const __nv_bfloat16* img[ROWS];
@@ -1373,7 +1374,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
   const int etid = threadIdx.x - EPI_WARP0 * 32;  // 0..NEPI-1
   const int ew = etid >> 5, lane = etid & 31;
   const int q = ew & 3, hcol = ew >> 2;
-  uint8_t* wbuf = cx.stage + ew * STAGE_WARP_BYTES;
+  uint8_t* wbuf = cx.stage + ew * STAGE_WARP_BYTES * (EPI_DB ? 2 : 1);
   const uint32_t wbuf_s = smem_u32(wbuf);
   uint32_t islot = 0, acc = 0, nrel = 0;
   for (;;) {
