@@ -557,21 +557,21 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
     // im2col gather with cp.async (C not a multiple of 64): 16-byte chunks of
     // 8 channels of one tap; thread -> chunk j = wtid & 7, rows (wtid>>3) + 12i
     constexpr int RSTEP = NWORK / 8;                  // 12
-    constexpr int ROWS = (BM + RSTEP - 1) / RSTEP;    // 11
+    constexpr int ROWS = (2 * BM + RSTEP - 1) / RSTEP; // 22: covers M-pair tiles (256 rows)
     constexpr int LAG = STAGES - 1;                   // stages in flight per thread (< STAGES)
+    const int rows_tile = BM * mrep;
     const int chunk = wtid & 7, rsub = wtid >> 3;
     const __nv_bfloat16* in = static_cast<const __nv_bfloat16*>(op.in);
-    const __nv_bfloat16* img[ROWS];
-    int hi0[ROWS], wi0[ROWS];
+    int img_off[ROWS], hi0[ROWS], wi0[ROWS];          // per gathered row: image offset, top-left tap
     const int HoWo = op.Ho * op.Wo;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
       const int row = rsub + RSTEP * i;
       const int m = m0 + row;
-      const bool ok = m < op.M && row < BM;
+      const bool ok = m < op.M && row < rows_tile;
       const int mm = ok ? m : 0;
       const int b = mm / HoWo, rem = mm - b * HoWo, ho = rem / op.Wo, wo = rem - (rem / op.Wo) * op.Wo;
-      img[i] = in + static_cast<size_t>(b) * op.H * op.W * op.ldi;
+      img_off[i] = b * op.H * op.W * op.ldi;
       hi0[i] = ok ? ho * op.stride - op.ph : -100000;
       wi0[i] = wo * op.stride - op.pw;
     }
@@ -580,11 +580,11 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       const uint32_t gi = g + i, stage = gi % STAGES;
       if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
       const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
+      const uint32_t b_dst = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
       const int k0 = (kb0 + i) * BK;
       if (wtid == 0) {
         mbar_expect_tx(&ctl->full[stage], bbytes);
-        tma_load_2d(ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES, op.tmap_b, &ctl->full[stage], k0,
-                    n0);
+        tma_load_2d(b_dst, op.tmap_b, &ctl->full[stage], k0, n0);
       }
       const int k = k0 + chunk * 8;
       const bool kok = k < op.K;
@@ -594,11 +594,13 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
 #pragma unroll
       for (int j = 0; j < ROWS; ++j) {
         const int row = rsub + RSTEP * j;
-        if (row < BM) {
+        if (row < rows_tile) {
           const int hi = hi0[j] + r, wi = wi0[j] + s;
           const bool ok = kok && hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
-          const __nv_bfloat16* src = ok ? img[j] + (static_cast<size_t>(hi) * op.W + wi) * op.ldi + c : in;
-          cp_async16(a_dst + row * 128 + ((chunk ^ (row & 7)) << 4), src, ok);
+          const __nv_bfloat16* src = ok ? in + img_off[j] + (static_cast<size_t>(hi) * op.W + wi) * op.ldi + c : in;
+          // rows of the second 128-row half land after the B block (M-pair tiles)
+          const uint32_t dst = row < BM ? a_dst + row * 128 : b_dst + A2_OFF + (row - BM) * 128;
+          cp_async16(dst + ((chunk ^ (row & 7)) << 4), src, ok);
         }
       }
       cp_async_commit();

@@ -629,19 +629,16 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           // narrow (Cout <= 128), very wide layers (>= 2 tiles per SM even
           // in pairs): half the items, so the per-item scheduling, epilogue
           // prologue and release costs are amortised over twice the work.
-          // They need TMA operand loads: a small-Cin layer switches from the
-          // gather to im2col with a 64-channel K stride (zero-filled).
           const long long m_rows = static_cast<long long>(B) * F.Ho * F.Wo;
           const int bn_est = F.Cout >= 128 ? 128 : roundup(F.Cout, 16);
           F.mrep = 1;
           // (a gather layer only if the im2col K stays short: a 7x7 stem
           //  would grow from 7 to 49 K-blocks)
-          const bool short_k = F.a_mode != A_GATHER || F.kh * F.kw <= 16;
-          if (!F.swap && F.Cout <= 128 && F.Cin <= 64 && short_k &&
-              cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= 2 * kSplitSms && !env_flag("GACER_NO_MPAIR")) {
+          // (the cp.async gather fills both 128-row halves too, so a small-Cin
+          //  layer keeps its short 8-channel K stride)
+          if (!F.swap && F.Cout <= 128 && F.Cin <= 64 &&
+              cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= 2 * kSplitSms && !env_flag("GACER_NO_MPAIR"))
             F.mrep = 2;
-            if (F.a_mode == A_GATHER) { F.a_mode = A_IM2COL; F.cread = c64; }
-          }
           // 1x1 stride-1 conv over a dense NHWC tensor is a plain GEMM: tiled TMA rows
           if (!F.swap && F.kh * F.kw == 1 && F.stride == 1 && o.pad_h == 0 && o.pad_w == 0 && c64 == c8 &&
               !env_flag("GACER_IM2COL_1X1")) {
