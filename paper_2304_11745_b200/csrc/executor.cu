@@ -1142,6 +1142,9 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 // any other item only when the ring is drained to depth 1, so a
 // latency-critical item of a small op never queues behind several long tiles
 // of a big op (head-of-line blocking inside the CTA).
+#ifndef GACER_NEWOP_DEPTH
+#define GACER_NEWOP_DEPTH 1   // in-flight depth allowed when the candidate starts a different op
+#endif
 __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = &g_ctl;
   uint32_t islot = 0, consumed = 0;
@@ -1204,7 +1207,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         }
         const int G1 = static_cast<int>(gridDim.x);
         const uint32_t allowed =
-            (cand.op != last_op) ? 1u : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
+            (cand.op != last_op) ? static_cast<uint32_t>(GACER_NEWOP_DEPTH) : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
                                                             : (cand.op_left > G1 ? 2u : 1u));
         sdbg(p, islot, 5, static_cast<int64_t>(allowed) * 1000 + (islot - consumed));
         while (islot - consumed >= allowed) {
