@@ -1,0 +1,68 @@
+"""the paper's Table 3 on B200 --
+V16(32) || R18(32) with the convs and the ReLUs after them batch-decomposed
+per the listed list_B (plans 1-5), executor makespan and bitwise-identical
+outputs.  The paper's latencies (80/66/72/78/85 ms on its GPU) are context;
+what is compared is the ORDERING (does plan 2 beat 1 and 5?).  Writes
+gpurun_out/d6_table3.json."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import bench  # noqa: E402
+import workloads  # noqa: E402
+from paper_2304_11745_b200 import gacer as G  # noqa: E402
+from paper_2304_11745_b200.runtime import Session  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PAPER_MS = {"1": 80, "2": 66, "3": 72, "4": 78, "5": 85}
+plans = []
+with open(os.path.join(ROOT, "tests", "golden", "table3_plans.txt")) as f:
+    for ln in f:
+        ln = ln.strip()
+        if ln and not ln.startswith("#"):
+            plans.append([t.strip() for t in ln.split("|")])
+names = ["vgg16", "resnet18"]
+tenants, xs = [], []
+for i, n in enumerate(names):
+    g = workloads.build_model(n)
+    tenants.append((g, workloads.make_params(g, 600 + i, "bf16"), 32, "bf16"))
+    xs.append(workloads.make_input(g, 32, 600 + i, "bf16"))
+stream = torch.cuda.Stream()
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda:0")
+torch.cuda.set_stream(stream)
+res = {"config": "V16(32) || R18(32), 224^2, bf16", "plans": {}}
+for part in ("priority", "work_conserving"):
+    s = Session(tenants, partition=part)
+    for t, x in enumerate(xs):
+        s.set_input(t, x)
+    ref = None
+    for pid, lv, lr in plans:
+        dec = []
+        for t, (g, lst) in enumerate(((tenants[0][0], lv), (tenants[1][0], lr))):
+            sizes = [int(v) for v in lst.split(",")]
+            if len(sizes) == 1:
+                continue
+            for i, op in enumerate(g.ops):
+                if op["kind"] == "conv" or (op["kind"] == "relu" and i > 0 and g.ops[i - 1]["kind"] == "conv"):
+                    dec.append((t, i + 1, "batch", sizes))
+        s.set_regulation(dec or None, None)
+        ms = float(np.median(bench.time_mode(G, s, torch, stream, "executor", 9, 3, flush)))
+        out = s.results()
+        same = ref is None or all(a.tobytes() == b.tobytes() for a, b in zip(ref, out))
+        ref = ref or out
+        res["plans"].setdefault(pid, {"v16_list_B": lv, "r18_list_B": lr, "paper_ms": PAPER_MS.get(pid)})
+        res["plans"][pid][f"{part}_ms"] = ms
+        res["plans"][pid][f"{part}_bitwise_equal_to_plan1"] = bool(same)
+        print(pid, lv, lr, part, f"{ms:.3f} ms", "identical" if same else "DIFFERENT", flush=True)
+    s.set_mode("sequential")
+    res[f"sequential_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, "sequential", 5, 2, flush)))
+    s.set_mode("multistream")
+    res[f"multistream_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, "multistream", 5, 2, flush)))
+    s.close()
+os.makedirs("gpurun_out", exist_ok=True)
+with open("gpurun_out/d6_table3.json", "w") as f:
+    json.dump(res, f, indent=1)
+print(json.dumps(res, indent=1))
