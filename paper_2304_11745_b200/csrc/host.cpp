@@ -149,6 +149,7 @@ struct Plan {
   std::vector<Seg> segs;
   std::vector<uint32_t> cluster_total;
   int n_chunk_counters = 0;
+  int input_counter0 = 0;                           // first of the per-tenant input-gate counters
   std::vector<std::vector<int>> fop_cluster;        // [tenant][fused op]
   std::vector<double> auto_share;                   // per tenant: SM need (work / chain latency)
 };
@@ -160,6 +161,7 @@ struct State {
   int num_sms = 148;
   gacer_options opts{};
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // host-buffer rounds: H2D copies + input gates
   std::vector<cudaStream_t> tstreams;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<Tenant> tenants;
@@ -843,7 +845,16 @@ OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
 
+PFN_cuStreamWriteValue32_v11070 g_write_value32 = nullptr;
+
 int load_tma_encoders() {
+  if (!g_write_value32) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q));
+    g_write_value32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
+    if (!g_write_value32) return set_err(GACER_E_CUDA, "cuStreamWriteValue32 not available");
+  }
   if (g_encode_tiled && g_encode_im2col) return 0;
   cudaDriverEntryPointQueryResult q;
   void* f = nullptr;
@@ -1041,6 +1052,11 @@ int compile_plan(Plan& P) {
       }
     }
   }
+  // one input-gate counter per tenant (after the chunk counters): the items
+  // that read the graph input wait for it, so a round whose H2D copies run on
+  // a copy stream starts each tenant as soon as its own input has landed
+  P.input_counter0 = counter;
+  counter += nt;
   P.n_chunk_counters = counter;
 
   // upward rank of every fused op (HEFT-style list scheduling): estimated
@@ -1140,8 +1156,9 @@ int compile_plan(Plan& P) {
             }
             std::set<int> dset;
             std::vector<Dep> dl;
+            if (F.in_t == 0) dl.push_back({P.input_counter0 + t, 1u});   // input gate (epoch-valued)
             for (int tin : {F.in_t, F.skip_t}) {
-              if (tin < 0) continue;
+              if (tin < 0 || tin == 0) continue;
               const Tensor& X = T.tensors[tin];
               const long long XHW = static_cast<long long>(X.H) * X.W;
               // flattened row range [lo, hi] of tensor tin this tile reads
@@ -1327,14 +1344,34 @@ int check_ready() {
   return 0;
 }
 
-int enqueue_round(cudaStream_t st, bool record_events = true) {
+// keep epoch*target far from 32-bit wrap (called before a round's epoch is used)
+int maybe_reset_epoch() {
+  if (S.epoch >= 0x7FFFFF00u / std::max<uint32_t>(1, 1 + static_cast<uint32_t>(S.plan.items.size())))
+    return reset_device_counters();
+  return 0;
+}
+
+// Input gates of round `ep` (executor modes): one epoch-valued counter per
+// tenant that the items reading the graph input wait for, written in stream
+// order on `st` (after that stream's input copies, if any).
+int write_input_gates(cudaStream_t st, uint32_t ep) {
+  for (size_t t = 0; t < S.tenants.size(); ++t) {
+    const CUdeviceptr a = reinterpret_cast<CUdeviceptr>(S.d_chunk_done + S.plan.input_counter0 + t);
+    if (g_write_value32(reinterpret_cast<CUstream>(st), a, ep, 0) != CUDA_SUCCESS)
+      return set_err(GACER_E_CUDA, "cuStreamWriteValue32 failed");
+  }
+  return 0;
+}
+
+int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written = false) {
   if (int rc = check_ready()) return rc;
   if (!st) st = S.stream;
   if (record_events) CUDA_TRY(cudaEventRecord(S.ev0, st));
   int launches = 0;
   if (S.mode == GACER_MODE_EXECUTOR) {
-    if (S.epoch >= 0x7FFFFF00u / std::max<uint32_t>(1, 1 + static_cast<uint32_t>(S.plan.items.size()))) {
-      if (int rc = reset_device_counters()) return rc;  // keep epoch*target far from wrap
+    if (!gates_written) {
+      if (int rc = maybe_reset_epoch()) return rc;
+      if (int rc = write_input_gates(st, S.epoch + 1)) return rc;
     }
     ExecParams p;
     std::memset(&p, 0, sizeof p);
@@ -1359,8 +1396,9 @@ int enqueue_round(cudaStream_t st, bool record_events = true) {
     // the paper's pointer mechanics (Fig. 6, Eq. 8): each cluster is issued
     // separately and the CPU waits for the GPU at every pointer before it
     // issues the next cluster -- the GPU idles for T_SW per pointer
-    if (S.epoch >= 0x7FFFFF00u / std::max<uint32_t>(1, 1 + static_cast<uint32_t>(S.plan.items.size()))) {
-      if (int rc = reset_device_counters()) return rc;
+    if (!gates_written) {
+      if (int rc = maybe_reset_epoch()) return rc;
+      if (int rc = write_input_gates(st, S.epoch + 1)) return rc;
     }
     ExecParams p;
     std::memset(&p, 0, sizeof p);
@@ -1505,6 +1543,8 @@ int gacer_shutdown(void) {
     if (S.d_tmaps) cudaFree(S.d_tmaps);
     for (cudaStream_t s : S.tstreams) cudaStreamDestroy(s);
     if (S.stream) cudaStreamDestroy(S.stream);
+    if (S.copy_stream) cudaStreamDestroy(S.copy_stream);
+    S.copy_stream = nullptr;
     if (S.ev0) cudaEventDestroy(S.ev0);
     if (S.ev1) cudaEventDestroy(S.ev1);
   }
@@ -1673,12 +1713,38 @@ int gacer_run_round_host(const void* const* host_inputs, void* const* host_outpu
   if (int rc = check_ready()) return rc;
   if (!host_inputs || !host_outputs) return set_err(GACER_E_INVALID_ARG, "NULL host arrays");
   CUDA_TRY(cudaEventRecord(S.ev0, S.stream));  // the e2e time includes both copies
-  for (size_t t = 0; t < S.tenants.size(); ++t) {
-    const Tenant& T = S.tenants[t];
-    const size_t bytes = static_cast<size_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
-    CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(T.in_dev), host_inputs[t], bytes, cudaMemcpyHostToDevice, S.stream));
+  const bool exec = S.mode == GACER_MODE_EXECUTOR || S.mode == GACER_MODE_EXECUTOR_HOSTSYNC;
+  if (exec) {
+    // executor: the input copies run on a copy stream, each followed by its
+    // tenant's input gate, while the round already runs -- a tenant's first
+    // items wait on the device for their own input only (copy/compute overlap)
+    if (!S.copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
+    if (int rc = maybe_reset_epoch()) return rc;
+    const uint32_t ep = S.epoch + 1;
+    CUDA_TRY(cudaStreamWaitEvent(S.copy_stream, S.ev0, 0));
+    for (size_t t = 0; t < S.tenants.size(); ++t) {
+      const Tenant& T = S.tenants[t];
+      const size_t bytes = static_cast<size_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
+      CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(T.in_dev), host_inputs[t], bytes, cudaMemcpyHostToDevice,
+                               S.copy_stream));
+      const CUdeviceptr a = reinterpret_cast<CUdeviceptr>(S.d_chunk_done + S.plan.input_counter0 + t);
+      if (g_write_value32(reinterpret_cast<CUstream>(S.copy_stream), a, ep, 0) != CUDA_SUCCESS)
+        return set_err(GACER_E_CUDA, "cuStreamWriteValue32 failed");
+    }
+    if (int rc = enqueue_round(S.stream, false, true)) return rc;
+    cudaEvent_t copied;   // the next round's copies must not overtake this one's reads
+    CUDA_TRY(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(copied, S.copy_stream));
+    CUDA_TRY(cudaStreamWaitEvent(S.stream, copied, 0));
+    cudaEventDestroy(copied);
+  } else {
+    for (size_t t = 0; t < S.tenants.size(); ++t) {
+      const Tenant& T = S.tenants[t];
+      const size_t bytes = static_cast<size_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
+      CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(T.in_dev), host_inputs[t], bytes, cudaMemcpyHostToDevice, S.stream));
+    }
+    if (int rc = enqueue_round(S.stream, false)) return rc;
   }
-  if (int rc = enqueue_round(S.stream, false)) return rc;
   for (size_t t = 0; t < S.tenants.size(); ++t) {
     const Tenant& T = S.tenants[t];
     CUDA_TRY(cudaMemcpyAsync(host_outputs[t], T.out_dev, static_cast<size_t>(T.batch) * T.out_features * 4,

@@ -129,3 +129,29 @@ def test_full_size_sampled_parity(cuda_ok, d2):
             r = forward_graph(g, p, x[n:n + 1])[0]
             err = np.max(np.abs(out[t][n] - r)) / np.max(np.abs(r))
             assert err <= 2e-2, (g.name, n, err)
+
+
+def test_host_buffer_round_matches_device_round(cuda_ok, d2):
+    """gacer_run_round_host (the e2e path): the input copies run on a copy
+    stream behind per-tenant input gates while the round already runs; the
+    outputs must be byte-identical to a round on device-resident inputs, for
+    several consecutive rounds and in both executor modes."""
+    import torch
+
+    from paper_2304_11745_b200 import gacer as G
+    from paper_2304_11745_b200.runtime import Session
+    ref, _ = run(d2)
+    s = Session([t[:4] for t in d2])
+    try:
+        host_in = [s.host_input(t, tt[4]) for t, tt in enumerate(d2)]
+        host_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in s.outputs]
+        for mode in ("executor", "executor_hostsync"):
+            s.set_mode(mode)
+            for _ in range(3):
+                for h in host_out:
+                    h.fill_(float("nan"))
+                G.gacer_run_round_host([h.data_ptr() for h in host_in], [h.data_ptr() for h in host_out])
+                for a, b in zip(ref, host_out):
+                    assert np.asarray(a).tobytes() == b.numpy().tobytes(), mode
+    finally:
+        s.close()
