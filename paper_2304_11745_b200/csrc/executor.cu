@@ -1815,6 +1815,10 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
   } else if (tid == 0) {
     ctl->n_segs_smem = 0;
   }
+  if (p.self_gates && blockIdx.x == 0 && tid == 0) {   // device-resident inputs: open the input gates
+    for (int i = 0; i < p.n_gates; ++i) atomicMax(p.chunk_done + p.gate0 + i, p.epoch);
+    fence_release_gpu();
+  }
   if (warp == MMA_WARP) tmem_alloc(&ctl->tmem_base, TMEM_COLS);
   tc_fence_before();
   __syncthreads();

@@ -143,6 +143,8 @@ struct ExecParams {
   int64_t* trace;           // optional [n_items * 8]
   int32_t n_tenants, n_clusters;
   int32_t k_first, k_last;  // clusters served by this launch (host-synchronised pointers: one each)
+  int32_t gate0, n_gates;   // per-tenant input-gate counters (chunk_done[gate0 .. gate0 + n_gates))
+  int32_t self_gates;       // 1: inputs are device-resident, the kernel opens the gates itself
   uint32_t epoch;           // round number since plan install, >= 1
   int32_t n_heads;
   int64_t watchdog_ns;

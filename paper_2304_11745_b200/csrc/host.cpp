@@ -1351,18 +1351,6 @@ int maybe_reset_epoch() {
   return 0;
 }
 
-// Input gates of round `ep` (executor modes): one epoch-valued counter per
-// tenant that the items reading the graph input wait for, written in stream
-// order on `st` (after that stream's input copies, if any).
-int write_input_gates(cudaStream_t st, uint32_t ep) {
-  for (size_t t = 0; t < S.tenants.size(); ++t) {
-    const CUdeviceptr a = reinterpret_cast<CUdeviceptr>(S.d_chunk_done + S.plan.input_counter0 + t);
-    if (g_write_value32(reinterpret_cast<CUstream>(st), a, ep, 0) != CUDA_SUCCESS)
-      return set_err(GACER_E_CUDA, "cuStreamWriteValue32 failed");
-  }
-  return 0;
-}
-
 int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written = false) {
   if (int rc = check_ready()) return rc;
   if (!st) st = S.stream;
@@ -1371,7 +1359,6 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
   if (S.mode == GACER_MODE_EXECUTOR) {
     if (!gates_written) {
       if (int rc = maybe_reset_epoch()) return rc;
-      if (int rc = write_input_gates(st, S.epoch + 1)) return rc;
     }
     ExecParams p;
     std::memset(&p, 0, sizeof p);
@@ -1390,6 +1377,9 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     if (const char* e = getenv("GACER_DBG_SPIN")) p.dbg_spin = atoll(e);
     p.k_first = 0;
     p.k_last = p.n_clusters - 1;
+    p.gate0 = S.plan.input_counter0;
+    p.n_gates = static_cast<int32_t>(S.tenants.size());
+    p.self_gates = gates_written ? 0 : 1;   // device-resident inputs: the kernel opens its gates
     CUDA_TRY(launch_executor(p, S.grid, st));
     launches = 1;
   } else if (S.mode == GACER_MODE_EXECUTOR_HOSTSYNC) {
@@ -1398,7 +1388,6 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     // issues the next cluster -- the GPU idles for T_SW per pointer
     if (!gates_written) {
       if (int rc = maybe_reset_epoch()) return rc;
-      if (int rc = write_input_gates(st, S.epoch + 1)) return rc;
     }
     ExecParams p;
     std::memset(&p, 0, sizeof p);
@@ -1413,8 +1402,13 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
+    p.gate0 = S.plan.input_counter0;
+    p.n_gates = static_cast<int32_t>(S.tenants.size());
+    bool first = true;
     for (int k = 0; k < p.n_clusters; ++k) {
       if (S.plan.cluster_total[k] == 0) continue;   // empty segment: nothing to issue
+      p.self_gates = (!gates_written && first) ? 1 : 0;   // the first launch opens the input gates
+      first = false;
       p.k_first = p.k_last = k;
       CUDA_TRY(launch_executor(p, S.grid, st));
       ++launches;
