@@ -359,12 +359,14 @@ def run_gacer(args, rank, world, dist):
                 traffic = json.load(f).get(args.config)
         except Exception:
             pass
+        fp32 = all(dt == "fp32" for *_, dt, _ in ts)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded inputs, random-init weights)",
+            "vs_baseline": None, "dtype": "f32" if fp32 else "bf16",
+            "data": "synthetic (seeded inputs, random-init weights)",
             "config": {"workload": args.config, "tenants": [f"{n}(B={B})" for n, _, _, B, _, _ in ts],
-                       "image": 224, "plan": best, "mode": "executor",
+                       "image": ts[0][1].in_h, "plan": best, "mode": "executor",
                        "parallelism": f"replica-per-gpu x{world}",
                        "l2": "flushed between steps (256 MB write, outside the events)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -372,6 +374,9 @@ def run_gacer(args, rank, world, dist):
                          "kernel": "gacer_executor",
                          "algorithmic": f"{flops / 1e9:.1f} GFLOP conv+FC (2*MAC) per launch",
                          "peak_source": f"{src} bf16_tflops (burst; kernel timed alone)"},
+            **({"roofline_note": "D1 (tiny fp32 tenants on CUDA cores) is latency-bound: a chain of "
+                                 "dependent single-tile ops; the TFLOP/s fraction is not meaningful"}
+               if fp32 else {}),
             "e2e": {"value": world * n_inf * args.steps / (e2e_total / 1000.0), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_round * args.steps,
@@ -400,7 +405,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gacer", choices=["gacer", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default=CONFIG, choices=["d2_r50_v16_mv2", "d3_five"])
+    ap.add_argument("--config", default=CONFIG, choices=["d1_tiny", "d2_r50_v16_mv2", "d3_five"])
     ap.add_argument("--plan", default="sweep", choices=["identity", "sweep"])
     ap.add_argument("--no-search", action="store_true", help="skip the Algorithm 1 plan search")
     ap.add_argument("--search-evals", type=int, default=30)

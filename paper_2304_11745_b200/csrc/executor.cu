@@ -624,31 +624,46 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
 // fp32 SIMT GEMM (fp32 tenants): conv / linear-as-conv, fixed K order
 // =====================================================================
 __device__ void simt_item(const OpDev& op, const Item& it, int tid, int nthr) {
+  // task = (output pixel m, 8 consecutive output channels): one input load
+  // feeds 8 FMAs, the 8 weights of a K step are two float4 loads from the
+  // K-outer weight layout [K][Cout rounded to 8].  Each output is still
+  // accumulated with fmaf in the fixed (r, s, c) order from 0.
   const float* in = static_cast<const float*>(op.in);
   const float* w = static_cast<const float*>(op.wt);
+  const int cpad = (op.Cout + 7) & ~7;
   const int m0 = it.mt * op.bm, n0 = it.nt * op.bn;
   const int HoWo = op.Ho * op.Wo;
-  for (int e = tid; e < op.bm * op.bn; e += nthr) {
-    const int m = m0 + e / op.bn, n = n0 + e % op.bn;
+  const int G = op.bn >> 3;
+  for (int e = tid; e < op.bm * G; e += nthr) {
+    const int m = m0 + e / G, n = n0 + (e % G) * 8;
     if (m >= op.M || n >= op.Cout) continue;
     const int b = m / HoWo, rem = m - b * HoWo, ho = rem / op.Wo, wo = rem - ho * op.Wo;
     const float* img = in + static_cast<size_t>(b) * op.H * op.W * op.ldi;
-    const float* wr = w + static_cast<size_t>(n) * op.K;
-    float acc = 0.0f;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int r = 0; r < op.kh; ++r) {
       const int hi = ho * op.stride - op.ph + r;
       for (int s = 0; s < op.kw; ++s) {
         const int wi = wo * op.stride - op.pw + s;
         const bool ok = hi >= 0 && hi < op.H && wi >= 0 && wi < op.W;
         const float* px = img + (static_cast<size_t>(hi) * op.W + wi) * op.ldi;
-        const float* wk = wr + (r * op.kw + s) * op.C;
-        for (int c = 0; c < op.C; ++c) acc = fmaf(ok ? px[c] : 0.0f, wk[c], acc);
+        const float* wk = w + static_cast<size_t>((r * op.kw + s) * op.C) * cpad + n;
+        for (int c = 0; c < op.C; ++c) {
+          const float x = ok ? px[c] : 0.0f;
+          const float4 w0 = *reinterpret_cast<const float4*>(wk + static_cast<size_t>(c) * cpad);
+          const float4 w1 = *reinterpret_cast<const float4*>(wk + static_cast<size_t>(c) * cpad + 4);
+          acc[0] = fmaf(x, w0.x, acc[0]); acc[1] = fmaf(x, w0.y, acc[1]);
+          acc[2] = fmaf(x, w0.z, acc[2]); acc[3] = fmaf(x, w0.w, acc[3]);
+          acc[4] = fmaf(x, w1.x, acc[4]); acc[5] = fmaf(x, w1.y, acc[5]);
+          acc[6] = fmaf(x, w1.z, acc[6]); acc[7] = fmaf(x, w1.w, acc[7]);
+        }
       }
     }
-    float y = fmaf(acc, op.scale[n], op.bias[n]);
-    if (op.has_skip) y += static_cast<const float*>(op.skip)[static_cast<size_t>(m) * op.lds + n];
-    y = apply_act(y, op.act);
-    static_cast<float*>(op.out)[static_cast<size_t>(m) * op.ldo + n] = y;
+    for (int j = 0; j < 8 && n + j < op.Cout; ++j) {
+      float y = fmaf(acc[j], op.scale[n + j], op.bias[n + j]);
+      if (op.has_skip) y += static_cast<const float*>(op.skip)[static_cast<size_t>(m) * op.lds + n + j];
+      y = apply_act(y, op.act);
+      static_cast<float*>(op.out)[static_cast<size_t>(m) * op.ldo + n + j] = y;
+    }
   }
 }
 

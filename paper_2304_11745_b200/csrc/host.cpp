@@ -610,12 +610,15 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         F.M = B * F.Ho * F.Wo; F.N = F.Cout;
         F.bm = 64; F.bn = 64;
         F.tiles_m = cdiv(F.M, F.bm); F.tiles_n = cdiv(F.Cout, F.bn);
-        F.w_f32.assign(static_cast<size_t>(F.Cout) * F.K, 0.0f);
+        // K-outer [K][Cout rounded to 8]: a thread's 8 output channels of one
+        // K step are two float4 loads (simt_item)
+        const int cpad = roundup(F.Cout, 8);
+        F.w_f32.assign(static_cast<size_t>(F.K) * cpad, 0.0f);
         for (int co = 0; co < F.Cout; ++co)
           for (int r = 0; r < F.kh; ++r)
             for (int s = 0; s < F.kw; ++s)
               for (int c = 0; c < F.Cin; ++c)
-                F.w_f32[static_cast<size_t>(co) * F.K + (r * F.kw + s) * F.cread + c] = wval(co, c, r, s);
+                F.w_f32[static_cast<size_t>((r * F.kw + s) * F.cread + c) * cpad + co] = wval(co, c, r, s);
       } else {
         F.swap = lin && X.ldc == X.C && F.skip_t < 0;
         // operand A: TMA im2col loads 64 channels of one tap per K-block and
