@@ -13,6 +13,11 @@ Contents
                   (§4.1 l.605-607; semantics SURVEY §8(c) C1), and
                   ``chunked_forward``: Eq. 5 applied literally (split, compute,
                   concat; §4.2 l.657-675).
+* ``train``    -- the training tenant (A11): BN-train forward, plain
+                  backward operators (``gacer_oracle_train.c``), mean
+                  softmax-CE, SGD momentum, and the replicas' gradient mean
+                  (A12, ``allreduce_mean``).  Pinned by finite differences,
+                  closed forms and PyTorch fp64 autograd (test_oracle_train.py).
 * ``plan``     -- the paper's plan semantics: segmentation by pointers (Eq. 7,
                   l.742-753) and clusters (Eq. 6, l.723-739).
 
@@ -21,5 +26,5 @@ for constant inputs, torch-CPU fp64 library routines for every operator and
 whole tenants, batch independence, Eq. 5 decomposition invariance, the Eq. 6/7
 worked examples of the paper (tests/golden/).
 """
-from . import ops, forward, plan  # noqa: F401
+from . import ops, forward, plan, train  # noqa: F401
 from .forward import forward_graph, chunked_forward  # noqa: F401

@@ -13,16 +13,17 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gacer_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "gacer_oracle_train.c")]   # forward ops, training backward ops
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc -O2 -fopenmp (no fast-math: IEEE fp64)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in _SRCS):
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared",
                                "-fno-fast-math", "-ffp-contract=off",
-                               "-o", _LIB, _SRC, "-lm"])
+                               "-o", _LIB, *_SRCS, "-lm"])
     return _LIB
 
 
