@@ -1,0 +1,101 @@
+/*
+ * gacer_train.h -- C ABI of the training tenant's CUDA-core operators
+ * (first part).
+ *
+ * A training tenant's step (SURVEY §8(c) "Training"; the paper trains with
+ * PyTorch defaults and states no hyper-parameters, §5.1 l.903-911)
+ * is: forward with BatchNorm in TRAINING mode (statistics of the replica's
+ * batch), mean softmax cross-entropy, backward, SGD with momentum.  This
+ * header exposes the HBM-bound, non-GEMM steps of that step as stream-ordered
+ * device calls, each the device twin of a function of the fp64 oracle
+ * (oracle/gacer_oracle_train.c) and checked against it per operator, fed the
+ * GPU's own bf16 tensors (SURVEY §8(c) C2b reading (1)).  The GEMM steps
+ * (conv dgrad / wgrad, linear backward on tcgen05) and their integration as
+ * executor work items are the next step of A11.
+ *
+ * Conventions:
+ *   - every tensor argument is a DEVICE pointer owned by the caller; no call
+ *     allocates, frees or synchronises; work is enqueued on `stream`
+ *     (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *   - activations are NHWC bf16, viewed as a row-major [M][C] matrix with
+ *     M = N*H*W rows (the executor's layout); C % 8 == 0 and 16-byte aligned
+ *     pointers are required (else GACER_E_SHAPE / GACER_E_INVALID_ARG).
+ *   - statistics, gradients of parameters, logits and SGD state are fp32.
+ *   - every reduction is summed in one fixed order: results are bitwise
+ *     reproducible run to run (north_star H4 applied to training).
+ *   - return GACER_OK (0) or a negative gacer_status (gacer.h); launch errors
+ *     return GACER_E_CUDA.
+ */
+#ifndef GACER_TRAIN_H_
+#define GACER_TRAIN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Scratch floats the BN reductions need: 2 * C * P partial sums plus 2 * C,
+ * with P = gacer_bn_partials(M, C) row blocks. */
+int32_t gacer_bn_partials(int64_t M, int32_t C);
+
+/* BatchNorm training forward (oracle_bn_train_fwd):
+ *   mean_c = (1/M) sum_m x[m,c],  var_c = (1/M) sum_m (x[m,c] - mean_c)^2 (biased),
+ *   y[m,c] = act(gamma_c (x[m,c] - mean_c) / sqrt(var_c + eps) + beta_c),
+ * act = ReLU when relu != 0 (the BN -> ReLU pair of a ResNet block), else
+ * identity.  x, y: bf16 [M][C] (y may alias x); gamma, beta: fp32 [C];
+ * mean, var: fp32 [C] outputs (saved for the backward); scratch: fp32,
+ * gacer_bn_partials(M, C) * 2 * C + 2 * C floats.  Per-block partial sums
+ * are fp32 in row order, combined across blocks in fp64 in block order. */
+int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float* gamma_dev,
+                           const float* beta_dev, float eps, int32_t relu, void* y_dev, float* mean_dev,
+                           float* var_dev, float* scratch_dev, void* stream);
+
+/* BatchNorm training backward (oracle_bn_train_bwd), xhat = (x - mean)/sqrt(var + eps):
+ *   dbeta_c = sum_m dy,  dgamma_c = sum_m dy * xhat,
+ *   dx = gamma_c / sqrt(var_c + eps) * (dy - dbeta_c / M - xhat * dgamma_c / M).
+ * x: the BN input (bf16 [M][C]), dy: the gradient of the BN output (bf16),
+ * mean/var from gacer_bn_train_fwd; outputs dx (bf16 [M][C], may alias dy),
+ * dgamma, dbeta (fp32 [C]); scratch as for the forward. */
+int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, int64_t M, int32_t C,
+                           const float* gamma_dev, const float* mean_dev, const float* var_dev, float eps,
+                           void* dx_dev, float* dgamma_dev, float* dbeta_dev, float* scratch_dev, void* stream);
+
+/* ReLU / ReLU6 backward on the forward INPUT x (oracle_relu_bwd):
+ * dx = dy where x > 0 (and x < 6 when six != 0), else 0.  bf16 [n]
+ * (n % 8 == 0); dx may alias dy. */
+int32_t gacer_relu_bwd(const void* x_dev, const void* dy_dev, int64_t n, int32_t six, void* dx_dev,
+                       void* stream);
+
+/* Max-pool backward, NHWC (oracle_maxpool_bwd): each output's gradient goes
+ * to the FIRST maximum of its window in row-major order,
+ * padded taps never win; gradients of an input shared by several windows are
+ * summed in (ho, wo) order (a gather: no atomics).  x: bf16 [N][H][W][C],
+ * dy: bf16 [N][Ho][Wo][C], dx: bf16 [N][H][W][C]. */
+int32_t gacer_maxpool_bwd(const void* x_dev, const void* dy_dev, int32_t N, int32_t H, int32_t W, int32_t C,
+                          int32_t KH, int32_t KW, int32_t stride, int32_t ph, int32_t pw, int32_t Ho, int32_t Wo,
+                          void* dx_dev, void* stream);
+
+/* Global-average-pool backward (oracle_gap_bwd): dx[n,p,c] = dy[n,c] / HW.
+ * dy: fp32 [N][C], dx: bf16 [N][HW][C]. */
+int32_t gacer_gap_bwd(const float* dy_dev, int32_t N, int32_t HW, int32_t C, void* dx_dev, void* stream);
+
+/* Mean softmax cross-entropy and its gradient (oracle_softmax_ce):
+ *   loss = (1/N) sum_n [logsumexp(z_n) - z_n[label_n]],
+ *   dz[n,j] = (softmax(z_n)_j - [j == label_n]) / N.
+ * z, dz: fp32 [N][Cls] (dz may alias z); labels: int32 [N] in [0, Cls)
+ * (out-of-range labels give loss = NaN for that row); loss: one fp32;
+ * scratch: N floats (per-row losses, summed in row order in fp64). */
+int32_t gacer_softmax_ce(const float* z_dev, const int32_t* labels_dev, int32_t N, int32_t Cls, float* loss_dev,
+                         float* dz_dev, float* scratch_dev, void* stream);
+
+/* SGD with momentum, PyTorch semantics (oracle_sgd_momentum):
+ * buf = g (first != 0) else momentum * buf + g;  w -= lr * buf.
+ * w, g, buf: fp32 [n], updated in place. */
+int32_t gacer_sgd_momentum(float* w_dev, const float* g_dev, float* buf_dev, int64_t n, float lr, float momentum,
+                           int32_t first, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GACER_TRAIN_H_ */

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgacer.so")
-SOURCES = ["host.cpp", "executor.cu"]
+SOURCES = ["host.cpp", "executor.cu", "train_ops.cu"]
 DEPS = SOURCES + ["gacer_dev.h"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Wno-deprecated-gpu-targets"]
@@ -17,8 +17,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    hdr = os.path.join(HERE, "..", "include", "gacer.h")
-    return any(os.path.getmtime(os.path.join(CSRC, f)) > t for f in DEPS) or os.path.getmtime(hdr) > t
+    hdrs = [os.path.join(HERE, "..", "include", h) for h in ("gacer.h", "gacer_train.h")]
+    return any(os.path.getmtime(os.path.join(CSRC, f)) > t for f in DEPS) or any(os.path.getmtime(h) > t for h in hdrs)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

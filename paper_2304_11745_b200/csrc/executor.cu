@@ -1121,7 +1121,10 @@ __device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& b
 
 __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, uint64_t t0, const OpDev& op) {
   // caller: all writes of the item are ordered before this thread (barrier);
-  // the release fence makes them visible at gpu scope before the counters
+  // the release fence makes them visible at gpu scope before the counters.
+  // The trace's end stamp is taken BEFORE the counters publish the item, so a
+  // dependent item's claim stamp is never earlier than it.
+  const uint64_t t_end = p.trace ? globaltimer() : 0;
   fence_release_gpu();
   dbg_mark(p, 8);
   atomicAdd(p.chunk_done + it.chunk, 1u);
@@ -1131,7 +1134,7 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
     int64_t* rec = p.trace + static_cast<size_t>(it.idx) * TRACE_FIELDS;
     rec[0] = op.tenant; rec[1] = it.op; rec[2] = smid(); rec[3] = it.idx;
     rec[4] = it.cluster; rec[5] = it.chunk;
-    rec[6] = static_cast<int64_t>(t0); rec[7] = static_cast<int64_t>(globaltimer());
+    rec[6] = static_cast<int64_t>(t0); rec[7] = static_cast<int64_t>(t_end);
   }
 }
 

@@ -47,6 +47,15 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+namespace gacer {
+// error reporting for the other translation units (train_ops.cu)
+int set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
+}  // namespace gacer
+
+namespace {
+
 // diagnostic switches: set and non-empty
 static bool env_flag(const char* name) {
   const char* v = getenv(name);

@@ -107,6 +107,19 @@ EXPORTS = {
     "gacer_get_trace": ([C.POINTER(C.c_int64), C.c_int32], C.c_int),
     "gacer_last_error": ([], C.c_char_p),
     "gacer_debug_timing": ([C.POINTER(C.c_int64), C.c_int64, C.c_int], C.c_int),
+    # include/gacer_train.h: training-tenant CUDA-core steps (device pointers as ints, stream as int)
+    "gacer_bn_partials": ([C.c_int64, C.c_int32], C.c_int32),
+    "gacer_bn_train_fwd": ([C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_float, C.c_int32,
+                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_bn_train_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                            C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_relu_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_maxpool_bwd": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 11 + [C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_gap_bwd": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_softmax_ce": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_void_p], C.c_int32),
+    "gacer_sgd_momentum": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_int32,
+                            C.c_void_p], C.c_int32),
 }
 
 _lib = None
@@ -319,3 +332,41 @@ def gacer_debug_timing(n_ops=1, reset=True, n_ctas=148, events=24):
     buf = np.zeros((n_ops, n_ctas, events), dtype=np.int64)
     _check(lib().gacer_debug_timing(buf.ctypes.data_as(C.POINTER(C.c_int64)), buf.size, int(reset)))
     return buf
+
+
+# ------------------------------------------------- training-tenant steps (A11)
+def _call(name, *args):
+    return _check(getattr(lib(), name)(*args))
+
+
+def bn_train_fwd(x, M, C_, gamma, beta, eps, relu, y, mean, var, scratch, stream=0):
+    """gacer_bn_train_fwd on device pointers (ints)."""
+    return _call("gacer_bn_train_fwd", x, M, C_, gamma, beta, eps, relu, y, mean, var, scratch, stream)
+
+
+def bn_train_bwd(x, dy, M, C_, gamma, mean, var, eps, dx, dgamma, dbeta, scratch, stream=0):
+    return _call("gacer_bn_train_bwd", x, dy, M, C_, gamma, mean, var, eps, dx, dgamma, dbeta, scratch, stream)
+
+
+def relu_bwd(x, dy, n, six, dx, stream=0):
+    return _call("gacer_relu_bwd", x, dy, n, six, dx, stream)
+
+
+def maxpool_bwd(x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, stream=0):
+    return _call("gacer_maxpool_bwd", x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, stream)
+
+
+def gap_bwd(dy, N, HW, C_, dx, stream=0):
+    return _call("gacer_gap_bwd", dy, N, HW, C_, dx, stream)
+
+
+def softmax_ce(z, labels, N, Cls, loss, dz, scratch, stream=0):
+    return _call("gacer_softmax_ce", z, labels, N, Cls, loss, dz, scratch, stream)
+
+
+def sgd_momentum(w, g, buf, n, lr, momentum, first, stream=0):
+    return _call("gacer_sgd_momentum", w, g, buf, n, lr, momentum, first, stream)
+
+
+def bn_partials(M, C_):
+    return lib().gacer_bn_partials(M, C_)

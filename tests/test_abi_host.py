@@ -23,14 +23,31 @@ def host():
 
 
 def test_exports_every_declared_symbol():
-    with open(os.path.join(ROOT, "include", "gacer.h")) as f:
-        hdr = f.read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(gacer_\w+)\s*\(", hdr, re.M))
-    assert len(declared) >= 14
+    declared = set()
+    for h in ("gacer.h", "gacer_train.h"):
+        with open(os.path.join(ROOT, "include", h)) as f:
+            hdr = f.read()
+        declared |= set(re.findall(r"^\s*(?:int|int32_t|const char\*)\s+(gacer_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 22
     lib = G.lib()
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(G.EXPORTS)
+
+
+def test_train_ops_reject_bad_shapes_without_touching_the_device():
+    """Argument validation of include/gacer_train.h runs on the host: bad
+    shapes / null pointers return an error code before any launch."""
+    with pytest.raises(G.GacerError) as e:
+        G.bn_train_fwd(16, 4, 12, 16, 16, 1e-5, 0, 16, 16, 16, 16)      # C % 8 != 0
+    assert e.value.name == "GACER_E_SHAPE"
+    with pytest.raises(G.GacerError) as e:
+        G.relu_bwd(0, 0, 8, 0, 0)
+    assert e.value.name == "GACER_E_INVALID_ARG"
+    with pytest.raises(G.GacerError) as e:
+        G.maxpool_bwd(16, 16, 1, 4, 4, 8, 3, 3, 2, 1, 1, 3, 2, 16)      # Ho inconsistent
+    assert e.value.name == "GACER_E_SHAPE"
+    assert G.bn_partials(100000, 64) == 148 * 4 and G.bn_partials(40, 64) == 2
 
 
 def chain_graph(n_ops, c=8, hw=4):

@@ -1,0 +1,147 @@
+"""GPU parity of the training tenant's CUDA-core steps (include/gacer_train.h,
+SURVEY §8(a) A11) against the fp64 oracle (oracle/train.py), per operator, fed
+the GPU's own bf16 tensors (SURVEY §8(c) C2b reading (1)).  Gates: max-norm
+relative error <= 2e-2 for bf16 outputs (Q2); fp32 statistics / parameter
+gradients within their fp32 rounding; bitwise reproducibility run to run.
+Shapes: ResNet-50 training tensors (B=64 replica at 56x56 / 7x7) cut down so
+the oracle finishes in seconds, plus ragged row counts that leave a partial
+row block."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def maxrel(a, r):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - r)) / max(np.max(np.abs(r)), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    from paper_2304_11745_b200 import gacer as G
+    from oracle import train as OT
+    return torch, G, OT
+
+
+def _bf16(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).cuda()
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _nchw(a, N, H, W, C):
+    return a.reshape(N, H, W, C).transpose(0, 3, 1, 2)
+
+
+@pytest.mark.parametrize("N,H,W,C", [(4, 14, 14, 64), (3, 7, 5, 256), (2, 7, 7, 2048), (5, 3, 3, 24)])
+def test_bn_train_fwd_bwd(T, N, H, W, C):
+    torch, G, OT = T
+    rng = np.random.default_rng(N * 1000 + C)
+    M = N * H * W
+    x = _bf16(torch, rng.normal(0.3, 1.7, size=(M, C)))
+    dy = _bf16(torch, rng.normal(0.0, 1.0, size=(M, C)))
+    gamma = torch.from_numpy(rng.uniform(0.5, 1.5, C).astype(np.float32)).cuda()
+    beta = torch.from_numpy(rng.uniform(-0.2, 0.2, C).astype(np.float32)).cuda()
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    mean, var, dg, db = (torch.empty(C, device="cuda") for _ in range(4))
+    scratch = torch.empty(G.bn_partials(M, C) * 2 * C + 2 * C, device="cuda")
+    for relu in (0, 1):
+        G.bn_train_fwd(x.data_ptr(), M, C, gamma.data_ptr(), beta.data_ptr(), 1e-5, relu, y.data_ptr(),
+                       mean.data_ptr(), var.data_ptr(), scratch.data_ptr())
+        torch.cuda.synchronize()
+        xn = _nchw(_np(x), N, H, W, C)
+        yo, mo, vo = OT.bn_train_fwd(xn, gamma.cpu().numpy(), beta.cpu().numpy(), 1e-5)
+        if relu:
+            yo = np.maximum(yo, 0)
+        assert maxrel(mean.cpu().numpy(), mo) < 1e-4 and maxrel(var.cpu().numpy(), vo) < 1e-4
+        assert maxrel(_nchw(_np(y), N, H, W, C), yo) <= 2e-2
+    G.bn_train_bwd(x.data_ptr(), dy.data_ptr(), M, C, gamma.data_ptr(), mean.data_ptr(), var.data_ptr(), 1e-5,
+                   dx.data_ptr(), dg.data_ptr(), db.data_ptr(), scratch.data_ptr())
+    torch.cuda.synchronize()
+    dxo, dgo, dbo = OT.bn_train_bwd(xn, _nchw(_np(dy), N, H, W, C), gamma.cpu().numpy(), mean.cpu().numpy().astype(np.float64),
+                                    var.cpu().numpy().astype(np.float64), 1e-5)
+    assert maxrel(dg.cpu().numpy(), dgo) < 1e-4
+    assert maxrel(db.cpu().numpy(), dbo) < 1e-4
+    assert maxrel(_nchw(_np(dx), N, H, W, C), dxo) <= 2e-2
+    # deterministic: a second backward is bitwise identical
+    dx2 = torch.empty_like(dx)
+    G.bn_train_bwd(x.data_ptr(), dy.data_ptr(), M, C, gamma.data_ptr(), mean.data_ptr(), var.data_ptr(), 1e-5,
+                   dx2.data_ptr(), dg.data_ptr(), db.data_ptr(), scratch.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx2)
+
+
+def test_relu_bwd_exact(T):
+    torch, G, OT = T
+    rng = np.random.default_rng(3)
+    vals = rng.normal(0, 4, size=4096)
+    vals[:6] = [0.0, 6.0, -0.0, 5.999, 6.001, 1e-30]
+    x = _bf16(torch, vals)
+    dy = _bf16(torch, rng.normal(size=4096))
+    for six in (0, 1):
+        dx = torch.empty_like(x)
+        G.relu_bwd(x.data_ptr(), dy.data_ptr(), 4096, six, dx.data_ptr())
+        torch.cuda.synchronize()
+        ref = OT.relu_bwd(_np(x), _np(dy), six=bool(six))
+        assert np.array_equal(_np(dx), ref)          # a mask: exact
+
+
+@pytest.mark.parametrize("N,H,W,C,k,s,p", [(2, 16, 16, 64, 3, 2, 1), (3, 9, 7, 16, 3, 2, 1), (2, 8, 8, 8, 2, 2, 0)])
+def test_maxpool_bwd(T, N, H, W, C, k, s, p):
+    torch, G, OT = T
+    rng = np.random.default_rng(H * W + C)
+    xv = rng.normal(size=(N, H, W, C))
+    xv[0, :2, :2, :] = 1.0                            # ties: first maximum in row-major order wins (Q14)
+    x = _bf16(torch, xv)
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    dy = _bf16(torch, rng.normal(size=(N, Ho, Wo, C)))
+    dx = torch.empty_like(x)
+    G.maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, W, C, k, k, s, p, p, Ho, Wo, dx.data_ptr())
+    torch.cuda.synchronize()
+    ref = OT.maxpool_bwd(_nchw(_np(x), N, H, W, C), _nchw(_np(dy), N, Ho, Wo, C), (k, k), s, (p, p))
+    got = _nchw(_np(dx), N, H, W, C)
+    assert np.array_equal(got != 0, ref != 0)           # the routing (argmax choice) is exact
+    assert maxrel(got, ref) <= 2e-2
+
+
+def test_gap_bwd_and_softmax_ce_and_sgd(T):
+    torch, G, OT = T
+    rng = np.random.default_rng(9)
+    N, HW, C = 6, 49, 2048
+    dy = torch.from_numpy(rng.normal(size=(N, C)).astype(np.float32)).cuda()
+    dx = torch.empty((N, HW, C), dtype=torch.bfloat16, device="cuda")
+    G.gap_bwd(dy.data_ptr(), N, HW, C, dx.data_ptr())
+    torch.cuda.synchronize()
+    ref = OT.gap_bwd(dy.cpu().numpy(), (N, C, 7, 7))
+    assert maxrel(_np(dx).transpose(0, 2, 1).reshape(N, C, 7, 7), ref) <= 2e-2
+    # softmax-CE over 1000 classes (ResNet-50's head), ragged row count
+    N, Cls = 13, 1000
+    z = torch.from_numpy((rng.normal(size=(N, Cls)) * 4).astype(np.float32)).cuda()
+    lab = rng.integers(0, Cls, size=N).astype(np.int32)
+    labels = torch.from_numpy(lab).cuda()
+    loss = torch.empty(1, device="cuda")
+    dz = torch.empty_like(z)
+    scratch = torch.empty(N, device="cuda")
+    G.softmax_ce(z.data_ptr(), labels.data_ptr(), N, Cls, loss.data_ptr(), dz.data_ptr(), scratch.data_ptr())
+    torch.cuda.synchronize()
+    lo, dzo = OT.softmax_ce(z.cpu().numpy(), lab)
+    assert abs(float(loss) - lo) / abs(lo) < 1e-5
+    assert maxrel(dz.cpu().numpy(), dzo) < 1e-5
+    # SGD momentum, two steps, vs the oracle's fp64 update
+    n = 100003
+    w0 = rng.normal(size=n).astype(np.float32)
+    g0, g1 = rng.normal(size=n).astype(np.float32), rng.normal(size=n).astype(np.float32)
+    w = torch.from_numpy(w0.copy()).cuda()
+    buf = torch.zeros(n, device="cuda")
+    for i, gg in enumerate((g0, g1)):
+        gt = torch.from_numpy(gg).cuda()
+        G.sgd_momentum(w.data_ptr(), gt.data_ptr(), buf.data_ptr(), n, 0.1, 0.9, int(i == 0))
+    torch.cuda.synchronize()
+    wr, br = w0.astype(np.float64), np.zeros(n)
+    OT.sgd_momentum(wr, g0, br, 0.1, 0.9, True)
+    OT.sgd_momentum(wr, g1, br, 0.1, 0.9, False)
+    assert np.max(np.abs(w.cpu().numpy() - wr)) < 1e-6
