@@ -9,9 +9,10 @@
  * header exposes the HBM-bound, non-GEMM steps of that step as stream-ordered
  * device calls, each the device twin of a function of the fp64 oracle
  * (oracle/gacer_oracle_train.c) and checked against it per operator, fed the
- * GPU's own bf16 tensors (SURVEY §8(c) C2b reading (1)).  The GEMM steps
- * (conv dgrad / wgrad, linear backward on tcgen05) and their integration as
- * executor work items are the next step of A11.
+ * GPU's own bf16 tensors (SURVEY §8(c) C2b reading (1)).  The tensor-core
+ * steps (conv dgrad / wgrad as implicit GEMMs on tcgen05) and the
+ * integration of the whole step as executor work items are the next step of
+ * A11; the FC backward (0.5 GFLOP for ResNet-50's head) runs on CUDA cores.
  *
  * Conventions:
  *   - every tensor argument is a DEVICE pointer owned by the caller; no call
@@ -35,8 +36,8 @@
 extern "C" {
 #endif
 
-/* Scratch floats the BN reductions need: 2 * C * P partial sums plus 2 * C,
- * with P = gacer_bn_partials(M, C) row blocks. */
+/* Scratch floats the BN calls need: 2 * C * P partial sums plus 4 * C
+ * per-channel constants, with P = gacer_bn_partials(M, C) row blocks. */
 int32_t gacer_bn_partials(int64_t M, int32_t C);
 
 /* BatchNorm training forward (oracle_bn_train_fwd):
@@ -45,7 +46,7 @@ int32_t gacer_bn_partials(int64_t M, int32_t C);
  * act = ReLU when relu != 0 (the BN -> ReLU pair of a ResNet block), else
  * identity.  x, y: bf16 [M][C] (y may alias x); gamma, beta: fp32 [C];
  * mean, var: fp32 [C] outputs (saved for the backward); scratch: fp32,
- * gacer_bn_partials(M, C) * 2 * C + 2 * C floats.  Per-block partial sums
+ * gacer_bn_partials(M, C) * 2 * C + 4 * C floats.  Per-block partial sums
  * are fp32 in row order, combined across blocks in fp64 in block order. */
 int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float* gamma_dev,
                            const float* beta_dev, float eps, int32_t relu, void* y_dev, float* mean_dev,
@@ -79,6 +80,15 @@ int32_t gacer_maxpool_bwd(const void* x_dev, const void* dy_dev, int32_t N, int3
 /* Global-average-pool backward (oracle_gap_bwd): dx[n,p,c] = dy[n,c] / HW.
  * dy: fp32 [N][C], dx: bf16 [N][HW][C]. */
 int32_t gacer_gap_bwd(const float* dy_dev, int32_t N, int32_t HW, int32_t C, void* dx_dev, void* stream);
+
+/* Fully-connected layer backward (oracle_linear_bwd), y[n,o] = b[o] + sum_k w[o,k] x[n,k]:
+ *   dx[n,k] = sum_o dy[n,o] w[o,k],  dw[o,k] = sum_n dy[n,o] x[n,k],  db[o] = sum_n dy[n,o].
+ * x: bf16 [N][K] (the saved forward input), w: fp32 [O][K] (master weights),
+ * dy: fp32 [N][O]; outputs dx fp32 [N][K] (may be NULL), dw fp32 [O][K],
+ * db fp32 [O] (may be NULL).  CUDA cores, one output per thread, summed in
+ * index order (ResNet-50's head: N=64, K=2048, O=1000, 0.5 GFLOP). */
+int32_t gacer_linear_bwd(const void* x_dev, const float* w_dev, const float* dy_dev, int32_t N, int32_t K, int32_t O,
+                         float* dx_dev, float* dw_dev, float* db_dev, void* stream);
 
 /* Mean softmax cross-entropy and its gradient (oracle_softmax_ce):
  *   loss = (1/N) sum_n [logsumexp(z_n) - z_n[label_n]],

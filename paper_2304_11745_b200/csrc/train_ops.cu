@@ -52,6 +52,10 @@ int num_partials(int64_t M) {
 // MODE 1: (sum dy, sum dy * xhat) with xhat = (x - mean) * invstd.
 // Thread layout: thread t owns 8-channel group g = t % G and row phase
 // t / G (RP phases), for channel groups g, g + G, ... when C / 8 > 256.
+// Four rows per thread are loaded before they are summed (16-byte loads in
+// flight: 4 x 4 KB per CTA); each thread still sums its rows in row order.
+constexpr int kUnroll = 4;
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) bn_partial_kernel(const __nv_bfloat16* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ dy, int64_t M, int C,
@@ -80,22 +84,34 @@ __global__ void __launch_bounds__(kThreads) bn_partial_kernel(const __nv_bfloat1
       }
     }
     if (ph < RP && g < G8) {
-      for (int64_t r = r0 + ph; r < r1; r += RP) {
-        float a[8];
-        unpack8(*reinterpret_cast<const uint4*>(x + r * C + g * 8), a);
-        if (MODE == 0) {
+      for (int64_t r = r0 + ph; r < r1; r += kUnroll * RP) {
+        uint4 va[kUnroll], vd[kUnroll];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            s1[j] += a[j];
-            s2[j] = fmaf(a[j], a[j], s2[j]);
-          }
-        } else {
-          float d[8];
-          unpack8(*reinterpret_cast<const uint4*>(dy + r * C + g * 8), d);
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t rr = r + u * RP;
+          va[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(x + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+          if (MODE == 1)
+            vd[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(dy + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            s1[j] += d[j];
-            s2[j] = fmaf(d[j], (a[j] - mu[j]) * is[j], s2[j]);
+        for (int u = 0; u < kUnroll; ++u) {
+          if (r + u * RP >= r1) break;
+          float a[8];
+          unpack8(va[u], a);
+          if (MODE == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              s1[j] += a[j];
+              s2[j] = fmaf(a[j], a[j], s2[j]);
+            }
+          } else {
+            float d[8];
+            unpack8(vd[u], d);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              s1[j] += d[j];
+              s2[j] = fmaf(d[j], (a[j] - mu[j]) * is[j], s2[j]);
+            }
           }
         }
       }
@@ -123,75 +139,99 @@ __global__ void __launch_bounds__(kThreads) bn_partial_kernel(const __nv_bfloat1
   }
 }
 
-// Combine the P partials of every channel in block order (fp64).
-// MODE 0 -> mean, biased var; MODE 1 -> dbeta = sum dy, dgamma = sum dy*xhat.
+// Combine the P partials of every channel in block order (fp64), then fold
+// the per-channel constants of the apply pass into `coef` (fp32 [k][C]):
+//   MODE 0 -> mean, biased var; coef = (scale, shift): y = x * scale + shift
+//   MODE 1 -> dgamma = sum dy*xhat, dbeta = sum dy; coef = (a, b, c):
+//             dx = a * dy + b * x + c  (the BN-backward formula expanded in x)
 template <int MODE>
-__global__ void bn_finalize_kernel(const float* __restrict__ part, int P, int64_t M, int C, float* __restrict__ o1,
-                                   float* __restrict__ o2) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void bn_finalize_kernel(const float* __restrict__ part, int P, int64_t M, int C,
+                                   const float* __restrict__ gamma, const float* __restrict__ beta,
+                                   const float* __restrict__ mean_in, const float* __restrict__ var_in, float eps,
+                                   float* __restrict__ o1, float* __restrict__ o2, float* __restrict__ coef) {
+  // one warp per channel: lane l sums partials l, l+32, ... in order, then a
+  // fixed xor-butterfly combines the lanes (the same order on every run)
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
   if (c >= C) return;
   double a = 0.0, b = 0.0;
-  for (int p = 0; p < P; ++p) {
+  for (int p = lane; p < P; p += 32) {
     a += part[(static_cast<size_t>(p) * 2 + 0) * C + c];
     b += part[(static_cast<size_t>(p) * 2 + 1) * C + c];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane != 0) return;
+  const double Md = static_cast<double>(M);
   if (MODE == 0) {
-    const double mu = a / static_cast<double>(M);
-    double v = b / static_cast<double>(M) - mu * mu;
+    const double mu = a / Md;
+    double v = b / Md - mu * mu;
+    v = v > 0.0 ? v : 0.0;
     o1[c] = static_cast<float>(mu);
-    o2[c] = static_cast<float>(v > 0.0 ? v : 0.0);
+    o2[c] = static_cast<float>(v);
+    const double sc = gamma[c] / sqrt(static_cast<double>(static_cast<float>(v)) + eps);
+    coef[c] = static_cast<float>(sc);
+    coef[C + c] = static_cast<float>(beta[c] - static_cast<double>(static_cast<float>(mu)) * sc);
   } else {
     o1[c] = static_cast<float>(b);   // dgamma
     o2[c] = static_cast<float>(a);   // dbeta
+    const double is = 1.0 / sqrt(static_cast<double>(var_in[c]) + eps);
+    const double gi = gamma[c] * is;
+    const double k = gi * is * static_cast<double>(static_cast<float>(b)) / Md;
+    coef[c] = static_cast<float>(gi);
+    coef[C + c] = static_cast<float>(-k);
+    coef[2 * C + c] = static_cast<float>(-gi * static_cast<double>(static_cast<float>(a)) / Md + k * mean_in[c]);
   }
 }
 
-// y = act(gamma (x - mean) invstd + beta)
-__global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16* x, int64_t M, int C,
-                                                            const float* __restrict__ gamma,
-                                                            const float* __restrict__ beta,
-                                                            const float* __restrict__ mean,
-                                                            const float* __restrict__ var, float eps, int relu,
-                                                            __nv_bfloat16* y) {
+// y = act(x * scale + shift); dx = a * dy + b * x + c.  Grid-stride over
+// 8-channel groups; the stride is a multiple of C/8 whenever C/8 divides 256
+// (every ResNet width), so a thread's channels are fixed and its constants
+// stay in registers.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) bn_elementwise_kernel(const __nv_bfloat16* x, const __nv_bfloat16* dy,
+                                                                  int64_t M, int C, const float* __restrict__ coef,
+                                                                  int relu, __nv_bfloat16* out) {
   const int G8 = C / 8;
   const int64_t n8 = M * G8;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c0 = static_cast<int>(i % G8) * 8;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool fixed = (stride % G8) == 0;
+  float k0[8], k1[8], k2[8];
+  int c0 = -1;
+  for (; i < n8; i += stride) {
+    const int c = (fixed && c0 >= 0) ? c0 : static_cast<int>(i % G8) * 8;
+    if (c != c0) {
+      c0 = c;
+      const float4* q0 = reinterpret_cast<const float4*>(coef + c);
+      const float4* q1 = reinterpret_cast<const float4*>(coef + C + c);
+      float4 u = q0[0], v = q0[1], w = q1[0], z = q1[1];
+      k0[0] = u.x; k0[1] = u.y; k0[2] = u.z; k0[3] = u.w; k0[4] = v.x; k0[5] = v.y; k0[6] = v.z; k0[7] = v.w;
+      k1[0] = w.x; k1[1] = w.y; k1[2] = w.z; k1[3] = w.w; k1[4] = z.x; k1[5] = z.y; k1[6] = z.z; k1[7] = z.w;
+      if (MODE == 1) {
+        const float4* q2 = reinterpret_cast<const float4*>(coef + 2 * C + c);
+        float4 p = q2[0], q = q2[1];
+        k2[0] = p.x; k2[1] = p.y; k2[2] = p.z; k2[3] = p.w; k2[4] = q.x; k2[5] = q.y; k2[6] = q.z; k2[7] = q.w;
+      }
+    }
     float a[8];
-    unpack8(reinterpret_cast<const uint4*>(x)[i], a);
+    unpack8(__ldcs(reinterpret_cast<const uint4*>(x) + i), a);
+    if (MODE == 0) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float is = rsqrtf(var[c0 + j] + eps);
-      float v = fmaf(gamma[c0 + j] * is, a[j] - mean[c0 + j], beta[c0 + j]);
-      a[j] = relu ? fmaxf(v, 0.0f) : v;
-    }
-    reinterpret_cast<uint4*>(y)[i] = pack8(a);
-  }
-}
-
-// dx = gamma invstd (dy - dbeta/M - xhat dgamma/M)
-__global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(
-    const __nv_bfloat16* x, const __nv_bfloat16* dy, int64_t M, int C,  // dx may alias dy (same-thread element)
-    const float* __restrict__ gamma, const float* __restrict__ mean, const float* __restrict__ var, float eps,
-    const float* __restrict__ dgamma, const float* __restrict__ dbeta, __nv_bfloat16* dx) {
-  const int G8 = C / 8;
-  const int64_t n8 = M * G8;
-  const float invM = 1.0f / static_cast<float>(M);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c0 = static_cast<int>(i % G8) * 8;
-    float a[8], d[8];
-    unpack8(reinterpret_cast<const uint4*>(x)[i], a);
-    unpack8(reinterpret_cast<const uint4*>(dy)[i], d);
+      for (int j = 0; j < 8; ++j) {
+        const float v = fmaf(a[j], k0[j], k1[j]);
+        a[j] = relu ? fmaxf(v, 0.0f) : v;
+      }
+    } else {
+      float d[8];
+      unpack8(__ldcs(reinterpret_cast<const uint4*>(dy) + i), d);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      const float is = rsqrtf(var[c] + eps);
-      const float xh = (a[j] - mean[c]) * is;
-      a[j] = gamma[c] * is * (d[j] - dbeta[c] * invM - xh * dgamma[c] * invM);
+      for (int j = 0; j < 8; ++j) a[j] = fmaf(k0[j], d[j], fmaf(k1[j], a[j], k2[j]));
     }
-    reinterpret_cast<uint4*>(dx)[i] = pack8(a);
+    __stcs(reinterpret_cast<uint4*>(out) + i, pack8(a));
   }
 }
 
@@ -276,6 +316,34 @@ __global__ void __launch_bounds__(kThreads) gap_bwd_kernel(const float* __restri
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = dy[static_cast<int64_t>(n) * C + g * 8 + j] * inv;
     reinterpret_cast<uint4*>(dx)[i] = pack8(v);
+  }
+}
+
+// FC backward: one output element per thread, reductions in index order
+__global__ void __launch_bounds__(kThreads) linear_dx_kernel(const float* __restrict__ w, const float* __restrict__ dy,
+                                                             int N, int K, int O, float* __restrict__ dx) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(N) * K) return;
+  const int n = static_cast<int>(i / K), k = static_cast<int>(i % K);
+  float a = 0.0f;
+  for (int o = 0; o < O; ++o) a = fmaf(dy[static_cast<int64_t>(n) * O + o], w[static_cast<int64_t>(o) * K + k], a);
+  dx[i] = a;
+}
+
+__global__ void __launch_bounds__(kThreads) linear_dw_kernel(const __nv_bfloat16* __restrict__ x,
+                                                             const float* __restrict__ dy, int N, int K, int O,
+                                                             float* __restrict__ dw, float* __restrict__ db) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(O) * K) return;
+  const int o = static_cast<int>(i / K), k = static_cast<int>(i % K);
+  float a = 0.0f;
+  for (int n = 0; n < N; ++n)
+    a = fmaf(dy[static_cast<int64_t>(n) * O + o], __bfloat162float(x[static_cast<int64_t>(n) * K + k]), a);
+  dw[i] = a;
+  if (db && k == 0) {
+    float b = 0.0f;
+    for (int n = 0; n < N; ++n) b += dy[static_cast<int64_t>(n) * O + o];
+    db[o] = b;
   }
 }
 
@@ -371,10 +439,12 @@ int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float*
   auto s = static_cast<cudaStream_t>(stream);
   const int P = num_partials(M);
   const auto* x = static_cast<const __nv_bfloat16*>(x_dev);
+  float* coef = scratch_dev + static_cast<size_t>(P) * 2 * C;
   bn_partial_kernel<0><<<P, kThreads, 0, s>>>(x, nullptr, M, C, nullptr, nullptr, 0.0f, scratch_dev);
-  bn_finalize_kernel<0><<<(C + 127) / 128, 128, 0, s>>>(scratch_dev, P, M, C, mean_dev, var_dev);
-  bn_apply_kernel<<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, M, C, gamma_dev, beta_dev, mean_dev, var_dev, eps,
-                                                             relu, static_cast<__nv_bfloat16*>(y_dev));
+  bn_finalize_kernel<0><<<(C + 7) / 8, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, beta_dev, nullptr, nullptr,
+                                                       eps, mean_dev, var_dev, coef);
+  bn_elementwise_kernel<0><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, nullptr, M, C, coef, relu,
+                                                                      static_cast<__nv_bfloat16*>(y_dev));
   return launched("bn_train_fwd");
 }
 
@@ -389,11 +459,12 @@ int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, int64_t M, int
   const int P = num_partials(M);
   const auto* x = static_cast<const __nv_bfloat16*>(x_dev);
   const auto* dy = static_cast<const __nv_bfloat16*>(dy_dev);
+  float* coef = scratch_dev + static_cast<size_t>(P) * 2 * C;
   bn_partial_kernel<1><<<P, kThreads, 0, s>>>(x, dy, M, C, mean_dev, var_dev, eps, scratch_dev);
-  bn_finalize_kernel<1><<<(C + 127) / 128, 128, 0, s>>>(scratch_dev, P, M, C, dgamma_dev, dbeta_dev);
-  bn_bwd_apply_kernel<<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, dy, M, C, gamma_dev, mean_dev, var_dev, eps,
-                                                                 dgamma_dev, dbeta_dev,
-                                                                 static_cast<__nv_bfloat16*>(dx_dev));
+  bn_finalize_kernel<1><<<(C + 7) / 8, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, nullptr, mean_dev, var_dev,
+                                                       eps, dgamma_dev, dbeta_dev, coef);
+  bn_elementwise_kernel<1><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, dy, M, C, coef, 0,
+                                                                      static_cast<__nv_bfloat16*>(dx_dev));
   return launched("bn_train_bwd");
 }
 
@@ -429,6 +500,22 @@ int32_t gacer_gap_bwd(const float* dy_dev, int32_t N, int32_t HW, int32_t C, voi
   gap_bwd_kernel<<<grid_for(static_cast<int64_t>(N) * HW * (C / 8)), kThreads, 0,
                    static_cast<cudaStream_t>(stream)>>>(dy_dev, N, HW, C, static_cast<__nv_bfloat16*>(dx_dev));
   return launched("gap_bwd");
+}
+
+int32_t gacer_linear_bwd(const void* x_dev, const float* w_dev, const float* dy_dev, int32_t N, int32_t K, int32_t O,
+                         float* dx_dev, float* dw_dev, float* db_dev, void* stream) {
+  if (N < 1 || K < 1 || O < 1) return bad(GACER_E_SHAPE, "linear_bwd: need N, K, O >= 1");
+  if (!x_dev || !w_dev || !dy_dev || !dw_dev) return bad(GACER_E_INVALID_ARG, "linear_bwd: null pointer");
+  auto s = static_cast<cudaStream_t>(stream);
+  if (dx_dev) {
+    const int64_t n = static_cast<int64_t>(N) * K;
+    linear_dx_kernel<<<static_cast<int>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(w_dev, dy_dev, N, K, O,
+                                                                                         dx_dev);
+  }
+  const int64_t n = static_cast<int64_t>(O) * K;
+  linear_dw_kernel<<<static_cast<int>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x_dev), dy_dev, N, K, O, dw_dev, db_dev);
+  return launched("linear_bwd");
 }
 
 int32_t gacer_softmax_ce(const float* z_dev, const int32_t* labels_dev, int32_t N, int32_t Cls, float* loss_dev,

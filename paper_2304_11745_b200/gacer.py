@@ -116,6 +116,8 @@ EXPORTS = {
     "gacer_relu_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_maxpool_bwd": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 11 + [C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_gap_bwd": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_linear_bwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                          C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_softmax_ce": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p], C.c_int32),
     "gacer_sgd_momentum": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_int32,
@@ -358,6 +360,10 @@ def maxpool_bwd(x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, stream=0
 
 def gap_bwd(dy, N, HW, C_, dx, stream=0):
     return _call("gacer_gap_bwd", dy, N, HW, C_, dx, stream)
+
+
+def linear_bwd(x, w, dy, N, K, O, dx, dw, db, stream=0):
+    return _call("gacer_linear_bwd", x, w, dy, N, K, O, dx, dw, db, stream)
 
 
 def softmax_ce(z, labels, N, Cls, loss, dz, scratch, stream=0):

@@ -48,7 +48,7 @@ def test_bn_train_fwd_bwd(T, N, H, W, C):
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
     mean, var, dg, db = (torch.empty(C, device="cuda") for _ in range(4))
-    scratch = torch.empty(G.bn_partials(M, C) * 2 * C + 2 * C, device="cuda")
+    scratch = torch.empty(G.bn_partials(M, C) * 2 * C + 4 * C, device="cuda")
     for relu in (0, 1):
         G.bn_train_fwd(x.data_ptr(), M, C, gamma.data_ptr(), beta.data_ptr(), 1e-5, relu, y.data_ptr(),
                        mean.data_ptr(), var.data_ptr(), scratch.data_ptr())
@@ -145,3 +145,19 @@ def test_gap_bwd_and_softmax_ce_and_sgd(T):
     OT.sgd_momentum(wr, g0, br, 0.1, 0.9, True)
     OT.sgd_momentum(wr, g1, br, 0.1, 0.9, False)
     assert np.max(np.abs(w.cpu().numpy() - wr)) < 1e-6
+
+
+@pytest.mark.parametrize("N,K,O", [(64, 2048, 1000), (5, 37, 11)])
+def test_linear_bwd(T, N, K, O):
+    torch, G, OT = T
+    rng = np.random.default_rng(K)
+    x = _bf16(torch, rng.normal(size=(N, K)))
+    w = torch.from_numpy(rng.normal(0, 0.05, size=(O, K)).astype(np.float32)).cuda()
+    dy = torch.from_numpy(rng.normal(size=(N, O)).astype(np.float32)).cuda()
+    dx, dw, db = torch.empty((N, K), device="cuda"), torch.empty((O, K), device="cuda"), torch.empty(O, device="cuda")
+    G.linear_bwd(x.data_ptr(), w.data_ptr(), dy.data_ptr(), N, K, O, dx.data_ptr(), dw.data_ptr(), db.data_ptr())
+    torch.cuda.synchronize()
+    rx, rw, rb = OT.linear_bwd(_np(x), w.cpu().numpy(), dy.cpu().numpy())
+    assert maxrel(dx.cpu().numpy(), rx) < 1e-5
+    assert maxrel(dw.cpu().numpy(), rw) < 1e-5
+    assert maxrel(db.cpu().numpy(), rb) < 1e-5
