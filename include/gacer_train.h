@@ -72,10 +72,11 @@ int32_t gacer_relu_bwd(const void* x_dev, const void* dy_dev, int64_t n, int32_t
  * to the FIRST maximum of its window in row-major order,
  * padded taps never win; gradients of an input shared by several windows are
  * summed in (ho, wo) order (a gather: no atomics).  x: bf16 [N][H][W][C],
- * dy: bf16 [N][Ho][Wo][C], dx: bf16 [N][H][W][C]. */
+ * dy: bf16 [N][Ho][Wo][C], dx: bf16 [N][H][W][C]; scratch: N*Ho*Wo*C bytes
+ * (8-byte aligned) for the windows' argmax tap indices (KH*KW <= 255). */
 int32_t gacer_maxpool_bwd(const void* x_dev, const void* dy_dev, int32_t N, int32_t H, int32_t W, int32_t C,
                           int32_t KH, int32_t KW, int32_t stride, int32_t ph, int32_t pw, int32_t Ho, int32_t Wo,
-                          void* dx_dev, void* stream);
+                          void* dx_dev, void* scratch_dev, void* stream);
 
 /* Global-average-pool backward (oracle_gap_bwd): dx[n,p,c] = dy[n,c] / HW.
  * dy: fp32 [N][C], dx: bf16 [N][HW][C]. */

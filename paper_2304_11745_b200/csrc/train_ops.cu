@@ -249,9 +249,48 @@ __global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const __nv_bfloat16*
   }
 }
 
-// One thread per (input pixel, 8-channel group): gathers the gradients of the
-// windows that cover it and whose first maximum it is, in (ho, wo) order.
-__global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
+// Max-pool backward in two passes.  Pass 1, one thread per (output window,
+// 8-channel group): the window's first maximum per channel (row-major tap
+// order, padded taps skipped) as a tap index byte.  Pass 2, one thread per
+// (input pixel, 8-channel group): gathers dy of the windows covering the
+// pixel whose recorded tap is this pixel, in (ho, wo) order -- no atomics.
+__global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                                  int W, int C, int KH, int KW, int S, int ph, int pw,
+                                                                  int Ho, int Wo, uint8_t* __restrict__ arg) {
+  const int G8 = C / 8;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * G8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int wo = static_cast<int>(pix % Wo), ho = static_cast<int>((pix / Wo) % Ho);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(Wo) * Ho));
+    float best[8];
+    uint32_t tap[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; tap[j] = 255u; }
+    for (int r = 0; r < KH; ++r) {
+      const int hh = ho * S - ph + r;
+      if (hh < 0 || hh >= H) continue;
+      for (int q = 0; q < KW; ++q) {
+        const int ww = wo * S - pw + q;
+        if (ww < 0 || ww >= W) continue;
+        float v[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hh) * W + ww) * C + g * 8), v);
+        const uint32_t id = static_cast<uint32_t>(r * KW + q);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (tap[j] == 255u || v[j] > best[j]) { best[j] = v[j]; tap[j] = id; }
+      }
+    }
+    uint2 o;
+    o.x = tap[0] | (tap[1] << 8) | (tap[2] << 16) | (tap[3] << 24);
+    o.y = tap[4] | (tap[5] << 8) | (tap[6] << 16) | (tap[7] << 24);
+    reinterpret_cast<uint2*>(arg)[i] = o;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __restrict__ arg,
                                                                const __nv_bfloat16* __restrict__ dy, int N, int H,
                                                                int W, int C, int KH, int KW, int S, int ph, int pw,
                                                                int Ho, int Wo, __nv_bfloat16* __restrict__ dx) {
@@ -261,7 +300,8 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int g = static_cast<int>(i % G8);
     const int64_t pix = i / G8;
-    const int wi = static_cast<int>(pix % W), hi = static_cast<int>((pix / W) % H), n = static_cast<int>(pix / (static_cast<int64_t>(W) * H));
+    const int wi = static_cast<int>(pix % W), hi = static_cast<int>((pix / W) % H);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(W) * H));
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // windows with ho*S - ph <= hi <= ho*S - ph + KH - 1
     int ho0 = hi + ph - KH + 1;
@@ -274,30 +314,20 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat
     wo1 = wo1 < Wo - 1 ? wo1 : Wo - 1;
     for (int ho = ho0; ho <= ho1; ++ho)
       for (int wo = wo0; wo <= wo1; ++wo) {
-        float best[8];
-        int arg[8];
+        const int64_t o = ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * G8 + g;
+        const uint2 t = reinterpret_cast<const uint2*>(arg)[o];
+        const uint32_t me = static_cast<uint32_t>((hi - (ho * S - ph)) * KW + (wi - (wo * S - pw)));
+        const uint32_t tt[8] = {t.x & 255u, (t.x >> 8) & 255u, (t.x >> 16) & 255u, t.x >> 24,
+                                t.y & 255u, (t.y >> 8) & 255u, (t.y >> 16) & 255u, t.y >> 24};
+        bool any = false;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; arg[j] = -1; }
-        for (int r = 0; r < KH; ++r) {
-          const int hh = ho * S - ph + r;
-          if (hh < 0 || hh >= H) continue;
-          for (int s = 0; s < KW; ++s) {
-            const int ww = wo * S - pw + s;
-            if (ww < 0 || ww >= W) continue;
-            float v[8];
-            unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hh) * W + ww) * C + g * 8), v);
-            const int id = hh * W + ww;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (arg[j] < 0 || v[j] > best[j]) { best[j] = v[j]; arg[j] = id; }
-          }
-        }
+        for (int j = 0; j < 8; ++j) any |= tt[j] == me;
+        if (!any) continue;
         float d[8];
-        unpack8(*reinterpret_cast<const uint4*>(dy + ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * C + g * 8), d);
-        const int me = hi * W + wi;
+        unpack8(reinterpret_cast<const uint4*>(dy)[o], d);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (arg[j] == me) acc[j] += d[j];
+          if (tt[j] == me) acc[j] += d[j];
       }
     reinterpret_cast<uint4*>(dx)[i] = pack8(acc);
   }
@@ -481,16 +511,20 @@ int32_t gacer_relu_bwd(const void* x_dev, const void* dy_dev, int64_t n, int32_t
 
 int32_t gacer_maxpool_bwd(const void* x_dev, const void* dy_dev, int32_t N, int32_t H, int32_t W, int32_t C,
                           int32_t KH, int32_t KW, int32_t stride, int32_t ph, int32_t pw, int32_t Ho, int32_t Wo,
-                          void* dx_dev, void* stream) {
-  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || KH < 1 || KW < 1 || stride < 1 || ph < 0 || pw < 0 ||
-      Ho != (H + 2 * ph - KH) / stride + 1 || Wo != (W + 2 * pw - KW) / stride + 1 || Ho < 1 || Wo < 1)
+                          void* dx_dev, void* scratch_dev, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || KH < 1 || KW < 1 || KH * KW > 255 || stride < 1 || ph < 0 ||
+      pw < 0 || Ho != (H + 2 * ph - KH) / stride + 1 || Wo != (W + 2 * pw - KW) / stride + 1 || Ho < 1 || Wo < 1)
     return bad(GACER_E_SHAPE, "maxpool_bwd: inconsistent shape");
-  if (!x_dev || !dy_dev || !dx_dev || !aligned16(x_dev) || !aligned16(dy_dev) || !aligned16(dx_dev))
+  if (!x_dev || !dy_dev || !dx_dev || !scratch_dev || !aligned16(x_dev) || !aligned16(dy_dev) || !aligned16(dx_dev) ||
+      (reinterpret_cast<uintptr_t>(scratch_dev) & 7u))
     return bad(GACER_E_INVALID_ARG, "maxpool_bwd: null or misaligned pointer");
-  maxpool_bwd_kernel<<<grid_for(static_cast<int64_t>(N) * H * W * (C / 8)), kThreads, 0,
-                       static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x_dev), static_cast<const __nv_bfloat16*>(dy_dev), N, H, W, C, KH, KW,
-      stride, ph, pw, Ho, Wo, static_cast<__nv_bfloat16*>(dx_dev));
+  auto s = static_cast<cudaStream_t>(stream);
+  auto* arg = static_cast<uint8_t*>(scratch_dev);
+  maxpool_argmax_kernel<<<grid_for(static_cast<int64_t>(N) * Ho * Wo * (C / 8)), kThreads, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x_dev), N, H, W, C, KH, KW, stride, ph, pw, Ho, Wo, arg);
+  maxpool_bwd_kernel<<<grid_for(static_cast<int64_t>(N) * H * W * (C / 8)), kThreads, 0, s>>>(
+      arg, static_cast<const __nv_bfloat16*>(dy_dev), N, H, W, C, KH, KW, stride, ph, pw, Ho, Wo,
+      static_cast<__nv_bfloat16*>(dx_dev));
   return launched("maxpool_bwd");
 }
 

@@ -114,7 +114,8 @@ EXPORTS = {
     "gacer_bn_train_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_relu_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
-    "gacer_maxpool_bwd": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 11 + [C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_maxpool_bwd": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 11 + [C.c_void_p, C.c_void_p, C.c_void_p],
+                          C.c_int32),
     "gacer_gap_bwd": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_linear_bwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                           C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
@@ -354,8 +355,8 @@ def relu_bwd(x, dy, n, six, dx, stream=0):
     return _call("gacer_relu_bwd", x, dy, n, six, dx, stream)
 
 
-def maxpool_bwd(x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, stream=0):
-    return _call("gacer_maxpool_bwd", x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, stream)
+def maxpool_bwd(x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, scratch, stream=0):
+    return _call("gacer_maxpool_bwd", x, dy, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, dx, scratch, stream)
 
 
 def gap_bwd(dy, N, HW, C_, dx, stream=0):

@@ -7,6 +7,7 @@ Algorithmic bytes per call (the two-pass algorithms' minimum traffic):
   bn_train_bwd  read x, dy twice (sums, apply) + write dx          = 5 * M*C*2 B
   relu_bwd      read x, dy + write dx                              = 3 * n*2 B
   maxpool_bwd   read x, dy + write dx (3x3/s2/p1 stem pool)        = (2*H*W + Ho*Wo)*N*C*2 B
+                (the argmax bytes, N*Ho*Wo*C, are not counted)
 Inputs are far larger than L2 (126 MB) except where noted; timings are CUDA
 events over 20 back-to-back calls after 3 warm-up calls.
 
@@ -63,7 +64,9 @@ def main():
     x = torch.randn(N * H * H * C, device="cuda").to(torch.bfloat16)
     dy = torch.randn(N * 56 * 56 * C, device="cuda").to(torch.bfloat16)
     dx = torch.empty_like(x)
-    t = timed(lambda: G.maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, H, C, 3, 3, 2, 1, 1, 56, 56, dx.data_ptr()))
+    arg = torch.empty(N * 56 * 56 * C, dtype=torch.uint8, device="cuda")
+    t = timed(lambda: G.maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, H, C, 3, 3, 2, 1, 1, 56, 56, dx.data_ptr(),
+                                    arg.data_ptr()))
     rows.append(("maxpool_bwd", "[64,112,112,64] 3x3/s2/p1", (2 * H * H + 56 * 56) * N * C * 2, t))
     out = []
     print(f"{'op':14s} {'shape':28s} {'MB':>8s} {'us':>8s} {'GB/s':>8s} {'frac':>6s}")

@@ -45,7 +45,7 @@ def test_train_ops_reject_bad_shapes_without_touching_the_device():
         G.relu_bwd(0, 0, 8, 0, 0)
     assert e.value.name == "GACER_E_INVALID_ARG"
     with pytest.raises(G.GacerError) as e:
-        G.maxpool_bwd(16, 16, 1, 4, 4, 8, 3, 3, 2, 1, 1, 3, 2, 16)      # Ho inconsistent
+        G.maxpool_bwd(16, 16, 1, 4, 4, 8, 3, 3, 2, 1, 1, 3, 2, 16, 16)  # Ho inconsistent
     assert e.value.name == "GACER_E_SHAPE"
     assert G.bn_partials(100000, 64) == 148 * 4 and G.bn_partials(40, 64) == 2
 

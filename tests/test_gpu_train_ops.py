@@ -100,7 +100,8 @@ def test_maxpool_bwd(T, N, H, W, C, k, s, p):
     Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
     dy = _bf16(torch, rng.normal(size=(N, Ho, Wo, C)))
     dx = torch.empty_like(x)
-    G.maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, W, C, k, k, s, p, p, Ho, Wo, dx.data_ptr())
+    arg = torch.empty(N * Ho * Wo * C, dtype=torch.uint8, device="cuda")
+    G.maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, W, C, k, k, s, p, p, Ho, Wo, dx.data_ptr(), arg.data_ptr())
     torch.cuda.synchronize()
     ref = OT.maxpool_bwd(_nchw(_np(x), N, H, W, C), _nchw(_np(dy), N, Ho, Wo, C), (k, k), s, (p, p))
     got = _nchw(_np(dx), N, H, W, C)
