@@ -140,3 +140,24 @@ def test_tenant_parity_d3_models(cuda_ok, name, hw, B):
     outs, _ = run_session([t])
     g, p, B, dt, x = t
     assert maxrel(outs[0], forward_graph(g, p, x)) <= 2e-2
+
+
+@pytest.mark.parametrize("cin,cout,k,pad,hw,B", [(64, 64, 3, 1, 14, 2), (256, 64, 1, 0, 14, 3), (64, 128, 3, 1, 28, 2)])
+def test_conv_dgrad_as_forward_conv(cuda_ok, cin, cout, k, pad, hw, B):
+    """A11 design check: the data gradient of a stride-1 conv IS a forward
+    conv of dy with the flipped, transposed filter, w'[ci,co,r,s] =
+    w[co,ci,K-1-r,K-1-s], pad K-1-p -- so it runs on the same tcgen05
+    implicit-GEMM path.  Executor output vs the oracle's dgrad (plain scatter
+    definition, oracle/gacer_oracle_train.c)."""
+    from oracle import train as OT
+    g = workloads.Graph("dgrad", cout, hw, hw)
+    g.conv(0, cout, cin, k, 1, k - 1 - pad)
+    w = workloads.make_params(g, 5 + cin, "bf16")[1]["w"]
+    w = w.reshape(cin, cout, k, k)                       # any bf16 filter of the forward conv [cout][cin]
+    w_fwd = np.ascontiguousarray(w.transpose(1, 0, 2, 3))          # forward filter [cout][cin][k][k]
+    w_dg = np.ascontiguousarray(w_fwd[:, :, ::-1, ::-1].transpose(1, 0, 2, 3))   # [cin][cout][k][k]
+    dy = workloads.make_input(g, B, 9 + cout, "bf16")              # [B][cout][hw][hw]
+    outs, _ = run_session([(g, {1: {"w": w_dg}}, B, "bf16", dy)])
+    got = nhwc_to_nchw(outs[0], B, hw, hw, cin)
+    ref, _, _ = OT.conv2d_bwd(np.zeros((B, cin, hw, hw)), w_fwd, dy, 1, (pad, pad))
+    assert maxrel(got, ref) <= 2e-2
