@@ -30,6 +30,9 @@ cudaError_t configure_kernels();
 cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s);
 cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, int kind, int n_items, int num_sms,
                       cudaStream_t s);
+cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
+                                void* out, cudaStream_t s);
+cudaError_t launch_fill(float* p, int n, float v, cudaStream_t s);
 }  // namespace gacer
 
 using namespace gacer;
@@ -1797,6 +1800,125 @@ int gacer_debug_timing(int64_t* out, int64_t cap, int reset) {
   if (out) CUDA_TRY(cudaMemcpy(out, S.d_dbg, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
   if (reset) CUDA_TRY(cudaMemset(S.d_dbg, 0, S.n_dbg * sizeof(int64_t)));
   return static_cast<int>(n);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// A11: convolution data gradient on the tcgen05 implicit-GEMM path
+// ------------------------------------------------------------------------
+namespace {
+struct DgradGeom {
+  int cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode, ph, pw, Hd, Wd;
+  size_t off_op, off_maps, off_scale, off_bias, off_w, bytes;
+};
+
+int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int pad_h, int pad_w, DgradGeom& g) {
+  if (N < 1 || H < 1 || W < 1 || Cin < 8 || Cin % 8 || Cout < 64 || Cout % 64 || KH < 1 || KW < 1 || pad_h < 0 ||
+      pad_w < 0 || pad_h > KH - 1 || pad_w > KW - 1)
+    return set_err(GACER_E_SHAPE, "conv_dgrad: need Cin %% 8 == 0, Cout %% 64 == 0, 0 <= pad <= k-1");
+  g.Hd = H + 2 * pad_h - KH + 1;                      // dy spatial size (forward output, stride 1)
+  g.Wd = W + 2 * pad_w - KW + 1;
+  if (g.Hd < 1 || g.Wd < 1) return set_err(GACER_E_SHAPE, "conv_dgrad: empty forward output");
+  g.ph = KH - 1 - pad_h;                              // the dgrad conv's padding
+  g.pw = KW - 1 - pad_w;
+  g.cread = Cout;                                     // dy channels, a multiple of 64
+  g.a_mode = (KH * KW == 1 && g.ph == 0 && g.pw == 0) ? A_ROWS : A_IM2COL;
+  g.K = KH * KW * g.cread;
+  g.Kpad = roundup(g.K, BK);
+  g.nkb = g.Kpad / BK;
+  g.M = N * H * W;
+  g.bn = Cin >= 128 ? 128 : roundup(Cin, 16);
+  g.tiles_m = cdiv(g.M, BM);
+  g.tiles_n = cdiv(Cin, g.bn);
+  g.rows = g.tiles_n * g.bn;
+  const int nsb = roundup(Cin, 8) + 8;
+  size_t o = 0;
+  auto take = [&](size_t n, size_t al) { o = (o + al - 1) / al * al; const size_t r = o; o += n; return r; };
+  g.off_op = take(sizeof(OpDev), 256);
+  g.off_maps = take(3 * sizeof(CUtensorMap), 128);
+  g.off_scale = take(nsb * sizeof(float), 16);
+  g.off_bias = take(nsb * sizeof(float), 16);
+  g.off_w = take(static_cast<size_t>(g.rows) * g.Kpad * 2, 256);
+  g.bytes = o;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t gacer_conv_dgrad_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
+                                   int32_t pad_h, int32_t pad_w) {
+  DgradGeom g;
+  if (int rc = dgrad_geom(N, H, W, Cin, Cout, KH, KW, pad_h, pad_w, g)) return rc;
+  return static_cast<int64_t>(g.bytes);
+}
+
+int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                         int32_t Cout, int32_t KH, int32_t KW, int32_t pad_h, int32_t pad_w, void* dx_dev,
+                         void* ws_dev, int64_t ws_bytes, void* stream) {
+  if (!S.inited || S.host_only) return set_err(GACER_E_STATE, "conv_dgrad: gacer_init on a device first");
+  DgradGeom g;
+  if (int rc = dgrad_geom(N, H, W, Cin, Cout, KH, KW, pad_h, pad_w, g)) return rc;
+  if (!dy_dev || !w_dev || !dx_dev || !ws_dev || ws_bytes < static_cast<int64_t>(g.bytes) ||
+      (reinterpret_cast<uintptr_t>(ws_dev) & 255) || (reinterpret_cast<uintptr_t>(dy_dev) & 15) ||
+      (reinterpret_cast<uintptr_t>(dx_dev) & 15))
+    return set_err(GACER_E_INVALID_ARG, "conv_dgrad: null/misaligned pointer or workspace too small");
+  if (int rc = load_tma_encoders()) return rc;
+  if (!S.d_error) { if (int rc = dev_upload<int32_t>(&S.d_error, nullptr, 1)) return rc; }
+  auto st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(ws_dev);
+  void* wt = ws + g.off_w;
+  float* scale = reinterpret_cast<float*>(ws + g.off_scale);
+  float* bias = reinterpret_cast<float*>(ws + g.off_bias);
+  const int nsb = roundup(Cin, 8) + 8;
+  CUDA_TRY(launch_dgrad_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
+  CUDA_TRY(launch_fill(scale, nsb, 1.0f, st));
+  CUDA_TRY(launch_fill(bias, nsb, 0.0f, st));
+  OpDev d;
+  std::memset(&d, 0, sizeof d);
+  d.kind = DK_GEMM;
+  d.act = ACT_NONE;
+  d.in = dy_dev;
+  d.B = N; d.H = g.Hd; d.W = g.Wd; d.C = g.cread; d.ldi = Cout;
+  d.out = dx_dev;
+  d.Ho = H; d.Wo = W; d.Cout = Cin; d.ldo = Cin;
+  d.kh = KH; d.kw = KW; d.stride = 1; d.ph = g.ph; d.pw = g.pw;
+  d.mrep = 1;
+  d.M = g.M; d.N = Cin; d.K = g.K; d.Kpad = g.Kpad;
+  d.tiles_m = g.tiles_m; d.tiles_n = g.tiles_n; d.bm = BM; d.bn = g.bn;
+  d.split_k = 1; d.nkb = g.nkb;
+  d.wt = wt; d.ldw = g.Kpad;
+  d.scale = scale; d.bias = bias;
+  d.a_mode = g.a_mode;
+  CUtensorMap maps[3];
+  std::memset(maps, 0, sizeof maps);
+  const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(ws + g.off_maps);
+  d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
+  int rc = (g.a_mode == A_IM2COL) ? encode_im2col(&maps[0], d, Cout) : encode_rows(&maps[0], dy_dev, g.K, g.M, Cout, BM);
+  if (!rc) rc = encode_rows(&maps[1], wt, g.Kpad, g.rows, g.Kpad, g.bn);
+  if (rc) return rc;
+  if ((static_cast<long long>(Cin) * 2) % 16 == 0) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(g.M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Cin) * 2};
+    const cuuint32_t box[2] = {64u, 32u};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode_tiled(&maps[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dx_dev, dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "conv_dgrad: output tensor map (%d)", static_cast<int>(r));
+    d.c_tma = 1;
+  }
+  // descriptors: pageable host -> device copies are staged before returning
+  CUDA_TRY(cudaMemcpyAsync(ws + g.off_maps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(ws + g.off_op, &d, sizeof d, cudaMemcpyHostToDevice, st));
+  ExecParams base;
+  std::memset(&base, 0, sizeof base);
+  base.error = S.d_error;
+  base.watchdog_ns = 2000000000LL;
+  CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + g.off_op), 0, DK_GEMM, g.tiles_m * g.tiles_n,
+                     S.num_sms, st));
+  return GACER_OK;
 }
 
 }  // extern "C"

@@ -452,6 +452,45 @@ int bad(int code, const char* msg) { return gacer::set_error(code, msg); }
 
 }  // namespace
 
+namespace gacer {
+// Conv data-gradient filter (stride 1): the forward filter w fp32
+// [Cout][Cin][KH][KW] flipped and transposed into the K-major bf16 B operand
+// of a forward conv over dy: row ci, column (r*KW + s)*cread + co holds
+// w[co][ci][KH-1-r][KW-1-s]; padded rows/columns are zero.
+__global__ void dgrad_filter_kernel(const float* __restrict__ w, int Cout, int Cin, int KH, int KW, int cread,
+                                    int Kpad, int rows, __nv_bfloat16* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(rows) * Kpad;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int ci = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
+    const int tap = k / cread, co = k % cread;
+    float v = 0.0f;
+    if (ci < Cin && tap < KH * KW && co < Cout) {
+      const int r = tap / KW, s = tap % KW;
+      v = w[((static_cast<int64_t>(co) * Cin + ci) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
+    }
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
+                                void* out, cudaStream_t s) {
+  dgrad_filter_kernel<<<grid_for(static_cast<int64_t>(rows) * Kpad), kThreads, 0, s>>>(
+      w, Cout, Cin, KH, KW, cread, Kpad, rows, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
+__global__ void fill_kernel(float* p, int n, float v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+cudaError_t launch_fill(float* p, int n, float v, cudaStream_t s) {
+  fill_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, n, v);
+  return cudaGetLastError();
+}
+}  // namespace gacer
+
 extern "C" {
 
 int32_t gacer_bn_partials(int64_t M, int32_t C) {

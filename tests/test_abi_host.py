@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol():
     for h in ("gacer.h", "gacer_train.h"):
         with open(os.path.join(ROOT, "include", h)) as f:
             hdr = f.read()
-        declared |= set(re.findall(r"^\s*(?:int|int32_t|const char\*)\s+(gacer_\w+)\s*\(", hdr, re.M))
+        declared |= set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(gacer_\w+)\s*\(", hdr, re.M))
     assert len(declared) >= 22
     lib = G.lib()
     for name in declared:
