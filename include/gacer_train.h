@@ -91,24 +91,27 @@ int32_t gacer_gap_bwd(const float* dy_dev, int32_t N, int32_t HW, int32_t C, voi
 int32_t gacer_linear_bwd(const void* x_dev, const float* w_dev, const float* dy_dev, int32_t N, int32_t K, int32_t O,
                          float* dx_dev, float* dw_dev, float* db_dev, void* stream);
 
-/* Convolution data gradient, stride 1 (oracle_conv2d_bwd_data), on the
- * tcgen05 implicit-GEMM path of the executor: for a forward conv
- * y = conv(x, w, pad) with stride 1,
- *   dx[n,ci,h,w] = sum_{co,r,s} dy[n,co,h+p-r,w+p-s] w[co,ci,r,s]
- *                = conv(dy, w', pad K-1-p),  w'[ci,co,r,s] = w[co,ci,K-1-r,K-1-s],
- * i.e. a forward conv of dy with the flipped, transposed filter; the call
- * packs w' (bf16, K-major) into the workspace and runs one single-op launch
- * of the executor kernel.  dy: bf16 NHWC [N][H+2p-KH+1][W+2p-KW+1][Cout];
- * w: fp32 [Cout][Cin][KH][KW] (the master weights); dx: bf16 NHWC
- * [N][H][W][Cin].  Cout % 64 == 0, Cin % 8 == 0, 0 <= pad <= k-1.
- * Workspace: gacer_conv_dgrad_workspace(...) bytes, 256-byte aligned.
- * Requires gacer_init on a device.  Stride > 1 (dy zero-dilated) and the
- * weight gradient are not yet provided. */
+/* Convolution data gradient (oracle_conv2d_bwd_data) on the tcgen05
+ * implicit-GEMM path of the executor.  For a forward conv y = conv(x, w,
+ * stride S, pad p):
+ *   dx[n,ci,h,w] = sum_{co,ho,wo,r,s : ho*S-p+r = h, wo*S-p+s = w} dy[n,co,ho,wo] w[co,ci,r,s]
+ *                = conv_stride1(dilate_S(dy), w', pad K-1-p),
+ *   w'[ci,co,r,s] = w[co,ci,K-1-r,K-1-s],
+ * i.e. a forward conv of dy (zero-dilated by S, plus the (H+2p-K) mod S
+ * trailing rows/columns no window reached) with the flipped, transposed
+ * filter.  The call packs w' (bf16, K-major) and, for S > 1, the dilated dy
+ * into the workspace, then runs one single-op launch of the executor kernel.
+ * dy: bf16 NHWC [N][Ho][Wo][Cout] (Ho = (H+2p-KH)/S + 1); w: fp32
+ * [Cout][Cin][KH][KW] (the master weights); dx: bf16 NHWC [N][H][W][Cin].
+ * Cout % 64 == 0, Cin % 8 == 0, 0 <= pad <= k-1.  Workspace:
+ * gacer_conv_dgrad_workspace(...) bytes, 256-byte aligned.  Requires
+ * gacer_init on a device.  (S > 1 spends S^2 x the MMA work on the zeros of
+ * the dilated dy; a phase-decomposed dgrad is the planned replacement.) */
 int64_t gacer_conv_dgrad_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
-                                   int32_t pad_h, int32_t pad_w);
+                                   int32_t stride, int32_t pad_h, int32_t pad_w);
 int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
-                         int32_t Cout, int32_t KH, int32_t KW, int32_t pad_h, int32_t pad_w, void* dx_dev,
-                         void* ws_dev, int64_t ws_bytes, void* stream);
+                         int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w,
+                         void* dx_dev, void* ws_dev, int64_t ws_bytes, void* stream);
 
 /* Mean softmax cross-entropy and its gradient (oracle_softmax_ce):
  *   loss = (1/N) sum_n [logsumexp(z_n) - z_n[label_n]],

@@ -33,6 +33,8 @@ cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, 
 cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
                                 void* out, cudaStream_t s);
 cudaError_t launch_fill(float* p, int n, float v, cudaStream_t s);
+cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, int Hdd, int Wdd, void* out,
+                          cudaStream_t s);
 }  // namespace gacer
 
 using namespace gacer;
@@ -1809,17 +1811,23 @@ int gacer_debug_timing(int64_t* out, int64_t cap, int reset) {
 // ------------------------------------------------------------------------
 namespace {
 struct DgradGeom {
-  int cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode, ph, pw, Hd, Wd;
-  size_t off_op, off_maps, off_scale, off_bias, off_w, bytes;
+  int cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode, ph, pw, Hd, Wd, Hdd, Wdd;
+  size_t off_op, off_maps, off_scale, off_bias, off_w, off_dil, bytes;
 };
 
-int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int pad_h, int pad_w, DgradGeom& g) {
-  if (N < 1 || H < 1 || W < 1 || Cin < 8 || Cin % 8 || Cout < 64 || Cout % 64 || KH < 1 || KW < 1 || pad_h < 0 ||
-      pad_w < 0 || pad_h > KH - 1 || pad_w > KW - 1)
-    return set_err(GACER_E_SHAPE, "conv_dgrad: need Cin %% 8 == 0, Cout %% 64 == 0, 0 <= pad <= k-1");
-  g.Hd = H + 2 * pad_h - KH + 1;                      // dy spatial size (forward output, stride 1)
-  g.Wd = W + 2 * pad_w - KW + 1;
-  if (g.Hd < 1 || g.Wd < 1) return set_err(GACER_E_SHAPE, "conv_dgrad: empty forward output");
+int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int pad_h, int pad_w,
+               DgradGeom& g) {
+  if (N < 1 || H < 1 || W < 1 || Cin < 8 || Cin % 8 || Cout < 64 || Cout % 64 || KH < 1 || KW < 1 || stride < 1 ||
+      pad_h < 0 || pad_w < 0 || pad_h > KH - 1 || pad_w > KW - 1)
+    return set_err(GACER_E_SHAPE, "conv_dgrad: need Cin %% 8 == 0, Cout %% 64 == 0, stride >= 1, 0 <= pad <= k-1");
+  g.Hd = (H + 2 * pad_h - KH) / stride + 1;           // dy spatial size (the forward output)
+  g.Wd = (W + 2 * pad_w - KW) / stride + 1;
+  if (H + 2 * pad_h < KH || W + 2 * pad_w < KW) return set_err(GACER_E_SHAPE, "conv_dgrad: empty forward output");
+  // stride > 1: dy zero-dilated by the stride, plus the rows/columns of x no
+  // window reached ((H + 2p - K) mod S), so the stride-1 dgrad conv of the
+  // dilated tensor has exactly H x W outputs
+  g.Hdd = stride == 1 ? g.Hd : (g.Hd - 1) * stride + 1 + (H + 2 * pad_h - KH) % stride;
+  g.Wdd = stride == 1 ? g.Wd : (g.Wd - 1) * stride + 1 + (W + 2 * pad_w - KW) % stride;
   g.ph = KH - 1 - pad_h;                              // the dgrad conv's padding
   g.pw = KW - 1 - pad_w;
   g.cread = Cout;                                     // dy channels, a multiple of 64
@@ -1840,6 +1848,7 @@ int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int pad_h
   g.off_scale = take(nsb * sizeof(float), 16);
   g.off_bias = take(nsb * sizeof(float), 16);
   g.off_w = take(static_cast<size_t>(g.rows) * g.Kpad * 2, 256);
+  g.off_dil = stride == 1 ? 0 : take(static_cast<size_t>(N) * g.Hdd * g.Wdd * Cout * 2, 256);
   g.bytes = o;
   return 0;
 }
@@ -1848,18 +1857,18 @@ int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int pad_h
 extern "C" {
 
 int64_t gacer_conv_dgrad_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
-                                   int32_t pad_h, int32_t pad_w) {
+                                   int32_t stride, int32_t pad_h, int32_t pad_w) {
   DgradGeom g;
-  if (int rc = dgrad_geom(N, H, W, Cin, Cout, KH, KW, pad_h, pad_w, g)) return rc;
+  if (int rc = dgrad_geom(N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g)) return rc;
   return static_cast<int64_t>(g.bytes);
 }
 
 int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
-                         int32_t Cout, int32_t KH, int32_t KW, int32_t pad_h, int32_t pad_w, void* dx_dev,
-                         void* ws_dev, int64_t ws_bytes, void* stream) {
+                         int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w,
+                         void* dx_dev, void* ws_dev, int64_t ws_bytes, void* stream) {
   if (!S.inited || S.host_only) return set_err(GACER_E_STATE, "conv_dgrad: gacer_init on a device first");
   DgradGeom g;
-  if (int rc = dgrad_geom(N, H, W, Cin, Cout, KH, KW, pad_h, pad_w, g)) return rc;
+  if (int rc = dgrad_geom(N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g)) return rc;
   if (!dy_dev || !w_dev || !dx_dev || !ws_dev || ws_bytes < static_cast<int64_t>(g.bytes) ||
       (reinterpret_cast<uintptr_t>(ws_dev) & 255) || (reinterpret_cast<uintptr_t>(dy_dev) & 15) ||
       (reinterpret_cast<uintptr_t>(dx_dev) & 15))
@@ -1873,14 +1882,19 @@ int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int3
   float* bias = reinterpret_cast<float*>(ws + g.off_bias);
   const int nsb = roundup(Cin, 8) + 8;
   CUDA_TRY(launch_dgrad_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
+  const void* src = dy_dev;
+  if (stride > 1) {
+    CUDA_TRY(launch_dilate(dy_dev, N, g.Hd, g.Wd, Cout, stride, g.Hdd, g.Wdd, ws + g.off_dil, st));
+    src = ws + g.off_dil;
+  }
   CUDA_TRY(launch_fill(scale, nsb, 1.0f, st));
   CUDA_TRY(launch_fill(bias, nsb, 0.0f, st));
   OpDev d;
   std::memset(&d, 0, sizeof d);
   d.kind = DK_GEMM;
   d.act = ACT_NONE;
-  d.in = dy_dev;
-  d.B = N; d.H = g.Hd; d.W = g.Wd; d.C = g.cread; d.ldi = Cout;
+  d.in = src;
+  d.B = N; d.H = g.Hdd; d.W = g.Wdd; d.C = g.cread; d.ldi = Cout;
   d.out = dx_dev;
   d.Ho = H; d.Wo = W; d.Cout = Cin; d.ldo = Cin;
   d.kh = KH; d.kw = KW; d.stride = 1; d.ph = g.ph; d.pw = g.pw;
@@ -1895,7 +1909,7 @@ int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int3
   std::memset(maps, 0, sizeof maps);
   const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(ws + g.off_maps);
   d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
-  int rc = (g.a_mode == A_IM2COL) ? encode_im2col(&maps[0], d, Cout) : encode_rows(&maps[0], dy_dev, g.K, g.M, Cout, BM);
+  int rc = (g.a_mode == A_IM2COL) ? encode_im2col(&maps[0], d, Cout) : encode_rows(&maps[0], src, g.K, g.M, Cout, BM);
   if (!rc) rc = encode_rows(&maps[1], wt, g.Kpad, g.rows, g.Kpad, g.bn);
   if (rc) return rc;
   if ((static_cast<long long>(Cin) * 2) % 16 == 0) {

@@ -480,6 +480,32 @@ cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int K
   return cudaGetLastError();
 }
 
+// Zero-dilated dy for a strided conv's data gradient: dyd[n][hh][ww][c] =
+// dy[n][hh/S][ww/S][c] when S divides hh and ww, else 0; Hdd x Wdd output.
+__global__ void dilate_kernel(const __nv_bfloat16* __restrict__ dy, int N, int Hd, int Wd, int C, int S, int Hdd,
+                              int Wdd, __nv_bfloat16* __restrict__ out) {
+  const int G8 = C / 8;
+  const int64_t total = static_cast<int64_t>(N) * Hdd * Wdd * G8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int ww = static_cast<int>(pix % Wdd), hh = static_cast<int>((pix / Wdd) % Hdd);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(Wdd) * Hdd));
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (hh % S == 0 && ww % S == 0 && hh / S < Hd && ww / S < Wd)
+      v = *reinterpret_cast<const uint4*>(dy + ((static_cast<int64_t>(n) * Hd + hh / S) * Wd + ww / S) * C + g * 8);
+    reinterpret_cast<uint4*>(out)[i] = v;
+  }
+}
+
+cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, int Hdd, int Wdd, void* out,
+                          cudaStream_t s) {
+  dilate_kernel<<<grid_for(static_cast<int64_t>(N) * Hdd * Wdd * (C / 8)), kThreads, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(dy), N, Hd, Wd, C, S, Hdd, Wdd, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
 __global__ void fill_kernel(float* p, int n, float v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;

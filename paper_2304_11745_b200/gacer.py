@@ -119,8 +119,8 @@ EXPORTS = {
     "gacer_gap_bwd": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_linear_bwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                           C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
-    "gacer_conv_dgrad_workspace": ([C.c_int32] * 9, C.c_int64),
-    "gacer_conv_dgrad": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 9 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "gacer_conv_dgrad_workspace": ([C.c_int32] * 10, C.c_int64),
+    "gacer_conv_dgrad": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 10 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
                          C.c_int32),
     "gacer_softmax_ce": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p], C.c_int32),
@@ -370,12 +370,12 @@ def linear_bwd(x, w, dy, N, K, O, dx, dw, db, stream=0):
     return _call("gacer_linear_bwd", x, w, dy, N, K, O, dx, dw, db, stream)
 
 
-def conv_dgrad_workspace(N, H, W, Cin, Cout, KH, KW, ph, pw):
-    return _check(lib().gacer_conv_dgrad_workspace(N, H, W, Cin, Cout, KH, KW, ph, pw))
+def conv_dgrad_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw):
+    return _check(lib().gacer_conv_dgrad_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw))
 
 
-def conv_dgrad(dy, w, N, H, W, Cin, Cout, KH, KW, ph, pw, dx, ws, ws_bytes, stream=0):
-    return _call("gacer_conv_dgrad", dy, w, N, H, W, Cin, Cout, KH, KW, ph, pw, dx, ws, ws_bytes, stream)
+def conv_dgrad(dy, w, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dx, ws, ws_bytes, stream=0):
+    return _call("gacer_conv_dgrad", dy, w, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dx, ws, ws_bytes, stream)
 
 
 def softmax_ce(z, labels, N, Cls, loss, dz, scratch, stream=0):

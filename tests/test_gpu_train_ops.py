@@ -164,31 +164,35 @@ def test_linear_bwd(T, N, K, O):
     assert maxrel(db.cpu().numpy(), rb) < 1e-5
 
 
-@pytest.mark.parametrize("N,H,W,Cin,Cout,k,p", [(4, 14, 14, 64, 64, 3, 1), (3, 14, 14, 256, 64, 1, 0),
-                                                 (2, 28, 28, 128, 128, 3, 1), (2, 9, 11, 72, 128, 3, 1),
-                                                 (2, 7, 7, 512, 2048, 1, 0)])
-def test_conv_dgrad_tcgen05(T, N, H, W, Cin, Cout, k, p):
-    """gacer_conv_dgrad (stride 1): the data gradient as a forward conv of dy
-    with the flipped, transposed filter on the executor's tcgen05 path, vs the
-    oracle's scatter definition (oracle_conv2d_bwd_data)."""
+@pytest.mark.parametrize("N,H,W,Cin,Cout,k,s,p", [(4, 14, 14, 64, 64, 3, 1, 1), (3, 14, 14, 256, 64, 1, 1, 0),
+                                                   (2, 28, 28, 128, 128, 3, 1, 1), (2, 9, 11, 72, 128, 3, 1, 1),
+                                                   (2, 7, 7, 512, 2048, 1, 1, 0),
+                                                   (2, 28, 28, 128, 128, 3, 2, 1),    # R50 layer2 3x3/s2, even H
+                                                   (2, 28, 28, 256, 512, 1, 2, 0),    # downsample 1x1/s2
+                                                   (2, 15, 13, 64, 64, 3, 2, 1),      # odd sizes
+                                                   (2, 32, 32, 8, 64, 7, 2, 3)])      # stem-like 7x7/s2
+def test_conv_dgrad_tcgen05(T, N, H, W, Cin, Cout, k, s, p):
+    """gacer_conv_dgrad: the data gradient as a stride-1 forward conv of the
+    (zero-dilated) dy with the flipped, transposed filter on the executor's
+    tcgen05 path, vs the oracle's scatter definition (oracle_conv2d_bwd_data)."""
     torch, G, OT = T
-    rng = np.random.default_rng(Cin + Cout + H)
-    Hd, Wd = H + 2 * p - k + 1, W + 2 * p - k + 1
+    rng = np.random.default_rng(Cin + Cout + H + s)
+    Hd, Wd = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
     dy = _bf16(torch, rng.normal(size=(N, Hd, Wd, Cout)))
     w = (rng.normal(size=(Cout, Cin, k, k)) * np.sqrt(2.0 / (Cin * k * k))).astype(np.float32)
     wd = torch.from_numpy(w).cuda()
     dx = torch.empty((N, H, W, Cin), dtype=torch.bfloat16, device="cuda")
     G.gacer_init(0)
     try:
-        nb = G.conv_dgrad_workspace(N, H, W, Cin, Cout, k, k, p, p)
+        nb = G.conv_dgrad_workspace(N, H, W, Cin, Cout, k, k, s, p, p)
         ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
         base = (ws.data_ptr() + 255) // 256 * 256
-        G.conv_dgrad(dy.data_ptr(), wd.data_ptr(), N, H, W, Cin, Cout, k, k, p, p, dx.data_ptr(), base, nb)
+        G.conv_dgrad(dy.data_ptr(), wd.data_ptr(), N, H, W, Cin, Cout, k, k, s, p, p, dx.data_ptr(), base, nb)
         torch.cuda.synchronize()
     finally:
         G.gacer_shutdown()
     wb = workloads_bf16(w)                       # the GEMM operand is the bf16-rounded filter
-    ref, _, _ = OT.conv2d_bwd(np.zeros((N, Cin, H, W)), wb, _nchw(_np(dy), N, Hd, Wd, Cout), 1, (p, p))
+    ref, _, _ = OT.conv2d_bwd(np.zeros((N, Cin, H, W)), wb, _nchw(_np(dy), N, Hd, Wd, Cout), s, (p, p))
     assert maxrel(_nchw(_np(dx), N, H, W, Cin), ref) <= 2e-2
 
 
