@@ -113,6 +113,25 @@ int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int3
                          int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w,
                          void* dx_dev, void* ws_dev, int64_t ws_bytes, void* stream);
 
+/* Convolution weight gradient (oracle_conv2d_bwd_weight) on the tcgen05
+ * GEMM path:  dw[co,ci,r,s] = sum_{n,ho,wo} dy[n,co,ho,wo] x[n,ci,ho*S-p+r,wo*S-p+s],
+ * a GEMM with M = Cout, N = KH*KW*Cin and the reduction over the
+ * N*Ho*Wo output pixels.  Both operands are made K-major along the pixel
+ * index (dy^T and the transposed im2col of x, zero-padded to a multiple of
+ * 64 pixels) in the workspace, the GEMM runs as one single-op launch of the
+ * executor kernel with a fixed split-K (partials summed in split order: the
+ * result is deterministic), and dw is written fp32 in the master weights'
+ * [Cout][Cin][KH][KW] order.  x: bf16 NHWC [N][H][W][Cin] (the saved
+ * forward input); dy: bf16 NHWC [N][Ho][Wo][Cout].  Workspace:
+ * gacer_conv_wgrad_workspace(...) bytes, 256-byte aligned (it holds the
+ * KH*KW-fold im2col; a streamed im2col producer is the planned replacement).
+ * Requires gacer_init on a device. */
+int64_t gacer_conv_wgrad_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
+                                   int32_t stride, int32_t pad_h, int32_t pad_w);
+int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                         int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w,
+                         float* dw_dev, void* ws_dev, int64_t ws_bytes, void* stream);
+
 /* Mean softmax cross-entropy and its gradient (oracle_softmax_ce):
  *   loss = (1/N) sum_n [logsumexp(z_n) - z_n[label_n]],
  *   dz[n,j] = (softmax(z_n)_j - [j == label_n]) / N.

@@ -35,6 +35,9 @@ cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int K
 cudaError_t launch_fill(float* p, int n, float v, cudaStream_t s);
 cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, int Hdd, int Wdd, void* out,
                           cudaStream_t s);
+cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, int Ho, int Wo, int KH, int KW, int S,
+                                    int ph, int pw, int64_t M, int Kpad, void* out, cudaStream_t s);
+cudaError_t launch_wgrad_permute(const float* g, int Cout, int Cin, int KH, int KW, float* dw, cudaStream_t s);
 }  // namespace gacer
 
 using namespace gacer;
@@ -1932,6 +1935,129 @@ int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int3
   base.watchdog_ns = 2000000000LL;
   CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + g.off_op), 0, DK_GEMM, g.tiles_m * g.tiles_n,
                      S.num_sms, st));
+  return GACER_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// A11: convolution weight gradient on the tcgen05 GEMM path
+// ------------------------------------------------------------------------
+namespace {
+struct WgradGeom {
+  int Ho, Wo, Ngemm, Kpad, nkb, bn, tiles_m, tiles_n, rows_a, rows_b, split;
+  int64_t M;
+  size_t off_op, off_maps, off_scale, off_bias, off_a, off_b, off_part, off_cnt, off_g, bytes;
+};
+
+int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int pad_h, int pad_w, WgradGeom& g) {
+  if (N < 1 || H < 1 || W < 1 || Cin < 1 || Cout < 1 || KH < 1 || KW < 1 || stride < 1 || pad_h < 0 || pad_w < 0 ||
+      H + 2 * pad_h < KH || W + 2 * pad_w < KW)
+    return set_err(GACER_E_SHAPE, "conv_wgrad: inconsistent shape");
+  g.Ho = (H + 2 * pad_h - KH) / stride + 1;
+  g.Wo = (W + 2 * pad_w - KW) / stride + 1;
+  g.M = static_cast<int64_t>(N) * g.Ho * g.Wo;          // the reduction length (pixels)
+  if (g.M > (int64_t(1) << 30)) return set_err(GACER_E_SHAPE, "conv_wgrad: too many pixels");
+  g.Ngemm = KH * KW * Cin;
+  g.Kpad = roundup(static_cast<int>(g.M), BK);
+  g.nkb = g.Kpad / BK;
+  g.bn = g.Ngemm >= 128 ? 128 : roundup(g.Ngemm, 16);
+  g.tiles_m = cdiv(Cout, BM);
+  g.tiles_n = cdiv(g.Ngemm, g.bn);
+  g.rows_a = g.tiles_m * BM;
+  g.rows_b = g.tiles_n * g.bn;
+  // split-K over the long pixel reduction, fixed by the shape (deterministic)
+  g.split = 1;
+  while (g.split < MAX_SPLIT && g.nkb / (g.split * 2) >= 8) g.split *= 2;
+  const int nsb = g.rows_b + 8;
+  const int tiles = g.tiles_m * g.tiles_n;
+  size_t o = 0;
+  auto take = [&](size_t n, size_t al) { o = (o + al - 1) / al * al; const size_t r = o; o += n; return r; };
+  g.off_op = take(sizeof(OpDev), 256);
+  g.off_maps = take(3 * sizeof(CUtensorMap), 128);
+  g.off_scale = take(nsb * sizeof(float), 16);
+  g.off_bias = take(nsb * sizeof(float), 16);
+  g.off_a = take(static_cast<size_t>(g.rows_a) * g.Kpad * 2, 256);
+  g.off_b = take(static_cast<size_t>(g.rows_b) * g.Kpad * 2, 256);
+  g.off_part = take(static_cast<size_t>(tiles) * g.split * BM * g.bn * sizeof(float), 256);
+  g.off_cnt = take(static_cast<size_t>(tiles) * sizeof(uint32_t), 256);
+  g.off_g = take(static_cast<size_t>(Cout) * g.Ngemm * sizeof(float), 256);
+  g.bytes = o;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t gacer_conv_wgrad_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
+                                   int32_t stride, int32_t pad_h, int32_t pad_w) {
+  WgradGeom g;
+  if (int rc = wgrad_geom(N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g)) return rc;
+  return static_cast<int64_t>(g.bytes);
+}
+
+int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                         int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w,
+                         float* dw_dev, void* ws_dev, int64_t ws_bytes, void* stream) {
+  if (!S.inited || S.host_only) return set_err(GACER_E_STATE, "conv_wgrad: gacer_init on a device first");
+  WgradGeom g;
+  if (int rc = wgrad_geom(N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g)) return rc;
+  if (!x_dev || !dy_dev || !dw_dev || !ws_dev || ws_bytes < static_cast<int64_t>(g.bytes) ||
+      (reinterpret_cast<uintptr_t>(ws_dev) & 255))
+    return set_err(GACER_E_INVALID_ARG, "conv_wgrad: null/misaligned pointer or workspace too small");
+  if (int rc = load_tma_encoders()) return rc;
+  if (!S.d_error) { if (int rc = dev_upload<int32_t>(&S.d_error, nullptr, 1)) return rc; }
+  auto st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(ws_dev);
+  void* a = ws + g.off_a;          // dy^T  [rows_a][Kpad]
+  void* b = ws + g.off_b;          // im2col(x)^T [rows_b][Kpad]
+  float* gbuf = reinterpret_cast<float*>(ws + g.off_g);
+  const int nsb = g.rows_b + 8;
+  CUDA_TRY(cudaMemsetAsync(a, 0, static_cast<size_t>(g.rows_a) * g.Kpad * 2, st));
+  CUDA_TRY(cudaMemsetAsync(b, 0, static_cast<size_t>(g.rows_b) * g.Kpad * 2, st));
+  CUDA_TRY(cudaMemsetAsync(ws + g.off_cnt, 0, static_cast<size_t>(g.tiles_m) * g.tiles_n * 4, st));
+  // dy [M][Cout] viewed as a 1x1 "im2col" of itself: the transpose
+  CUDA_TRY(launch_transpose_im2col(dy_dev, static_cast<int>(g.M), 1, 1, Cout, 1, 1, 1, 1, 1, 0, 0, g.M, g.Kpad, a, st));
+  CUDA_TRY(launch_transpose_im2col(x_dev, N, H, W, Cin, g.Ho, g.Wo, KH, KW, stride, pad_h, pad_w, g.M, g.Kpad, b, st));
+  CUDA_TRY(launch_fill(reinterpret_cast<float*>(ws + g.off_scale), nsb, 1.0f, st));
+  CUDA_TRY(launch_fill(reinterpret_cast<float*>(ws + g.off_bias), nsb, 0.0f, st));
+  OpDev d;
+  std::memset(&d, 0, sizeof d);
+  d.kind = DK_GEMM;
+  d.act = ACT_NONE;
+  d.out_f32 = 1;
+  d.in = a;
+  d.B = 1; d.H = 1; d.W = 1; d.C = g.Kpad; d.ldi = g.Kpad;
+  d.out = gbuf;
+  d.Ho = 1; d.Wo = 1; d.Cout = g.Ngemm; d.ldo = g.Ngemm;
+  d.kh = 1; d.kw = 1; d.stride = 1;
+  d.mrep = 1;
+  d.M = Cout; d.N = g.Ngemm; d.K = g.Kpad; d.Kpad = g.Kpad;
+  d.tiles_m = g.tiles_m; d.tiles_n = g.tiles_n; d.bm = BM; d.bn = g.bn;
+  d.split_k = g.split; d.nkb = g.nkb;
+  d.wt = b; d.ldw = g.Kpad;
+  d.scale = reinterpret_cast<float*>(ws + g.off_scale);
+  d.bias = reinterpret_cast<float*>(ws + g.off_bias);
+  d.partial = reinterpret_cast<float*>(ws + g.off_part);
+  d.tile_cnt = reinterpret_cast<uint32_t*>(ws + g.off_cnt);
+  d.a_mode = A_ROWS;
+  CUtensorMap maps[3];
+  std::memset(maps, 0, sizeof maps);
+  const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(ws + g.off_maps);
+  d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
+  d.c_tma = 0;                                   // fp32 rows stored directly
+  int rc = encode_rows(&maps[0], a, g.Kpad, g.rows_a, g.Kpad, BM);
+  if (!rc) rc = encode_rows(&maps[1], b, g.Kpad, g.rows_b, g.Kpad, g.bn);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(ws + g.off_maps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(ws + g.off_op, &d, sizeof d, cudaMemcpyHostToDevice, st));
+  ExecParams base;
+  std::memset(&base, 0, sizeof base);
+  base.error = S.d_error;
+  base.watchdog_ns = 2000000000LL;
+  CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + g.off_op), 0, DK_GEMM,
+                     g.tiles_m * g.tiles_n * g.split, S.num_sms, st));
+  CUDA_TRY(launch_wgrad_permute(gbuf, Cout, Cin, KH, KW, dw_dev, st));
   return GACER_OK;
 }
 

@@ -506,6 +506,68 @@ cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, i
   return cudaGetLastError();
 }
 
+// Weight-gradient operands: both GEMM operands K-major along the pixel
+// index m (the reduction), i.e. the transposes of the NHWC tensors, row
+// stride Kpad, zero-filled past M.  32x32 smem tiles keep reads and writes
+// coalesced.  Tap t = (r, s) of the im2col operand reads x at
+// (ho*S - p + r, wo*S - p + s) (zero outside the image).
+__global__ void __launch_bounds__(256) transpose_im2col_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                               int W, int C, int Ho, int Wo, int KW, int S, int ph,
+                                                               int pw, int64_t M, int Kpad,
+                                                               __nv_bfloat16* __restrict__ out) {
+  __shared__ __nv_bfloat16 tile[32][33];
+  const int t = blockIdx.z;
+  const int r = t / KW, q = t % KW;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {       // read: rows m0+i, channels c0+threadIdx.x
+    const int64_t m = m0 + i;
+    const int c = c0 + threadIdx.x;
+    __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
+    if (m < M && c < C) {
+      const int wo = static_cast<int>(m % Wo), ho = static_cast<int>((m / Wo) % Ho);
+      const int n = static_cast<int>(m / (static_cast<int64_t>(Wo) * Ho));
+      const int hi = ho * S - ph + r, wi = wo * S - pw + q;
+      if (hi >= 0 && hi < H && wi >= 0 && wi < W) v = x[((static_cast<int64_t>(n) * H + hi) * W + wi) * C + c];
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {       // write: row (t, c0+i), columns m0+threadIdx.x
+    const int c = c0 + i;
+    const int64_t m = m0 + threadIdx.x;
+    if (c < C && m < Kpad) out[(static_cast<int64_t>(t) * C + c) * Kpad + m] = tile[threadIdx.x][i];
+  }
+}
+
+cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, int Ho, int Wo, int KH, int KW, int S,
+                                    int ph, int pw, int64_t M, int Kpad, void* out, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>((Kpad + 31) / 32), static_cast<unsigned>((C + 31) / 32),
+                  static_cast<unsigned>(KH * KW));
+  transpose_im2col_kernel<<<grid, dim3(32, 8), 0, s>>>(static_cast<const __nv_bfloat16*>(x), N, H, W, C, Ho, Wo, KW,
+                                                        S, ph, pw, M, Kpad, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
+// dW from the GEMM's [Cout][(r*KW + s)*Cin + ci] order to the master
+// weights' [Cout][Cin][KH][KW] order.
+__global__ void wgrad_permute_kernel(const float* __restrict__ g, int Cout, int Cin, int KH, int KW,
+                                     float* __restrict__ dw) {
+  const int64_t total = static_cast<int64_t>(Cout) * Cin * KH * KW;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(i % KW), r = static_cast<int>((i / KW) % KH);
+    const int ci = static_cast<int>((i / (KW * KH)) % Cin), co = static_cast<int>(i / (static_cast<int64_t>(KW) * KH * Cin));
+    dw[i] = g[static_cast<int64_t>(co) * (KH * KW * Cin) + (r * KW + s) * Cin + ci];
+  }
+}
+
+cudaError_t launch_wgrad_permute(const float* g, int Cout, int Cin, int KH, int KW, float* dw, cudaStream_t s) {
+  wgrad_permute_kernel<<<grid_for(static_cast<int64_t>(Cout) * Cin * KH * KW), kThreads, 0, s>>>(g, Cout, Cin, KH, KW,
+                                                                                                dw);
+  return cudaGetLastError();
+}
+
 __global__ void fill_kernel(float* p, int n, float v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;

@@ -122,6 +122,9 @@ EXPORTS = {
     "gacer_conv_dgrad_workspace": ([C.c_int32] * 10, C.c_int64),
     "gacer_conv_dgrad": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 10 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
                          C.c_int32),
+    "gacer_conv_wgrad_workspace": ([C.c_int32] * 10, C.c_int64),
+    "gacer_conv_wgrad": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 10 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+                         C.c_int32),
     "gacer_softmax_ce": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p], C.c_int32),
     "gacer_sgd_momentum": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_int32,
@@ -376,6 +379,14 @@ def conv_dgrad_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw):
 
 def conv_dgrad(dy, w, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dx, ws, ws_bytes, stream=0):
     return _call("gacer_conv_dgrad", dy, w, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dx, ws, ws_bytes, stream)
+
+
+def conv_wgrad_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw):
+    return _check(lib().gacer_conv_wgrad_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw))
+
+
+def conv_wgrad(x, dy, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dw, ws, ws_bytes, stream=0):
+    return _call("gacer_conv_wgrad", x, dy, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dw, ws, ws_bytes, stream)
 
 
 def softmax_ce(z, labels, N, Cls, loss, dz, scratch, stream=0):

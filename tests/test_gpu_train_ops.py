@@ -196,6 +196,36 @@ def test_conv_dgrad_tcgen05(T, N, H, W, Cin, Cout, k, s, p):
     assert maxrel(_nchw(_np(dx), N, H, W, Cin), ref) <= 2e-2
 
 
+@pytest.mark.parametrize("N,H,W,Cin,Cout,k,s,p", [(4, 14, 14, 64, 64, 3, 1, 1), (3, 14, 14, 256, 64, 1, 1, 0),
+                                                   (2, 28, 28, 128, 128, 3, 2, 1), (2, 15, 13, 64, 72, 3, 2, 1),
+                                                   (2, 7, 7, 512, 2048, 1, 1, 0), (2, 32, 32, 8, 64, 7, 2, 3)])
+def test_conv_wgrad_tcgen05(T, N, H, W, Cin, Cout, k, s, p):
+    """gacer_conv_wgrad: dW as a GEMM over the output pixels on the
+    executor's tcgen05 path (fixed split-K), vs the oracle's definition
+    (oracle_conv2d_bwd_weight); deterministic run to run."""
+    torch, G, OT = T
+    rng = np.random.default_rng(Cin * 3 + Cout + H + s)
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    x = _bf16(torch, rng.normal(size=(N, H, W, Cin)))
+    dy = _bf16(torch, rng.normal(size=(N, Ho, Wo, Cout)))
+    dw = torch.empty((Cout, Cin, k, k), device="cuda")
+    dw2 = torch.empty_like(dw)
+    G.gacer_init(0)
+    try:
+        nb = G.conv_wgrad_workspace(N, H, W, Cin, Cout, k, k, s, p, p)
+        ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
+        base = (ws.data_ptr() + 255) // 256 * 256
+        for out in (dw, dw2):
+            G.conv_wgrad(x.data_ptr(), dy.data_ptr(), N, H, W, Cin, Cout, k, k, s, p, p, out.data_ptr(), base, nb)
+        torch.cuda.synchronize()
+    finally:
+        G.gacer_shutdown()
+    _, ref, _ = OT.conv2d_bwd(_nchw(_np(x), N, H, W, Cin), np.zeros((Cout, Cin, k, k)),
+                              _nchw(_np(dy), N, Ho, Wo, Cout), s, (p, p))
+    assert maxrel(dw.cpu().numpy(), ref) <= 1e-3       # fp32 accumulation of exact bf16 products
+    assert torch.equal(dw, dw2)
+
+
 def workloads_bf16(a):
     import workloads
     return workloads.bf16_round(np.asarray(a, np.float32)).astype(np.float64)
