@@ -1737,6 +1737,12 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
               s8[0] += ld[ks][0].x; s8[1] += ld[ks][0].y; s8[2] += ld[ks][0].z; s8[3] += ld[ks][0].w;
               s8[4] += ld[ks][1].x; s8[5] += ld[ks][1].y; s8[6] += ld[ks][1].z; s8[7] += ld[ks][1].w;
             }
+          for (int ks = MAX_SPLIT; ks < split; ++ks) {   // long reductions (weight gradients), in split order
+            const float4* qp = reinterpret_cast<const float4*>(part + static_cast<size_t>(ks) * (BM * bn)) + row;
+            const float4 a = __ldcg(qp + (c >> 2) * BM), b = __ldcg(qp + ((c >> 2) + 1) * BM);
+            s8[0] += a.x; s8[1] += a.y; s8[2] += a.z; s8[3] += a.w;
+            s8[4] += b.x; s8[5] += b.y; s8[6] += b.z; s8[7] += b.w;
+          }
           if (swap) {
             epilogue_store8_swap(op, m, n0 + c, s8, sc_row, bi_row);
           } else {

@@ -48,7 +48,8 @@ constexpr int NTHREADS = 384;
 constexpr int CC_THREADS = NWORK; // threads that execute a CUDA-core item
 constexpr int CC_RUN = 8;         // consecutive output pixels per thread in the row-run window kernel
 constexpr int CC_TASKS_PER_THREAD = 4;
-constexpr int MAX_SPLIT = 4;      // split-K factor cap (fixed per layer shape)
+constexpr int MAX_SPLIT = 4;      // split-K factor cap of forward layers (fixed per layer shape)
+constexpr int MAX_SPLIT_LONG = 64; // cap for the long pixel reductions of weight gradients
 constexpr int LOOKAHEAD = 3;      // max claimed items not yet picked up by every role (per CTA)
 constexpr int INLINE_DEPS = 4;    // dependencies stored inside the Item
 constexpr int MAX_SMEM_SEGS = 256;

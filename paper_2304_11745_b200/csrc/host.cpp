@@ -1967,8 +1967,11 @@ int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.rows_a = g.tiles_m * BM;
   g.rows_b = g.tiles_n * g.bn;
   // split-K over the long pixel reduction, fixed by the shape (deterministic)
+  // (about two waves of items over the SMs, each split >= 8 K-blocks)
   g.split = 1;
-  while (g.split < MAX_SPLIT && g.nkb / (g.split * 2) >= 8) g.split *= 2;
+  while (g.split < MAX_SPLIT_LONG && g.tiles_m * g.tiles_n * g.split * 2 <= 2 * kSplitSms &&
+         g.nkb / (g.split * 2) >= 8)
+    g.split *= 2;
   const int nsb = g.rows_b + 8;
   const int tiles = g.tiles_m * g.tiles_n;
   size_t o = 0;
@@ -2013,8 +2016,12 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   void* b = ws + g.off_b;          // im2col(x)^T [rows_b][Kpad]
   float* gbuf = reinterpret_cast<float*>(ws + g.off_g);
   const int nsb = g.rows_b + 8;
-  CUDA_TRY(cudaMemsetAsync(a, 0, static_cast<size_t>(g.rows_a) * g.Kpad * 2, st));
-  CUDA_TRY(cudaMemsetAsync(b, 0, static_cast<size_t>(g.rows_b) * g.Kpad * 2, st));
+  // the transposes write every column < Kpad of the real rows; only the
+  // padding rows (Cout.. and KH*KW*Cin.. up to the tile multiple) need zeros
+  const size_t rowb = static_cast<size_t>(g.Kpad) * 2;
+  if (g.rows_a > Cout) CUDA_TRY(cudaMemsetAsync(static_cast<uint8_t*>(a) + Cout * rowb, 0, (g.rows_a - Cout) * rowb, st));
+  if (g.rows_b > g.Ngemm)
+    CUDA_TRY(cudaMemsetAsync(static_cast<uint8_t*>(b) + g.Ngemm * rowb, 0, (g.rows_b - g.Ngemm) * rowb, st));
   CUDA_TRY(cudaMemsetAsync(ws + g.off_cnt, 0, static_cast<size_t>(g.tiles_m) * g.tiles_n * 4, st));
   // dy [M][Cout] viewed as a 1x1 "im2col" of itself: the transpose
   CUDA_TRY(launch_transpose_im2col(dy_dev, static_cast<int>(g.M), 1, 1, Cout, 1, 1, 1, 1, 1, 0, 0, g.M, g.Kpad, a, st));

@@ -508,44 +508,64 @@ cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, i
 
 // Weight-gradient operands: both GEMM operands K-major along the pixel
 // index m (the reduction), i.e. the transposes of the NHWC tensors, row
-// stride Kpad, zero-filled past M.  32x32 smem tiles keep reads and writes
-// coalesced.  Tap t = (r, s) of the im2col operand reads x at
+// stride Kpad, zero-filled past M.  64x64 smem tiles keep reads and writes
+// coalesced and 16 bytes wide.  Tap t = (r, s) of the im2col operand reads x at
 // (ho*S - p + r, wo*S - p + s) (zero outside the image).
 __global__ void __launch_bounds__(256) transpose_im2col_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                                int W, int C, int Ho, int Wo, int KW, int S, int ph,
                                                                int pw, int64_t M, int Kpad,
                                                                __nv_bfloat16* __restrict__ out) {
-  __shared__ __nv_bfloat16 tile[32][33];
+  // 64 pixels x 64 channels per CTA: 16-byte loads along the channels,
+  // a transposed smem tile, 16-byte stores along the pixels
+  constexpr int T = 64, LD = T + 8;
+  __shared__ __align__(16) __nv_bfloat16 tile[T][LD];   // [channel][pixel]
   const int t = blockIdx.z;
   const int r = t / KW, q = t % KW;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 32;
-  const int c0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += 8) {       // read: rows m0+i, channels c0+threadIdx.x
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * T;
+  const int c0 = blockIdx.y * T;
+  const bool vec = (C % 8) == 0;
+  for (int e = threadIdx.x; e < T * (T / 8); e += blockDim.x) {
+    const int i = e / (T / 8), cg = (e % (T / 8)) * 8;        // pixel row i, channel group cg
     const int64_t m = m0 + i;
-    const int c = c0 + threadIdx.x;
-    __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
-    if (m < M && c < C) {
+    __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(0.0f);
+    if (m < M && c0 + cg < C) {
       const int wo = static_cast<int>(m % Wo), ho = static_cast<int>((m / Wo) % Ho);
       const int n = static_cast<int>(m / (static_cast<int64_t>(Wo) * Ho));
       const int hi = ho * S - ph + r, wi = wo * S - pw + q;
-      if (hi >= 0 && hi < H && wi >= 0 && wi < W) v = x[((static_cast<int64_t>(n) * H + hi) * W + wi) * C + c];
+      if (hi >= 0 && hi < H && wi >= 0 && wi < W) {
+        const __nv_bfloat16* src = x + ((static_cast<int64_t>(n) * H + hi) * W + wi) * C + c0 + cg;
+        if (vec) {
+          const uint4 u = *reinterpret_cast<const uint4*>(src);
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = h[j];
+        } else {
+          for (int j = 0; j < 8 && c0 + cg + j < C; ++j) v[j] = src[j];
+        }
+      }
     }
-    tile[i][threadIdx.x] = v;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tile[cg + j][i] = v[j];
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += 8) {       // write: row (t, c0+i), columns m0+threadIdx.x
-    const int c = c0 + i;
-    const int64_t m = m0 + threadIdx.x;
-    if (c < C && m < Kpad) out[(static_cast<int64_t>(t) * C + c) * Kpad + m] = tile[threadIdx.x][i];
+  for (int e = threadIdx.x; e < T * (T / 8); e += blockDim.x) {
+    const int cc = e / (T / 8), mg = (e % (T / 8)) * 8;       // channel row cc, pixel group mg
+    const int c = c0 + cc;
+    const int64_t m = m0 + mg;
+    if (c < C && m < Kpad)                                      // Kpad is a multiple of 64: whole groups
+      *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(t) * C + c) * Kpad + m) =
+          *reinterpret_cast<const uint4*>(&tile[cc][mg]);
   }
 }
 
 cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, int Ho, int Wo, int KH, int KW, int S,
                                     int ph, int pw, int64_t M, int Kpad, void* out, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>((Kpad + 31) / 32), static_cast<unsigned>((C + 31) / 32),
+  const dim3 grid(static_cast<unsigned>((Kpad + 63) / 64), static_cast<unsigned>((C + 63) / 64),
                   static_cast<unsigned>(KH * KW));
-  transpose_im2col_kernel<<<grid, dim3(32, 8), 0, s>>>(static_cast<const __nv_bfloat16*>(x), N, H, W, C, Ho, Wo, KW,
-                                                        S, ph, pw, M, Kpad, static_cast<__nv_bfloat16*>(out));
+  transpose_im2col_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), N, H, W, C, Ho, Wo, KW, S, ph,
+                                               pw, M, Kpad, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError();
 }
 

@@ -68,7 +68,46 @@ def main():
     t = timed(lambda: G.maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, H, C, 3, 3, 2, 1, 1, 56, 56, dx.data_ptr(),
                                     arg.data_ptr()))
     rows.append(("maxpool_bwd", "[64,112,112,64] 3x3/s2/p1", (2 * H * H + 56 * 56) * N * C * 2, t))
+    # conv backward GEMMs on tcgen05 at ResNet-50 B=64 layer shapes; FLOP =
+    # 2 * N*Ho*Wo * Cout * Cin*KH*KW each (dgrad, wgrad), vs the measured bf16
+    # peak (TFLOP/s rows: "bytes" column holds FLOP)
+    G.gacer_init(0)
+    tflop_rows = []
+    try:
+        for (H, Cin, Cout, k, st, p) in [(56, 64, 64, 3, 1, 1), (56, 256, 64, 1, 1, 0), (56, 64, 256, 1, 1, 0),
+                                         (28, 128, 128, 3, 1, 1), (14, 256, 256, 3, 1, 1), (7, 512, 512, 3, 1, 1),
+                                         (56, 128, 128, 3, 2, 1)]:
+            Ho = (H + 2 * p - k) // st + 1
+            x = torch.randn(B, H, H, Cin, device="cuda").to(torch.bfloat16)
+            dy = torch.randn(B, Ho, Ho, Cout, device="cuda").to(torch.bfloat16)
+            w = torch.randn(Cout, Cin, k, k, device="cuda")
+            dx = torch.empty_like(x)
+            dw = torch.empty_like(w)
+            flop = 2.0 * B * Ho * Ho * Cout * Cin * k * k
+            nb = G.conv_dgrad_workspace(B, H, H, Cin, Cout, k, k, st, p, p)
+            ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
+            base = (ws.data_ptr() + 255) // 256 * 256
+            t = timed(lambda: G.conv_dgrad(dy.data_ptr(), w.data_ptr(), B, H, H, Cin, Cout, k, k, st, p, p,
+                                           dx.data_ptr(), base, nb))
+            tflop_rows.append(("conv_dgrad", f"{H}x{H} {Cin}->{Cout} k{k} s{st}", flop, t))
+            nb = G.conv_wgrad_workspace(B, H, H, Cin, Cout, k, k, st, p, p)
+            ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
+            base = (ws.data_ptr() + 255) // 256 * 256
+            t = timed(lambda: G.conv_wgrad(x.data_ptr(), dy.data_ptr(), B, H, H, Cin, Cout, k, k, st, p, p,
+                                           dw.data_ptr(), base, nb))
+            tflop_rows.append(("conv_wgrad", f"{H}x{H} {Cin}->{Cout} k{k} s{st}", flop, t))
+            del x, dy, w, dx, dw, ws
+    finally:
+        G.gacer_shutdown()
+    tpeak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))["bf16_tflops"]
     out = []
+    print(f"{'op':14s} {'shape':28s} {'GFLOP':>8s} {'us':>8s} {'TF/s':>8s} {'frac':>6s}")
+    for name, shape, flop, t in tflop_rows:
+        tf = flop / t / 1e12
+        print(f"{name:14s} {shape:28s} {flop / 1e9:8.2f} {t * 1e6:8.1f} {tf:8.1f} {tf / tpeak:6.3f}")
+        out.append({"op": name, "shape": shape, "flop": flop, "us": t * 1e6, "tflops": tf,
+                    "frac_of_measured_bf16": tf / tpeak, "includes": "operand staging kernels + GEMM"})
     print(f"{'op':14s} {'shape':28s} {'MB':>8s} {'us':>8s} {'GB/s':>8s} {'frac':>6s}")
     for name, shape, nbytes, t in rows:
         gbs = nbytes / t / 1e9
