@@ -132,6 +132,37 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
                          int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w,
                          float* dw_dev, void* ws_dev, int64_t ws_bytes, void* stream);
 
+/* Training forward conv (the conv of a conv -> BN-train pair: raw output,
+ * no folded BN): y = conv(x, w, stride, pad) on the tcgen05 implicit-GEMM
+ * path of the executor (one single-op launch), the filter packed to bf16
+ * K-major from the device-resident fp32 master weights on every call (they
+ * change every SGD step).  x: bf16 NHWC [N][H][W][Cin] (Cin % 8 == 0; TMA
+ * im2col when Cin % 64 == 0, else the cp.async gather); w: fp32
+ * [Cout][Cin][KH][KW]; y: bf16 NHWC [N][Ho][Wo][Cout] (Cout % 8 == 0).
+ * Workspace: gacer_conv_fwd_workspace(...) bytes, 256-byte aligned. */
+int64_t gacer_conv_fwd_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
+                                 int32_t stride, int32_t pad_h, int32_t pad_w);
+int32_t gacer_conv_fwd(const void* x_dev, const float* w_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                       int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w, void* y_dev,
+                       void* ws_dev, int64_t ws_bytes, void* stream);
+
+/* Max-pool forward, NHWC bf16 (oracle_maxpool; padded taps never win). */
+int32_t gacer_maxpool_fwd(const void* x_dev, int32_t N, int32_t H, int32_t W, int32_t C, int32_t KH, int32_t KW,
+                          int32_t stride, int32_t ph, int32_t pw, int32_t Ho, int32_t Wo, void* y_dev, void* stream);
+
+/* Residual add (oracle_add), then ReLU when relu != 0: y = a + b; bf16 [n],
+ * n % 8 == 0; y may alias a or b. */
+int32_t gacer_add(const void* a_dev, const void* b_dev, int64_t n, int32_t relu, void* y_dev, void* stream);
+
+/* Global average pool forward (oracle_gap): y[n][c] = (1/HW) sum_p x[n][p][c],
+ * fp32 sum in pixel order; x bf16 [N][HW][C], y bf16 [N][C]. */
+int32_t gacer_gap_fwd(const void* x_dev, int32_t N, int32_t HW, int32_t C, void* y_dev, void* stream);
+
+/* FC forward (oracle_linear): z[n][o] = b[o] + sum_k w[o][k] x[n][k]; x bf16
+ * [N][K], w fp32 [O][K], b fp32 [O] (may be NULL), z fp32 [N][O] (logits). */
+int32_t gacer_linear_fwd(const void* x_dev, const float* w_dev, const float* b_dev, int32_t N, int32_t K, int32_t O,
+                         float* z_dev, void* stream);
+
 /* Mean softmax cross-entropy and its gradient (oracle_softmax_ce):
  *   loss = (1/N) sum_n [logsumexp(z_n) - z_n[label_n]],
  *   dz[n,j] = (softmax(z_n)_j - [j == label_n]) / N.

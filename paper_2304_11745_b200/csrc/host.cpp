@@ -38,6 +38,8 @@ cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, i
 cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, int Ho, int Wo, int KH, int KW, int S,
                                     int ph, int pw, int64_t M, int Kpad, void* out, cudaStream_t s);
 cudaError_t launch_wgrad_permute(const float* g, int Cout, int Cin, int KH, int KW, float* dw, cudaStream_t s);
+cudaError_t launch_fwd_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
+                              void* out, cudaStream_t s);
 }  // namespace gacer
 
 using namespace gacer;
@@ -2065,6 +2067,129 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + g.off_op), 0, DK_GEMM,
                      g.tiles_m * g.tiles_n * g.split, S.num_sms, st));
   CUDA_TRY(launch_wgrad_permute(gbuf, Cout, Cin, KH, KW, dw_dev, st));
+  return GACER_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// A11: training forward conv (raw output, BN applied by gacer_bn_train_fwd)
+// with device-resident fp32 master weights, on the same tcgen05 path
+// ------------------------------------------------------------------------
+namespace {
+struct FwdGeom {
+  int Ho, Wo, cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode;
+  size_t off_op, off_maps, off_scale, off_bias, off_w, bytes;
+};
+
+int fwd_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int ph, int pw, FwdGeom& g) {
+  if (N < 1 || H < 1 || W < 1 || Cin < 8 || Cin % 8 || Cout < 8 || Cout % 8 || KH < 1 || KW < 1 || stride < 1 ||
+      ph < 0 || pw < 0 || H + 2 * ph < KH || W + 2 * pw < KW)
+    return set_err(GACER_E_SHAPE, "conv_fwd: need Cin %% 8 == 0, Cout %% 8 == 0 and a non-empty output");
+  g.Ho = (H + 2 * ph - KH) / stride + 1;
+  g.Wo = (W + 2 * pw - KW) / stride + 1;
+  if (Cin % 64 == 0) {
+    g.cread = Cin;
+    g.a_mode = (KH * KW == 1 && stride == 1 && ph == 0 && pw == 0) ? A_ROWS : A_IM2COL;
+  } else {
+    g.cread = Cin;                       // cp.async gather, 8-channel granules
+    g.a_mode = A_GATHER;
+  }
+  g.K = KH * KW * g.cread;
+  g.Kpad = roundup(g.K, BK);
+  g.nkb = g.Kpad / BK;
+  g.M = N * g.Ho * g.Wo;
+  g.bn = Cout >= 128 ? 128 : roundup(Cout, 16);
+  g.tiles_m = cdiv(g.M, BM);
+  g.tiles_n = cdiv(Cout, g.bn);
+  g.rows = g.tiles_n * g.bn;
+  const int nsb = g.rows + 8;
+  size_t o = 0;
+  auto take = [&](size_t n, size_t al) { o = (o + al - 1) / al * al; const size_t r = o; o += n; return r; };
+  g.off_op = take(sizeof(OpDev), 256);
+  g.off_maps = take(3 * sizeof(CUtensorMap), 128);
+  g.off_scale = take(nsb * sizeof(float), 16);
+  g.off_bias = take(nsb * sizeof(float), 16);
+  g.off_w = take(static_cast<size_t>(g.rows) * g.Kpad * 2, 256);
+  g.bytes = o;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t gacer_conv_fwd_workspace(int32_t N, int32_t H, int32_t W, int32_t Cin, int32_t Cout, int32_t KH, int32_t KW,
+                                 int32_t stride, int32_t pad_h, int32_t pad_w) {
+  FwdGeom g;
+  if (int rc = fwd_geom(N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g)) return rc;
+  return static_cast<int64_t>(g.bytes);
+}
+
+int32_t gacer_conv_fwd(const void* x_dev, const float* w_dev, int32_t N, int32_t H, int32_t W, int32_t Cin,
+                       int32_t Cout, int32_t KH, int32_t KW, int32_t stride, int32_t pad_h, int32_t pad_w, void* y_dev,
+                       void* ws_dev, int64_t ws_bytes, void* stream) {
+  if (!S.inited || S.host_only) return set_err(GACER_E_STATE, "conv_fwd: gacer_init on a device first");
+  FwdGeom g;
+  if (int rc = fwd_geom(N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g)) return rc;
+  if (!x_dev || !w_dev || !y_dev || !ws_dev || ws_bytes < static_cast<int64_t>(g.bytes) ||
+      (reinterpret_cast<uintptr_t>(ws_dev) & 255) || (reinterpret_cast<uintptr_t>(x_dev) & 15) ||
+      (reinterpret_cast<uintptr_t>(y_dev) & 15))
+    return set_err(GACER_E_INVALID_ARG, "conv_fwd: null/misaligned pointer or workspace too small");
+  if (int rc = load_tma_encoders()) return rc;
+  if (!S.d_error) { if (int rc = dev_upload<int32_t>(&S.d_error, nullptr, 1)) return rc; }
+  auto st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(ws_dev);
+  void* wt = ws + g.off_w;
+  float* scale = reinterpret_cast<float*>(ws + g.off_scale);
+  float* bias = reinterpret_cast<float*>(ws + g.off_bias);
+  const int nsb = g.rows + 8;
+  CUDA_TRY(launch_fwd_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
+  CUDA_TRY(launch_fill(scale, nsb, 1.0f, st));
+  CUDA_TRY(launch_fill(bias, nsb, 0.0f, st));
+  OpDev d;
+  std::memset(&d, 0, sizeof d);
+  d.kind = DK_GEMM;
+  d.act = ACT_NONE;
+  d.in = x_dev;
+  d.B = N; d.H = H; d.W = W; d.C = g.cread; d.ldi = Cin;
+  d.out = y_dev;
+  d.Ho = g.Ho; d.Wo = g.Wo; d.Cout = Cout; d.ldo = Cout;
+  d.kh = KH; d.kw = KW; d.stride = stride; d.ph = pad_h; d.pw = pad_w;
+  d.mrep = 1;
+  d.M = g.M; d.N = Cout; d.K = g.K; d.Kpad = g.Kpad;
+  d.tiles_m = g.tiles_m; d.tiles_n = g.tiles_n; d.bm = BM; d.bn = g.bn;
+  d.split_k = 1; d.nkb = g.nkb;
+  d.wt = wt; d.ldw = g.Kpad;
+  d.scale = scale; d.bias = bias;
+  d.a_mode = g.a_mode;
+  CUtensorMap maps[3];
+  std::memset(maps, 0, sizeof maps);
+  const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(ws + g.off_maps);
+  d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
+  int rc = 0;
+  if (g.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, Cin);
+  else if (g.a_mode == A_ROWS) rc = encode_rows(&maps[0], x_dev, g.K, g.M, Cin, BM);
+  if (!rc) rc = encode_rows(&maps[1], wt, g.Kpad, g.rows, g.Kpad, g.bn);
+  if (rc) return rc;
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(g.M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Cout) * 2};
+    const cuuint32_t box[2] = {64u, 32u};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode_tiled(&maps[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y_dev, dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "conv_fwd: output tensor map (%d)", static_cast<int>(r));
+    d.c_tma = 1;
+  }
+  CUDA_TRY(cudaMemcpyAsync(ws + g.off_maps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(ws + g.off_op, &d, sizeof d, cudaMemcpyHostToDevice, st));
+  ExecParams base;
+  std::memset(&base, 0, sizeof base);
+  base.error = S.d_error;
+  base.watchdog_ns = 2000000000LL;
+  CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + g.off_op), 0, DK_GEMM, g.tiles_m * g.tiles_n,
+                     S.num_sms, st));
   return GACER_OK;
 }
 

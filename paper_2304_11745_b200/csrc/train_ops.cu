@@ -349,6 +349,90 @@ __global__ void __launch_bounds__(kThreads) gap_bwd_kernel(const float* __restri
   }
 }
 
+// ---------------------------------------------------------------- forward
+// (the training step's non-GEMM forward ops; the inference executor fuses
+//  these into its work items, the training step still runs them per op)
+__global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                               int W, int C, int KH, int KW, int S, int ph, int pw,
+                                                               int Ho, int Wo, __nv_bfloat16* __restrict__ y) {
+  const int G8 = C / 8;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * G8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int wo = static_cast<int>(pix % Wo), ho = static_cast<int>((pix / Wo) % Ho);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(Wo) * Ho));
+    float best[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+    for (int r = 0; r < KH; ++r) {
+      const int hh = ho * S - ph + r;
+      if (hh < 0 || hh >= H) continue;
+      for (int q = 0; q < KW; ++q) {
+        const int ww = wo * S - pw + q;
+        if (ww < 0 || ww >= W) continue;
+        float v[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hh) * W + ww) * C + g * 8), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) best[j] = fmaxf(best[j], v[j]);
+      }
+    }
+    reinterpret_cast<uint4*>(y)[i] = pack8(best);
+  }
+}
+
+// y = a + b (then ReLU when relu != 0), bf16 [n], n % 8 == 0
+__global__ void __launch_bounds__(kThreads) add_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, int64_t n8,
+                                                       int relu, __nv_bfloat16* y) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float u[8], v[8];
+    unpack8(reinterpret_cast<const uint4*>(a)[i], u);
+    unpack8(reinterpret_cast<const uint4*>(b)[i], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float t = u[j] + v[j];
+      u[j] = relu ? fmaxf(t, 0.0f) : t;
+    }
+    reinterpret_cast<uint4*>(y)[i] = pack8(u);
+  }
+}
+
+// y[n][c] = (1/HW) sum_p x[n][p][c], summed in pixel order (fp32), bf16 out
+__global__ void __launch_bounds__(kThreads) gap_fwd_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW, int C,
+                                                           __nv_bfloat16* __restrict__ y) {
+  const int G8 = C / 8;
+  const int64_t total = static_cast<int64_t>(N) * G8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % G8), n = static_cast<int>(i / G8);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < HW; ++p) {
+      float v[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + (static_cast<int64_t>(n) * HW + p) * C + g * 8), v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] /= static_cast<float>(HW);
+    reinterpret_cast<uint4*>(y)[i] = pack8(acc);
+  }
+}
+
+// z[n][o] = b[o] + sum_k w[o][k] x[n][k] (x bf16, w fp32), summed in k order
+__global__ void __launch_bounds__(kThreads) linear_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const float* __restrict__ w, const float* __restrict__ b,
+                                                              int N, int K, int O, float* __restrict__ z) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(N) * O) return;
+  const int n = static_cast<int>(i / O), o = static_cast<int>(i % O);
+  float a = b ? b[o] : 0.0f;
+  for (int k = 0; k < K; ++k)
+    a = fmaf(__bfloat162float(x[static_cast<int64_t>(n) * K + k]), w[static_cast<int64_t>(o) * K + k], a);
+  z[i] = a;
+}
+
 // FC backward: one output element per thread, reductions in index order
 __global__ void __launch_bounds__(kThreads) linear_dx_kernel(const float* __restrict__ w, const float* __restrict__ dy,
                                                              int N, int K, int O, float* __restrict__ dx) {
@@ -457,17 +541,22 @@ namespace gacer {
 // [Cout][Cin][KH][KW] flipped and transposed into the K-major bf16 B operand
 // of a forward conv over dy: row ci, column (r*KW + s)*cread + co holds
 // w[co][ci][KH-1-r][KW-1-s]; padded rows/columns are zero.
+// (forward = 1: the plain forward B operand, row co, column (r*KW + s)*cread + ci
+//  holding w[co][ci][r][s])
 __global__ void dgrad_filter_kernel(const float* __restrict__ w, int Cout, int Cin, int KH, int KW, int cread,
-                                    int Kpad, int rows, __nv_bfloat16* __restrict__ out) {
+                                    int Kpad, int rows, int forward, __nv_bfloat16* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(rows) * Kpad;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int ci = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
-    const int tap = k / cread, co = k % cread;
+    const int row = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
+    const int tap = k / cread, col = k % cread;
     float v = 0.0f;
-    if (ci < Cin && tap < KH * KW && co < Cout) {
+    if (forward) {
+      if (row < Cout && tap < KH * KW && col < Cin)
+        v = w[((static_cast<int64_t>(row) * Cin + col) * KH + tap / KW) * KW + tap % KW];
+    } else if (row < Cin && tap < KH * KW && col < Cout) {
       const int r = tap / KW, s = tap % KW;
-      v = w[((static_cast<int64_t>(co) * Cin + ci) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
+      v = w[((static_cast<int64_t>(col) * Cin + row) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
     }
     out[i] = __float2bfloat16_rn(v);
   }
@@ -476,7 +565,14 @@ __global__ void dgrad_filter_kernel(const float* __restrict__ w, int Cout, int C
 cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
                                 void* out, cudaStream_t s) {
   dgrad_filter_kernel<<<grid_for(static_cast<int64_t>(rows) * Kpad), kThreads, 0, s>>>(
-      w, Cout, Cin, KH, KW, cread, Kpad, rows, static_cast<__nv_bfloat16*>(out));
+      w, Cout, Cin, KH, KW, cread, Kpad, rows, 0, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
+                              void* out, cudaStream_t s) {
+  dgrad_filter_kernel<<<grid_for(static_cast<int64_t>(rows) * Kpad), kThreads, 0, s>>>(
+      w, Cout, Cin, KH, KW, cread, Kpad, rows, 1, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError();
 }
 
@@ -681,6 +777,51 @@ int32_t gacer_gap_bwd(const float* dy_dev, int32_t N, int32_t HW, int32_t C, voi
   gap_bwd_kernel<<<grid_for(static_cast<int64_t>(N) * HW * (C / 8)), kThreads, 0,
                    static_cast<cudaStream_t>(stream)>>>(dy_dev, N, HW, C, static_cast<__nv_bfloat16*>(dx_dev));
   return launched("gap_bwd");
+}
+
+int32_t gacer_maxpool_fwd(const void* x_dev, int32_t N, int32_t H, int32_t W, int32_t C, int32_t KH, int32_t KW,
+                          int32_t stride, int32_t ph, int32_t pw, int32_t Ho, int32_t Wo, void* y_dev, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || KH < 1 || KW < 1 || stride < 1 || ph < 0 || pw < 0 ||
+      Ho != (H + 2 * ph - KH) / stride + 1 || Wo != (W + 2 * pw - KW) / stride + 1 || Ho < 1 || Wo < 1)
+    return bad(GACER_E_SHAPE, "maxpool_fwd: inconsistent shape");
+  if (!x_dev || !y_dev || !aligned16(x_dev) || !aligned16(y_dev))
+    return bad(GACER_E_INVALID_ARG, "maxpool_fwd: null or misaligned pointer");
+  maxpool_fwd_kernel<<<grid_for(static_cast<int64_t>(N) * Ho * Wo * (C / 8)), kThreads, 0,
+                       static_cast<cudaStream_t>(stream)>>>(static_cast<const __nv_bfloat16*>(x_dev), N, H, W, C, KH,
+                                                            KW, stride, ph, pw, Ho, Wo,
+                                                            static_cast<__nv_bfloat16*>(y_dev));
+  return launched("maxpool_fwd");
+}
+
+int32_t gacer_add(const void* a_dev, const void* b_dev, int64_t n, int32_t relu, void* y_dev, void* stream) {
+  if (n < 0 || n % 8) return bad(GACER_E_SHAPE, "add: n % 8 != 0");
+  if (!a_dev || !b_dev || !y_dev || !aligned16(a_dev) || !aligned16(b_dev) || !aligned16(y_dev))
+    return bad(GACER_E_INVALID_ARG, "add: null or misaligned pointer");
+  if (n == 0) return GACER_OK;
+  add_kernel<<<grid_for(n / 8), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(a_dev), static_cast<const __nv_bfloat16*>(b_dev), n / 8, relu,
+      static_cast<__nv_bfloat16*>(y_dev));
+  return launched("add");
+}
+
+int32_t gacer_gap_fwd(const void* x_dev, int32_t N, int32_t HW, int32_t C, void* y_dev, void* stream) {
+  if (N < 1 || HW < 1 || C < 8 || C % 8) return bad(GACER_E_SHAPE, "gap_fwd: need C % 8 == 0");
+  if (!x_dev || !y_dev || !aligned16(x_dev) || !aligned16(y_dev))
+    return bad(GACER_E_INVALID_ARG, "gap_fwd: null or misaligned pointer");
+  gap_fwd_kernel<<<grid_for(static_cast<int64_t>(N) * (C / 8)), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x_dev), N, HW, C, static_cast<__nv_bfloat16*>(y_dev));
+  return launched("gap_fwd");
+}
+
+int32_t gacer_linear_fwd(const void* x_dev, const float* w_dev, const float* b_dev, int32_t N, int32_t K, int32_t O,
+                         float* z_dev, void* stream) {
+  if (N < 1 || K < 1 || O < 1) return bad(GACER_E_SHAPE, "linear_fwd: need N, K, O >= 1");
+  if (!x_dev || !w_dev || !z_dev) return bad(GACER_E_INVALID_ARG, "linear_fwd: null pointer");
+  const int64_t n = static_cast<int64_t>(N) * O;
+  linear_fwd_kernel<<<static_cast<int>((n + kThreads - 1) / kThreads), kThreads, 0,
+                      static_cast<cudaStream_t>(stream)>>>(static_cast<const __nv_bfloat16*>(x_dev), w_dev, b_dev, N,
+                                                           K, O, z_dev);
+  return launched("linear_fwd");
 }
 
 int32_t gacer_linear_bwd(const void* x_dev, const float* w_dev, const float* dy_dev, int32_t N, int32_t K, int32_t O,

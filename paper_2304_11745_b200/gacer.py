@@ -125,6 +125,14 @@ EXPORTS = {
     "gacer_conv_wgrad_workspace": ([C.c_int32] * 10, C.c_int64),
     "gacer_conv_wgrad": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 10 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
                          C.c_int32),
+    "gacer_conv_fwd_workspace": ([C.c_int32] * 10, C.c_int64),
+    "gacer_conv_fwd": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 10 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+                       C.c_int32),
+    "gacer_maxpool_fwd": ([C.c_void_p] + [C.c_int32] * 11 + [C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_add": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_gap_fwd": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_linear_fwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                          C.c_void_p], C.c_int32),
     "gacer_softmax_ce": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p], C.c_int32),
     "gacer_sgd_momentum": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_int32,
@@ -387,6 +395,30 @@ def conv_wgrad_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw):
 
 def conv_wgrad(x, dy, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dw, ws, ws_bytes, stream=0):
     return _call("gacer_conv_wgrad", x, dy, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, dw, ws, ws_bytes, stream)
+
+
+def conv_fwd_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw):
+    return _check(lib().gacer_conv_fwd_workspace(N, H, W, Cin, Cout, KH, KW, stride, ph, pw))
+
+
+def conv_fwd(x, w, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, y, ws, ws_bytes, stream=0):
+    return _call("gacer_conv_fwd", x, w, N, H, W, Cin, Cout, KH, KW, stride, ph, pw, y, ws, ws_bytes, stream)
+
+
+def maxpool_fwd(x, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, y, stream=0):
+    return _call("gacer_maxpool_fwd", x, N, H, W, C_, KH, KW, stride, ph, pw, Ho, Wo, y, stream)
+
+
+def add(a, b, n, relu, y, stream=0):
+    return _call("gacer_add", a, b, n, relu, y, stream)
+
+
+def gap_fwd(x, N, HW, C_, y, stream=0):
+    return _call("gacer_gap_fwd", x, N, HW, C_, y, stream)
+
+
+def linear_fwd(x, w, b, N, K, O, z, stream=0):
+    return _call("gacer_linear_fwd", x, w, b, N, K, O, z, stream)
 
 
 def softmax_ce(z, labels, N, Cls, loss, dz, scratch, stream=0):
