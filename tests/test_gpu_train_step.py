@@ -162,3 +162,29 @@ def test_small_resnet_sgd_step_matches_oracle():
     assert errs["loss"] <= 2e-2 and errs["fc_w"] <= 2e-2 and errs["fc_b"] <= 2e-2 and errs["fc_sgd"] <= 2e-2, errs
     assert errs["block_dC3"] <= 2e-2 and errs["block_dW3"] <= 2e-2, errs
     assert max(v for k, v in errs.items() if k.startswith(("conv", "bn"))) <= 0.5, errs
+
+
+def test_nccl_gradient_mean_on_comm_stream():
+    """A12 transport on the device: the bucketed NCCL all-reduce of CUDA
+    gradient tensors on a dedicated stream (world size 1 here: the box has
+    one GPU; the 2-rank arithmetic is checked with gloo on the CPU)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2304_11745_b200.grad_allreduce import GradBuckets
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        shapes = [(64, 3, 7, 7), (1000, 2048), (1000,)]
+        g = [torch.randn(sh, device="cuda") for sh in shapes]
+        ref = [t.clone() for t in g]
+        comm = torch.cuda.Stream()
+        comm.wait_stream(torch.cuda.current_stream())
+        GradBuckets(shapes, bucket_bytes=1 << 20).reduce_mean(g, dist, stream=comm)
+        torch.cuda.current_stream().wait_stream(comm)
+        torch.cuda.synchronize()
+        assert all(torch.equal(a, b) for a, b in zip(g, ref))
+    finally:
+        dist.destroy_process_group()

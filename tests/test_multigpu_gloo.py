@@ -66,3 +66,45 @@ def test_gloo_world2_max_over_ranks():
         assert t == 2.0                    # max over ranks
         assert abs(thr - 48.0 / 2.0) < 1e-12
         assert placement == res[0][3]      # every rank computes the same placement
+
+
+def _grad_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    from paper_2304_11745_b200.grad_allreduce import GradBuckets
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shapes = [(64, 3, 7, 7), (64,), (256, 64, 1, 1), (1000, 2048), (1000,)]
+    rng = np.random.default_rng(100 + rank)               # each replica's own gradients
+    grads = [torch.from_numpy(rng.normal(size=s).astype(np.float32)) for s in shapes]
+    mine = [g.clone().numpy() for g in grads]
+    b = GradBuckets(shapes, bucket_bytes=1 << 20)         # several buckets
+    b.reduce_mean(grads, dist)
+    q.put((rank, mine, [g.numpy() for g in grads], len(b.buckets)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_gradient_mean_matches_oracle():
+    """A12: the bucketed all-reduce of the replicas' gradients equals the
+    oracle's replica mean (oracle/train.py allreduce_mean) on every rank."""
+    from oracle.train import allreduce_mean
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    import numpy as np
+    per_rank = [{i: {"g": g} for i, g in enumerate(r[1])} for r in res]
+    ref = allreduce_mean(per_rank)
+    for rank, _, reduced, nb in res:
+        assert nb >= 3
+        for i, g in enumerate(reduced):
+            assert np.allclose(g, ref[i]["g"], rtol=1e-6, atol=1e-7), (rank, i)
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][2], res[1][2]))   # identical on every rank
