@@ -1,0 +1,227 @@
+"""Sequential training step of one tenant from the device operators of
+include/gacer_train.h (first version).
+
+Host-side sequencing only: every arithmetic step is a call into libgacer.so
+(tcgen05 conv forward / dgrad / wgrad through single-op executor launches,
+the CUDA-core BN-train / pooling / FC / loss / SGD kernels); this module
+walks the tenant's operator list forward and then in reverse, allocates the
+saved activations and gradients in HBM, and issues the calls in order on one
+stream.  It is the training analog of the inference path's sequential
+baseline mode; running the step as executor work items (and in C) is the
+next step.
+
+Supported operator patterns (those of ResNet-18/34/50/101 and the test
+CNNs): conv -> bn -> [relu], add -> [relu], maxpool, gap -> [flatten] ->
+linear.  A ReLU is fused into its producer (BN apply or residual add); its
+backward mask is taken from the ReLU output (y > 0 iff x > 0).  Layout:
+NHWC bf16 activations, fp32 master weights / BN parameters / gradients /
+momentum buffers; a 3-channel input is zero-padded to 8 channels (the conv
+operand granule), with zero-padded filter channels that stay zero.
+BN running statistics are not updated (they do not enter the step's loss
+or gradients)."""
+from __future__ import annotations
+
+from typing import Dict, List
+
+import numpy as np
+
+from . import gacer as G
+
+
+def _pad8(c: int) -> int:
+    return (c + 7) // 8 * 8
+
+
+class SequentialTrainer:
+    def __init__(self, graph, params, batch: int, lr: float = 0.1, momentum: float = 0.9):
+        import torch
+        self.torch = torch
+        self.g, self.B, self.lr, self.mom = graph, batch, lr, momentum
+        self.ops = {op["id"]: op for op in graph.ops}
+        self.consumers: Dict[int, List[int]] = {}
+        for op in graph.ops:
+            for p in op["preds"]:
+                self.consumers.setdefault(p, []).append(op["id"])
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+        # shapes (NHWC) and parameters
+        self.shape = {0: (graph.in_h, graph.in_w, _pad8(graph.in_c))}
+        self.params: Dict[int, Dict[str, object]] = {}
+        self.fused_relu: Dict[int, int] = {}      # producer id -> relu id
+        for op in graph.ops:
+            k, oid = op["kind"], op["id"]
+            h, w, c = self.shape[op["preds"][0]]
+            if k == "conv":
+                if op["groups"] != 1 or op.get("bias"):
+                    raise NotImplementedError("grouped / biased conv training is not supported yet")
+                st = op["stride"]
+                ho, wo = (h + 2 * op["ph"] - op["kh"]) // st + 1, (w + 2 * op["pw"] - op["kw"]) // st + 1
+                wt = np.zeros((op["c_out"], c, op["kh"], op["kw"]), np.float32)
+                wt[:, :op["c_in"]] = params[oid]["w"]
+                self.params[oid] = {"w": dev(wt)}
+                self.shape[oid] = (ho, wo, op["c_out"])
+            elif k == "bn":
+                self.params[oid] = {"gamma": dev(params[oid]["gamma"]), "beta": dev(params[oid]["beta"])}
+                self.shape[oid] = (h, w, c)
+            elif k == "maxpool":
+                st = op["stride"]
+                self.shape[oid] = ((h + 2 * op["ph"] - op["kh"]) // st + 1, (w + 2 * op["pw"] - op["kw"]) // st + 1, c)
+            elif k == "gap":
+                self.shape[oid] = (1, 1, c)
+            elif k in ("flatten", "dropout", "relu", "add"):
+                self.shape[oid] = (h, w, c)
+            elif k == "linear":
+                self.params[oid] = {"w": dev(params[oid]["w"])}
+                if "b" in params[oid]:
+                    self.params[oid]["b"] = dev(params[oid]["b"])
+                self.shape[oid] = (1, 1, op["c_out"])
+            else:
+                raise NotImplementedError(f"training of {k!r}")
+            if k == "relu":
+                prod = op["preds"][0]
+                if self.ops[prod]["kind"] not in ("bn", "add") or len(self.consumers[prod]) != 1:
+                    raise NotImplementedError("a ReLU is trained fused into its BN or residual-add producer")
+                self.fused_relu[prod] = oid
+        self.bufs = {pid: {n: torch.zeros_like(t) for n, t in p.items()} for pid, p in self.params.items()}
+        self.first = True
+        # one workspace for every conv call (the largest need)
+        need = 1 << 20
+        for op in graph.ops:
+            if op["kind"] != "conv":
+                continue
+            h, w, c = self.shape[op["preds"][0]]
+            a = (self.B, h, w, c, op["c_out"], op["kh"], op["kw"], op["stride"], op["ph"], op["pw"])
+            need = max(need, G.conv_fwd_workspace(*a), G.conv_wgrad_workspace(*a))
+            if op["preds"][0] != 0:
+                need = max(need, G.conv_dgrad_workspace(*a))
+        self.ws = torch.empty(need + 256, dtype=torch.uint8, device="cuda")
+        self.WS, self.NB = (self.ws.data_ptr() + 255) // 256 * 256, need
+        maxmc = max(self.B * s[0] * s[1] * s[2] for s in self.shape.values())
+        maxc = max(s[2] for s in self.shape.values())
+        self.bn_scratch = torch.empty(G.bn_partials(maxmc, 8) * 2 * maxc + 4 * maxc + 64, device="cuda")
+        self.argmax = torch.empty(maxmc, dtype=torch.uint8, device="cuda")
+
+    # ---------------------------------------------------------------- step
+    def step(self, x_nhwc8, labels):
+        """One SGD step: x_nhwc8 bf16 [B][H][W][pad8(C)] and labels int32 [B]
+        on the device.  Returns the loss (a 1-element fp32 device tensor) and
+        the parameter gradients {op_id: {name: tensor}}."""
+        torch, B, P = self.torch, self.B, (lambda t: t.data_ptr())
+        bf = lambda shape: torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        f32 = lambda *shape: torch.empty(shape, device="cuda")
+        out = {0: x_nhwc8}
+        saved = {}
+        logits = None
+        for op in self.g.ops:
+            k, oid = op["kind"], op["id"]
+            pred = op["preds"][0]
+            h, w, c = self.shape[pred]
+            ho, wo, co = self.shape[oid]
+            if k == "conv":
+                y = bf((B, ho, wo, co))
+                G.conv_fwd(P(out[pred]), P(self.params[oid]["w"]), B, h, w, c, co, op["kh"], op["kw"], op["stride"],
+                           op["ph"], op["pw"], P(y), self.WS, self.NB)
+                out[oid] = y
+            elif k == "bn":
+                y = bf((B, h, w, c))
+                mean, var = f32(c), f32(c)
+                relu = 1 if oid in self.fused_relu else 0
+                G.bn_train_fwd(P(out[pred]), B * h * w, c, P(self.params[oid]["gamma"]), P(self.params[oid]["beta"]),
+                               op["eps"], relu, P(y), P(mean), P(var), P(self.bn_scratch))
+                saved[oid] = (mean, var)
+                out[oid] = y
+            elif k == "relu":
+                out[oid] = out[pred]                  # fused into the producer
+            elif k == "add":
+                y = bf((B, h, w, c))
+                G.add(P(out[op["preds"][0]]), P(out[op["preds"][1]]), y.numel(), 1 if oid in self.fused_relu else 0,
+                      P(y))
+                out[oid] = y
+            elif k == "maxpool":
+                y = bf((B, ho, wo, c))
+                G.maxpool_fwd(P(out[pred]), B, h, w, c, op["kh"], op["kw"], op["stride"], op["ph"], op["pw"], ho, wo,
+                              P(y))
+                out[oid] = y
+            elif k == "gap":
+                y = bf((B, c))
+                G.gap_fwd(P(out[pred]), B, h * w, c, P(y))
+                out[oid] = y
+            elif k in ("flatten", "dropout"):
+                out[oid] = out[pred]
+            elif k == "linear":
+                z = f32(B, co)
+                b = self.params[oid].get("b")
+                G.linear_fwd(P(out[pred]), P(self.params[oid]["w"]), P(b) if b is not None else None, B, c, co, P(z))
+                out[oid] = z
+                logits = z
+        ncls = logits.shape[1]
+        loss, dz = f32(1), f32(B, ncls)
+        G.softmax_ce(P(logits), P(labels), B, ncls, P(loss), P(dz), P(f32(B)))
+        # ---------------------------------------------------------- backward
+        grads: Dict[int, Dict[str, object]] = {}
+        dval = {self.g.ops[-1]["id"]: dz}
+
+        def acc(tid, g):
+            if tid == 0:
+                return
+            if tid in dval:
+                G.add(P(dval[tid]), P(g), g.numel(), 0, P(dval[tid]))
+            else:
+                dval[tid] = g
+
+        for op in reversed(self.g.ops):
+            k, oid = op["kind"], op["id"]
+            dy = dval.pop(oid, None)
+            if dy is None:
+                continue
+            pred = op["preds"][0]
+            h, w, c = self.shape[pred]
+            ho, wo, co = self.shape[oid]
+            if k == "linear":
+                dx = f32(B, c)
+                gw = f32(co, c)
+                gb = f32(co) if "b" in self.params[oid] else None
+                G.linear_bwd(P(out[pred]), P(self.params[oid]["w"]), P(dy), B, c, co, P(dx), P(gw),
+                             P(gb) if gb is not None else None)
+                grads[oid] = {"w": gw, **({"b": gb} if gb is not None else {})}
+                acc(pred, dx)
+            elif k in ("flatten", "dropout"):
+                acc(pred, dy)
+            elif k == "gap":
+                dx = bf((B, h, w, c))
+                G.gap_bwd(P(dy), B, h * w, c, P(dx))
+                acc(pred, dx)
+            elif k == "relu":
+                G.relu_bwd(P(out[oid]), P(dy), dy.numel(), 0, P(dy))
+                acc(pred, dy)
+            elif k == "add":
+                acc(op["preds"][0], dy)
+                acc(op["preds"][1], dy.clone())
+            elif k == "bn":
+                dx = bf((B, h, w, c))
+                gg, gb = f32(c), f32(c)
+                mean, var = saved[oid]
+                G.bn_train_bwd(P(out[pred]), P(dy), B * h * w, c, P(self.params[oid]["gamma"]), P(mean), P(var),
+                               op["eps"], P(dx), P(gg), P(gb), P(self.bn_scratch))
+                grads[oid] = {"gamma": gg, "beta": gb}
+                acc(pred, dx)
+            elif k == "maxpool":
+                dx = bf((B, h, w, c))
+                G.maxpool_bwd(P(out[pred]), P(dy), B, h, w, c, op["kh"], op["kw"], op["stride"], op["ph"], op["pw"],
+                              ho, wo, P(dx), P(self.argmax))
+                acc(pred, dx)
+            elif k == "conv":
+                gw = f32(co, c, op["kh"], op["kw"])
+                a = (B, h, w, c, co, op["kh"], op["kw"], op["stride"], op["ph"], op["pw"])
+                G.conv_wgrad(P(out[pred]), P(dy), *a, P(gw), self.WS, self.NB)
+                grads[oid] = {"w": gw}
+                if pred != 0:
+                    dx = bf((B, h, w, c))
+                    G.conv_dgrad(P(dy), P(self.params[oid]["w"]), *a, P(dx), self.WS, self.NB)
+                    acc(pred, dx)
+        # ---------------------------------------------------------- SGD
+        for oid, gd in grads.items():
+            for n, gt in gd.items():
+                pt = self.params[oid][n]
+                G.sgd_momentum(P(pt), P(gt), P(self.bufs[oid][n]), pt.numel(), self.lr, self.mom, int(self.first))
+        self.first = False
+        return loss, grads
