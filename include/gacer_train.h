@@ -159,7 +159,8 @@ int32_t gacer_add(const void* a_dev, const void* b_dev, int64_t n, int32_t relu,
 int32_t gacer_gap_fwd(const void* x_dev, int32_t N, int32_t HW, int32_t C, void* y_dev, void* stream);
 
 /* FC forward (oracle_linear): z[n][o] = b[o] + sum_k w[o][k] x[n][k]; x bf16
- * [N][K], w fp32 [O][K], b fp32 [O] (may be NULL), z fp32 [N][O] (logits). */
+ * [N][K], w fp32 [O][K], b fp32 [O] (may be NULL), z fp32 [N][O] (logits).
+ * One warp per output (lane-strided k, fixed butterfly: deterministic). */
 int32_t gacer_linear_fwd(const void* x_dev, const float* w_dev, const float* b_dev, int32_t N, int32_t K, int32_t O,
                          float* z_dev, void* stream);
 

@@ -420,17 +420,23 @@ __global__ void __launch_bounds__(kThreads) gap_fwd_kernel(const __nv_bfloat16* 
   }
 }
 
-// z[n][o] = b[o] + sum_k w[o][k] x[n][k] (x bf16, w fp32), summed in k order
+// z[n][o] = b[o] + sum_k w[o][k] x[n][k] (x bf16, w fp32): one warp per
+// output, lane l sums k = l, l+32, ... (coalesced rows of w and x), then a
+// fixed xor-butterfly combines the lanes (deterministic)
 __global__ void __launch_bounds__(kThreads) linear_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                               const float* __restrict__ w, const float* __restrict__ b,
                                                               int N, int K, int O, float* __restrict__ z) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<int64_t>(N) * O) return;
-  const int n = static_cast<int>(i / O), o = static_cast<int>(i % O);
-  float a = b ? b[o] : 0.0f;
-  for (int k = 0; k < K; ++k)
-    a = fmaf(__bfloat162float(x[static_cast<int64_t>(n) * K + k]), w[static_cast<int64_t>(o) * K + k], a);
-  z[i] = a;
+  const int64_t wid = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= static_cast<int64_t>(N) * O) return;
+  const int n = static_cast<int>(wid / O), o = static_cast<int>(wid % O);
+  const __nv_bfloat16* xr = x + static_cast<int64_t>(n) * K;
+  const float* wr = w + static_cast<int64_t>(o) * K;
+  float a = 0.0f;
+  for (int k = lane; k < K; k += 32) a = fmaf(__bfloat162float(xr[k]), wr[k], a);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+  if (lane == 0) z[wid] = a + (b ? b[o] : 0.0f);
 }
 
 // FC backward: one output element per thread, reductions in index order
@@ -817,7 +823,7 @@ int32_t gacer_linear_fwd(const void* x_dev, const float* w_dev, const float* b_d
                          float* z_dev, void* stream) {
   if (N < 1 || K < 1 || O < 1) return bad(GACER_E_SHAPE, "linear_fwd: need N, K, O >= 1");
   if (!x_dev || !w_dev || !z_dev) return bad(GACER_E_INVALID_ARG, "linear_fwd: null pointer");
-  const int64_t n = static_cast<int64_t>(N) * O;
+  const int64_t n = static_cast<int64_t>(N) * O * 32;   // one warp per output
   linear_fwd_kernel<<<static_cast<int>((n + kThreads - 1) / kThreads), kThreads, 0,
                       static_cast<cudaStream_t>(stream)>>>(static_cast<const __nv_bfloat16*>(x_dev), w_dev, b_dev, N,
                                                            K, O, z_dev);
