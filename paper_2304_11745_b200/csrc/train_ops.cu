@@ -149,22 +149,28 @@ __global__ void bn_finalize_kernel(const float* __restrict__ part, int P, int64_
                                    const float* __restrict__ gamma, const float* __restrict__ beta,
                                    const float* __restrict__ mean_in, const float* __restrict__ var_in, float eps,
                                    float* __restrict__ o1, float* __restrict__ o2, float* __restrict__ coef) {
-  // one warp per channel: lane l sums partials l, l+32, ... in order, then a
-  // fixed xor-butterfly combines the lanes (the same order on every run)
-  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (c >= C) return;
+  // 32 channels per CTA, lane = channel (coalesced rows of the partials);
+  // warp w sums the partials p = w, w+8, ... in order, then warp 0 adds the
+  // eight warp sums in warp order (the same order on every run)
+  __shared__ double red[2][8][32];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   double a = 0.0, b = 0.0;
-  for (int p = lane; p < P; p += 32) {
-    a += part[(static_cast<size_t>(p) * 2 + 0) * C + c];
-    b += part[(static_cast<size_t>(p) * 2 + 1) * C + c];
+  if (c < C)
+    for (int p = wp; p < P; p += 8) {
+      a += part[(static_cast<size_t>(p) * 2 + 0) * C + c];
+      b += part[(static_cast<size_t>(p) * 2 + 1) * C + c];
+    }
+  red[0][wp][lane] = a;
+  red[1][wp][lane] = b;
+  __syncthreads();
+  if (wp != 0 || c >= C) return;
+  a = red[0][0][lane];
+  b = red[1][0][lane];
+  for (int q = 1; q < 8; ++q) {
+    a += red[0][q][lane];
+    b += red[1][q][lane];
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  if (lane != 0) return;
   const double Md = static_cast<double>(M);
   if (MODE == 0) {
     const double mu = a / Md;
@@ -720,7 +726,7 @@ int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float*
   const auto* x = static_cast<const __nv_bfloat16*>(x_dev);
   float* coef = scratch_dev + static_cast<size_t>(P) * 2 * C;
   bn_partial_kernel<0><<<P, kThreads, 0, s>>>(x, nullptr, M, C, nullptr, nullptr, 0.0f, scratch_dev);
-  bn_finalize_kernel<0><<<(C + 7) / 8, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, beta_dev, nullptr, nullptr,
+  bn_finalize_kernel<0><<<(C + 31) / 32, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, beta_dev, nullptr, nullptr,
                                                        eps, mean_dev, var_dev, coef);
   bn_elementwise_kernel<0><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, nullptr, M, C, coef, relu,
                                                                       static_cast<__nv_bfloat16*>(y_dev));
@@ -740,7 +746,7 @@ int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, int64_t M, int
   const auto* dy = static_cast<const __nv_bfloat16*>(dy_dev);
   float* coef = scratch_dev + static_cast<size_t>(P) * 2 * C;
   bn_partial_kernel<1><<<P, kThreads, 0, s>>>(x, dy, M, C, mean_dev, var_dev, eps, scratch_dev);
-  bn_finalize_kernel<1><<<(C + 7) / 8, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, nullptr, mean_dev, var_dev,
+  bn_finalize_kernel<1><<<(C + 31) / 32, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, nullptr, mean_dev, var_dev,
                                                        eps, dgamma_dev, dbeta_dev, coef);
   bn_elementwise_kernel<1><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, dy, M, C, coef, 0,
                                                                       static_cast<__nv_bfloat16*>(dx_dev));
