@@ -205,6 +205,9 @@ struct State {
   uint32_t* d_cluster_total = nullptr;
   uint32_t* d_exit = nullptr;
   int32_t* d_error = nullptr;
+  float* d_ones = nullptr;    // unit BN scale / zero bias of the standalone GEMM calls (A11)
+  float* d_zeros = nullptr;
+  int n_unit = 0;
   int64_t* d_trace = nullptr;
   int64_t* d_dbg = nullptr;     // GACER_DEBUG_TIMING=1: per-CTA milestones
   size_t n_dbg = 0;
@@ -1563,6 +1566,8 @@ int gacer_shutdown(void) {
     S.copy_stream = nullptr;
     if (S.ev0) cudaEventDestroy(S.ev0);
     if (S.ev1) cudaEventDestroy(S.ev1);
+    if (S.d_ones) cudaFree(S.d_ones);
+    if (S.d_zeros) cudaFree(S.d_zeros);
   }
   S = State();
   return GACER_OK;
@@ -1811,13 +1816,37 @@ int gacer_debug_timing(int64_t* out, int64_t cap, int reset) {
 
 }  // extern "C"
 
+// Library-owned unit scale / zero bias vectors for the standalone GEMM calls
+// (no folded BN): written once, grown on demand (cudaFree synchronises the
+// device, so launches still reading the old vectors have finished).
+namespace {
+int unit_vectors(int n, const float** ones, const float** zeros) {
+  if (n > S.n_unit) {
+    const int m = std::max(n, 4096);
+    if (S.d_ones) cudaFree(S.d_ones);
+    if (S.d_zeros) cudaFree(S.d_zeros);
+    S.d_ones = S.d_zeros = nullptr;
+    S.n_unit = 0;
+    CUDA_TRY(cudaMalloc(&S.d_ones, m * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&S.d_zeros, m * sizeof(float)));
+    std::vector<float> h(m, 1.0f);
+    CUDA_TRY(cudaMemcpy(S.d_ones, h.data(), m * sizeof(float), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(S.d_zeros, 0, m * sizeof(float)));
+    S.n_unit = m;
+  }
+  *ones = S.d_ones;
+  *zeros = S.d_zeros;
+  return 0;
+}
+}  // namespace
+
 // ------------------------------------------------------------------------
 // A11: convolution data gradient on the tcgen05 implicit-GEMM path
 // ------------------------------------------------------------------------
 namespace {
 struct DgradGeom {
   int cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode, ph, pw, Hd, Wd, Hdd, Wdd;
-  size_t off_op, off_maps, off_scale, off_bias, off_w, off_dil, bytes;
+  size_t off_op, off_maps, off_w, off_dil, bytes;
 };
 
 int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int pad_h, int pad_w,
@@ -1845,13 +1874,10 @@ int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.tiles_m = cdiv(g.M, BM);
   g.tiles_n = cdiv(Cin, g.bn);
   g.rows = g.tiles_n * g.bn;
-  const int nsb = roundup(Cin, 8) + 8;
   size_t o = 0;
   auto take = [&](size_t n, size_t al) { o = (o + al - 1) / al * al; const size_t r = o; o += n; return r; };
   g.off_op = take(sizeof(OpDev), 256);
   g.off_maps = take(3 * sizeof(CUtensorMap), 128);
-  g.off_scale = take(nsb * sizeof(float), 16);
-  g.off_bias = take(nsb * sizeof(float), 16);
   g.off_w = take(static_cast<size_t>(g.rows) * g.Kpad * 2, 256);
   g.off_dil = stride == 1 ? 0 : take(static_cast<size_t>(N) * g.Hdd * g.Wdd * Cout * 2, 256);
   g.bytes = o;
@@ -1883,17 +1909,15 @@ int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int3
   auto st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(ws_dev);
   void* wt = ws + g.off_w;
-  float* scale = reinterpret_cast<float*>(ws + g.off_scale);
-  float* bias = reinterpret_cast<float*>(ws + g.off_bias);
-  const int nsb = roundup(Cin, 8) + 8;
+  const float *scale = nullptr, *bias = nullptr;
+  const int nsb = g.rows + 8;
   CUDA_TRY(launch_dgrad_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
   const void* src = dy_dev;
   if (stride > 1) {
     CUDA_TRY(launch_dilate(dy_dev, N, g.Hd, g.Wd, Cout, stride, g.Hdd, g.Wdd, ws + g.off_dil, st));
     src = ws + g.off_dil;
   }
-  CUDA_TRY(launch_fill(scale, nsb, 1.0f, st));
-  CUDA_TRY(launch_fill(bias, nsb, 0.0f, st));
+  if (int rc0 = unit_vectors(nsb, &scale, &bias)) return rc0;
   OpDev d;
   std::memset(&d, 0, sizeof d);
   d.kind = DK_GEMM;
@@ -1949,7 +1973,7 @@ namespace {
 struct WgradGeom {
   int Ho, Wo, Ngemm, Kpad, nkb, bn, tiles_m, tiles_n, rows_a, rows_b, split;
   int64_t M;
-  size_t off_op, off_maps, off_scale, off_bias, off_a, off_b, off_part, off_cnt, off_g, bytes;
+  size_t off_op, off_maps, off_a, off_b, off_part, off_cnt, off_g, bytes;
 };
 
 int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int pad_h, int pad_w, WgradGeom& g) {
@@ -1974,14 +1998,11 @@ int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   while (g.split < MAX_SPLIT_LONG && g.tiles_m * g.tiles_n * g.split * 2 <= 2 * kSplitSms &&
          g.nkb / (g.split * 2) >= 8)
     g.split *= 2;
-  const int nsb = g.rows_b + 8;
   const int tiles = g.tiles_m * g.tiles_n;
   size_t o = 0;
   auto take = [&](size_t n, size_t al) { o = (o + al - 1) / al * al; const size_t r = o; o += n; return r; };
   g.off_op = take(sizeof(OpDev), 256);
   g.off_maps = take(3 * sizeof(CUtensorMap), 128);
-  g.off_scale = take(nsb * sizeof(float), 16);
-  g.off_bias = take(nsb * sizeof(float), 16);
   g.off_a = take(static_cast<size_t>(g.rows_a) * g.Kpad * 2, 256);
   g.off_b = take(static_cast<size_t>(g.rows_b) * g.Kpad * 2, 256);
   g.off_part = take(static_cast<size_t>(tiles) * g.split * BM * g.bn * sizeof(float), 256);
@@ -2028,8 +2049,8 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   // dy [M][Cout] viewed as a 1x1 "im2col" of itself: the transpose
   CUDA_TRY(launch_transpose_im2col(dy_dev, static_cast<int>(g.M), 1, 1, Cout, 1, 1, 1, 1, 1, 0, 0, g.M, g.Kpad, a, st));
   CUDA_TRY(launch_transpose_im2col(x_dev, N, H, W, Cin, g.Ho, g.Wo, KH, KW, stride, pad_h, pad_w, g.M, g.Kpad, b, st));
-  CUDA_TRY(launch_fill(reinterpret_cast<float*>(ws + g.off_scale), nsb, 1.0f, st));
-  CUDA_TRY(launch_fill(reinterpret_cast<float*>(ws + g.off_bias), nsb, 0.0f, st));
+  const float *ones = nullptr, *zeros = nullptr;
+  if (int rc0 = unit_vectors(nsb, &ones, &zeros)) return rc0;
   OpDev d;
   std::memset(&d, 0, sizeof d);
   d.kind = DK_GEMM;
@@ -2045,8 +2066,8 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   d.tiles_m = g.tiles_m; d.tiles_n = g.tiles_n; d.bm = BM; d.bn = g.bn;
   d.split_k = g.split; d.nkb = g.nkb;
   d.wt = b; d.ldw = g.Kpad;
-  d.scale = reinterpret_cast<float*>(ws + g.off_scale);
-  d.bias = reinterpret_cast<float*>(ws + g.off_bias);
+  d.scale = ones;
+  d.bias = zeros;
   d.partial = reinterpret_cast<float*>(ws + g.off_part);
   d.tile_cnt = reinterpret_cast<uint32_t*>(ws + g.off_cnt);
   d.a_mode = A_ROWS;
@@ -2079,7 +2100,7 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
 namespace {
 struct FwdGeom {
   int Ho, Wo, cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode;
-  size_t off_op, off_maps, off_scale, off_bias, off_w, bytes;
+  size_t off_op, off_maps, off_w, bytes;
 };
 
 int fwd_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int ph, int pw, FwdGeom& g) {
@@ -2103,13 +2124,10 @@ int fwd_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride,
   g.tiles_m = cdiv(g.M, BM);
   g.tiles_n = cdiv(Cout, g.bn);
   g.rows = g.tiles_n * g.bn;
-  const int nsb = g.rows + 8;
   size_t o = 0;
   auto take = [&](size_t n, size_t al) { o = (o + al - 1) / al * al; const size_t r = o; o += n; return r; };
   g.off_op = take(sizeof(OpDev), 256);
   g.off_maps = take(3 * sizeof(CUtensorMap), 128);
-  g.off_scale = take(nsb * sizeof(float), 16);
-  g.off_bias = take(nsb * sizeof(float), 16);
   g.off_w = take(static_cast<size_t>(g.rows) * g.Kpad * 2, 256);
   g.bytes = o;
   return 0;
@@ -2140,12 +2158,10 @@ int32_t gacer_conv_fwd(const void* x_dev, const float* w_dev, int32_t N, int32_t
   auto st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(ws_dev);
   void* wt = ws + g.off_w;
-  float* scale = reinterpret_cast<float*>(ws + g.off_scale);
-  float* bias = reinterpret_cast<float*>(ws + g.off_bias);
+  const float *scale = nullptr, *bias = nullptr;
   const int nsb = g.rows + 8;
   CUDA_TRY(launch_fwd_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
-  CUDA_TRY(launch_fill(scale, nsb, 1.0f, st));
-  CUDA_TRY(launch_fill(bias, nsb, 0.0f, st));
+  if (int rc0 = unit_vectors(nsb, &scale, &bias)) return rc0;
   OpDev d;
   std::memset(&d, 0, sizeof d);
   d.kind = DK_GEMM;
