@@ -1696,7 +1696,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->tempty[abuf]);
     ++acc;
-    if (split > 1) {
+    if (split > 1 && !opg.partials_only) {   // last arrival reduces the splits in order
       named_bar_sync(2, NEPI);
       if (etid == 0) {
         __threadfence();

@@ -91,7 +91,8 @@ struct OpDev {
                            // DW: [kh*kw][C] channel-minor
   int32_t ldw, pad2;
   const void* act_b;       // swap-AB: activations as the B operand, row stride ldb (elements)
-  int32_t ldb, pad3;
+  int32_t ldb;
+  int32_t partials_only;   // split-K: write the per-split partials only (reduced by a separate kernel)
   const float* scale;      // [Cout] folded BN scale (1 if no BN)
   const float* bias;       // [Cout] folded BN shift + conv bias
   float* partial;          // split-K workspace [tiles][split][BM*bn] fp32

@@ -40,6 +40,8 @@ cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, i
 cudaError_t launch_wgrad_permute(const float* g, int Cout, int Cin, int KH, int KW, float* dw, cudaStream_t s);
 cudaError_t launch_fwd_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
                               void* out, cudaStream_t s);
+cudaError_t launch_wgrad_reduce(const float* part, int Cout, int Cin, int KH, int KW, int bn, int tiles_n, int split,
+                                float* dw, cudaStream_t s);
 }  // namespace gacer
 
 using namespace gacer;
@@ -2069,6 +2071,7 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   d.scale = ones;
   d.bias = zeros;
   d.partial = reinterpret_cast<float*>(ws + g.off_part);
+  d.partials_only = g.split > 1 ? 1 : 0;
   d.tile_cnt = reinterpret_cast<uint32_t*>(ws + g.off_cnt);
   d.a_mode = A_ROWS;
   CUtensorMap maps[3];
@@ -2087,7 +2090,10 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   base.watchdog_ns = 2000000000LL;
   CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + g.off_op), 0, DK_GEMM,
                      g.tiles_m * g.tiles_n * g.split, S.num_sms, st));
-  CUDA_TRY(launch_wgrad_permute(gbuf, Cout, Cin, KH, KW, dw_dev, st));
+  if (g.split > 1)   // the splits are summed in order by a parallel kernel, straight into dW's layout
+    CUDA_TRY(launch_wgrad_reduce(d.partial, Cout, Cin, KH, KW, g.bn, g.tiles_n, g.split, dw_dev, st));
+  else
+    CUDA_TRY(launch_wgrad_permute(gbuf, Cout, Cin, KH, KW, dw_dev, st));
   return GACER_OK;
 }
 

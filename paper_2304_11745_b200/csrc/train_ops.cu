@@ -690,6 +690,47 @@ __global__ void wgrad_permute_kernel(const float* __restrict__ g, int Cout, int 
   }
 }
 
+// Weight-gradient split-K reduction: the GEMM's per-split partial tiles
+// (layout [tile][split][bn/4][128 rows] float4) summed in split order, written
+// straight into dW's master [Cout][Cin][KH][KW] layout.  One thread per
+// (4-column group, row): consecutive threads read consecutive float4 rows.
+__global__ void __launch_bounds__(kThreads) wgrad_reduce_kernel(const float* __restrict__ part, int Cout, int Cin,
+                                                                int KH, int KW, int bn, int tiles_n, int split,
+                                                                float* __restrict__ dw) {
+  const int Ng = KH * KW * Cin;
+  const int g4 = (Ng + 3) / 4;
+  const int64_t total = static_cast<int64_t>(g4) * Cout;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int co = static_cast<int>(i % Cout), q = static_cast<int>(i / Cout);
+    const int n0 = q * 4;
+    const int tile = (co / 128) * tiles_n + n0 / bn;
+    const int r = co % 128, c4 = (n0 % bn) / 4;
+    const float4* src = reinterpret_cast<const float4*>(part) +
+                        (static_cast<int64_t>(tile) * split * (bn / 4) + c4) * 128 + r;
+    float4 a = src[0];
+    for (int ks = 1; ks < split; ++ks) {
+      const float4 b = src[static_cast<int64_t>(ks) * (bn / 4) * 128];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    const float v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + j;
+      if (n >= Ng) break;
+      const int tap = n / Cin, ci = n % Cin;
+      dw[((static_cast<int64_t>(co) * Cin + ci) * KH + tap / KW) * KW + tap % KW] = v[j];
+    }
+  }
+}
+
+cudaError_t launch_wgrad_reduce(const float* part, int Cout, int Cin, int KH, int KW, int bn, int tiles_n, int split,
+                                float* dw, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>((KH * KW * Cin + 3) / 4) * Cout;
+  wgrad_reduce_kernel<<<grid_for(total), kThreads, 0, s>>>(part, Cout, Cin, KH, KW, bn, tiles_n, split, dw);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_wgrad_permute(const float* g, int Cout, int Cin, int KH, int KW, float* dw, cudaStream_t s) {
   wgrad_permute_kernel<<<grid_for(static_cast<int64_t>(Cout) * Cin * KH * KW), kThreads, 0, s>>>(g, Cout, Cin, KH, KW,
                                                                                                 dw);
