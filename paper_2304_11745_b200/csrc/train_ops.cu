@@ -625,8 +625,12 @@ __global__ void __launch_bounds__(256) transpose_im2col_kernel(const __nv_bfloat
                                                                __nv_bfloat16* __restrict__ out) {
   // 64 pixels x 64 channels per CTA: 16-byte loads along the channels,
   // a transposed smem tile, 16-byte stores along the pixels
-  constexpr int T = 64, LD = T + 8;
-  __shared__ __align__(16) __nv_bfloat16 tile[T][LD];   // [channel][pixel]
+  // [channel][pixel] tile, 16-byte pixel blocks XOR-swizzled by the channel
+  // octet: the transposing scalar stores of a warp hit 32 distinct banks and
+  // the 16-byte row reads stay contiguous
+  constexpr int T = 64;
+  __shared__ __align__(16) __nv_bfloat16 tile[T * T];
+  auto at = [](int c, int i) { return c * T + ((((i >> 3) ^ (c >> 3)) & 7) << 3) + (i & 7); };
   const int t = blockIdx.z;
   const int r = t / KW, q = t % KW;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * T;
@@ -639,8 +643,11 @@ __global__ void __launch_bounds__(256) transpose_im2col_kernel(const __nv_bfloat
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(0.0f);
     if (m < M && c0 + cg < C) {
-      const int wo = static_cast<int>(m % Wo), ho = static_cast<int>((m / Wo) % Ho);
-      const int n = static_cast<int>(m / (static_cast<int64_t>(Wo) * Ho));
+      const uint32_t m32 = static_cast<uint32_t>(m);        // M < 2^30 (checked on the host): 32-bit division
+      const uint32_t pq = m32 / static_cast<uint32_t>(Wo);   // (n, ho) of the pixel
+      const int wo = static_cast<int>(m32 - pq * static_cast<uint32_t>(Wo));
+      const int n = static_cast<int>(pq / static_cast<uint32_t>(Ho));
+      const int ho = static_cast<int>(pq - static_cast<uint32_t>(n) * static_cast<uint32_t>(Ho));
       const int hi = ho * S - ph + r, wi = wo * S - pw + q;
       if (hi >= 0 && hi < H && wi >= 0 && wi < W) {
         const __nv_bfloat16* src = x + ((static_cast<int64_t>(n) * H + hi) * W + wi) * C + c0 + cg;
@@ -655,7 +662,7 @@ __global__ void __launch_bounds__(256) transpose_im2col_kernel(const __nv_bfloat
       }
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) tile[cg + j][i] = v[j];
+    for (int j = 0; j < 8; ++j) tile[at(cg + j, i)] = v[j];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < T * (T / 8); e += blockDim.x) {
@@ -664,7 +671,7 @@ __global__ void __launch_bounds__(256) transpose_im2col_kernel(const __nv_bfloat
     const int64_t m = m0 + mg;
     if (c < C && m < Kpad)                                      // Kpad is a multiple of 64: whole groups
       *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(t) * C + c) * Kpad + m) =
-          *reinterpret_cast<const uint4*>(&tile[cc][mg]);
+          *reinterpret_cast<const uint4*>(&tile[at(cc, mg)]);
   }
 }
 
