@@ -81,7 +81,23 @@ class SequentialTrainer:
                 if self.ops[prod]["kind"] not in ("bn", "add") or len(self.consumers[prod]) != 1:
                     raise NotImplementedError("a ReLU is trained fused into its BN or residual-add producer")
                 self.fused_relu[prod] = oid
-        self.bufs = {pid: {n: torch.zeros_like(t) for n, t in p.items()} for pid, p in self.params.items()}
+        # one flat fp32 buffer each for the parameters, their gradients and
+        # the momentum buffers: the SGD update is ONE launch over the whole
+        # model, and the gradient all-reduce (A12) sees one contiguous buffer
+        keys = [(pid, n) for pid in self.params for n in self.params[pid]]
+        total = sum(self.params[pid][n].numel() for pid, n in keys)
+        self.flat_p = torch.empty(total, device="cuda")
+        self.flat_g = torch.zeros(total, device="cuda")
+        self.flat_m = torch.zeros(total, device="cuda")
+        self.gview: Dict[int, Dict[str, object]] = {}
+        off = 0
+        for pid, n in keys:
+            t = self.params[pid][n]
+            k = t.numel()
+            self.flat_p[off:off + k].copy_(t.reshape(-1))
+            self.params[pid][n] = self.flat_p[off:off + k].view(t.shape)
+            self.gview.setdefault(pid, {})[n] = self.flat_g[off:off + k].view(t.shape)
+            off += k
         self.first = True
         # one workspace for every conv call (the largest need)
         need = 1 << 20
@@ -178,8 +194,8 @@ class SequentialTrainer:
             ho, wo, co = self.shape[oid]
             if k == "linear":
                 dx = f32(B, c)
-                gw = f32(co, c)
-                gb = f32(co) if "b" in self.params[oid] else None
+                gw = self.gview[oid]["w"]
+                gb = self.gview[oid].get("b")
                 G.linear_bwd(P(out[pred]), P(self.params[oid]["w"]), P(dy), B, c, co, P(dx), P(gw),
                              P(gb) if gb is not None else None)
                 grads[oid] = {"w": gw, **({"b": gb} if gb is not None else {})}
@@ -198,7 +214,7 @@ class SequentialTrainer:
                 acc(op["preds"][1], dy.clone())
             elif k == "bn":
                 dx = bf((B, h, w, c))
-                gg, gb = f32(c), f32(c)
+                gg, gb = self.gview[oid]["gamma"], self.gview[oid]["beta"]
                 mean, var = saved[oid]
                 G.bn_train_bwd(P(out[pred]), P(dy), B * h * w, c, P(self.params[oid]["gamma"]), P(mean), P(var),
                                op["eps"], P(dx), P(gg), P(gb), P(self.bn_scratch))
@@ -210,7 +226,7 @@ class SequentialTrainer:
                               ho, wo, P(dx), P(self.argmax))
                 acc(pred, dx)
             elif k == "conv":
-                gw = f32(co, c, op["kh"], op["kw"])
+                gw = self.gview[oid]["w"]
                 a = (B, h, w, c, co, op["kh"], op["kw"], op["stride"], op["ph"], op["pw"])
                 G.conv_wgrad(P(out[pred]), P(dy), *a, P(gw), self.WS, self.NB)
                 grads[oid] = {"w": gw}
@@ -219,9 +235,9 @@ class SequentialTrainer:
                     G.conv_dgrad(P(dy), P(self.params[oid]["w"]), *a, P(dx), self.WS, self.NB)
                     acc(pred, dx)
         # ---------------------------------------------------------- SGD
-        for oid, gd in grads.items():
-            for n, gt in gd.items():
-                pt = self.params[oid][n]
-                G.sgd_momentum(P(pt), P(gt), P(self.bufs[oid][n]), pt.numel(), self.lr, self.mom, int(self.first))
+        # (every parameter has a gradient: a ResNet's whole parameter set is
+        #  written by the backward pass above, so one launch updates it all)
+        G.sgd_momentum(P(self.flat_p), P(self.flat_g), P(self.flat_m), self.flat_p.numel(), self.lr, self.mom,
+                       int(self.first))
         self.first = False
         return loss, grads
