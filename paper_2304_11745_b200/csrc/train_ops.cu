@@ -156,11 +156,26 @@ __global__ void bn_finalize_kernel(const float* __restrict__ part, int P, int64_
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   double a = 0.0, b = 0.0;
-  if (c < C)
-    for (int p = wp; p < P; p += 8) {
+  if (c < C) {
+    int p = wp;
+    for (; p + 24 < P; p += 32) {     // four partials' loads in flight, summed in order
+      float x0[4], x1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = part[(static_cast<size_t>(p + 8 * u) * 2 + 0) * C + c];
+        x1[u] = part[(static_cast<size_t>(p + 8 * u) * 2 + 1) * C + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a += x0[u];
+        b += x1[u];
+      }
+    }
+    for (; p < P; p += 8) {
       a += part[(static_cast<size_t>(p) * 2 + 0) * C + c];
       b += part[(static_cast<size_t>(p) * 2 + 1) * C + c];
     }
+  }
   red[0][wp][lane] = a;
   red[1][wp][lane] = b;
   __syncthreads();
