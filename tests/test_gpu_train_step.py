@@ -231,3 +231,35 @@ def test_sequential_trainer_resnet_step(name, hw, B):
     # within 2e-2 on the device's own tensors (test_gpu_train_ops.py)
     assert maxrel(gw, grads_o[fc]["w"]) <= (3e-2 if name == "resnet50" else 2e-2)
     assert l2 < l1
+
+
+def test_training_step_is_bitwise_reproducible():
+    """SURVEY §8(c) C2b reading (4): the training step's gradients and updated
+    weights are bitwise identical run to run (fixed-order reductions
+    everywhere, no atomics on values)."""
+    import torch
+    from paper_2304_11745_b200 import gacer as G
+    from paper_2304_11745_b200.train_driver import SequentialTrainer
+
+    g = workloads.build_model("resnet18", 64)
+    B = 4
+    params = workloads.make_params(g, 43, "fp32")
+    x = workloads.make_input(g, B, 43, "bf16")
+    labels = workloads.make_labels(B, 43)
+    xp = np.zeros((B, 64, 64, 8), np.float32)
+    xp[..., :3] = x.transpose(0, 2, 3, 1)
+    outs = []
+    G.gacer_init(0)
+    try:
+        xd = torch.from_numpy(xp).to(torch.bfloat16).cuda()
+        lab = torch.from_numpy(labels).cuda()
+        for _ in range(2):
+            tr = SequentialTrainer(g, params, B)
+            loss, _ = tr.step(xd, lab)
+            torch.cuda.synchronize()
+            outs.append((float(loss), tr.flat_g.clone(), tr.flat_p.clone()))
+            del tr
+    finally:
+        G.gacer_shutdown()
+    assert outs[0][0] == outs[1][0]
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
