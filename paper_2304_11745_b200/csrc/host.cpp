@@ -1872,7 +1872,10 @@ int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.Kpad = roundup(g.K, BK);
   g.nkb = g.Kpad / BK;
   g.M = N * H * W;
-  g.bn = Cin >= 128 ? 128 : roundup(Cin, 16);
+  // 128x256 tiles for wide outputs (half the A-operand smem traffic per FLOP,
+  // the mainloop being smem-port bound: DESIGN §4.1) when the M tiles still
+  // cover the SMs
+  g.bn = (Cin >= 256 && cdiv(g.M, BM) >= kSplitSms) ? 256 : (Cin >= 128 ? 128 : roundup(Cin, 16));
   g.tiles_m = cdiv(g.M, BM);
   g.tiles_n = cdiv(Cin, g.bn);
   g.rows = g.tiles_n * g.bn;
@@ -2126,7 +2129,7 @@ int fwd_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride,
   g.Kpad = roundup(g.K, BK);
   g.nkb = g.Kpad / BK;
   g.M = N * g.Ho * g.Wo;
-  g.bn = Cout >= 128 ? 128 : roundup(Cout, 16);
+  g.bn = (Cout >= 256 && cdiv(g.M, BM) >= kSplitSms) ? 256 : (Cout >= 128 ? 128 : roundup(Cout, 16));
   g.tiles_m = cdiv(g.M, BM);
   g.tiles_n = cdiv(Cout, g.bn);
   g.rows = g.tiles_n * g.bn;
