@@ -1992,7 +1992,7 @@ int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.Ngemm = KH * KW * Cin;
   g.Kpad = roundup(static_cast<int>(g.M), BK);
   g.nkb = g.Kpad / BK;
-  g.bn = g.Ngemm >= 128 ? 128 : roundup(g.Ngemm, 16);
+  g.bn = g.Ngemm >= 256 ? 256 : (g.Ngemm >= 128 ? 128 : roundup(g.Ngemm, 16));   // 128x256 tiles: half the dy^T smem traffic per FLOP
   g.tiles_m = cdiv(Cout, BM);
   g.tiles_n = cdiv(g.Ngemm, g.bn);
   g.rows_a = g.tiles_m * BM;
