@@ -32,55 +32,66 @@ def _pad8(c: int) -> int:
     return (c + 7) // 8 * 8
 
 
+def plan_graph(graph):
+    """Host-side plan of a training graph: NHWC shape (H, W, C) of every
+    tensor (the input's C padded to 8) and the ReLUs fused into their
+    producer ({producer id: relu id}).  Raises NotImplementedError for
+    operator patterns the device path does not train."""
+    consumers: Dict[int, List[int]] = {}
+    for op in graph.ops:
+        for p in op["preds"]:
+            consumers.setdefault(p, []).append(op["id"])
+    ops = {op["id"]: op for op in graph.ops}
+    shape = {0: (graph.in_h, graph.in_w, _pad8(graph.in_c))}
+    fused: Dict[int, int] = {}
+    for op in graph.ops:
+        k, oid = op["kind"], op["id"]
+        h, w, c = shape[op["preds"][0]]
+        if k == "conv":
+            if op["groups"] != 1 or op.get("bias"):
+                raise NotImplementedError("grouped / biased conv training is not supported yet")
+            st = op["stride"]
+            shape[oid] = ((h + 2 * op["ph"] - op["kh"]) // st + 1, (w + 2 * op["pw"] - op["kw"]) // st + 1, op["c_out"])
+        elif k == "maxpool":
+            st = op["stride"]
+            shape[oid] = ((h + 2 * op["ph"] - op["kh"]) // st + 1, (w + 2 * op["pw"] - op["kw"]) // st + 1, c)
+        elif k == "gap":
+            shape[oid] = (1, 1, c)
+        elif k == "linear":
+            shape[oid] = (1, 1, op["c_out"])
+        elif k in ("bn", "flatten", "dropout", "relu", "add"):
+            shape[oid] = (h, w, c)
+        else:
+            raise NotImplementedError(f"training of {k!r}")
+        if k == "relu":
+            prod = op["preds"][0]
+            if ops.get(prod, {}).get("kind") not in ("bn", "add") or len(consumers[prod]) != 1:
+                raise NotImplementedError("a ReLU is trained fused into its BN or residual-add producer")
+            fused[prod] = oid
+    return shape, fused
+
+
 class SequentialTrainer:
     def __init__(self, graph, params, batch: int, lr: float = 0.1, momentum: float = 0.9):
         import torch
         self.torch = torch
         self.g, self.B, self.lr, self.mom = graph, batch, lr, momentum
-        self.ops = {op["id"]: op for op in graph.ops}
-        self.consumers: Dict[int, List[int]] = {}
-        for op in graph.ops:
-            for p in op["preds"]:
-                self.consumers.setdefault(p, []).append(op["id"])
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
-        # shapes (NHWC) and parameters
-        self.shape = {0: (graph.in_h, graph.in_w, _pad8(graph.in_c))}
+        self.shape, self.fused_relu = plan_graph(graph)
         self.params: Dict[int, Dict[str, object]] = {}
-        self.fused_relu: Dict[int, int] = {}      # producer id -> relu id
         for op in graph.ops:
             k, oid = op["kind"], op["id"]
-            h, w, c = self.shape[op["preds"][0]]
             if k == "conv":
-                if op["groups"] != 1 or op.get("bias"):
-                    raise NotImplementedError("grouped / biased conv training is not supported yet")
-                st = op["stride"]
-                ho, wo = (h + 2 * op["ph"] - op["kh"]) // st + 1, (w + 2 * op["pw"] - op["kw"]) // st + 1
+                c = self.shape[op["preds"][0]][2]
                 wt = np.zeros((op["c_out"], c, op["kh"], op["kw"]), np.float32)
-                wt[:, :op["c_in"]] = params[oid]["w"]
+                wt[:, :op["c_in"]] = params[oid]["w"]        # zero filter channels for the padded input
                 self.params[oid] = {"w": dev(wt)}
-                self.shape[oid] = (ho, wo, op["c_out"])
             elif k == "bn":
                 self.params[oid] = {"gamma": dev(params[oid]["gamma"]), "beta": dev(params[oid]["beta"])}
-                self.shape[oid] = (h, w, c)
-            elif k == "maxpool":
-                st = op["stride"]
-                self.shape[oid] = ((h + 2 * op["ph"] - op["kh"]) // st + 1, (w + 2 * op["pw"] - op["kw"]) // st + 1, c)
-            elif k == "gap":
-                self.shape[oid] = (1, 1, c)
-            elif k in ("flatten", "dropout", "relu", "add"):
-                self.shape[oid] = (h, w, c)
             elif k == "linear":
                 self.params[oid] = {"w": dev(params[oid]["w"])}
                 if "b" in params[oid]:
                     self.params[oid]["b"] = dev(params[oid]["b"])
-                self.shape[oid] = (1, 1, op["c_out"])
-            else:
-                raise NotImplementedError(f"training of {k!r}")
-            if k == "relu":
-                prod = op["preds"][0]
-                if self.ops[prod]["kind"] not in ("bn", "add") or len(self.consumers[prod]) != 1:
-                    raise NotImplementedError("a ReLU is trained fused into its BN or residual-add producer")
-                self.fused_relu[prod] = oid
         # one flat fp32 buffer each for the parameters, their gradients and
         # the momentum buffers: the SGD update is ONE launch over the whole
         # model, and the gradient all-reduce (A12) sees one contiguous buffer
