@@ -18,6 +18,10 @@
  * device-side cluster counters (no host stream events), producer->consumer
  * order by device-side dependency counters.
  *
+ * The training tenant's operators (conv forward / dgrad /
+ * wgrad on the same tcgen05 path, BN-train, pooling / FC backward,
+ * softmax-CE, SGD) are declared in gacer_train.h.
+ *
  * Conventions (all calls):
  *   - return value >= 0 on success (an id where documented), else a negative
  *     gacer_status; gacer_last_error() then holds a message.
