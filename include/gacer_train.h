@@ -57,8 +57,11 @@ int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float*
  *   dx = gamma_c / sqrt(var_c + eps) * (dy - dbeta_c / M - xhat * dgamma_c / M).
  * x: the BN input (bf16 [M][C]), dy: the gradient of the BN output (bf16),
  * mean/var from gacer_bn_train_fwd; outputs dx (bf16 [M][C], may alias dy),
- * dgamma, dbeta (fp32 [C]); scratch as for the forward. */
-int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, int64_t M, int32_t C,
+ * dgamma, dbeta (fp32 [C]); scratch as for the forward.  relu_y (may be
+ * NULL): the output of a ReLU fused behind this BN (gacer_bn_train_fwd with
+ * relu = 1); dy is then the gradient of that ReLU's output and is masked by
+ * relu_y > 0 first (the ReLU backward, oracle_relu_bwd, fused in). */
+int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, const void* relu_y_dev, int64_t M, int32_t C,
                            const float* gamma_dev, const float* mean_dev, const float* var_dev, float eps,
                            void* dx_dev, float* dgamma_dev, float* dbeta_dev, float* scratch_dev, void* stream);
 

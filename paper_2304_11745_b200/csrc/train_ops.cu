@@ -58,7 +58,8 @@ constexpr int kUnroll = 4;
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) bn_partial_kernel(const __nv_bfloat16* __restrict__ x,
-                                                              const __nv_bfloat16* __restrict__ dy, int64_t M, int C,
+                                                              const __nv_bfloat16* __restrict__ dy,
+                                                              const __nv_bfloat16* __restrict__ ym, int64_t M, int C,
                                                               const float* __restrict__ mean,
                                                               const float* __restrict__ var, float eps,
                                                               float* __restrict__ part) {
@@ -85,13 +86,15 @@ __global__ void __launch_bounds__(kThreads) bn_partial_kernel(const __nv_bfloat1
     }
     if (ph < RP && g < G8) {
       for (int64_t r = r0 + ph; r < r1; r += kUnroll * RP) {
-        uint4 va[kUnroll], vd[kUnroll];
+        uint4 va[kUnroll], vd[kUnroll], vm[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const int64_t rr = r + u * RP;
           va[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(x + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
-          if (MODE == 1)
+          if (MODE == 1) {
             vd[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(dy + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+            vm[u] = (ym && rr < r1) ? __ldcs(reinterpret_cast<const uint4*>(ym + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+          }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -107,6 +110,12 @@ __global__ void __launch_bounds__(kThreads) bn_partial_kernel(const __nv_bfloat1
           } else {
             float d[8];
             unpack8(vd[u], d);
+            if (ym) {                        // fused ReLU backward: the mask of the BN's ReLU output
+              float mk[8];
+              unpack8(vm[u], mk);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               s1[j] += d[j];
@@ -214,6 +223,7 @@ __global__ void bn_finalize_kernel(const float* __restrict__ part, int P, int64_
 // stay in registers.
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) bn_elementwise_kernel(const __nv_bfloat16* x, const __nv_bfloat16* dy,
+                                                                  const __nv_bfloat16* ym,
                                                                   int64_t M, int C, const float* __restrict__ coef,
                                                                   int relu, __nv_bfloat16* out) {
   const int G8 = C / 8;
@@ -249,6 +259,12 @@ __global__ void __launch_bounds__(kThreads) bn_elementwise_kernel(const __nv_bfl
     } else {
       float d[8];
       unpack8(__ldcs(reinterpret_cast<const uint4*>(dy) + i), d);
+      if (ym) {
+        float mk[8];
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(ym) + i), mk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[j] = fmaf(k0[j], d[j], fmaf(k1[j], a[j], k2[j]));
     }
@@ -788,30 +804,32 @@ int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float*
   const int P = num_partials(M);
   const auto* x = static_cast<const __nv_bfloat16*>(x_dev);
   float* coef = scratch_dev + static_cast<size_t>(P) * 2 * C;
-  bn_partial_kernel<0><<<P, kThreads, 0, s>>>(x, nullptr, M, C, nullptr, nullptr, 0.0f, scratch_dev);
+  bn_partial_kernel<0><<<P, kThreads, 0, s>>>(x, nullptr, nullptr, M, C, nullptr, nullptr, 0.0f, scratch_dev);
   bn_finalize_kernel<0><<<(C + 31) / 32, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, beta_dev, nullptr, nullptr,
                                                        eps, mean_dev, var_dev, coef);
-  bn_elementwise_kernel<0><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, nullptr, M, C, coef, relu,
+  bn_elementwise_kernel<0><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, nullptr, nullptr, M, C, coef, relu,
                                                                       static_cast<__nv_bfloat16*>(y_dev));
   return launched("bn_train_fwd");
 }
 
-int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, int64_t M, int32_t C, const float* gamma_dev,
-                           const float* mean_dev, const float* var_dev, float eps, void* dx_dev, float* dgamma_dev,
-                           float* dbeta_dev, float* scratch_dev, void* stream) {
+int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, const void* relu_y_dev, int64_t M, int32_t C,
+                           const float* gamma_dev, const float* mean_dev, const float* var_dev, float eps, void* dx_dev,
+                           float* dgamma_dev, float* dbeta_dev, float* scratch_dev, void* stream) {
   if (M < 1 || C < 8 || C % 8) return bad(GACER_E_SHAPE, "bn_train_bwd: need M >= 1 and C % 8 == 0");
   if (!x_dev || !dy_dev || !dx_dev || !gamma_dev || !mean_dev || !var_dev || !dgamma_dev || !dbeta_dev ||
-      !scratch_dev || !aligned16(x_dev) || !aligned16(dy_dev) || !aligned16(dx_dev))
+      !scratch_dev || !aligned16(x_dev) || !aligned16(dy_dev) || !aligned16(dx_dev) ||
+      (relu_y_dev && !aligned16(relu_y_dev)))
     return bad(GACER_E_INVALID_ARG, "bn_train_bwd: null or misaligned pointer");
+  const auto* ym = static_cast<const __nv_bfloat16*>(relu_y_dev);
   auto s = static_cast<cudaStream_t>(stream);
   const int P = num_partials(M);
   const auto* x = static_cast<const __nv_bfloat16*>(x_dev);
   const auto* dy = static_cast<const __nv_bfloat16*>(dy_dev);
   float* coef = scratch_dev + static_cast<size_t>(P) * 2 * C;
-  bn_partial_kernel<1><<<P, kThreads, 0, s>>>(x, dy, M, C, mean_dev, var_dev, eps, scratch_dev);
+  bn_partial_kernel<1><<<P, kThreads, 0, s>>>(x, dy, ym, M, C, mean_dev, var_dev, eps, scratch_dev);
   bn_finalize_kernel<1><<<(C + 31) / 32, 256, 0, s>>>(scratch_dev, P, M, C, gamma_dev, nullptr, mean_dev, var_dev,
                                                        eps, dgamma_dev, dbeta_dev, coef);
-  bn_elementwise_kernel<1><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, dy, M, C, coef, 0,
+  bn_elementwise_kernel<1><<<grid_for(M * (C / 8)), kThreads, 0, s>>>(x, dy, ym, M, C, coef, 0,
                                                                       static_cast<__nv_bfloat16*>(dx_dev));
   return launched("bn_train_bwd");
 }

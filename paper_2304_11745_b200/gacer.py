@@ -111,8 +111,9 @@ EXPORTS = {
     "gacer_bn_partials": ([C.c_int64, C.c_int32], C.c_int32),
     "gacer_bn_train_fwd": ([C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_float, C.c_int32,
                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
-    "gacer_bn_train_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
-                            C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int32),
+    "gacer_bn_train_bwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                            C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+                           C.c_int32),
     "gacer_relu_bwd": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p], C.c_int32),
     "gacer_maxpool_bwd": ([C.c_void_p, C.c_void_p] + [C.c_int32] * 11 + [C.c_void_p, C.c_void_p, C.c_void_p],
                           C.c_int32),
@@ -361,8 +362,8 @@ def bn_train_fwd(x, M, C_, gamma, beta, eps, relu, y, mean, var, scratch, stream
     return _call("gacer_bn_train_fwd", x, M, C_, gamma, beta, eps, relu, y, mean, var, scratch, stream)
 
 
-def bn_train_bwd(x, dy, M, C_, gamma, mean, var, eps, dx, dgamma, dbeta, scratch, stream=0):
-    return _call("gacer_bn_train_bwd", x, dy, M, C_, gamma, mean, var, eps, dx, dgamma, dbeta, scratch, stream)
+def bn_train_bwd(x, dy, M, C_, gamma, mean, var, eps, dx, dgamma, dbeta, scratch, stream=0, relu_y=None):
+    return _call("gacer_bn_train_bwd", x, dy, relu_y, M, C_, gamma, mean, var, eps, dx, dgamma, dbeta, scratch, stream)
 
 
 def relu_bwd(x, dy, n, six, dx, stream=0):

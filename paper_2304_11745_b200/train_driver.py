@@ -78,6 +78,7 @@ class SequentialTrainer:
         self.g, self.B, self.lr, self.mom = graph, batch, lr, momentum
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
         self.shape, self.fused_relu = plan_graph(graph)
+        self.kind = {op["id"]: op["kind"] for op in graph.ops}
         self.params: Dict[int, Dict[str, object]] = {}
         for op in graph.ops:
             k, oid = op["kind"], op["id"]
@@ -185,6 +186,7 @@ class SequentialTrainer:
         G.softmax_ce(P(logits), P(labels), B, ncls, P(loss), P(dz), P(f32(B)))
         # ---------------------------------------------------------- backward
         grads: Dict[int, Dict[str, object]] = {}
+        relu_mask: Dict[int, object] = {}
         dval = {self.g.ops[-1]["id"]: dz}
 
         def acc(tid, g):
@@ -218,7 +220,10 @@ class SequentialTrainer:
                 G.gap_bwd(P(dy), B, h * w, c, P(dx))
                 acc(pred, dx)
             elif k == "relu":
-                G.relu_bwd(P(out[oid]), P(dy), dy.numel(), 0, P(dy))
+                if self.kind[pred] == "bn":
+                    relu_mask[pred] = out[oid]        # applied inside the BN backward (fused)
+                else:
+                    G.relu_bwd(P(out[oid]), P(dy), dy.numel(), 0, P(dy))
                 acc(pred, dy)
             elif k == "add":
                 acc(op["preds"][0], dy)
@@ -227,8 +232,10 @@ class SequentialTrainer:
                 dx = bf((B, h, w, c))
                 gg, gb = self.gview[oid]["gamma"], self.gview[oid]["beta"]
                 mean, var = saved[oid]
+                ym = relu_mask.pop(oid, None)
                 G.bn_train_bwd(P(out[pred]), P(dy), B * h * w, c, P(self.params[oid]["gamma"]), P(mean), P(var),
-                               op["eps"], P(dx), P(gg), P(gb), P(self.bn_scratch))
+                               op["eps"], P(dx), P(gg), P(gb), P(self.bn_scratch),
+                               relu_y=P(ym) if ym is not None else None)
                 grads[oid] = {"gamma": gg, "beta": gb}
                 acc(pred, dx)
             elif k == "maxpool":

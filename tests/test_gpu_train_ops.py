@@ -67,6 +67,19 @@ def test_bn_train_fwd_bwd(T, N, H, W, C):
     assert maxrel(dg.cpu().numpy(), dgo) < 1e-4
     assert maxrel(db.cpu().numpy(), dbo) < 1e-4
     assert maxrel(_nchw(_np(dx), N, H, W, C), dxo) <= 2e-2
+    # the ReLU backward fused into the BN backward (mask = ReLU output > 0)
+    yr = torch.empty_like(x)
+    G.bn_train_fwd(x.data_ptr(), M, C, gamma.data_ptr(), beta.data_ptr(), 1e-5, 1, yr.data_ptr(),
+                   mean.data_ptr(), var.data_ptr(), scratch.data_ptr())
+    dxm = torch.empty_like(x)
+    G.bn_train_bwd(x.data_ptr(), dy.data_ptr(), M, C, gamma.data_ptr(), mean.data_ptr(), var.data_ptr(), 1e-5,
+                   dxm.data_ptr(), dg.data_ptr(), db.data_ptr(), scratch.data_ptr(), relu_y=yr.data_ptr())
+    torch.cuda.synchronize()
+    dym = OT.relu_bwd(_nchw(_np(yr), N, H, W, C), _nchw(_np(dy), N, H, W, C))
+    dxo2, dgo2, _ = OT.bn_train_bwd(xn, dym, gamma.cpu().numpy(), mean.cpu().numpy().astype(np.float64),
+                                    var.cpu().numpy().astype(np.float64), 1e-5)
+    assert maxrel(dg.cpu().numpy(), dgo2) < 1e-4
+    assert maxrel(_nchw(_np(dxm), N, H, W, C), dxo2) <= 2e-2
     # deterministic: a second backward is bitwise identical
     dx2 = torch.empty_like(dx)
     G.bn_train_bwd(x.data_ptr(), dy.data_ptr(), M, C, gamma.data_ptr(), mean.data_ptr(), var.data_ptr(), 1e-5,
