@@ -189,11 +189,16 @@ class SequentialTrainer:
         relu_mask: Dict[int, object] = {}
         dval = {self.g.ops[-1]["id"]: dz}
 
+        shared = set()        # gradient tensors held by two dval entries (a residual add): copy on write
+
         def acc(tid, g):
             if tid == 0:
                 return
             if tid in dval:
-                G.add(P(dval[tid]), P(g), g.numel(), 0, P(dval[tid]))
+                cur = dval[tid]
+                dst = cur if id(cur) not in shared else torch.empty_like(cur)
+                G.add(P(cur), P(g), g.numel(), 0, P(dst))
+                dval[tid] = dst
             else:
                 dval[tid] = g
 
@@ -223,11 +228,14 @@ class SequentialTrainer:
                 if self.kind[pred] == "bn":
                     relu_mask[pred] = out[oid]        # applied inside the BN backward (fused)
                 else:
-                    G.relu_bwd(P(out[oid]), P(dy), dy.numel(), 0, P(dy))
+                    dst = dy if id(dy) not in shared else torch.empty_like(dy)
+                    G.relu_bwd(P(out[oid]), P(dy), dy.numel(), 0, P(dst))
+                    dy = dst
                 acc(pred, dy)
             elif k == "add":
+                shared.add(id(dy))                # both inputs receive dy itself (no copy)
                 acc(op["preds"][0], dy)
-                acc(op["preds"][1], dy.clone())
+                acc(op["preds"][1], dy)
             elif k == "bn":
                 dx = bf((B, h, w, c))
                 gg, gb = self.gview[oid]["gamma"], self.gview[oid]["beta"]
