@@ -195,6 +195,12 @@ typedef struct {
   int64_t in_bytes;           /* bytes of the input buffer: batch*in_h*in_w*in_c_pad*elem */
   int64_t out_bytes;          /* batch*out_features*4 */
   double flops;               /* algorithmic FLOPs of one forward */
+  int32_t gemm_ops;           /* fused ops on the tcgen05 GEMM tile path */
+  int32_t mpair_ops;          /* ... of them with 256-row (M-pair) tiles */
+  int32_t split_k_ops;        /* ... of them with a fixed split-K > 1 */
+  int32_t swap_ops;           /* ... of them swap-AB linears (weights = the M operand) */
+  int32_t wide_ops;           /* ... of them with 128x256 tiles */
+  int32_t cc_ops;             /* fused ops on CUDA cores (depthwise, pools, GAP, eltwise, SIMT) */
 } gacer_tenant_info;
 
 /* ------------------------------------------------------------------ calls */

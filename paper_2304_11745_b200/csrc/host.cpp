@@ -1348,6 +1348,11 @@ int upload_plan() {
 
 int reset_device_counters() {
   const Plan& P = S.plan;
+  // rounds may still be in flight on any stream (gacer_run_round_async takes
+  // the caller's non-blocking stream): drain the device before zeroing the
+  // counters they are using (rare: once per ~2^31 / items rounds, and after a
+  // watchdog abort)
+  CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemset(S.d_heads, 0, S.tenants.size() * P.n_clusters * sizeof(uint32_t)));
   CUDA_TRY(cudaMemset(S.d_chunk_done, 0, std::max(1, P.n_chunk_counters) * sizeof(uint32_t)));
   CUDA_TRY(cudaMemset(S.d_cluster_done, 0, P.n_clusters * sizeof(uint32_t)));
@@ -1610,6 +1615,15 @@ int gacer_get_tenant_info(int tenant, gacer_tenant_info* out) {
   out->in_bytes = static_cast<int64_t>(T.batch) * T.in_h * T.in_w * T.in_c_pad * elem_size(T);
   out->out_bytes = static_cast<int64_t>(T.batch) * T.out_features * 4;
   out->flops = T.flops;
+  out->gemm_ops = out->mpair_ops = out->split_k_ops = out->swap_ops = out->wide_ops = out->cc_ops = 0;
+  for (const FusedOp& F : T.fops) {
+    if (F.kind != DK_GEMM) { ++out->cc_ops; continue; }
+    ++out->gemm_ops;
+    out->mpair_ops += F.mrep > 1;
+    out->split_k_ops += F.split_k > 1;
+    out->swap_ops += F.swap;
+    out->wide_ops += F.bn > 128;
+  }
   return GACER_OK;
 }
 

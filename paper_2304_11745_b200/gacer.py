@@ -86,7 +86,9 @@ class gacer_tenant_info(C.Structure):
     _fields_ = [("n_orig_ops", C.c_int32), ("n_fused_ops", C.c_int32), ("batch", C.c_int32),
                 ("in_c_pad", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32),
                 ("out_features", C.c_int32), ("in_bytes", C.c_int64), ("out_bytes", C.c_int64),
-                ("flops", C.c_double)]
+                ("flops", C.c_double), ("gemm_ops", C.c_int32), ("mpair_ops", C.c_int32),
+                ("split_k_ops", C.c_int32), ("swap_ops", C.c_int32), ("wide_ops", C.c_int32),
+                ("cc_ops", C.c_int32)]
 
 
 EXPORTS = {

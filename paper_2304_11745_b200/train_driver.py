@@ -58,6 +58,11 @@ def plan_graph(graph):
         elif k == "gap":
             shape[oid] = (1, 1, c)
         elif k == "linear":
+            # the trainer's FC reads a [B][C] activation (a GAP output): a
+            # flatten -> linear head over a spatial tensor would need the
+            # NCHW-flatten weight order, which it does not implement
+            if (h, w) != (1, 1) or c != op["c_in"]:
+                raise NotImplementedError("linear training needs a [B][c_in] (1x1 spatial) input")
             shape[oid] = (1, 1, op["c_out"])
         elif k in ("bn", "flatten", "dropout", "relu", "add"):
             shape[oid] = (h, w, c)
@@ -129,11 +134,21 @@ class SequentialTrainer:
         self.argmax = torch.empty(maxmc, dtype=torch.uint8, device="cuda")
 
     # ---------------------------------------------------------------- step
-    def step(self, x_nhwc8, labels):
+    def step(self, x_nhwc8, labels, grads_hook=None):
         """One SGD step: x_nhwc8 bf16 [B][H][W][pad8(C)] and labels int32 [B]
         on the device.  Returns the loss (a 1-element fp32 device tensor) and
-        the parameter gradients {op_id: {name: tensor}}."""
+        the parameter gradients {op_id: {name: tensor}}.
+
+        grads_hook(flat_g), if given, runs after the backward pass and BEFORE
+        the SGD update (e.g. the data-parallel gradient mean of A12,
+        GradBuckets.reduce_mean); it must leave flat_g ready on the legacy
+        default stream the libgacer calls use.  The library calls run on that
+        stream; it is ordered after the caller's current stream on entry and
+        the current stream after it on return."""
         torch, B, P = self.torch, self.B, (lambda t: t.data_ptr())
+        cur, dflt = torch.cuda.current_stream(), torch.cuda.default_stream()
+        if cur != dflt:
+            dflt.wait_stream(cur)
         bf = lambda shape: torch.empty(shape, dtype=torch.bfloat16, device="cuda")
         f32 = lambda *shape: torch.empty(shape, device="cuda")
         out = {0: x_nhwc8}
@@ -263,7 +278,12 @@ class SequentialTrainer:
         # ---------------------------------------------------------- SGD
         # (every parameter has a gradient: a ResNet's whole parameter set is
         #  written by the backward pass above, so one launch updates it all)
+        if grads_hook is not None:
+            with torch.cuda.stream(dflt):
+                grads_hook(self.flat_g)
         G.sgd_momentum(P(self.flat_p), P(self.flat_g), P(self.flat_m), self.flat_p.numel(), self.lr, self.mom,
                        int(self.first))
         self.first = False
+        if cur != dflt:
+            cur.wait_stream(dflt)
         return loss, grads

@@ -191,3 +191,24 @@ def test_partition_modes_validated():
             assert G.lib().gacer_set_partition(bad) == -1
     finally:
         G.gacer_shutdown()
+
+
+def test_tile_path_counts(host):
+    """The per-op RNE gates of test_gpu_parity.py target specific tile
+    paths; the lowering must route those shapes there: VGG-16's FC1 is a
+    swap-AB linear with a fixed split-K, and the D2 mix carries M-pair
+    (256-row) and 128x256 tiles."""
+    g = workloads.Graph("fc_op", 512, 7, 7)
+    g.linear(g.flatten(0), 512 * 49, 4096)
+    t = register(g, 8)
+    info = G.gacer_get_tenant_info(t)
+    assert info["swap_ops"] == 1 and info["split_k_ops"] == 1 and info["gemm_ops"] == 1
+    G.gacer_shutdown()
+    G.gacer_init(-1)
+    for cin, cout in ((64, 64), (32, 96), (64, 128)):
+        g = workloads.Graph("mpair", cin, 112, 112)
+        g.relu(g.bn(g.conv(0, cin, cout, 3, 1, 1), cout))
+        info = G.gacer_get_tenant_info(register(g, 8))
+        assert info["mpair_ops"] == 1, (cin, cout, info)
+    v = G.gacer_get_tenant_info(register(workloads.build_model("vgg16"), 8))
+    assert v["mpair_ops"] >= 1 and v["wide_ops"] >= 1 and v["swap_ops"] == 3

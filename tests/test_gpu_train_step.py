@@ -190,7 +190,7 @@ def test_nccl_gradient_mean_on_comm_stream():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,hw,B", [("resnet50", 128, 8), ("resnet18", 64, 8)])
+@pytest.mark.parametrize("name,hw,B", [("resnet50", 224, 16), ("resnet18", 64, 8)])
 def test_sequential_trainer_resnet_step(name, hw, B):
     """The whole ResNet training step driven by train_driver.SequentialTrainer
     (every step a libgacer.so call) vs the oracle's fp64 step: loss and FC
@@ -224,12 +224,12 @@ def test_sequential_trainer_resnet_step(name, hw, B):
         G.gacer_shutdown()
     print(name, l1, loss_o, maxrel(gw, grads_o[fc]["w"]), l2)
     assert abs(l1 - loss_o) / abs(loss_o) <= 2e-2
-    # FC gradient: 2e-2 (C2b reading (3)); ResNet-50's is looser, 3e-2: its
-    # error vs the fp64 forward is the bf16-activation conditioning of deep
-    # small-batch BN and falls with the BN sample count (measured 0.145 at
-    # 32^2, 0.041 at 64^2, 0.022 at 128^2, B=8), while every operator is
-    # within 2e-2 on the device's own tensors (test_gpu_train_ops.py)
-    assert maxrel(gw, grads_o[fc]["w"]) <= (3e-2 if name == "resnet50" else 2e-2)
+    # FC gradient: 2e-2 (SURVEY §8(c) C2b reading (3)).  ResNet-50 runs at
+    # 224^2, B=16, the configuration C2b measured (FC gradient ~1e-2 with
+    # bf16 stores): its error vs the fp64 forward is the bf16-activation
+    # conditioning of deep BN nets and grows as the BN sample count shrinks
+    # (C2b), so small-image cases do not test the kernels
+    assert maxrel(gw, grads_o[fc]["w"]) <= 2e-2
     assert l2 < l1
 
 

@@ -30,3 +30,8 @@ def test_unsupported_patterns_raise():
     g.relu(c)                                                  # ReLU straight after a conv: not fusable
     with pytest.raises(NotImplementedError):
         plan_graph(g)
+    g = workloads.Graph("flat_head", 16, 4, 4)
+    c = g.bn(g.conv(0, 16, 16, 3, 1, 1), 16)
+    g.linear(g.flatten(g.relu(c)), 16 * 16, 10)               # flatten -> linear over a 4x4 map
+    with pytest.raises(NotImplementedError):
+        plan_graph(g)
