@@ -220,15 +220,23 @@ def run_reference(args, rank):
 
 
 def time_mode(G, s, torch, stream, mode, steps, warmup, flush):
-    s.set_mode(mode)
+    """Per-round device times (CUDA events on `stream`, L2 flushed before
+    every round outside the events).  mode "<baseline>_graph" replays the
+    baseline round captured as a CUDA graph (gacer_capture_baseline)."""
+    if mode.endswith("_graph"):
+        G.gacer_capture_baseline(mode[:-len("_graph")])
+        run = lambda: G.gacer_run_baseline_graph(stream.cuda_stream)
+    else:
+        s.set_mode(mode)
+        run = lambda: G.gacer_run_round_async(stream.cuda_stream)
     for _ in range(warmup):
-        G.gacer_run_round_async(stream.cuda_stream)
+        run()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for a, b in evs:
         flush.zero_()
         a.record(stream)
-        G.gacer_run_round_async(stream.cuda_stream)
+        run()
         b.record(stream)
     torch.cuda.synchronize()
     return [a.elapsed_time(b) for a, b in evs]
@@ -325,7 +333,7 @@ def run_gacer(args, rank, world, dist):
 
     # ---- same-kernel baselines (makespan per round), same timing protocol
     base = {}
-    for mode in ("sequential", "multistream"):
+    for mode in ("sequential", "multistream", "sequential_graph", "multistream_graph"):
         tm = time_mode(G, sess, torch, stream, mode, args.steps, args.warmup, flush)
         m = max_over_ranks(float(np.mean(tm)), dist, f"cuda:{dev}")
         base[mode] = {"ms_per_round": m, "inferences_per_s": world * n_inf / (m / 1000.0),
@@ -387,6 +395,8 @@ def run_gacer(args, rank, world, dist):
             "baselines": base,
             "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
             "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,
+            "speedup_vs_sequential_graph": base["sequential_graph"]["ms_per_round"] / ms_step,
+            "speedup_vs_multistream_graph": base["multistream_graph"]["ms_per_round"] / ms_step,
             "makespan_ms": {"p10": float(np.percentile(times, 10)), "p50": float(np.median(times)),
                             "p90": float(np.percentile(times, 90))},
         }

@@ -107,7 +107,17 @@ typedef struct {
   const gacer_op_desc* ops;
   int32_t in_c, in_h, in_w;   /* per-sample input shape (C, H, W) */
   int32_t dtype;              /* gacer_dtype of activations/weights on the GPU */
-  int32_t train;              /* must be 0 in this version (training tenants: not built yet) */
+  int32_t train;              /* 1: a TRAINING tenant (the
+                                 techniques "are applicable to both the training and inference
+                                 phases").  Its round is one SGD step: BN in training mode
+                                 (per-batch statistics), mean softmax cross-entropy over the
+                                 labels (gacer_bind_labels), backward, SGD with momentum
+                                 (lr, momentum; PyTorch semantics).  dtype must be BF16; the
+                                 graph is a ResNet-style DFG (conv without bias, BN, ReLU fused
+                                 into its BN / residual-add producer, add, max-pool, GAP,
+                                 flatten, a final LINEAR producing the logits); other patterns
+                                 return GACER_E_UNSUPPORTED_OP.  Pointers index its step
+                                 (gacer_sync_pointers); it takes no decomposition. */
   float lr, momentum;
 } gacer_graph;
 
@@ -174,6 +184,8 @@ typedef struct {
                                  are bit-identical either way. */
 } gacer_options;
 
+#define GACER_MAX_STAT_TENANTS 16   /* tenants with per-tenant occupancy counters */
+
 typedef struct {
   double last_round_ms;       /* device time of the last round (CUDA events) */
   int64_t n_items;            /* work items per round under the current plan */
@@ -183,6 +195,17 @@ typedef struct {
   int32_t n_tenants;
   double tensor_flops;        /* algorithmic conv+FC FLOPs per round (2*MAC) */
   double cc_bytes;            /* algorithmic bytes of the CUDA-core ops per round */
+  /* Executor occupancy (the Fig. 8 analog, §5.3 l.979-981), from
+   * device counters every executor round accumulates; averaged over the
+   * executor rounds since the previous gacer_get_stats call (0 if none): */
+  int32_t stat_rounds;        /* executor rounds the figures below average over */
+  int32_t pad0;
+  double tenant_sm_ns[GACER_MAX_STAT_TENANTS]; /* per tenant: sum over its items of (release - claim)
+                                 time on its CTA (SM-ns; items pipelined inside one CTA overlap) */
+  double barrier_wait_ns;     /* sum over CTAs of the time spent waiting at sync pointers
+                                 (cluster barriers, A5) -- the device T_SW (CTA-ns) */
+  double ready_wait_ns;       /* sum over CTAs of the time spent with unclaimed but unready work
+                                 (dependency stalls; CTA-ns) */
 } gacer_round_stats;
 
 typedef struct {
@@ -201,7 +224,25 @@ typedef struct {
   int32_t swap_ops;           /* ... of them swap-AB linears (weights = the M operand) */
   int32_t wide_ops;           /* ... of them with 128x256 tiles */
   int32_t cc_ops;             /* fused ops on CUDA cores (depthwise, pools, GAP, eltwise, SIMT) */
+  int32_t train;              /* 1: a training tenant (its round is one SGD step) */
+  int32_t n_steps;            /* training: 2 n_orig_ops + 1 step positions (pointer range) */
+  int64_t n_params;           /* training: floats in the flat parameter buffer */
 } gacer_tenant_info;
+
+/* Device buffers of a training tenant (library-owned; valid until
+ * gacer_shutdown).  Flat fp32 parameter / gradient / momentum buffers in
+ * registration order: CONV2D weight [c_out][c_in padded to 8][kh][kw], BN
+ * gamma then beta, LINEAR weight [c_out][c_in] then bias (gacer_train_param
+ * gives each slice). */
+typedef struct {
+  const float* loss;          /* 1 float: the step's mean softmax cross-entropy */
+  float* params;              /* master weights, updated in place by each round's SGD step */
+  const float* grads;         /* gradients of the last step */
+  float* momentum;            /* SGD momentum buffers (zero before the first step) */
+  int64_t n_params;
+  int32_t n_ops;              /* executor ops of one step */
+  int32_t pad;
+} gacer_train_state;
 
 /* ------------------------------------------------------------------ calls */
 
@@ -228,6 +269,16 @@ int gacer_get_tenant_info(int tenant, gacer_tenant_info* out);
  * (logits [B][classes] for a 1x1 output).  Both 16-byte aligned; both must
  * outlive every round that uses them. */
 int gacer_bind_io(int tenant, const void* input_dev, void* output_dev);
+
+/* Training tenants: bind the int32 [B] labels (device, 4-byte aligned; must
+ * outlive the rounds using it); the graph input is bound with gacer_bind_io
+ * (NHWC bf16 images) together with the float32 [B][classes] logits buffer. */
+int gacer_bind_labels(int tenant, const void* labels_dev);
+int gacer_get_train_state(int tenant, gacer_train_state* out);
+/* Offset and length (floats) of parameter `which` (0: conv/linear weight or
+ * BN gamma; 1: linear bias or BN beta) of ORIGINAL op op_index (1-based) in
+ * the flat buffers. */
+int gacer_train_param(int tenant, int32_t op_index, int32_t which, int64_t* offset, int64_t* count);
 
 /* Install a regulation plan (mask/list_B/list_C and Matrix_P).  Either
  * argument may be NULL (no decomposition / no pointers).  Atomic: on error
@@ -262,6 +313,21 @@ int gacer_set_mode(int mode);               /* gacer_mode */
  * library stream) and returns. */
 int gacer_run_round(void);
 int gacer_run_round_async(void* stream);
+
+/* The baselines as CUDA graphs (sequential and multi-stream
+ * "reported plain and with CUDA Graphs"; the paper's Stream-Parallel
+ * comparator, §5.1 l.925).  gacer_capture_baseline(mode), mode =
+ * GACER_MODE_SEQUENTIAL or GACER_MODE_MULTISTREAM, captures ONE round of that
+ * mode's per-op launches (the same tile functions, order and stream topology
+ * as gacer_run_round in that mode) into a library-owned CUDA graph, replacing
+ * any previous capture; the current mode is left unchanged.  Needs bound I/O.
+ * gacer_run_baseline_graph(stream) replays it on `stream` (NULL = the
+ * library stream); gacer_get_stats().kernel_launches then reports the
+ * captured round's kernel count.  Re-registration or re-binding I/O discards
+ * the capture (GACER_E_STATE until captured again).  Outputs are
+ * byte-identical to the executor's. */
+int gacer_capture_baseline(int mode);
+int gacer_run_baseline_graph(void* stream);
 
 /* End-to-end round with HOST buffers: copies host_inputs[t] (layout as
  * gacer_bind_io, pinned memory recommended) to the bound device inputs, runs

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgacer.so")
 SOURCES = ["host.cpp", "executor.cu", "train_ops.cu"]
-DEPS = SOURCES + ["gacer_dev.h"]
+DEPS = SOURCES + ["gacer_dev.h", "train_dev.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Wno-deprecated-gpu-targets"]
 

@@ -27,6 +27,7 @@
 #include <stdint.h>
 
 #include "gacer_dev.h"
+#include "train_dev.cuh"
 
 namespace gacer {
 
@@ -125,6 +126,10 @@ __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_pin16(uint32_t (&r)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(r[i]));
+}
 // keep the uses of r after the preceding tcgen05.wait::ld (the registers are
 // written asynchronously; the empty asm orders every use after the wait)
 __device__ __forceinline__ void tmem_pin32(uint32_t* r) {
@@ -158,29 +163,42 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Diagnostics probes (GACER_DEBUG_TIMING=1 at run time) are compiled in only
+// with -DGACER_DIAG=1: they hold registers across the role loops.
+#ifndef GACER_DIAG
+#define GACER_DIAG 0
+#endif
 __shared__ uint32_t g_dbg_seen;   // per-CTA: milestones already recorded (no global load per probe)
 __device__ __forceinline__ void dbg_mark(const ExecParams& p, int ev) {
+#if GACER_DIAG
   if (p.dbg && !(g_dbg_seen & (1u << ev))) {   // first occurrence only
     atomicOr(&g_dbg_seen, 1u << ev);
     p.dbg[static_cast<size_t>(blockIdx.x) * DBG_EVENTS + ev] = static_cast<int64_t>(globaltimer());
   }
+#endif
 }
 
 // per-k-block timeline of CTA 0 (GACER_DEBUG_TIMING): [0,256) MMA saw stage
 // full, [256,512) producer issued the stage, [512,768) epilogue (tfull, done)
 constexpr size_t KDBG_OFF = static_cast<size_t>(400) * 148 * DBG_EVENTS;
 __device__ __forceinline__ void kdbg(const ExecParams& p, int slot, uint32_t i) {
+#if GACER_DIAG
   if (p.dbg && blockIdx.x == 0 && i < 256) p.dbg[KDBG_OFF + slot * 256 + i] = static_cast<int64_t>(globaltimer());
+#endif
 }
 
 // scheduler stamps of CTA 0's first 24 claims (GACER_DEBUG_TIMING): globaltimer
 __device__ __forceinline__ void sdbg(const ExecParams& p, uint32_t n, int j, int64_t v) {
+#if GACER_DIAG
   if (p.dbg && blockIdx.x == 0 && n < 24) p.dbg[KDBG_OFF + 1024 + n * 8 + j] = v;
+#endif
 }
 
 // epilogue clock64 stamps of CTA 0's first 8 GEMM items (GACER_DEBUG_TIMING)
 __device__ __forceinline__ void edbg(const ExecParams& p, int point, uint32_t acc) {
+#if GACER_DIAG
   if (p.dbg && blockIdx.x == 0 && acc < 8) p.dbg[KDBG_OFF + 768 + acc * 16 + point] = static_cast<int64_t>(clock64());
+#endif
 }
 
 // gpu-scope fences.  __threadfence() is fence.sc.gpu: MEMBAR.SC.GPU plus an
@@ -312,6 +330,7 @@ struct SmemCtl {
   int32_t epi_flag;
   int32_t n_segs_smem;
   int32_t pad;
+  unsigned long long st_ns[STAT_TENANTS + 2];   // this CTA's occupancy counters (flushed at exit)
   __align__(16) float red[CC_THREADS * 8]; // GAP fixed-order reduction scratch / dw weights (float4 reads)
   float epi_scale[BN_MAX];   // epilogue: folded BN scale / bias of the tile's columns
   float epi_bias[BN_MAX];
@@ -1124,7 +1143,9 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
   // the release fence makes them visible at gpu scope before the counters.
   // The trace's end stamp is taken BEFORE the counters publish the item, so a
   // dependent item's claim stamp is never earlier than it.
-  const uint64_t t_end = p.trace ? globaltimer() : 0;
+  const uint64_t t_end = (p.trace || p.stats) ? globaltimer() : 0;
+  if (p.stats && op.tenant < STAT_TENANTS)
+    atomicAdd(&g_ctl.st_ns[op.tenant], static_cast<unsigned long long>(t_end - t0));
   fence_release_gpu();
   dbg_mark(p, 8);
   atomicAdd(p.chunk_done + it.chunk, 1u);
@@ -1204,14 +1225,18 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         if (st == 2) {
           // every item of cluster k is claimed: the synchronisation pointer --
           // wait until every item of cluster k (all tenants) is done.
+          const uint64_t tb = p.stats ? globaltimer() : 0;
           if (!spin_ge(p.cluster_done + k, p.epoch * p.cluster_total[k], p)) { claimed = -3; break; }
+          if (p.stats && k < p.k_last) ctl->st_ns[STAT_TENANTS] += globaltimer() - tb;
           dbg_mark(p, 10);
           ++k;
           spins = 0;
           continue;
         }
         if (st == 0) {  // unclaimed work exists but none of it is ready: back off, rescan
+          const uint64_t tw = p.stats ? globaltimer() : 0;
           __nanosleep(spins < 4 ? 64u : (spins < 8 ? 256u : 512u));
+          if (p.stats) ctl->st_ns[STAT_TENANTS + 1] += globaltimer() - tw;
           if (spins++ == 0) t0 = globaltimer();
           if ((spins & 31) == 0) {
             if (*reinterpret_cast<volatile int32_t*>(p.error)) { claimed = -3; break; }
@@ -1268,7 +1293,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
       if (n_claimed > 0) rs.it = its[j];
       rs.idx = n_claimed > 0 ? idxs[j] : -1;
       rs.kind = n_claimed > 0 ? its[j].kind : 0;
-      rs.t0 = p.trace ? globaltimer() : 0;
+      rs.t0 = (p.trace || p.stats) ? globaltimer() : 0;
       mbar_arrive(&ctl->rfull[slot]);
       ++islot;
     }
@@ -1276,6 +1301,15 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   }
 }
 
+// A training-tenant operator's item: virtual blocks [mt * bm, ...) of its
+// grid on the worker group.  Not inlined: the operators' register needs stay
+// out of the worker loop's allocation (the GEMM producer path shares it).
+__device__ __noinline__ void vgrid_item(const OpDev& op, int mt, int wtid, uint8_t* smem) {
+  const int v0 = mt * op.bm, v1 = min(v0 + op.bm, op.vblocks);
+  for (int vb = v0; vb < v1; ++vb) run_vgrid(op.vfn, op.va, vb, op.vblocks, wtid, NWORK, smem);
+}
+
+template <bool TRAIN>
 __device__ void worker_role(const ExecParams& p, Ctx& cx) {
   SmemCtl* ctl = &g_ctl;
   const int wtid = threadIdx.x - WORK_WARP0 * 32;  // 0..NWORK-1
@@ -1310,13 +1344,18 @@ __device__ void worker_role(const ExecParams& p, Ctx& cx) {
     } else {
       if (wtid == 0 && p.trace && p.single_op < 0)
         p.trace[static_cast<size_t>(rs.it.idx) * TRACE_FIELDS + 8] = static_cast<int64_t>(globaltimer());
-      if (op.win) {
-        // the staged window op borrows the GEMM smem ring: wait until the MMA
-        // has consumed every stage produced so far (MMAs complete in order)
+      if (op.win || op.kind == DK_VGRID) {
+        // the staged window op / virtual-grid op borrows the GEMM smem ring:
+        // wait until the MMA has consumed every stage produced so far (MMAs
+        // complete in order)
         if (g > 0) mbar_wait(&ctl->empty[(g - 1) % STAGES], ((g - 1) / STAGES) & 1);
         if (wtid == 0 && p.trace && p.single_op < 0)   // ring drained (diagnostics)
           p.trace[static_cast<size_t>(rs.it.idx) * TRACE_FIELDS + 9] = static_cast<int64_t>(globaltimer());
-        window_smem(op, rs.it, wtid, NWORK, smem_u32(cx.ring), 1);
+        if (TRAIN && op.kind == DK_VGRID) {
+          vgrid_item(op, rs.it.mt, wtid, cx.ring);
+        } else {
+          window_smem(op, rs.it, wtid, NWORK, smem_u32(cx.ring), 1);
+        }
       } else {
         run_cc(op, rs.it, wtid, ctl->red);
       }
@@ -1365,7 +1404,7 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
       tc_fence_after();
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
-      if (!(p.dbg && (p.dbg_spin & 1))) {  // diagnostics: odd dbg_spin skips the MMAs
+      if (!(GACER_DIAG && p.dbg && (p.dbg_spin & 1))) {  // diagnostics: odd dbg_spin skips the MMAs
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
           umma_bf16(d, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
@@ -1383,6 +1422,51 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     umma_commit(&ctl->tfull[abuf]);
     dbg_mark(p, 5);
     ++acc;
+  }
+}
+
+// One 16-column sub-chunk of the lean staged epilogue: y = clamp(acc *
+// scale + bias [+ skip], lo, hi) -> bf16 RNE -> the warp's 128-byte-swizzled
+// staging rows (columns cin..cin+15 of the 64-column chunk).  scale/bias: the
+// tile's staged columns, read as warp-uniform 16-byte broadcasts.  Same IEEE
+// operations in the same order as every other epilogue path.
+__device__ __forceinline__ void epi_chunk16(const uint32_t (&r)[16], const float* esc, const float* ebi, bool skip,
+                                            const uint4 (&sk)[2], float lo, float hi, int cin, uint32_t sbuf,
+                                            int lane) {
+#pragma unroll
+  for (int g8 = 0; g8 < 2; ++g8) {
+    const float4 s0 = *reinterpret_cast<const float4*>(esc + g8 * 8);
+    const float4 s1 = *reinterpret_cast<const float4*>(esc + g8 * 8 + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(ebi + g8 * 8);
+    const float4 b1 = *reinterpret_cast<const float4*>(ebi + g8 * 8 + 4);
+    const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    float y[8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[g8 * 8 + j]), __uint_as_float(r[g8 * 8 + j + 1])),
+                                  make_float2(sv[j], sv[j + 1]), make_float2(bv[j], bv[j + 1]));
+      y[j] = o.x;
+      y[j + 1] = o.y;
+    }
+    if (skip) {
+      float sv8[8];
+      bf16x8_to_f32(sk[g8], sv8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[j] += sv8[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
+    const uint32_t ch = static_cast<uint32_t>((cin + g8 * 8) >> 3);   // 16-byte chunk of the 128-byte row
+    sts128(sbuf + lane * 128 + ((ch ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+           pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+  }
+}
+__device__ __forceinline__ void load_skip16(uint4 (&k)[2], const __nv_bfloat16* skrow, int c, int c_hi, int cout_left) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int cc = c + u * 8;
+    k[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -1436,9 +1520,10 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     if (swap) {
       if (m < op.Cout) { sc_row = op.scale[m]; bi_row = op.bias[m]; }
     } else {
-      for (int j = etid; j < bn; j += NEPI) {
-        ctl->epi_scale[j] = op.scale[n0 + j];
-        ctl->epi_bias[j] = op.bias[n0 + j];
+      for (int j = etid; j < bn; j += NEPI) {   // columns past Cout (a ragged last N-tile) are never stored
+        const bool in = n0 + j < op.Cout;
+        ctl->epi_scale[j] = in ? op.scale[n0 + j] : 0.0f;
+        ctl->epi_bias[j] = in ? op.bias[n0 + j] : 0.0f;
       }
     }
     bool do_skip = op.has_skip && split == 1 && m < op.M && !swap;
@@ -1459,10 +1544,12 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     if (etid == 0 && p.trace && p.single_op < 0)
       p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 9] = static_cast<int64_t>(globaltimer());
     tc_fence_after();
+#if GACER_DIAG
     if (p.dbg && p.dbg_spin) {   // diagnostic: delay the TMEM read after tfull
       const long long ts = clock64();
       while (clock64() - ts < p.dbg_spin) {}
     }
+#endif
     if (etid == 0) edbg(p, 11, acc);
     uint32_t taddr = cx.tmem + abuf * BN_MAX + (static_cast<uint32_t>(q * 32) << 16);
     float* part = opg.partial + static_cast<size_t>(tile) * split * (BM * bn);
@@ -1542,71 +1629,52 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
         p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
     } else if (split == 1 && staged && !op.out_f32) {
-      // lean staged bf16 path: branch-free activation clamp, 64-column
-      // staging chunks (a compile-time constant), scale/bias by shuffle
+      // lean staged bf16 path, software-pipelined over 64-column steps: the
+      // TMEM load of the second 32 columns is in flight while the first are
+      // converted (and the next step's first 32 while the second are);
+      // scale/bias are read as warp-uniform 16-byte smem broadcasts; the
+      // activation clamp is branch-free; each 64-column step is one
+      // double-buffered staging chunk and one TMA store.
       const float lo = op.act == ACT_NONE ? -INFINITY : 0.0f;
       const float hi = op.act == ACT_RELU6 ? 6.0f : INFINITY;
       const bool skip = do_skip;
       const int row0 = m0 + q * 32;
-      for (int c = c_lo; c < c_hi; c += 32) {
-        uint32_t r[32];
-        tmem_ld16_nw(taddr + c, r);
-        tmem_ld16_nw(taddr + c + 16, r + 16);   // c + 32 <= BN_MAX: columns past c_hi are never stored
-        const float sc_l = ctl->epi_scale[c + lane], bi_l = ctl->epi_bias[c + lane];
-        if (skip) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int cc = c + 32 + u * 8;
-            skB[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
-          }
-        }
-        const int cin = (c - c_lo) & 63;
-        // staging buffer of this 64-column chunk (EPI_DB: two per warp, the
-        // store of one chunk overlaps the conversion of the next)
+      // 16-column sub-chunks ping-pong between two register sets: the TMEM
+      // load of sub-chunk k+1 is in flight while sub-chunk k is converted
+      uint32_t ra[16], rb[16];
+      uint4 ka[2], kb[2];                    // residual values of the current / next sub-chunk
+      ka[0] = skA[0]; ka[1] = skA[1];
+      tmem_ld16_nw(taddr + c_lo, ra);
+      for (int c = c_lo; c < c_hi; c += 64) {
         const uint32_t sbuf = wbuf_s + (EPI_DB ? (((c - c_lo) >> 6) & 1) * STAGE_WARP_BYTES : 0);
-        if (cin == 0 && c > c_lo) {            // a new chunk: its buffer's previous store must have been read
+        if (c > c_lo) {                        // this buffer's previous store must have been read
           if (lane == 0) {
             if (EPI_DB) bulk_wait_read1();
             else bulk_wait_read0();
           }
           __syncwarp();
         }
-        tmem_wait();
 #pragma unroll
-        for (int g8 = 0; g8 < 4; ++g8) {
-          float y[8];
-#pragma unroll
-          for (int j = 0; j < 8; j += 2) {
-            const int jj = g8 * 8 + j;
-            const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1])),
-                                        make_float2(__shfl_sync(0xffffffffu, sc_l, jj), __shfl_sync(0xffffffffu, sc_l, jj + 1)),
-                                        make_float2(__shfl_sync(0xffffffffu, bi_l, jj), __shfl_sync(0xffffffffu, bi_l, jj + 1)));
-            y[j] = o.x;
-            y[j + 1] = o.y;
-          }
-          if (skip) {
-            float sv[8];
-            bf16x8_to_f32(skA[g8], sv);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) y[j] += sv[j];
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
-          const uint32_t ch = static_cast<uint32_t>((cin + g8 * 8) >> 3);   // 16-byte chunk of the 128-byte row
-          sts128(sbuf + lane * 128 + ((ch ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
-                 pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+        for (int sub = 0; sub < 4; sub += 2) {
+          const int ca = c + sub * 16, cb = ca + 16;   // columns of ra / rb
+          if (ca >= c_hi) break;
+          tmem_wait();
+          tmem_pin16(ra);
+          if (cb < c_hi) tmem_ld16_nw(taddr + cb, rb);   // cb + 16 <= BN_MAX: never past the accumulator
+          if (skip) load_skip16(kb, skrow, cb, c_hi, cout_left);
+          epi_chunk16(ra, ctl->epi_scale + ca, ctl->epi_bias + ca, skip, ka, lo, hi, sub * 16, sbuf, lane);
+          if (cb >= c_hi) break;
+          tmem_wait();
+          tmem_pin16(rb);
+          if (cb + 16 < c_hi) tmem_ld16_nw(taddr + cb + 16, ra);
+          if (skip) load_skip16(ka, skrow, cb + 16, c_hi, cout_left);
+          epi_chunk16(rb, ctl->epi_scale + cb, ctl->epi_bias + cb, skip, kb, lo, hi, sub * 16 + 16, sbuf, lane);
         }
-        if (cin == 32 || c + 32 >= c_hi) {     // 64-column chunk complete: TMA-store it
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(op.tmap_c, sbuf, n0 + c - cin, row0);
-            bulk_commit();
-          }
-        }
-        if (skip) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) skA[u] = skB[u];
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(op.tmap_c, sbuf, n0 + c, row0);
+          bulk_commit();
         }
       }
       if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
@@ -1815,6 +1883,7 @@ __device__ void releaser_role(const ExecParams& p, Ctx& cx) {
   }
 }
 
+template <bool TRAIN>
 __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Ctx cx;
@@ -1831,6 +1900,7 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
     for (int r = 0; r < ITEM_RING; ++r) { mbar_init(&ctl->lfull[r], 1); mbar_init(&ctl->lempty[r], 1); }
     fence_mbar_init();
   }
+  for (int i = tid; i < STAT_TENANTS + 2; i += NTHREADS) ctl->st_ns[i] = 0;
   if (p.single_op < 0) {  // cache the queue segments
     const int ns = p.n_tenants * p.n_clusters;
     const int nc = ns < MAX_SMEM_SEGS ? ns : MAX_SMEM_SEGS;
@@ -1856,7 +1926,7 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
     if ((tid & 31) == 0) mma_role(p, cx);
     else if ((tid & 31) == 1 && p.single_op < 0) releaser_role(p, cx);
   } else if (warp < EPI_WARP0) {
-    worker_role(p, cx);
+    worker_role<TRAIN>(p, cx);
   } else {
     epilogue_role(p, cx);
   }
@@ -1865,6 +1935,8 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
   __syncthreads();
   if (tid == 0) dbg_mark(p, 11);
   if (warp == MMA_WARP) tmem_dealloc(cx.tmem, TMEM_COLS);
+  if (p.stats && p.single_op < 0 && tid < STAT_TENANTS + 2 && ctl->st_ns[tid])
+    atomicAdd(p.stats + tid, ctl->st_ns[tid]);
   if (tid == 0 && p.single_op < 0) {
     __threadfence();
     const uint32_t old = atomicAdd(p.exit_count, 1u);
@@ -1878,7 +1950,16 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
 
 extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor(ExecParams p) {
   extern __shared__ uint8_t smem_raw[];
-  executor_body(p, smem_raw);
+  executor_body<false>(p, smem_raw);
+}
+
+// The same executor with the training tenant's virtual-grid items (DK_VGRID)
+// compiled in; launched only for rounds with a training tenant.  A separate
+// instantiation keeps the operators' call out of the inference kernel's
+// register allocation (it made the TMA producer loop spill).
+extern "C" __global__ void __launch_bounds__(NTHREADS, 1) gacer_executor_train(ExecParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  executor_body<true>(p, smem_raw);
 }
 
 // Standalone CUDA-core op kernel (baselines): one item per CTA, same tile function.
@@ -1887,8 +1968,14 @@ extern "C" __global__ void __launch_bounds__(CC_THREADS) op_cc_kernel(const OpDe
   extern __shared__ __align__(1024) uint8_t win_buf[];
   const OpDev& op = ops[op_idx];
   const Item it = decode_single(op, op_idx, blockIdx.x);
-  if (op.win) window_smem(op, it, threadIdx.x, CC_THREADS, smem_u32(win_buf), 1);
-  else run_cc(op, it, threadIdx.x, red);
+  if (op.kind == DK_VGRID) {
+    const int v0 = it.mt * op.bm, v1 = min(v0 + op.bm, op.vblocks);
+    for (int vb = v0; vb < v1; ++vb) run_vgrid(op.vfn, op.va, vb, op.vblocks, threadIdx.x, CC_THREADS, win_buf);
+  } else if (op.win) {
+    window_smem(op, it, threadIdx.x, CC_THREADS, smem_u32(win_buf), 1);
+  } else {
+    run_cc(op, it, threadIdx.x, red);
+  }
 }
 
 // =====================================================================
@@ -1900,11 +1987,14 @@ cudaError_t configure_kernels() {
   static_assert(WIN_SMEM_BYTES <= SMEM_RING_BYTES, "window staging must fit in the GEMM ring");
   cudaError_t e = cudaFuncSetAttribute(gacer_executor, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(gacer_executor_train, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(op_cc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIN_SMEM_BYTES);
 }
 
-cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s) {
-  gacer_executor<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
+cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s, bool train) {
+  if (train) gacer_executor_train<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
+  else gacer_executor<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -16,6 +16,39 @@ enum DevKind : int32_t {
   DK_GAP = 5,
   DK_SIMT_GEMM = 6,// fp32 conv / linear on CUDA cores (FFMA), fixed K order
   DK_ELTWISE = 7,  // y = act(a [+ b]) standalone elementwise
+  DK_VGRID = 8,    // a training-tenant CUDA-core operator run as a virtual grid (train_dev.cuh)
+};
+
+// Virtual-grid operators of the training tenant (train_dev.cuh documents each
+// one's argument mapping).
+enum VFn : int32_t {
+  VF_NONE = 0,
+  VF_BN_PARTIAL, VF_BN_FINALIZE, VF_BN_APPLY, VF_RELU_BWD, VF_ADD,
+  VF_MAXPOOL_FWD, VF_MAXPOOL_ARGMAX, VF_MAXPOOL_BWD, VF_GAP_FWD, VF_GAP_BWD,
+  VF_LINEAR_FWD, VF_LINEAR_DX, VF_LINEAR_DW, VF_SOFTMAX_CE, VF_MEAN, VF_SGD,
+  VF_FILTER, VF_DILATE, VF_TRANSPOSE_IM2COL, VF_WGRAD_PERMUTE, VF_WGRAD_REDUCE,
+};
+
+// Virtual-grid geometry, shared by the host lowering and the standalone calls.
+constexpr int VG_THREADS = 192;               // = NWORK: the executor's worker group
+constexpr int VG_MAX_PARTIALS = 148 * 4;      // row blocks of a BN reduction
+constexpr int VG_ROWS_PER_BLOCK_MIN = 32;
+inline int vg_bn_partials(int64_t M) {        // BN partial-sum row blocks for M rows
+  int64_t p = (M + VG_ROWS_PER_BLOCK_MIN - 1) / VG_ROWS_PER_BLOCK_MIN;
+  return static_cast<int>(p < VG_MAX_PARTIALS ? (p < 1 ? 1 : p) : VG_MAX_PARTIALS);
+}
+inline int vg_grid_for(int64_t work) {        // grid-stride ops: blocks for `work` thread tasks
+  int64_t b = (work + VG_THREADS - 1) / VG_THREADS;
+  const int64_t cap = 148 * 8;
+  return static_cast<int>(b < cap ? (b < 1 ? 1 : b) : cap);
+}
+
+// Arguments of a virtual-grid operator: pointers, 64-bit sizes, ints, floats.
+struct VArgs {
+  const void* p[8];
+  int64_t n[2];
+  int32_t i[14];
+  float f[4];
 };
 
 enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2 };
@@ -102,6 +135,10 @@ struct OpDev {
   int32_t a_mode;          // AMode
   int32_t c_tma;           // 1: epilogue stores through smem staging + TMA tensor store (tmap_c)
   const void* tmap_c;      // CUtensorMap of the output [M rows][Cout] (row stride ldo)
+  // DK_VGRID: operator, virtual grid size; an item runs virtual blocks
+  // [mt * bm, min((mt + 1) * bm, vblocks))
+  int32_t vfn, vblocks;
+  VArgs va;
 };
 
 // One work item: one output tile (mt, nt) of one op, K-slice ks.  Items are
@@ -154,7 +191,10 @@ struct ExecParams {
   int32_t own_first;        // 1: the CTA's own tenant (pref[0]) wins over higher-ranked items
   int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
   int64_t dbg_spin;         // diagnostics: epilogue delay (clocks) between tfull and the TMEM read
+  unsigned long long* stats;// [STAT_TENANTS + 2] accumulating ns: per-tenant item time (claim -> release),
+                            // then CTA time at cluster barriers, then CTA time with only unready work
 };
+constexpr int STAT_TENANTS = 16;
 constexpr int DBG_EVENTS = 24;
 // trace record per item: tenant, op, smid, idx, cluster, chunk, t_claim,
 // t_release, t_start, t_acc_ready (GEMM), t_epilogue_done (GEMM), reserved

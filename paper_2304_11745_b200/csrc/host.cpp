@@ -27,7 +27,7 @@
 namespace gacer {
 int executor_smem_bytes();
 cudaError_t configure_kernels();
-cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s);
+cudaError_t launch_executor(const ExecParams& p, int grid, cudaStream_t s, bool train);
 cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, int kind, int n_items, int num_sms,
                       cudaStream_t s);
 cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
@@ -134,8 +134,48 @@ struct FusedOp {
   int a_mode = A_GATHER;        // GEMM operand-A load path
 };
 
+// ---------------------------------------------------------------- training tenant (A11)
+// A training tenant's round is its whole SGD step (SURVEY §8 "Rounds"):
+// forward, softmax-CE, backward in reverse topological order, the update --
+// lowered at registration into a list of executor ops (tcgen05 GEMMs and
+// virtual-grid CUDA-core operators, train_dev.cuh) over library-owned
+// buffers.  Buffers are referenced symbolically and resolved when the op
+// table is built (the graph input / logits / labels are bound later).
+constexpr int TBUF_IN = -2, TBUF_OUT = -3, TBUF_LABELS = -4;
+struct TRef {
+  int buf = -1;        // -1: null; >= 0 library buffer; TBUF_*: bound buffers
+  size_t off = 0;      // byte offset
+};
+struct TrainOp {
+  int kind = DK_VGRID;           // DK_VGRID or DK_GEMM
+  int vfn = 0, vblocks = 0, per = 1;   // virtual-grid op: function, grid, virtual blocks per item
+  VArgs va{};
+  TRef vp[8];                    // VArgs pointer slots
+  OpDev gd{};                    // GEMM: geometry (pointers resolved at build time)
+  TRef g_in, g_out, g_wt, g_part, g_scale, g_bias;
+  int gemm_kind = 0;             // 0 forward conv, 1 data gradient, 2 weight gradient
+  int im2col_c = 0;              // real channels of the im2col tensor map
+  int a_ld = 0, a_rows = 0, b_rows = 0;
+  std::vector<int> deps;         // producer ops (indices into tops): RAW / WAR / WAW on buffers
+  bool reads_input = false;      // reads the bound images or labels (input gate)
+  int step_pos = 1;              // 1-based position in the step's issue order (pointer clusters)
+  int items = 1;
+  double flops = 0, bytes = 0;
+};
+
 struct Tenant {
   int batch = 0, dtype = 0, n_orig = 0;
+  // training tenant (gacer_graph.train != 0)
+  bool train = false;
+  int n_steps = 0;                   // 2 n_orig + 1 step positions (forward, backward, update)
+  std::vector<TrainOp> tops;
+  std::vector<size_t> tbuf_bytes;
+  std::vector<void*> tbufs;
+  std::vector<float> h_params;       // initial master parameters (uploaded once)
+  int buf_params = -1, buf_grads = -1, buf_mom = -1, buf_loss = -1;
+  std::map<std::pair<int, int>, std::pair<int64_t, int64_t>> param_slice;  // (orig op, which) -> (offset, count)
+  const void* labels_dev = nullptr;
+  float lr = 0.1f, momentum = 0.9f;
   int in_c = 0, in_h = 0, in_w = 0, in_c_pad = 0;
   std::vector<int> orig_kind;
   std::vector<int> orig_out_c;    // c_out for chunk validation
@@ -185,6 +225,11 @@ struct State {
   cudaStream_t copy_stream = nullptr;   // host-buffer rounds: H2D copies + input gates
   std::vector<cudaStream_t> tstreams;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_fork = nullptr;           // multi-stream baseline: fork / join (no timing)
+  std::vector<cudaEvent_t> tjoin;
+  cudaGraphExec_t base_graph = nullptr;    // captured baseline round (gacer_capture_baseline)
+  int base_graph_mode = -1;
+  int base_graph_launches = 0;
   std::vector<Tenant> tenants;
   std::vector<double> user_share;   // gacer_set_sm_shares (empty = automatic)
   Plan plan;
@@ -207,6 +252,9 @@ struct State {
   uint32_t* d_cluster_total = nullptr;
   uint32_t* d_exit = nullptr;
   int32_t* d_error = nullptr;
+  unsigned long long* d_stats = nullptr;   // executor occupancy counters (accumulating)
+  std::vector<unsigned long long> stats_prev;
+  int stat_rounds = 0;                     // executor rounds since the last gacer_get_stats
   float* d_ones = nullptr;    // unit BN scale / zero bias of the standalone GEMM calls (A11)
   float* d_zeros = nullptr;
   int n_unit = 0;
@@ -241,6 +289,11 @@ int dev_upload(T** dptr, const T* src, size_t n) {
 
 bool is_alias(int k) { return k == GACER_OP_FLATTEN || k == GACER_OP_DROPOUT || k == GACER_OP_CONCAT; }
 
+int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, int>& pos);   // defined below
+bool has_train_tenant();
+int build_train_opdev(const Tenant& T, int tenant_id, const TrainOp& op, OpDev& d, CUtensorMap* maps, bool encode);
+int upload_train_tenant(Tenant& T);
+
 // ------------------------------------------------------------------------
 // registration: validation + shape inference + fusion + packing
 // ------------------------------------------------------------------------
@@ -250,7 +303,6 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
   if (batch < 1) return set_err(GACER_E_INVALID_ARG, "batch must be >= 1");
   if (g->dtype != GACER_DTYPE_BF16 && g->dtype != GACER_DTYPE_FP32)
     return set_err(GACER_E_INVALID_ARG, "unknown dtype %d", g->dtype);
-  if (g->train) return set_err(GACER_E_UNSUPPORTED_OP, "training tenants are not supported in this version");
   if (g->in_c < 1 || g->in_h < 1 || g->in_w < 1) return set_err(GACER_E_SHAPE, "bad input shape");
   const bool f32 = g->dtype == GACER_DTYPE_FP32;
   T.batch = batch;
@@ -404,6 +456,11 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
       T.orig_tensor[i] = static_cast<int>(T.tensors.size());
       T.tensors.push_back(y);
     }
+  }
+
+  if (g->train) {
+    if (f32) return set_err(GACER_E_UNSUPPORTED_OP, "training tenants run in bf16 (SURVEY Q1)");
+    return lower_train(g, batch, T, pos);
   }
 
   // effective consumers: look through flatten / dropout aliases
@@ -798,6 +855,7 @@ char* tensor_addr(const Tenant& T, int t) {
 }
 
 int upload_tenant(Tenant& T) {
+  if (T.train) return upload_train_tenant(T);
   for (size_t b = 0; b < T.bufs.size(); ++b)
     if (T.buf_bytes[b]) CUDA_TRY(cudaMalloc(&T.bufs[b], T.buf_bytes[b]));
   for (FusedOp& F : T.fops) {
@@ -826,6 +884,7 @@ int upload_tenant(Tenant& T) {
 
 void free_tenant(Tenant& T) {
   for (void* p : T.bufs) if (p) cudaFree(p);
+  for (void* p : T.tbufs) if (p) cudaFree(p);
   for (FusedOp& F : T.fops) {
     for (void* p : {static_cast<void*>(F.d_w), static_cast<void*>(F.d_scale), static_cast<void*>(F.d_bias),
                     static_cast<void*>(F.d_partial), static_cast<void*>(F.d_tile_cnt)})
@@ -928,14 +987,28 @@ int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c) {
 }
 
 int rebuild_op_table() {
+  if (S.base_graph) {   // the captured baseline bakes op-table pointers
+    cudaGraphExecDestroy(S.base_graph);
+    S.base_graph = nullptr;
+    S.base_graph_mode = -1;
+  }
   S.h_ops.clear();
   std::vector<const FusedOp*> fops;
+  std::vector<std::pair<int, const TrainOp*>> tops;   // training ops: (tenant, op)
   for (size_t t = 0; t < S.tenants.size(); ++t) {
     Tenant& T = S.tenants[t];
     T.op_base = static_cast<int>(S.h_ops.size());
     for (const FusedOp& F : T.fops) {
       S.h_ops.push_back(make_opdev(T, static_cast<int>(t), F));
       fops.push_back(&F);
+      tops.push_back({-1, nullptr});
+    }
+    for (const TrainOp& op : T.tops) {
+      OpDev d;
+      if (int rc = build_train_opdev(T, static_cast<int>(t), op, d, nullptr, false)) return rc;
+      S.h_ops.push_back(d);
+      fops.push_back(nullptr);
+      tops.push_back({static_cast<int>(t), &op});
     }
   }
   if (S.host_only) return 0;
@@ -952,6 +1025,14 @@ int rebuild_op_table() {
   for (size_t i = 0; i < n; ++i) {
     OpDev& d = S.h_ops[i];
     if (d.kind != DK_GEMM) continue;
+    if (tops[i].second) {   // training-tenant GEMM: its own operand layouts
+      const Tenant& T = S.tenants[tops[i].first];
+      if (int rc = build_train_opdev(T, tops[i].first, *tops[i].second, d, &maps[3 * i], true)) return rc;
+      d.tmap_a = S.d_tmaps + 3 * i;
+      d.tmap_b = S.d_tmaps + 3 * i + 1;
+      d.tmap_c = S.d_tmaps + 3 * i + 2;
+      continue;
+    }
     const FusedOp& F = *fops[i];
     d.a_mode = F.a_mode;
     d.tmap_a = S.d_tmaps + 3 * i;
@@ -1025,6 +1106,19 @@ int compile_plan(Plan& P) {
   int counter = 0;
   for (int t = 0; t < nt; ++t) {
     const Tenant& T = S.tenants[t];
+    if (T.train) {   // training tenant: whole-op counters, clusters by step position
+      cr[t].resize(T.tops.size());
+      P.fop_cluster[t].resize(T.tops.size());
+      for (size_t f = 0; f < T.tops.size(); ++f) {
+        const TrainOp& op = T.tops[f];
+        P.fop_cluster[t][f] = cluster_of_orig(P, t, op.step_pos - 1);
+        ChunkRange r{0, op.kind == DK_GEMM ? op.gd.tiles_m : op.items, 0, op.kind == DK_GEMM ? op.gd.tiles_n : 1, 0, 0};
+        r.n_items = static_cast<uint32_t>(op.items);
+        r.counter = counter++;
+        cr[t][f].push_back(r);
+      }
+      continue;
+    }
     cr[t].resize(T.fops.size());
     P.fop_cluster[t].resize(T.fops.size());
     for (size_t f = 0; f < T.fops.size(); ++f) {
@@ -1093,6 +1187,40 @@ int compile_plan(Plan& P) {
   P.auto_share.assign(nt, 1.0);
   for (int t = 0; t < nt; ++t) {
     const Tenant& T = S.tenants[t];
+    if (T.train) {
+      // per op: one item's latency (GEMM: its K-blocks at the executor's
+      // measured per-SM rate; CUDA-core: its share of the op's bytes at
+      // ~10 GB/s per SM) plus the per-op latency floor; rank = the longest
+      // remaining dependency chain (HEFT upward rank over op.deps)
+      const size_t nf = T.tops.size();
+      std::vector<double> est(nf), rk(nf, 0.0), wk(nf, 0.0);
+      for (size_t f = 0; f < nf; ++f) {
+        const TrainOp& op = T.tops[f];
+        double item_ns;
+        if (op.kind == DK_GEMM) {
+          const double kblocks = static_cast<double>(op.gd.nkb) / op.gd.split_k;
+          item_ns = kblocks * BK * BM * op.gd.bn * 2.0 / 2700.0 + 1500.0;
+        } else {
+          item_ns = op.bytes / std::max(1, op.items) / 10.0 + 2000.0;
+        }
+        wk[f] = op.items * item_ns / kSplitSms;
+        est[f] = 10000.0 + std::max(item_ns, wk[f]);
+      }
+      std::vector<double> best(nf, 0.0);
+      for (size_t f = nf; f-- > 0;) {
+        rk[f] = est[f] + best[f];
+        for (int d : T.tops[f].deps) best[d] = std::max(best[d], rk[f]);
+      }
+      rank[t].resize(nf);
+      double work_ns = 0.0, chain_ns = 0.0;
+      for (size_t f = 0; f < nf; ++f) {
+        rank[t][f] = static_cast<uint32_t>(std::min(rk[f], 4.0e9));
+        work_ns += wk[f];
+        chain_ns = std::max(chain_ns, rk[f]);
+      }
+      P.auto_share[t] = std::min(1.0, work_ns / std::max(1.0, chain_ns));
+      continue;
+    }
     const size_t nf = T.fops.size();
     std::vector<double> est(nf), rk(nf, 0.0), wk(nf, 0.0);
     for (size_t f = 0; f < nf; ++f) {
@@ -1151,6 +1279,42 @@ int compile_plan(Plan& P) {
   std::vector<std::vector<std::vector<int32_t>>> seg_items(nt, std::vector<std::vector<int32_t>>(P.n_clusters));
   for (int t = 0; t < nt; ++t) {
     const Tenant& T = S.tenants[t];
+    if (T.train) {
+      for (size_t f = 0; f < T.tops.size(); ++f) {
+        const TrainOp& op = T.tops[f];
+        const ChunkRange& r = cr[t][f][0];
+        const int k = P.fop_cluster[t][f];
+        std::vector<Dep> dl;
+        if (op.reads_input) dl.push_back({P.input_counter0 + t, 1u});   // input gate (images, labels)
+        for (int d : op.deps) dl.push_back({cr[t][d][0].counter, cr[t][d][0].n_items});
+        int dep_begin = 0;
+        if (dl.size() > static_cast<size_t>(INLINE_DEPS)) {
+          dep_begin = static_cast<int>(P.deps.size());
+          P.deps.insert(P.deps.end(), dl.begin(), dl.end());
+        }
+        const int split = op.kind == DK_GEMM ? op.gd.split_k : 1;
+        for (int mt = r.m0; mt < r.m1; ++mt)
+          for (int ntile = r.n0; ntile < r.n1; ++ntile)
+            for (int ks = 0; ks < split; ++ks) {
+              Item it;
+              std::memset(&it, 0, sizeof it);
+              it.op = T.op_base + static_cast<int>(f);
+              it.mt = mt; it.nt = ntile; it.ks = ks;
+              it.dep_begin = dep_begin;
+              it.dep_count = static_cast<int>(dl.size());
+              if (dl.size() <= static_cast<size_t>(INLINE_DEPS))
+                for (size_t d = 0; d < dl.size(); ++d) { it.dc[d] = dl[d].counter; it.dt[d] = dl[d].target; }
+              it.chunk = r.counter;
+              it.cluster = k;
+              it.prio = rank[t][f];
+              it.kind = op.kind;
+              seg_items[t][k].push_back(static_cast<int32_t>(P.items.size()));
+              P.items.push_back(it);
+              P.cluster_total[k] += 1;
+            }
+      }
+      continue;
+    }
     for (size_t f = 0; f < T.fops.size(); ++f) {
       const FusedOp& F = T.fops[f];
       const int k = P.fop_cluster[t][f];
@@ -1337,6 +1501,10 @@ int upload_plan() {
   if ((rc = dev_upload(&S.d_cluster_total, P.cluster_total.data(), P.cluster_total.size()))) return rc;
   if (!S.d_exit && (rc = dev_upload<uint32_t>(&S.d_exit, nullptr, 1))) return rc;
   if (!S.d_error && (rc = dev_upload<int32_t>(&S.d_error, nullptr, 1))) return rc;
+  if (!S.d_stats && (rc = dev_upload<unsigned long long>(&S.d_stats, nullptr, STAT_TENANTS + 2))) return rc;
+  S.stats_prev.assign(STAT_TENANTS + 2, 0);
+  CUDA_TRY(cudaMemset(S.d_stats, 0, (STAT_TENANTS + 2) * sizeof(unsigned long long)));
+  S.stat_rounds = 0;
   if (S.d_trace) { cudaFree(S.d_trace); S.d_trace = nullptr; }
   if (S.opts.trace) {
     CUDA_TRY(cudaMalloc(&S.d_trace, P.items.size() * TRACE_FIELDS * sizeof(int64_t)));
@@ -1371,8 +1539,8 @@ int check_ready() {
   if (S.host_only) return set_err(GACER_E_STATE, "host-only instance cannot run rounds");
   if (S.tenants.empty()) return set_err(GACER_E_STATE, "no tenants registered");
   for (size_t t = 0; t < S.tenants.size(); ++t)
-    if (!S.tenants[t].in_dev || !S.tenants[t].out_dev)
-      return set_err(GACER_E_STATE, "tenant %zu has unbound I/O", t);
+    if (!S.tenants[t].in_dev || !S.tenants[t].out_dev || (S.tenants[t].train && !S.tenants[t].labels_dev))
+      return set_err(GACER_E_STATE, "tenant %zu has unbound I/O%s", t, S.tenants[t].train ? " or labels" : "");
   return 0;
 }
 
@@ -1397,10 +1565,11 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.segs = S.d_segs;
     p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
     p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
-    p.error = S.d_error; p.trace = S.d_trace;
+    p.error = S.d_error; p.trace = S.d_trace; p.stats = S.d_stats;
     p.n_tenants = static_cast<int>(S.tenants.size());
     p.n_clusters = S.plan.n_clusters;
     p.epoch = ++S.epoch;
+    ++S.stat_rounds;
     p.n_heads = p.n_tenants * p.n_clusters;
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
@@ -1412,7 +1581,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.gate0 = S.plan.input_counter0;
     p.n_gates = static_cast<int32_t>(S.tenants.size());
     p.self_gates = gates_written ? 0 : 1;   // device-resident inputs: the kernel opens its gates
-    CUDA_TRY(launch_executor(p, S.grid, st));
+    CUDA_TRY(launch_executor(p, S.grid, st, has_train_tenant()));
     launches = 1;
   } else if (S.mode == GACER_MODE_EXECUTOR_HOSTSYNC) {
     // the paper's pointer mechanics (Fig. 6, Eq. 8): each cluster is issued
@@ -1426,10 +1595,11 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.segs = S.d_segs;
     p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
     p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
-    p.error = S.d_error; p.trace = S.d_trace;
+    p.error = S.d_error; p.trace = S.d_trace; p.stats = S.d_stats;
     p.n_tenants = static_cast<int>(S.tenants.size());
     p.n_clusters = S.plan.n_clusters;
     p.epoch = ++S.epoch;
+    ++S.stat_rounds;
     p.n_heads = p.n_tenants * p.n_clusters;
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
@@ -1442,7 +1612,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
       p.self_gates = (!gates_written && first) ? 1 : 0;   // the first launch opens the input gates
       first = false;
       p.k_first = p.k_last = k;
-      CUDA_TRY(launch_executor(p, S.grid, st));
+      CUDA_TRY(launch_executor(p, S.grid, st, has_train_tenant()));
       ++launches;
       if (k + 1 < p.n_clusters) CUDA_TRY(cudaStreamSynchronize(st));   // the CPU-side pointer
     }
@@ -1451,37 +1621,47 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     if (ms) {
       while (S.tstreams.size() < S.tenants.size()) {
         cudaStream_t s;
+        cudaEvent_t e;
         CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         S.tstreams.push_back(s);
+        S.tjoin.push_back(e);
       }
+      if (!S.ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&S.ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(S.ev_fork, st));   // fork: also joins the streams into a graph capture
     }
     for (size_t t = 0; t < S.tenants.size(); ++t) {
       cudaStream_t ts = st;
       if (ms) {
         ts = S.tstreams[t];
-        CUDA_TRY(cudaStreamWaitEvent(ts, S.ev0, 0));
+        CUDA_TRY(cudaStreamWaitEvent(ts, S.ev_fork, 0));
       }
       const Tenant& T = S.tenants[t];
-      for (size_t f = 0; f < T.fops.size(); ++f) {
-        const FusedOp& F = T.fops[f];
-        const int nb = F.tiles_m * F.tiles_n * (F.kind == DK_GEMM ? F.split_k : 1);
+      const size_t n_ops = T.train ? T.tops.size() : T.fops.size();
+      for (size_t f = 0; f < n_ops; ++f) {
+        int kind, nb;
+        if (T.train) {
+          kind = T.tops[f].kind;
+          nb = T.tops[f].items;
+        } else {
+          const FusedOp& F = T.fops[f];
+          kind = F.kind;
+          nb = F.tiles_m * F.tiles_n * (F.kind == DK_GEMM ? F.split_k : 1);
+        }
         ExecParams base;
         std::memset(&base, 0, sizeof base);
         base.error = S.d_error;
         base.watchdog_ns = 2000000000LL;
         base.dbg = S.d_dbg;
         if (const char* e = getenv("GACER_DBG_SPIN")) base.dbg_spin = atoll(e);
-        CUDA_TRY(launch_op(base, S.d_ops, T.op_base + static_cast<int>(f), F.kind, nb, S.num_sms, ts));
+        CUDA_TRY(launch_op(base, S.d_ops, T.op_base + static_cast<int>(f), kind, nb, S.num_sms, ts));
         ++launches;
       }
     }
     if (ms) {
       for (size_t t = 0; t < S.tenants.size(); ++t) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventRecord(e, S.tstreams[t]));
-        CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
-        cudaEventDestroy(e);
+        CUDA_TRY(cudaEventRecord(S.tjoin[t], S.tstreams[t]));
+        CUDA_TRY(cudaStreamWaitEvent(st, S.tjoin[t], 0));
       }
     }
   }
@@ -1511,8 +1691,9 @@ void free_plan_device() {
                   static_cast<void*>(S.d_segs), static_cast<void*>(S.d_pref), static_cast<void*>(S.d_heads),
                   static_cast<void*>(S.d_chunk_done), static_cast<void*>(S.d_cluster_done),
                   static_cast<void*>(S.d_cluster_total), static_cast<void*>(S.d_exit),
-                  static_cast<void*>(S.d_error), static_cast<void*>(S.d_trace)})
+                  static_cast<void*>(S.d_error), static_cast<void*>(S.d_trace), static_cast<void*>(S.d_stats)})
     if (p) cudaFree(p);
+  S.d_stats = nullptr;
   S.d_items = nullptr; S.d_deps = nullptr; S.d_queue = nullptr; S.d_segs = nullptr; S.d_pref = nullptr;
   S.d_heads = nullptr; S.d_chunk_done = nullptr; S.d_cluster_done = nullptr; S.d_cluster_total = nullptr;
   S.d_exit = nullptr; S.d_error = nullptr; S.d_trace = nullptr;
@@ -1568,6 +1749,9 @@ int gacer_shutdown(void) {
     if (S.d_ops) cudaFree(S.d_ops);
     if (S.d_tmaps) cudaFree(S.d_tmaps);
     for (cudaStream_t s : S.tstreams) cudaStreamDestroy(s);
+    for (cudaEvent_t e : S.tjoin) cudaEventDestroy(e);
+    if (S.ev_fork) cudaEventDestroy(S.ev_fork);
+    if (S.base_graph) cudaGraphExecDestroy(S.base_graph);
     if (S.stream) cudaStreamDestroy(S.stream);
     if (S.copy_stream) cudaStreamDestroy(S.copy_stream);
     S.copy_stream = nullptr;
@@ -1606,7 +1790,7 @@ int gacer_get_tenant_info(int tenant, gacer_tenant_info* out) {
     return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
   const Tenant& T = S.tenants[tenant];
   out->n_orig_ops = T.n_orig;
-  out->n_fused_ops = static_cast<int32_t>(T.fops.size());
+  out->n_fused_ops = static_cast<int32_t>(T.train ? T.tops.size() : T.fops.size());
   out->batch = T.batch;
   out->in_c_pad = T.in_c_pad;
   out->in_h = T.in_h;
@@ -1616,6 +1800,15 @@ int gacer_get_tenant_info(int tenant, gacer_tenant_info* out) {
   out->out_bytes = static_cast<int64_t>(T.batch) * T.out_features * 4;
   out->flops = T.flops;
   out->gemm_ops = out->mpair_ops = out->split_k_ops = out->swap_ops = out->wide_ops = out->cc_ops = 0;
+  out->train = T.train ? 1 : 0;
+  out->n_steps = T.n_steps;
+  out->n_params = T.train ? static_cast<int64_t>(T.tbuf_bytes[T.buf_params] / 4) : 0;
+  for (const TrainOp& op : T.tops) {
+    if (op.kind != DK_GEMM) { ++out->cc_ops; continue; }
+    ++out->gemm_ops;
+    out->split_k_ops += op.gd.split_k > 1;
+    out->wide_ops += op.gd.bn > 128;
+  }
   for (const FusedOp& F : T.fops) {
     if (F.kind != DK_GEMM) { ++out->cc_ops; continue; }
     ++out->gemm_ops;
@@ -1639,6 +1832,46 @@ int gacer_bind_io(int tenant, const void* input_dev, void* output_dev) {
   return rebuild_op_table();
 }
 
+int gacer_bind_labels(int tenant, const void* labels_dev) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()))
+    return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
+  if (!S.tenants[tenant].train) return set_err(GACER_E_INVALID_ARG, "tenant %d is not a training tenant", tenant);
+  if (!labels_dev || (reinterpret_cast<uintptr_t>(labels_dev) & 3)) return set_err(GACER_E_INVALID_ARG, "bad labels buffer");
+  S.tenants[tenant].labels_dev = labels_dev;
+  return rebuild_op_table();
+}
+
+int gacer_get_train_state(int tenant, gacer_train_state* out) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !out)
+    return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
+  const Tenant& T = S.tenants[tenant];
+  if (!T.train) return set_err(GACER_E_INVALID_ARG, "tenant %d is not a training tenant", tenant);
+  std::memset(out, 0, sizeof *out);
+  out->n_params = static_cast<int64_t>(T.tbuf_bytes[T.buf_params] / 4);
+  out->n_ops = static_cast<int32_t>(T.tops.size());
+  if (S.host_only) return GACER_OK;
+  out->loss = static_cast<const float*>(T.tbufs[T.buf_loss]);
+  out->params = static_cast<float*>(T.tbufs[T.buf_params]);
+  out->grads = static_cast<const float*>(T.tbufs[T.buf_grads]);
+  out->momentum = static_cast<float*>(T.tbufs[T.buf_mom]);
+  return GACER_OK;
+}
+
+int gacer_train_param(int tenant, int32_t op_index, int32_t which, int64_t* offset, int64_t* count) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !offset || !count)
+    return set_err(GACER_E_INVALID_ARG, "bad arguments");
+  const Tenant& T = S.tenants[tenant];
+  auto it = T.param_slice.find({op_index - 1, which});
+  if (!T.train || op_index < 1 || it == T.param_slice.end())
+    return set_err(GACER_E_INVALID_ARG, "op %d of tenant %d has no parameter %d", op_index, tenant, which);
+  *offset = it->second.first;
+  *count = it->second.second;
+  return GACER_OK;
+}
+
 int gacer_set_regulation(const gacer_decomposition* dec, const gacer_sync_pointers* sp) {
   if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
   if (S.sticky_cuda) return set_err(GACER_E_CUDA, "sticky CUDA error");
@@ -1654,8 +1887,11 @@ int gacer_set_regulation(const gacer_decomposition* dec, const gacer_sync_pointe
       int prev = 0;
       for (int j = 0; j < sp->n_pointers; ++j) {
         const int c = sp->cuts[static_cast<size_t>(t) * sp->n_pointers + j];
-        if (c < 0 || c > S.tenants[t].n_orig)
-          return set_err(GACER_E_CUT_OUT_OF_RANGE, "tenant %d pointer %d = %d outside [0, %d]", t, j, c, S.tenants[t].n_orig);
+        // a training tenant's operator list is its step: forward 1..n,
+        // backward n+1..2n (reverse order), the update 2n+1
+        const int lim = S.tenants[t].train ? S.tenants[t].n_steps : S.tenants[t].n_orig;
+        if (c < 0 || c > lim)
+          return set_err(GACER_E_CUT_OUT_OF_RANGE, "tenant %d pointer %d = %d outside [0, %d]", t, j, c, lim);
         if (c < prev) return set_err(GACER_E_UNSORTED_CUTS, "tenant %d pointers decrease at %d", t, j);
         prev = c;
         P.cuts[t].push_back(c);
@@ -1670,6 +1906,8 @@ int gacer_set_regulation(const gacer_decomposition* dec, const gacer_sync_pointe
       const Tenant& T = S.tenants[c.tenant];
       if (c.op_index < 1 || c.op_index > T.n_orig) return set_err(GACER_E_INVALID_ARG, "chunking %d: bad op_index", i);
       if (c.axis == GACER_AXIS_NONE) continue;  // mask(O) = 0
+      if (T.train)   // BN statistics span the whole per-replica batch
+        return set_err(GACER_E_INVALID_ARG, "chunking %d: a training tenant's operators are not decomposed", i);
       if (c.axis != GACER_AXIS_BATCH && c.axis != GACER_AXIS_CHANNEL)
         return set_err(GACER_E_INVALID_ARG, "chunking %d: bad axis", i);
       if (c.n_chunks < 1 || !c.sizes)
@@ -1701,7 +1939,7 @@ int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n) {
   if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !out)
     return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
   const Tenant& T = S.tenants[tenant];
-  const int m = std::min(n, T.n_orig);
+  const int m = std::min(n, T.train ? T.n_steps : T.n_orig);   // training tenants: per step position
   for (int i = 0; i < m; ++i) out[i] = cluster_of_orig(S.plan, tenant, i);
   return m;
 }
@@ -1740,6 +1978,45 @@ int gacer_set_mode(int mode) {
 }
 
 int gacer_run_round_async(void* stream) { return enqueue_round(static_cast<cudaStream_t>(stream)); }
+
+// The sequential / multi-stream baselines as a CUDA graph: one round of the
+// mode's per-op launches (same tile functions, same order, same streams
+// topology) captured once and replayed, so the comparison with the
+// one-launch executor is not a comparison with host launch overhead
+// ("Each is reported plain and with CUDA Graphs").
+int gacer_capture_baseline(int mode) {
+  if (int rc = check_ready()) return rc;
+  if (mode != GACER_MODE_SEQUENTIAL && mode != GACER_MODE_MULTISTREAM)
+    return set_err(GACER_E_INVALID_ARG, "only the sequential / multi-stream baselines are captured (mode %d)", mode);
+  if (S.base_graph) { cudaGraphExecDestroy(S.base_graph); S.base_graph = nullptr; S.base_graph_mode = -1; }
+  const int saved = S.mode;
+  S.mode = mode;
+  CUDA_TRY(cudaStreamSynchronize(S.stream));
+  CUDA_TRY(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = enqueue_round(S.stream, /*record_events=*/false);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(S.stream, &g);
+  S.mode = saved;
+  if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+  if (ec != cudaSuccess) return set_err(GACER_E_CUDA, "baseline capture failed: %s", cudaGetErrorString(ec));
+  const cudaError_t ei = cudaGraphInstantiate(&S.base_graph, g, 0);
+  cudaGraphDestroy(g);
+  if (ei != cudaSuccess) return set_err(GACER_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ei));
+  S.base_graph_mode = mode;
+  S.base_graph_launches = S.last_launches;
+  return GACER_OK;
+}
+
+int gacer_run_baseline_graph(void* stream) {
+  if (int rc = check_ready()) return rc;
+  if (!S.base_graph) return set_err(GACER_E_STATE, "no captured baseline (gacer_capture_baseline)");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : S.stream;
+  CUDA_TRY(cudaEventRecord(S.ev0, st));
+  CUDA_TRY(cudaGraphLaunch(S.base_graph, st));
+  CUDA_TRY(cudaEventRecord(S.ev1, st));
+  S.last_launches = S.base_graph_launches;
+  return GACER_OK;
+}
 
 int gacer_run_round(void) {
   if (int rc = enqueue_round(S.stream)) return rc;
@@ -1801,11 +2078,27 @@ int gacer_get_stats(gacer_round_stats* out) {
   out->kernel_launches = S.last_launches;
   out->n_tenants = static_cast<int32_t>(S.tenants.size());
   for (const Tenant& T : S.tenants) {
-    out->n_fused_ops += static_cast<int32_t>(T.fops.size());
+    out->n_fused_ops += static_cast<int32_t>(T.fops.size() + T.tops.size());
+    for (const TrainOp& op : T.tops) {
+      if (op.kind == DK_GEMM) out->tensor_flops += op.flops;
+      else out->cc_bytes += op.bytes;
+    }
     for (const FusedOp& F : T.fops) {
       if (F.kind == DK_GEMM || F.kind == DK_SIMT_GEMM) out->tensor_flops += F.flops;
       else out->cc_bytes += F.bytes;
     }
+  }
+  if (!S.host_only && S.d_stats && S.stat_rounds > 0) {
+    std::vector<unsigned long long> cur(STAT_TENANTS + 2, 0);
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(cur.data(), S.d_stats, cur.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    const double r = static_cast<double>(S.stat_rounds);
+    out->stat_rounds = S.stat_rounds;
+    for (int t = 0; t < STAT_TENANTS; ++t) out->tenant_sm_ns[t] = static_cast<double>(cur[t] - S.stats_prev[t]) / r;
+    out->barrier_wait_ns = static_cast<double>(cur[STAT_TENANTS] - S.stats_prev[STAT_TENANTS]) / r;
+    out->ready_wait_ns = static_cast<double>(cur[STAT_TENANTS + 1] - S.stats_prev[STAT_TENANTS + 1]) / r;
+    S.stats_prev = cur;
+    S.stat_rounds = 0;
   }
   return GACER_OK;
 }
@@ -2233,3 +2526,646 @@ int32_t gacer_conv_fwd(const void* x_dev, const float* w_dev, int32_t N, int32_t
 }
 
 }  // extern "C"
+
+// ========================================================================
+// A11: the training tenant's step as executor ops (gacer_graph.train != 0)
+// ========================================================================
+// The step is the one train_driver.SequentialTrainer issues call by call
+// (the same operators, geometries, thread counts and reduction orders, so the
+// two give identical bits), lowered once into executor ops: forward (conv =
+// filter pack + tcgen05 GEMM, BN-train = partial sums / fp64 finalize /
+// apply(+ReLU), residual add(+ReLU), max-pool, GAP, FC), softmax-CE + mean,
+// the backward in reverse topological order (FC, GAP, ReLU, residual-add
+// gradient sharing, BN backward with the fused ReLU mask, max-pool argmax /
+// gather, conv weight gradient = operand transposes + split-K GEMM + ordered
+// reduction, conv data gradient = flipped filter pack (+ zero dilation) +
+// GEMM), and ONE SGD-momentum op over the flat parameter buffer.  Every op
+// depends on the last writer of each buffer it touches and on the readers of
+// each buffer it overwrites (op-level counters on the device).
+namespace {
+
+struct TrainLowering {
+  Tenant& T;
+  int B;
+  std::vector<int> last_writer;               // per library buffer
+  std::vector<std::vector<int>> readers;
+  std::map<int, int> sp_writer;               // special (bound) buffers
+  std::map<int, std::vector<int>> sp_readers;
+  int step = 1;
+
+  explicit TrainLowering(Tenant& t, int b) : T(t), B(b) {}
+
+  int buf(size_t bytes) {
+    T.tbuf_bytes.push_back(std::max<size_t>(bytes, 16));
+    T.tbufs.push_back(nullptr);
+    last_writer.push_back(-1);
+    readers.emplace_back();
+    return static_cast<int>(T.tbuf_bytes.size()) - 1;
+  }
+  int& writer_of(int b) { return b >= 0 ? last_writer[b] : sp_writer.emplace(b, -1).first->second; }
+  std::vector<int>& readers_of(int b) { return b >= 0 ? readers[b] : sp_readers[b]; }
+  // bytes an op moves through buffer b (the flat parameter / gradient /
+  // momentum buffers are touched per slice: not counted, see the SGD op)
+  double bytes_of(int b) const {
+    if (b < 0 || b == T.buf_params || b == T.buf_grads || b == T.buf_mom) return 0.0;
+    return static_cast<double>(T.tbuf_bytes[b]);
+  }
+
+  // append op with its buffer accesses; returns its index
+  int add(TrainOp&& op, std::initializer_list<int> rd, std::initializer_list<int> wr) {
+    const int me = static_cast<int>(T.tops.size());
+    std::set<int> dep;
+    for (int b : rd) {
+      if (b == -1) continue;
+      if (b == TBUF_IN || b == TBUF_LABELS) op.reads_input = true;
+      if (writer_of(b) >= 0) dep.insert(writer_of(b));
+      op.bytes += bytes_of(b);
+    }
+    for (int b : wr) {
+      if (b == -1) continue;
+      if (writer_of(b) >= 0) dep.insert(writer_of(b));
+      for (int r : readers_of(b)) dep.insert(r);
+      op.bytes += bytes_of(b);
+    }
+    dep.erase(me);
+    op.deps.assign(dep.begin(), dep.end());
+    for (int b : rd) if (b != -1) readers_of(b).push_back(me);
+    for (int b : wr) {
+      if (b == -1) continue;
+      writer_of(b) = me;
+      readers_of(b).clear();
+    }
+    op.step_pos = step;
+    if (op.kind == DK_VGRID) {
+      // items: about two waves of the SMs' worth of virtual-block ranges
+      op.per = std::max(1, cdiv(op.vblocks, 2 * kSplitSms));
+      op.items = cdiv(op.vblocks, op.per);
+    } else {
+      op.items = op.gd.tiles_m * op.gd.tiles_n * op.gd.split_k;
+    }
+    T.tops.push_back(std::move(op));
+    return me;
+  }
+
+  static TrainOp vg(int fn, int nvb) {
+    TrainOp o;
+    o.kind = DK_VGRID;
+    o.vfn = fn;
+    o.vblocks = std::max(1, nvb);
+    std::memset(&o.va, 0, sizeof o.va);
+    return o;
+  }
+};
+
+}  // namespace
+
+namespace {
+
+int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, int>& pos) {
+  const int n = g->n_ops;
+  const int B = batch;
+  T.train = true;
+  T.n_steps = 2 * n + 1;
+  T.lr = g->lr;
+  T.momentum = g->momentum;
+  TrainLowering L(T, B);
+  auto idx_of = [&](int id) { return id == 0 ? -1 : pos.at(id); };
+  // ---- plan: shapes (NHWC, the input padded to 8 channels) and the fusable ReLUs
+  struct Shp { int h, w, c; };
+  std::vector<Shp> shp(n);
+  const Shp in_shape{T.in_h, T.in_w, T.in_c_pad};
+  auto shape_of = [&](int id) { return id == 0 ? in_shape : shp[pos.at(id)]; };
+  std::vector<std::vector<int>> consumers(n + 1);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < g->ops[i].n_preds; ++j) consumers[idx_of(g->ops[i].preds[j]) + 1].push_back(i);
+  std::vector<int> fused_relu(n, -1);   // producer (bn / add) -> its ReLU
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    const Shp x = shape_of(o.preds[0]);
+    switch (o.kind) {
+      case GACER_OP_CONV2D:
+        if (o.groups != 1 || (o.flags & GACER_FLAG_BIAS))
+          return set_err(GACER_E_UNSUPPORTED_OP, "op %d: training supports ungrouped convs without bias", o.id);
+        shp[i] = {(x.h + 2 * o.pad_h - o.kh) / o.stride + 1, (x.w + 2 * o.pad_w - o.kw) / o.stride + 1, o.c_out};
+        if (o.c_out % 8) return set_err(GACER_E_UNSUPPORTED_OP, "op %d: training needs c_out %% 8 == 0", o.id);
+        break;
+      case GACER_OP_MAXPOOL:
+        shp[i] = {(x.h + 2 * o.pad_h - o.kh) / o.stride + 1, (x.w + 2 * o.pad_w - o.kw) / o.stride + 1, x.c};
+        break;
+      case GACER_OP_GAP: shp[i] = {1, 1, x.c}; break;
+      case GACER_OP_LINEAR:
+        if (x.h != 1 || x.w != 1 || x.c != o.c_in)
+          return set_err(GACER_E_UNSUPPORTED_OP, "op %d: training FC needs a [B][c_in] (1x1) input", o.id);
+        shp[i] = {1, 1, o.c_out};
+        break;
+      case GACER_OP_BN: case GACER_OP_FLATTEN: case GACER_OP_DROPOUT: case GACER_OP_RELU: case GACER_OP_ADD:
+        shp[i] = x;
+        break;
+      default:
+        return set_err(GACER_E_UNSUPPORTED_OP, "op %d: kind %d has no training lowering", o.id, o.kind);
+    }
+    if (o.kind == GACER_OP_RELU) {
+      const int pr = idx_of(o.preds[0]);
+      if (pr < 0 || (g->ops[pr].kind != GACER_OP_BN && g->ops[pr].kind != GACER_OP_ADD) || consumers[pr + 1].size() != 1)
+        return set_err(GACER_E_UNSUPPORTED_OP, "op %d: a ReLU is trained fused into its BN or residual-add producer",
+                       o.id);
+      fused_relu[pr] = i;
+    }
+  }
+  if (g->ops[n - 1].kind != GACER_OP_LINEAR)
+    return set_err(GACER_E_UNSUPPORTED_OP, "training needs the last op to be the FC producing the logits");
+  const int ncls = g->ops[n - 1].c_out;
+  T.out_features = ncls;
+
+  // ---- flat fp32 parameters (registration order: conv w (input channels
+  //      padded), bn gamma, beta, linear w, b), gradients, momentum
+  int64_t np = 0;
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    auto slot = [&](int which, int64_t cnt) { T.param_slice[{i, which}] = {np, cnt}; np += cnt; };
+    if (o.kind == GACER_OP_CONV2D) slot(0, static_cast<int64_t>(o.c_out) * shape_of(o.preds[0]).c * o.kh * o.kw);
+    else if (o.kind == GACER_OP_BN) { slot(0, shape_of(o.preds[0]).c); slot(1, shape_of(o.preds[0]).c); }
+    else if (o.kind == GACER_OP_LINEAR) { slot(0, static_cast<int64_t>(o.c_out) * o.c_in); if (o.flags & GACER_FLAG_BIAS) slot(1, o.c_out); }
+  }
+  T.h_params.assign(np, 0.0f);
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    if (o.kind == GACER_OP_CONV2D) {
+      if (!o.weight) return set_err(GACER_E_INVALID_ARG, "op %d: missing weight", o.id);
+      const int cp = shape_of(o.preds[0]).c;
+      float* w = T.h_params.data() + T.param_slice[{i, 0}].first;
+      for (int co = 0; co < o.c_out; ++co)
+        for (int ci = 0; ci < o.c_in; ++ci)
+          for (int r = 0; r < o.kh * o.kw; ++r)
+            w[(static_cast<size_t>(co) * cp + ci) * o.kh * o.kw + r] = o.weight[(static_cast<size_t>(co) * o.c_in + ci) * o.kh * o.kw + r];
+    } else if (o.kind == GACER_OP_BN) {
+      const int c = shape_of(o.preds[0]).c;
+      std::memcpy(T.h_params.data() + T.param_slice[{i, 0}].first, o.bn_gamma, c * sizeof(float));
+      std::memcpy(T.h_params.data() + T.param_slice[{i, 1}].first, o.bn_beta, c * sizeof(float));
+    } else if (o.kind == GACER_OP_LINEAR) {
+      std::memcpy(T.h_params.data() + T.param_slice[{i, 0}].first, o.weight,
+                  static_cast<size_t>(o.c_out) * o.c_in * sizeof(float));
+      if (o.flags & GACER_FLAG_BIAS) {
+        if (!o.bias) return set_err(GACER_E_INVALID_ARG, "op %d: missing bias", o.id);
+        std::memcpy(T.h_params.data() + T.param_slice[{i, 1}].first, o.bias, o.c_out * sizeof(float));
+      }
+    }
+  }
+  T.buf_params = L.buf(np * 4);
+  T.buf_grads = L.buf(np * 4);
+  T.buf_mom = L.buf(np * 4);
+  T.buf_loss = L.buf(4);
+  auto pref = [&](int i, int which) { TRef r; r.buf = T.buf_params; r.off = T.param_slice.at({i, which}).first * 4; return r; };
+  auto gref = [&](int i, int which) { TRef r; r.buf = T.buf_grads; r.off = T.param_slice.at({i, which}).first * 4; return r; };
+  auto bref = [](int b) { TRef r; r.buf = b; return r; };
+  // unit scale / zero bias of the GEMM epilogues (no folded BN in training)
+  int maxrows = 8;
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    if (o.kind == GACER_OP_CONV2D) maxrows = std::max({maxrows, o.c_out, shape_of(o.preds[0]).c * o.kh * o.kw});
+  }
+  maxrows = roundup(maxrows, 256) + 8;
+  const int buf_ones = L.buf(static_cast<size_t>(maxrows) * 4), buf_zeros = L.buf(static_cast<size_t>(maxrows) * 4);
+  // (filled at upload: ones = 1.0f; zeros stay zero)
+  T.param_slice[{-1, 0}] = {buf_ones, maxrows};
+
+  // ---- forward
+  std::vector<int> out(n, -1);   // output buffer of each op (after aliasing)
+  auto out_of = [&](int id) { return id == 0 ? TBUF_IN : out[pos.at(id)]; };
+  std::vector<std::pair<int, int>> saved(n, {-1, -1});   // BN: (mean, var)
+  int logits = -1;
+  for (int i = 0; i < n; ++i) {
+    const gacer_op_desc& o = g->ops[i];
+    L.step = i + 1;
+    const Shp x = shape_of(o.preds[0]), y = shp[i];
+    const int xb = out_of(o.preds[0]);
+    switch (o.kind) {
+      case GACER_OP_CONV2D: {
+        FwdGeom fg;
+        if (int rc = fwd_geom(B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, fg)) return rc;
+        const int wp = L.buf(static_cast<size_t>(fg.rows) * fg.Kpad * 2);
+        TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(fg.rows) * fg.Kpad));
+        f.vp[0] = pref(i, 0); f.vp[1] = bref(wp);
+        f.va.i[0] = o.c_out; f.va.i[1] = x.c; f.va.i[2] = o.kh; f.va.i[3] = o.kw; f.va.i[4] = fg.cread;
+        f.va.i[5] = fg.Kpad; f.va.i[6] = fg.rows; f.va.i[7] = 1;
+        L.add(std::move(f), {T.buf_params}, {wp});
+        const int yb = L.buf(static_cast<size_t>(B) * y.h * y.w * y.c * 2);
+        TrainOp m;
+        m.kind = DK_GEMM;
+        m.gemm_kind = 0;
+        OpDev& d = m.gd;
+        std::memset(&d, 0, sizeof d);
+        d.kind = DK_GEMM; d.act = ACT_NONE;
+        d.B = B; d.H = x.h; d.W = x.w; d.C = fg.cread; d.ldi = x.c;
+        d.Ho = fg.Ho; d.Wo = fg.Wo; d.Cout = o.c_out; d.ldo = o.c_out;
+        d.kh = o.kh; d.kw = o.kw; d.stride = o.stride; d.ph = o.pad_h; d.pw = o.pad_w; d.mrep = 1;
+        d.M = fg.M; d.N = o.c_out; d.K = fg.K; d.Kpad = fg.Kpad;
+        d.tiles_m = fg.tiles_m; d.tiles_n = fg.tiles_n; d.bm = BM; d.bn = fg.bn; d.split_k = 1; d.nkb = fg.nkb;
+        d.ldw = fg.Kpad; d.a_mode = fg.a_mode;
+        m.g_in = bref(xb); m.g_out = bref(yb); m.g_wt = bref(wp);
+        m.g_scale = bref(buf_ones); m.g_bias = bref(buf_zeros);
+        m.im2col_c = x.c; m.a_ld = x.c; m.a_rows = fg.M; m.b_rows = fg.rows;
+        m.flops = 2.0 * fg.M * o.c_out * static_cast<double>(x.c) * o.kh * o.kw;
+        L.add(std::move(m), {xb, wp, buf_ones, buf_zeros}, {yb});
+        out[i] = yb;
+        break;
+      }
+      case GACER_OP_BN: {
+        const int64_t M = static_cast<int64_t>(B) * x.h * x.w;
+        const int C = x.c, P = vg_bn_partials(M);
+        const int part = L.buf(static_cast<size_t>(P) * 2 * C * 4 + 4 * C * 4);
+        const int mean = L.buf(C * 4), var = L.buf(C * 4);
+        const int yb = L.buf(static_cast<size_t>(M) * C * 2);
+        TRef coef = bref(part);
+        coef.off = static_cast<size_t>(P) * 2 * C * 4;
+        TrainOp a = TrainLowering::vg(VF_BN_PARTIAL, P);
+        a.vp[0] = bref(xb); a.vp[5] = bref(part); a.va.n[0] = M; a.va.i[0] = 0; a.va.i[1] = C;
+        L.add(std::move(a), {xb}, {part});
+        TrainOp f = TrainLowering::vg(VF_BN_FINALIZE, cdiv(C, 32));
+        f.vp[0] = bref(part); f.vp[1] = pref(i, 0); f.vp[2] = pref(i, 1); f.vp[3] = bref(xb); f.vp[5] = bref(mean);
+        f.vp[6] = bref(var); f.vp[7] = coef;
+        f.va.n[0] = M; f.va.i[0] = 0; f.va.i[1] = C; f.va.i[2] = P; f.va.f[0] = o.bn_eps;
+        L.add(std::move(f), {part, T.buf_params, xb}, {mean, var, part});
+        TrainOp e = TrainLowering::vg(VF_BN_APPLY, vg_grid_for(M * (C / 8)));
+        e.vp[0] = bref(xb); e.vp[3] = coef; e.vp[4] = bref(yb);
+        e.va.n[0] = M; e.va.i[0] = 0; e.va.i[1] = C; e.va.i[2] = fused_relu[i] >= 0 ? 1 : 0;
+        L.add(std::move(e), {xb, part}, {yb});
+        saved[i] = {mean, var};
+        out[i] = yb;
+        break;
+      }
+      case GACER_OP_RELU:
+      case GACER_OP_FLATTEN:
+      case GACER_OP_DROPOUT:
+        out[i] = xb;        // fused into the producer / identity
+        break;
+      case GACER_OP_ADD: {
+        const int bb = out_of(o.preds[1]);
+        const int yb = L.buf(static_cast<size_t>(B) * x.h * x.w * x.c * 2);
+        const int64_t n8 = static_cast<int64_t>(B) * x.h * x.w * x.c / 8;
+        TrainOp a = TrainLowering::vg(VF_ADD, vg_grid_for(n8));
+        a.vp[0] = bref(xb); a.vp[1] = bref(bb); a.vp[2] = bref(yb);
+        a.va.n[0] = n8; a.va.i[0] = fused_relu[i] >= 0 ? 1 : 0;
+        L.add(std::move(a), {xb, bb}, {yb});
+        out[i] = yb;
+        break;
+      }
+      case GACER_OP_MAXPOOL: {
+        const int yb = L.buf(static_cast<size_t>(B) * y.h * y.w * x.c * 2);
+        TrainOp a = TrainLowering::vg(VF_MAXPOOL_FWD, vg_grid_for(static_cast<int64_t>(B) * y.h * y.w * (x.c / 8)));
+        a.vp[0] = bref(xb); a.vp[1] = bref(yb);
+        const int iv[11] = {B, x.h, x.w, x.c, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, y.h, y.w};
+        std::memcpy(a.va.i, iv, sizeof iv);
+        L.add(std::move(a), {xb}, {yb});
+        out[i] = yb;
+        break;
+      }
+      case GACER_OP_GAP: {
+        const int yb = L.buf(static_cast<size_t>(B) * x.c * 2);
+        TrainOp a = TrainLowering::vg(VF_GAP_FWD, vg_grid_for(static_cast<int64_t>(B) * (x.c / 8)));
+        a.vp[0] = bref(xb); a.vp[1] = bref(yb);
+        a.va.i[0] = B; a.va.i[1] = x.h * x.w; a.va.i[2] = x.c;
+        L.add(std::move(a), {xb}, {yb});
+        out[i] = yb;
+        break;
+      }
+      case GACER_OP_LINEAR: {
+        const bool last = i == n - 1;
+        const int zb = last ? TBUF_OUT : L.buf(static_cast<size_t>(B) * o.c_out * 4);
+        TrainOp a = TrainLowering::vg(VF_LINEAR_FWD, vg_grid_for(static_cast<int64_t>(B) * o.c_out * 32));
+        a.vp[0] = bref(xb); a.vp[1] = pref(i, 0);
+        if (o.flags & GACER_FLAG_BIAS) a.vp[2] = pref(i, 1);
+        a.vp[3] = bref(zb);
+        a.va.i[0] = B; a.va.i[1] = o.c_in; a.va.i[2] = o.c_out;
+        L.add(std::move(a), {xb, T.buf_params}, {zb});
+        out[i] = zb;
+        if (last) logits = zb;
+        break;
+      }
+    }
+  }
+  // ---- loss: mean softmax cross-entropy over the labels
+  L.step = n;
+  const int dz = L.buf(static_cast<size_t>(B) * ncls * 4), rowloss = L.buf(static_cast<size_t>(B) * 4);
+  {
+    TrainOp a = TrainLowering::vg(VF_SOFTMAX_CE, B);
+    a.vp[0] = bref(logits); a.vp[1] = bref(TBUF_LABELS); a.vp[2] = bref(dz); a.vp[3] = bref(rowloss);
+    a.va.i[0] = B; a.va.i[1] = ncls;
+    L.add(std::move(a), {logits, TBUF_LABELS}, {dz, rowloss});
+    TrainOp m = TrainLowering::vg(VF_MEAN, 1);
+    m.vp[0] = bref(rowloss); m.vp[1] = bref(T.buf_loss); m.va.i[0] = B;
+    L.add(std::move(m), {rowloss}, {T.buf_loss});
+  }
+  // ---- backward (reverse issue order)
+  std::map<int, int> dval;            // orig op index (-1: input) -> gradient buffer of its output
+  std::set<int> shared;               // gradient buffers held by two dval entries (a residual add): copy on write
+  std::map<int, int> relu_mask;       // bn op -> the output of its fused ReLU
+  dval[n - 1] = dz;
+  auto acc = [&](int tid, int gb, size_t bytes) {
+    if (tid < 0) return;
+    auto it = dval.find(tid);
+    if (it == dval.end()) { dval[tid] = gb; return; }
+    const int cur = it->second;
+    const int dst = shared.count(cur) ? L.buf(bytes) : cur;
+    TrainOp a = TrainLowering::vg(VF_ADD, vg_grid_for(static_cast<int64_t>(bytes / 16)));
+    a.vp[0] = bref(cur); a.vp[1] = bref(gb); a.vp[2] = bref(dst);
+    a.va.n[0] = static_cast<int64_t>(bytes / 16); a.va.i[0] = 0;
+    L.add(std::move(a), {cur, gb}, {dst});
+    dval[tid] = dst;
+  };
+  for (int i = n - 1; i >= 0; --i) {
+    const gacer_op_desc& o = g->ops[i];
+    L.step = 2 * n - i;
+    auto itd = dval.find(i);
+    if (itd == dval.end()) continue;
+    int dy = itd->second;
+    dval.erase(itd);
+    const int pred = idx_of(o.preds[0]);
+    const Shp x = shape_of(o.preds[0]), y = shp[i];
+    const int xb = out_of(o.preds[0]);
+    const size_t xbytes = static_cast<size_t>(B) * x.h * x.w * x.c * 2;
+    switch (o.kind) {
+      case GACER_OP_LINEAR: {
+        const int dx = L.buf(static_cast<size_t>(B) * x.c * 4);
+        TrainOp a = TrainLowering::vg(VF_LINEAR_DX, vg_grid_for(static_cast<int64_t>(B) * x.c));
+        a.vp[0] = pref(i, 0); a.vp[1] = bref(dy); a.vp[2] = bref(dx);
+        a.va.i[0] = B; a.va.i[1] = x.c; a.va.i[2] = o.c_out;
+        L.add(std::move(a), {T.buf_params, dy}, {dx});
+        TrainOp w = TrainLowering::vg(VF_LINEAR_DW, vg_grid_for(static_cast<int64_t>(o.c_out) * x.c));
+        w.vp[0] = bref(xb); w.vp[1] = bref(dy); w.vp[2] = gref(i, 0);
+        if (o.flags & GACER_FLAG_BIAS) w.vp[3] = gref(i, 1);
+        w.va.i[0] = B; w.va.i[1] = x.c; w.va.i[2] = o.c_out;
+        L.add(std::move(w), {xb, dy}, {T.buf_grads});
+        acc(pred, dx, static_cast<size_t>(B) * x.c * 4);
+        break;
+      }
+      case GACER_OP_FLATTEN: case GACER_OP_DROPOUT:
+        acc(pred, dy, 0);
+        break;
+      case GACER_OP_GAP: {
+        const int dx = L.buf(xbytes);
+        TrainOp a = TrainLowering::vg(VF_GAP_BWD, vg_grid_for(static_cast<int64_t>(B) * x.h * x.w * (x.c / 8)));
+        a.vp[0] = bref(dy); a.vp[1] = bref(dx);
+        a.va.i[0] = B; a.va.i[1] = x.h * x.w; a.va.i[2] = x.c;
+        L.add(std::move(a), {dy}, {dx});
+        acc(pred, dx, xbytes);
+        break;
+      }
+      case GACER_OP_RELU: {
+        if (g->ops[pred].kind == GACER_OP_BN) {
+          relu_mask[pred] = out[i];           // applied inside the BN backward (fused)
+        } else {
+          const int dst = shared.count(dy) ? L.buf(xbytes) : dy;
+          TrainOp a = TrainLowering::vg(VF_RELU_BWD, vg_grid_for(static_cast<int64_t>(xbytes / 16)));
+          a.vp[0] = bref(out[i]); a.vp[1] = bref(dy); a.vp[2] = bref(dst);
+          a.va.n[0] = static_cast<int64_t>(xbytes / 16); a.va.i[0] = 0;
+          L.add(std::move(a), {out[i], dy}, {dst});
+          dy = dst;
+        }
+        acc(pred, dy, xbytes);
+        break;
+      }
+      case GACER_OP_ADD:
+        shared.insert(dy);                    // both inputs receive dy itself (no copy)
+        acc(idx_of(o.preds[0]), dy, xbytes);
+        acc(idx_of(o.preds[1]), dy, xbytes);
+        break;
+      case GACER_OP_BN: {
+        const int64_t M = static_cast<int64_t>(B) * x.h * x.w;
+        const int C = x.c, P = vg_bn_partials(M);
+        const int part = L.buf(static_cast<size_t>(P) * 2 * C * 4 + 4 * C * 4);
+        const int dx = L.buf(xbytes);
+        TRef coef = bref(part);
+        coef.off = static_cast<size_t>(P) * 2 * C * 4;
+        auto im = relu_mask.find(i);
+        const int ym = im == relu_mask.end() ? -1 : im->second;
+        if (im != relu_mask.end()) relu_mask.erase(im);
+        TrainOp a = TrainLowering::vg(VF_BN_PARTIAL, P);
+        a.vp[0] = bref(xb); a.vp[1] = bref(dy); if (ym >= 0) a.vp[2] = bref(ym);
+        a.vp[3] = bref(saved[i].first); a.vp[4] = bref(saved[i].second); a.vp[5] = bref(part);
+        a.va.n[0] = M; a.va.i[0] = 1; a.va.i[1] = C; a.va.f[0] = o.bn_eps;
+        L.add(std::move(a), {xb, dy, ym, saved[i].first, saved[i].second}, {part});
+        TrainOp f = TrainLowering::vg(VF_BN_FINALIZE, cdiv(C, 32));
+        f.vp[0] = bref(part); f.vp[1] = pref(i, 0); f.vp[3] = bref(saved[i].first); f.vp[4] = bref(saved[i].second);
+        f.vp[5] = gref(i, 0); f.vp[6] = gref(i, 1); f.vp[7] = coef;
+        f.va.n[0] = M; f.va.i[0] = 1; f.va.i[1] = C; f.va.i[2] = P; f.va.f[0] = o.bn_eps;
+        L.add(std::move(f), {part, T.buf_params, saved[i].first, saved[i].second}, {T.buf_grads, part});
+        TrainOp e = TrainLowering::vg(VF_BN_APPLY, vg_grid_for(M * (C / 8)));
+        e.vp[0] = bref(xb); e.vp[1] = bref(dy); if (ym >= 0) e.vp[2] = bref(ym); e.vp[3] = coef; e.vp[4] = bref(dx);
+        e.va.n[0] = M; e.va.i[0] = 1; e.va.i[1] = C;
+        L.add(std::move(e), {xb, dy, ym, part}, {dx});
+        acc(pred, dx, xbytes);
+        break;
+      }
+      case GACER_OP_MAXPOOL: {
+        const int arg = L.buf(static_cast<size_t>(B) * y.h * y.w * x.c);
+        const int dx = L.buf(xbytes);
+        const int iv[11] = {B, x.h, x.w, x.c, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, y.h, y.w};
+        TrainOp a = TrainLowering::vg(VF_MAXPOOL_ARGMAX, vg_grid_for(static_cast<int64_t>(B) * y.h * y.w * (x.c / 8)));
+        a.vp[0] = bref(xb); a.vp[1] = bref(arg);
+        std::memcpy(a.va.i, iv, sizeof iv);
+        L.add(std::move(a), {xb}, {arg});
+        TrainOp b2 = TrainLowering::vg(VF_MAXPOOL_BWD, vg_grid_for(static_cast<int64_t>(B) * x.h * x.w * (x.c / 8)));
+        b2.vp[0] = bref(arg); b2.vp[1] = bref(dy); b2.vp[2] = bref(dx);
+        std::memcpy(b2.va.i, iv, sizeof iv);
+        L.add(std::move(b2), {arg, dy}, {dx});
+        acc(pred, dx, xbytes);
+        break;
+      }
+      case GACER_OP_CONV2D: {
+        // weight gradient: dW = dy^T . im2col(x), both operands staged K-major
+        // along the pixel index, split-K over the pixels, ordered reduction
+        WgradGeom wg;
+        if (int rc = wgrad_geom(B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, wg)) return rc;
+        const int ab = L.buf(static_cast<size_t>(wg.rows_a) * wg.Kpad * 2);
+        const int bb = L.buf(static_cast<size_t>(wg.rows_b) * wg.Kpad * 2);
+        const int tiles = wg.tiles_m * wg.tiles_n;
+        const int part = L.buf(static_cast<size_t>(tiles) * wg.split * BM * wg.bn * 4);
+        const int gbuf = wg.split > 1 ? -1 : L.buf(static_cast<size_t>(o.c_out) * wg.Ngemm * 4);
+        {
+          TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, (wg.Kpad / 64) * cdiv(o.c_out, 64));
+          t.vp[0] = bref(dy); t.vp[1] = bref(ab);
+          t.va.n[0] = wg.M;
+          const int iv[12] = {static_cast<int>(wg.M), 1, 1, o.c_out, 1, 1, 1, 1, 0, 0, wg.Kpad, 1};
+          std::memcpy(t.va.i, iv, sizeof iv);
+          L.add(std::move(t), {dy}, {ab});
+        }
+        {
+          TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, (wg.Kpad / 64) * cdiv(x.c, 64) * o.kh * o.kw);
+          t.vp[0] = bref(xb); t.vp[1] = bref(bb);
+          t.va.n[0] = wg.M;
+          const int iv[12] = {B, x.h, x.w, x.c, wg.Ho, wg.Wo, o.kw, o.stride, o.pad_h, o.pad_w, wg.Kpad, o.kh};
+          std::memcpy(t.va.i, iv, sizeof iv);
+          L.add(std::move(t), {xb}, {bb});
+        }
+        {
+          TrainOp m;
+          m.kind = DK_GEMM;
+          m.gemm_kind = 2;
+          OpDev& d = m.gd;
+          std::memset(&d, 0, sizeof d);
+          d.kind = DK_GEMM; d.act = ACT_NONE; d.out_f32 = 1;
+          d.B = 1; d.H = 1; d.W = 1; d.C = wg.Kpad; d.ldi = wg.Kpad;
+          d.Ho = 1; d.Wo = 1; d.Cout = wg.Ngemm; d.ldo = wg.Ngemm;
+          d.kh = 1; d.kw = 1; d.stride = 1; d.mrep = 1;
+          d.M = o.c_out; d.N = wg.Ngemm; d.K = wg.Kpad; d.Kpad = wg.Kpad;
+          d.tiles_m = wg.tiles_m; d.tiles_n = wg.tiles_n; d.bm = BM; d.bn = wg.bn;
+          d.split_k = wg.split; d.nkb = wg.nkb; d.ldw = wg.Kpad;
+          d.partials_only = wg.split > 1 ? 1 : 0;
+          d.a_mode = A_ROWS;
+          m.g_in = bref(ab); m.g_wt = bref(bb); m.g_part = bref(part); m.g_out = bref(gbuf);
+          m.g_scale = bref(buf_ones); m.g_bias = bref(buf_zeros);
+          m.a_ld = wg.Kpad; m.a_rows = wg.rows_a; m.b_rows = wg.rows_b;
+          m.flops = 2.0 * o.c_out * static_cast<double>(wg.Ngemm) * wg.M;
+          L.add(std::move(m), {ab, bb, buf_ones, buf_zeros}, {part, gbuf});
+        }
+        if (wg.split > 1) {
+          TrainOp r = TrainLowering::vg(VF_WGRAD_REDUCE, vg_grid_for(static_cast<int64_t>((wg.Ngemm + 3) / 4) * o.c_out));
+          r.vp[0] = bref(part); r.vp[1] = gref(i, 0);
+          r.va.i[0] = o.c_out; r.va.i[1] = x.c; r.va.i[2] = o.kh; r.va.i[3] = o.kw; r.va.i[4] = wg.bn;
+          r.va.i[5] = wg.tiles_n; r.va.i[6] = wg.split;
+          L.add(std::move(r), {part}, {T.buf_grads});
+        } else {
+          TrainOp r = TrainLowering::vg(VF_WGRAD_PERMUTE, vg_grid_for(static_cast<int64_t>(o.c_out) * x.c * o.kh * o.kw));
+          r.vp[0] = bref(gbuf); r.vp[1] = gref(i, 0);
+          r.va.i[0] = o.c_out; r.va.i[1] = x.c; r.va.i[2] = o.kh; r.va.i[3] = o.kw;
+          L.add(std::move(r), {gbuf}, {T.buf_grads});
+        }
+        if (pred >= 0) {
+          // data gradient: a forward conv of (zero-dilated) dy with the
+          // flipped, transposed filter
+          DgradGeom dg;
+          if (int rc = dgrad_geom(B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, dg)) return rc;
+          const int wp = L.buf(static_cast<size_t>(dg.rows) * dg.Kpad * 2);
+          TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(dg.rows) * dg.Kpad));
+          f.vp[0] = pref(i, 0); f.vp[1] = bref(wp);
+          f.va.i[0] = o.c_out; f.va.i[1] = x.c; f.va.i[2] = o.kh; f.va.i[3] = o.kw; f.va.i[4] = dg.cread;
+          f.va.i[5] = dg.Kpad; f.va.i[6] = dg.rows; f.va.i[7] = 0;
+          L.add(std::move(f), {T.buf_params}, {wp});
+          int src = dy;
+          if (o.stride > 1) {
+            src = L.buf(static_cast<size_t>(B) * dg.Hdd * dg.Wdd * o.c_out * 2);
+            TrainOp dl = TrainLowering::vg(VF_DILATE, vg_grid_for(static_cast<int64_t>(B) * dg.Hdd * dg.Wdd * (o.c_out / 8)));
+            dl.vp[0] = bref(dy); dl.vp[1] = bref(src);
+            const int iv[7] = {B, dg.Hd, dg.Wd, o.c_out, o.stride, dg.Hdd, dg.Wdd};
+            std::memcpy(dl.va.i, iv, sizeof iv);
+            L.add(std::move(dl), {dy}, {src});
+          }
+          const int dx = L.buf(xbytes);
+          TrainOp m;
+          m.kind = DK_GEMM;
+          m.gemm_kind = 1;
+          OpDev& d = m.gd;
+          std::memset(&d, 0, sizeof d);
+          d.kind = DK_GEMM; d.act = ACT_NONE;
+          d.B = B; d.H = dg.Hdd; d.W = dg.Wdd; d.C = dg.cread; d.ldi = o.c_out;
+          d.Ho = x.h; d.Wo = x.w; d.Cout = x.c; d.ldo = x.c;
+          d.kh = o.kh; d.kw = o.kw; d.stride = 1; d.ph = dg.ph; d.pw = dg.pw; d.mrep = 1;
+          d.M = dg.M; d.N = x.c; d.K = dg.K; d.Kpad = dg.Kpad;
+          d.tiles_m = dg.tiles_m; d.tiles_n = dg.tiles_n; d.bm = BM; d.bn = dg.bn; d.split_k = 1; d.nkb = dg.nkb;
+          d.ldw = dg.Kpad; d.a_mode = dg.a_mode;
+          m.g_in = bref(src); m.g_out = bref(dx); m.g_wt = bref(wp);
+          m.g_scale = bref(buf_ones); m.g_bias = bref(buf_zeros);
+          m.im2col_c = o.c_out; m.a_ld = o.c_out; m.a_rows = dg.M; m.b_rows = dg.rows;
+          m.flops = 2.0 * dg.M * x.c * static_cast<double>(o.c_out) * o.kh * o.kw;
+          L.add(std::move(m), {src, wp, buf_ones, buf_zeros}, {dx});
+          acc(pred, dx, xbytes);
+        }
+        break;
+      }
+    }
+  }
+  // ---- the update: SGD with momentum over the flat parameters
+  L.step = 2 * n + 1;
+  {
+    TrainOp a = TrainLowering::vg(VF_SGD, vg_grid_for(np));
+    a.vp[0] = bref(T.buf_params); a.vp[1] = bref(T.buf_grads); a.vp[2] = bref(T.buf_mom);
+    a.va.n[0] = np; a.va.i[0] = 0; a.va.f[0] = T.lr; a.va.f[1] = T.momentum;
+    a.bytes = 5.0 * 4.0 * static_cast<double>(np);   // read w, g, buf; write w, buf
+    L.add(std::move(a), {T.buf_params, T.buf_grads, T.buf_mom}, {T.buf_params, T.buf_mom});
+  }
+  T.flops = 0;
+  for (const TrainOp& o : T.tops) T.flops += o.flops;
+  return 0;
+}
+
+}  // namespace
+
+namespace {
+
+bool has_train_tenant() {
+  for (const Tenant& T : S.tenants) if (T.train) return true;
+  return false;
+}
+
+// device address of a symbolic training-tenant buffer reference
+void* tref_addr(const Tenant& T, const TRef& r) {
+  char* base = nullptr;
+  if (r.buf >= 0) base = static_cast<char*>(T.tbufs[r.buf]);
+  else if (r.buf == TBUF_IN) base = const_cast<char*>(static_cast<const char*>(T.in_dev));
+  else if (r.buf == TBUF_OUT) base = static_cast<char*>(T.out_dev);
+  else if (r.buf == TBUF_LABELS) base = const_cast<char*>(static_cast<const char*>(T.labels_dev));
+  return base ? base + r.off : nullptr;
+}
+
+// The OpDev of training op f with its buffers resolved; GEMM ops also get
+// their tensor maps encoded into maps[0..2] (A, B, output) when every buffer
+// exists (device mode, I/O bound).
+int build_train_opdev(const Tenant& T, int tenant_id, const TrainOp& op, OpDev& d, CUtensorMap* maps, bool encode) {
+  if (op.kind == DK_VGRID) {
+    std::memset(&d, 0, sizeof d);
+    d.kind = DK_VGRID;
+    d.tenant = tenant_id;
+    d.vfn = op.vfn;
+    d.vblocks = op.vblocks;
+    d.bm = op.per;
+    d.tiles_m = op.items;
+    d.tiles_n = 1;
+    d.split_k = 1;
+    d.va = op.va;
+    for (int j = 0; j < 8; ++j) d.va.p[j] = tref_addr(T, op.vp[j]);
+    return 0;
+  }
+  d = op.gd;
+  d.tenant = tenant_id;
+  d.in = tref_addr(T, op.g_in);
+  d.out = tref_addr(T, op.g_out);
+  d.wt = tref_addr(T, op.g_wt);
+  d.partial = static_cast<float*>(tref_addr(T, op.g_part));
+  d.scale = static_cast<const float*>(tref_addr(T, op.g_scale));
+  d.bias = static_cast<const float*>(tref_addr(T, op.g_bias));
+  d.c_tma = 0;
+  if (!encode || !d.in || !d.wt) return 0;
+  int rc = 0;
+  if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, op.im2col_c);
+  else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[0], d.in, op.gemm_kind == 2 ? d.Kpad : d.K, op.a_rows, op.a_ld, BM);
+  if (!rc) rc = encode_rows(&maps[1], d.wt, d.Kpad, op.b_rows, d.Kpad, d.bn);
+  if (rc) return rc;
+  if (op.gemm_kind != 2 && d.out && (static_cast<long long>(d.ldo) * 2) % 16 == 0) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Cout), static_cast<cuuint64_t>(d.M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ldo) * 2};
+    const cuuint32_t box[2] = {64u, 32u};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode_tiled(&maps[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d.out, dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "training op: output tensor map (%d)", static_cast<int>(r));
+    d.c_tma = 1;
+  }
+  return 0;
+}
+
+int upload_train_tenant(Tenant& T) {
+  for (size_t b = 0; b < T.tbufs.size(); ++b) {
+    CUDA_TRY(cudaMalloc(&T.tbufs[b], T.tbuf_bytes[b]));
+    CUDA_TRY(cudaMemset(T.tbufs[b], 0, T.tbuf_bytes[b]));   // zero: padding rows, momentum, gradients
+  }
+  CUDA_TRY(cudaMemcpy(T.tbufs[T.buf_params], T.h_params.data(), T.h_params.size() * 4, cudaMemcpyHostToDevice));
+  const auto ones = T.param_slice.at({-1, 0});
+  CUDA_TRY(launch_fill(static_cast<float*>(T.tbufs[ones.first]), static_cast<int>(ones.second), 1.0f, nullptr));
+  CUDA_TRY(cudaDeviceSynchronize());
+  std::vector<float>().swap(T.h_params);
+  return 0;
+}
+
+}  // namespace

@@ -1,0 +1,799 @@
+// train_dev.cuh -- the training tenant's CUDA-core operators (SURVEY.md §8(a)
+// A11) as "virtual grid" device functions, shared by the standalone C-ABI
+// calls of include/gacer_train.h (train_ops.cu: one vgrid_kernel launch of
+// nvb blocks x VG_THREADS) and by the executor's DK_VGRID work items
+// (executor.cu: the worker group runs a range of virtual blocks).  Same code,
+// same thread count, same virtual-block decomposition => bit-identical
+// results in both paths.
+//
+// Every function is   f(const VArgs& a, vb, nvb, tid, nthr, smem)
+// and behaves like block vb of an nvb-block grid of nthr threads: grid-stride
+// loops stride by nvb * nthr; block-level reductions use named barrier 1 over
+// nthr threads and the caller's shared-memory scratch (VG_SMEM_BYTES).
+// Reductions are deterministic: fixed row ranges per virtual block summed in
+// row order (fp32), block partials combined in block order (fp64), no atomics.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "gacer_dev.h"
+
+namespace gacer {
+
+static_assert(VG_THREADS == NWORK, "virtual blocks run on the executor's worker group");
+constexpr int VG_SMEM_BYTES = 2 * VG_THREADS * 8 * 4;   // largest scratch (BN partial sums)
+
+__device__ __forceinline__ void vg_bar(int nthr) { asm volatile("bar.sync 1, %0;\n" ::"r"(nthr) : "memory"); }
+
+__device__ __forceinline__ void vg_unpack8(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ uint32_t vg_pack2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint4 vg_pack8(const float* f) {
+  return make_uint4(vg_pack2(f[0], f[1]), vg_pack2(f[2], f[3]), vg_pack2(f[4], f[5]), vg_pack2(f[6], f[7]));
+}
+
+#define VG_LOOP(i, total) \
+  for (int64_t i = static_cast<int64_t>(vb) * nthr + tid; i < (total); i += static_cast<int64_t>(nvb) * nthr)
+
+// ------------------------------------------------------------------ BN
+// BN partial sums over row block vb (of P = nvb blocks).  mode 0 (forward
+// statistics): (sum (x - K), sum (x - K)^2) with the per-channel shift K =
+// x[0][c] (shifted sums: no cancellation when |mean| >> std); mode 1
+// (backward): (sum dy', sum dy' * xhat), dy' = dy masked by the fused ReLU's
+// output ym when given, xhat = (x - mean) * rsqrt(var + eps).
+// Thread t owns 8-channel group gl = t % G and row phase t / G.
+// a: p0 x, p1 dy, p2 ym, p3 mean, p4 var, p5 part [P][2][C] (out); n0 M;
+//    i0 mode, i1 C; f0 eps
+__device__ inline void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[1]);
+  const __nv_bfloat16* ym = static_cast<const __nv_bfloat16*>(a.p[2]);
+  const float* mean = static_cast<const float*>(a.p[3]);
+  const float* var = static_cast<const float*>(a.p[4]);
+  float* part = static_cast<float*>(const_cast<void*>(a.p[5]));
+  const int64_t M = a.n[0];
+  const int mode = a.i[0], C = a.i[1];
+  const float eps = a.f[0];
+  float* red = reinterpret_cast<float*>(smem);           // [2][nthr * 8]
+  constexpr int kUnroll = 4;
+  const int G8 = C / 8;
+  const int G = G8 < nthr ? G8 : nthr;
+  const int RP = nthr / G;
+  const int gl = tid % G, ph = tid / G;
+  const int64_t rows = (M + nvb - 1) / nvb;
+  const int64_t r0 = vb * rows;
+  const int64_t r1 = r0 + rows < M ? r0 + rows : M;
+  for (int gbase = 0; gbase < G8; gbase += G) {
+    const int g = gbase + gl;
+    float s1[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float mu[8], is[8];
+    const bool active = ph < RP && g < G8;
+    if (active) {
+      if (mode == 1) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          mu[j] = mean[g * 8 + j];
+          is[j] = rsqrtf(var[g * 8 + j] + eps);
+        }
+      } else {
+        vg_unpack8(*reinterpret_cast<const uint4*>(x + g * 8), mu);   // the shift K (row 0)
+      }
+    }
+    if (active) {
+      for (int64_t r = r0 + ph; r < r1; r += kUnroll * RP) {
+        uint4 va[kUnroll], vd[kUnroll], vm[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t rr = r + u * RP;
+          va[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(x + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+          if (mode == 1) {
+            vd[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(dy + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+            vm[u] = (ym && rr < r1) ? __ldcs(reinterpret_cast<const uint4*>(ym + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          if (r + u * RP >= r1) break;
+          float v[8];
+          vg_unpack8(va[u], v);
+          if (mode == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float d = v[j] - mu[j];
+              s1[j] += d;
+              s2[j] = fmaf(d, d, s2[j]);
+            }
+          } else {
+            float d[8];
+            vg_unpack8(vd[u], d);
+            if (ym) {                        // fused ReLU backward: the mask of the BN's ReLU output
+              float mk[8];
+              vg_unpack8(vm[u], mk);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              s1[j] += d[j];
+              s2[j] = fmaf(d[j], (v[j] - mu[j]) * is[j], s2[j]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      red[tid * 8 + j] = s1[j];
+      red[nthr * 8 + tid * 8 + j] = s2[j];
+    }
+    vg_bar(nthr);
+    if (ph == 0 && g < G8) {          // combine the row phases in phase order
+      for (int q = 1; q < RP; ++q)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s1[j] += red[(q * G + gl) * 8 + j];
+          s2[j] += red[nthr * 8 + (q * G + gl) * 8 + j];
+        }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        part[(static_cast<size_t>(vb) * 2 + 0) * C + g * 8 + j] = s1[j];
+        part[(static_cast<size_t>(vb) * 2 + 1) * C + g * 8 + j] = s2[j];
+      }
+    }
+    vg_bar(nthr);
+  }
+}
+
+// Combine the P partials of 32 channels (block vb) in block order (fp64),
+// then fold the apply pass's per-channel constants into coef (fp32 [k][C]):
+//   mode 0 -> o1 = mean, o2 = biased var; coef = (scale, shift)
+//   mode 1 -> o1 = dgamma = sum dy*xhat, o2 = dbeta = sum dy; coef = (a, b, c)
+//             with dx = a * dy + b * x + c (BN backward expanded in x)
+// Warp w sums partials p = w, w + W, ... (W = nthr / 32 warps) in order, then
+// warp 0 adds the W warp sums in warp order.
+// a: p0 part, p1 gamma, p2 beta, p3 x (mode 0: the shift rows) / mean_in
+//    (mode 1), p4 var_in (mode 1), p5 o1, p6 o2, p7 coef; n0 M; i0 mode,
+//    i1 C, i2 P; f0 eps
+__device__ inline void vg_bn_finalize(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+  (void)nvb;
+  const float* part = static_cast<const float*>(a.p[0]);
+  const float* gamma = static_cast<const float*>(a.p[1]);
+  const float* beta = static_cast<const float*>(a.p[2]);
+  const int64_t M = a.n[0];
+  const int mode = a.i[0], C = a.i[1], P = a.i[2];
+  const float eps = a.f[0];
+  float* o1 = static_cast<float*>(const_cast<void*>(a.p[5]));
+  float* o2 = static_cast<float*>(const_cast<void*>(a.p[6]));
+  float* coef = static_cast<float*>(const_cast<void*>(a.p[7]));
+  const int W = nthr >> 5;
+  double* red = reinterpret_cast<double*>(smem);        // [2][W][32]
+  const int lane = tid & 31, wp = tid >> 5;
+  const int c = vb * 32 + lane;
+  double s = 0.0, q = 0.0;
+  if (c < C && wp < W) {
+    int p = wp;
+    for (; p + 3 * W < P; p += 4 * W) {     // four partials' loads in flight, summed in order
+      float x0[4], x1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = part[(static_cast<size_t>(p + W * u) * 2 + 0) * C + c];
+        x1[u] = part[(static_cast<size_t>(p + W * u) * 2 + 1) * C + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += x0[u];
+        q += x1[u];
+      }
+    }
+    for (; p < P; p += W) {
+      s += part[(static_cast<size_t>(p) * 2 + 0) * C + c];
+      q += part[(static_cast<size_t>(p) * 2 + 1) * C + c];
+    }
+  }
+  if (wp < W) {
+    red[wp * 32 + lane] = s;
+    red[(W + wp) * 32 + lane] = q;
+  }
+  vg_bar(nthr);
+  if (wp == 0 && c < C) {
+    s = red[lane];
+    q = red[W * 32 + lane];
+    for (int w = 1; w < W; ++w) {
+      s += red[w * 32 + lane];
+      q += red[(W + w) * 32 + lane];
+    }
+    const double Md = static_cast<double>(M);
+    if (mode == 0) {
+      const double K = __bfloat162float(static_cast<const __nv_bfloat16*>(a.p[3])[c]);   // the shift
+      const double d = s / Md;
+      double v = q / Md - d * d;
+      v = v > 0.0 ? v : 0.0;
+      const double mu = K + d;
+      o1[c] = static_cast<float>(mu);
+      o2[c] = static_cast<float>(v);
+      const double sc = gamma[c] / sqrt(static_cast<double>(static_cast<float>(v)) + eps);
+      coef[c] = static_cast<float>(sc);
+      coef[C + c] = static_cast<float>(beta[c] - static_cast<double>(static_cast<float>(mu)) * sc);
+    } else {
+      const float* mean_in = static_cast<const float*>(a.p[3]);
+      const float* var_in = static_cast<const float*>(a.p[4]);
+      o1[c] = static_cast<float>(q);   // dgamma
+      o2[c] = static_cast<float>(s);   // dbeta
+      const double is = 1.0 / sqrt(static_cast<double>(var_in[c]) + eps);
+      const double gi = gamma[c] * is;
+      const double k = gi * is * static_cast<double>(static_cast<float>(q)) / Md;
+      coef[c] = static_cast<float>(gi);
+      coef[C + c] = static_cast<float>(-k);
+      coef[2 * C + c] = static_cast<float>(-gi * static_cast<double>(static_cast<float>(s)) / Md + k * mean_in[c]);
+    }
+  }
+  vg_bar(nthr);   // the scratch is reused by the next virtual block
+}
+
+// y = act(x * scale + shift) (mode 0); dx = a * dy + b * x + c (mode 1).
+// a: p0 x, p1 dy, p2 ym, p3 coef, p4 out; n0 M; i0 mode, i1 C, i2 relu
+__device__ inline void vg_bn_apply(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[1]);
+  const __nv_bfloat16* ym = static_cast<const __nv_bfloat16*>(a.p[2]);
+  const float* coef = static_cast<const float*>(a.p[3]);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[4]));
+  const int64_t M = a.n[0];
+  const int mode = a.i[0], C = a.i[1], relu = a.i[2];
+  const int G8 = C / 8;
+  float k0[8], k1[8], k2[8];
+  int c0 = -1;
+  VG_LOOP(i, M * G8) {
+    const int c = static_cast<int>(i % G8) * 8;
+    if (c != c0) {
+      c0 = c;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        k0[j] = coef[c + j];
+        k1[j] = coef[C + c + j];
+        k2[j] = mode == 1 ? coef[2 * C + c + j] : 0.0f;
+      }
+    }
+    float v[8];
+    vg_unpack8(__ldcs(reinterpret_cast<const uint4*>(x) + i), v);
+    if (mode == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float t = fmaf(v[j], k0[j], k1[j]);
+        v[j] = relu ? fmaxf(t, 0.0f) : t;
+      }
+    } else {
+      float d[8];
+      vg_unpack8(__ldcs(reinterpret_cast<const uint4*>(dy) + i), d);
+      if (ym) {
+        float mk[8];
+        vg_unpack8(__ldcs(reinterpret_cast<const uint4*>(ym) + i), mk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = fmaf(k0[j], d[j], fmaf(k1[j], v[j], k2[j]));
+    }
+    __stcs(reinterpret_cast<uint4*>(out) + i, vg_pack8(v));
+  }
+}
+
+// ------------------------------------------------------------------ elementwise
+// dx = dy where x > 0 (and x < 6 for ReLU6), else 0.  a: p0 x, p1 dy, p2 dx; n0 n8; i0 six
+__device__ inline void vg_relu_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const uint4* x = static_cast<const uint4*>(a.p[0]);
+  const uint4* dy = static_cast<const uint4*>(a.p[1]);
+  uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[2]));
+  const int six = a.i[0];
+  VG_LOOP(i, a.n[0]) {
+    float v[8], d[8];
+    vg_unpack8(x[i], v);
+    vg_unpack8(dy[i], d);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = (v[j] > 0.0f && (!six || v[j] < 6.0f)) ? d[j] : 0.0f;
+    dx[i] = vg_pack8(d);
+  }
+}
+
+// y = a + b (ReLU when relu != 0).  a: p0 a, p1 b, p2 y; n0 n8; i0 relu
+__device__ inline void vg_add(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const uint4* pa = static_cast<const uint4*>(a.p[0]);
+  const uint4* pb = static_cast<const uint4*>(a.p[1]);
+  uint4* y = static_cast<uint4*>(const_cast<void*>(a.p[2]));
+  const int relu = a.i[0];
+  VG_LOOP(i, a.n[0]) {
+    float u[8], v[8];
+    vg_unpack8(pa[i], u);
+    vg_unpack8(pb[i], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float t = u[j] + v[j];
+      u[j] = relu ? fmaxf(t, 0.0f) : t;
+    }
+    y[i] = vg_pack8(u);
+  }
+}
+
+// ------------------------------------------------------------------ pooling
+// ints: i0 N, i1 H, i2 W, i3 C, i4 KH, i5 KW, i6 S, i7 ph, i8 pw, i9 Ho, i10 Wo
+// Max-pool forward.  a: p0 x, p1 y
+__device__ inline void vg_maxpool_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  uint4* y = static_cast<uint4*>(const_cast<void*>(a.p[1]));
+  const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], KH = a.i[4], KW = a.i[5], S = a.i[6], ph = a.i[7],
+            pw = a.i[8], Ho = a.i[9], Wo = a.i[10];
+  const int G8 = C / 8;
+  VG_LOOP(i, static_cast<int64_t>(N) * Ho * Wo * G8) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int wo = static_cast<int>(pix % Wo), ho = static_cast<int>((pix / Wo) % Ho);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(Wo) * Ho));
+    float best[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+    for (int r = 0; r < KH; ++r) {
+      const int hh = ho * S - ph + r;
+      if (hh < 0 || hh >= H) continue;
+      for (int q = 0; q < KW; ++q) {
+        const int ww = wo * S - pw + q;
+        if (ww < 0 || ww >= W) continue;
+        float v[8];
+        vg_unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hh) * W + ww) * C + g * 8), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) best[j] = fmaxf(best[j], v[j]);
+      }
+    }
+    y[i] = vg_pack8(best);
+  }
+}
+
+// Max-pool backward, pass 1: per (output window, 8-channel group) the first
+// maximum per channel (row-major tap order, padded taps skipped, Q14) as a
+// tap index byte.  a: p0 x, p1 arg (uint8 [N*Ho*Wo*C])
+__device__ inline void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  uint2* arg = static_cast<uint2*>(const_cast<void*>(a.p[1]));
+  const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], KH = a.i[4], KW = a.i[5], S = a.i[6], ph = a.i[7],
+            pw = a.i[8], Ho = a.i[9], Wo = a.i[10];
+  const int G8 = C / 8;
+  VG_LOOP(i, static_cast<int64_t>(N) * Ho * Wo * G8) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int wo = static_cast<int>(pix % Wo), ho = static_cast<int>((pix / Wo) % Ho);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(Wo) * Ho));
+    float best[8];
+    uint32_t tap[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; tap[j] = 255u; }
+    for (int r = 0; r < KH; ++r) {
+      const int hh = ho * S - ph + r;
+      if (hh < 0 || hh >= H) continue;
+      for (int q = 0; q < KW; ++q) {
+        const int ww = wo * S - pw + q;
+        if (ww < 0 || ww >= W) continue;
+        float v[8];
+        vg_unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hh) * W + ww) * C + g * 8), v);
+        const uint32_t id = static_cast<uint32_t>(r * KW + q);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (tap[j] == 255u || v[j] > best[j]) { best[j] = v[j]; tap[j] = id; }
+      }
+    }
+    uint2 o;
+    o.x = tap[0] | (tap[1] << 8) | (tap[2] << 16) | (tap[3] << 24);
+    o.y = tap[4] | (tap[5] << 8) | (tap[6] << 16) | (tap[7] << 24);
+    arg[i] = o;
+  }
+}
+
+// Max-pool backward, pass 2: per (input pixel, 8-channel group) the sum of dy
+// over the windows whose recorded tap is this pixel, in (ho, wo) order.
+// a: p0 arg, p1 dy, p2 dx
+__device__ inline void vg_maxpool_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const uint2* arg = static_cast<const uint2*>(a.p[0]);
+  const uint4* dy = static_cast<const uint4*>(a.p[1]);
+  uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[2]));
+  const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], KH = a.i[4], KW = a.i[5], S = a.i[6], ph = a.i[7],
+            pw = a.i[8], Ho = a.i[9], Wo = a.i[10];
+  const int G8 = C / 8;
+  VG_LOOP(i, static_cast<int64_t>(N) * H * W * G8) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int wi = static_cast<int>(pix % W), hi = static_cast<int>((pix / W) % H);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(W) * H));
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int ho0 = hi + ph - KH + 1;
+    ho0 = ho0 <= 0 ? 0 : (ho0 + S - 1) / S;
+    int ho1 = (hi + ph) / S;
+    ho1 = ho1 < Ho - 1 ? ho1 : Ho - 1;
+    int wo0 = wi + pw - KW + 1;
+    wo0 = wo0 <= 0 ? 0 : (wo0 + S - 1) / S;
+    int wo1 = (wi + pw) / S;
+    wo1 = wo1 < Wo - 1 ? wo1 : Wo - 1;
+    for (int ho = ho0; ho <= ho1; ++ho)
+      for (int wo = wo0; wo <= wo1; ++wo) {
+        const int64_t o = ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * G8 + g;
+        const uint2 t = arg[o];
+        const uint32_t me = static_cast<uint32_t>((hi - (ho * S - ph)) * KW + (wi - (wo * S - pw)));
+        const uint32_t tt[8] = {t.x & 255u, (t.x >> 8) & 255u, (t.x >> 16) & 255u, t.x >> 24,
+                                t.y & 255u, (t.y >> 8) & 255u, (t.y >> 16) & 255u, t.y >> 24};
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) any |= tt[j] == me;
+        if (!any) continue;
+        float d[8];
+        vg_unpack8(dy[o], d);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (tt[j] == me) acc[j] += d[j];
+      }
+    dx[i] = vg_pack8(acc);
+  }
+}
+
+// GAP backward: dx[n][p][c] = dy[n][c] / HW.  a: p0 dy (f32 [N][C]), p1 dx; i0 N, i1 HW, i2 C
+__device__ inline void vg_gap_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const float* dy = static_cast<const float*>(a.p[0]);
+  uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[1]));
+  const int N = a.i[0], HW = a.i[1], C = a.i[2];
+  const int G8 = C / 8;
+  const float inv = 1.0f / static_cast<float>(HW);
+  VG_LOOP(i, static_cast<int64_t>(N) * HW * G8) {
+    const int g = static_cast<int>(i % G8);
+    const int n = static_cast<int>(i / (static_cast<int64_t>(HW) * G8));
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = dy[static_cast<int64_t>(n) * C + g * 8 + j] * inv;
+    dx[i] = vg_pack8(v);
+  }
+}
+
+// GAP forward: y[n][c] = (1/HW) sum_p x[n][p][c] in pixel order (fp32), bf16.
+// a: p0 x, p1 y; i0 N, i1 HW, i2 C
+__device__ inline void vg_gap_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  uint4* y = static_cast<uint4*>(const_cast<void*>(a.p[1]));
+  const int N = a.i[0], HW = a.i[1], C = a.i[2];
+  const int G8 = C / 8;
+  VG_LOOP(i, static_cast<int64_t>(N) * G8) {
+    const int g = static_cast<int>(i % G8), n = static_cast<int>(i / G8);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < HW; ++p) {
+      float v[8];
+      vg_unpack8(*reinterpret_cast<const uint4*>(x + (static_cast<int64_t>(n) * HW + p) * C + g * 8), v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] /= static_cast<float>(HW);
+    y[i] = vg_pack8(acc);
+  }
+}
+
+// ------------------------------------------------------------------ FC
+// z[n][o] = b[o] + sum_k w[o][k] x[n][k]: one warp per output, lane l sums
+// k = l, l+32, ..., then a fixed xor butterfly.  a: p0 x (bf16), p1 w (f32),
+// p2 b (nullable), p3 z (f32); i0 N, i1 K, i2 O
+__device__ inline void vg_linear_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  const float* w = static_cast<const float*>(a.p[1]);
+  const float* b = static_cast<const float*>(a.p[2]);
+  float* z = static_cast<float*>(const_cast<void*>(a.p[3]));
+  const int N = a.i[0], K = a.i[1], O = a.i[2];
+  const int lane = tid & 31;
+  const int64_t nw = static_cast<int64_t>(nvb) * (nthr >> 5);
+  for (int64_t wid = static_cast<int64_t>(vb) * (nthr >> 5) + (tid >> 5); wid < static_cast<int64_t>(N) * O;
+       wid += nw) {
+    const int n = static_cast<int>(wid / O), o = static_cast<int>(wid % O);
+    const __nv_bfloat16* xr = x + static_cast<int64_t>(n) * K;
+    const float* wr = w + static_cast<int64_t>(o) * K;
+    float s = 0.0f;
+    for (int k = lane; k < K; k += 32) s = fmaf(__bfloat162float(xr[k]), wr[k], s);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) z[wid] = s + (b ? b[o] : 0.0f);
+  }
+}
+
+// dx[n][k] = sum_o dy[n][o] w[o][k] in o order.  a: p0 w, p1 dy, p2 dx (f32); i0 N, i1 K, i2 O
+__device__ inline void vg_linear_dx(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const float* w = static_cast<const float*>(a.p[0]);
+  const float* dy = static_cast<const float*>(a.p[1]);
+  float* dx = static_cast<float*>(const_cast<void*>(a.p[2]));
+  const int N = a.i[0], K = a.i[1], O = a.i[2];
+  VG_LOOP(i, static_cast<int64_t>(N) * K) {
+    const int n = static_cast<int>(i / K), k = static_cast<int>(i % K);
+    float s = 0.0f;
+    for (int o = 0; o < O; ++o) s = fmaf(dy[static_cast<int64_t>(n) * O + o], w[static_cast<int64_t>(o) * K + k], s);
+    dx[i] = s;
+  }
+}
+
+// dw[o][k] = sum_n dy[n][o] x[n][k], db[o] = sum_n dy[n][o] (n order).
+// a: p0 x (bf16), p1 dy, p2 dw, p3 db (nullable); i0 N, i1 K, i2 O
+__device__ inline void vg_linear_dw(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  const float* dy = static_cast<const float*>(a.p[1]);
+  float* dw = static_cast<float*>(const_cast<void*>(a.p[2]));
+  float* db = static_cast<float*>(const_cast<void*>(a.p[3]));
+  const int N = a.i[0], K = a.i[1], O = a.i[2];
+  VG_LOOP(i, static_cast<int64_t>(O) * K) {
+    const int o = static_cast<int>(i / K), k = static_cast<int>(i % K);
+    float s = 0.0f;
+    for (int n = 0; n < N; ++n)
+      s = fmaf(dy[static_cast<int64_t>(n) * O + o], __bfloat162float(x[static_cast<int64_t>(n) * K + k]), s);
+    dw[i] = s;
+    if (db && k == 0) {
+      float t = 0.0f;
+      for (int n = 0; n < N; ++n) t += dy[static_cast<int64_t>(n) * O + o];
+      db[o] = t;
+    }
+  }
+}
+
+// Softmax cross-entropy of row vb: fixed-order reductions (max, then sum of
+// exp): thread partials over j = tid, tid + nthr, ..., then thread 0 combines
+// them in thread order.  dz = (softmax - onehot) / N (may alias z); rowloss[n].
+// a: p0 z, p1 labels (int32), p2 dz, p3 rowloss; i0 N, i1 Cls
+__device__ inline void vg_softmax_ce(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+  (void)nvb;
+  const float* z = static_cast<const float*>(a.p[0]);
+  const int32_t* labels = static_cast<const int32_t*>(a.p[1]);
+  float* dz = static_cast<float*>(const_cast<void*>(a.p[2]));
+  float* rowloss = static_cast<float*>(const_cast<void*>(a.p[3]));
+  const int N = a.i[0], Cls = a.i[1];
+  float* red = reinterpret_cast<float*>(smem);   // [nthr + 2]
+  const int n = vb;
+  const float* zr = z + static_cast<int64_t>(n) * Cls;
+  float m = -INFINITY;
+  for (int j = tid; j < Cls; j += nthr) m = fmaxf(m, zr[j]);
+  red[tid] = m;
+  vg_bar(nthr);
+  if (tid == 0) {
+    float t = red[0];
+    for (int q = 1; q < nthr; ++q) t = fmaxf(t, red[q]);
+    red[nthr] = t;
+  }
+  vg_bar(nthr);
+  m = red[nthr];
+  float s = 0.0f;
+  for (int j = tid; j < Cls; j += nthr) s += expf(zr[j] - m);
+  vg_bar(nthr);
+  red[tid] = s;
+  vg_bar(nthr);
+  if (tid == 0) {
+    float t = red[0];
+    for (int q = 1; q < nthr; ++q) t += red[q];
+    red[nthr + 1] = t;
+  }
+  vg_bar(nthr);
+  const float sum = red[nthr + 1];
+  const int lab = labels[n];
+  const bool ok = lab >= 0 && lab < Cls;
+  const float zl = ok ? zr[lab] : 0.0f;   // read before dz (which may alias z) is written
+  vg_bar(nthr);
+  const float invN = 1.0f / static_cast<float>(N);
+  for (int j = tid; j < Cls; j += nthr)
+    dz[static_cast<int64_t>(n) * Cls + j] = (expf(zr[j] - m) / sum - (j == lab ? 1.0f : 0.0f)) * invN;
+  if (tid == 0) rowloss[n] = ok ? (logf(sum) + m) - zl : NAN;
+  vg_bar(nthr);   // the scratch is reused by the next virtual block
+}
+
+// out = mean of v[0..N) in index order (fp64).  a: p0 v, p1 out; i0 N
+__device__ inline void vg_mean(const VArgs& a, int vb, int, int tid, int, uint8_t*) {
+  if (vb != 0 || tid != 0) return;
+  const float* v = static_cast<const float*>(a.p[0]);
+  const int N = a.i[0];
+  double s = 0.0;
+  for (int i = 0; i < N; ++i) s += v[i];
+  *static_cast<float*>(const_cast<void*>(a.p[1])) = static_cast<float>(s / N);
+}
+
+// SGD with momentum (PyTorch semantics): buf = mom * buf + g (buf = g on the
+// first step: a zero-initialised buf gives exactly that), w -= lr * buf.
+// a: p0 w, p1 g, p2 buf; n0 n; i0 first; f0 lr, f1 momentum
+__device__ inline void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  float* w = static_cast<float*>(const_cast<void*>(a.p[0]));
+  const float* g = static_cast<const float*>(a.p[1]);
+  float* buf = static_cast<float*>(const_cast<void*>(a.p[2]));
+  const int first = a.i[0];
+  const float lr = a.f[0], mom = a.f[1];
+  VG_LOOP(i, a.n[0]) {
+    const float b = first ? g[i] : fmaf(mom, buf[i], g[i]);
+    buf[i] = b;
+    w[i] = fmaf(-lr, b, w[i]);
+  }
+}
+
+// ------------------------------------------------------------------ GEMM operand staging
+// Conv filter packing from the fp32 master weights w [Cout][Cin][KH][KW] into
+// a K-major bf16 GEMM B operand [rows][Kpad]: forward = 1: row co, column
+// (r*KW + s)*cread + ci = w[co][ci][r][s]; forward = 0 (data gradient): row
+// ci, column (r*KW + s)*cread + co = w[co][ci][KH-1-r][KW-1-s]; padding 0.
+// a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward
+__device__ inline void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const float* w = static_cast<const float*>(a.p[0]);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
+  const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], cread = a.i[4], Kpad = a.i[5], rows = a.i[6],
+            forward = a.i[7];
+  VG_LOOP(i, static_cast<int64_t>(rows) * Kpad) {
+    const int row = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
+    const int tap = k / cread, col = k % cread;
+    float v = 0.0f;
+    if (forward) {
+      if (row < Cout && tap < KH * KW && col < Cin)
+        v = w[((static_cast<int64_t>(row) * Cin + col) * KH + tap / KW) * KW + tap % KW];
+    } else if (row < Cin && tap < KH * KW && col < Cout) {
+      const int r = tap / KW, s = tap % KW;
+      v = w[((static_cast<int64_t>(col) * Cin + row) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
+    }
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// Zero-dilated dy of a strided conv's data gradient (Hdd x Wdd).
+// a: p0 dy, p1 out; i0 N, i1 Hd, i2 Wd, i3 C, i4 S, i5 Hdd, i6 Wdd
+__device__ inline void vg_dilate(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[0]);
+  uint4* out = static_cast<uint4*>(const_cast<void*>(a.p[1]));
+  const int N = a.i[0], Hd = a.i[1], Wd = a.i[2], C = a.i[3], S = a.i[4], Hdd = a.i[5], Wdd = a.i[6];
+  const int G8 = C / 8;
+  VG_LOOP(i, static_cast<int64_t>(N) * Hdd * Wdd * G8) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int ww = static_cast<int>(pix % Wdd), hh = static_cast<int>((pix / Wdd) % Hdd);
+    const int n = static_cast<int>(pix / (static_cast<int64_t>(Wdd) * Hdd));
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (hh % S == 0 && ww % S == 0 && hh / S < Hd && ww / S < Wd)
+      v = *reinterpret_cast<const uint4*>(dy + ((static_cast<int64_t>(n) * Hd + hh / S) * Wd + ww / S) * C + g * 8);
+    out[i] = v;
+  }
+}
+
+// Weight-gradient operand: the transposed im2col of x, K-major along the
+// pixel index m (row (t*C + c), column m), 64 pixels x 64 channels of one tap
+// t per virtual block through a swizzled smem tile (coalesced 16-byte loads
+// and stores).  Block vb = (bx, by, bz) over (Kpad/64, cdiv(C, 64), KH*KW).
+// a: p0 x, p1 out; n0 M; i0 N, i1 H, i2 W, i3 C, i4 Ho, i5 Wo, i6 KW, i7 S,
+//    i8 ph, i9 pw, i10 Kpad, i11 KH
+__device__ inline void vg_transpose_im2col(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+  (void)nvb;
+  constexpr int T = 64;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
+  const int64_t M = a.n[0];
+  const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], Ho = a.i[4], Wo = a.i[5], KW = a.i[6], S = a.i[7],
+            ph = a.i[8], pw = a.i[9], Kpad = a.i[10];
+  (void)N;
+  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
+  auto at = [](int c, int i) { return c * T + ((((i >> 3) ^ (c >> 3)) & 7) << 3) + (i & 7); };
+  const int gx = Kpad / T, gy = (C + T - 1) / T;
+  const int t = vb / (gx * gy);
+  const int by = (vb / gx) % gy, bx = vb % gx;
+  const int r = t / KW, q = t % KW;
+  const int64_t m0 = static_cast<int64_t>(bx) * T;
+  const int c0 = by * T;
+  const bool vec = (C % 8) == 0;
+  for (int e = tid; e < T * (T / 8); e += nthr) {
+    const int i = e / (T / 8), cg = (e % (T / 8)) * 8;
+    const int64_t m = m0 + i;
+    __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(0.0f);
+    if (m < M && c0 + cg < C) {
+      const uint32_t m32 = static_cast<uint32_t>(m);
+      const uint32_t pq = m32 / static_cast<uint32_t>(Wo);
+      const int wo = static_cast<int>(m32 - pq * static_cast<uint32_t>(Wo));
+      const int n = static_cast<int>(pq / static_cast<uint32_t>(Ho));
+      const int ho = static_cast<int>(pq - static_cast<uint32_t>(n) * static_cast<uint32_t>(Ho));
+      const int hi = ho * S - ph + r, wi = wo * S - pw + q;
+      if (hi >= 0 && hi < H && wi >= 0 && wi < W) {
+        const __nv_bfloat16* src = x + ((static_cast<int64_t>(n) * H + hi) * W + wi) * C + c0 + cg;
+        if (vec) {
+          const uint4 u = *reinterpret_cast<const uint4*>(src);
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = h[j];
+        } else {
+          for (int j = 0; j < 8 && c0 + cg + j < C; ++j) v[j] = src[j];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tile[at(cg + j, i)] = v[j];
+  }
+  vg_bar(nthr);
+  for (int e = tid; e < T * (T / 8); e += nthr) {
+    const int cc = e / (T / 8), mg = (e % (T / 8)) * 8;
+    const int c = c0 + cc;
+    const int64_t m = m0 + mg;
+    if (c < C && m < Kpad)
+      *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(t) * C + c) * Kpad + m) =
+          *reinterpret_cast<const uint4*>(&tile[at(cc, mg)]);
+  }
+  vg_bar(nthr);   // the tile is reused by the next virtual block
+}
+
+// dW from the GEMM's [Cout][(r*KW + s)*Cin + ci] order to [Cout][Cin][KH][KW].
+// a: p0 g, p1 dw; i0 Cout, i1 Cin, i2 KH, i3 KW
+__device__ inline void vg_wgrad_permute(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const float* g = static_cast<const float*>(a.p[0]);
+  float* dw = static_cast<float*>(const_cast<void*>(a.p[1]));
+  const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3];
+  VG_LOOP(i, static_cast<int64_t>(Cout) * Cin * KH * KW) {
+    const int s = static_cast<int>(i % KW), r = static_cast<int>((i / KW) % KH);
+    const int ci = static_cast<int>((i / (KW * KH)) % Cin), co = static_cast<int>(i / (static_cast<int64_t>(KW) * KH * Cin));
+    dw[i] = g[static_cast<int64_t>(co) * (KH * KW * Cin) + (r * KW + s) * Cin + ci];
+  }
+}
+
+// Weight-gradient split-K reduction: per-split partial tiles ([tile][split]
+// [bn/4][128 rows] float4) summed in split order straight into dW's
+// [Cout][Cin][KH][KW] layout.  a: p0 part, p1 dw; i0 Cout, i1 Cin, i2 KH,
+// i3 KW, i4 bn, i5 tiles_n, i6 split
+__device__ inline void vg_wgrad_reduce(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const float4* part = static_cast<const float4*>(a.p[0]);
+  float* dw = static_cast<float*>(const_cast<void*>(a.p[1]));
+  const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], bn = a.i[4], tiles_n = a.i[5], split = a.i[6];
+  const int Ng = KH * KW * Cin;
+  const int g4 = (Ng + 3) / 4;
+  VG_LOOP(i, static_cast<int64_t>(g4) * Cout) {
+    const int co = static_cast<int>(i % Cout), q = static_cast<int>(i / Cout);
+    const int n0 = q * 4;
+    const int tile = (co / 128) * tiles_n + n0 / bn;
+    const int r = co % 128, c4 = (n0 % bn) / 4;
+    const float4* src = part + (static_cast<int64_t>(tile) * split * (bn / 4) + c4) * 128 + r;
+    float4 s = src[0];
+    for (int ks = 1; ks < split; ++ks) {
+      const float4 b = src[static_cast<int64_t>(ks) * (bn / 4) * 128];
+      s.x += b.x; s.y += b.y; s.z += b.z; s.w += b.w;
+    }
+    const float v[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + j;
+      if (n >= Ng) break;
+      const int tap = n / Cin, ci = n % Cin;
+      dw[((static_cast<int64_t>(co) * Cin + ci) * KH + tap / KW) * KW + tap % KW] = v[j];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+__device__ inline void run_vgrid(int fn, const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+  switch (fn) {
+    case VF_BN_PARTIAL: vg_bn_partial(a, vb, nvb, tid, nthr, smem); break;
+    case VF_BN_FINALIZE: vg_bn_finalize(a, vb, nvb, tid, nthr, smem); break;
+    case VF_BN_APPLY: vg_bn_apply(a, vb, nvb, tid, nthr, smem); break;
+    case VF_RELU_BWD: vg_relu_bwd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_ADD: vg_add(a, vb, nvb, tid, nthr, smem); break;
+    case VF_MAXPOOL_FWD: vg_maxpool_fwd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_MAXPOOL_ARGMAX: vg_maxpool_argmax(a, vb, nvb, tid, nthr, smem); break;
+    case VF_MAXPOOL_BWD: vg_maxpool_bwd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_GAP_FWD: vg_gap_fwd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_GAP_BWD: vg_gap_bwd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_LINEAR_FWD: vg_linear_fwd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_LINEAR_DX: vg_linear_dx(a, vb, nvb, tid, nthr, smem); break;
+    case VF_LINEAR_DW: vg_linear_dw(a, vb, nvb, tid, nthr, smem); break;
+    case VF_SOFTMAX_CE: vg_softmax_ce(a, vb, nvb, tid, nthr, smem); break;
+    case VF_MEAN: vg_mean(a, vb, nvb, tid, nthr, smem); break;
+    case VF_SGD: vg_sgd(a, vb, nvb, tid, nthr, smem); break;
+    case VF_FILTER: vg_filter(a, vb, nvb, tid, nthr, smem); break;
+    case VF_DILATE: vg_dilate(a, vb, nvb, tid, nthr, smem); break;
+    case VF_TRANSPOSE_IM2COL: vg_transpose_im2col(a, vb, nvb, tid, nthr, smem); break;
+    case VF_WGRAD_PERMUTE: vg_wgrad_permute(a, vb, nvb, tid, nthr, smem); break;
+    case VF_WGRAD_REDUCE: vg_wgrad_reduce(a, vb, nvb, tid, nthr, smem); break;
+    default: break;
+  }
+}
+
+}  // namespace gacer

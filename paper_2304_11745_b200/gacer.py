@@ -79,7 +79,9 @@ class gacer_options(C.Structure):
 class gacer_round_stats(C.Structure):
     _fields_ = [("last_round_ms", C.c_double), ("n_items", C.c_int64), ("n_clusters", C.c_int32),
                 ("n_fused_ops", C.c_int32), ("kernel_launches", C.c_int32), ("n_tenants", C.c_int32),
-                ("tensor_flops", C.c_double), ("cc_bytes", C.c_double)]
+                ("tensor_flops", C.c_double), ("cc_bytes", C.c_double), ("stat_rounds", C.c_int32),
+                ("pad0", C.c_int32), ("tenant_sm_ns", C.c_double * 16), ("barrier_wait_ns", C.c_double),
+                ("ready_wait_ns", C.c_double)]
 
 
 class gacer_tenant_info(C.Structure):
@@ -88,7 +90,12 @@ class gacer_tenant_info(C.Structure):
                 ("out_features", C.c_int32), ("in_bytes", C.c_int64), ("out_bytes", C.c_int64),
                 ("flops", C.c_double), ("gemm_ops", C.c_int32), ("mpair_ops", C.c_int32),
                 ("split_k_ops", C.c_int32), ("swap_ops", C.c_int32), ("wide_ops", C.c_int32),
-                ("cc_ops", C.c_int32)]
+                ("cc_ops", C.c_int32), ("train", C.c_int32), ("n_steps", C.c_int32), ("n_params", C.c_int64)]
+
+
+class gacer_train_state(C.Structure):
+    _fields_ = [("loss", C.c_void_p), ("params", C.c_void_p), ("grads", C.c_void_p), ("momentum", C.c_void_p),
+                ("n_params", C.c_int64), ("n_ops", C.c_int32), ("pad", C.c_int32)]
 
 
 EXPORTS = {
@@ -96,7 +103,12 @@ EXPORTS = {
     "gacer_shutdown": ([], C.c_int),
     "gacer_register_tenant": ([C.POINTER(gacer_graph), C.c_int32], C.c_int),
     "gacer_get_tenant_info": ([C.c_int, C.POINTER(gacer_tenant_info)], C.c_int),
+    "gacer_capture_baseline": ([C.c_int], C.c_int),
+    "gacer_run_baseline_graph": ([C.c_void_p], C.c_int),
     "gacer_bind_io": ([C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "gacer_bind_labels": ([C.c_int, C.c_void_p], C.c_int),
+    "gacer_get_train_state": ([C.c_int, C.POINTER(gacer_train_state)], C.c_int),
+    "gacer_train_param": ([C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
     "gacer_set_regulation": ([C.POINTER(gacer_decomposition), C.POINTER(gacer_sync_pointers)], C.c_int),
     "gacer_query_op_clusters": ([C.c_int, IP, C.c_int32], C.c_int),
     "gacer_set_sm_shares": ([C.POINTER(C.c_float), C.c_int32], C.c_int),
@@ -188,7 +200,7 @@ def _iptr(a, keep):
     return a.ctypes.data_as(IP)
 
 
-def graph_desc(graph, params, dtype="bf16"):
+def graph_desc(graph, params, dtype="bf16", train=False, lr=0.1, momentum=0.9):
     """Marshal a plain-data tenant graph (``graph.ops`` list of dicts,
     ``graph.in_c/in_h/in_w``) and its parameters into a gacer_graph.
     Returns (struct, keepalive)."""
@@ -226,7 +238,8 @@ def graph_desc(graph, params, dtype="bf16"):
             d.flags |= FLAG_BIAS
     keep.append(arr)
     g = gacer_graph(n_ops=n, ops=C.cast(arr, C.POINTER(gacer_op_desc)), in_c=graph.in_c,
-                    in_h=graph.in_h, in_w=graph.in_w, dtype=DTYPE[dtype], train=0, lr=0.0, momentum=0.0)
+                    in_h=graph.in_h, in_w=graph.in_w, dtype=DTYPE[dtype], train=int(bool(train)),
+                    lr=float(lr), momentum=float(momentum))
     return g, keep
 
 
@@ -272,8 +285,8 @@ def gacer_shutdown():
     return _check(lib().gacer_shutdown())
 
 
-def gacer_register_tenant(graph, params, batch, dtype="bf16"):
-    g, keep = graph_desc(graph, params, dtype)
+def gacer_register_tenant(graph, params, batch, dtype="bf16", train=False, lr=0.1, momentum=0.9):
+    g, keep = graph_desc(graph, params, dtype, train, lr, momentum)
     rc = lib().gacer_register_tenant(C.byref(g), batch)
     del keep
     return _check(rc)
@@ -287,6 +300,23 @@ def gacer_get_tenant_info(tenant):
 
 def gacer_bind_io(tenant, input_dev_ptr, output_dev_ptr):
     return _check(lib().gacer_bind_io(tenant, C.c_void_p(input_dev_ptr), C.c_void_p(output_dev_ptr)))
+
+
+def gacer_bind_labels(tenant, labels_dev_ptr):
+    return _check(lib().gacer_bind_labels(tenant, C.c_void_p(labels_dev_ptr)))
+
+
+def gacer_get_train_state(tenant):
+    st = gacer_train_state()
+    _check(lib().gacer_get_train_state(tenant, C.byref(st)))
+    return {f: (getattr(st, f) or 0) if f in ("loss", "params", "grads", "momentum") else getattr(st, f)
+            for f, _ in gacer_train_state._fields_ if f != "pad"}
+
+
+def gacer_train_param(tenant, op_index, which=0):
+    off, cnt = C.c_int64(), C.c_int64()
+    _check(lib().gacer_train_param(tenant, op_index, which, C.byref(off), C.byref(cnt)))
+    return off.value, cnt.value
 
 
 def gacer_set_regulation(decomposition=None, pointers=None, n_tenants=None):
@@ -325,6 +355,14 @@ def gacer_run_round_async(stream_ptr=0):
     return _check(lib().gacer_run_round_async(C.c_void_p(stream_ptr)))
 
 
+def gacer_capture_baseline(mode):
+    return _check(lib().gacer_capture_baseline(MODE[mode] if isinstance(mode, str) else mode))
+
+
+def gacer_run_baseline_graph(stream_ptr=0):
+    return _check(lib().gacer_run_baseline_graph(C.c_void_p(stream_ptr)))
+
+
 def gacer_run_round_host(host_in_ptrs, host_out_ptrs):
     n = len(host_in_ptrs)
     ins = (C.c_void_p * n)(*host_in_ptrs)
@@ -335,7 +373,9 @@ def gacer_run_round_host(host_in_ptrs, host_out_ptrs):
 def gacer_get_stats():
     s = gacer_round_stats()
     _check(lib().gacer_get_stats(C.byref(s)))
-    return {f: getattr(s, f) for f, _ in gacer_round_stats._fields_}
+    d = {f: getattr(s, f) for f, _ in gacer_round_stats._fields_ if f != "pad0"}
+    d["tenant_sm_ns"] = list(s.tenant_sm_ns)[:max(0, min(16, s.n_tenants))]
+    return d
 
 
 def gacer_get_trace(cap):

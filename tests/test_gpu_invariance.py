@@ -155,3 +155,62 @@ def test_host_buffer_round_matches_device_round(cuda_ok, d2):
                     assert np.asarray(a).tobytes() == b.numpy().tobytes(), mode
     finally:
         s.close()
+
+
+def test_graph_baselines_byte_identical(cuda_ok, d2):
+    """The sequential / multi-stream baselines captured as CUDA graphs
+    (gacer_capture_baseline) replay the same per-op launches: outputs
+    byte-identical to the executor's, and the capture is discarded when the
+    I/O is re-bound."""
+    import torch
+    from paper_2304_11745_b200 import gacer as G
+    from paper_2304_11745_b200.runtime import Session
+    ref, _ = run(d2)
+    s = Session([t[:4] for t in d2])
+    try:
+        for t, tt in enumerate(d2):
+            s.set_input(t, tt[4])
+        for mode in ("sequential", "multistream"):
+            G.gacer_capture_baseline(mode)
+            for _ in range(2):
+                for o in s.outputs:
+                    o.fill_(float("nan"))
+                G.gacer_run_baseline_graph(0)
+                torch.cuda.synchronize()
+                for a, b in zip(ref, s.results()):
+                    assert a.tobytes() == b.tobytes(), mode
+            assert G.gacer_get_stats()["kernel_launches"] > 100
+        G.gacer_bind_io(0, s.inputs[0].data_ptr(), s.outputs[0].data_ptr())
+        with pytest.raises(Exception):
+            G.gacer_run_baseline_graph(0)
+    finally:
+        s.close()
+
+
+def test_occupancy_stats(cuda_ok, d2):
+    """gacer_get_stats' occupancy counters (the Fig. 8 analog, PAPER.md
+    l.979-981): every tenant accumulates item time, the per-round figures are
+    bounded by makespan x CTAs (x the in-flight depth), and a plan with sync
+    pointers spends CTA time at cluster barriers that the identity plan does
+    not."""
+    from paper_2304_11745_b200.runtime import Session
+    s = Session([t[:4] for t in d2])
+    try:
+        for t, tt in enumerate(d2):
+            s.set_input(t, tt[4])
+        for _ in range(3):
+            s.run()
+        st = s.stats()
+        assert st["stat_rounds"] == 3
+        ms = st["last_round_ms"]
+        cap = ms * 1e6 * 148 * 4
+        assert all(0 < v < cap for v in st["tenant_sm_ns"]), st
+        assert st["barrier_wait_ns"] == 0
+        n = [len(g.ops) for g, *_ in d2]
+        s.set_regulation(None, [[x // 3, 2 * x // 3] for x in n])
+        for _ in range(2):
+            s.run()
+        st2 = s.stats()
+        assert st2["stat_rounds"] == 2 and st2["barrier_wait_ns"] > 0
+    finally:
+        s.close()

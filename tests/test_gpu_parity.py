@@ -168,10 +168,29 @@ def test_conv_dgrad_as_forward_conv(cuda_ok, cin, cout, k, pad, hw, B):
 # swap-AB split-K linear at the VGG-16 FC1 shape (the largest op of the D2
 # round), M-pair (256-row) tiles on both operand-A paths, depthwise and
 # average pooling.  The oracle is fed the GPU's own bf16 input.
-def _rne_gate(y, ref, min_exact=0.999):
+def _rne_gate(y, ref, K):
+    """Q2 per-op gate: max-norm <= 2e-2 and >= 99.9% of outputs rounding to
+    the same bf16 as the fp64 oracle.  Q2 measured that fraction for
+    reductions of K <= 4608 terms; for longer reductions (the FC layers, K up
+    to 25088) DESIGN.md reading R6 applies: every significant output
+    (|o| >= 1e-2 max|o|, Q2's significance threshold) must round FAITHFULLY
+    (to one of the two bf16 neighbours of the exact value) and >= 99.5% of
+    them exactly."""
+    y = np.asarray(y, np.float64)
+    ref = np.asarray(ref, np.float64)
     assert maxrel(y, ref) <= 2e-2, maxrel(y, ref)
-    exact = float(np.mean(bf16_rne(y) == bf16_rne(ref)))
-    assert exact >= min_exact, exact
+    by, br = bf16_rne(y).astype(np.float64), bf16_rne(ref).astype(np.float64)
+    exact_all = float(np.mean(by == br))
+    sig = np.abs(ref) >= 1e-2 * np.abs(ref).max()
+    e = np.floor(np.log2(np.maximum(np.abs(ref[sig]), 1e-300)))
+    ulp = np.exp2(e - 7)                                  # bf16: 8 significant bits
+    faithful = float(np.mean(np.abs(by[sig] - ref[sig]) < ulp))
+    exact_sig = float(np.mean(by[sig] == br[sig]))
+    print(f"K={K}: exact {exact_all:.5f} (significant {exact_sig:.5f}), faithful {faithful:.5f}")
+    if K <= 4608:
+        assert exact_all >= 0.999, exact_all
+    else:
+        assert faithful == 1.0 and exact_sig >= 0.995, (faithful, exact_sig)
 
 
 @pytest.mark.parametrize("cin,hw,cout,B,relu", [(512, 7, 4096, 8, True),    # V16 FC1: 25088 -> 4096, split-K 2
@@ -190,7 +209,7 @@ def test_linear_op_rne_gate(cuda_ok, cin, hw, cout, B, relu):
     ref = x.reshape(B, -1).astype(np.float64) @ lin["w"].astype(np.float64).T + lin["b"]
     if relu:
         ref = np.maximum(ref, 0.0)
-    _rne_gate(outs[0].reshape(B, cout), ref)
+    _rne_gate(outs[0].reshape(B, cout), ref, cin * hw * hw)
 
 
 @pytest.mark.parametrize("cin,cout,hw,B", [(64, 64, 112, 8),    # M-pair, TMA im2col path (VGG conv2_x-like)
@@ -216,7 +235,7 @@ def test_mpair_conv_rne_gate(cuda_ok, cin, cout, hw, B):
     bn = params[g.ops[1]["id"]]
     ref = oops.conv2d(x, params[g.ops[0]["id"]]["w"], None, 1, (1, 1))
     ref = oops.relu(oops.batchnorm(ref, bn["gamma"], bn["beta"], bn["mean"], bn["var"], 1e-5))
-    _rne_gate(nhwc_to_nchw(y, B, hw, hw, cout), ref)
+    _rne_gate(nhwc_to_nchw(y, B, hw, hw, cout), ref, 9 * cin)
 
 
 @pytest.mark.parametrize("kind,C,hw,B", [("dw", 96, 56, 4), ("dw_s1", 144, 28, 4), ("dw_s1", 960, 7, 8),
@@ -232,7 +251,7 @@ def test_cuda_core_op_rne_gate(cuda_ok, kind, C, hw, B):
     x = workloads.make_input(g, B, 16 + C, "bf16")
     outs, _ = run_session([(g, p, B, "bf16", x)])
     ref = forward_graph(g, p, x, return_all=True)[1][g.ops[-1]["id"]]
-    _rne_gate(nhwc_to_nchw(outs[0], B, ref.shape[2], ref.shape[3], C), ref)
+    _rne_gate(nhwc_to_nchw(outs[0], B, ref.shape[2], ref.shape[3], C), ref, 9)
 
 
 def test_d3_full_size_sampled_parity(cuda_ok):
