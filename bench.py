@@ -408,6 +408,147 @@ def run_gacer(args, rank, world, dist):
     sess.close()
 
 
+def run_d4(args, rank, world, dist):
+    """D4 (BASELINE.json configs[3]): ResNet-50 TRAINING (B=64, one SGD step
+    per round: forward, softmax-CE, backward, SGD-momentum update) co-located
+    with VGG-16 + MobileNetV2 inference (B=8 each) in ONE executor round.
+    Reports the inference aggregate (value) and the training images/s of the
+    same rounds, against the sequential and multi-stream baselines of the
+    same operators (plain and CUDA-graphed) and each side alone."""
+    import torch
+    import workloads
+    from workloads.zoo import CONFIG_INDEX, TRAIN_CONFIGS
+    from paper_2304_11745_b200 import gacer as G
+    from paper_2304_11745_b200.placement import max_over_ranks, replica_seed
+    from paper_2304_11745_b200.runtime import Session
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    spec = TRAIN_CONFIGS["d4_mixed"]
+    ts = []
+    for i, (name, B, dt, train) in enumerate(spec):
+        g = workloads.build_model(name)
+        seed = workloads.tenant_seed(CONFIG_INDEX["d4_mixed"], i)
+        ts.append((name, g, workloads.make_params(g, seed, "fp32" if train else dt), B, dt,
+                   workloads.make_input(g, B, replica_seed(seed, rank), dt), train,
+                   workloads.make_labels(B, replica_seed(seed, rank)) if train else None))
+    stream = torch.cuda.Stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
+    torch.cuda.set_stream(stream)
+
+    def session(sel):
+        s = Session([(g, p, B, dt, {"train": True}) if tr else (g, p, B, dt)
+                     for j, (_, g, p, B, dt, _, tr, _) in enumerate(ts) if j in sel], device=dev)
+        for k, j in enumerate(sel):
+            s.set_input(k, ts[j][5])
+            if ts[j][6]:
+                s.set_labels(k, ts[j][7])
+        return s
+
+    n_inf = sum(B for _, _, _, B, _, _, tr, _ in ts if not tr)
+    n_train = sum(B for _, _, _, B, _, _, tr, _ in ts if tr)
+    res = {}
+    # ---- each side alone (context)
+    for label, sel in (("train_alone", [0]), ("inference_alone", [1, 2])):
+        s = session(sel)
+        res[label] = float(np.median(time_mode(G, s, torch, stream, "executor", max(3, args.steps // 2),
+                                               args.warmup, flush)))
+        s.close()
+    # ---- the mixed round: plans (SM partition / shares), then the timed run
+    s = session([0, 1, 2])
+    st = G.gacer_get_stats()
+    plans = {"priority": ("priority", None), "hybrid": ("hybrid", None),
+             "work_conserving": ("work_conserving", None), "strict[.7,.2,.1]": ("strict", [0.7, 0.2, 0.1])}
+    plan_ms = {}
+    for name, (part, sh) in plans.items():
+        G.gacer_set_partition(part)
+        G.gacer_set_sm_shares(sh)
+        plan_ms[name] = float(np.median(time_mode(G, s, torch, stream, "executor", 3, 2, flush)))
+    best = min(plan_ms, key=plan_ms.get)
+    G.gacer_set_partition(plans[best][0])
+    G.gacer_set_sm_shares(plans[best][1])
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        times = time_mode(G, s, torch, stream, "executor", args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    total_ms = max_over_ranks(float(np.sum(times)), dist, f"cuda:{dev}")
+    ms_step = total_ms / args.steps
+    occ = G.gacer_get_stats()
+    base = {}
+    for mode in ("sequential", "multistream", "sequential_graph", "multistream_graph"):
+        tm = time_mode(G, s, torch, stream, mode, max(3, args.steps // 2), args.warmup, flush)
+        m = max_over_ranks(float(np.mean(tm)), dist, f"cuda:{dev}")
+        base[mode] = {"ms_per_round": m, "inferences_per_s": world * n_inf / (m / 1000.0),
+                      "train_images_per_s": world * n_train / (m / 1000.0),
+                      "kernel_launches_per_round": G.gacer_get_stats()["kernel_launches"]}
+    s.set_mode("executor")
+    # ---- e2e: host buffers (images of all three tenants copied in, logits out)
+    host_in = [s.host_input(t, ts[j][5]) for t, j in enumerate([0, 1, 2])]
+    host_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in s.outputs]
+    for _ in range(args.warmup):
+        G.gacer_run_round_host([h.data_ptr() for h in host_in], [h.data_ptr() for h in host_out])
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        G.gacer_run_round_host([h.data_ptr() for h in host_in], [h.data_ptr() for h in host_out])
+        e2e_ms.append(G.gacer_get_stats()["last_round_ms"])
+    e2e_total = max_over_ranks(float(np.sum(e2e_ms)), dist, f"cuda:{dev}")
+    loss = float(s.train_state(0)[0].item())
+    if rank == 0:
+        peaks, src = load_peaks()
+        # algorithmic training FLOPs: forward + data gradient + weight
+        # gradient = 3 x the forward conv+FC FLOPs (SURVEY §8(a) A11)
+        g50 = ts[0][1]
+        G.gacer_init(-1)
+        fwd = G.gacer_get_tenant_info(G.gacer_register_tenant(g50, ts[0][2], n_train, "bf16"))["flops"]
+        G.gacer_shutdown()
+        flops = 3.0 * fwd + sum(i["flops"] for i in s.info[1:])
+        achieved = flops / (ms_step / 1000.0) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        line = {
+            "metric": METRIC, "value": world * n_inf * args.steps / (total_ms / 1000.0), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded inputs and labels, random-init weights)",
+            "config": {"workload": "d4_mixed", "tenants": ["resnet50(train, B=64)", "vgg16(B=8)",
+                                                           "mobilenet_v2(B=8)"],
+                       "image": 224, "plan": best, "mode": "executor",
+                       "parallelism": f"replica-per-gpu x{world}",
+                       "l2": "flushed between steps (256 MB write, outside the events)"},
+            "train_images_per_s": world * n_train * args.steps / (total_ms / 1000.0),
+            "train_loss_last": loss,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "gacer_executor_train",
+                         "algorithmic": f"{flops / 1e9:.1f} GFLOP per round: 3 x ResNet-50 forward (B=64) "
+                                        f"+ VGG-16 and MobileNetV2 forward (B=8)",
+                         "peak_source": f"{src} bf16_tflops_sustained (seconds-long step)"},
+            "e2e": {"value": world * n_inf * args.steps / (e2e_total / 1000.0), "unit": UNIT,
+                    "h2d_bytes_per_step": int(sum(i["in_bytes"] for i in s.info)),
+                    "d2h_bytes_per_step": int(sum(i["out_bytes"] for i in s.info))},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "plans_ms": plan_ms,
+            "alone_ms": res,
+            "baselines": base,
+            "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
+            "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,
+            "speedup_vs_sequential_graph": base["sequential_graph"]["ms_per_round"] / ms_step,
+            "speedup_vs_multistream_graph": base["multistream_graph"]["ms_per_round"] / ms_step,
+            "speedup_vs_alone_sum": (res["train_alone"] + res["inference_alone"]) / ms_step,
+            "occupancy_sm_ms": [v / 1e6 for v in occ["tenant_sm_ns"]],
+            "makespan_ms": {"p10": float(np.percentile(times, 10)), "p50": float(np.median(times)),
+                            "p90": float(np.percentile(times, 90))},
+            "n_items_per_round": st["n_items"],
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -415,7 +556,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gacer", choices=["gacer", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default=CONFIG, choices=["d1_tiny", "d2_r50_v16_mv2", "d3_five"])
+    ap.add_argument("--config", default=CONFIG, choices=["d1_tiny", "d2_r50_v16_mv2", "d3_five", "d4_mixed"])
     ap.add_argument("--plan", default="sweep", choices=["identity", "sweep"])
     ap.add_argument("--no-search", action="store_true", help="skip the Algorithm 1 plan search")
     ap.add_argument("--search-evals", type=int, default=30)
@@ -434,6 +575,8 @@ def main():
         dist = dist_mod
     if args.impl == "reference":
         run_reference(args, rank)
+    elif args.config == "d4_mixed":
+        run_d4(args, rank, world, dist)
     else:
         run_gacer(args, rank, world, dist)
     if dist:

@@ -347,6 +347,11 @@ int gacer_get_trace(int64_t* records, int32_t cap);
 
 const char* gacer_last_error(void);
 
+/* Diagnostics: describe lowered op `op` of the global op table (the op field
+ * of gacer_get_trace records): out[6] = {device kind, virtual-grid function,
+ * items per round, tenant, GEMM tile N, K-blocks}. */
+int gacer_describe_op(int32_t op, int32_t* out);
+
 /* Diagnostics only (not on the method's path): when the process runs with
  * GACER_DEBUG_TIMING=1, kernels record %globaltimer milestones per CTA
  * ([op slot][cta][16] int64; executor rounds use slot 0).  Copies up to cap

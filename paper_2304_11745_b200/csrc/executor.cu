@@ -344,7 +344,13 @@ constexpr bool EPI_STAGED = NEPI == 128;
 #ifndef GACER_EPI_DB
 #define GACER_EPI_DB 1
 #endif
-constexpr bool EPI_DB = GACER_EPI_DB != 0;              // double-buffered staging (needs the smem of a ring stage)
+constexpr bool EPI_DB = GACER_EPI_DB != 0;
+// lean staged epilogue variant: 0 = 32-column steps, scale/bias by warp
+// shuffles; 1 = software-pipelined 16-column TMEM loads, scale/bias as
+// 16-byte smem broadcasts
+#ifndef GACER_EPI_V
+#define GACER_EPI_V 0
+#endif              // double-buffered staging (needs the smem of a ring stage)
 constexpr int SMEM_STAGE_BYTES = EPI_STAGED ? (NEPI / 32) * STAGE_WARP_BYTES * (EPI_DB ? 2 : 1) : 0;
 constexpr int SMEM_BYTES = SMEM_RING_BYTES + SMEM_STAGE_BYTES + 1024 /*align slack*/;
 // The control block is a static __shared__ object (not carved from the
@@ -1629,6 +1635,79 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
         p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
     } else if (split == 1 && staged && !op.out_f32) {
+#if GACER_EPI_V == 0
+      // lean staged bf16 path: branch-free activation clamp, 64-column
+      // staging chunks (a compile-time constant), scale/bias by shuffle
+      const float lo = op.act == ACT_NONE ? -INFINITY : 0.0f;
+      const float hi = op.act == ACT_RELU6 ? 6.0f : INFINITY;
+      const bool skip = do_skip;
+      const int row0 = m0 + q * 32;
+      for (int c = c_lo; c < c_hi; c += 32) {
+        uint32_t r[32];
+        tmem_ld16_nw(taddr + c, r);
+        tmem_ld16_nw(taddr + c + 16, r + 16);   // c + 32 <= BN_MAX: columns past c_hi are never stored
+        const float sc_l = ctl->epi_scale[c + lane], bi_l = ctl->epi_bias[c + lane];
+        if (skip) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cc = c + 32 + u * 8;
+            skB[u] = (cc < c_hi && cc < cout_left) ? *reinterpret_cast<const uint4*>(skrow + cc) : make_uint4(0, 0, 0, 0);
+          }
+        }
+        const int cin = (c - c_lo) & 63;
+        // staging buffer of this 64-column chunk (EPI_DB: two per warp, the
+        // store of one chunk overlaps the conversion of the next)
+        const uint32_t sbuf = wbuf_s + (EPI_DB ? (((c - c_lo) >> 6) & 1) * STAGE_WARP_BYTES : 0);
+        if (cin == 0 && c > c_lo) {            // a new chunk: its buffer's previous store must have been read
+          if (lane == 0) {
+            if (EPI_DB) bulk_wait_read1();
+            else bulk_wait_read0();
+          }
+          __syncwarp();
+        }
+        tmem_wait();
+#pragma unroll
+        for (int g8 = 0; g8 < 4; ++g8) {
+          float y[8];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const int jj = g8 * 8 + j;
+            const float2 o = __ffma2_rn(make_float2(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1])),
+                                        make_float2(__shfl_sync(0xffffffffu, sc_l, jj), __shfl_sync(0xffffffffu, sc_l, jj + 1)),
+                                        make_float2(__shfl_sync(0xffffffffu, bi_l, jj), __shfl_sync(0xffffffffu, bi_l, jj + 1)));
+            y[j] = o.x;
+            y[j + 1] = o.y;
+          }
+          if (skip) {
+            float sv[8];
+            bf16x8_to_f32(skA[g8], sv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] += sv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], lo), hi);
+          const uint32_t ch = static_cast<uint32_t>((cin + g8 * 8) >> 3);   // 16-byte chunk of the 128-byte row
+          sts128(sbuf + lane * 128 + ((ch ^ (lane & 7)) << 4), pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+                 pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+        }
+        if (cin == 32 || c + 32 >= c_hi) {     // 64-column chunk complete: TMA-store it
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(op.tmap_c, sbuf, n0 + c - cin, row0);
+            bulk_commit();
+          }
+        }
+        if (skip) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) skA[u] = skB[u];
+        }
+      }
+      if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
+        p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
+      if (lane == 0) bulk_wait0();        // stores complete before the item is released
+      __syncwarp();
+#else
       // lean staged bf16 path, software-pipelined over 64-column steps: the
       // TMEM load of the second 32 columns is in flight while the first are
       // converted (and the next step's first 32 while the second are);
@@ -1681,6 +1760,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
         p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
       if (lane == 0) bulk_wait0();        // stores complete before the item is released
       __syncwarp();
+#endif
     } else if (split == 1) {
       for (int c = c_lo; c < c_hi; c += 32) {
         uint32_t r[32];

@@ -1565,7 +1565,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.segs = S.d_segs;
     p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
     p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
-    p.error = S.d_error; p.trace = S.d_trace; p.stats = S.d_stats;
+    p.error = S.d_error; p.trace = S.d_trace; p.stats = env_flag("GACER_NO_STATS") ? nullptr : S.d_stats;
     p.n_tenants = static_cast<int>(S.tenants.size());
     p.n_clusters = S.plan.n_clusters;
     p.epoch = ++S.epoch;
@@ -1595,7 +1595,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.ops = S.d_ops; p.items = S.d_items; p.deps = S.d_deps; p.segs = S.d_segs;
     p.cta_pref = S.d_pref; p.heads = S.d_heads; p.chunk_done = S.d_chunk_done;
     p.cluster_done = S.d_cluster_done; p.cluster_total = S.d_cluster_total; p.exit_count = S.d_exit;
-    p.error = S.d_error; p.trace = S.d_trace; p.stats = S.d_stats;
+    p.error = S.d_error; p.trace = S.d_trace; p.stats = env_flag("GACER_NO_STATS") ? nullptr : S.d_stats;
     p.n_tenants = static_cast<int>(S.tenants.size());
     p.n_clusters = S.plan.n_clusters;
     p.epoch = ++S.epoch;
@@ -2112,6 +2112,22 @@ int gacer_get_trace(int64_t* records, int32_t cap) {
 }
 
 const char* gacer_last_error(void) { return g_err.c_str(); }
+
+// Diagnostics: the lowered op `op` of the global op table (the trace's op
+// field): out[0] = device kind (DK_*), [1] = virtual-grid function (VF_*),
+// [2] = items per round, [3] = tenant, [4] = GEMM tile N, [5] = K-blocks.
+int gacer_describe_op(int32_t op, int32_t* out) {
+  if (!S.inited || !out || op < 0 || op >= static_cast<int>(S.h_ops.size()))
+    return set_err(GACER_E_INVALID_ARG, "bad op index %d", op);
+  const OpDev& d = S.h_ops[op];
+  out[0] = d.kind;
+  out[1] = d.vfn;
+  out[2] = d.tiles_m * d.tiles_n * (d.kind == DK_GEMM ? d.split_k : 1);
+  out[3] = d.tenant;
+  out[4] = d.bn;
+  out[5] = d.nkb;
+  return GACER_OK;
+}
 
 // Diagnostics (not part of the method): GACER_DEBUG_TIMING=1 milestones.
 int gacer_debug_timing(int64_t* out, int64_t cap, int reset) {

@@ -120,6 +120,7 @@ EXPORTS = {
     "gacer_get_stats": ([C.POINTER(gacer_round_stats)], C.c_int),
     "gacer_get_trace": ([C.POINTER(C.c_int64), C.c_int32], C.c_int),
     "gacer_last_error": ([], C.c_char_p),
+    "gacer_describe_op": ([C.c_int32, IP], C.c_int),
     "gacer_debug_timing": ([C.POINTER(C.c_int64), C.c_int64, C.c_int], C.c_int),
     # include/gacer_train.h: training-tenant CUDA-core steps (device pointers as ints, stream as int)
     "gacer_bn_partials": ([C.c_int64, C.c_int32], C.c_int32),
@@ -382,6 +383,12 @@ def gacer_get_trace(cap):
     buf = np.zeros((cap, 12), dtype=np.int64)
     n = _check(lib().gacer_get_trace(buf.ctypes.data_as(C.POINTER(C.c_int64)), cap))
     return buf[:n]
+
+
+def gacer_describe_op(op):
+    out = np.zeros(6, dtype=np.int32)
+    _check(lib().gacer_describe_op(op, out.ctypes.data_as(IP)))
+    return dict(zip(("kind", "vfn", "items", "tenant", "bn", "nkb"), out.tolist()))
 
 
 def gacer_last_error():

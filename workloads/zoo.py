@@ -350,7 +350,15 @@ CONFIGS: Dict[str, list] = {
                 ("resnet101", 16, "bf16"), ("inception_v3", 16, "bf16"),
                 ("mobilenet_v2", 16, "bf16")],
 }
-CONFIG_INDEX = {"d1_tiny": 1, "d2_r50_v16_mv2": 2, "d3_five": 3}
+CONFIG_INDEX = {"d1_tiny": 1, "d2_r50_v16_mv2": 2, "d3_five": 3, "d4_mixed": 4}
+# BASELINE.json configs[3] (D4): ResNet-50 TRAINING (batch 64; one SGD step per
+# round) co-located with MobileNetV2 + VGG-16 inference (batch 8, SURVEY §8(d)
+# D4: the inference batch is unstated in BASELINE, 8 as in D2).  Entries:
+# (model, batch, dtype, train)
+TRAIN_CONFIGS: Dict[str, list] = {
+    "d4_mixed": [("resnet50", 64, "bf16", True), ("vgg16", 8, "bf16", False),
+                 ("mobilenet_v2", 8, "bf16", False)],
+}
 
 
 def config_tenants(cfg: str):
