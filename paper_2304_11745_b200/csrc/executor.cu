@@ -1057,8 +1057,10 @@ __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& 
   const uint64_t t0 = globaltimer();
   uint32_t it = 0, ns = 32;
   while (ld_relaxed(ctr) < target) {
-    __nanosleep(ns);              // exponential backoff: 148 CTAs poll a few hot lines
-    ns = ns < 512 ? ns * 2 : 512;
+    if (it >= 8) {                // a few back-to-back polls first (the release is often imminent),
+      __nanosleep(ns);            // then exponential backoff: 148 CTAs poll a few hot lines
+      ns = ns < 512 ? ns * 2 : 512;
+    }
     if ((++it & 63) == 0) {
       if (*reinterpret_cast<volatile int32_t*>(p.error)) return false;
       if (static_cast<int64_t>(globaltimer() - t0) > p.watchdog_ns) {
@@ -1114,13 +1116,16 @@ __device__ __forceinline__ Seg get_seg(const ExecParams& p, const SmemCtl* ctl, 
 // the others fill its residue (l.447-453).  Unready heads are never claimed,
 // which keeps the wait-for graph acyclic.
 // Returns 1 (candidate in si/h/cand), 0 (unclaimed work, none ready),
-// 2 (every item of cluster k claimed).
+// 2 (every item of cluster k claimed), 3 (claim-ahead: no ready head, the
+// best unready head in si/h/cand).
 __device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& best_si, uint32_t& best_h,
                           Item& cand) {
   const int32_t* pref = p.cta_pref + static_cast<size_t>(blockIdx.x) * p.n_tenants;
   bool unclaimed = false;
   best_si = -1;
   uint32_t best_prio = 0;
+  int u_si = -1;
+  uint32_t u_h = 0, u_prio = 0;
   for (int j = 0; j < p.n_tenants; ++j) {
     const int t = pref[j];
     if (t < 0) break;
@@ -1134,14 +1139,24 @@ __device__ int scan_ready(const ExecParams& p, const SmemCtl* ctl, int k, int& b
     const uint32_t prio = ip->prio;
     if (best_si >= 0 && prio <= best_prio) continue;
     const Item c = *ip;
-    if (!deps_ready(p, c)) continue;
+    if (!deps_ready(p, c)) {
+      if (p.claim_ahead && (u_si < 0 || prio > u_prio)) { u_si = si; u_h = h; u_prio = prio; }
+      continue;
+    }
     best_si = si;
     best_h = h;
     best_prio = prio;
     cand = c;
     if (j == 0 && p.own_first) return 1;  // the CTA's own tenant (SM partition) comes first
   }
-  return best_si >= 0 ? 1 : (unclaimed ? 0 : 2);
+  if (best_si >= 0) return 1;
+  if (u_si >= 0) {
+    best_si = u_si;
+    best_h = u_h;
+    cand = p.items[get_seg(p, ctl, u_si).begin + u_h];
+    return 3;
+  }
+  return unclaimed ? 0 : 2;
 }
 
 __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it, uint64_t t0, const OpDev& op) {
@@ -1255,9 +1270,14 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
           continue;
         }
         const int G1 = static_cast<int>(gridDim.x);
+        // claim-ahead (st == 3): only once this CTA's ring is drained (the
+        // CTA would otherwise idle); the dependency wait below then overlaps
+        // the producers' tails instead of following them
         const uint32_t allowed =
-            (cand.op != last_op) ? static_cast<uint32_t>(GACER_NEWOP_DEPTH) : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
-                                                            : (cand.op_left > G1 ? 2u : 1u));
+            st == 3 ? 1u
+                    : (cand.op != last_op) ? static_cast<uint32_t>(GACER_NEWOP_DEPTH)
+                                           : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
+                                                                 : (cand.op_left > G1 ? 2u : 1u));
         sdbg(p, islot, 5, static_cast<int64_t>(allowed) * 1000 + (islot - consumed));
         while (islot - consumed >= allowed) {
           mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
@@ -1272,7 +1292,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         const uint32_t got = min(want, static_cast<uint32_t>(sg.size) - idx);
         bool abort = false;
         for (uint32_t j = 0; j < got; ++j) {
-          if (idx == h && j == 0) {
+          if (idx == h && j == 0 && st != 3) {
             its[j] = cand;
           } else {
             // a later item than the one checked: its dependencies are items

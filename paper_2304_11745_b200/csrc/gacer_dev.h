@@ -43,6 +43,26 @@ inline int vg_grid_for(int64_t work) {        // grid-stride ops: blocks for `wo
   return static_cast<int>(b < cap ? (b < 1 ? 1 : b) : cap);
 }
 
+// BN apply: a grid whose thread stride (blocks x VG_THREADS) is a multiple of
+// C / 8 for every C / 8 dividing 768 (C <= 2048: a multiple of 4 blocks), so
+// each thread keeps one channel group
+inline int vg_apply_blocks(int64_t work) { return (vg_grid_for(work) + 3) / 4 * 4; }
+
+// Weight-gradient operand transpose tiles: TC channels x (16384 / TC) pixels
+// (narrow inputs, e.g. the 8-channel stem image, take long pixel runs)
+#ifdef __CUDACC__
+#define GACER_HD __host__ __device__
+#else
+#define GACER_HD
+#endif
+GACER_HD inline int vg_transpose_tc(int C) { int c = (C + 7) / 8 * 8; return c < 64 ? c : 64; }
+constexpr int VG_TRANSPOSE_TILE = 16384;       // elements per transpose tile (32 KB of smem)
+GACER_HD inline int vg_transpose_blocks(int C, int KH, int KW, int Kpad) {
+  const int tc = vg_transpose_tc(C), tp = VG_TRANSPOSE_TILE / tc;
+  return ((Kpad + tp - 1) / tp) * ((C + tc - 1) / tc) * KH * KW;
+}
+constexpr int VG_MAX_BN_C = 2048;             // BN channels (per-channel constants staged in smem)
+
 // Arguments of a virtual-grid operator: pointers, 64-bit sizes, ints, floats.
 struct VArgs {
   const void* p[8];
@@ -191,6 +211,8 @@ struct ExecParams {
   int32_t own_first;        // 1: the CTA's own tenant (pref[0]) wins over higher-ranked items
   int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
   int64_t dbg_spin;         // diagnostics: epilogue delay (clocks) between tfull and the TMEM read
+  int32_t claim_ahead;      // 1: with no ready item, claim the best unready head and wait on its deps
+  int32_t pad_ca;
   unsigned long long* stats;// [STAT_TENANTS + 2] accumulating ns: per-tenant item time (claim -> release),
                             // then CTA time at cluster barriers, then CTA time with only unready work
 };

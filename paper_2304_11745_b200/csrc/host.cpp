@@ -69,6 +69,12 @@ int set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
 namespace {
 
 // diagnostic switches: set and non-empty
+static bool env_flag(const char* name);
+// claim-ahead scheduling (executor.cu scan_ready): GACER_CLAIM_AHEAD=0/1 overrides the default
+static bool claim_ahead_enabled() {
+  const char* e = getenv("GACER_CLAIM_AHEAD");
+  return e ? e[0] == '1' : true;
+}
 static bool env_flag(const char* name) {
   const char* v = getenv(name);
   return v && v[0] && v[0] != '0';
@@ -1574,6 +1580,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
+    p.claim_ahead = claim_ahead_enabled();
     p.dbg = S.d_dbg;
     if (const char* e = getenv("GACER_DBG_SPIN")) p.dbg_spin = atoll(e);
     p.k_first = 0;
@@ -1604,6 +1611,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.watchdog_ns = static_cast<int64_t>(S.opts.watchdog_ms > 0 ? S.opts.watchdog_ms : 2000) * 1000000LL;
     p.single_op = -1;
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
+    p.claim_ahead = claim_ahead_enabled();
     p.gate0 = S.plan.input_counter0;
     p.n_gates = static_cast<int32_t>(S.tenants.size());
     bool first = true;
@@ -2613,8 +2621,9 @@ struct TrainLowering {
     }
     op.step_pos = step;
     if (op.kind == DK_VGRID) {
-      // items: about two waves of the SMs' worth of virtual-block ranges
-      op.per = std::max(1, cdiv(op.vblocks, 2 * kSplitSms));
+      // items: one wave of the SMs' worth of virtual-block ranges (streaming
+      // operators: per-item claim/release overhead amortised)
+      op.per = std::max(1, cdiv(op.vblocks, kSplitSms));
       op.items = cdiv(op.vblocks, op.per);
     } else {
       op.items = op.gd.tiles_m * op.gd.tiles_n * op.gd.split_k;
@@ -2674,7 +2683,11 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
           return set_err(GACER_E_UNSUPPORTED_OP, "op %d: training FC needs a [B][c_in] (1x1) input", o.id);
         shp[i] = {1, 1, o.c_out};
         break;
-      case GACER_OP_BN: case GACER_OP_FLATTEN: case GACER_OP_DROPOUT: case GACER_OP_RELU: case GACER_OP_ADD:
+      case GACER_OP_BN:
+        if (x.c > VG_MAX_BN_C) return set_err(GACER_E_UNSUPPORTED_OP, "op %d: training BN over > 2048 channels", o.id);
+        shp[i] = x;
+        break;
+      case GACER_OP_FLATTEN: case GACER_OP_DROPOUT: case GACER_OP_RELU: case GACER_OP_ADD:
         shp[i] = x;
         break;
       default:
@@ -2802,7 +2815,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         f.vp[6] = bref(var); f.vp[7] = coef;
         f.va.n[0] = M; f.va.i[0] = 0; f.va.i[1] = C; f.va.i[2] = P; f.va.f[0] = o.bn_eps;
         L.add(std::move(f), {part, T.buf_params, xb}, {mean, var, part});
-        TrainOp e = TrainLowering::vg(VF_BN_APPLY, vg_grid_for(M * (C / 8)));
+        TrainOp e = TrainLowering::vg(VF_BN_APPLY, vg_apply_blocks(M * (C / 8)));
         e.vp[0] = bref(xb); e.vp[3] = coef; e.vp[4] = bref(yb);
         e.va.n[0] = M; e.va.i[0] = 0; e.va.i[1] = C; e.va.i[2] = fused_relu[i] >= 0 ? 1 : 0;
         L.add(std::move(e), {xb, part}, {yb});
@@ -2966,7 +2979,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         f.vp[5] = gref(i, 0); f.vp[6] = gref(i, 1); f.vp[7] = coef;
         f.va.n[0] = M; f.va.i[0] = 1; f.va.i[1] = C; f.va.i[2] = P; f.va.f[0] = o.bn_eps;
         L.add(std::move(f), {part, T.buf_params, saved[i].first, saved[i].second}, {T.buf_grads, part});
-        TrainOp e = TrainLowering::vg(VF_BN_APPLY, vg_grid_for(M * (C / 8)));
+        TrainOp e = TrainLowering::vg(VF_BN_APPLY, vg_apply_blocks(M * (C / 8)));
         e.vp[0] = bref(xb); e.vp[1] = bref(dy); if (ym >= 0) e.vp[2] = bref(ym); e.vp[3] = coef; e.vp[4] = bref(dx);
         e.va.n[0] = M; e.va.i[0] = 1; e.va.i[1] = C;
         L.add(std::move(e), {xb, dy, ym, part}, {dx});
@@ -2999,7 +3012,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         const int part = L.buf(static_cast<size_t>(tiles) * wg.split * BM * wg.bn * 4);
         const int gbuf = wg.split > 1 ? -1 : L.buf(static_cast<size_t>(o.c_out) * wg.Ngemm * 4);
         {
-          TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, (wg.Kpad / 64) * cdiv(o.c_out, 64));
+          TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, vg_transpose_blocks(o.c_out, 1, 1, wg.Kpad));
           t.vp[0] = bref(dy); t.vp[1] = bref(ab);
           t.va.n[0] = wg.M;
           const int iv[12] = {static_cast<int>(wg.M), 1, 1, o.c_out, 1, 1, 1, 1, 0, 0, wg.Kpad, 1};
@@ -3007,7 +3020,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
           L.add(std::move(t), {dy}, {ab});
         }
         {
-          TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, (wg.Kpad / 64) * cdiv(x.c, 64) * o.kh * o.kw);
+          TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, vg_transpose_blocks(x.c, o.kh, o.kw, wg.Kpad));
           t.vp[0] = bref(xb); t.vp[1] = bref(bb);
           t.va.n[0] = wg.M;
           const int iv[12] = {B, x.h, x.w, x.c, wg.Ho, wg.Wo, o.kw, o.stride, o.pad_h, o.pad_w, wg.Kpad, o.kh};

@@ -21,7 +21,12 @@
 namespace gacer {
 
 static_assert(VG_THREADS == NWORK, "virtual blocks run on the executor's worker group");
-constexpr int VG_SMEM_BYTES = 2 * VG_THREADS * 8 * 4;   // largest scratch (BN partial sums)
+constexpr int VG_SMEM_BYTES = 16384 * 2;      // largest scratch: a transpose tile (>= BN constants 3 x 2048 floats)
+
+// Each operator is its own (non-inlined) function: the executor dispatches
+// them from one switch, and inlining would give every operator the register
+// allocation of the heaviest one (spills).
+#define VG_FN static __device__ __noinline__
 
 __device__ __forceinline__ void vg_bar(int nthr) { asm volatile("bar.sync 1, %0;\n" ::"r"(nthr) : "memory"); }
 
@@ -53,7 +58,7 @@ __device__ __forceinline__ uint4 vg_pack8(const float* f) {
 // Thread t owns 8-channel group gl = t % G and row phase t / G.
 // a: p0 x, p1 dy, p2 ym, p3 mean, p4 var, p5 part [P][2][C] (out); n0 M;
 //    i0 mode, i1 C; f0 eps
-__device__ inline void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+VG_FN void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[1]);
   const __nv_bfloat16* ym = static_cast<const __nv_bfloat16*>(a.p[2]);
@@ -64,7 +69,7 @@ __device__ inline void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, i
   const int mode = a.i[0], C = a.i[1];
   const float eps = a.f[0];
   float* red = reinterpret_cast<float*>(smem);           // [2][nthr * 8]
-  constexpr int kUnroll = 4;
+  constexpr int kUnroll = 8;                             // rows per thread with loads in flight (summed in row order)
   const int G8 = C / 8;
   const int G = G8 < nthr ? G8 : nthr;
   const int RP = nthr / G;
@@ -163,7 +168,7 @@ __device__ inline void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, i
 // a: p0 part, p1 gamma, p2 beta, p3 x (mode 0: the shift rows) / mean_in
 //    (mode 1), p4 var_in (mode 1), p5 o1, p6 o2, p7 coef; n0 M; i0 mode,
 //    i1 C, i2 P; f0 eps
-__device__ inline void vg_bn_finalize(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+VG_FN void vg_bn_finalize(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
   (void)nvb;
   const float* part = static_cast<const float*>(a.p[0]);
   const float* gamma = static_cast<const float*>(a.p[1]);
@@ -240,93 +245,152 @@ __device__ inline void vg_bn_finalize(const VArgs& a, int vb, int nvb, int tid, 
 }
 
 // y = act(x * scale + shift) (mode 0); dx = a * dy + b * x + c (mode 1).
+// The host sizes the grid so the stride nvb * nthr is a multiple of C / 8
+// (vg_apply_blocks): every thread keeps one 8-channel group and its
+// constants in registers; VG_UNROLL 16-byte groups' loads are in flight.
 // a: p0 x, p1 dy, p2 ym, p3 coef, p4 out; n0 M; i0 mode, i1 C, i2 relu
-__device__ inline void vg_bn_apply(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
-  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
-  const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[1]);
-  const __nv_bfloat16* ym = static_cast<const __nv_bfloat16*>(a.p[2]);
+constexpr int VG_UNROLL = 8;   // 16-byte groups per thread with loads in flight
+template <int MODE>
+VG_FN void vg_bn_apply_t(const VArgs& a, int vb, int nvb, int tid, int nthr) {
+  constexpr int U = MODE == 0 ? VG_UNROLL : VG_UNROLL / 2;   // (mode 1 streams three tensors)
+  const uint4* x = static_cast<const uint4*>(a.p[0]);
+  const uint4* dy = static_cast<const uint4*>(a.p[1]);
+  const uint4* ym = static_cast<const uint4*>(a.p[2]);
   const float* coef = static_cast<const float*>(a.p[3]);
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[4]));
+  uint4* out = static_cast<uint4*>(const_cast<void*>(a.p[4]));
   const int64_t M = a.n[0];
-  const int mode = a.i[0], C = a.i[1], relu = a.i[2];
+  constexpr int mode = MODE;
+  const int C = a.i[1], relu = a.i[2];
   const int G8 = C / 8;
+  const int64_t total = M * G8, stride = static_cast<int64_t>(nvb) * nthr;
+  const int64_t first = static_cast<int64_t>(vb) * nthr + tid;
+  const bool fixed = (stride % G8) == 0;
   float k0[8], k1[8], k2[8];
   int c0 = -1;
-  VG_LOOP(i, M * G8) {
-    const int c = static_cast<int>(i % G8) * 8;
-    if (c != c0) {
-      c0 = c;
+  for (int64_t i0 = first; i0 < total; i0 += U * stride) {
+    uint4 vx[U], vd[U], vm[U];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        k0[j] = coef[c + j];
-        k1[j] = coef[C + c + j];
-        k2[j] = mode == 1 ? coef[2 * C + c + j] : 0.0f;
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        vx[u] = __ldcs(x + i);
+        if (mode == 1) {
+          vd[u] = __ldcs(dy + i);
+          if (ym) vm[u] = __ldcs(ym + i);
+        }
       }
     }
-    float v[8];
-    vg_unpack8(__ldcs(reinterpret_cast<const uint4*>(x) + i), v);
-    if (mode == 0) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float t = fmaf(v[j], k0[j], k1[j]);
-        v[j] = relu ? fmaxf(t, 0.0f) : t;
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        const int c = (fixed && c0 >= 0) ? c0 : static_cast<int>(i % G8) * 8;
+        if (c != c0) {
+          c0 = c;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            k0[j] = coef[c + j];
+            k1[j] = coef[C + c + j];
+            k2[j] = mode == 1 ? coef[2 * C + c + j] : 0.0f;
+          }
+        }
+        float v[8];
+        vg_unpack8(vx[u], v);
+        if (mode == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float t = fmaf(v[j], k0[j], k1[j]);
+            v[j] = relu ? fmaxf(t, 0.0f) : t;
+          }
+        } else {
+          float d[8];
+          vg_unpack8(vd[u], d);
+          if (ym) {
+            float mk[8];
+            vg_unpack8(vm[u], mk);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = fmaf(k0[j], d[j], fmaf(k1[j], v[j], k2[j]));
+        }
+        __stcs(out + i, vg_pack8(v));
       }
-    } else {
-      float d[8];
-      vg_unpack8(__ldcs(reinterpret_cast<const uint4*>(dy) + i), d);
-      if (ym) {
-        float mk[8];
-        vg_unpack8(__ldcs(reinterpret_cast<const uint4*>(ym) + i), mk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = fmaf(k0[j], d[j], fmaf(k1[j], v[j], k2[j]));
     }
-    __stcs(reinterpret_cast<uint4*>(out) + i, vg_pack8(v));
   }
+}
+
+VG_FN void vg_bn_apply(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  if (a.i[0] == 0) vg_bn_apply_t<0>(a, vb, nvb, tid, nthr);
+  else vg_bn_apply_t<1>(a, vb, nvb, tid, nthr);
 }
 
 // ------------------------------------------------------------------ elementwise
 // dx = dy where x > 0 (and x < 6 for ReLU6), else 0.  a: p0 x, p1 dy, p2 dx; n0 n8; i0 six
-__device__ inline void vg_relu_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_relu_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const uint4* x = static_cast<const uint4*>(a.p[0]);
   const uint4* dy = static_cast<const uint4*>(a.p[1]);
   uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[2]));
   const int six = a.i[0];
-  VG_LOOP(i, a.n[0]) {
-    float v[8], d[8];
-    vg_unpack8(x[i], v);
-    vg_unpack8(dy[i], d);
+  const int64_t total = a.n[0], stride = static_cast<int64_t>(nvb) * nthr;
+  for (int64_t i0 = static_cast<int64_t>(vb) * nthr + tid; i0 < total; i0 += VG_UNROLL * stride) {
+    uint4 vx[VG_UNROLL], vd[VG_UNROLL];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) d[j] = (v[j] > 0.0f && (!six || v[j] < 6.0f)) ? d[j] : 0.0f;
-    dx[i] = vg_pack8(d);
+    for (int u = 0; u < VG_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) { vx[u] = x[i]; vd[u] = dy[i]; }
+    }
+#pragma unroll
+    for (int u = 0; u < VG_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        float v[8], d[8];
+        vg_unpack8(vx[u], v);
+        vg_unpack8(vd[u], d);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = (v[j] > 0.0f && (!six || v[j] < 6.0f)) ? d[j] : 0.0f;
+        dx[i] = vg_pack8(d);
+      }
+    }
   }
 }
 
 // y = a + b (ReLU when relu != 0).  a: p0 a, p1 b, p2 y; n0 n8; i0 relu
-__device__ inline void vg_add(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_add(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const uint4* pa = static_cast<const uint4*>(a.p[0]);
   const uint4* pb = static_cast<const uint4*>(a.p[1]);
   uint4* y = static_cast<uint4*>(const_cast<void*>(a.p[2]));
   const int relu = a.i[0];
-  VG_LOOP(i, a.n[0]) {
-    float u[8], v[8];
-    vg_unpack8(pa[i], u);
-    vg_unpack8(pb[i], v);
+  const int64_t total = a.n[0], stride = static_cast<int64_t>(nvb) * nthr;
+  for (int64_t i0 = static_cast<int64_t>(vb) * nthr + tid; i0 < total; i0 += VG_UNROLL * stride) {
+    uint4 va[VG_UNROLL], vb2[VG_UNROLL];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float t = u[j] + v[j];
-      u[j] = relu ? fmaxf(t, 0.0f) : t;
+    for (int u = 0; u < VG_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) { va[u] = pa[i]; vb2[u] = pb[i]; }
     }
-    y[i] = vg_pack8(u);
+#pragma unroll
+    for (int u = 0; u < VG_UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        float p[8], q[8];
+        vg_unpack8(va[u], p);
+        vg_unpack8(vb2[u], q);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float t = p[j] + q[j];
+          p[j] = relu ? fmaxf(t, 0.0f) : t;
+        }
+        y[i] = vg_pack8(p);
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------ pooling
 // ints: i0 N, i1 H, i2 W, i3 C, i4 KH, i5 KW, i6 S, i7 ph, i8 pw, i9 Ho, i10 Wo
 // Max-pool forward.  a: p0 x, p1 y
-__device__ inline void vg_maxpool_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_maxpool_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   uint4* y = static_cast<uint4*>(const_cast<void*>(a.p[1]));
   const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], KH = a.i[4], KW = a.i[5], S = a.i[6], ph = a.i[7],
@@ -359,7 +423,7 @@ __device__ inline void vg_maxpool_fwd(const VArgs& a, int vb, int nvb, int tid, 
 // Max-pool backward, pass 1: per (output window, 8-channel group) the first
 // maximum per channel (row-major tap order, padded taps skipped, Q14) as a
 // tap index byte.  a: p0 x, p1 arg (uint8 [N*Ho*Wo*C])
-__device__ inline void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   uint2* arg = static_cast<uint2*>(const_cast<void*>(a.p[1]));
   const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], KH = a.i[4], KW = a.i[5], S = a.i[6], ph = a.i[7],
@@ -398,7 +462,7 @@ __device__ inline void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int ti
 // Max-pool backward, pass 2: per (input pixel, 8-channel group) the sum of dy
 // over the windows whose recorded tap is this pixel, in (ho, wo) order.
 // a: p0 arg, p1 dy, p2 dx
-__device__ inline void vg_maxpool_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_maxpool_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const uint2* arg = static_cast<const uint2*>(a.p[0]);
   const uint4* dy = static_cast<const uint4*>(a.p[1]);
   uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[2]));
@@ -441,7 +505,7 @@ __device__ inline void vg_maxpool_bwd(const VArgs& a, int vb, int nvb, int tid, 
 }
 
 // GAP backward: dx[n][p][c] = dy[n][c] / HW.  a: p0 dy (f32 [N][C]), p1 dx; i0 N, i1 HW, i2 C
-__device__ inline void vg_gap_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_gap_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* dy = static_cast<const float*>(a.p[0]);
   uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[1]));
   const int N = a.i[0], HW = a.i[1], C = a.i[2];
@@ -459,7 +523,7 @@ __device__ inline void vg_gap_bwd(const VArgs& a, int vb, int nvb, int tid, int 
 
 // GAP forward: y[n][c] = (1/HW) sum_p x[n][p][c] in pixel order (fp32), bf16.
 // a: p0 x, p1 y; i0 N, i1 HW, i2 C
-__device__ inline void vg_gap_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_gap_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   uint4* y = static_cast<uint4*>(const_cast<void*>(a.p[1]));
   const int N = a.i[0], HW = a.i[1], C = a.i[2];
@@ -483,7 +547,7 @@ __device__ inline void vg_gap_fwd(const VArgs& a, int vb, int nvb, int tid, int 
 // z[n][o] = b[o] + sum_k w[o][k] x[n][k]: one warp per output, lane l sums
 // k = l, l+32, ..., then a fixed xor butterfly.  a: p0 x (bf16), p1 w (f32),
 // p2 b (nullable), p3 z (f32); i0 N, i1 K, i2 O
-__device__ inline void vg_linear_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_linear_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   const float* w = static_cast<const float*>(a.p[1]);
   const float* b = static_cast<const float*>(a.p[2]);
@@ -505,7 +569,7 @@ __device__ inline void vg_linear_fwd(const VArgs& a, int vb, int nvb, int tid, i
 }
 
 // dx[n][k] = sum_o dy[n][o] w[o][k] in o order.  a: p0 w, p1 dy, p2 dx (f32); i0 N, i1 K, i2 O
-__device__ inline void vg_linear_dx(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_linear_dx(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* w = static_cast<const float*>(a.p[0]);
   const float* dy = static_cast<const float*>(a.p[1]);
   float* dx = static_cast<float*>(const_cast<void*>(a.p[2]));
@@ -520,7 +584,7 @@ __device__ inline void vg_linear_dx(const VArgs& a, int vb, int nvb, int tid, in
 
 // dw[o][k] = sum_n dy[n][o] x[n][k], db[o] = sum_n dy[n][o] (n order).
 // a: p0 x (bf16), p1 dy, p2 dw, p3 db (nullable); i0 N, i1 K, i2 O
-__device__ inline void vg_linear_dw(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_linear_dw(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   const float* dy = static_cast<const float*>(a.p[1]);
   float* dw = static_cast<float*>(const_cast<void*>(a.p[2]));
@@ -544,7 +608,7 @@ __device__ inline void vg_linear_dw(const VArgs& a, int vb, int nvb, int tid, in
 // exp): thread partials over j = tid, tid + nthr, ..., then thread 0 combines
 // them in thread order.  dz = (softmax - onehot) / N (may alias z); rowloss[n].
 // a: p0 z, p1 labels (int32), p2 dz, p3 rowloss; i0 N, i1 Cls
-__device__ inline void vg_softmax_ce(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+VG_FN void vg_softmax_ce(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
   (void)nvb;
   const float* z = static_cast<const float*>(a.p[0]);
   const int32_t* labels = static_cast<const int32_t*>(a.p[1]);
@@ -589,7 +653,7 @@ __device__ inline void vg_softmax_ce(const VArgs& a, int vb, int nvb, int tid, i
 }
 
 // out = mean of v[0..N) in index order (fp64).  a: p0 v, p1 out; i0 N
-__device__ inline void vg_mean(const VArgs& a, int vb, int, int tid, int, uint8_t*) {
+VG_FN void vg_mean(const VArgs& a, int vb, int, int tid, int, uint8_t*) {
   if (vb != 0 || tid != 0) return;
   const float* v = static_cast<const float*>(a.p[0]);
   const int N = a.i[0];
@@ -601,7 +665,7 @@ __device__ inline void vg_mean(const VArgs& a, int vb, int, int tid, int, uint8_
 // SGD with momentum (PyTorch semantics): buf = mom * buf + g (buf = g on the
 // first step: a zero-initialised buf gives exactly that), w -= lr * buf.
 // a: p0 w, p1 g, p2 buf; n0 n; i0 first; f0 lr, f1 momentum
-__device__ inline void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   float* w = static_cast<float*>(const_cast<void*>(a.p[0]));
   const float* g = static_cast<const float*>(a.p[1]);
   float* buf = static_cast<float*>(const_cast<void*>(a.p[2]));
@@ -620,7 +684,7 @@ __device__ inline void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr
 // (r*KW + s)*cread + ci = w[co][ci][r][s]; forward = 0 (data gradient): row
 // ci, column (r*KW + s)*cread + co = w[co][ci][KH-1-r][KW-1-s]; padding 0.
 // a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward
-__device__ inline void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* w = static_cast<const float*>(a.p[0]);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
   const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], cread = a.i[4], Kpad = a.i[5], rows = a.i[6],
@@ -642,7 +706,7 @@ __device__ inline void vg_filter(const VArgs& a, int vb, int nvb, int tid, int n
 
 // Zero-dilated dy of a strided conv's data gradient (Hdd x Wdd).
 // a: p0 dy, p1 out; i0 N, i1 Hd, i2 Wd, i3 C, i4 S, i5 Hdd, i6 Wdd
-__device__ inline void vg_dilate(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_dilate(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[0]);
   uint4* out = static_cast<uint4*>(const_cast<void*>(a.p[1]));
   const int N = a.i[0], Hd = a.i[1], Wd = a.i[2], C = a.i[3], S = a.i[4], Hdd = a.i[5], Wdd = a.i[6];
@@ -660,31 +724,32 @@ __device__ inline void vg_dilate(const VArgs& a, int vb, int nvb, int tid, int n
 }
 
 // Weight-gradient operand: the transposed im2col of x, K-major along the
-// pixel index m (row (t*C + c), column m), 64 pixels x 64 channels of one tap
-// t per virtual block through a swizzled smem tile (coalesced 16-byte loads
-// and stores).  Block vb = (bx, by, bz) over (Kpad/64, cdiv(C, 64), KH*KW).
+// pixel index m (row (t*C + c), column m), TC channels x TP = 16384 / TC
+// pixels of one tap t per virtual block (vg_transpose_tc) through a smem
+// tile (coalesced 16-byte loads and stores; 64-pixel segments XOR-swizzled by
+// the channel octet so the transposing scalar stores hit distinct banks).
+// Block vb = (bx, by, bz) over (cdiv(Kpad, TP), cdiv(C, TC), KH*KW).
 // a: p0 x, p1 out; n0 M; i0 N, i1 H, i2 W, i3 C, i4 Ho, i5 Wo, i6 KW, i7 S,
 //    i8 ph, i9 pw, i10 Kpad, i11 KH
-__device__ inline void vg_transpose_im2col(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
+VG_FN void vg_transpose_im2col(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
   (void)nvb;
-  constexpr int T = 64;
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
   const int64_t M = a.n[0];
-  const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], Ho = a.i[4], Wo = a.i[5], KW = a.i[6], S = a.i[7],
+  const int H = a.i[1], W = a.i[2], C = a.i[3], Ho = a.i[4], Wo = a.i[5], KW = a.i[6], S = a.i[7],
             ph = a.i[8], pw = a.i[9], Kpad = a.i[10];
-  (void)N;
+  const int TC = vg_transpose_tc(C), TP = VG_TRANSPOSE_TILE / TC, GPR = TC / 8;   // channel groups per pixel
   __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
-  auto at = [](int c, int i) { return c * T + ((((i >> 3) ^ (c >> 3)) & 7) << 3) + (i & 7); };
-  const int gx = Kpad / T, gy = (C + T - 1) / T;
+  auto at = [TP](int c, int i) { return c * TP + (i & ~63) + ((((i >> 3) ^ (c >> 3)) & 7) << 3) + (i & 7); };
+  const int gx = (Kpad + TP - 1) / TP, gy = (C + TC - 1) / TC;
   const int t = vb / (gx * gy);
   const int by = (vb / gx) % gy, bx = vb % gx;
   const int r = t / KW, q = t % KW;
-  const int64_t m0 = static_cast<int64_t>(bx) * T;
-  const int c0 = by * T;
+  const int64_t m0 = static_cast<int64_t>(bx) * TP;
+  const int c0 = by * TC;
   const bool vec = (C % 8) == 0;
-  for (int e = tid; e < T * (T / 8); e += nthr) {
-    const int i = e / (T / 8), cg = (e % (T / 8)) * 8;
+  for (int e = tid; e < TP * GPR; e += nthr) {
+    const int i = e / GPR, cg = (e % GPR) * 8;
     const int64_t m = m0 + i;
     __nv_bfloat16 v[8];
 #pragma unroll
@@ -712,8 +777,8 @@ __device__ inline void vg_transpose_im2col(const VArgs& a, int vb, int nvb, int 
     for (int j = 0; j < 8; ++j) tile[at(cg + j, i)] = v[j];
   }
   vg_bar(nthr);
-  for (int e = tid; e < T * (T / 8); e += nthr) {
-    const int cc = e / (T / 8), mg = (e % (T / 8)) * 8;
+  for (int e = tid; e < TC * (TP / 8); e += nthr) {
+    const int cc = e / (TP / 8), mg = (e % (TP / 8)) * 8;
     const int c = c0 + cc;
     const int64_t m = m0 + mg;
     if (c < C && m < Kpad)
@@ -725,7 +790,7 @@ __device__ inline void vg_transpose_im2col(const VArgs& a, int vb, int nvb, int 
 
 // dW from the GEMM's [Cout][(r*KW + s)*Cin + ci] order to [Cout][Cin][KH][KW].
 // a: p0 g, p1 dw; i0 Cout, i1 Cin, i2 KH, i3 KW
-__device__ inline void vg_wgrad_permute(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_wgrad_permute(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* g = static_cast<const float*>(a.p[0]);
   float* dw = static_cast<float*>(const_cast<void*>(a.p[1]));
   const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3];
@@ -740,7 +805,7 @@ __device__ inline void vg_wgrad_permute(const VArgs& a, int vb, int nvb, int tid
 // [bn/4][128 rows] float4) summed in split order straight into dW's
 // [Cout][Cin][KH][KW] layout.  a: p0 part, p1 dw; i0 Cout, i1 Cin, i2 KH,
 // i3 KW, i4 bn, i5 tiles_n, i6 split
-__device__ inline void vg_wgrad_reduce(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+VG_FN void vg_wgrad_reduce(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float4* part = static_cast<const float4*>(a.p[0]);
   float* dw = static_cast<float*>(const_cast<void*>(a.p[1]));
   const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], bn = a.i[4], tiles_n = a.i[5], split = a.i[6];

@@ -100,7 +100,7 @@ VArgs transpose_args(const void* x, int N, int H, int W, int C, int Ho, int Wo, 
   return a;
 }
 
-int transpose_blocks(int C, int KH, int KW, int Kpad) { return (Kpad / 64) * ((C + 63) / 64) * KH * KW; }
+int transpose_blocks(int C, int KH, int KW, int Kpad) { return vg_transpose_blocks(C, KH, KW, Kpad); }
 
 cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, int Ho, int Wo, int KH, int KW, int S,
                                     int ph, int pw, int64_t M, int Kpad, void* out, cudaStream_t s) {
@@ -144,7 +144,8 @@ int32_t gacer_bn_partials(int64_t M, int32_t C) {
 int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float* gamma_dev, const float* beta_dev,
                            float eps, int32_t relu, void* y_dev, float* mean_dev, float* var_dev, float* scratch_dev,
                            void* stream) {
-  if (M < 1 || C < 8 || C % 8) return bad(GACER_E_SHAPE, "bn_train_fwd: need M >= 1 and C % 8 == 0");
+  if (M < 1 || C < 8 || C % 8 || C > VG_MAX_BN_C)
+    return bad(GACER_E_SHAPE, "bn_train_fwd: need M >= 1, C % 8 == 0 and C <= 2048");
   if (!x_dev || !y_dev || !gamma_dev || !beta_dev || !mean_dev || !var_dev || !scratch_dev ||
       !aligned16(x_dev) || !aligned16(y_dev))
     return bad(GACER_E_INVALID_ARG, "bn_train_fwd: null or misaligned pointer");
@@ -160,14 +161,15 @@ int32_t gacer_bn_train_fwd(const void* x_dev, int64_t M, int32_t C, const float*
   vlaunch(VF_BN_FINALIZE, f, (C + 31) / 32, s);
   VArgs e = vargs();
   e.p[0] = x_dev; e.p[3] = coef; e.p[4] = y_dev; e.n[0] = M; e.i[0] = 0; e.i[1] = C; e.i[2] = relu;
-  vlaunch(VF_BN_APPLY, e, vg_grid_for(M * (C / 8)), s);
+  vlaunch(VF_BN_APPLY, e, gacer::vg_apply_blocks(M * (C / 8)), s);
   return launched("bn_train_fwd");
 }
 
 int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, const void* relu_y_dev, int64_t M, int32_t C,
                            const float* gamma_dev, const float* mean_dev, const float* var_dev, float eps, void* dx_dev,
                            float* dgamma_dev, float* dbeta_dev, float* scratch_dev, void* stream) {
-  if (M < 1 || C < 8 || C % 8) return bad(GACER_E_SHAPE, "bn_train_bwd: need M >= 1 and C % 8 == 0");
+  if (M < 1 || C < 8 || C % 8 || C > VG_MAX_BN_C)
+    return bad(GACER_E_SHAPE, "bn_train_bwd: need M >= 1, C % 8 == 0 and C <= 2048");
   if (!x_dev || !dy_dev || !dx_dev || !gamma_dev || !mean_dev || !var_dev || !dgamma_dev || !dbeta_dev ||
       !scratch_dev || !aligned16(x_dev) || !aligned16(dy_dev) || !aligned16(dx_dev) ||
       (relu_y_dev && !aligned16(relu_y_dev)))
@@ -186,7 +188,7 @@ int32_t gacer_bn_train_bwd(const void* x_dev, const void* dy_dev, const void* re
   VArgs e = vargs();
   e.p[0] = x_dev; e.p[1] = dy_dev; e.p[2] = relu_y_dev; e.p[3] = coef; e.p[4] = dx_dev; e.n[0] = M; e.i[0] = 1;
   e.i[1] = C;
-  vlaunch(VF_BN_APPLY, e, vg_grid_for(M * (C / 8)), s);
+  vlaunch(VF_BN_APPLY, e, gacer::vg_apply_blocks(M * (C / 8)), s);
   return launched("bn_train_bwd");
 }
 
