@@ -124,14 +124,23 @@ typedef struct {
 /* Spatial regulation for one operator: the mask entry and list_B (l.667,
  * l.683-684).  op_index is the 1-based position of the op in the tenant's
  * ORIGINAL (pre-fusion) op list.  axis BATCH: sizes sum to the batch (Eq. 5);
- * axis CHANNEL: sizes sum to c_out.  sm_budget is reserved (may be NULL). */
+ * axis CHANNEL: sizes sum to c_out.
+ * sm_budget (nullable; [n_chunks], each >= 0, 0 = unlimited): the chunk's
+ * resource share W(O^B) (l.597-601; "by controlling the number j, we can
+ * control the spatial granularity", l.667-668): at most sm_budget[j] items of
+ * chunk j are claimed-and-not-complete at any time, so the chunk occupies at
+ * most that many SMs (one item runs on one SM; the others serve other
+ * tenants).  Enforced on the device by a per-chunk semaphore counter; it
+ * changes WHEN tiles run, never what they compute (results are bit-identical
+ * with and without budgets).  A single chunk (n_chunks = 1, sizes = {B})
+ * budgets an undecomposed operator.  Negative values: GACER_E_INVALID_ARG. */
 typedef struct {
   int32_t tenant;
   int32_t op_index;
   int32_t axis;               /* gacer_axis */
   int32_t n_chunks;
   const int32_t* sizes;       /* [n_chunks], each >= 1 */
-  const int32_t* sm_budget;   /* reserved, may be NULL */
+  const int32_t* sm_budget;   /* [n_chunks] max items in flight per chunk, 0 = unlimited; may be NULL */
 } gacer_chunking;
 
 typedef struct {

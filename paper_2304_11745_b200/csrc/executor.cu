@@ -151,6 +151,20 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;
   return d;
 }
+// MN-major SWIZZLE_128B canonical layout (CUTLASS cute UMMA Layout_MN_SW128):
+// 64 MN-elements per 128-byte row, one row per K index, 8 K rows per
+// 1024-byte swizzle atom (SBO = 1024 between atoms along K), the next 64
+// MN-elements LBO = 8192 bytes further (one 64 x 64 TMA box).  A K step of 16
+// advances the start address by 16 rows = 2048 bytes.
+__device__ __forceinline__ uint64_t make_sdesc_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(8192 >> 4) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
 // Instruction descriptor kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1),
 // B bf16 (bits 10-12 = 1), both K-major, N>>3 at bits 17-22, M>>4 at 24-28.
 __device__ __forceinline__ uint32_t make_idesc(int n) {
@@ -548,7 +562,11 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       }
       // M-pair tiles: the second 128-row A block lands in the stage's B region
       // after the (<= 16 KB, bn <= 128) B block
-      const uint32_t tx = A_STAGE_BYTES * mrep + bbytes;
+      // A_MN: only the 64-column B boxes inside the GEMM's N (columns past it
+      // are never stored, their smem is left as is)
+      const int nbq = a_mode == A_MN ? min(op.bn, op.N - n0 + 63) / 64 : 0;
+      const uint32_t tx = a_mode == A_MN ? A_STAGE_BYTES + static_cast<uint32_t>(nbq) * 8192u
+                                         : A_STAGE_BYTES * mrep + bbytes;
       // first K-block of this item whose stage (g + i) % NPROD belongs to producer pj
       const int i0 = (pj - static_cast<int>(g % NPROD) + NPROD) % NPROD;
 #pragma unroll 1
@@ -560,6 +578,24 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
         const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
         const uint32_t b_dst = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
         const int k = (kb0 + i) * BK;
+        if (a_mode == A_MN) {
+          // K-block = output pixels [k, k + 64): A = dy rows (two 64-channel
+          // boxes), B = one im2col box per 64 GEMM columns (tap, c0)
+          tma_load_2d(a_dst, tmap_a, bar, m0, k);
+          tma_load_2d(a_dst + 8192, tmap_a, bar, m0 + 64, k);
+          const int HoWo = op.Ho * op.Wo;
+          const int img = k / HoWo, rem = k - img * HoWo;
+          const int ho = rem / op.Wo, wo = rem - ho * op.Wo;
+          const int wi = wo * op.stride - op.pw, hi = ho * op.stride - op.ph;
+          for (int q = 0; q < nbq; ++q) {
+            const int n = n0 + q * 64;
+            const int tap = n / C, c0 = n - tap * C;
+            tma_load_im2col_4d(b_dst + q * 8192, tmap_b, bar, c0, wi, hi, img, static_cast<uint16_t>(tap % kw),
+                               static_cast<uint16_t>(tap / kw));
+          }
+          kdbg(p, 1, gi);
+          continue;
+        }
         if (a_mode == A_IM2COL) {
           const int tap = k / C;
           const int c0 = k - tap * C;
@@ -1040,6 +1076,7 @@ __device__ __forceinline__ Item decode_single(const OpDev& op, int op_idx, int b
   it.mt = b / op.tiles_n;
   it.dep_begin = it.dep_count = 0;
   it.chunk = -1;
+  it.bud = -1;
   it.cluster = 0;
   it.prio = 0;
   it.idx = -1;
@@ -1076,6 +1113,7 @@ __device__ bool spin_ge(const uint32_t* ctr, uint32_t target, const ExecParams& 
 // Non-blocking readiness test of an item's producer-chunk dependencies
 // (relaxed loads; the caller fences once after claiming).
 __device__ __forceinline__ bool deps_ready(const ExecParams& p, const Item& it) {
+  if (it.bud >= 0 && ld_relaxed(p.chunk_done + it.bud) < (p.epoch - 1u) * it.btot + it.boff) return false;
   if (it.dep_count <= INLINE_DEPS) {
     bool ok = true;
 #pragma unroll
@@ -1170,6 +1208,7 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
   fence_release_gpu();
   dbg_mark(p, 8);
   atomicAdd(p.chunk_done + it.chunk, 1u);
+  if (it.bud >= 0) atomicAdd(p.chunk_done + it.bud, 1u);
   atomicAdd(p.cluster_done + it.cluster, 1u);
   dbg_mark(p, 9);
   if (p.trace) {
@@ -1183,6 +1222,7 @@ __device__ __forceinline__ void release_item(const ExecParams& p, const Item& it
 // Wait (blocking) until the item's dependencies are complete; false on abort.
 __device__ bool wait_deps(const ExecParams& p, const Item& it) {
   if (deps_ready(p, it)) { fence_acquire_gpu(); return true; }   // usual case: one parallel check
+  if (it.bud >= 0 && !spin_ge(p.chunk_done + it.bud, (p.epoch - 1u) * it.btot + it.boff, p)) return false;
   if (it.dep_count <= INLINE_DEPS) {
     for (int d = 0; d < it.dep_count; ++d)
       if (!spin_ge(p.chunk_done + it.dc[d], p.epoch * it.dt[d], p)) return false;
@@ -1332,6 +1372,10 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
 // out of the worker loop's allocation (the GEMM producer path shares it).
 __device__ __noinline__ void vgrid_item(const OpDev& op, int mt, int wtid, uint8_t* smem) {
   const int v0 = mt * op.bm, v1 = min(v0 + op.bm, op.vblocks);
+  if (vg_streamable(op.vfn)) {   // HBM-streaming operators: staged through the ring with bulk copies
+    vg_stream_item(op.vfn, op.va, v0, v1, op.vblocks, wtid, NWORK, smem, SMEM_RING_BYTES);
+    return;
+  }
   for (int vb = v0; vb < v1; ++vb) run_vgrid(op.vfn, op.va, vb, op.vblocks, wtid, NWORK, smem);
 }
 
@@ -1413,7 +1457,8 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     if (acc >= 2) mbar_wait(&ctl->tempty[abuf], ((acc / 2) + 1) & 1);
     tc_fence_after();
     const uint32_t d = cx.tmem + abuf * BN_MAX;
-    const uint32_t idesc = make_idesc(op.bn);
+    const bool mn = op.a_mode == A_MN;    // both operands MN-major (weight gradient)
+    const uint32_t idesc = make_idesc(op.bn) | (mn ? ((1u << 15) | (1u << 16)) : 0u);
     const int mrep = op.mrep;
     const uint32_t d2 = d + static_cast<uint32_t>(op.bn);   // second accumulator (M-pair tiles)
     bool stamped = false;
@@ -1431,10 +1476,17 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
       if (!(GACER_DIAG && p.dbg && (p.dbg_spin & 1))) {  // diagnostics: odd dbg_spin skips the MMAs
+        if (mn) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(d, make_sdesc_mn(a_base + kk * 2048), make_sdesc_mn(b_base + kk * 2048), idesc,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+        } else {
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
           umma_bf16(d, make_sdesc(a_base + kk * 32), make_sdesc(b_base + kk * 32), idesc,
                     (i > 0 || kk > 0) ? 1u : 0u);
+        }
         if (mrep > 1) {
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
@@ -2070,6 +2122,10 @@ extern "C" __global__ void __launch_bounds__(CC_THREADS) op_cc_kernel(const OpDe
   const Item it = decode_single(op, op_idx, blockIdx.x);
   if (op.kind == DK_VGRID) {
     const int v0 = it.mt * op.bm, v1 = min(v0 + op.bm, op.vblocks);
+    if (vg_streamable(op.vfn)) {
+      vg_stream_item(op.vfn, op.va, v0, v1, op.vblocks, threadIdx.x, CC_THREADS, win_buf, WIN_SMEM_BYTES);
+      return;
+    }
     for (int vb = v0; vb < v1; ++vb) run_vgrid(op.vfn, op.va, vb, op.vblocks, threadIdx.x, CC_THREADS, win_buf);
   } else if (op.win) {
     window_smem(op, it, threadIdx.x, CC_THREADS, smem_u32(win_buf), 1);

@@ -110,7 +110,11 @@ constexpr int WIN_IN_BYTES = 96 * 1024;   // window_smem: staged input rows of o
 constexpr int WIN_SMEM_BYTES = WIN_IN_BYTES + (9 + 2) * 64 * 4 + 1024;  // + dw weights/scale/bias (kh*kw <= 9)
 
 // operand A load mode of a GEMM op
-enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2 };
+// A_MN: weight-gradient GEMM with both operands MN-major, read in place (no
+// staged transposes): A = dy [pixels][Cout] (2-D TMA, 64 channels x 64
+// pixels per box), B = im2col(x) (im2col TMA, 64 pixels x 64 channels of one
+// tap per box); K runs over the output pixels.
+enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2, A_MN = 3 };
 
 struct OpDev {
   int32_t kind;            // DevKind
@@ -176,6 +180,14 @@ struct Item {
   int32_t dep_begin;
   int32_t dc[INLINE_DEPS]; // producer chunk counters
   uint32_t dt[INLINE_DEPS];// their per-round targets
+  // SM budget of the item's chunk (gacer_chunking.sm_budget; the paper's
+  // W(O^B) share): bud = the chunk's budget counter (-1:
+  // none), incremented by every released item of the chunk; this item (the
+  // j-th of its chunk in queue order, budget b) is ready only once
+  // counter >= (epoch - 1) * btot + boff, boff = max(0, j - b + 1), so at most
+  // b items of the chunk are claimed and not yet complete at any time.
+  int32_t bud;
+  uint32_t btot, boff;
 };
 
 struct Dep {

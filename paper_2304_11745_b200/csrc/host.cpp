@@ -203,6 +203,7 @@ struct Tenant {
 struct Chunking {
   int axis = GACER_AXIS_NONE;
   std::vector<int> sizes;
+  std::vector<int> budget;   // per chunk: max items in flight (0 = unlimited); empty = none
 };
 
 struct Plan {
@@ -975,7 +976,7 @@ int encode_rows(CUtensorMap* m, const void* base, int cols, int rows, int ld, in
 // NHWC bf16 activation as an im2col view: 128 output pixels x 64 channels of
 // one filter tap per load (pixelsPerColumn = BM, channelsPerPixel = BK).
 // Bounding box per CUTLASS fprop convention: lower = -pad, upper = pad - (k-1).
-int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c) {
+int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c, int pix_box = BM) {
   // globalDim[0] is the tensor's real channel count: channels [Cin, cread)
   // of a 64-channel box are out of bounds and zero-filled by the TMA
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(real_c), static_cast<cuuint64_t>(d.W),
@@ -986,7 +987,8 @@ int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c) {
   const int upper[2] = {d.pw - (d.kw - 1), d.ph - (d.kh - 1)};
   const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(d.stride), static_cast<cuuint32_t>(d.stride), 1};
   CUresult r = g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d.in), dims, st, lower, upper,
-                               BK, BM, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               BK, static_cast<cuuint32_t>(pix_box), es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "cuTensorMapEncodeIm2col failed (%d)", static_cast<int>(r));
   return 0;
@@ -1085,6 +1087,8 @@ struct ChunkRange {
   int m0, m1, n0, n1;  // tile ranges
   int counter;
   uint32_t n_items;
+  int budget = 0;      // gacer_chunking.sm_budget of this chunk (0 = unlimited)
+  int bud = -1;        // its budget counter (items released), -1 = none
   // Completion counters at M-tile granularity (ops whose M axis is output
   // pixels or samples): mc[mt - m0] counts the items of M-tile mt in this
   // chunk (target mc_items).  A consumer waits only for the producer tiles
@@ -1134,7 +1138,7 @@ int compile_plan(Plan& P) {
       for (int m : F.members) {
         auto it = P.chunks.find({t, m});
         if (it == P.chunks.end()) continue;
-        if (ch && (ch->axis != it->second.axis || ch->sizes != it->second.sizes))
+        if (ch && (ch->axis != it->second.axis || ch->sizes != it->second.sizes || ch->budget != it->second.budget))
           return set_err(GACER_E_INVALID_ARG, "tenant %d: fused ops %d and %d carry different chunkings", t,
                          F.head + 1, m + 1);
         ch = &it->second;
@@ -1157,12 +1161,14 @@ int compile_plan(Plan& P) {
         }
         const int ntiles = on_m ? F.tiles_m : F.tiles_n;
         long long u = 0;
-        for (int s : ch->sizes) {
+        for (size_t j = 0; j < ch->sizes.size(); ++j) {
+          const int s = ch->sizes[j];
           const long long a = u * unit, b = (u + s) * unit;
           int t0 = static_cast<int>((a + tsz - 1) / tsz), t1 = static_cast<int>((b + tsz - 1) / tsz);
           t0 = std::min(t0, ntiles); t1 = std::min(t1, ntiles);
           if (on_m) ranges.push_back({t0, t1, 0, F.tiles_n, 0, 0});
           else ranges.push_back({0, F.tiles_m, t0, t1, 0, 0});
+          if (!ch->budget.empty()) ranges.back().budget = ch->budget[j];
           u += s;
         }
       }
@@ -1176,6 +1182,9 @@ int compile_plan(Plan& P) {
         } else {
           r.counter = counter++;
         }
+        // SM budget W(O^B) (l.597-601): a semaphore counter of the chunk's
+        // released items; only when it binds (fewer than the chunk's items)
+        if (r.budget > 0 && static_cast<uint32_t>(r.budget) < r.n_items) r.bud = counter++;
       }
     }
   }
@@ -1311,6 +1320,7 @@ int compile_plan(Plan& P) {
               if (dl.size() <= static_cast<size_t>(INLINE_DEPS))
                 for (size_t d = 0; d < dl.size(); ++d) { it.dc[d] = dl[d].counter; it.dt[d] = dl[d].target; }
               it.chunk = r.counter;
+              it.bud = -1;
               it.cluster = k;
               it.prio = rank[t][f];
               it.kind = op.kind;
@@ -1327,6 +1337,7 @@ int compile_plan(Plan& P) {
       const int split = (F.kind == DK_GEMM) ? F.split_k : 1;
       for (const ChunkRange& r : cr[t][f]) {
         if (!r.n_items) continue;
+        uint32_t jchunk = 0;   // position of the next item within its chunk (queue order)
         for (int mt = r.m0; mt < r.m1; ++mt)
           for (int ntile = r.n0; ntile < r.n1; ++ntile) {
             // input rows this tile reads, as a flattened row range of each
@@ -1407,6 +1418,13 @@ int compile_plan(Plan& P) {
               if (dl.size() <= static_cast<size_t>(INLINE_DEPS))
                 for (size_t d = 0; d < dl.size(); ++d) { it.dc[d] = dl[d].counter; it.dt[d] = dl[d].target; }
               it.chunk = r.mc.empty() ? r.counter : r.mc[mt - r.m0];
+              it.bud = -1;
+              if (r.bud >= 0) {   // every item of the chunk counts; item j >= budget waits
+                it.bud = r.bud;
+                it.btot = r.n_items;
+                it.boff = jchunk >= static_cast<uint32_t>(r.budget) ? jchunk - static_cast<uint32_t>(r.budget) + 1u : 0u;
+              }
+              ++jchunk;
               it.cluster = k;
               it.prio = rank[t][f];
               it.kind = F.kind;
@@ -1933,6 +1951,11 @@ int gacer_set_regulation(const gacer_decomposition* dec, const gacer_sync_pointe
       Chunking ch;
       ch.axis = c.axis;
       ch.sizes.assign(c.sizes, c.sizes + c.n_chunks);
+      if (c.sm_budget) {
+        for (int j = 0; j < c.n_chunks; ++j)
+          if (c.sm_budget[j] < 0) return set_err(GACER_E_INVALID_ARG, "chunking %d: negative sm_budget", i);
+        ch.budget.assign(c.sm_budget, c.sm_budget + c.n_chunks);
+      }
       if (!P.chunks.emplace(std::make_pair(c.tenant, o), ch).second)
         return set_err(GACER_E_INVALID_ARG, "chunking %d: op %d decomposed twice", i, c.op_index);
     }
@@ -2347,6 +2370,35 @@ int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.bytes = o;
   return 0;
 }
+
+// Weight gradient with MN-major operands read in place (A_MN): needs whole
+// 64-channel boxes per tap (Cin % 64 == 0) and 16-byte NHWC rows.  Fills the
+// GEMM fields of d that differ from the staged (A_ROWS) form and encodes the
+// two tensor maps: dy [Mpix][Cout] as 64 x 64 boxes, x as an im2col view with
+// 64-pixel columns.
+bool wgrad_mn_ok(int Cin, int Cout) { return Cin % 64 == 0 && Cout % 8 == 0; }
+
+int wgrad_mn_setup(OpDev& d, CUtensorMap* maps, const void* x, const void* dy, int N, int H, int W, int Cin, int Cout,
+                   int KH, int KW, int stride, int pad_h, int pad_w, const WgradGeom& g, bool encode) {
+  d.a_mode = A_MN;
+  d.in = dy;
+  d.wt = x;
+  d.B = N; d.H = H; d.W = W; d.C = Cin; d.ldi = Cin;
+  d.Ho = g.Ho; d.Wo = g.Wo;
+  d.kh = KH; d.kw = KW; d.stride = stride; d.ph = pad_h; d.pw = pad_w;
+  if (!encode || !x || !dy) return 0;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(g.M)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Cout) * 2};
+  const cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(BK)};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode_tiled(&maps[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(dy), dims, strides, box,
+                              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "wgrad: dy tensor map (%d)", static_cast<int>(r));
+  OpDev v = d;          // the im2col view of x (the forward conv's geometry, 64-pixel columns)
+  v.in = x;
+  return encode_im2col(&maps[1], v, Cin, BK);
+}
 }  // namespace
 
 extern "C" {
@@ -2382,9 +2434,12 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   if (g.rows_b > g.Ngemm)
     CUDA_TRY(cudaMemsetAsync(static_cast<uint8_t*>(b) + g.Ngemm * rowb, 0, (g.rows_b - g.Ngemm) * rowb, st));
   CUDA_TRY(cudaMemsetAsync(ws + g.off_cnt, 0, static_cast<size_t>(g.tiles_m) * g.tiles_n * 4, st));
-  // dy [M][Cout] viewed as a 1x1 "im2col" of itself: the transpose
-  CUDA_TRY(launch_transpose_im2col(dy_dev, static_cast<int>(g.M), 1, 1, Cout, 1, 1, 1, 1, 1, 0, 0, g.M, g.Kpad, a, st));
-  CUDA_TRY(launch_transpose_im2col(x_dev, N, H, W, Cin, g.Ho, g.Wo, KH, KW, stride, pad_h, pad_w, g.M, g.Kpad, b, st));
+  const bool mn = wgrad_mn_ok(Cin, Cout) && !env_flag("GACER_WGRAD_STAGED");
+  if (!mn) {
+    // dy [M][Cout] viewed as a 1x1 "im2col" of itself: the transpose
+    CUDA_TRY(launch_transpose_im2col(dy_dev, static_cast<int>(g.M), 1, 1, Cout, 1, 1, 1, 1, 1, 0, 0, g.M, g.Kpad, a, st));
+    CUDA_TRY(launch_transpose_im2col(x_dev, N, H, W, Cin, g.Ho, g.Wo, KH, KW, stride, pad_h, pad_w, g.M, g.Kpad, b, st));
+  }
   const float *ones = nullptr, *zeros = nullptr;
   if (int rc0 = unit_vectors(nsb, &ones, &zeros)) return rc0;
   OpDev d;
@@ -2413,8 +2468,13 @@ int32_t gacer_conv_wgrad(const void* x_dev, const void* dy_dev, int32_t N, int32
   const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(ws + g.off_maps);
   d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
   d.c_tma = 0;                                   // fp32 rows stored directly
-  int rc = encode_rows(&maps[0], a, g.Kpad, g.rows_a, g.Kpad, BM);
-  if (!rc) rc = encode_rows(&maps[1], b, g.Kpad, g.rows_b, g.Kpad, g.bn);
+  int rc = 0;
+  if (mn) {
+    rc = wgrad_mn_setup(d, maps, x_dev, dy_dev, N, H, W, Cin, Cout, KH, KW, stride, pad_h, pad_w, g, true);
+  } else {
+    rc = encode_rows(&maps[0], a, g.Kpad, g.rows_a, g.Kpad, BM);
+    if (!rc) rc = encode_rows(&maps[1], b, g.Kpad, g.rows_b, g.Kpad, g.bn);
+  }
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(ws + g.off_maps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(ws + g.off_op, &d, sizeof d, cudaMemcpyHostToDevice, st));
@@ -3006,12 +3066,15 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         // along the pixel index, split-K over the pixels, ordered reduction
         WgradGeom wg;
         if (int rc = wgrad_geom(B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, wg)) return rc;
-        const int ab = L.buf(static_cast<size_t>(wg.rows_a) * wg.Kpad * 2);
-        const int bb = L.buf(static_cast<size_t>(wg.rows_b) * wg.Kpad * 2);
+        // MN-major operands read in place (no staged transposes) when every
+        // 64-channel box lies inside one tap; the stem (3 channels) stages
+        const bool mn = wgrad_mn_ok(x.c, o.c_out) && !env_flag("GACER_WGRAD_STAGED");
+        const int ab = mn ? -1 : L.buf(static_cast<size_t>(wg.rows_a) * wg.Kpad * 2);
+        const int bb = mn ? -1 : L.buf(static_cast<size_t>(wg.rows_b) * wg.Kpad * 2);
         const int tiles = wg.tiles_m * wg.tiles_n;
         const int part = L.buf(static_cast<size_t>(tiles) * wg.split * BM * wg.bn * 4);
         const int gbuf = wg.split > 1 ? -1 : L.buf(static_cast<size_t>(o.c_out) * wg.Ngemm * 4);
-        {
+        if (!mn) {
           TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, vg_transpose_blocks(o.c_out, 1, 1, wg.Kpad));
           t.vp[0] = bref(dy); t.vp[1] = bref(ab);
           t.va.n[0] = wg.M;
@@ -3019,7 +3082,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
           std::memcpy(t.va.i, iv, sizeof iv);
           L.add(std::move(t), {dy}, {ab});
         }
-        {
+        if (!mn) {
           TrainOp t = TrainLowering::vg(VF_TRANSPOSE_IM2COL, vg_transpose_blocks(x.c, o.kh, o.kw, wg.Kpad));
           t.vp[0] = bref(xb); t.vp[1] = bref(bb);
           t.va.n[0] = wg.M;
@@ -3042,11 +3105,19 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
           d.split_k = wg.split; d.nkb = wg.nkb; d.ldw = wg.Kpad;
           d.partials_only = wg.split > 1 ? 1 : 0;
           d.a_mode = A_ROWS;
-          m.g_in = bref(ab); m.g_wt = bref(bb); m.g_part = bref(part); m.g_out = bref(gbuf);
+          m.g_part = bref(part); m.g_out = bref(gbuf);
           m.g_scale = bref(buf_ones); m.g_bias = bref(buf_zeros);
-          m.a_ld = wg.Kpad; m.a_rows = wg.rows_a; m.b_rows = wg.rows_b;
           m.flops = 2.0 * o.c_out * static_cast<double>(wg.Ngemm) * wg.M;
-          L.add(std::move(m), {ab, bb, buf_ones, buf_zeros}, {part, gbuf});
+          if (mn) {
+            wgrad_mn_setup(d, nullptr, nullptr, nullptr, B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h,
+                           o.pad_w, wg, false);
+            m.g_in = bref(dy); m.g_wt = bref(xb);
+            L.add(std::move(m), {dy, xb, buf_ones, buf_zeros}, {part, gbuf});
+          } else {
+            m.g_in = bref(ab); m.g_wt = bref(bb);
+            m.a_ld = wg.Kpad; m.a_rows = wg.rows_a; m.b_rows = wg.rows_b;
+            L.add(std::move(m), {ab, bb, buf_ones, buf_zeros}, {part, gbuf});
+          }
         }
         if (wg.split > 1) {
           TrainOp r = TrainLowering::vg(VF_WGRAD_REDUCE, vg_grid_for(static_cast<int64_t>((wg.Ngemm + 3) / 4) * o.c_out));
@@ -3166,10 +3237,17 @@ int build_train_opdev(const Tenant& T, int tenant_id, const TrainOp& op, OpDev& 
   d.c_tma = 0;
   if (!encode || !d.in || !d.wt) return 0;
   int rc = 0;
-  if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, op.im2col_c);
-  else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[0], d.in, op.gemm_kind == 2 ? d.Kpad : d.K, op.a_rows, op.a_ld, BM);
-  if (!rc) rc = encode_rows(&maps[1], d.wt, d.Kpad, op.b_rows, d.Kpad, d.bn);
-  if (rc) return rc;
+  if (d.a_mode == A_MN) {
+    WgradGeom wg;
+    rc = wgrad_geom(d.B, d.H, d.W, d.C, d.M, d.kh, d.kw, d.stride, d.ph, d.pw, wg);
+    if (!rc) rc = wgrad_mn_setup(d, maps, d.wt, d.in, d.B, d.H, d.W, d.C, d.M, d.kh, d.kw, d.stride, d.ph, d.pw, wg, true);
+    if (rc) return rc;
+  } else {
+    if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, op.im2col_c);
+    else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[0], d.in, op.gemm_kind == 2 ? d.Kpad : d.K, op.a_rows, op.a_ld, BM);
+    if (!rc) rc = encode_rows(&maps[1], d.wt, d.Kpad, op.b_rows, d.Kpad, d.bn);
+    if (rc) return rc;
+  }
   if (op.gemm_kind != 2 && d.out && (static_cast<long long>(d.ldo) * 2) % 16 == 0) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Cout), static_cast<cuuint64_t>(d.M)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ldo) * 2};

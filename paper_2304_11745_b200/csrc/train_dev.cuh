@@ -833,6 +833,274 @@ VG_FN void vg_wgrad_reduce(const VArgs& a, int vb, int nvb, int tid, int nthr, u
   }
 }
 
+// ------------------------------------------------------------------ staged streaming
+// The elementwise operators (BN apply, ReLU backward, add, SGD) read and write
+// whole tensors once: HBM-bound.  Inside the executor only the 192-thread
+// worker group of ONE CTA per SM runs them, so register-held loads cannot
+// keep enough bytes in flight (~36 KB per SM measured ~0.9 TB/s chip-wide).
+// Staged path: one thread streams the item's contiguous range through shared
+// memory with bulk async copies (cp.async.bulk, mbarrier complete_tx), NS
+// stages of n_in x 8 KB in flight; the group computes in place and one
+// thread writes each chunk back with a bulk store.  Same per-element IEEE
+// operations as the register path (results bit-identical); only the
+// element -> thread assignment differs.
+constexpr int VGS_CH = 512;                   // 16-byte groups per chunk (8 KB per tensor)
+constexpr int VGS_MAX_STAGES = 8;
+
+__device__ __forceinline__ uint32_t vgs_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void vgs_mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(vgs_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void vgs_mbar_inval(uint64_t* b) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(vgs_u32(b)) : "memory");
+}
+__device__ __forceinline__ void vgs_mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(vgs_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void vgs_mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P;\nVGS_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra VGS_WAIT;\n}\n" ::"r"(vgs_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void vgs_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(vgs_u32(dst)), "l"(src), "r"(bytes), "r"(vgs_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void vgs_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+               ::"l"(dst), "r"(vgs_u32(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void vgs_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void vgs_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void vgs_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+// Operators as staged-stream kernels: in-place compute on the smem chunk.
+//   n_in input tensors (16-byte groups), results written over slot out_slot[k]
+//   and stored to out[k].  prepare(): per-item constants into `extra` smem.
+struct VgsBnApply {   // a: p0 x, p1 dy, p2 ym, p3 coef, p4 out; n0 M; i0 mode, i1 C, i2 relu
+  const VArgs& a;
+  int n_in, C, G8, mode, relu;
+  __device__ explicit VgsBnApply(const VArgs& a_) : a(a_) {
+    mode = a.i[0]; C = a.i[1]; G8 = C / 8; relu = a.i[2];
+    n_in = mode == 0 ? 1 : (a.p[2] ? 3 : 2);
+  }
+  __device__ const void* in(int k) const { return a.p[k]; }
+  __device__ int n_out() const { return 1; }
+  __device__ void* out(int) const { return const_cast<void*>(a.p[4]); }
+  __device__ int out_slot(int) const { return 0; }
+  __device__ int extra_bytes() const { return (mode == 0 ? 2 : 3) * C * 4; }
+  __device__ void prepare(float* ex, int tid, int nthr) const {
+    const float* coef = static_cast<const float*>(a.p[3]);
+    const int n = (mode == 0 ? 2 : 3) * C;
+    for (int i = tid; i < n; i += nthr) ex[i] = coef[i];
+  }
+  __device__ void apply(uint4* const* sl, int j, int64_t gi, const float* ex) const {
+    const int c = static_cast<int>(gi % G8) * 8;
+    float v[8];
+    vg_unpack8(sl[0][j], v);
+    const float4* k0 = reinterpret_cast<const float4*>(ex + c);
+    const float4* k1 = reinterpret_cast<const float4*>(ex + C + c);
+    const float4 a0 = k0[0], a1 = k0[1], b0 = k1[0], b1 = k1[1];
+    const float K0[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float K1[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    if (mode == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float t = fmaf(v[q], K0[q], K1[q]);
+        v[q] = relu ? fmaxf(t, 0.0f) : t;
+      }
+    } else {
+      const float4* k2 = reinterpret_cast<const float4*>(ex + 2 * C + c);
+      const float4 c0 = k2[0], c1 = k2[1];
+      const float K2[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      float d[8];
+      vg_unpack8(sl[1][j], d);
+      if (n_in == 3) {
+        float mk[8];
+        vg_unpack8(sl[2][j], mk);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = mk[q] > 0.0f ? d[q] : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = fmaf(K0[q], d[q], fmaf(K1[q], v[q], K2[q]));
+    }
+    sl[0][j] = vg_pack8(v);
+  }
+};
+struct VgsReluBwd {   // a: p0 x, p1 dy, p2 dx; n0 n8; i0 six
+  const VArgs& a;
+  int n_in = 2;
+  __device__ explicit VgsReluBwd(const VArgs& a_) : a(a_) {}
+  __device__ const void* in(int k) const { return a.p[k]; }
+  __device__ int n_out() const { return 1; }
+  __device__ void* out(int) const { return const_cast<void*>(a.p[2]); }
+  __device__ int out_slot(int) const { return 1; }
+  __device__ int extra_bytes() const { return 0; }
+  __device__ void prepare(float*, int, int) const {}
+  __device__ void apply(uint4* const* sl, int j, int64_t, const float*) const {
+    const int six = a.i[0];
+    float v[8], d[8];
+    vg_unpack8(sl[0][j], v);
+    vg_unpack8(sl[1][j], d);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = (v[q] > 0.0f && (!six || v[q] < 6.0f)) ? d[q] : 0.0f;
+    sl[1][j] = vg_pack8(d);
+  }
+};
+struct VgsAdd {       // a: p0 a, p1 b, p2 y; n0 n8; i0 relu
+  const VArgs& a;
+  int n_in = 2;
+  __device__ explicit VgsAdd(const VArgs& a_) : a(a_) {}
+  __device__ const void* in(int k) const { return a.p[k]; }
+  __device__ int n_out() const { return 1; }
+  __device__ void* out(int) const { return const_cast<void*>(a.p[2]); }
+  __device__ int out_slot(int) const { return 0; }
+  __device__ int extra_bytes() const { return 0; }
+  __device__ void prepare(float*, int, int) const {}
+  __device__ void apply(uint4* const* sl, int j, int64_t, const float*) const {
+    const int relu = a.i[0];
+    float p[8], q8[8];
+    vg_unpack8(sl[0][j], p);
+    vg_unpack8(sl[1][j], q8);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float t = p[q] + q8[q];
+      p[q] = relu ? fmaxf(t, 0.0f) : t;
+    }
+    sl[0][j] = vg_pack8(p);
+  }
+};
+struct VgsSgd {       // fp32 float4 groups.  a: p0 w, p1 g, p2 buf; n0 n; i0 first; f0 lr, f1 momentum
+  const VArgs& a;
+  int n_in = 3;
+  __device__ explicit VgsSgd(const VArgs& a_) : a(a_) {}
+  __device__ const void* in(int k) const { return a.p[k]; }
+  __device__ int n_out() const { return 2; }
+  __device__ void* out(int k) const { return const_cast<void*>(a.p[k == 0 ? 0 : 2]); }
+  __device__ int out_slot(int k) const { return k == 0 ? 0 : 2; }
+  __device__ int extra_bytes() const { return 0; }
+  __device__ void prepare(float*, int, int) const {}
+  __device__ void apply(uint4* const* sl, int j, int64_t, const float*) const {
+    const int first = a.i[0];
+    const float lr = a.f[0], mom = a.f[1];
+    float* w = reinterpret_cast<float*>(sl[0] + j);
+    const float* g = reinterpret_cast<const float*>(sl[1] + j);
+    float* buf = reinterpret_cast<float*>(sl[2] + j);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float b = first ? g[q] : fmaf(mom, buf[q], g[q]);
+      buf[q] = b;
+      w[q] = fmaf(-lr, b, w[q]);
+    }
+  }
+};
+
+// Stream 16-byte groups [g0, g1) of the operator through `smem` (smem_bytes).
+template <class Op>
+__device__ void vgs_run(const Op& op, int64_t g0, int64_t g1, int tid, int nthr, uint8_t* smem, int smem_bytes) {
+  if (g1 <= g0) return;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                      // [VGS_MAX_STAGES]
+  float* extra = reinterpret_cast<float*>(smem + 128);
+  const int ex_bytes = (op.extra_bytes() + 127) & ~127;
+  uint8_t* stages = smem + 128 + ex_bytes;
+  const int stage_bytes = op.n_in * VGS_CH * 16;
+  int ns = (smem_bytes - 128 - ex_bytes) / stage_bytes;
+  ns = ns > VGS_MAX_STAGES ? VGS_MAX_STAGES : ns;
+  const int64_t nch = (g1 - g0 + VGS_CH - 1) / VGS_CH;
+  auto chunk_len = [&](int64_t k) -> int {
+    const int64_t b = g0 + k * VGS_CH, e = b + VGS_CH < g1 ? b + VGS_CH : g1;
+    return static_cast<int>(e - b);
+  };
+  auto issue_load = [&](int64_t k) {
+    const int st = static_cast<int>(k % ns);
+    const int len = chunk_len(k);
+    const uint32_t bytes = static_cast<uint32_t>(len) * 16u;
+    vgs_mbar_expect(&bars[st], bytes * op.n_in);
+    for (int t = 0; t < op.n_in; ++t)
+      vgs_load(stages + st * stage_bytes + t * VGS_CH * 16,
+               static_cast<const uint8_t*>(op.in(t)) + (g0 + k * VGS_CH) * 16, bytes, &bars[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < ns; ++st) vgs_mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");   // acquired inputs -> the async proxy
+    for (int64_t k = 0; k < nch && k < ns; ++k) issue_load(k);
+  }
+  op.prepare(extra, tid, nthr);
+  vg_bar(nthr);
+  for (int64_t k = 0; k < nch; ++k) {
+    const int st = static_cast<int>(k % ns);
+    vgs_mbar_wait(&bars[st], static_cast<uint32_t>((k / ns) & 1));
+    uint4* sl[3];
+    for (int t = 0; t < 3; ++t)
+      sl[t] = reinterpret_cast<uint4*>(stages + st * stage_bytes + (t < op.n_in ? t : 0) * VGS_CH * 16);
+    const int len = chunk_len(k);
+    const int64_t base = g0 + k * VGS_CH;
+    for (int j = tid; j < len; j += nthr) op.apply(sl, j, base + j, extra);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic smem writes -> bulk store
+    vg_bar(nthr);
+    if (tid == 0) {
+      for (int o = 0; o < op.n_out(); ++o)
+        vgs_store(static_cast<uint8_t*>(op.out(o)) + base * 16, sl[op.out_slot(o)], static_cast<uint32_t>(len) * 16u);
+      vgs_commit();
+      if (k + ns < nch) {
+        vgs_wait_read0();   // the stage's results are read out before it is refilled
+        issue_load(k + ns);
+      }
+    }
+  }
+  if (tid == 0) {
+    vgs_wait0();                                           // results written before the item is released
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    for (int st = 0; st < ns; ++st) vgs_mbar_inval(&bars[st]);
+  }
+  vg_bar(nthr);
+}
+
+__device__ __forceinline__ bool vg_streamable(int fn) {
+  return fn == VF_BN_APPLY || fn == VF_RELU_BWD || fn == VF_ADD || fn == VF_SGD;
+}
+
+// Virtual blocks [v0, v1) of an nvb-block streaming operator, staged: the
+// blocks' 16-byte groups form one contiguous range (block vb owns groups
+// [vb * per, (vb + 1) * per)).  SGD's fp32 tail (n % 4) is done by thread 0 of
+// the item that owns the last group.
+VG_FN void vg_stream_item(int fn, const VArgs& a, int v0, int v1, int nvb, int tid, int nthr, uint8_t* smem,
+                          int smem_bytes) {
+  int64_t total;
+  switch (fn) {
+    case VF_BN_APPLY: total = a.n[0] * (a.i[1] / 8); break;
+    case VF_SGD: total = a.n[0] / 4; break;
+    default: total = a.n[0]; break;
+  }
+  const int64_t per = (total + nvb - 1) / nvb;
+  const int64_t g0 = v0 * per < total ? v0 * per : total;
+  const int64_t g1 = v1 * per < total ? v1 * per : total;
+  switch (fn) {
+    case VF_BN_APPLY: vgs_run(VgsBnApply(a), g0, g1, tid, nthr, smem, smem_bytes); break;
+    case VF_RELU_BWD: vgs_run(VgsReluBwd(a), g0, g1, tid, nthr, smem, smem_bytes); break;
+    case VF_ADD: vgs_run(VgsAdd(a), g0, g1, tid, nthr, smem, smem_bytes); break;
+    case VF_SGD: {
+      vgs_run(VgsSgd(a), g0, g1, tid, nthr, smem, smem_bytes);
+      if (v1 >= nvb && tid == 0) {   // fp32 tail past the last full float4 group
+        float* w = static_cast<float*>(const_cast<void*>(a.p[0]));
+        const float* g = static_cast<const float*>(a.p[1]);
+        float* buf = static_cast<float*>(const_cast<void*>(a.p[2]));
+        for (int64_t i = total * 4; i < a.n[0]; ++i) {
+          const float b = a.i[0] ? g[i] : fmaf(a.f[1], buf[i], g[i]);
+          buf[i] = b;
+          w[i] = fmaf(-a.f[0], b, w[i]);
+        }
+      }
+      break;
+    }
+    default: break;
+  }
+}
+
 // ------------------------------------------------------------------ dispatch
 __device__ inline void run_vgrid(int fn, const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
   switch (fn) {

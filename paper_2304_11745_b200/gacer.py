@@ -245,19 +245,21 @@ def graph_desc(graph, params, dtype="bf16", train=False, lr=0.1, momentum=0.9):
 
 
 def regulation_desc(decomposition=None, pointers=None, n_tenants=None):
-    """decomposition: list of (tenant, op_index (1-based), axis, sizes);
+    """decomposition: list of (tenant, op_index (1-based), axis, sizes[, sm_budget]);
     pointers: list (per tenant) of cut lists.  Returns (dec*, ptr*, keep)."""
     keep = []
     dp = None
     if decomposition is not None:
         n = len(decomposition)
         arr = (gacer_chunking * max(n, 1))()
-        for i, (t, oi, axis, sizes) in enumerate(decomposition):
+        for i, ent in enumerate(decomposition):
+            t, oi, axis, sizes = ent[:4]
+            budget = ent[4] if len(ent) > 4 else None   # per-chunk SM budgets (0 = unlimited)
             arr[i].tenant, arr[i].op_index = t, oi
             arr[i].axis = AXIS[axis] if isinstance(axis, str) else axis
             arr[i].n_chunks = len(sizes) if sizes is not None else 0
             arr[i].sizes = _iptr(sizes, keep) if sizes is not None else None
-            arr[i].sm_budget = None
+            arr[i].sm_budget = _iptr(budget, keep) if budget is not None else None
         keep.append(arr)
         dec = gacer_decomposition(n=n, items=C.cast(arr, C.POINTER(gacer_chunking)))
         keep.append(dec)

@@ -127,6 +127,7 @@ def test_error_codes_plan(host):
         ((None, [[7], [1]]), "GACER_E_CUT_OUT_OF_RANGE"),
         ((None, [[3, 2], [1, 1]]), "GACER_E_UNSORTED_CUTS"),
         ((None, [[-1], [1]]), "GACER_E_CUT_OUT_OF_RANGE"),
+        (([(0, 1, "batch", [1, 1], [2, -1])], None), "GACER_E_INVALID_ARG"),  # sm_budget < 0
     ]
     for (dec, ptr), name in cases:
         with pytest.raises(G.GacerError) as e:
@@ -162,6 +163,26 @@ def test_table3_plans_accepted(host):
         G.gacer_set_regulation(dec, None, n_tenants=2)
         # chunks own whole tiles: the decomposition never adds or drops work
         assert G.gacer_get_stats()["n_items"] == base
+
+
+def test_sm_budgets_accepted_and_work_preserving(host):
+    """gacer_chunking.sm_budget (W(O^B), l.597-601): per-chunk budgets are
+    part of a legal plan, a single chunk budgets an undecomposed op, and
+    budgets never add or drop work items (they only gate WHEN items run)."""
+    v16, r18 = workloads.build_model("vgg16"), workloads.build_model("resnet18")
+    register(v16, 8)
+    register(r18, 8)
+    base = G.gacer_get_stats()["n_items"]
+    convs = [i + 1 for i, op in enumerate(v16.ops) if op["kind"] == "conv"]
+    dec = [(0, i, "batch", [8], [24]) for i in convs]
+    dec += [(1, i + 1, "batch", [4, 4], [16, 0]) for i, op in enumerate(r18.ops) if op["kind"] == "conv"]
+    G.gacer_set_regulation(dec, [[len(v16.ops) // 2], [len(r18.ops) // 2]], n_tenants=2)
+    assert G.gacer_get_stats()["n_items"] == base
+    # a fused op whose members carry different budgets is rejected
+    i = convs[0]
+    with pytest.raises(G.GacerError) as e:
+        G.gacer_set_regulation([(0, i, "batch", [8], [24]), (0, i + 1, "batch", [8], [12])], None, n_tenants=2)
+    assert e.value.name == "GACER_E_INVALID_ARG"
 
 
 def test_identity_plan_and_fusion_counts(host):
