@@ -242,3 +242,32 @@ def test_conv_wgrad_tcgen05(T, N, H, W, Cin, Cout, k, s, p):
 def workloads_bf16(a):
     import workloads
     return workloads.bf16_round(np.asarray(a, np.float32)).astype(np.float64)
+
+
+@pytest.mark.parametrize("N,H,W,Cin,Cout,k,s,p", [(4, 14, 14, 64, 64, 3, 1, 1), (2, 15, 13, 64, 72, 3, 2, 1),
+                                                   (2, 7, 7, 512, 2048, 1, 1, 0)])
+def test_conv_wgrad_mn_major_matches_staged(T, N, H, W, Cin, Cout, k, s, p, monkeypatch):
+    """The weight gradient read in place with MN-major UMMA operands (A = dy,
+    B = the im2col TMA view of x; no staged transposes) computes the same
+    products in the same K order as the staged K-major form: the two agree to
+    fp32 rounding of the accumulation."""
+    torch, G, OT = T
+    rng = np.random.default_rng(Cin + 5 * Cout + H)
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    x = _bf16(torch, rng.normal(size=(N, H, W, Cin)))
+    dy = _bf16(torch, rng.normal(size=(N, Ho, Wo, Cout)))
+    outs = []
+    for staged in ("0", "1"):
+        monkeypatch.setenv("GACER_WGRAD_STAGED", staged)
+        dw = torch.empty((Cout, Cin, k, k), device="cuda")
+        G.gacer_init(0)
+        try:
+            nb = G.conv_wgrad_workspace(N, H, W, Cin, Cout, k, k, s, p, p)
+            ws = torch.zeros(nb + 256, dtype=torch.uint8, device="cuda")
+            base = (ws.data_ptr() + 255) // 256 * 256
+            G.conv_wgrad(x.data_ptr(), dy.data_ptr(), N, H, W, Cin, Cout, k, k, s, p, p, dw.data_ptr(), base, nb)
+            torch.cuda.synchronize()
+        finally:
+            G.gacer_shutdown()
+        outs.append(dw.cpu().numpy())
+    assert maxrel(outs[0], outs[1]) <= 1e-5, maxrel(outs[0], outs[1])
