@@ -48,6 +48,12 @@ def _apply(op, params, ins):
     if k == "linear":
         p = params[op["id"]]
         return ops.linear(x.reshape(x.shape[0], -1), p["w"], p.get("b"))
+    if k == "hardswish":
+        return ops.hardswish(x)
+    if k == "hardsigmoid":
+        return ops.hardsigmoid(x)
+    if k == "mul":          # squeeze-and-excitation scale: x * s broadcast over H, W
+        return ops.scale_channels(x, ins[1])
     if k == "add":
         return ops.add(ins[0], ins[1])
     if k == "concat":
@@ -98,9 +104,9 @@ def _channel_chunk(op, params, ins, c0, c1):
         return _apply(sub, _slice_params(op, params, c0, c1), ins)
     if k in ("bn",):
         return _apply(sub, _slice_params(op, params, c0, c1), [ins[0][:, c0:c1]])
-    if k in ("relu", "relu6", "maxpool", "avgpool", "gap", "dropout"):
+    if k in ("relu", "relu6", "hardswish", "hardsigmoid", "maxpool", "avgpool", "gap", "dropout"):
         return _apply(sub, params, [ins[0][:, c0:c1]])
-    if k == "add":
+    if k in ("add", "mul"):
         return _apply(sub, params, [a[:, c0:c1] for a in ins])
     raise ValueError(f"channel split not defined for {k}")
 

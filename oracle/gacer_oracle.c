@@ -154,6 +154,36 @@ void oracle_add(const double* a, const double* b, size_t n, double* y) {
   for (size_t i = 0; i < n; ++i) y[i] = a[i] + b[i];
 }
 
+/* hardswish (MobileNetV3, PyTorch Hardswish): y = x * relu6(x + 3) / 6 */
+void oracle_hardswish(const double* x, size_t n, double* y) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < n; ++i) {
+    double t = x[i] + 3.0;
+    t = t < 0.0 ? 0.0 : (t > 6.0 ? 6.0 : t);
+    y[i] = x[i] * t / 6.0;
+  }
+}
+
+/* hardsigmoid (PyTorch Hardsigmoid, the SE gate of MobileNetV3):
+ * y = relu6(x + 3) / 6 */
+void oracle_hardsigmoid(const double* x, size_t n, double* y) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < n; ++i) {
+    double t = x[i] + 3.0;
+    t = t < 0.0 ? 0.0 : (t > 6.0 ? 6.0 : t);
+    y[i] = t / 6.0;
+  }
+}
+
+/* channel scale (squeeze-and-excitation): y[n,c,p] = x[n,c,p] * s[n,c] */
+void oracle_scale_channels(const double* x, const double* s, int N, int C, int HW, double* y) {
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int n = 0; n < N; ++n)
+    for (int c = 0; c < C; ++c)
+      for (int p = 0; p < HW; ++p)
+        y[((size_t)n * C + c) * HW + p] = x[((size_t)n * C + c) * HW + p] * s[(size_t)n * C + c];
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   extern int omp_get_max_threads(void);

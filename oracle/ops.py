@@ -42,6 +42,9 @@ def lib():
         _lib.oracle_gap.argtypes = [D, i, i, i, D]
         _lib.oracle_linear.argtypes = [D, D, D, i, i, i, D]
         _lib.oracle_add.argtypes = [D, D, sz, D]
+        _lib.oracle_hardswish.argtypes = [D, sz, D]
+        _lib.oracle_hardsigmoid.argtypes = [D, sz, D]
+        _lib.oracle_scale_channels.argtypes = [D, D, i, i, i, D]
         _lib.oracle_num_threads.restype = ctypes.c_int
     return _lib
 
@@ -136,6 +139,31 @@ def add(a, b):
     assert a.shape == b.shape
     y = np.empty_like(a)
     lib().oracle_add(_p(a), _p(b), a.size, _p(y))
+    return y
+
+
+def hardswish(x):
+    x = _f64(x)
+    y = np.empty_like(x)
+    lib().oracle_hardswish(_p(x), x.size, _p(y))
+    return y
+
+
+def hardsigmoid(x):
+    x = _f64(x)
+    y = np.empty_like(x)
+    lib().oracle_hardsigmoid(_p(x), x.size, _p(y))
+    return y
+
+
+def scale_channels(x, s):
+    """y[n, c, ...] = x[n, c, ...] * s[n, c] (s: [N, C] or [N, C, 1, 1])."""
+    x = _f64(x)
+    N, C = x.shape[:2]
+    s = _f64(s).reshape(N, C)
+    HW = int(np.prod(x.shape[2:])) if x.ndim > 2 else 1
+    y = np.empty_like(x)
+    lib().oracle_scale_channels(_p(x), _p(s), N, C, HW, _p(y))
     return y
 
 

@@ -30,8 +30,10 @@ def load_into_torch(graph, params, tmodel):
                 m.running_var.copy_(torch.from_numpy(p["var"]))
                 m.eps = op["eps"]
             else:
-                assert tuple(m.weight.shape) == p["w"].shape, (op, m)
-                m.weight.copy_(torch.from_numpy(p["w"]))
+                # (a linear of ours may be torchvision's 1x1 conv on a pooled
+                #  map: MobileNetV3's squeeze-and-excitation FCs)
+                assert m.weight.numel() == p["w"].size and m.weight.shape[0] == p["w"].shape[0], (op, m)
+                m.weight.copy_(torch.from_numpy(p["w"]).reshape(m.weight.shape))
                 if "b" in p:
                     m.bias.copy_(torch.from_numpy(p["b"]))
                 else:
@@ -49,11 +51,14 @@ TV = {
     "alexnet": lambda: torchvision.models.alexnet(),
     "inception_v3": lambda: torchvision.models.inception_v3(
         aux_logits=False, init_weights=False, transform_input=False),
+    "mobilenet_v3_large": lambda: torchvision.models.mobilenet_v3_large(),
+    "densenet121": lambda: torchvision.models.densenet121(),
 }
 
 CASES = [("resnet18", 64, 2), ("resnet50", 64, 2), ("mobilenet_v2", 64, 2),
          ("alexnet", 224, 1), ("vgg16", 224, 1), ("inception_v3", 224, 1),
-         ("resnet101", 64, 1), ("resnet34", 64, 1)]
+         ("resnet101", 64, 1), ("resnet34", 64, 1), ("mobilenet_v3_large", 64, 2),
+         ("densenet121", 64, 1)]
 
 
 @pytest.mark.parametrize("name,hw,batch", CASES)
@@ -95,7 +100,8 @@ def test_tiny_tenants_vs_torch():
     assert np.max(np.abs(forward_graph(g, p, x) - t.numpy())) < 1e-12
 
 
-@pytest.mark.parametrize("name,hw", [("resnet18", 32), ("mobilenet_v2", 32)])
+@pytest.mark.parametrize("name,hw", [("resnet18", 32), ("mobilenet_v2", 32), ("mobilenet_v3_large", 32),
+                                     ("densenet121", 32)])
 def test_batch_independence(name, hw):
     g = workloads.build_model(name, hw)
     p = workloads.make_params(g, 3)
@@ -110,7 +116,7 @@ def test_chunked_forward_is_exact(seed):
     """Eq. 5 decomposition (batch and channel) reproduces the undecomposed
     forward bit-for-bit in fp64."""
     rng = np.random.default_rng(seed)
-    name = ["resnet18", "mobilenet_v2"][seed % 2]
+    name = ["resnet18", "mobilenet_v2", "mobilenet_v3_large", "densenet121"][seed % 4]
     g = workloads.build_model(name, 32)
     p = workloads.make_params(g, seed)
     B = 4
@@ -125,7 +131,7 @@ def test_chunked_forward_is_exact(seed):
             cuts = np.sort(rng.choice(np.arange(1, B), size=n - 1, replace=False)) if n > 1 else []
             sizes = np.diff(np.concatenate([[0], cuts, [B]])).astype(int).tolist()
             dec[op["id"]] = ("batch", sizes)
-        elif r < 0.5 and op["kind"] in ("conv", "linear", "bn", "relu", "relu6"):
+        elif r < 0.5 and op["kind"] in ("conv", "linear", "bn", "relu", "relu6", "hardswish"):
             C = op.get("c_out", op.get("c"))
             if C is None or C < 2:
                 continue

@@ -130,3 +130,25 @@ def test_linear_bn_vs_torch():
     ref = F.batch_norm(torch.from_numpy(x), torch.from_numpy(m), torch.from_numpy(v),
                        torch.from_numpy(g), torch.from_numpy(be), False, 0.0, 1e-3).numpy()
     assert rel(ops.batchnorm(x, g, be, m, v, 1e-3), ref) < 1e-14
+
+
+def test_hardswish_hardsigmoid_closed_forms():
+    """MobileNetV3's activations (PAPER.md l.903, "M3"): PyTorch's
+    definitions x * relu6(x + 3) / 6 and relu6(x + 3) / 6 at hand-checked
+    points -- the knees (-3, 3), the saturation, the midpoint."""
+    x = np.array([-5.0, -3.0, -1.5, 0.0, 1.0, 3.0, 4.5])
+    assert np.array_equal(ops.hardswish(x), np.array([0.0, 0.0, -0.375, 0.0, 4.0 / 6.0, 3.0, 4.5]))
+    assert np.array_equal(ops.hardsigmoid(x), np.array([0.0, 0.0, 0.25, 0.5, 4.0 / 6.0, 1.0, 1.0]))
+
+
+def test_hardswish_hardsigmoid_scale_vs_torch():
+    import torch.nn.functional as F
+    rng = np.random.default_rng(5)
+    x = rng.normal(scale=4.0, size=(3, 5, 4, 6))
+    t = torch.from_numpy(x)
+    assert np.max(np.abs(ops.hardswish(x) - F.hardswish(t).numpy())) < 1e-15
+    assert np.max(np.abs(ops.hardsigmoid(x) - F.hardsigmoid(t).numpy())) < 1e-15
+    s = rng.uniform(0, 1, size=(3, 5))
+    ref = x * s[:, :, None, None]                 # numpy broadcasting (a library routine)
+    assert np.array_equal(ops.scale_channels(x, s), ref)
+    assert np.array_equal(ops.scale_channels(x, s.reshape(3, 5, 1, 1)), ref)

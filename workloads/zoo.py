@@ -71,6 +71,16 @@ class Graph:
     def linear(self, x, c_in, c_out, bias=True):
         return self._add("linear", [x], c_in=c_in, c_out=c_out, bias=bias)
 
+    def hardswish(self, x):
+        return self._add("hardswish", [x])
+
+    def hardsigmoid(self, x):
+        return self._add("hardsigmoid", [x])
+
+    def mul(self, x, s):
+        """x [N, C, H, W] * s [N, C] broadcast over H, W (squeeze-and-excitation)"""
+        return self._add("mul", [x, s])
+
     def add(self, a, b):
         return self._add("add", [a, b])
 
@@ -92,6 +102,8 @@ class Graph:
             y = self.relu(y)
         elif act == "relu6":
             y = self.relu6(y)
+        elif act == "hardswish":
+            y = self.hardswish(y)
         return y
 
 
@@ -318,6 +330,93 @@ def inception_v3() -> Graph:
     return g
 
 
+# --------------------------------------------------------------------------
+# MobileNetV3-large (torchvision mobilenet_v3_large; the paper's "M3", PAPER.md
+# l.903).  BN eps 1e-3; squeeze-and-excitation = GAP -> FC(+ReLU) -> FC ->
+# hardsigmoid -> channel scale (torchvision's 1x1 convs on the pooled map,
+# written as linears); gain-1 init as for MobileNetV2.
+# --------------------------------------------------------------------------
+def _make_divisible(v, d=8):
+    nv = max(d, int(v + d / 2) // d * d)
+    if nv < 0.9 * v:
+        nv += d
+    return nv
+
+
+def mobilenet_v3_large() -> Graph:
+    g = Graph("mobilenet_v3_large", 3, 224, 224, init_gain=1.0)
+    eps = 1e-3
+    x = g.cba(0, 3, 16, 3, 2, 1, act="hardswish", eps=eps)
+    c_in = 16
+    cfg = [(3, 16, 16, False, "relu", 1), (3, 64, 24, False, "relu", 2), (3, 72, 24, False, "relu", 1),
+           (5, 72, 40, True, "relu", 2), (5, 120, 40, True, "relu", 1), (5, 120, 40, True, "relu", 1),
+           (3, 240, 80, False, "hardswish", 2), (3, 200, 80, False, "hardswish", 1),
+           (3, 184, 80, False, "hardswish", 1), (3, 184, 80, False, "hardswish", 1),
+           (3, 480, 112, True, "hardswish", 1), (3, 672, 112, True, "hardswish", 1),
+           (5, 672, 160, True, "hardswish", 2), (5, 960, 160, True, "hardswish", 1),
+           (5, 960, 160, True, "hardswish", 1)]
+    for k, exp, out, se, act, stride in cfg:
+        use_res = stride == 1 and c_in == out
+        y = x
+        if exp != c_in:
+            y = g.cba(y, c_in, exp, 1, act=act, eps=eps)
+        y = g.cba(y, exp, exp, k, stride, (k - 1) // 2, groups=exp, act=act, eps=eps)
+        if se:
+            sq = _make_divisible(exp // 4, 8)
+            s = g.gap(y)
+            s = g.relu(g.linear(s, exp, sq))
+            s = g.hardsigmoid(g.linear(s, sq, exp))
+            y = g.mul(y, s)
+        y = g.cba(y, exp, out, 1, act=None, eps=eps, res_last=use_res)
+        x = g.add(y, x) if use_res else y
+        c_in = out
+    x = g.cba(x, c_in, 960, 1, act="hardswish", eps=eps)
+    x = g.gap(x)
+    x = g.flatten(x)
+    x = g.hardswish(g.linear(x, 960, 1280))
+    x = g.dropout(x)
+    x = g.linear(x, 1280, 1000)
+    g.n_classes = 1000
+    return g
+
+
+# --------------------------------------------------------------------------
+# DenseNet-121 (torchvision densenet121; the paper's "D121").
+# Dense layer = BN -> ReLU -> conv1x1 (4 x 32) -> BN -> ReLU -> conv3x3 (32),
+# its input the concatenation of every earlier feature map of the block
+# (written as nested concats: feat_l = concat(feat_{l-1}, y_l), one channel
+# prefix of the block's buffer each); transition = BN -> ReLU -> conv1x1
+# (C/2) -> avgpool 2x2; head = BN -> ReLU -> GAP -> FC.
+# --------------------------------------------------------------------------
+def densenet121() -> Graph:
+    g = Graph("densenet121", 3, 224, 224)
+    x = g.conv(0, 3, 64, 7, 2, 3)
+    x = g.relu(g.bn(x, 64))
+    x = g.maxpool(x, 3, 2, 1)
+    c = 64
+    for bi, n_layers in enumerate((6, 12, 24, 16)):
+        feat = x
+        for _ in range(n_layers):
+            h = g.relu(g.bn(feat, c))
+            h = g.conv(h, c, 128, 1)
+            h = g.relu(g.bn(h, 128))
+            y = g.conv(h, 128, 32, 3, 1, 1)
+            feat = g.concat([feat, y])
+            c += 32
+        x = feat
+        if bi < 3:
+            x = g.relu(g.bn(x, c))
+            x = g.conv(x, c, c // 2, 1)
+            x = g.avgpool(x, 2, 2)
+            c //= 2
+    x = g.relu(g.bn(x, c))
+    x = g.gap(x)
+    x = g.flatten(x)
+    x = g.linear(x, c, 1000)
+    g.n_classes = 1000
+    return g
+
+
 MODELS = {
     "tiny_cnn": tiny_cnn,
     "tiny_mlp": tiny_mlp,
@@ -329,6 +428,8 @@ MODELS = {
     "alexnet": alexnet,
     "mobilenet_v2": mobilenet_v2,
     "inception_v3": inception_v3,
+    "mobilenet_v3_large": mobilenet_v3_large,
+    "densenet121": densenet121,
 }
 
 
@@ -349,8 +450,16 @@ CONFIGS: Dict[str, list] = {
     "d3_five": [("alexnet", 16, "bf16"), ("resnet18", 16, "bf16"),
                 ("resnet101", 16, "bf16"), ("inception_v3", 16, "bf16"),
                 ("mobilenet_v2", 16, "bf16")],
+    # the paper's Table 2 vision mixes at batch 8
+    # (the paper's batches are unstated there): not BASELINE configs, used by
+    # the plan sweeps and NEXT-2
+    "t2_alex_v16_r18": [("alexnet", 8, "bf16"), ("vgg16", 8, "bf16"), ("resnet18", 8, "bf16")],
+    "t2_r50_v16_m3": [("resnet50", 8, "bf16"), ("vgg16", 8, "bf16"), ("mobilenet_v3_large", 8, "bf16")],
+    "t2_r101_d121_m3": [("resnet101", 8, "bf16"), ("densenet121", 8, "bf16"),
+                        ("mobilenet_v3_large", 8, "bf16")],
 }
-CONFIG_INDEX = {"d1_tiny": 1, "d2_r50_v16_mv2": 2, "d3_five": 3, "d4_mixed": 4}
+CONFIG_INDEX = {"d1_tiny": 1, "d2_r50_v16_mv2": 2, "d3_five": 3, "d4_mixed": 4,
+                "t2_alex_v16_r18": 6, "t2_r50_v16_m3": 7, "t2_r101_d121_m3": 8}
 # BASELINE.json configs[3] (D4): ResNet-50 TRAINING (batch 64; one SGD step per
 # round) co-located with MobileNetV2 + VGG-16 inference (batch 8, SURVEY §8(d)
 # D4: the inference batch is unstated in BASELINE, 8 as in D2).  Entries:
