@@ -556,7 +556,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gacer", choices=["gacer", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default=CONFIG, choices=["d1_tiny", "d2_r50_v16_mv2", "d3_five", "d4_mixed"])
+    ap.add_argument("--config", default=CONFIG, choices=["d1_tiny", "d2_r50_v16_mv2", "d3_five", "d4_mixed",
+                                                         "t2_alex_v16_r18", "t2_r50_v16_m3", "t2_r101_d121_m3"])
     ap.add_argument("--plan", default="sweep", choices=["identity", "sweep"])
     ap.add_argument("--no-search", action="store_true", help="skip the Algorithm 1 plan search")
     ap.add_argument("--search-evals", type=int, default=30)

@@ -73,7 +73,10 @@ typedef enum {
   GACER_OP_RELU = 9,
   GACER_OP_RELU6 = 10,
   GACER_OP_FLATTEN = 11, /* NCHW-order flatten (identity on the data; reorders LINEAR weights) */
-  GACER_OP_DROPOUT = 12  /* identity (inference) */
+  GACER_OP_DROPOUT = 12, /* identity (inference) */
+  GACER_OP_HARDSWISH = 13,   /* x * relu6(x + 3) / 6 (MobileNetV3, "M3") */
+  GACER_OP_HARDSIGMOID = 14, /* relu6(x + 3) / 6 (the squeeze-and-excitation gate) */
+  GACER_OP_MUL = 15          /* 2 preds: x [C,H,W] * s [C,1,1] broadcast over H, W (SE channel scale) */
 } gacer_op_kind;
 
 typedef enum { GACER_DTYPE_BF16 = 1, GACER_DTYPE_FP32 = 2 } gacer_dtype;

@@ -255,6 +255,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 __device__ __forceinline__ float apply_act(float v, int act) {
   if (act == ACT_RELU) v = fmaxf(v, 0.0f);
   else if (act == ACT_RELU6) v = fminf(fmaxf(v, 0.0f), 6.0f);
+  else if (act == ACT_HSWISH) v = v * fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
+  else if (act == ACT_HSIGMOID) v = fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
   return v;
 }
 
@@ -766,7 +768,22 @@ __device__ __forceinline__ void cc_pixel(const OpDev& op, int m, int c, int HoWo
   float y[8];
   if (op.kind == DK_ELTWISE) {
     load8<F32>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
-    if (op.has_skip) {
+    if (op.affine) {   // standalone BatchNorm (folded scale / bias), e.g. DenseNet's pre-activation
+      const float4 s0 = *reinterpret_cast<const float4*>(op.scale + c);
+      const float4 s1 = *reinterpret_cast<const float4*>(op.scale + c + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(op.bias + c);
+      const float4 b1 = *reinterpret_cast<const float4*>(op.bias + c + 4);
+      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
+    }
+    if (op.has_skip == 2) {   // channel scale: * s[n][c] (squeeze-and-excitation)
+      float s[8];
+      load8<F32>(op.skip, static_cast<size_t>(b) * op.lds + c, s);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] *= s[q];
+    } else if (op.has_skip) {
       float s[8];
       load8<F32>(op.skip, static_cast<size_t>(m) * op.lds + c, s);
 #pragma unroll
@@ -1647,7 +1664,8 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
                                                          : make_uint4(0, 0, 0, 0);
       }
     }
-    if (split == 1 && !staged && !op.out_f32 && !swap) {
+    const bool lean_act = op.act <= ACT_RELU6;   // clamp-only activations (hardswish: general path)
+    if (split == 1 && !staged && !op.out_f32 && !swap && lean_act) {
       // lean direct bf16 path: same math as the staged path below, each
       // thread storing its row's 8-column groups with 16-byte global stores
       // (no staging buffer, no TMA-store waits)
@@ -1706,7 +1724,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       }
       if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
         p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
-    } else if (split == 1 && staged && !op.out_f32) {
+    } else if (split == 1 && staged && !op.out_f32 && lean_act) {
 #if GACER_EPI_V == 0
       // lean staged bf16 path: branch-free activation clamp, 64-column
       // staging chunks (a compile-time constant), scale/bias by shuffle

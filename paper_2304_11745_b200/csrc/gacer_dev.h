@@ -71,7 +71,7 @@ struct VArgs {
   float f[4];
 };
 
-enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2 };
+enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2, ACT_HSWISH = 3, ACT_HSIGMOID = 4 };
 
 // GEMM tile geometry
 constexpr int BM = 128;           // rows per tile (UMMA M)
@@ -124,7 +124,7 @@ struct OpDev {
   int32_t f32;             // 1 = fp32 tenant (inputs/weights fp32), 0 = bf16
   int32_t swap;            // GEMM: 1 = swap-AB linear (A = weights, B = activations)
   int32_t cip;             // avgpool count_include_pad
-  int32_t has_skip;
+  int32_t has_skip;        // 1: + skip (same shape); 2: * skip[n][c] (channel scale, DK_ELTWISE)
 
   // input activation tensor, NHWC: elem(n,h,w,c) = in[((n*H + h)*W + w)*ldi + c]
   const void* in;
@@ -146,7 +146,8 @@ struct OpDev {
   int32_t split_k, nkb;    // nkb = Kpad / BK
   const void* wt;          // packed weights: bf16 [Npad or Mpad][Kpad] K-major (fp32 [Cout][K] for SIMT);
                            // DW: [kh*kw][C] channel-minor
-  int32_t ldw, pad2;
+  int32_t ldw;
+  int32_t affine;          // DK_ELTWISE: y = x * scale + bias first (a standalone BatchNorm)
   const void* act_b;       // swap-AB: activations as the B operand, row stride ldb (elements)
   int32_t ldb;
   int32_t partials_only;   // split-K: write the per-split partials only (reduced by a separate kernel)

@@ -117,6 +117,8 @@ struct FusedOp {
   int in_t = -1, skip_t = -1, out_t = -1;
   int act = ACT_NONE;
   bool swap = false;
+  bool affine = false;   // DK_ELTWISE: a standalone BatchNorm (scale / bias applied first)
+  bool mul = false;      // DK_ELTWISE: channel scale by skip_t [B][C] (squeeze-and-excitation)
   // geometry
   int Cin = 0, H = 0, W = 0, Cout = 0, Ho = 0, Wo = 0;
   int kh = 1, kw = 1, stride = 1, ph = 0, pw = 0;
@@ -303,6 +305,17 @@ int upload_train_tenant(Tenant& T);
 
 // ------------------------------------------------------------------------
 // registration: validation + shape inference + fusion + packing
+// activation op kind -> fused activation (ACT_NONE: not an activation)
+int act_of(int kind) {
+  switch (kind) {
+    case GACER_OP_RELU: return ACT_RELU;
+    case GACER_OP_RELU6: return ACT_RELU6;
+    case GACER_OP_HARDSWISH: return ACT_HSWISH;
+    case GACER_OP_HARDSIGMOID: return ACT_HSIGMOID;
+    default: return ACT_NONE;
+  }
+}
+
 // ------------------------------------------------------------------------
 int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
   const int n = g->n_ops;
@@ -385,7 +398,9 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
       case GACER_OP_CONCAT: if (o.n_preds < 1) rc = set_err(GACER_E_INVALID_ARG, "concat needs preds"); break;
       case GACER_OP_CONV2D: case GACER_OP_LINEAR: case GACER_OP_MAXPOOL: case GACER_OP_AVGPOOL:
       case GACER_OP_GAP: case GACER_OP_BN: case GACER_OP_RELU: case GACER_OP_RELU6:
+      case GACER_OP_HARDSWISH: case GACER_OP_HARDSIGMOID:
       case GACER_OP_FLATTEN: case GACER_OP_DROPOUT: rc = need_preds(1); break;
+      case GACER_OP_MUL: rc = need_preds(2); break;
       default: rc = set_err(GACER_E_UNSUPPORTED_OP, "op %d: unknown kind %d", o.id, o.kind);
     }
     if (rc) return rc;
@@ -435,8 +450,15 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;
         break;
       case GACER_OP_RELU: case GACER_OP_RELU6: case GACER_OP_DROPOUT:
+      case GACER_OP_HARDSWISH: case GACER_OP_HARDSIGMOID:
         y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;
         break;
+      case GACER_OP_MUL: {   // x [C,H,W] * s [C,1,1] (squeeze-and-excitation channel scale)
+        const Tensor& sc = T.tensors[tens_of(o.preds[1])];
+        if (sc.C != x.C || sc.H != 1 || sc.W != 1) return set_err(GACER_E_SHAPE, "op %d: mul scale shape", o.id);
+        y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;
+        break;
+      }
       case GACER_OP_FLATTEN:
         y.C = x.C; y.H = x.H; y.W = x.W; T.orig_out_c[i] = x.C;   // data unchanged (NHWC storage)
         break;
@@ -518,8 +540,8 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           if (a == b || other == 0) break;  // x + x or a skip from the raw input: not fused
           F.skip_t = other;
           has_add = true;
-        } else if (co.kind == GACER_OP_RELU || co.kind == GACER_OP_RELU6) {
-          F.act = co.kind == GACER_OP_RELU ? ACT_RELU : ACT_RELU6;
+        } else if (act_of(co.kind) != ACT_NONE) {
+          F.act = act_of(co.kind);
           F.members.push_back(c);
           taken[c] = 1;
           tail = c;
@@ -552,12 +574,24 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         try_extend(false, false);
         break;
       }
-      case GACER_OP_RELU: case GACER_OP_RELU6:
+      case GACER_OP_MUL: {
         F.kind = DK_ELTWISE;
-        F.act = o.kind == GACER_OP_RELU ? ACT_RELU : ACT_RELU6;
+        F.skip_t = tens_of(o.preds[1]);
+        F.mul = true;
+        try_extend(false, false);
+        break;
+      }
+      case GACER_OP_RELU: case GACER_OP_RELU6: case GACER_OP_HARDSWISH: case GACER_OP_HARDSIGMOID:
+        F.kind = DK_ELTWISE;
+        F.act = act_of(o.kind);
         break;
       case GACER_OP_BN:
-        return set_err(GACER_E_UNSUPPORTED_OP, "op %d: BatchNorm not preceded by a fusable conv", o.id);
+        // a BatchNorm no conv produces (DenseNet's pre-activation on a concat):
+        // a per-channel affine CUDA-core op, its activation fused
+        F.kind = DK_ELTWISE;
+        F.affine = true;
+        try_extend(false, false);
+        break;
       default:
         return set_err(GACER_E_UNSUPPORTED_OP, "op %d: kind %d not lowered", o.id, o.kind);
     }
@@ -609,8 +643,13 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
       Tensor& P = T.tensors[pt];
       std::vector<int> cs;
       eff(P.producer_orig + 1, cs);
-      if (pt == 0 || cs.size() != 1 || P.sliced || P.buf == -2)
-        return set_err(GACER_E_UNSUPPORTED_OP, "concat op %d: input %d must be an op output consumed only by the concat",
+      // the producer writes straight into the concat buffer: it may feed one
+      // concat only (other consumers just read the slice -- DenseNet's
+      // nested feature concats, feat_l = concat(feat_{l-1}, y_l))
+      int n_concat = 0;
+      for (int c : cs) n_concat += g->ops[c].kind == GACER_OP_CONCAT;
+      if (pt == 0 || n_concat != 1 || P.sliced || P.buf == -2)
+        return set_err(GACER_E_UNSUPPORTED_OP, "concat op %d: input %d must be an op output feeding only this concat",
                        g->ops[i].id, g->ops[i].preds[j]);
       P.buf = C.buf;
       P.coff = C.coff + off;
@@ -656,7 +695,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
     if (F.in_t != 0 && X.C % 8 && F.kind != DK_SIMT_GEMM)
       return set_err(GACER_E_UNSUPPORTED_OP, "op %d: channel count %d not a multiple of 8", o.id, X.C);
     if ((Y.coff % 8) || (Y.ldc % 8 && Y.buf != -2)) return set_err(GACER_E_UNSUPPORTED_OP, "op %d: unaligned concat slice", o.id);
-    if (F.skip_t >= 0) {
+    if (F.skip_t >= 0 && !F.mul) {
       const Tensor& Sk = T.tensors[F.skip_t];
       if (Sk.C != Y.C || Sk.H != Y.H || Sk.W != Y.W) return set_err(GACER_E_SHAPE, "op %d: residual shape", o.id);
     }
@@ -912,7 +951,8 @@ OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
   d.f32 = f32 ? 1 : 0;
   d.swap = F.swap ? 1 : 0;
   d.cip = F.cip ? 1 : 0;
-  d.has_skip = F.skip_t >= 0 ? 1 : 0;
+  d.has_skip = F.skip_t >= 0 ? (F.mul ? 2 : 1) : 0;
+  d.affine = F.affine ? 1 : 0;
   d.in = tensor_addr(T, F.in_t);
   d.B = T.batch; d.H = F.H; d.W = F.W;
   d.C = (F.kind == DK_GEMM) ? F.cread : F.Cin;
@@ -1371,7 +1411,9 @@ int compile_plan(Plan& P) {
               const long long XHW = static_cast<long long>(X.H) * X.W;
               // flattened row range [lo, hi] of tensor tin this tile reads
               long long lo = s_lo * XHW, hi = (s_hi + 1) * XHW - 1;
-              if (tin == F.skip_t && F.rows_are_pixels && F.kind != DK_GAP) {
+              if (tin == F.skip_t && F.mul) {
+                // channel scale [B][C]: the samples of the tile's rows (lo, hi as set)
+              } else if (tin == F.skip_t && F.rows_are_pixels && F.kind != DK_GAP) {
                 lo = static_cast<long long>(mt) * F.bm;   // residual: same pixels as the output
                 hi = std::min<long long>(F.M, lo + F.bm) - 1;
               } else if (px_lo >= 0) {

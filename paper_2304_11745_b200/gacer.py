@@ -33,7 +33,8 @@ E = {
 STATUS = {v: k for k, v in E.items()}
 
 OP = {"conv": 1, "linear": 2, "maxpool": 3, "avgpool": 4, "gap": 5, "add": 6, "concat": 7,
-      "bn": 8, "relu": 9, "relu6": 10, "flatten": 11, "dropout": 12}
+      "bn": 8, "relu": 9, "relu6": 10, "flatten": 11, "dropout": 12,
+      "hardswish": 13, "hardsigmoid": 14, "mul": 15}
 DTYPE = {"bf16": 1, "fp32": 2}
 AXIS = {"none": 0, "batch": 1, "channel": 2}
 MODE = {"executor": 0, "sequential": 1, "multistream": 2, "executor_hostsync": 3}

@@ -268,3 +268,24 @@ def test_occupancy_stats(cuda_ok, d2):
         assert st2["stat_rounds"] == 2 and st2["barrier_wait_ns"] > 0
     finally:
         s.close()
+
+
+def test_bitwise_next2_mix(cuda_ok):
+    """Table 2's R101+D121+M3 mix (at 64^2 / B=2): outputs
+    byte-identical across random batch / channel plans (with SM budgets),
+    pointers, partitions and the two baselines."""
+    ts = []
+    for i, name in enumerate(("resnet101", "densenet121", "mobilenet_v3_large")):
+        g = workloads.build_model(name, 64)
+        ts.append((g, workloads.make_params(g, 80 + i, "bf16"), 2, "bf16", workloads.make_input(g, 2, 80 + i, "bf16")))
+    ref, _ = run(ts)
+    rng = np.random.default_rng(99)
+    variants = [dict(mode="sequential"), dict(mode="multistream"), dict(partition="work_conserving")]
+    for k in range(3):
+        dec, ptr = random_plan(ts, rng, n_pointers=k + 1)
+        dec = [d + ([int(rng.integers(0, 40))] * len(d[3]),) if j % 3 == 0 else d for j, d in enumerate(dec)]
+        variants.append(dict(plan=(dec, ptr)))
+    for v in variants:
+        out, _ = run(ts, **v)
+        for t, (a, b) in enumerate(zip(ref, out)):
+            assert a.tobytes() == b.tobytes(), (t, {kk: v[kk] for kk in v if kk != "plan"})

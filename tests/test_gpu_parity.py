@@ -142,6 +142,18 @@ def test_tenant_parity_d3_models(cuda_ok, name, hw, B):
     assert maxrel(outs[0], forward_graph(g, p, x)) <= 2e-2
 
 
+@pytest.mark.parametrize("name,hw,B", [("mobilenet_v3_large", 224, 2), ("densenet121", 224, 1),
+                                       ("densenet121", 64, 3), ("mobilenet_v3_large", 64, 3)])
+def test_tenant_parity_next2_models(cuda_ok, name, hw, B):
+    """NEXT-2: the paper's M3 (hardswish, 5x5 depthwise,
+    squeeze-and-excitation) and D121 (standalone BN+ReLU on nested zero-copy
+    concats) through the executor vs the fp64 oracle, 2e-2 (north_star)."""
+    t = make_tenant(name, B, "bf16", 4000 + B, hw)
+    outs, _ = run_session([t])
+    g, p, B, dt, x = t
+    assert maxrel(outs[0], forward_graph(g, p, x)) <= 2e-2
+
+
 @pytest.mark.parametrize("cin,cout,k,pad,hw,B", [(64, 64, 3, 1, 14, 2), (256, 64, 1, 0, 14, 3), (64, 128, 3, 1, 28, 2)])
 def test_conv_dgrad_as_forward_conv(cuda_ok, cin, cout, k, pad, hw, B):
     """A11 design check: the data gradient of a stride-1 conv IS a forward
