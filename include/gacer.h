@@ -239,6 +239,8 @@ typedef struct {
   int32_t train;              /* 1: a training tenant (its round is one SGD step) */
   int32_t n_steps;            /* training: 2 n_orig_ops + 1 step positions (pointer range) */
   int64_t n_params;           /* training: floats in the flat parameter buffer */
+  int32_t op_base;            /* global executor index of the tenant's first operator */
+  int32_t pad_info;
 } gacer_tenant_info;
 
 /* Device buffers of a training tenant (library-owned; valid until
@@ -302,6 +304,14 @@ int gacer_set_regulation(const gacer_decomposition* decomposition,
  * (out[i] for op i+1), i.e. Eq. 6/7 as compiled.  n = capacity of out. */
 int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n);
 
+/* Fused operator of every ORIGINAL op of `tenant` (out[i] for op i+1): the
+ * tenant-local index of the executor operator that computes it (conv + BN +
+ * add + activation lowered into one), -1 for aliases (flatten, dropout,
+ * concat).  The executor's global op index (device trace, gacer_describe_op)
+ * is gacer_tenant_info.op_base + out[i].  For the planner's lookup table
+ * (W and T per operator).  Inference tenants only. */
+int gacer_query_op_fused(int tenant, int32_t* out, int32_t n);
+
 /* SM partition of the executor (the paper's resource share W, §4.1
  * l.597-601): shares[t] > 0 is tenant t's relative share of the executor's
  * CTAs; each CTA serves its tenant's ready items first and (in the
@@ -359,9 +369,11 @@ int gacer_get_trace(int64_t* records, int32_t cap);
 
 const char* gacer_last_error(void);
 
-/* Diagnostics: describe lowered op `op` of the global op table (the op field
- * of gacer_get_trace records): out[6] = {device kind, virtual-grid function,
- * items per round, tenant, GEMM tile N, K-blocks}. */
+/* Describe lowered op `op` of the global op table (the op field of
+ * gacer_get_trace records): out[8] = {device kind, virtual-grid function,
+ * items per round, tenant, GEMM tile N, K-blocks, algorithmic bytes (inputs +
+ * outputs + weights, capped at 2^31 - 1), MFLOP}.  Diagnostics and the
+ * planner's lookup table. */
 int gacer_describe_op(int32_t op, int32_t* out);
 
 /* Diagnostics only (not on the method's path): when the process runs with

@@ -1871,6 +1871,8 @@ int gacer_get_tenant_info(int tenant, gacer_tenant_info* out) {
   out->train = T.train ? 1 : 0;
   out->n_steps = T.n_steps;
   out->n_params = T.train ? static_cast<int64_t>(T.tbuf_bytes[T.buf_params] / 4) : 0;
+  out->op_base = T.op_base;
+  out->pad_info = 0;
   for (const TrainOp& op : T.tops) {
     if (op.kind != DK_GEMM) { ++out->cc_ops; continue; }
     ++out->gemm_ops;
@@ -2014,6 +2016,17 @@ int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n) {
   const Tenant& T = S.tenants[tenant];
   const int m = std::min(n, T.train ? T.n_steps : T.n_orig);   // training tenants: per step position
   for (int i = 0; i < m; ++i) out[i] = cluster_of_orig(S.plan, tenant, i);
+  return m;
+}
+
+int gacer_query_op_fused(int tenant, int32_t* out, int32_t n) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !out)
+    return set_err(GACER_E_INVALID_ARG, "bad tenant id %d", tenant);
+  const Tenant& T = S.tenants[tenant];
+  if (T.train) return set_err(GACER_E_INVALID_ARG, "tenant %d is a training tenant", tenant);
+  const int m = std::min(n, T.n_orig);
+  for (int i = 0; i < m; ++i) out[i] = T.orig_fused[i];
   return m;
 }
 
@@ -2199,6 +2212,16 @@ int gacer_describe_op(int32_t op, int32_t* out) {
   out[3] = d.tenant;
   out[4] = d.bn;
   out[5] = d.nkb;
+  // algorithmic bytes (inputs + outputs + weights) and MFLOP of the fused op
+  // (the planner's lookup table: HBM share W_bw, NEXT-3); training ops: 0
+  double bytes = 0.0, flops = 0.0;
+  for (const Tenant& T : S.tenants)
+    if (!T.train && op >= T.op_base && op < T.op_base + static_cast<int>(T.fops.size())) {
+      bytes = T.fops[op - T.op_base].bytes;
+      flops = T.fops[op - T.op_base].flops;
+    }
+  out[6] = static_cast<int32_t>(std::min(bytes, 2147483647.0));
+  out[7] = static_cast<int32_t>(std::min(flops / 1e6, 2147483647.0));
   return GACER_OK;
 }
 

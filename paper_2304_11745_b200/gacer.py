@@ -91,7 +91,8 @@ class gacer_tenant_info(C.Structure):
                 ("out_features", C.c_int32), ("in_bytes", C.c_int64), ("out_bytes", C.c_int64),
                 ("flops", C.c_double), ("gemm_ops", C.c_int32), ("mpair_ops", C.c_int32),
                 ("split_k_ops", C.c_int32), ("swap_ops", C.c_int32), ("wide_ops", C.c_int32),
-                ("cc_ops", C.c_int32), ("train", C.c_int32), ("n_steps", C.c_int32), ("n_params", C.c_int64)]
+                ("cc_ops", C.c_int32), ("train", C.c_int32), ("n_steps", C.c_int32), ("n_params", C.c_int64),
+                ("op_base", C.c_int32), ("pad_info", C.c_int32)]
 
 
 class gacer_train_state(C.Structure):
@@ -112,6 +113,7 @@ EXPORTS = {
     "gacer_train_param": ([C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
     "gacer_set_regulation": ([C.POINTER(gacer_decomposition), C.POINTER(gacer_sync_pointers)], C.c_int),
     "gacer_query_op_clusters": ([C.c_int, IP, C.c_int32], C.c_int),
+    "gacer_query_op_fused": ([C.c_int, IP, C.c_int32], C.c_int),
     "gacer_set_sm_shares": ([C.POINTER(C.c_float), C.c_int32], C.c_int),
     "gacer_set_partition": ([C.c_int32], C.c_int),
     "gacer_set_mode": ([C.c_int], C.c_int),
@@ -336,6 +338,12 @@ def gacer_query_op_clusters(tenant, n_ops):
     return out[:n].tolist()
 
 
+def gacer_query_op_fused(tenant, n_ops):
+    out = np.zeros(n_ops, dtype=np.int32)
+    n = _check(lib().gacer_query_op_fused(tenant, out.ctypes.data_as(IP), n_ops))
+    return out[:n].tolist()
+
+
 def gacer_set_partition(partition="priority"):
     return _check(lib().gacer_set_partition(PARTITION[partition] if isinstance(partition, str) else int(partition)))
 
@@ -389,9 +397,9 @@ def gacer_get_trace(cap):
 
 
 def gacer_describe_op(op):
-    out = np.zeros(6, dtype=np.int32)
+    out = np.zeros(8, dtype=np.int32)
     _check(lib().gacer_describe_op(op, out.ctypes.data_as(IP)))
-    return dict(zip(("kind", "vfn", "items", "tenant", "bn", "nkb"), out.tolist()))
+    return dict(zip(("kind", "vfn", "items", "tenant", "bn", "nkb", "bytes", "mflop"), out.tolist()))
 
 
 def gacer_last_error():
