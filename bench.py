@@ -219,13 +219,16 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def time_mode(G, s, torch, stream, mode, steps, warmup, flush):
+def time_mode(G, s, torch, stream, mode, steps, warmup, flush, ar=None):
     """Per-round device times (CUDA events on `stream`, L2 flushed before
     every round outside the events).  mode "<baseline>_graph" replays the
     baseline round captured as a CUDA graph (gacer_capture_baseline)."""
     if mode.endswith("_graph"):
         G.gacer_capture_baseline(mode[:-len("_graph")])
         run = lambda: G.gacer_run_baseline_graph(stream.cuda_stream)
+    elif ar is not None:          # a round with the overlapped gradient exchange (A12)
+        s.set_mode(mode)
+        run = lambda: ar.enqueue_round(stream)
     else:
         s.set_mode(mode)
         run = lambda: G.gacer_run_round_async(stream.cuda_stream)
@@ -436,9 +439,24 @@ def run_d4(args, rank, world, dist):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
     torch.cuda.set_stream(stream)
 
+    # A12: the data-parallel gradient mean of the training tenant inside the
+    # round (NCCL on a communication stream, bucket waits on the executor's
+    # counters, SGD behind the gradient gate); SMs left to the collective
+    dp = dist is not None or args.allreduce
+    reserve = 12 if dp else 0
+    if dp and dist is None:            # world size 1: a one-rank NCCL group exercises the same path
+        import torch.distributed as dist_mod
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist_mod.init_process_group("nccl", rank=0, world_size=1)
+        dp_group = dist_mod
+    else:
+        dp_group = dist
+
     def session(sel):
         s = Session([(g, p, B, dt, {"train": True}) if tr else (g, p, B, dt)
-                     for j, (_, g, p, B, dt, _, tr, _) in enumerate(ts) if j in sel], device=dev)
+                     for j, (_, g, p, B, dt, _, tr, _) in enumerate(ts) if j in sel], device=dev,
+                    num_ctas=(148 - reserve) if (dp and 0 in sel) else 0)
         for k, j in enumerate(sel):
             s.set_input(k, ts[j][5])
             if ts[j][6]:
@@ -457,13 +475,17 @@ def run_d4(args, rank, world, dist):
     # ---- the mixed round: plans (SM partition / shares), then the timed run
     s = session([0, 1, 2])
     st = G.gacer_get_stats()
+    ar = None
+    if dp:
+        from paper_2304_11745_b200.grad_allreduce import ExecutorAllReduce
+        ar = ExecutorAllReduce(s, 0, dp_group)
     plans = {"priority": ("priority", None), "hybrid": ("hybrid", None),
              "work_conserving": ("work_conserving", None), "strict[.7,.2,.1]": ("strict", [0.7, 0.2, 0.1])}
     plan_ms = {}
     for name, (part, sh) in plans.items():
         G.gacer_set_partition(part)
         G.gacer_set_sm_shares(sh)
-        plan_ms[name] = float(np.median(time_mode(G, s, torch, stream, "executor", 3, 2, flush)))
+        plan_ms[name] = float(np.median(time_mode(G, s, torch, stream, "executor", 3, 2, flush, ar)))
     best = min(plan_ms, key=plan_ms.get)
     G.gacer_set_partition(plans[best][0])
     G.gacer_set_sm_shares(plans[best][1])
@@ -471,7 +493,7 @@ def run_d4(args, rank, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
-        times = time_mode(G, s, torch, stream, "executor", args.steps, args.warmup, flush)
+        times = time_mode(G, s, torch, stream, "executor", args.steps, args.warmup, flush, ar)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -479,14 +501,19 @@ def run_d4(args, rank, world, dist):
     ms_step = total_ms / args.steps
     occ = G.gacer_get_stats()
     base = {}
-    for mode in ("sequential", "multistream", "sequential_graph", "multistream_graph"):
-        tm = time_mode(G, s, torch, stream, mode, max(3, args.steps // 2), args.warmup, flush)
+    # (graph baselines are not captured with the data-parallel gradient gate)
+    for mode in ("sequential", "multistream") + (() if dp else ("sequential_graph", "multistream_graph")):
+        tm = time_mode(G, s, torch, stream, mode, max(3, args.steps // 2), args.warmup, flush, ar)
         m = max_over_ranks(float(np.mean(tm)), dist, f"cuda:{dev}")
         base[mode] = {"ms_per_round": m, "inferences_per_s": world * n_inf / (m / 1000.0),
                       "train_images_per_s": world * n_train / (m / 1000.0),
                       "kernel_launches_per_round": G.gacer_get_stats()["kernel_launches"]}
     s.set_mode("executor")
     # ---- e2e: host buffers (images of all three tenants copied in, logits out)
+    # (a blocking host-buffer round: the gradient exchange is not enqueued
+    #  behind it, so the gate is switched off for this leg)
+    if ar is not None:
+        ar.close()
     host_in = [s.host_input(t, ts[j][5]) for t, j in enumerate([0, 1, 2])]
     host_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in s.outputs]
     for _ in range(args.warmup):
@@ -544,9 +571,15 @@ def run_d4(args, rank, world, dist):
             "makespan_ms": {"p10": float(np.percentile(times, 10)), "p50": float(np.median(times)),
                             "p90": float(np.percentile(times, 90))},
             "n_items_per_round": st["n_items"],
+            "grad_allreduce": ({"buckets": len(ar.buckets), "bytes": int(4 * sum(n for _, n in ar.buckets)),
+                                "world": world, "reserved_sms": reserve, "transport": "nccl",
+                                "overlap": "bucket waits on the executor's completion counters"}
+                               if ar is not None else None),
         }
         print(json.dumps(line), flush=True)
     s.close()
+    if dp and dist is None:
+        dp_group.destroy_process_group()
 
 
 def main():
@@ -561,6 +594,8 @@ def main():
     ap.add_argument("--plan", default="sweep", choices=["identity", "sweep"])
     ap.add_argument("--no-search", action="store_true", help="skip the Algorithm 1 plan search")
     ap.add_argument("--search-evals", type=int, default=30)
+    ap.add_argument("--allreduce", action="store_true",
+                    help="d4_mixed at N=1: run the training tenant's gradient all-reduce path anyway")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

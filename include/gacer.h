@@ -300,6 +300,38 @@ int gacer_train_param(int tenant, int32_t op_index, int32_t which, int64_t* offs
 int gacer_set_regulation(const gacer_decomposition* decomposition,
                          const gacer_sync_pointers* sync_pointers);
 
+/* ---- A12: data-parallel gradient exchange of a training tenant (north_star:
+ * "NCCL over NVLink is used only for the gradient all-reduce of data-parallel
+ * training tenants").  The round's backward writes
+ * the flat gradients; with the exchange enabled the SGD update additionally
+ * waits for a per-tenant gradient gate.  The caller (one process per GPU,
+ * torch.distributed / NCCL) enqueues on a communication stream, per bucket:
+ * gacer_stream_wait_grads (device-side waits for the ops producing that
+ * slice of the gradients, so the all-reduce of the last layers overlaps the
+ * rest of the backward), its all-reduce + 1/G, and after the last bucket
+ * gacer_stream_open_grad_gate.  Launch the executor with fewer CTAs than SMs
+ * (gacer_options.num_ctas) so the collective's kernels find free SMs. */
+
+/* Enable (1) / disable (0) the gradient gate of training tenant `tenant`
+ * (recompiles the current plan; drains the device). */
+int gacer_train_set_allreduce(int tenant, int32_t enable);
+
+/* Buckets over the flat gradient buffer, last layers first: whole parameter
+ * slices grouped up to bucket_bytes (a larger single slice is its own
+ * bucket).  out[2b] = float offset, out[2b+1] = float count (out may be NULL
+ * to count).  Returns the number of buckets. */
+int gacer_train_buckets(int tenant, int64_t bucket_bytes, int64_t* out, int32_t cap);
+
+/* Enqueue on `stream` a device-side wait until every op writing gradient
+ * floats [offset, offset + count) of the most recently enqueued round has
+ * completed (executor: cuStreamWaitValue32 on their completion counters;
+ * baseline modes: the round's backward-done event). */
+int gacer_stream_wait_grads(void* stream, int tenant, int64_t offset, int64_t count);
+
+/* Enqueue on `stream` the opening of the tenant's gradient gate for the most
+ * recently enqueued round (its SGD update may then run). */
+int gacer_stream_open_grad_gate(void* stream, int tenant);
+
 /* Cluster index of every ORIGINAL op of `tenant` under the current plan
  * (out[i] for op i+1), i.e. Eq. 6/7 as compiled.  n = capacity of out. */
 int gacer_query_op_clusters(int tenant, int32_t* out, int32_t n);

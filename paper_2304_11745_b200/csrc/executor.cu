@@ -2112,6 +2112,12 @@ __device__ void executor_body(const ExecParams& p, uint8_t* smem_raw) {
     const uint32_t old = atomicAdd(p.exit_count, 1u);
     if (old == gridDim.x - 1) {  // last CTA out re-arms the claim counters
       for (int i = 0; i < p.n_heads; ++i) p.heads[i] = 0;
+      // an aborted round (watchdog): saturate every completion counter so
+      // that stream-side waits on them (gacer_stream_wait_grads) release
+      // instead of blocking their stream forever; the host resets the
+      // counters before the next round (sticky GACER_E_DEADLOCK path)
+      if (*reinterpret_cast<volatile int32_t*>(p.error))
+        for (int i = 0; i < p.n_counters; ++i) p.chunk_done[i] = 0xFFFFFFFFu;
       *p.exit_count = 0;
       __threadfence();
     }

@@ -225,7 +225,7 @@ struct ExecParams {
   int64_t* dbg;             // optional [gridDim.x * DBG_EVENTS] %globaltimer milestones (diagnostics)
   int64_t dbg_spin;         // diagnostics: epilogue delay (clocks) between tfull and the TMEM read
   int32_t claim_ahead;      // 1: with no ready item, claim the best unready head and wait on its deps
-  int32_t pad_ca;
+  int32_t n_counters;       // chunk_done entries (saturated on a watchdog abort)
   unsigned long long* stats;// [STAT_TENANTS + 2] accumulating ns: per-tenant item time (claim -> release),
                             // then CTA time at cluster barriers, then CTA time with only unready work
 };

@@ -165,6 +165,7 @@ struct TrainOp {
   int im2col_c = 0;              // real channels of the im2col tensor map
   int a_ld = 0, a_rows = 0, b_rows = 0;
   std::vector<int> deps;         // producer ops (indices into tops): RAW / WAR / WAW on buffers
+  std::vector<std::pair<int64_t, int64_t>> grad_ranges;   // flat-gradient slices written (floats)
   bool reads_input = false;      // reads the bound images or labels (input gate)
   int step_pos = 1;              // 1-based position in the step's issue order (pointer clusters)
   int items = 1;
@@ -181,6 +182,7 @@ struct Tenant {
   std::vector<void*> tbufs;
   std::vector<float> h_params;       // initial master parameters (uploaded once)
   int buf_params = -1, buf_grads = -1, buf_mom = -1, buf_loss = -1;
+  bool grad_gate = false;            // A12: the SGD op waits for the gradient all-reduce gate
   std::map<std::pair<int, int>, std::pair<int64_t, int64_t>> param_slice;  // (orig op, which) -> (offset, count)
   const void* labels_dev = nullptr;
   float lr = 0.1f, momentum = 0.9f;
@@ -220,6 +222,7 @@ struct Plan {
   std::vector<uint32_t> cluster_total;
   int n_chunk_counters = 0;
   int input_counter0 = 0;                           // first of the per-tenant input-gate counters
+  int grad_gate0 = 0;                               // first of the per-tenant gradient gates (A12)
   std::vector<std::vector<int>> fop_cluster;        // [tenant][fused op]
   std::vector<double> auto_share;                   // per tenant: SM need (work / chain latency)
 };
@@ -232,6 +235,11 @@ struct State {
   gacer_options opts{};
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;   // host-buffer rounds: H2D copies + input gates
+  // A12 (gradient all-reduce of data-parallel training tenants): baseline-mode
+  // gates (round-numbered words the SGD launch waits on) and backward-done events
+  uint32_t* d_bgate = nullptr;
+  uint32_t round_no = 0;
+  std::vector<cudaEvent_t> bwd_event;
   std::vector<cudaStream_t> tstreams;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t ev_fork = nullptr;           // multi-stream baseline: fork / join (no timing)
@@ -979,6 +987,7 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
 
 PFN_cuStreamWriteValue32_v11070 g_write_value32 = nullptr;
+PFN_cuStreamWaitValue32_v11070 g_wait_value32 = nullptr;
 
 int load_tma_encoders() {
   if (!g_write_value32) {
@@ -987,6 +996,9 @@ int load_tma_encoders() {
     CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q));
     g_write_value32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
     if (!g_write_value32) return set_err(GACER_E_CUDA, "cuStreamWriteValue32 not available");
+    CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q));
+    g_wait_value32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
+    if (!g_wait_value32) return set_err(GACER_E_CUDA, "cuStreamWaitValue32 not available");
   }
   if (g_encode_tiled && g_encode_im2col) return 0;
   cudaDriverEntryPointQueryResult q;
@@ -1233,6 +1245,10 @@ int compile_plan(Plan& P) {
   // a copy stream starts each tenant as soon as its own input has landed
   P.input_counter0 = counter;
   counter += nt;
+  // A12: per-tenant gradient gates (opened by the communication stream after
+  // the data-parallel all-reduce; the SGD op of a gated tenant waits for it)
+  P.grad_gate0 = counter;
+  counter += nt;
   P.n_chunk_counters = counter;
 
   // upward rank of every fused op (HEFT-style list scheduling): estimated
@@ -1341,6 +1357,8 @@ int compile_plan(Plan& P) {
         const int k = P.fop_cluster[t][f];
         std::vector<Dep> dl;
         if (op.reads_input) dl.push_back({P.input_counter0 + t, 1u});   // input gate (images, labels)
+        if (T.grad_gate && op.kind == DK_VGRID && op.vfn == VF_SGD)
+          dl.push_back({P.grad_gate0 + t, 1u});                          // all-reduced gradients (A12)
         for (int d : op.deps) dl.push_back({cr[t][d][0].counter, cr[t][d][0].n_items});
         int dep_begin = 0;
         if (dl.size() > static_cast<size_t>(INLINE_DEPS)) {
@@ -1622,6 +1640,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
   if (!st) st = S.stream;
   if (record_events) CUDA_TRY(cudaEventRecord(S.ev0, st));
   int launches = 0;
+  ++S.round_no;
   if (S.mode == GACER_MODE_EXECUTOR) {
     if (!gates_written) {
       if (int rc = maybe_reset_epoch()) return rc;
@@ -1641,6 +1660,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.single_op = -1;
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
     p.claim_ahead = claim_ahead_enabled();
+    p.n_counters = std::max(1, S.plan.n_chunk_counters);
     p.dbg = S.d_dbg;
     if (const char* e = getenv("GACER_DBG_SPIN")) p.dbg_spin = atoll(e);
     p.k_first = 0;
@@ -1672,6 +1692,7 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
     p.single_op = -1;
     p.own_first = S.opts.partition == GACER_PARTITION_PRIORITY ? 0 : 1;
     p.claim_ahead = claim_ahead_enabled();
+    p.n_counters = std::max(1, S.plan.n_chunk_counters);
     p.gate0 = S.plan.input_counter0;
     p.n_gates = static_cast<int32_t>(S.tenants.size());
     bool first = true;
@@ -1708,6 +1729,14 @@ int enqueue_round(cudaStream_t st, bool record_events = true, bool gates_written
       const size_t n_ops = T.train ? T.tops.size() : T.fops.size();
       for (size_t f = 0; f < n_ops; ++f) {
         int kind, nb;
+        if (T.train && T.grad_gate && T.tops[f].kind == DK_VGRID && T.tops[f].vfn == VF_SGD) {
+          // A12 in a baseline round: the gradients are complete here; the
+          // update waits until the communication stream has reduced them
+          CUDA_TRY(cudaEventRecord(S.bwd_event[t], ts));
+          if (g_wait_value32(reinterpret_cast<CUstream>(ts), reinterpret_cast<CUdeviceptr>(S.d_bgate + t),
+                             S.round_no, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return set_err(GACER_E_CUDA, "cuStreamWaitValue32 failed");
+        }
         if (T.train) {
           kind = T.tops[f].kind;
           nb = T.tops[f].items;
@@ -1942,6 +1971,104 @@ int gacer_train_param(int tenant, int32_t op_index, int32_t which, int64_t* offs
   return GACER_OK;
 }
 
+// ---- A12: the data-parallel gradient exchange of a training tenant
+int gacer_train_set_allreduce(int tenant, int32_t enable) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !S.tenants[tenant].train)
+    return set_err(GACER_E_INVALID_ARG, "tenant %d is not a training tenant", tenant);
+  Tenant& T = S.tenants[tenant];
+  if (T.grad_gate == (enable != 0)) return GACER_OK;
+  if (!S.host_only) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (!S.d_bgate) {
+      CUDA_TRY(cudaMalloc(&S.d_bgate, 64 * sizeof(uint32_t)));
+      CUDA_TRY(cudaMemset(S.d_bgate, 0, 64 * sizeof(uint32_t)));
+    }
+    while (S.bwd_event.size() < S.tenants.size()) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      S.bwd_event.push_back(e);
+    }
+  }
+  if (tenant >= 64) return set_err(GACER_E_INVALID_ARG, "at most 64 tenants with a gradient gate");
+  T.grad_gate = enable != 0;
+  Plan P;                      // recompile the current plan with / without the gate
+  P.cuts = S.plan.cuts;
+  P.chunks = S.plan.chunks;
+  if (int rc = compile_plan(P)) return rc;
+  S.plan = std::move(P);
+  return upload_plan();
+}
+
+int gacer_train_buckets(int tenant, int64_t bucket_bytes, int64_t* out, int32_t cap) {
+  if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !S.tenants[tenant].train || bucket_bytes < 4)
+    return set_err(GACER_E_INVALID_ARG, "bad arguments");
+  const Tenant& T = S.tenants[tenant];
+  // parameter slices from the END of the flat buffer (the last layers'
+  // gradients are produced first in backward), grouped while <= bucket_bytes
+  std::vector<std::pair<int64_t, int64_t>> sl;
+  for (const auto& kv : T.param_slice)
+    if (kv.first.first >= 0) sl.push_back(kv.second);
+  std::sort(sl.begin(), sl.end());
+  const int64_t cap_f = std::max<int64_t>(1, bucket_bytes / 4);
+  std::vector<std::pair<int64_t, int64_t>> bk;   // (offset, count)
+  int64_t hi = -1, lo = -1;
+  for (auto it = sl.rbegin(); it != sl.rend(); ++it) {
+    const int64_t a = it->first, e = it->first + it->second;
+    if (hi < 0) { lo = a; hi = e; continue; }
+    if (hi - a > cap_f) { bk.push_back({lo, hi - lo}); hi = e; }
+    lo = a;
+  }
+  if (hi >= 0) bk.push_back({lo, hi - lo});
+  if (out)
+    for (int b = 0; b < static_cast<int>(bk.size()) && b < cap; ++b) { out[2 * b] = bk[b].first; out[2 * b + 1] = bk[b].second; }
+  return static_cast<int>(bk.size());
+}
+
+int gacer_stream_wait_grads(void* stream, int tenant, int64_t offset, int64_t count) {
+  if (int rc = check_ready()) return rc;
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !S.tenants[tenant].grad_gate)
+    return set_err(GACER_E_INVALID_ARG, "tenant %d has no gradient gate (gacer_train_set_allreduce)", tenant);
+  const Tenant& T = S.tenants[tenant];
+  auto st = reinterpret_cast<CUstream>(stream);
+  if (S.mode != GACER_MODE_EXECUTOR) {   // baselines: the backward-done event of the enqueued round
+    CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), S.bwd_event[tenant], 0));
+    return GACER_OK;
+  }
+  // executor: the completion counters of every op writing into the range
+  // (a training op's items share one whole-op counter; its first item carries it)
+  std::vector<int> ctr(T.tops.size(), -1);
+  for (const Item& it : S.plan.items) {
+    const int f = it.op - T.op_base;
+    if (f >= 0 && f < static_cast<int>(ctr.size()) && ctr[f] < 0) ctr[f] = it.chunk;
+  }
+  for (size_t f = 0; f < T.tops.size(); ++f) {
+    const TrainOp& op = T.tops[f];
+    bool hit = false;
+    for (const auto& r : op.grad_ranges) hit |= r.first < offset + count && r.first + r.second > offset;
+    if (!hit) continue;
+    if (ctr[f] < 0) return set_err(GACER_E_STATE, "gradient op %zu has no items", f);
+    const uint32_t target = S.epoch * static_cast<uint32_t>(op.items);
+    if (g_wait_value32(st, reinterpret_cast<CUdeviceptr>(S.d_chunk_done + ctr[f]), target,
+                       CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return set_err(GACER_E_CUDA, "cuStreamWaitValue32 failed");
+  }
+  return GACER_OK;
+}
+
+int gacer_stream_open_grad_gate(void* stream, int tenant) {
+  if (int rc = check_ready()) return rc;
+  if (tenant < 0 || tenant >= static_cast<int>(S.tenants.size()) || !S.tenants[tenant].grad_gate)
+    return set_err(GACER_E_INVALID_ARG, "tenant %d has no gradient gate", tenant);
+  auto st = reinterpret_cast<CUstream>(stream);
+  if (g_write_value32(st, reinterpret_cast<CUdeviceptr>(S.d_chunk_done + S.plan.grad_gate0 + tenant), S.epoch, 0) !=
+          CUDA_SUCCESS ||
+      g_write_value32(st, reinterpret_cast<CUdeviceptr>(S.d_bgate + tenant), S.round_no, 0) != CUDA_SUCCESS)
+    return set_err(GACER_E_CUDA, "cuStreamWriteValue32 failed");
+  return GACER_OK;
+}
+
 int gacer_set_regulation(const gacer_decomposition* dec, const gacer_sync_pointers* sp) {
   if (!S.inited) return set_err(GACER_E_STATE, "gacer_init not called");
   if (S.sticky_cuda) return set_err(GACER_E_CUDA, "sticky CUDA error");
@@ -2075,6 +2202,9 @@ int gacer_capture_baseline(int mode) {
   if (mode != GACER_MODE_SEQUENTIAL && mode != GACER_MODE_MULTISTREAM)
     return set_err(GACER_E_INVALID_ARG, "only the sequential / multi-stream baselines are captured (mode %d)", mode);
   if (S.base_graph) { cudaGraphExecDestroy(S.base_graph); S.base_graph = nullptr; S.base_graph_mode = -1; }
+  for (const Tenant& T : S.tenants)
+    if (T.grad_gate)   // the round-numbered gradient gate cannot be baked into a graph
+      return set_err(GACER_E_STATE, "baseline graphs are not captured with a data-parallel training tenant");
   const int saved = S.mode;
   S.mode = mode;
   CUDA_TRY(cudaStreamSynchronize(S.stream));
@@ -2700,6 +2830,7 @@ struct TrainLowering {
   std::vector<std::vector<int>> readers;
   std::map<int, int> sp_writer;               // special (bound) buffers
   std::map<int, std::vector<int>> sp_readers;
+  std::vector<int> grad_writers;              // ops writing (disjoint) slices of the flat gradients
   int step = 1;
 
   explicit TrainLowering(Tenant& t, int b) : T(t), B(b) {}
@@ -2727,20 +2858,36 @@ struct TrainLowering {
     for (int b : rd) {
       if (b == -1) continue;
       if (b == TBUF_IN || b == TBUF_LABELS) op.reads_input = true;
+      if (b == T.buf_grads) {   // the update reads every gradient slice
+        dep.insert(grad_writers.begin(), grad_writers.end());
+        continue;
+      }
       if (writer_of(b) >= 0) dep.insert(writer_of(b));
       op.bytes += bytes_of(b);
     }
     for (int b : wr) {
       if (b == -1) continue;
+      if (b == T.buf_grads) continue;   // disjoint per-parameter slices: no WAW between writers
       if (writer_of(b) >= 0) dep.insert(writer_of(b));
       for (int r : readers_of(b)) dep.insert(r);
       op.bytes += bytes_of(b);
     }
     dep.erase(me);
     op.deps.assign(dep.begin(), dep.end());
-    for (int b : rd) if (b != -1) readers_of(b).push_back(me);
+    for (int b : rd) if (b != -1 && b != T.buf_grads) readers_of(b).push_back(me);
     for (int b : wr) {
       if (b == -1) continue;
+      if (b == T.buf_grads) {
+        grad_writers.push_back(me);
+        // the slices it writes (its VArgs pointer slots into the buffer)
+        for (const TRef& r : op.vp)
+          if (r.buf == T.buf_grads) {
+            const int64_t off = static_cast<int64_t>(r.off / 4);
+            for (const auto& kv : T.param_slice)
+              if (kv.second.first == off) op.grad_ranges.push_back({off, kv.second.second});
+          }
+        continue;
+      }
       writer_of(b) = me;
       readers_of(b).clear();
     }

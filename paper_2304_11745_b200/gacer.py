@@ -114,6 +114,10 @@ EXPORTS = {
     "gacer_set_regulation": ([C.POINTER(gacer_decomposition), C.POINTER(gacer_sync_pointers)], C.c_int),
     "gacer_query_op_clusters": ([C.c_int, IP, C.c_int32], C.c_int),
     "gacer_query_op_fused": ([C.c_int, IP, C.c_int32], C.c_int),
+    "gacer_train_set_allreduce": ([C.c_int, C.c_int32], C.c_int),
+    "gacer_train_buckets": ([C.c_int, C.c_int64, C.POINTER(C.c_int64), C.c_int32], C.c_int),
+    "gacer_stream_wait_grads": ([C.c_void_p, C.c_int, C.c_int64, C.c_int64], C.c_int),
+    "gacer_stream_open_grad_gate": ([C.c_void_p, C.c_int], C.c_int),
     "gacer_set_sm_shares": ([C.POINTER(C.c_float), C.c_int32], C.c_int),
     "gacer_set_partition": ([C.c_int32], C.c_int),
     "gacer_set_mode": ([C.c_int], C.c_int),
@@ -342,6 +346,25 @@ def gacer_query_op_fused(tenant, n_ops):
     out = np.zeros(n_ops, dtype=np.int32)
     n = _check(lib().gacer_query_op_fused(tenant, out.ctypes.data_as(IP), n_ops))
     return out[:n].tolist()
+
+
+def gacer_train_set_allreduce(tenant, enable=True):
+    return _check(lib().gacer_train_set_allreduce(tenant, int(bool(enable))))
+
+
+def gacer_train_buckets(tenant, bucket_bytes):
+    n = _check(lib().gacer_train_buckets(tenant, int(bucket_bytes), None, 0))
+    out = np.zeros(2 * max(n, 1), dtype=np.int64)
+    _check(lib().gacer_train_buckets(tenant, int(bucket_bytes), out.ctypes.data_as(C.POINTER(C.c_int64)), n))
+    return [(int(out[2 * b]), int(out[2 * b + 1])) for b in range(n)]
+
+
+def gacer_stream_wait_grads(stream, tenant, offset, count):
+    return _check(lib().gacer_stream_wait_grads(C.c_void_p(stream), tenant, int(offset), int(count)))
+
+
+def gacer_stream_open_grad_gate(stream, tenant):
+    return _check(lib().gacer_stream_open_grad_gate(C.c_void_p(stream), tenant))
 
 
 def gacer_set_partition(partition="priority"):

@@ -73,3 +73,62 @@ def grads_as_list(grads: Dict[int, Dict[str, object]]) -> Tuple[List, List[Tuple
     """Flatten {op_id: {name: tensor}} into a list in (op_id, name) order."""
     keys = [(oid, n) for oid in sorted(grads) for n in sorted(grads[oid])]
     return [grads[o][n] for o, n in keys], keys
+
+
+class ExecutorAllReduce:
+    """A12 inside a GACER round: the training
+    tenant's gradient mean over the data-parallel group, overlapped with its
+    own backward pass.
+
+    Per round: the executor launch on the compute stream, then on a
+    communication stream, bucket by bucket (last layers first,
+    ``gacer_train_buckets``): a device-side wait for the ops that write the
+    bucket's gradient slice (``gacer_stream_wait_grads``: stream memory waits
+    on the executor's completion counters -- the collective of the last
+    layers starts while the earlier layers' backward still runs), the NCCL
+    all-reduce (SUM) of that slice of the library's flat fp32 gradient buffer
+    and the 1/G scale; after the last bucket the tenant's gradient gate opens
+    (``gacer_stream_open_grad_gate``) and the SGD item of the round, which
+    waits on it, applies the mean.  The executor must leave SMs free for the
+    collective's kernels (Session(num_ctas=#SMs - reserve)).
+
+    Plumbing only: the gradients are produced and consumed by libgacer's
+    kernels; torch.distributed (NCCL) is the transport."""
+
+    def __init__(self, session, tenant: int, dist, group=None, bucket_bytes: int = BUCKET_BYTES,
+                 comm_stream=None):
+        import torch
+        from . import gacer as G
+        self.G, self.dist, self.group, self.t = G, dist, group, tenant
+        G.gacer_train_set_allreduce(tenant, True)
+        self.buckets = G.gacer_train_buckets(tenant, bucket_bytes)
+        _, _, self.grads, _ = session.train_state(tenant)
+        self.world = dist.get_world_size(group)
+        self.comm = comm_stream or torch.cuda.Stream(device=session.device)
+        # create the communicator now: NCCL's lazy initialisation inside a
+        # round could synchronise the device while the executor waits for
+        # the gradient gate (a deadlock until the watchdog fires)
+        with torch.cuda.stream(self.comm):
+            w = torch.zeros(8, device=self.grads.device)
+            dist.all_reduce(w, group=group)
+        torch.cuda.synchronize(session.device)
+
+    def enqueue_round(self, stream) -> None:
+        """One round (every tenant's step / forward) with the overlapped
+        gradient exchange of this tenant; all work is enqueued, nothing
+        blocks the host."""
+        import torch
+        G = self.G
+        G.gacer_run_round_async(stream.cuda_stream)
+        cs = self.comm.cuda_stream
+        with torch.cuda.stream(self.comm):
+            for off, n in self.buckets:
+                G.gacer_stream_wait_grads(cs, self.t, off, n)
+                v = self.grads[off:off + n]
+                self.dist.all_reduce(v, op=self.dist.ReduceOp.SUM, group=self.group)
+                if self.world > 1:
+                    v.mul_(1.0 / self.world)
+            G.gacer_stream_open_grad_gate(cs, self.t)
+
+    def close(self):
+        self.G.gacer_train_set_allreduce(self.t, False)
