@@ -564,8 +564,9 @@ def run_d4(args, rank, world, dist):
             "baselines": base,
             "speedup_vs_sequential": base["sequential"]["ms_per_round"] / ms_step,
             "speedup_vs_multistream": base["multistream"]["ms_per_round"] / ms_step,
-            "speedup_vs_sequential_graph": base["sequential_graph"]["ms_per_round"] / ms_step,
-            "speedup_vs_multistream_graph": base["multistream_graph"]["ms_per_round"] / ms_step,
+            **({"speedup_vs_sequential_graph": base["sequential_graph"]["ms_per_round"] / ms_step,
+                "speedup_vs_multistream_graph": base["multistream_graph"]["ms_per_round"] / ms_step}
+               if "sequential_graph" in base else {}),
             "speedup_vs_alone_sum": (res["train_alone"] + res["inference_alone"]) / ms_step,
             "occupancy_sm_ms": [v / 1e6 for v in occ["tenant_sm_ns"]],
             "makespan_ms": {"p10": float(np.percentile(times, 10)), "p50": float(np.median(times)),

@@ -165,6 +165,17 @@ __device__ __forceinline__ uint64_t make_sdesc_mn(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;
   return d;
 }
+// K-major SWIZZLE_NONE ("interleave") canonical layout: core matrices of 8
+// rows x 16 bytes (8 K-elements), rows 16 B apart; SBO = bytes between 8-row
+// groups, LBO = bytes between the two 8-element K chunks of a K=16 step.
+__device__ __forceinline__ uint64_t make_sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;   // layout type 0 (SWIZZLE_NONE)
+}
 // Instruction descriptor kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1),
 // B bf16 (bits 10-12 = 1), both K-major, N>>3 at bits 17-22, M>>4 at 24-28.
 __device__ __forceinline__ uint32_t make_idesc(int n) {
@@ -252,11 +263,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // RNE, .x = a (low half)
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// ReLU / ReLU6 only: MobileNetV3's hardswish / hardsigmoid are separate
+// eltwise ops (cc_item_ext, out of line) -- inlined here, their extra
+// branches perturbed the register allocation of the hot epilogue and window
+// loops (same-box A/B: +10 us per op on plain conv+ReLU layers)
 __device__ __forceinline__ float apply_act(float v, int act) {
   if (act == ACT_RELU) v = fmaxf(v, 0.0f);
   else if (act == ACT_RELU6) v = fminf(fmaxf(v, 0.0f), 6.0f);
-  else if (act == ACT_HSWISH) v = v * fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
-  else if (act == ACT_HSIGMOID) v = fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
   return v;
 }
 
@@ -551,7 +564,7 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       fence_proxy_async_global();   // acquired producer data -> this thread's TMA reads
       // im2col start (top-left input tap) of each 128-row half of the tile
       int w0[2] = {0, 0}, h0[2] = {0, 0}, img0[2] = {0, 0};
-      if (a_mode == A_IM2COL) {
+      if (a_mode == A_IM2COL || a_mode == A_IM2COL8) {
         const int HoWo = op.Ho * op.Wo, Wo = op.Wo;
         for (int hf = 0; hf < mrep; ++hf) {
           const int mm = m0 + hf * BM;
@@ -580,6 +593,27 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
         const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
         const uint32_t b_dst = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
         const int k = (kb0 + i) * BK;
+#ifndef GACER_NO_I8_CODE
+        if (a_mode == A_IM2COL8) {
+          // 8 taps of 8 channels: one 128-pixel x 16-byte im2col box per tap
+          // (taps past kh*kw: a channel start past the tensor -> zero fill),
+          // then the pre-packed weight block with one bulk copy
+          const int taps = op.kh * kw;
+          const int kb = kb0 + i;
+#pragma unroll 1
+          for (int j = 0; j < 8; ++j) {
+            const int tap = kb * 8 + j;
+            const bool ok = tap < taps;
+            const int r = ok ? tap / kw : 0, sx = ok ? tap - (tap / kw) * kw : 0;
+            tma_load_im2col_4d(a_dst + j * 2048, tmap_a, bar, ok ? 0 : 8, w0[0], h0[0], img0[0],
+                               static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
+          }
+          const size_t blk = (static_cast<size_t>(it.nt) * op.nkb + kb) * static_cast<size_t>(bbytes);
+          vgs_load(cx.ring + (b_dst - ring_base), static_cast<const uint8_t*>(op.wt) + blk, bbytes, bar);
+          kdbg(p, 1, gi);
+          continue;
+        }
+#endif
         if (a_mode == A_MN) {
           // K-block = output pixels [k, k + 64): A = dy rows (two 64-channel
           // boxes), B = one im2col box per 64 GEMM columns (tap, c0)
@@ -768,22 +802,7 @@ __device__ __forceinline__ void cc_pixel(const OpDev& op, int m, int c, int HoWo
   float y[8];
   if (op.kind == DK_ELTWISE) {
     load8<F32>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
-    if (op.affine) {   // standalone BatchNorm (folded scale / bias), e.g. DenseNet's pre-activation
-      const float4 s0 = *reinterpret_cast<const float4*>(op.scale + c);
-      const float4 s1 = *reinterpret_cast<const float4*>(op.scale + c + 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(op.bias + c);
-      const float4 b1 = *reinterpret_cast<const float4*>(op.bias + c + 4);
-      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-      const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
-    }
-    if (op.has_skip == 2) {   // channel scale: * s[n][c] (squeeze-and-excitation)
-      float s[8];
-      load8<F32>(op.skip, static_cast<size_t>(b) * op.lds + c, s);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) y[q] *= s[q];
-    } else if (op.has_skip) {
+    if (op.has_skip) {
       float s[8];
       load8<F32>(op.skip, static_cast<size_t>(m) * op.lds + c, s);
 #pragma unroll
@@ -1077,8 +1096,55 @@ __device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
   }
 }
 
+// Eltwise ops of the NEXT-2 tenants, out of line (own register allocation):
+// a standalone BatchNorm (folded scale / bias; DenseNet's pre-activation on
+// a concat), the squeeze-and-excitation channel scale x * s[n][c], and the
+// hardswish / hardsigmoid activations (PyTorch's definitions); y = act(
+// (x * scale + bias) [+ skip | * s]), 8 channels per task as cc_item.
+__device__ __noinline__ void cc_item_ext(const OpDev& op, const Item& it, int tid) {
+  const int G = op.bn >> 3;
+  const int c = it.nt * op.bn + (tid % G) * 8;
+  if (c >= op.Cout) return;
+  const int HoWo = op.Ho * op.Wo;
+  const int pstep = CC_THREADS / G;
+  const int mb = it.mt * op.bm + tid / G;
+  float sc[8], bi[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { sc[q] = op.affine ? op.scale[c + q] : 1.0f; bi[q] = op.affine ? op.bias[c + q] : 0.0f; }
+  for (int j = 0; j < CC_TASKS_PER_THREAD; ++j) {
+    const int m = mb + j * pstep;
+    if (m >= op.M) break;
+    float y[8], s[8];
+    if (op.f32) load8<true>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
+    else load8<false>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
+    if (op.affine) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], sc[q], bi[q]);
+    }
+    if (op.has_skip) {
+      const size_t row = op.has_skip == 2 ? static_cast<size_t>(m / HoWo) : static_cast<size_t>(m);
+      if (op.f32) load8<true>(op.skip, row * op.lds + c, s);
+      else load8<false>(op.skip, row * op.lds + c, s);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = op.has_skip == 2 ? y[q] * s[q] : y[q] + s[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float v = y[q];
+      if (op.act == ACT_RELU) v = fmaxf(v, 0.0f);
+      else if (op.act == ACT_RELU6) v = fminf(fmaxf(v, 0.0f), 6.0f);
+      else if (op.act == ACT_HSWISH) v = v * (fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f));
+      else if (op.act == ACT_HSIGMOID) v = fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
+      y[q] = v;
+    }
+    if (op.f32) store8<true>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+    else store8<false>(op.out, static_cast<size_t>(m) * op.ldo + c, y, op.out_f32);
+  }
+}
+
 __device__ __forceinline__ void run_cc(const OpDev& op, const Item& it, int tid, float* red) {
-  if (op.kind == DK_SIMT_GEMM) simt_item(op, it, tid, CC_THREADS);
+  if (op.kind == DK_ELTWISE && (op.act > ACT_RELU6 || op.affine || op.has_skip == 2)) cc_item_ext(op, it, tid);
+  else if (op.kind == DK_SIMT_GEMM) simt_item(op, it, tid, CC_THREADS);
   else if (op.f32) cc_item<true>(op, it, tid, red);
   else cc_item<false>(op, it, tid, red);
 }
@@ -1475,6 +1541,7 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     tc_fence_after();
     const uint32_t d = cx.tmem + abuf * BN_MAX;
     const bool mn = op.a_mode == A_MN;    // both operands MN-major (weight gradient)
+    const bool i8 = op.a_mode == A_IM2COL8;   // no-swizzle core-matrix layout (8-channel stems)
     const uint32_t idesc = make_idesc(op.bn) | (mn ? ((1u << 15) | (1u << 16)) : 0u);
     const int mrep = op.mrep;
     const uint32_t d2 = d + static_cast<uint32_t>(op.bn);   // second accumulator (M-pair tiles)
@@ -1498,6 +1565,14 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
           for (int kk = 0; kk < BK / 16; ++kk)
             umma_bf16(d, make_sdesc_mn(a_base + kk * 2048), make_sdesc_mn(b_base + kk * 2048), idesc,
                       (i > 0 || kk > 0) ? 1u : 0u);
+#ifndef GACER_NO_I8_CODE
+        } else if (i8) {
+          const uint32_t lbo_b = static_cast<uint32_t>(op.bn) * 16u;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(d, make_sdesc_none(a_base + kk * 4096, 2048, 128),
+                      make_sdesc_none(b_base + kk * 2 * lbo_b, lbo_b, 128), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+#endif
         } else {
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
@@ -1664,8 +1739,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
                                                          : make_uint4(0, 0, 0, 0);
       }
     }
-    const bool lean_act = op.act <= ACT_RELU6;   // clamp-only activations (hardswish: general path)
-    if (split == 1 && !staged && !op.out_f32 && !swap && lean_act) {
+    if (split == 1 && !staged && !op.out_f32 && !swap) {
       // lean direct bf16 path: same math as the staged path below, each
       // thread storing its row's 8-column groups with 16-byte global stores
       // (no staging buffer, no TMA-store waits)
@@ -1724,7 +1798,7 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
       }
       if (etid == 0 && p.trace && p.single_op < 0)   // column loop done (diagnostics)
         p.trace[static_cast<size_t>(it.idx) * TRACE_FIELDS + 11] = static_cast<int64_t>(globaltimer());
-    } else if (split == 1 && staged && !op.out_f32 && lean_act) {
+    } else if (split == 1 && staged && !op.out_f32) {
 #if GACER_EPI_V == 0
       // lean staged bf16 path: branch-free activation clamp, 64-column
       // staging chunks (a compile-time constant), scale/bias by shuffle

@@ -114,7 +114,13 @@ constexpr int WIN_SMEM_BYTES = WIN_IN_BYTES + (9 + 2) * 64 * 4 + 1024;  // + dw 
 // staged transposes): A = dy [pixels][Cout] (2-D TMA, 64 channels x 64
 // pixels per box), B = im2col(x) (im2col TMA, 64 pixels x 64 channels of one
 // tap per box); K runs over the output pixels.
-enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2, A_MN = 3 };
+// A_IM2COL8: an 8-channel input (the graph's RGB image padded to 8): each
+// K-block holds 8 filter taps; A = 8 im2col TMA boxes of 128 pixels x 8
+// channels (16 B) in the no-swizzle K-major core-matrix layout (8 rows x
+// 16 B per core matrix, SBO 128 B, the next tap LBO 2 KB), B = the weights
+// pre-packed in the same layout per (N-tile, K-block) and fetched with one
+// bulk copy.  Replaces the cp.async gather for stems (7x7 s2, 11x11 s4, 3x3).
+enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2, A_MN = 3, A_IM2COL8 = 4 };
 
 struct OpDev {
   int32_t kind;            // DevKind

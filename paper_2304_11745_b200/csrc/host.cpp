@@ -548,7 +548,8 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           if (a == b || other == 0) break;  // x + x or a skip from the raw input: not fused
           F.skip_t = other;
           has_add = true;
-        } else if (act_of(co.kind) != ACT_NONE) {
+        } else if (co.kind == GACER_OP_RELU || co.kind == GACER_OP_RELU6) {
+          // (hardswish / hardsigmoid stay separate eltwise ops: executor.cu cc_item_ext)
           F.act = act_of(co.kind);
           F.members.push_back(c);
           taken[c] = 1;
@@ -764,6 +765,11 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           const int c8 = roundup(F.Cin, 8), c64 = roundup(F.Cin, 64);
           const bool tma = c64 == c8 || F.kh * F.kw == 1 || 2 * c64 <= 3 * c8;
           F.a_mode = F.swap ? A_ROWS : (tma ? A_IM2COL : A_GATHER);
+          // an 8-channel input with a large filter (7x7, 11x11 stems): 8 taps
+          // per K-block by TMA.  (3x3: the cp.async gather's M-pair tiles win
+          // in a round -- same-box A/B on D2)
+          if (F.a_mode == A_GATHER && c8 == 8 && X.ldc == 8 && F.kh * F.kw >= 25 && !env_flag("GACER_NO_IM2COL8"))
+            F.a_mode = A_IM2COL8;
           F.cread = (F.a_mode == A_IM2COL) ? c64 : c8;
           // M-pair tiles (two 128-row accumulators sharing each B stage) for
           // narrow (Cout <= 128), very wide layers (>= 2 tiles per SM even
@@ -776,7 +782,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           //  would grow from 7 to 49 K-blocks)
           // (the cp.async gather fills both 128-row halves too, so a small-Cin
           //  layer keeps its short 8-channel K stride)
-          if (!F.swap && F.Cout <= 128 && F.Cin <= 64 &&
+          if (!F.swap && F.a_mode != A_IM2COL8 && F.Cout <= 128 && F.Cin <= 64 &&
               cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= 2 * kSplitSms && !env_flag("GACER_NO_MPAIR"))
             F.mrep = 2;
           // 1x1 stride-1 conv over a dense NHWC tensor is a plain GEMM: tiled TMA rows
@@ -830,9 +836,19 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         for (int co = 0; co < F.Cout; ++co)
           for (int r = 0; r < F.kh; ++r)
             for (int s = 0; s < F.kw; ++s)
-              for (int c = 0; c < F.Cin; ++c)
-                F.w_bf16[static_cast<size_t>(co) * F.Kpad + (r * F.kw + s) * F.cread + c] =
-                    f32_to_bf16_rne(wval(co, c, r, s));
+              for (int c = 0; c < F.Cin; ++c) {
+                const int k = (r * F.kw + s) * F.cread + c;
+                size_t at = static_cast<size_t>(co) * F.Kpad + k;
+                if (F.a_mode == A_IM2COL8) {
+                  // per (N-tile, K-block) a contiguous bn x 64 block in the
+                  // no-swizzle K-major core-matrix layout the MMA reads:
+                  // (n % 8) * 16 B + (n / 8) * 128 B + (k % 8) * 2 B + (k % 64 / 8) * bn * 16 B
+                  const int nt = co / F.bn, n = co % F.bn, kb = k / BK, kk = k % BK;
+                  at = (static_cast<size_t>(nt) * F.nkb + kb) * F.bn * BK +
+                       ((n % 8) * 8 + (n / 8) * 64 + (kk % 8) + (kk / 8) * F.bn * 8);
+                }
+                F.w_bf16[at] = f32_to_bf16_rne(wval(co, c, r, s));
+              }
         F.scale.resize(roundup(F.Cout, 8) + 8, 0.0f);
         F.bias.resize(roundup(F.Cout, 8) + 8, 0.0f);
       }
@@ -1028,7 +1044,8 @@ int encode_rows(CUtensorMap* m, const void* base, int cols, int rows, int ld, in
 // NHWC bf16 activation as an im2col view: 128 output pixels x 64 channels of
 // one filter tap per load (pixelsPerColumn = BM, channelsPerPixel = BK).
 // Bounding box per CUTLASS fprop convention: lower = -pad, upper = pad - (k-1).
-int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c, int pix_box = BM) {
+int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c, int pix_box = BM, int ch_box = BK,
+                  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   // globalDim[0] is the tensor's real channel count: channels [Cin, cread)
   // of a 64-channel box are out of bounds and zero-filled by the TMA
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(real_c), static_cast<cuuint64_t>(d.W),
@@ -1039,8 +1056,8 @@ int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c, int pix_box = BM) 
   const int upper[2] = {d.pw - (d.kw - 1), d.ph - (d.kh - 1)};
   const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(d.stride), static_cast<cuuint32_t>(d.stride), 1};
   CUresult r = g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d.in), dims, st, lower, upper,
-                               BK, static_cast<cuuint32_t>(pix_box), es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_128B,
+                               static_cast<cuuint32_t>(ch_box), static_cast<cuuint32_t>(pix_box), es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "cuTensorMapEncodeIm2col failed (%d)", static_cast<int>(r));
   return 0;
@@ -1106,8 +1123,10 @@ int rebuild_op_table() {
       if (!rc) rc = encode_rows(&maps[3 * i + 1], d.act_b, d.K, d.B, d.ldb, d.bn);
     } else {
       if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[3 * i], d, F.Cin);
+      else if (d.a_mode == A_IM2COL8) rc = encode_im2col(&maps[3 * i], d, F.Cin, BM, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
       else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[3 * i], d.in, d.K, d.M, d.ldi, BM);
-      if (!rc) rc = encode_rows(&maps[3 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
+      if (!rc && d.a_mode != A_IM2COL8)   // (IM2COL8: B is a bulk copy of pre-packed blocks)
+        rc = encode_rows(&maps[3 * i + 1], d.wt, d.Kpad, d.tiles_n * d.bn, d.Kpad, d.bn);
       // output [M][Cout] (row stride ldo) for the TMA-store epilogue
       const int esz = d.out_f32 ? 4 : 2;
       const bool ok = (static_cast<long long>(d.ldo) * esz) % 16 == 0 &&

@@ -174,6 +174,8 @@ def lib():
             raise RuntimeError(f"{LIB_PATH} not built; run __graft_entry__.build()")
         _lib = C.CDLL(LIB_PATH)
         for name, (args, res) in EXPORTS.items():
+            if os.environ.get("GACER_LIB") and not hasattr(_lib, name):
+                continue          # an older A/B build may lack newer entry points
             f = getattr(_lib, name)
             f.argtypes = args
             f.restype = res
