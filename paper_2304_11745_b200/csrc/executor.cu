@@ -337,6 +337,10 @@ constexpr int TMEM_COLS = 2 * BN_MAX;   // double-buffered accumulators
 constexpr int A2_OFF = 16384;            // M-pair tiles: second A block inside the stage's B region
 constexpr int RING_CONSUMERS = 1 + 1 + NEPI / 32;  // worker group, MMA thread, epilogue warps
 
+struct EpiItem {             // the epilogue's copy of an Item: the fields it and the releaser use
+  int32_t op, mt, nt, ks, idx, chunk, cluster, bud;
+};
+
 struct RingSlot {            // scheduler -> workers / MMA / epilogue
   Item it;
   int32_t idx;               // item index, -1 = STOP
@@ -563,16 +567,22 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       const void* tmap_b = op.tmap_b;
       fence_proxy_async_global();   // acquired producer data -> this thread's TMA reads
       // im2col start (top-left input tap) of each 128-row half of the tile
-      int w0[2] = {0, 0}, h0[2] = {0, 0}, img0[2] = {0, 0};
+      // (scalars, not arrays: a dynamically indexed array lives in local
+      //  memory, and the other roles' gpu-scope fences invalidate L1, so each
+      //  K-block's reload would be an L2 round trip)
+      int w0a = 0, h0a = 0, img0a = 0, w0b = 0, h0b = 0, img0b = 0;
       if (a_mode == A_IM2COL || a_mode == A_IM2COL8) {
         const int HoWo = op.Ho * op.Wo, Wo = op.Wo;
-        for (int hf = 0; hf < mrep; ++hf) {
-          const int mm = m0 + hf * BM;
-          img0[hf] = mm / HoWo;
-          const int rem = mm - img0[hf] * HoWo;
-          const int ho = rem / Wo, wo = rem - (rem / Wo) * Wo;
-          w0[hf] = wo * op.stride - op.pw;
-          h0[hf] = ho * op.stride - op.ph;
+        img0a = m0 / HoWo;
+        int rem = m0 - img0a * HoWo;
+        w0a = (rem % Wo) * op.stride - op.pw;
+        h0a = (rem / Wo) * op.stride - op.ph;
+        if (mrep > 1) {
+          const int mm = m0 + BM;
+          img0b = mm / HoWo;
+          rem = mm - img0b * HoWo;
+          w0b = (rem % Wo) * op.stride - op.pw;
+          h0b = (rem / Wo) * op.stride - op.ph;
         }
       }
       // M-pair tiles: the second 128-row A block lands in the stage's B region
@@ -605,7 +615,7 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
             const int tap = kb * 8 + j;
             const bool ok = tap < taps;
             const int r = ok ? tap / kw : 0, sx = ok ? tap - (tap / kw) * kw : 0;
-            tma_load_im2col_4d(a_dst + j * 2048, tmap_a, bar, ok ? 0 : 8, w0[0], h0[0], img0[0],
+            tma_load_im2col_4d(a_dst + j * 2048, tmap_a, bar, ok ? 0 : 8, w0a, h0a, img0a,
                                static_cast<uint16_t>(sx), static_cast<uint16_t>(r));
           }
           const size_t blk = (static_cast<size_t>(it.nt) * op.nkb + kb) * static_cast<size_t>(bbytes);
@@ -636,10 +646,10 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
           const int tap = k / C;
           const int c0 = k - tap * C;
           const int r = tap / kw, sx = tap - r * kw;
-          tma_load_im2col_4d(a_dst, tmap_a, bar, c0, w0[0], h0[0], img0[0], static_cast<uint16_t>(sx),
+          tma_load_im2col_4d(a_dst, tmap_a, bar, c0, w0a, h0a, img0a, static_cast<uint16_t>(sx),
                              static_cast<uint16_t>(r));
           if (mrep > 1)
-            tma_load_im2col_4d(b_dst + A2_OFF, tmap_a, bar, c0, w0[1], h0[1], img0[1], static_cast<uint16_t>(sx),
+            tma_load_im2col_4d(b_dst + A2_OFF, tmap_a, bar, c0, w0b, h0b, img0b, static_cast<uint16_t>(sx),
                                static_cast<uint16_t>(r));
         } else {
           tma_load_2d(a_dst, tmap_a, bar, k, m0);
@@ -1307,8 +1317,9 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
   if (deps_ready(p, it)) { fence_acquire_gpu(); return true; }   // usual case: one parallel check
   if (it.bud >= 0 && !spin_ge(p.chunk_done + it.bud, (p.epoch - 1u) * it.btot + it.boff, p)) return false;
   if (it.dep_count <= INLINE_DEPS) {
-    for (int d = 0; d < it.dep_count; ++d)
-      if (!spin_ge(p.chunk_done + it.dc[d], p.epoch * it.dt[d], p)) return false;
+#pragma unroll
+    for (int d = 0; d < INLINE_DEPS; ++d)   // (static indices: the Item stays in registers)
+      if (d < it.dep_count && !spin_ge(p.chunk_done + it.dc[d], p.epoch * it.dt[d], p)) return false;
   } else {
     for (int d = 0; d < it.dep_count; ++d) {
       const Dep dp = p.deps[it.dep_begin + d];
@@ -1336,8 +1347,10 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
   int last_op = -1;
   const int big = 4 * static_cast<int>(gridDim.x);
   for (;;) {
-    Item its[2];
-    int32_t idxs[2];
+    // one claimed item per pass, in scalars (an indexed Item array would
+    // live in local memory: L2 round trips after every acquire fence)
+    Item itm;
+    int32_t iidx = -1;
     int n_claimed = 0;
     int claimed = -1;
     if (p.single_op >= 0) {
@@ -1349,9 +1362,9 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
       const int n = op.tiles_m * op.tiles_n * (op.kind == DK_GEMM ? op.split_k : 1);
       claimed = sidx < n ? sidx : -2;
       if (claimed >= 0) {
-        its[0] = decode_single(op, p.single_op, sidx);
-        its[0].kind = op.kind;
-        idxs[0] = claimed;
+        itm = decode_single(op, p.single_op, sidx);
+        itm.kind = op.kind;
+        iidx = claimed;
         n_claimed = 1;
       }
       sidx += gridDim.x;
@@ -1408,40 +1421,34 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         }
         sdbg(p, islot, 2, static_cast<int64_t>(globaltimer()));
         const Seg sg = get_seg(p, ctl, si);
-        const uint32_t want = 1;
-        const uint32_t idx = atomicAdd(p.heads + si, want);
+        const uint32_t idx = atomicAdd(p.heads + si, 1u);
         sdbg(p, islot, 3, static_cast<int64_t>(globaltimer()));
         if (idx >= static_cast<uint32_t>(sg.size)) continue;  // lost the race for the last item(s)
-        const uint32_t got = min(want, static_cast<uint32_t>(sg.size) - idx);
-        bool abort = false;
-        for (uint32_t j = 0; j < got; ++j) {
-          if (idx == h && j == 0 && st != 3) {
-            its[j] = cand;
-          } else {
-            // a later item than the one checked: its dependencies are items
-            // claimed before it, so this wait terminates
-            its[j] = p.items[sg.begin + idx + j];
-            if (!wait_deps(p, its[j])) { abort = true; break; }
-          }
-          idxs[j] = sg.begin + static_cast<int>(idx + j);
+        if (idx == h && st != 3) {
+          itm = cand;
+        } else {
+          // a later item than the one checked: its dependencies are items
+          // claimed before it, so this wait terminates
+          itm = p.items[sg.begin + idx];
+          if (!wait_deps(p, itm)) { claimed = -3; break; }
         }
-        if (abort) { claimed = -3; break; }
-        n_claimed = static_cast<int>(got);
-        claimed = idxs[0];
-        last_op = its[got - 1].op;
+        iidx = sg.begin + static_cast<int>(idx);
+        n_claimed = 1;
+        claimed = iidx;
+        last_op = itm.op;
       }
       if (claimed >= 0) fence_acquire_gpu();  // acquire side (pairs with the producers' release)
     }
     dbg_mark(p, 1);
     sdbg(p, islot, 4, static_cast<int64_t>(globaltimer()));
-    sdbg(p, islot, 6, claimed >= 0 ? its[0].op : -1);
+    sdbg(p, islot, 6, claimed >= 0 ? itm.op : -1);
     if (claimed < 0) n_claimed = 0;
-    for (int j = 0; j < (n_claimed > 0 ? n_claimed : 1); ++j) {
+    {
       const uint32_t slot = islot % ITEM_RING;  // free: islot - consumed < LOOKAHEAD < ITEM_RING
       RingSlot& rs = ctl->ring[slot];
-      if (n_claimed > 0) rs.it = its[j];
-      rs.idx = n_claimed > 0 ? idxs[j] : -1;
-      rs.kind = n_claimed > 0 ? its[j].kind : 0;
+      if (n_claimed > 0) rs.it = itm;
+      rs.idx = n_claimed > 0 ? iidx : -1;
+      rs.kind = n_claimed > 0 ? itm.kind : 0;
       rs.t0 = (p.trace || p.stats) ? globaltimer() : 0;
       mbar_arrive(&ctl->rfull[slot]);
       ++islot;
@@ -1659,7 +1666,10 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     mbar_wait(&ctl->rfull[slot], (islot / ITEM_RING) & 1);
     const int idx = ctl->ring[slot].idx;
     const int kind = ctl->ring[slot].kind;
-    const Item it = ctl->ring[slot].it;
+    // only the Item fields the epilogue and the release need (a whole Item
+    // held across the epilogue spilled to local memory)
+    const RingSlot& rsl = ctl->ring[slot];
+    const EpiItem it{rsl.it.op, rsl.it.mt, rsl.it.nt, rsl.it.ks, rsl.it.idx, rsl.it.chunk, rsl.it.cluster, rsl.it.bud};
     const uint64_t t0 = ctl->ring[slot].t0;
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->rempty[slot]);
@@ -2092,7 +2102,8 @@ __device__ void epilogue_role(const ExecParams& p, Ctx& cx) {
     if (etid == 0 && p.single_op < 0) {   // hand the release to the releaser lane
       const uint32_t ls = nrel % ITEM_RING;
       if (nrel >= ITEM_RING) mbar_wait(&ctl->lempty[ls], ((nrel / ITEM_RING) + 1) & 1);
-      ctl->rel[ls].it = it;
+      Item& ri = ctl->rel[ls].it;   // what release_item reads
+      ri.op = it.op; ri.idx = it.idx; ri.chunk = it.chunk; ri.cluster = it.cluster; ri.bud = it.bud;
       ctl->rel[ls].t0 = t0;
       ctl->rel[ls].idx = idx;
       mbar_arrive(&ctl->lfull[ls]);
