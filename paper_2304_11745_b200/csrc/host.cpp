@@ -1131,7 +1131,11 @@ int rebuild_op_table() {
       const int esz = d.out_f32 ? 4 : 2;
       const bool ok = (static_cast<long long>(d.ldo) * esz) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
-      if (!rc && ok && !env_flag("GACER_NO_TMA_STORE")) {
+      // (GACER_DIRECT_SMALL=n, diagnostics: ops of <= n items store directly)
+      const long long items = static_cast<long long>(d.tiles_m) * d.tiles_n * d.split_k;
+      const char* ds = getenv("GACER_DIRECT_SMALL");
+      const bool small_direct = ds && items <= atoll(ds);
+      if (!rc && ok && !env_flag("GACER_NO_TMA_STORE") && !small_direct) {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.Cout), static_cast<cuuint64_t>(d.M)};
         const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ldo) * esz};
         const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32u};  // 32 rows x 128 B
