@@ -374,6 +374,9 @@ constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 row
 // TMA-store staging only with 4 epilogue warps: 8 warps' staging rows do not
 // fit beside the ring; they store their rows directly (16 B per thread)
 constexpr bool EPI_STAGED = NEPI == 128;
+#ifndef GACER_PROD_SPLIT
+#define GACER_PROD_SPLIT 1
+#endif
 #ifndef GACER_EPI_DB
 #define GACER_EPI_DB 1
 #endif
@@ -557,8 +560,14 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
     // filling the stages gi = j (mod NPROD): one thread's TMA loads complete
     // at only ~27-35 B/clk (measured, scripts/micro/tma_rate.cu), far below
     // what the MMA consumes, so the issue is spread over several threads.
-    const int pj = wtid >> 5;
-    if ((wtid & 31) == 0 && pj < NPROD) {
+    // GACER_PROD_SPLIT: the A and the B loads of a stage are issued by two
+    // threads (lane 0 of worker warps pj and pj + NPROD), doubling the TMA
+    // issue parallelism of the plain im2col / rows paths
+    const int pw = wtid >> 5;
+    const int role = (GACER_PROD_SPLIT && pw >= NPROD) ? 1 : 0;   // 0: A loads + arrival, 1: B loads
+    const int pj = pw - role * NPROD;
+    const bool split_ab = GACER_PROD_SPLIT && (op.a_mode == A_IM2COL || op.a_mode == A_ROWS);
+    if ((wtid & 31) == 0 && pj < NPROD && (role == 0 || split_ab)) {
       // every OpDev field the loop needs is loaded once into registers: the
       // SM's L1 is invalidated by the gpu-scope fences of the other roles,
       // so a global re-load per K-block would cost an L2 round trip each
@@ -599,10 +608,14 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
         const uint32_t gi = g + i, stage = gi % STAGES;
         if (gi >= STAGES) mbar_wait(&ctl->empty[stage], ((gi / STAGES) + 1) & 1);
         uint64_t* bar = &ctl->full[stage];
-        mbar_arrive_expect_tx(bar, tx);
         const uint32_t a_dst = ring_base + stage * A_STAGE_BYTES;
         const uint32_t b_dst = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
         const int k = (kb0 + i) * BK;
+        if (role == 1) {   // (the stage's tx count is armed by its A producer; complete_tx may come first)
+          tma_load_2d(b_dst, tmap_b, bar, k, n0);
+          continue;
+        }
+        mbar_arrive_expect_tx(bar, tx);
 #ifndef GACER_NO_I8_CODE
         if (a_mode == A_IM2COL8) {
           // 8 taps of 8 channels: one 128-pixel x 16-byte im2col box per tap
@@ -655,7 +668,7 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
           tma_load_2d(a_dst, tmap_a, bar, k, m0);
           if (mrep > 1) tma_load_2d(b_dst + A2_OFF, tmap_a, bar, k, m0 + BM);
         }
-        tma_load_2d(b_dst, tmap_b, bar, k, n0);
+        if (!split_ab) tma_load_2d(b_dst, tmap_b, bar, k, n0);
         kdbg(p, 1, gi);
       }
       if (pj == 0) dbg_mark(p, 2);
