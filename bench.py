@@ -99,6 +99,22 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "n_samples": len(self.samples)}
 
 
+class _stdout_to_stderr:
+    """NCCL's communicator creation prints its version on stdout; the
+    bench's stdout is one JSON line, so fd 1 points at stderr meanwhile."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 # ------------------------------------------------------------------ workload
 def make_workload(cfg=CONFIG, rank=0):
     """The config's tenants with seeded random-init weights; each rank (GPU
@@ -448,7 +464,8 @@ def run_d4(args, rank, world, dist):
         import torch.distributed as dist_mod
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29541")
-        dist_mod.init_process_group("nccl", rank=0, world_size=1)
+        with _stdout_to_stderr():
+            dist_mod.init_process_group("nccl", rank=0, world_size=1)
         dp_group = dist_mod
     else:
         dp_group = dist
@@ -478,7 +495,8 @@ def run_d4(args, rank, world, dist):
     ar = None
     if dp:
         from paper_2304_11745_b200.grad_allreduce import ExecutorAllReduce
-        ar = ExecutorAllReduce(s, 0, dp_group)
+        with _stdout_to_stderr():      # (the communicator is created here)
+            ar = ExecutorAllReduce(s, 0, dp_group)
     plans = {"priority": ("priority", None), "hybrid": ("hybrid", None),
              "work_conserving": ("work_conserving", None), "strict[.7,.2,.1]": ("strict", [0.7, 0.2, 0.1])}
     plan_ms = {}
@@ -608,7 +626,10 @@ def main():
         if args.impl == "gacer":
             import torch
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist_mod.init_process_group(backend)
+        with _stdout_to_stderr():
+            dist_mod.init_process_group(backend)
+            if backend == "nccl":
+                dist_mod.barrier()     # creates the communicator (prints the NCCL version)
         dist = dist_mod
     if args.impl == "reference":
         run_reference(args, rank)

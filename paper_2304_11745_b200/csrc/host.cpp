@@ -39,7 +39,7 @@ cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, i
                                     int ph, int pw, int64_t M, int Kpad, void* out, cudaStream_t s);
 cudaError_t launch_wgrad_permute(const float* g, int Cout, int Cin, int KH, int KW, float* dw, cudaStream_t s);
 cudaError_t launch_fwd_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
-                              void* out, cudaStream_t s);
+                              void* out, cudaStream_t s, int block_bn = 0);
 cudaError_t launch_wgrad_reduce(const float* part, int Cout, int Cin, int KH, int KW, int bn, int tiles_n, int split,
                                 float* dw, cudaStream_t s);
 }  // namespace gacer
@@ -2730,6 +2730,9 @@ int fwd_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride,
   if (Cin % 64 == 0) {
     g.cread = Cin;
     g.a_mode = (KH * KW == 1 && stride == 1 && ph == 0 && pw == 0) ? A_ROWS : A_IM2COL;
+  } else if (Cin == 8 && KH * KW >= 25 && !env_flag("GACER_NO_IM2COL8")) {
+    g.cread = 8;                         // the image stem: 8 taps per K-block by TMA (A_IM2COL8)
+    g.a_mode = A_IM2COL8;
   } else {
     g.cread = Cin;                       // cp.async gather, 8-channel granules
     g.a_mode = A_GATHER;
@@ -2778,7 +2781,8 @@ int32_t gacer_conv_fwd(const void* x_dev, const float* w_dev, int32_t N, int32_t
   void* wt = ws + g.off_w;
   const float *scale = nullptr, *bias = nullptr;
   const int nsb = g.rows + 8;
-  CUDA_TRY(launch_fwd_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
+  CUDA_TRY(launch_fwd_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st,
+                             g.a_mode == A_IM2COL8 ? g.bn : 0));
   if (int rc0 = unit_vectors(nsb, &scale, &bias)) return rc0;
   OpDev d;
   std::memset(&d, 0, sizeof d);
@@ -2802,8 +2806,9 @@ int32_t gacer_conv_fwd(const void* x_dev, const float* w_dev, int32_t N, int32_t
   d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
   int rc = 0;
   if (g.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, Cin);
+  else if (g.a_mode == A_IM2COL8) rc = encode_im2col(&maps[0], d, Cin, BM, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
   else if (g.a_mode == A_ROWS) rc = encode_rows(&maps[0], x_dev, g.K, g.M, Cin, BM);
-  if (!rc) rc = encode_rows(&maps[1], wt, g.Kpad, g.rows, g.Kpad, g.bn);
+  if (!rc && g.a_mode != A_IM2COL8) rc = encode_rows(&maps[1], wt, g.Kpad, g.rows, g.Kpad, g.bn);
   if (rc) return rc;
   {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(g.M)};
@@ -2916,9 +2921,13 @@ struct TrainLowering {
     }
     op.step_pos = step;
     if (op.kind == DK_VGRID) {
-      // items: one wave of the SMs' worth of virtual-block ranges (streaming
-      // operators: per-item claim/release overhead amortised)
-      op.per = std::max(1, cdiv(op.vblocks, kSplitSms));
+      // items: one wave of the executor's CTAs' worth of virtual-block ranges
+      // (streaming operators: per-item claim/release overhead amortised).
+      // The grid of this instance, not the SM count: with SMs reserved for a
+      // collective, 148 items on 136 CTAs would take two waves.  Results do
+      // not depend on it (the virtual-block decomposition is fixed).
+      const int grid = S.opts.num_ctas > 0 ? S.opts.num_ctas : (S.num_sms > 0 ? S.num_sms : kSplitSms);
+      op.per = std::max(1, cdiv(op.vblocks, grid));
       op.items = cdiv(op.vblocks, op.per);
     } else {
       op.items = op.gd.tiles_m * op.gd.tiles_n * op.gd.split_k;
@@ -3072,6 +3081,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         f.vp[0] = pref(i, 0); f.vp[1] = bref(wp);
         f.va.i[0] = o.c_out; f.va.i[1] = x.c; f.va.i[2] = o.kh; f.va.i[3] = o.kw; f.va.i[4] = fg.cread;
         f.va.i[5] = fg.Kpad; f.va.i[6] = fg.rows; f.va.i[7] = 1;
+        f.va.i[8] = fg.a_mode == A_IM2COL8 ? fg.bn : 0;   // block layout of the 8-channel TMA path
         L.add(std::move(f), {T.buf_params}, {wp});
         const int yb = L.buf(static_cast<size_t>(B) * y.h * y.w * y.c * 2);
         TrainOp m;
@@ -3479,8 +3489,9 @@ int build_train_opdev(const Tenant& T, int tenant_id, const TrainOp& op, OpDev& 
     if (rc) return rc;
   } else {
     if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, op.im2col_c);
+    else if (d.a_mode == A_IM2COL8) rc = encode_im2col(&maps[0], d, op.im2col_c, BM, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
     else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[0], d.in, op.gemm_kind == 2 ? d.Kpad : d.K, op.a_rows, op.a_ld, BM);
-    if (!rc) rc = encode_rows(&maps[1], d.wt, d.Kpad, op.b_rows, d.Kpad, d.bn);
+    if (!rc && d.a_mode != A_IM2COL8) rc = encode_rows(&maps[1], d.wt, d.Kpad, op.b_rows, d.Kpad, d.bn);
     if (rc) return rc;
   }
   if (op.gemm_kind != 2 && d.out && (static_cast<long long>(d.ldo) * 2) % 16 == 0) {

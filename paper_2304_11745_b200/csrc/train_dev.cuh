@@ -683,14 +683,21 @@ VG_FN void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) 
 // a K-major bf16 GEMM B operand [rows][Kpad]: forward = 1: row co, column
 // (r*KW + s)*cread + ci = w[co][ci][r][s]; forward = 0 (data gradient): row
 // ci, column (r*KW + s)*cread + co = w[co][ci][KH-1-r][KW-1-s]; padding 0.
-// a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward
+// a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward, i8 block bn
 VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* w = static_cast<const float*>(a.p[0]);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
   const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], cread = a.i[4], Kpad = a.i[5], rows = a.i[6],
-            forward = a.i[7];
+            forward = a.i[7], bbn = a.i[8];
   VG_LOOP(i, static_cast<int64_t>(rows) * Kpad) {
     const int row = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
+    // bbn > 0: the A_IM2COL8 block layout -- per (N-tile, K-block) a bn x 64
+    // block in the no-swizzle core-matrix layout (same bijection as the
+    // inference packing in host.cpp)
+    const int64_t dst = bbn > 0 ? (static_cast<int64_t>(row / bbn) * (Kpad / 64) + k / 64) * bbn * 64 +
+                                      ((row % bbn) % 8) * 8 + ((row % bbn) / 8) * 64 + (k % 64) % 8 +
+                                      ((k % 64) / 8) * bbn * 8
+                                : i;
     const int tap = k / cread, col = k % cread;
     float v = 0.0f;
     if (forward) {
@@ -700,7 +707,7 @@ VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t
       const int r = tap / KW, s = tap % KW;
       v = w[((static_cast<int64_t>(col) * Cin + row) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
     }
-    out[i] = __float2bfloat16_rn(v);
+    out[dst] = __float2bfloat16_rn(v);
   }
 }
 

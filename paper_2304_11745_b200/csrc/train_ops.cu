@@ -75,10 +75,11 @@ cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int K
 }
 
 cudaError_t launch_fwd_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
-                              void* out, cudaStream_t s) {
+                              void* out, cudaStream_t s, int block_bn) {
   VArgs a = vargs();
   a.p[0] = w; a.p[1] = out;
   a.i[0] = Cout; a.i[1] = Cin; a.i[2] = KH; a.i[3] = KW; a.i[4] = cread; a.i[5] = Kpad; a.i[6] = rows; a.i[7] = 1;
+  a.i[8] = block_bn;
   return vlaunch(VF_FILTER, a, vg_grid_for(static_cast<int64_t>(rows) * Kpad), s);
 }
 

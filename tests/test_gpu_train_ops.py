@@ -271,3 +271,36 @@ def test_conv_wgrad_mn_major_matches_staged(T, N, H, W, Cin, Cout, k, s, p, monk
             G.gacer_shutdown()
         outs.append(dw.cpu().numpy())
     assert maxrel(outs[0], outs[1]) <= 1e-5, maxrel(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("N,H,W,Cin,Cout,k,s,p", [(2, 32, 32, 8, 64, 7, 2, 3), (3, 40, 36, 8, 64, 7, 2, 3),
+                                                   (2, 16, 16, 64, 64, 3, 1, 1), (2, 14, 14, 8, 32, 3, 1, 1)])
+def test_conv_fwd_train_tcgen05(T, N, H, W, Cin, Cout, k, s, p):
+    """gacer_conv_fwd (the training tenant's forward conv on device-resident
+    fp32 master weights): the 7x7 stem through the 8-channel TMA path
+    (A_IM2COL8: per-tap 16-byte im2col boxes, block-packed weights), 3x3 64
+    channels through TMA im2col, 8-channel 3x3 through the gather -- vs the
+    oracle's direct convolution of the bf16-rounded filter, 2e-2 and 99.9%
+    exact bf16 RNE."""
+    torch, G, OT = T
+    from oracle import ops as oops
+    rng = np.random.default_rng(Cin * 7 + Cout + H)
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    x = _bf16(torch, rng.normal(size=(N, H, W, Cin)))
+    w = (rng.normal(size=(Cout, Cin, k, k)) * np.sqrt(2.0 / (Cin * k * k))).astype(np.float32)
+    wd = torch.from_numpy(w).cuda()
+    y = torch.empty((N, Ho, Wo, Cout), dtype=torch.bfloat16, device="cuda")
+    G.gacer_init(0)
+    try:
+        nb = G.conv_fwd_workspace(N, H, W, Cin, Cout, k, k, s, p, p)
+        ws = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
+        base = (ws.data_ptr() + 255) // 256 * 256
+        G.conv_fwd(x.data_ptr(), wd.data_ptr(), N, H, W, Cin, Cout, k, k, s, p, p, y.data_ptr(), base, nb)
+        torch.cuda.synchronize()
+    finally:
+        G.gacer_shutdown()
+    ref = oops.conv2d(_nchw(_np(x), N, H, W, Cin), workloads_bf16(w), None, s, (p, p))
+    got = _nchw(_np(y), N, Ho, Wo, Cout)
+    assert maxrel(got, ref) <= 2e-2
+    rne = workloads_bf16(ref.astype(np.float32)).astype(np.float64)
+    assert np.mean(got == rne) >= 0.999, np.mean(got == rne)
