@@ -2,8 +2,8 @@
 draws T tenants with replacement from {AlexNet, VGG-16, ResNet-18, ResNet-50,
 ResNet-101, Inception-v3, MobileNetV2} (seed 5000 + point id) at batch B, and
 measures the executor (identity plan and the best SM partition) against the
-sequential and one-stream-per-tenant baselines (same kernels), L2 flushed
-between rounds.  Writes gpurun_out/d5_sweep.json."""
+sequential and one-stream-per-tenant baselines (same kernels; plain and
+captured as CUDA graphs), L2 flushed between rounds.  Writes gpurun_out/d5_sweep.json."""
 import json
 import os
 import sys
@@ -17,7 +17,7 @@ from paper_2304_11745_b200 import gacer as G  # noqa: E402
 from paper_2304_11745_b200.runtime import Session  # noqa: E402
 
 POOL = ["alexnet", "vgg16", "resnet18", "resnet50", "resnet101", "inception_v3", "mobilenet_v2"]
-POINTS = [(2, 4), (4, 4), (8, 4), (16, 1), (4, 16), (8, 16)]   # (tenants, batch)
+POINTS = [(2, 4), (4, 4), (8, 4), (16, 1), (4, 16), (8, 16), (2, 64), (4, 64)]   # (tenants, batch)
 stream = torch.cuda.Stream()
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda:0")
 torch.cuda.set_stream(stream)
@@ -34,7 +34,7 @@ for pid, (T, B) in enumerate(POINTS):
     for t, x in enumerate(xs):
         s.set_input(t, x)
     row = {"point": pid, "tenants": names, "batch": B}
-    for mode in ("sequential", "multistream"):
+    for mode in ("sequential", "multistream", "sequential_graph", "multistream_graph"):
         row[f"{mode}_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, mode, 5, 2, flush)))
     best = None
     for part in ("priority", "work_conserving", "hybrid"):
@@ -46,6 +46,8 @@ for pid, (T, B) in enumerate(POINTS):
     row["inferences_per_s"] = T * B / (best / 1000.0)
     row["speedup_vs_sequential"] = row["sequential_ms"] / best
     row["speedup_vs_multistream"] = row["multistream_ms"] / best
+    row["speedup_vs_multistream_graph"] = row["multistream_graph_ms"] / best
+    row["executor_identity_vs_multistream_graph"] = row["multistream_graph_ms"] / row["executor_priority_ms"]
     s.close()
     out.append(row)
     print(json.dumps(row), flush=True)

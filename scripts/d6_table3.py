@@ -61,6 +61,8 @@ for part in ("priority", "work_conserving"):
     res[f"sequential_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, "sequential", 5, 2, flush)))
     s.set_mode("multistream")
     res[f"multistream_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, "multistream", 5, 2, flush)))
+    res["multistream_graph_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, "multistream_graph", 5, 2, flush)))
+    res["sequential_graph_ms"] = float(np.median(bench.time_mode(G, s, torch, stream, "sequential_graph", 5, 2, flush)))
     s.close()
 os.makedirs("gpurun_out", exist_ok=True)
 with open("gpurun_out/d6_table3.json", "w") as f:
