@@ -26,8 +26,29 @@ enum VFn : int32_t {
   VF_BN_PARTIAL, VF_BN_FINALIZE, VF_BN_APPLY, VF_RELU_BWD, VF_ADD,
   VF_MAXPOOL_FWD, VF_MAXPOOL_ARGMAX, VF_MAXPOOL_BWD, VF_GAP_FWD, VF_GAP_BWD,
   VF_LINEAR_FWD, VF_LINEAR_DX, VF_LINEAR_DW, VF_SOFTMAX_CE, VF_MEAN, VF_SGD,
-  VF_FILTER, VF_DILATE, VF_TRANSPOSE_IM2COL, VF_WGRAD_PERMUTE, VF_WGRAD_REDUCE,
+  VF_FILTER, VF_DILATE, VF_TRANSPOSE_IM2COL, VF_WGRAD_PERMUTE, VF_WGRAD_REDUCE, VF_PHASE_SCATTER,
 };
+
+// Phase decomposition of a strided conv's data gradient (stride S): input
+// pixel h with (h + p) mod S = a receives exactly the taps r = a + S i, from
+// dy rows u - i with u = (h + p - a) / S -- a stride-1 conv of dy with the
+// KI = ceil((K - a) / S)-tap sub-filter over the output rows u in [u0, u1).
+struct DgPhase {
+  int K;        // taps of the phase along this dimension (0: no tap reaches it)
+  int u0, n;    // first output index u and the count of them (u in [u0, u0 + n))
+  int pad;      // the phase conv's low padding: K - 1 - u0 (its first window starts at u0 - (K - 1))
+};
+__host__ __device__ inline DgPhase dg_phase(int a, int K, int S, int p, int H) {
+  DgPhase d;
+  d.K = a < K ? (K - a + S - 1) / S : 0;
+  const int lo = p - a;                                   // h + p - a = S u  =>  u >= (p - a) / S for h >= 0
+  d.u0 = lo <= 0 ? 0 : (lo + S - 1) / S;
+  const int hi = H - 1 + p - a;                           // h <= H - 1
+  d.n = hi < 0 ? 0 : hi / S + 1 - d.u0;
+  if (d.n < 0) d.n = 0;
+  d.pad = d.K - 1 - d.u0;
+  return d;
+}
 
 // Virtual-grid geometry, shared by the host lowering and the standalone calls.
 constexpr int VG_THREADS = 192;               // = NWORK: the executor's worker group

@@ -33,6 +33,10 @@ cudaError_t launch_op(const ExecParams& base, const OpDev* ops_dev, int op_idx, 
 cudaError_t launch_dgrad_filter(const float* w, int Cout, int Cin, int KH, int KW, int cread, int Kpad, int rows,
                                 void* out, cudaStream_t s);
 cudaError_t launch_fill(float* p, int n, float v, cudaStream_t s);
+cudaError_t launch_dgrad_phase_filter(const float* w, int Cout, int Cin, int KI, int KJ, int cread, int Kpad, int rows,
+                                      int S, int pa, int pb, int KH, int KW, void* out, cudaStream_t s);
+cudaError_t launch_phase_scatter(const void* const* phase_out, int N, int H, int W, int C, int S, int ph, int pw,
+                                 int KH, int KW, void* dx, cudaStream_t s);
 cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, int Hdd, int Wdd, void* out,
                           cudaStream_t s);
 cudaError_t launch_transpose_im2col(const void* x, int N, int H, int W, int C, int Ho, int Wo, int KH, int KW, int S,
@@ -163,6 +167,8 @@ struct TrainOp {
   TRef g_in, g_out, g_wt, g_part, g_scale, g_bias;
   int gemm_kind = 0;             // 0 forward conv, 1 data gradient, 2 weight gradient
   int im2col_c = 0;              // real channels of the im2col tensor map
+  bool has_upper = false;        // explicit im2col upper corner (dgrad phases)
+  int im2col_upper[2] = {0, 0};
   int a_ld = 0, a_rows = 0, b_rows = 0;
   std::vector<int> deps;         // producer ops (indices into tops): RAW / WAR / WAW on buffers
   std::vector<std::pair<int64_t, int64_t>> grad_ranges;   // flat-gradient slices written (floats)
@@ -1045,7 +1051,7 @@ int encode_rows(CUtensorMap* m, const void* base, int cols, int rows, int ld, in
 // one filter tap per load (pixelsPerColumn = BM, channelsPerPixel = BK).
 // Bounding box per CUTLASS fprop convention: lower = -pad, upper = pad - (k-1).
 int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c, int pix_box = BM, int ch_box = BK,
-                  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+                  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B, const int* upper_hw = nullptr) {
   // globalDim[0] is the tensor's real channel count: channels [Cin, cread)
   // of a 64-channel box are out of bounds and zero-filled by the TMA
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(real_c), static_cast<cuuint64_t>(d.W),
@@ -1053,7 +1059,9 @@ int encode_im2col(CUtensorMap* m, const OpDev& d, int real_c, int pix_box = BM, 
   const cuuint64_t st[3] = {static_cast<cuuint64_t>(d.ldi) * 2, static_cast<cuuint64_t>(d.ldi) * 2 * d.W,
                             static_cast<cuuint64_t>(d.ldi) * 2 * d.W * d.H};
   const int lower[2] = {-d.pw, -d.ph};
-  const int upper[2] = {d.pw - (d.kw - 1), d.ph - (d.kh - 1)};
+  // (upper_hw: an explicit upper corner -- the output count per row is
+  //  W + upper - lower, e.g. the phases of a strided conv's data gradient)
+  const int upper[2] = {upper_hw ? upper_hw[1] : d.pw - (d.kw - 1), upper_hw ? upper_hw[0] : d.ph - (d.kh - 1)};
   const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(d.stride), static_cast<cuuint32_t>(d.stride), 1};
   CUresult r = g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d.in), dims, st, lower, upper,
                                static_cast<cuuint32_t>(ch_box), static_cast<cuuint32_t>(pix_box), es,
@@ -2418,10 +2426,26 @@ int unit_vectors(int n, const float** ones, const float** zeros) {
 // A11: convolution data gradient on the tcgen05 implicit-GEMM path
 // ------------------------------------------------------------------------
 namespace {
+struct DgPhaseGemm {        // one phase (a, b) of a strided conv's data gradient
+  int a, b;
+  DgPhase vh, vw;
+  int K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode;
+  int upper[2];              // explicit im2col upper corner (h, w)
+  size_t off_op, off_maps, off_w, off_out;
+};
 struct DgradGeom {
   int cread, K, Kpad, nkb, bn, tiles_m, tiles_n, rows, M, a_mode, ph, pw, Hd, Wd, Hdd, Wdd;
   size_t off_op, off_maps, off_w, off_dil, bytes;
+  // stride > 1: phase-decomposed (no zero-dilated dy): one stride-1 GEMM per
+  // phase with taps, then a scatter into dx (GACER_DGRAD_DILATE=1: the
+  // zero-dilated form)
+  bool phased = false;
+  std::vector<DgPhaseGemm> phases;
 };
+
+int dgrad_tile_bn(int Cin, int M) {
+  return (Cin >= 256 && cdiv(M, BM) >= kSplitSms) ? 256 : (Cin >= 128 ? 128 : roundup(Cin, 16));
+}
 
 int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int stride, int pad_h, int pad_w,
                DgradGeom& g) {
@@ -2457,8 +2481,60 @@ int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.off_maps = take(3 * sizeof(CUtensorMap), 128);
   g.off_w = take(static_cast<size_t>(g.rows) * g.Kpad * 2, 256);
   g.off_dil = stride == 1 ? 0 : take(static_cast<size_t>(N) * g.Hdd * g.Wdd * Cout * 2, 256);
+  g.phased = false;
+  g.phases.clear();
+  if (stride > 1 && !env_flag("GACER_DGRAD_DILATE")) {
+    bool ok = true;
+    for (int a = 0; a < stride && ok; ++a)
+      for (int b = 0; b < stride && ok; ++b) {
+        DgPhaseGemm q;
+        q.a = a; q.b = b;
+        q.vh = dg_phase(a, KH, stride, pad_h, H);
+        q.vw = dg_phase(b, KW, stride, pad_w, W);
+        if (q.vh.K == 0 || q.vw.K == 0 || q.vh.n == 0 || q.vw.n == 0) { q.K = 0; g.phases.push_back(q); continue; }
+        if (q.vh.pad < 0 || q.vw.pad < 0) { ok = false; break; }
+        q.K = q.vh.K * q.vw.K * Cout;
+        q.Kpad = roundup(q.K, BK);
+        q.nkb = q.Kpad / BK;
+        q.M = N * q.vh.n * q.vw.n;
+        q.a_mode = (q.vh.K * q.vw.K == 1 && q.vh.pad == 0 && q.vw.pad == 0 && q.vh.n == g.Hd && q.vw.n == g.Wd)
+                       ? A_ROWS : A_IM2COL;
+        q.bn = dgrad_tile_bn(Cin, q.M);
+        q.tiles_m = cdiv(q.M, BM);
+        q.tiles_n = cdiv(Cin, q.bn);
+        q.rows = q.tiles_n * q.bn;
+        q.upper[0] = q.vh.n - g.Hd - q.vh.pad;   // output rows per image = Hd + upper - lower
+        q.upper[1] = q.vw.n - g.Wd - q.vw.pad;
+        g.phases.push_back(q);
+      }
+    if (ok) {
+      g.phased = true;
+      for (DgPhaseGemm& q : g.phases) {
+        if (q.K == 0) continue;
+        q.off_op = take(sizeof(OpDev), 256);
+        q.off_maps = take(3 * sizeof(CUtensorMap), 128);
+        q.off_w = take(static_cast<size_t>(q.rows) * q.Kpad * 2, 256);
+        q.off_out = take(static_cast<size_t>(q.M) * Cin * 2, 256);
+      }
+    } else {
+      g.phases.clear();
+    }
+  }
   g.bytes = o;
   return 0;
+}
+
+// The OpDev of one phase GEMM (a stride-1 forward conv of dy with the
+// phase's flipped sub-filter; dense output [N][n_a][n_b][Cin]).
+void dgrad_phase_opdev(OpDev& d, const DgPhaseGemm& q, int N, int Hd, int Wd, int Cin, int Cout) {
+  std::memset(&d, 0, sizeof d);
+  d.kind = DK_GEMM; d.act = ACT_NONE;
+  d.B = N; d.H = Hd; d.W = Wd; d.C = Cout; d.ldi = Cout;
+  d.Ho = q.vh.n; d.Wo = q.vw.n; d.Cout = Cin; d.ldo = Cin;
+  d.kh = q.vh.K; d.kw = q.vw.K; d.stride = 1; d.ph = q.vh.pad; d.pw = q.vw.pad; d.mrep = 1;
+  d.M = q.M; d.N = Cin; d.K = q.K; d.Kpad = q.Kpad;
+  d.tiles_m = q.tiles_m; d.tiles_n = q.tiles_n; d.bm = BM; d.bn = q.bn; d.split_k = 1; d.nkb = q.nkb;
+  d.ldw = q.Kpad; d.a_mode = q.a_mode;
 }
 }  // namespace
 
@@ -2488,6 +2564,52 @@ int32_t gacer_conv_dgrad(const void* dy_dev, const float* w_dev, int32_t N, int3
   void* wt = ws + g.off_w;
   const float *scale = nullptr, *bias = nullptr;
   const int nsb = g.rows + 8;
+  if (g.phased) {
+    // phase decomposition: per phase with taps a stride-1 GEMM of dy with the
+    // flipped sub-filter (dense output), then one scatter into dx
+    const void* outs[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (const DgPhaseGemm& q : g.phases) {
+      if (q.K == 0) continue;
+      void* qw = ws + q.off_w;
+      void* qo = ws + q.off_out;
+      outs[q.a * stride + q.b] = qo;
+      CUDA_TRY(launch_dgrad_phase_filter(w_dev, Cout, Cin, q.vh.K, q.vw.K, Cout, q.Kpad, q.rows, stride, q.a, q.b, KH,
+                                         KW, qw, st));
+      if (int rc0 = unit_vectors(q.rows + 8, &scale, &bias)) return rc0;
+      OpDev d;
+      dgrad_phase_opdev(d, q, N, g.Hd, g.Wd, Cin, Cout);
+      d.in = dy_dev; d.out = qo; d.wt = qw; d.scale = scale; d.bias = bias;
+      CUtensorMap maps[3];
+      std::memset(maps, 0, sizeof maps);
+      const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(ws + q.off_maps);
+      d.tmap_a = dmaps; d.tmap_b = dmaps + 1; d.tmap_c = dmaps + 2;
+      int rc = q.a_mode == A_IM2COL ? encode_im2col(&maps[0], d, Cout, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B, q.upper)
+                                    : encode_rows(&maps[0], dy_dev, q.K, q.M, Cout, BM);
+      if (!rc) rc = encode_rows(&maps[1], qw, q.Kpad, q.rows, q.Kpad, q.bn);
+      if (rc) return rc;
+      {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(q.M)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Cin) * 2};
+        const cuuint32_t box[2] = {64u, 32u};
+        const cuuint32_t es[2] = {1, 1};
+        CUresult r = g_encode_tiled(&maps[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qo, dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "conv_dgrad: phase output map (%d)", static_cast<int>(r));
+        d.c_tma = 1;
+      }
+      CUDA_TRY(cudaMemcpyAsync(ws + q.off_maps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(ws + q.off_op, &d, sizeof d, cudaMemcpyHostToDevice, st));
+      ExecParams base;
+      std::memset(&base, 0, sizeof base);
+      base.error = S.d_error;
+      base.watchdog_ns = 2000000000LL;
+      CUDA_TRY(launch_op(base, reinterpret_cast<const OpDev*>(ws + q.off_op), 0, DK_GEMM, q.tiles_m * q.tiles_n,
+                         S.num_sms, st));
+    }
+    CUDA_TRY(launch_phase_scatter(outs, N, H, W, Cin, stride, pad_h, pad_w, KH, KW, dx_dev, st));
+    return GACER_OK;
+  }
   CUDA_TRY(launch_dgrad_filter(w_dev, Cout, Cin, KH, KW, g.cread, g.Kpad, g.rows, wt, st));
   const void* src = dy_dev;
   if (stride > 1) {
@@ -3381,6 +3503,46 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
           // flipped, transposed filter
           DgradGeom dg;
           if (int rc = dgrad_geom(B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, dg)) return rc;
+          if (dg.phased) {
+            // phase decomposition (no zero-dilated dy, no S^2 zero work): per
+            // phase with taps the flipped sub-filter and a stride-1 GEMM of dy,
+            // then one scatter of the phases into dx
+            int pbuf[4] = {-1, -1, -1, -1};
+            for (const DgPhaseGemm& q : dg.phases) {
+              if (q.K == 0) continue;
+              const int qw = L.buf(static_cast<size_t>(q.rows) * q.Kpad * 2);
+              TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(q.rows) * q.Kpad));
+              f.vp[0] = pref(i, 0); f.vp[1] = bref(qw);
+              const int iv[14] = {o.c_out, x.c, q.vh.K, q.vw.K, o.c_out, q.Kpad, q.rows, 0, 0, o.stride, q.a, q.b,
+                                  o.kh, o.kw};
+              std::memcpy(f.va.i, iv, sizeof iv);
+              L.add(std::move(f), {T.buf_params}, {qw});
+              const int qo = L.buf(static_cast<size_t>(q.M) * x.c * 2);
+              pbuf[q.a * o.stride + q.b] = qo;
+              TrainOp m;
+              m.kind = DK_GEMM;
+              m.gemm_kind = 1;
+              dgrad_phase_opdev(m.gd, q, B, dg.Hd, dg.Wd, x.c, o.c_out);
+              m.g_in = bref(dy); m.g_out = bref(qo); m.g_wt = bref(qw);
+              m.g_scale = bref(buf_ones); m.g_bias = bref(buf_zeros);
+              m.im2col_c = o.c_out; m.a_ld = o.c_out; m.a_rows = q.M; m.b_rows = q.rows;
+              m.has_upper = q.a_mode == A_IM2COL;
+              m.im2col_upper[0] = q.upper[0]; m.im2col_upper[1] = q.upper[1];
+              m.flops = 2.0 * q.M * x.c * static_cast<double>(q.K);
+              L.add(std::move(m), {dy, qw, buf_ones, buf_zeros}, {qo});
+            }
+            const int dx = L.buf(xbytes);
+            TrainOp sc = TrainLowering::vg(VF_PHASE_SCATTER,
+                                           vg_grid_for(static_cast<int64_t>(B) * x.h * x.w * (x.c / 8)));
+            for (int k = 0; k < 4; ++k) sc.vp[k] = bref(pbuf[k]);
+            sc.vp[4] = bref(dx);
+            sc.va.n[0] = static_cast<int64_t>(B) * x.h * x.w * (x.c / 8);
+            const int sv[9] = {B, x.h, x.w, x.c, o.stride, o.pad_h, o.pad_w, o.kh, o.kw};
+            std::memcpy(sc.va.i, sv, sizeof sv);
+            L.add(std::move(sc), {pbuf[0], pbuf[1], pbuf[2], pbuf[3]}, {dx});
+            acc(pred, dx, xbytes);
+            break;
+          }
           const int wp = L.buf(static_cast<size_t>(dg.rows) * dg.Kpad * 2);
           TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(dg.rows) * dg.Kpad));
           f.vp[0] = pref(i, 0); f.vp[1] = bref(wp);
@@ -3488,7 +3650,9 @@ int build_train_opdev(const Tenant& T, int tenant_id, const TrainOp& op, OpDev& 
     if (!rc) rc = wgrad_mn_setup(d, maps, d.wt, d.in, d.B, d.H, d.W, d.C, d.M, d.kh, d.kw, d.stride, d.ph, d.pw, wg, true);
     if (rc) return rc;
   } else {
-    if (d.a_mode == A_IM2COL) rc = encode_im2col(&maps[0], d, op.im2col_c);
+    if (d.a_mode == A_IM2COL)
+      rc = encode_im2col(&maps[0], d, op.im2col_c, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B,
+                         op.has_upper ? op.im2col_upper : nullptr);
     else if (d.a_mode == A_IM2COL8) rc = encode_im2col(&maps[0], d, op.im2col_c, BM, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
     else if (d.a_mode == A_ROWS) rc = encode_rows(&maps[0], d.in, op.gemm_kind == 2 ? d.Kpad : d.K, op.a_rows, op.a_ld, BM);
     if (!rc && d.a_mode != A_IM2COL8) rc = encode_rows(&maps[1], d.wt, d.Kpad, op.b_rows, d.Kpad, d.bn);

@@ -683,12 +683,14 @@ VG_FN void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) 
 // a K-major bf16 GEMM B operand [rows][Kpad]: forward = 1: row co, column
 // (r*KW + s)*cread + ci = w[co][ci][r][s]; forward = 0 (data gradient): row
 // ci, column (r*KW + s)*cread + co = w[co][ci][KH-1-r][KW-1-s]; padding 0.
-// a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward, i8 block bn
+// a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward, i8 block bn,
+//    i9 phase stride S (dgrad sub-filter; 0: none), i10/i11 phase (a, b), i12/i13 the full KH, KW
 VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* w = static_cast<const float*>(a.p[0]);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
   const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], cread = a.i[4], Kpad = a.i[5], rows = a.i[6],
             forward = a.i[7], bbn = a.i[8];
+  const int phS = a.i[9], pa = a.i[10], pb = a.i[11], KHf = a.i[12], KWf = a.i[13];   // dgrad phase (phS > 0)
   VG_LOOP(i, static_cast<int64_t>(rows) * Kpad) {
     const int row = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
     // bbn > 0: the A_IM2COL8 block layout -- per (N-tile, K-block) a bn x 64
@@ -705,9 +707,43 @@ VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t
         v = w[((static_cast<int64_t>(row) * Cin + col) * KH + tap / KW) * KW + tap % KW];
     } else if (row < Cin && tap < KH * KW && col < Cout) {
       const int r = tap / KW, s = tap % KW;
-      v = w[((static_cast<int64_t>(col) * Cin + row) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
+      if (phS > 0)   // the phase (pa, pb) sub-filter of a strided conv, flipped: tap (r, s) = full tap
+                     // (pa + S (KH - 1 - r), pb + S (KW - 1 - s)) of the KHf x KWf filter
+        v = w[((static_cast<int64_t>(col) * Cin + row) * KHf + (pa + phS * (KH - 1 - r))) * KWf +
+              (pb + phS * (KW - 1 - s))];
+      else
+        v = w[((static_cast<int64_t>(col) * Cin + row) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
     }
     out[dst] = __float2bfloat16_rn(v);
+  }
+}
+
+// Phase-decomposed data gradient of a stride-S conv: dx pixel (h, w) of phase
+// (a, b) = ((h + ph) mod S, (w + pw) mod S) is element (u - u0_a, v - v0_b)
+// of that phase's stride-1 dgrad conv output P_ab [N][n_a][n_b][C] (DgPhase),
+// u = (h + ph - a) / S; a phase no tap reaches is 0.  16-byte groups.
+// a: p0..p3 P_ab (index a * S + b; null = no taps); n0 total groups; i0 N, i1 H, i2 W, i3 C, i4 S,
+//    i5 ph, i6 pw, i7 KH, i8 KW, p4 dx
+VG_FN void vg_phase_scatter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], S = a.i[4], ph = a.i[5], pw = a.i[6], KH = a.i[7],
+            KW = a.i[8];
+  uint4* dx = static_cast<uint4*>(const_cast<void*>(a.p[4]));
+  const int G8 = C / 8;
+  (void)N;
+  VG_LOOP(i, a.n[0]) {
+    const int g = static_cast<int>(i % G8);
+    const int64_t pix = i / G8;
+    const int w = static_cast<int>(pix % W), h = static_cast<int>((pix / W) % H);
+    const int64_t n = pix / (static_cast<int64_t>(W) * H);
+    const int pa = (h + ph) % S, pb = (w + pw) % S;
+    const uint4* src = static_cast<const uint4*>(a.p[pa * S + pb]);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (src) {
+      const DgPhase da = dg_phase(pa, KH, S, ph, H), db = dg_phase(pb, KW, S, pw, W);
+      const int u = (h + ph - pa) / S - da.u0, q = (w + pw - pb) / S - db.u0;
+      v = src[((n * da.n + u) * db.n + q) * G8 + g];
+    }
+    dx[i] = v;
   }
 }
 
@@ -1129,6 +1165,7 @@ __device__ inline void run_vgrid(int fn, const VArgs& a, int vb, int nvb, int ti
     case VF_SGD: vg_sgd(a, vb, nvb, tid, nthr, smem); break;
     case VF_FILTER: vg_filter(a, vb, nvb, tid, nthr, smem); break;
     case VF_DILATE: vg_dilate(a, vb, nvb, tid, nthr, smem); break;
+    case VF_PHASE_SCATTER: vg_phase_scatter(a, vb, nvb, tid, nthr, smem); break;
     case VF_TRANSPOSE_IM2COL: vg_transpose_im2col(a, vb, nvb, tid, nthr, smem); break;
     case VF_WGRAD_PERMUTE: vg_wgrad_permute(a, vb, nvb, tid, nthr, smem); break;
     case VF_WGRAD_REDUCE: vg_wgrad_reduce(a, vb, nvb, tid, nthr, smem); break;

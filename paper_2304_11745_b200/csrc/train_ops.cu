@@ -83,6 +83,25 @@ cudaError_t launch_fwd_filter(const float* w, int Cout, int Cin, int KH, int KW,
   return vlaunch(VF_FILTER, a, vg_grid_for(static_cast<int64_t>(rows) * Kpad), s);
 }
 
+cudaError_t launch_dgrad_phase_filter(const float* w, int Cout, int Cin, int KI, int KJ, int cread, int Kpad, int rows,
+                                      int S, int pa, int pb, int KH, int KW, void* out, cudaStream_t s) {
+  VArgs a = vargs();
+  a.p[0] = w; a.p[1] = out;
+  a.i[0] = Cout; a.i[1] = Cin; a.i[2] = KI; a.i[3] = KJ; a.i[4] = cread; a.i[5] = Kpad; a.i[6] = rows; a.i[7] = 0;
+  a.i[9] = S; a.i[10] = pa; a.i[11] = pb; a.i[12] = KH; a.i[13] = KW;
+  return vlaunch(VF_FILTER, a, vg_grid_for(static_cast<int64_t>(rows) * Kpad), s);
+}
+
+cudaError_t launch_phase_scatter(const void* const* phase_out, int N, int H, int W, int C, int S, int ph, int pw,
+                                 int KH, int KW, void* dx, cudaStream_t s) {
+  VArgs a = vargs();
+  for (int i = 0; i < S * S && i < 4; ++i) a.p[i] = phase_out[i];
+  a.p[4] = dx;
+  a.n[0] = static_cast<int64_t>(N) * H * W * (C / 8);
+  a.i[0] = N; a.i[1] = H; a.i[2] = W; a.i[3] = C; a.i[4] = S; a.i[5] = ph; a.i[6] = pw; a.i[7] = KH; a.i[8] = KW;
+  return vlaunch(VF_PHASE_SCATTER, a, vg_grid_for(a.n[0]), s);
+}
+
 cudaError_t launch_dilate(const void* dy, int N, int Hd, int Wd, int C, int S, int Hdd, int Wdd, void* out,
                           cudaStream_t s) {
   VArgs a = vargs();
