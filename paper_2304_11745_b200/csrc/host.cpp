@@ -2483,7 +2483,14 @@ int dgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
   g.off_dil = stride == 1 ? 0 : take(static_cast<size_t>(N) * g.Hdd * g.Wdd * Cout * 2, 256);
   g.phased = false;
   g.phases.clear();
-  if (stride > 1 && !env_flag("GACER_DGRAD_DILATE")) {
+  // phases when the filter is no larger than the stride (1x1 / 2x2 at s2:
+  // the dilated form would spend 3/4 of its MMA work on zeros and the phases
+  // are few, dense GEMMs); larger filters keep the dilated form by default --
+  // measured standalone at R50 B=64: 1x1 s2 phases 0.18 vs dilated 0.33 ms,
+  // 3x3 s2 phases 0.17-0.22 vs dilated 0.12-0.18 ms (four small launches)
+  // GACER_DGRAD_PHASES=1 / GACER_DGRAD_DILATE=1 force either form.
+  const bool want_phases = env_flag("GACER_DGRAD_PHASES") || (KH <= stride && KW <= stride);
+  if (stride > 1 && want_phases && !env_flag("GACER_DGRAD_DILATE")) {
     bool ok = true;
     for (int a = 0; a < stride && ok; ++a)
       for (int b = 0; b < stride && ok; ++b) {
