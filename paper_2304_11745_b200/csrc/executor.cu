@@ -598,9 +598,12 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       // after the (<= 16 KB, bn <= 128) B block
       // A_MN: only the 64-column B boxes inside the GEMM's N (columns past it
       // are never stored, their smem is left as is)
-      const int nbq = a_mode == A_MN ? min(op.bn, op.N - n0 + 63) / 64 : 0;
+      // A_MN8: one 1 KB box per tap (8 GEMM columns) inside the GEMM's N
+      const int nbq = a_mode == A_MN ? min(op.bn, op.N - n0 + 63) / 64
+                                     : (a_mode == A_MN8 ? min(op.bn, op.N - n0 + 7) / 8 : 0);
       const uint32_t tx = a_mode == A_MN ? A_STAGE_BYTES + static_cast<uint32_t>(nbq) * 8192u
-                                         : A_STAGE_BYTES * mrep + bbytes;
+                          : a_mode == A_MN8 ? A_STAGE_BYTES + static_cast<uint32_t>(nbq) * 1024u
+                                            : A_STAGE_BYTES * mrep + bbytes;
       // first K-block of this item whose stage (g + i) % NPROD belongs to producer pj
       const int i0 = (pj - static_cast<int>(g % NPROD) + NPROD) % NPROD;
 #pragma unroll 1
@@ -637,19 +640,22 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
           continue;
         }
 #endif
-        if (a_mode == A_MN) {
+        if (a_mode == A_MN || a_mode == A_MN8) {
           // K-block = output pixels [k, k + 64): A = dy rows (two 64-channel
-          // boxes), B = one im2col box per 64 GEMM columns (tap, c0)
+          // boxes), B = one im2col box per 64 GEMM columns (tap, c0) -- or,
+          // 8 channels (A_MN8), one 8-column box per tap
           tma_load_2d(a_dst, tmap_a, bar, m0, k);
           tma_load_2d(a_dst + 8192, tmap_a, bar, m0 + 64, k);
           const int HoWo = op.Ho * op.Wo;
           const int img = k / HoWo, rem = k - img * HoWo;
           const int ho = rem / op.Wo, wo = rem - ho * op.Wo;
           const int wi = wo * op.stride - op.pw, hi = ho * op.stride - op.ph;
+          const int qw = a_mode == A_MN ? 64 : 8;
+          const uint32_t qb = a_mode == A_MN ? 8192u : 1024u;
           for (int q = 0; q < nbq; ++q) {
-            const int n = n0 + q * 64;
+            const int n = n0 + q * qw;
             const int tap = n / C, c0 = n - tap * C;
-            tma_load_im2col_4d(b_dst + q * 8192, tmap_b, bar, c0, wi, hi, img, static_cast<uint16_t>(tap % kw),
+            tma_load_im2col_4d(b_dst + q * qb, tmap_b, bar, c0, wi, hi, img, static_cast<uint16_t>(tap % kw),
                                static_cast<uint16_t>(tap / kw));
           }
           kdbg(p, 1, gi);
@@ -1560,7 +1566,8 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
     if (acc >= 2) mbar_wait(&ctl->tempty[abuf], ((acc / 2) + 1) & 1);
     tc_fence_after();
     const uint32_t d = cx.tmem + abuf * BN_MAX;
-    const bool mn = op.a_mode == A_MN;    // both operands MN-major (weight gradient)
+    const bool mn = op.a_mode == A_MN || op.a_mode == A_MN8;   // both operands MN-major (weight gradient)
+    const bool mn8 = op.a_mode == A_MN8;
     const bool i8 = op.a_mode == A_IM2COL8;   // no-swizzle core-matrix layout (8-channel stems)
     const uint32_t idesc = make_idesc(op.bn) | (mn ? ((1u << 15) | (1u << 16)) : 0u);
     const int mrep = op.mrep;
@@ -1580,7 +1587,12 @@ __device__ void mma_role(const ExecParams& p, Ctx& cx) {
       const uint32_t a_base = ring_base + stage * A_STAGE_BYTES;
       const uint32_t b_base = ring_base + STAGES * A_STAGE_BYTES + stage * B_STAGE_BYTES;
       if (!(GACER_DIAG && p.dbg && (p.dbg_spin & 1))) {  // diagnostics: odd dbg_spin skips the MMAs
-        if (mn) {
+        if (mn8) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(d, make_sdesc_mn(a_base + kk * 2048), make_sdesc_none(b_base + kk * 256, 128, 1024), idesc,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+        } else if (mn) {
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
             umma_bf16(d, make_sdesc_mn(a_base + kk * 2048), make_sdesc_mn(b_base + kk * 2048), idesc,

@@ -141,7 +141,10 @@ constexpr int WIN_SMEM_BYTES = WIN_IN_BYTES + (9 + 2) * 64 * 4 + 1024;  // + dw 
 // 16 B per core matrix, SBO 128 B, the next tap LBO 2 KB), B = the weights
 // pre-packed in the same layout per (N-tile, K-block) and fetched with one
 // bulk copy.  Replaces the cp.async gather for stems (7x7 s2, 11x11 s4, 3x3).
-enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2, A_MN = 3, A_IM2COL8 = 4 };
+// A_MN8: A_MN for an 8-channel input (the stem's weight gradient): B = one
+// im2col box of 64 pixels x 8 channels per tap, in the no-swizzle MN-major
+// core-matrix layout (K rows 16 B apart, LBO 128 B, the next tap SBO 1 KB).
+enum AMode : int32_t { A_GATHER = 0, A_IM2COL = 1, A_ROWS = 2, A_MN = 3, A_IM2COL8 = 4, A_MN8 = 5 };
 
 struct OpDev {
   int32_t kind;            // DevKind

@@ -2723,11 +2723,11 @@ int wgrad_geom(int N, int H, int W, int Cin, int Cout, int KH, int KW, int strid
 // GEMM fields of d that differ from the staged (A_ROWS) form and encodes the
 // two tensor maps: dy [Mpix][Cout] as 64 x 64 boxes, x as an im2col view with
 // 64-pixel columns.
-bool wgrad_mn_ok(int Cin, int Cout) { return Cin % 64 == 0 && Cout % 8 == 0; }
+bool wgrad_mn_ok(int Cin, int Cout) { return (Cin % 64 == 0 || Cin == 8) && Cout % 8 == 0; }
 
 int wgrad_mn_setup(OpDev& d, CUtensorMap* maps, const void* x, const void* dy, int N, int H, int W, int Cin, int Cout,
                    int KH, int KW, int stride, int pad_h, int pad_w, const WgradGeom& g, bool encode) {
-  d.a_mode = A_MN;
+  d.a_mode = Cin == 8 ? A_MN8 : A_MN;
   d.in = dy;
   d.wt = x;
   d.B = N; d.H = H; d.W = W; d.C = Cin; d.ldi = Cin;
@@ -2744,6 +2744,7 @@ int wgrad_mn_setup(OpDev& d, CUtensorMap* maps, const void* x, const void* dy, i
   if (r != CUDA_SUCCESS) return set_err(GACER_E_CUDA, "wgrad: dy tensor map (%d)", static_cast<int>(r));
   OpDev v = d;          // the im2col view of x (the forward conv's geometry, 64-pixel columns)
   v.in = x;
+  if (Cin == 8) return encode_im2col(&maps[1], v, Cin, BK, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
   return encode_im2col(&maps[1], v, Cin, BK);
 }
 }  // namespace
@@ -3651,7 +3652,7 @@ int build_train_opdev(const Tenant& T, int tenant_id, const TrainOp& op, OpDev& 
   d.c_tma = 0;
   if (!encode || !d.in || !d.wt) return 0;
   int rc = 0;
-  if (d.a_mode == A_MN) {
+  if (d.a_mode == A_MN || d.a_mode == A_MN8) {
     WgradGeom wg;
     rc = wgrad_geom(d.B, d.H, d.W, d.C, d.M, d.kh, d.kw, d.stride, d.ph, d.pw, wg);
     if (!rc) rc = wgrad_mn_setup(d, maps, d.wt, d.in, d.B, d.H, d.W, d.C, d.M, d.kh, d.kw, d.stride, d.ph, d.pw, wg, true);

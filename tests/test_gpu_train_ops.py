@@ -245,7 +245,8 @@ def workloads_bf16(a):
 
 
 @pytest.mark.parametrize("N,H,W,Cin,Cout,k,s,p", [(4, 14, 14, 64, 64, 3, 1, 1), (2, 15, 13, 64, 72, 3, 2, 1),
-                                                   (2, 7, 7, 512, 2048, 1, 1, 0)])
+                                                   (2, 7, 7, 512, 2048, 1, 1, 0),
+                                                   (2, 32, 32, 8, 64, 7, 2, 3), (3, 30, 34, 8, 64, 7, 2, 3)])
 def test_conv_wgrad_mn_major_matches_staged(T, N, H, W, Cin, Cout, k, s, p, monkeypatch):
     """The weight gradient read in place with MN-major UMMA operands (A = dy,
     B = the im2col TMA view of x; no staged transposes) computes the same
