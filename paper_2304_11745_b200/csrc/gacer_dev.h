@@ -27,6 +27,19 @@ enum VFn : int32_t {
   VF_MAXPOOL_FWD, VF_MAXPOOL_ARGMAX, VF_MAXPOOL_BWD, VF_GAP_FWD, VF_GAP_BWD,
   VF_LINEAR_FWD, VF_LINEAR_DX, VF_LINEAR_DW, VF_SOFTMAX_CE, VF_MEAN, VF_SGD,
   VF_FILTER, VF_DILATE, VF_TRANSPOSE_IM2COL, VF_WGRAD_PERMUTE, VF_WGRAD_REDUCE, VF_PHASE_SCATTER,
+  VF_FILTER_ALL,
+};
+
+// One filter-packing job of the training tenant's step (VF_FILTER_ALL packs
+// every conv's forward and data-gradient GEMM operand in one operator):
+// the vg_filter arguments with resolved pointers; `start` = the job's first
+// element in the concatenated output index space.
+struct FilterJob {
+  const float* w;
+  void* out;
+  int64_t start;
+  int32_t i[14];        // vg_filter's i0..i13
+  int32_t pad[2];
 };
 
 // Phase decomposition of a strided conv's data gradient (stride S): input

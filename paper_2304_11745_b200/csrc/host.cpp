@@ -189,6 +189,11 @@ struct Tenant {
   std::vector<float> h_params;       // initial master parameters (uploaded once)
   int buf_params = -1, buf_grads = -1, buf_mom = -1, buf_loss = -1;
   bool grad_gate = false;            // A12: the SGD op waits for the gradient all-reduce gate
+  // the step's filter packing as one operator (VF_FILTER_ALL): its jobs with
+  // unresolved buffers, the op index and the device job table's buffer
+  struct FJob { TRef w, out; int32_t i[14]; int64_t n; };
+  std::vector<FJob> fjobs;
+  int fall_op = -1, fall_table = -1;
   std::map<std::pair<int, int>, std::pair<int64_t, int64_t>> param_slice;  // (orig op, which) -> (offset, count)
   const void* labels_dev = nullptr;
   float lr = 0.1f, momentum = 0.9f;
@@ -2991,6 +2996,40 @@ struct TrainLowering {
   std::vector<int> grad_writers;              // ops writing (disjoint) slices of the flat gradients
   int step = 1;
 
+  // A filter-packing job: appended to the step's single VF_FILTER_ALL op
+  // (created at the first job, issued before every GEMM that reads a packed
+  // operand); `out` becomes written by that op.
+  void filter_job(TRef w, int out, const int32_t (&iv)[14]) {
+    if (T.fall_op < 0) {
+      TrainOp fa = vg(VF_FILTER_ALL, 1);
+      T.fall_op = add(std::move(fa), {T.buf_params}, {});
+    }
+    Tenant::FJob j;
+    j.w = w;
+    j.out.buf = out;
+    std::memcpy(j.i, iv, sizeof iv);
+    j.n = static_cast<int64_t>(iv[6]) * iv[5];
+    T.fjobs.push_back(j);
+    writer_of(out) = T.fall_op;
+    readers_of(out).clear();
+  }
+  // size the filter op's grid and job table once every job is known
+  void finish_filters() {
+    if (T.fall_op < 0) return;
+    int64_t total = 0;
+    for (const Tenant::FJob& j : T.fjobs) total += j.n;
+    T.fall_table = buf(T.fjobs.size() * sizeof(FilterJob));
+    TrainOp& fa = T.tops[T.fall_op];
+    fa.vblocks = vg_grid_for(total);
+    fa.va.n[0] = total;
+    fa.va.i[0] = static_cast<int32_t>(T.fjobs.size());
+    fa.vp[0].buf = T.fall_table;
+    fa.bytes = static_cast<double>(total) * 6.0;
+    const int grid = S.opts.num_ctas > 0 ? S.opts.num_ctas : (S.num_sms > 0 ? S.num_sms : kSplitSms);
+    fa.per = std::max(1, cdiv(fa.vblocks, grid));
+    fa.items = cdiv(fa.vblocks, fa.per);
+  }
+
   explicit TrainLowering(Tenant& t, int b) : T(t), B(b) {}
 
   int buf(size_t bytes) {
@@ -3207,12 +3246,12 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         FwdGeom fg;
         if (int rc = fwd_geom(B, x.h, x.w, x.c, o.c_out, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, fg)) return rc;
         const int wp = L.buf(static_cast<size_t>(fg.rows) * fg.Kpad * 2);
-        TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(fg.rows) * fg.Kpad));
-        f.vp[0] = pref(i, 0); f.vp[1] = bref(wp);
-        f.va.i[0] = o.c_out; f.va.i[1] = x.c; f.va.i[2] = o.kh; f.va.i[3] = o.kw; f.va.i[4] = fg.cread;
-        f.va.i[5] = fg.Kpad; f.va.i[6] = fg.rows; f.va.i[7] = 1;
-        f.va.i[8] = fg.a_mode == A_IM2COL8 ? fg.bn : 0;   // block layout of the 8-channel TMA path
-        L.add(std::move(f), {T.buf_params}, {wp});
+        {
+          const int32_t iv[14] = {o.c_out, x.c, o.kh, o.kw, fg.cread, fg.Kpad, fg.rows, 1,
+                                  fg.a_mode == A_IM2COL8 ? fg.bn : 0,   // block layout of the 8-channel TMA path
+                                  0, 0, 0, 0, 0};
+          L.filter_job(pref(i, 0), wp, iv);
+        }
         const int yb = L.buf(static_cast<size_t>(B) * y.h * y.w * y.c * 2);
         TrainOp m;
         m.kind = DK_GEMM;
@@ -3519,12 +3558,9 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
             for (const DgPhaseGemm& q : dg.phases) {
               if (q.K == 0) continue;
               const int qw = L.buf(static_cast<size_t>(q.rows) * q.Kpad * 2);
-              TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(q.rows) * q.Kpad));
-              f.vp[0] = pref(i, 0); f.vp[1] = bref(qw);
-              const int iv[14] = {o.c_out, x.c, q.vh.K, q.vw.K, o.c_out, q.Kpad, q.rows, 0, 0, o.stride, q.a, q.b,
-                                  o.kh, o.kw};
-              std::memcpy(f.va.i, iv, sizeof iv);
-              L.add(std::move(f), {T.buf_params}, {qw});
+              const int32_t iv[14] = {o.c_out, x.c, q.vh.K, q.vw.K, o.c_out, q.Kpad, q.rows, 0, 0, o.stride, q.a,
+                                      q.b, o.kh, o.kw};
+              L.filter_job(pref(i, 0), qw, iv);
               const int qo = L.buf(static_cast<size_t>(q.M) * x.c * 2);
               pbuf[q.a * o.stride + q.b] = qo;
               TrainOp m;
@@ -3552,11 +3588,10 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
             break;
           }
           const int wp = L.buf(static_cast<size_t>(dg.rows) * dg.Kpad * 2);
-          TrainOp f = TrainLowering::vg(VF_FILTER, vg_grid_for(static_cast<int64_t>(dg.rows) * dg.Kpad));
-          f.vp[0] = pref(i, 0); f.vp[1] = bref(wp);
-          f.va.i[0] = o.c_out; f.va.i[1] = x.c; f.va.i[2] = o.kh; f.va.i[3] = o.kw; f.va.i[4] = dg.cread;
-          f.va.i[5] = dg.Kpad; f.va.i[6] = dg.rows; f.va.i[7] = 0;
-          L.add(std::move(f), {T.buf_params}, {wp});
+          {
+            const int32_t iv[14] = {o.c_out, x.c, o.kh, o.kw, dg.cread, dg.Kpad, dg.rows, 0, 0, 0, 0, 0, 0, 0};
+            L.filter_job(pref(i, 0), wp, iv);
+          }
           int src = dy;
           if (o.stride > 1) {
             src = L.buf(static_cast<size_t>(B) * dg.Hdd * dg.Wdd * o.c_out * 2);
@@ -3599,6 +3634,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
     a.bytes = 5.0 * 4.0 * static_cast<double>(np);   // read w, g, buf; write w, buf
     L.add(std::move(a), {T.buf_params, T.buf_grads, T.buf_mom}, {T.buf_params, T.buf_mom});
   }
+  L.finish_filters();
   T.flops = 0;
   for (const TrainOp& o : T.tops) T.flops += o.flops;
   return 0;
@@ -3684,6 +3720,19 @@ int upload_train_tenant(Tenant& T) {
   for (size_t b = 0; b < T.tbufs.size(); ++b) {
     CUDA_TRY(cudaMalloc(&T.tbufs[b], T.tbuf_bytes[b]));
     CUDA_TRY(cudaMemset(T.tbufs[b], 0, T.tbuf_bytes[b]));   // zero: padding rows, momentum, gradients
+  }
+  if (T.fall_table >= 0) {   // the filter op's job table with resolved pointers
+    std::vector<FilterJob> jt(T.fjobs.size());
+    int64_t start = 0;
+    for (size_t k = 0; k < T.fjobs.size(); ++k) {
+      std::memset(&jt[k], 0, sizeof jt[k]);
+      jt[k].w = static_cast<const float*>(tref_addr(T, T.fjobs[k].w));
+      jt[k].out = tref_addr(T, T.fjobs[k].out);
+      jt[k].start = start;
+      std::memcpy(jt[k].i, T.fjobs[k].i, sizeof jt[k].i);
+      start += T.fjobs[k].n;
+    }
+    CUDA_TRY(cudaMemcpy(T.tbufs[T.fall_table], jt.data(), jt.size() * sizeof(FilterJob), cudaMemcpyHostToDevice));
   }
   CUDA_TRY(cudaMemcpy(T.tbufs[T.buf_params], T.h_params.data(), T.h_params.size() * 4, cudaMemcpyHostToDevice));
   const auto ones = T.param_slice.at({-1, 0});

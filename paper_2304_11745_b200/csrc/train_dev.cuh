@@ -685,13 +685,12 @@ VG_FN void vg_sgd(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) 
 // ci, column (r*KW + s)*cread + co = w[co][ci][KH-1-r][KW-1-s]; padding 0.
 // a: p0 w, p1 out; i0 Cout, i1 Cin, i2 KH, i3 KW, i4 cread, i5 Kpad, i6 rows, i7 forward, i8 block bn,
 //    i9 phase stride S (dgrad sub-filter; 0: none), i10/i11 phase (a, b), i12/i13 the full KH, KW
-VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
-  const float* w = static_cast<const float*>(a.p[0]);
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
-  const int Cout = a.i[0], Cin = a.i[1], KH = a.i[2], KW = a.i[3], cread = a.i[4], Kpad = a.i[5], rows = a.i[6],
-            forward = a.i[7], bbn = a.i[8];
-  const int phS = a.i[9], pa = a.i[10], pb = a.i[11], KHf = a.i[12], KWf = a.i[13];   // dgrad phase (phS > 0)
-  VG_LOOP(i, static_cast<int64_t>(rows) * Kpad) {
+// One packed element i of a filter job (the body of vg_filter / vg_filter_all).
+__device__ __forceinline__ void filter_elem(const float* w, __nv_bfloat16* out, const int32_t* ai, int64_t i) {
+  const int Cout = ai[0], Cin = ai[1], KH = ai[2], KW = ai[3], cread = ai[4], Kpad = ai[5], forward = ai[7],
+            bbn = ai[8];
+  const int phS = ai[9], pa = ai[10], pb = ai[11], KHf = ai[12], KWf = ai[13];   // dgrad phase (phS > 0)
+  {
     const int row = static_cast<int>(i / Kpad), k = static_cast<int>(i % Kpad);
     // bbn > 0: the A_IM2COL8 block layout -- per (N-tile, K-block) a bn x 64
     // block in the no-swizzle core-matrix layout (same bijection as the
@@ -715,6 +714,51 @@ VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t
         v = w[((static_cast<int64_t>(col) * Cin + row) * KH + (KH - 1 - r)) * KW + (KW - 1 - s)];
     }
     out[dst] = __float2bfloat16_rn(v);
+  }
+}
+
+VG_FN void vg_filter(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const float* w = static_cast<const float*>(a.p[0]);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(const_cast<void*>(a.p[1]));
+  VG_LOOP(i, static_cast<int64_t>(a.i[6]) * a.i[5]) filter_elem(w, out, a.i, i);
+}
+
+// Every filter job of the step in one operator (one grid over the jobs'
+// concatenated outputs; the job of an element by binary search on `start`):
+// the same packed values as one vg_filter per conv, without ~100 per-conv
+// operators.  a: p0 FilterJob[n], i0 n, n0 total elements
+VG_FN void vg_filter_all(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
+  const FilterJob* jobs = static_cast<const FilterJob*>(a.p[0]);
+  const int n = a.i[0];
+  const int64_t total = a.n[0];
+  // block vb: a contiguous element range, threads strided by nthr; a thread
+  // finds its first job by binary search, then walks the jobs forward
+  const int64_t per = (total + nvb - 1) / nvb;
+  const int64_t e0 = vb * per + tid, e1 = (vb + 1) * per < total ? (vb + 1) * per : total;
+  if (e0 >= e1) return;
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].start <= e0) lo = mid; else hi = mid - 1;
+  }
+  int j = lo;
+  int64_t jstart = jobs[j].start, jnext = j + 1 < n ? jobs[j + 1].start : total;
+  const float* w = jobs[j].w;
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(jobs[j].out);
+  int32_t iv[14];
+#pragma unroll
+  for (int q = 0; q < 14; ++q) iv[q] = jobs[j].i[q];
+  for (int64_t e = e0; e < e1; e += nthr) {
+    while (e >= jnext) {
+      ++j;
+      jstart = jobs[j].start;
+      jnext = j + 1 < n ? jobs[j + 1].start : total;
+      w = jobs[j].w;
+      out = static_cast<__nv_bfloat16*>(jobs[j].out);
+#pragma unroll
+      for (int q = 0; q < 14; ++q) iv[q] = jobs[j].i[q];
+    }
+    filter_elem(w, out, iv, e - jstart);
   }
 }
 
@@ -1164,6 +1208,7 @@ __device__ inline void run_vgrid(int fn, const VArgs& a, int vb, int nvb, int ti
     case VF_MEAN: vg_mean(a, vb, nvb, tid, nthr, smem); break;
     case VF_SGD: vg_sgd(a, vb, nvb, tid, nthr, smem); break;
     case VF_FILTER: vg_filter(a, vb, nvb, tid, nthr, smem); break;
+    case VF_FILTER_ALL: vg_filter_all(a, vb, nvb, tid, nthr, smem); break;
     case VF_DILATE: vg_dilate(a, vb, nvb, tid, nthr, smem); break;
     case VF_PHASE_SCATTER: vg_phase_scatter(a, vb, nvb, tid, nthr, smem); break;
     case VF_TRANSPOSE_IM2COL: vg_transpose_im2col(a, vb, nvb, tid, nthr, smem); break;

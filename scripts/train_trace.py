@@ -26,7 +26,7 @@ desc = {int(o): G.gacer_describe_op(int(o)) for o in np.unique(tr[:, 1])}
 s.close()
 VF = ["none", "bn_partial", "bn_finalize", "bn_apply", "relu_bwd", "add", "maxpool_fwd", "maxpool_argmax",
       "maxpool_bwd", "gap_fwd", "gap_bwd", "linear_fwd", "linear_dx", "linear_dw", "softmax_ce", "mean", "sgd",
-      "filter", "dilate", "transpose_im2col", "wgrad_permute", "wgrad_reduce", "phase_scatter"]
+      "filter", "dilate", "transpose_im2col", "wgrad_permute", "wgrad_reduce", "phase_scatter", "filter_all"]
 t0 = tr[:, 6].min()
 print(f"{name} B={B} {hw}^2 train step alone: {st['last_round_ms']:.2f} ms, items {len(tr)}")
 # per op: span (first claim .. last release), sum of item durations (SM-us)
