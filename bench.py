@@ -78,7 +78,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)   # the timed region is ~0.2 s: sample densely
 
     def __enter__(self):
         if self.ok:
@@ -194,6 +194,41 @@ def cpu_oracle_sample(ts, budget_s=30.0):
     dt_s = time.perf_counter() - t0
     desc = f"1 image of each of {n} tenant(s) of the mix (fp64 oracle, OpenMP)"
     return n / dt_s, oops.num_threads(), desc, dt_s
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_oracle_single_thread(cfg, tenant="mobilenet_v2"):
+    """The OMP_NUM_THREADS=1 arm of the oracle baseline (a subprocess: the
+    OpenMP team size is fixed at library load): one image of one tenant of
+    the mix (the smallest: the whole arm stays within seconds)."""
+    import subprocess
+    code = (
+        "import sys, time; sys.path.insert(0, %r)\n"
+        "import bench, workloads\n"
+        "from oracle import forward_graph\n"
+        "from oracle import ops as oops\n"
+        "ts = [t for t in bench.make_workload(%r) if t[0] == %r]\n"
+        "_, g, p, B, dt, x = ts[0]\n"
+        "t0 = time.perf_counter(); forward_graph(g, p, x[:1]); s = time.perf_counter() - t0\n"
+        "print(1.0 / s, oops.num_threads())\n" % (ROOT, cfg, tenant))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                             timeout=300).stdout.split()
+        return {"value": float(out[0]), "unit": UNIT, "cores": int(out[1]),
+                "sample": f"1 image of {tenant} (fp64 oracle, OMP_NUM_THREADS=1)"}
+    except Exception as e:   # a baseline detail, never a reason to fail the bench
+        return {"unavailable": str(e)[:200]}
 
 
 # ------------------------------------------------------------------ main arms
@@ -422,7 +457,8 @@ def run_gacer(args, rank, world, dist):
         if world == 1 and not args.no_cpu_baseline:
             v, cores, desc, secs = cpu_oracle_sample(ts, budget_s=30.0)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                    "sample": desc}
+                                    "sample": desc, "cpu_model": cpu_model(),
+                                    "single_thread": cpu_oracle_single_thread(args.config)}
         print(json.dumps(line), flush=True)
     sess.close()
 
@@ -604,7 +640,7 @@ def run_d4(args, rank, world, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gacer", choices=["gacer", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -240,7 +240,11 @@ typedef struct {
   int32_t n_steps;            /* training: 2 n_orig_ops + 1 step positions (pointer range) */
   int64_t n_params;           /* training: floats in the flat parameter buffer */
   int32_t op_base;            /* global executor index of the tenant's first operator */
-  int32_t pad_info;
+  int32_t reused_tensors;     /* activation tensors placed in an earlier tensor's buffer
+                                 (liveness-based reuse: set GACER_REUSE=1
+                                 before registration; off by default) */
+  int64_t act_bytes;          /* device bytes of the tenant's activation buffers */
+  int64_t act_bytes_private;  /* ... if every activation tensor had its own buffer */
 } gacer_tenant_info;
 
 /* Device buffers of a training tenant (library-owned; valid until

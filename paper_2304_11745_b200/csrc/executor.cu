@@ -292,6 +292,25 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// L2 evict-first policy: for operands read exactly once per round (the
+// swap-AB linear weights -- VGG-16's FC1 alone streams 205 MB through L2,
+// which would otherwise evict the other tenants' L2-resident activations)
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* tmap, uint64_t* bar, int c, int w,
                                                    int h, int n, uint16_t ow, uint16_t oh) {
   asm volatile(
@@ -376,6 +395,14 @@ constexpr int STAGE_WARP_BYTES = 32 * 128;           // epilogue staging: 32 row
 constexpr bool EPI_STAGED = NEPI == 128;
 #ifndef GACER_PROD_SPLIT
 #define GACER_PROD_SPLIT 1
+#endif
+#ifndef GACER_WPREFETCH
+#define GACER_WPREFETCH 0  // L2 prefetch of the next GEMM ops' weights on an op's first tile
+                           // (measured: D2 1.814 -> 1.906 ms -- the bulk prefetches occupy the
+                           //  SM's TMA unit ahead of its own operand loads; not adopted)
+#endif
+#ifndef GACER_L2_HINTS
+#define GACER_L2_HINTS 1   // evict-first L2 policy on read-once weight streams (swap-AB linear)
 #endif
 #ifndef GACER_EPI_DB
 #define GACER_EPI_DB 1
@@ -574,6 +601,9 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
       const int a_mode = op.a_mode, C = op.C, kw = op.kw;
       const void* tmap_a = op.tmap_a;
       const void* tmap_b = op.tmap_b;
+      // swap-AB linear: A = the weights, each element read by one item only
+      const bool stream_a = op.swap == 2 && a_mode == A_ROWS && GACER_L2_HINTS;
+      const uint64_t pol_ef = stream_a ? l2_policy_evict_first() : 0ull;
       fence_proxy_async_global();   // acquired producer data -> this thread's TMA reads
       // im2col start (top-left input tap) of each 128-row half of the tile
       // (scalars, not arrays: a dynamically indexed array lives in local
@@ -670,6 +700,8 @@ __device__ void produce_gemm(const OpDev& op, const Item& it, Ctx& cx, uint32_t&
           if (mrep > 1)
             tma_load_im2col_4d(b_dst + A2_OFF, tmap_a, bar, c0, w0b, h0b, img0b, static_cast<uint16_t>(sx),
                                static_cast<uint16_t>(r));
+        } else if (stream_a) {
+          tma_load_2d_hint(a_dst, tmap_a, bar, k, m0, pol_ef);
         } else {
           tma_load_2d(a_dst, tmap_a, bar, k, m0);
           if (mrep > 1) tma_load_2d(b_dst + A2_OFF, tmap_a, bar, k, m0 + BM);
@@ -1473,6 +1505,21 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
       ++islot;
     }
     if (claimed < 0) break;
+#if GACER_WPREFETCH
+    // the op's first tile (exactly one per op in every plan): pull the next
+    // GEMM ops' weights into L2 while this op runs (after the hand-off, so
+    // the claimed item is not delayed)
+    if (p.single_op < 0 && itm.mt == 0 && itm.nt == 0 && itm.ks == 0) {
+      const OpDev& op = p.ops[itm.op];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t bytes = op.pf_bytes[j];
+        const char* src = static_cast<const char*>(op.pf_ptr[j]);
+        for (uint32_t off = 0; off < bytes; off += 262144u)
+          l2_prefetch(src + off, min(262144u, bytes - off));
+      }
+    }
+#endif
   }
 }
 

@@ -138,7 +138,10 @@ constexpr int CC_TASKS_PER_THREAD = 4;
 constexpr int MAX_SPLIT = 4;      // split-K factor cap of forward layers (fixed per layer shape)
 constexpr int MAX_SPLIT_LONG = 64; // cap for the long pixel reductions of weight gradients
 constexpr int LOOKAHEAD = 3;      // max claimed items not yet picked up by every role (per CTA)
-constexpr int INLINE_DEPS = 4;    // dependencies stored inside the Item
+#ifndef GACER_INLINE_DEPS
+#define GACER_INLINE_DEPS 4
+#endif
+constexpr int INLINE_DEPS = GACER_INLINE_DEPS;    // dependencies stored inside the Item
 constexpr int MAX_SMEM_SEGS = 256;
 constexpr int WIN_IN_BYTES = 96 * 1024;   // window_smem: staged input rows of one image segment
 constexpr int WIN_SMEM_BYTES = WIN_IN_BYTES + (9 + 2) * 64 * 4 + 1024;  // + dw weights/scale/bias (kh*kw <= 9)
@@ -165,7 +168,7 @@ struct OpDev {
   int32_t act;             // Act
   int32_t out_f32;         // output dtype: 1 = float32, 0 = bf16 (or f32 for fp32 tenants: see elem)
   int32_t f32;             // 1 = fp32 tenant (inputs/weights fp32), 0 = bf16
-  int32_t swap;            // GEMM: 1 = swap-AB linear (A = weights, B = activations)
+  int32_t swap;            // GEMM: 1 = swap-AB linear (A = weights, B = activations); 2 = same, A loaded L2 evict-first
   int32_t cip;             // avgpool count_include_pad
   int32_t has_skip;        // 1: + skip (same shape); 2: * skip[n][c] (channel scale, DK_ELTWISE)
 
@@ -207,6 +210,11 @@ struct OpDev {
   // [mt * bm, min((mt + 1) * bm, vblocks))
   int32_t vfn, vblocks;
   VArgs va;
+  // L2 prefetch on this op's first item (tile 0, 0, 0): the packed weights of
+  // the tenant's next GEMM ops (a chain op's first weight tiles otherwise
+  // come from DRAM on its critical path).  bytes 0 = none.
+  const void* pf_ptr[2];
+  uint32_t pf_bytes[2];
 };
 
 // One work item: one output tile (mt, nt) of one op, K-slice ks.  Items are

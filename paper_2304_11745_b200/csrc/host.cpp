@@ -112,6 +112,10 @@ struct Tensor {
   int producer_orig = -1;  // original op producing it (-1 = input)
   std::vector<int> writers;  // fused ops writing (a slice of) it
   bool sliced = false;     // storage is a slice of a concat tensor
+  // liveness-based buffer reuse: the tensors that occupied this tensor's
+  // buffer before it, most recent first (the plan compiler adds
+  // write-after-read dependencies on their readers, tile by tile)
+  std::vector<int> war_prev;
 };
 
 struct FusedOp {
@@ -137,6 +141,7 @@ struct FusedOp {
   std::vector<float> scale, bias;
   // device
   void* d_w = nullptr;
+  size_t w_bytes = 0;    // bytes of the packed device weights
   float* d_scale = nullptr;
   float* d_bias = nullptr;
   float* d_partial = nullptr;
@@ -336,6 +341,73 @@ int act_of(int kind) {
 }
 
 // ------------------------------------------------------------------------
+// Liveness-based reuse of activation buffers (a round wrote
+// every activation to its own buffer, 685 MB of DRAM write-back per D2
+// round).  In issue order, a tensor whose buffer holds only itself (no
+// concat slices; one writer; not the graph input or output) takes over the
+// buffer of an earlier tensor whose last reader is at least GACER_REUSE_DIST
+// (default 2) fused ops before its writer: best fit among the free buffers
+// large enough, else the largest free one, grown.  The tenant's footprint
+// then stays near its live set, which L2 can hold.  Correctness does not
+// rest on the issue order: the plan compiler gives every tile of the new
+// writer write-after-read dependencies on the reader tiles of the previous
+// occupants that touch its bytes (compile_plan, war_deps).
+void reuse_buffers(Tenant& T) {
+  const int nt = static_cast<int>(T.tensors.size());
+  const int nb = static_cast<int>(T.bufs.size());
+  int dist = 2;
+  if (const char* e = getenv("GACER_REUSE_DIST")) dist = std::max(1, atoi(e));
+  // only tensors of at least min_bytes take part (the small tensors of the
+  // late, latency-bound layers would gain no DRAM traffic and pay the
+  // write-after-read dependency checks)
+  size_t min_bytes = 0;
+  if (const char* e = getenv("GACER_REUSE_MIN_KB")) min_bytes = static_cast<size_t>(std::max(0, atoi(e))) * 1024u;
+  std::vector<int> holders(nb, 0);
+  for (int t = 1; t < nt; ++t)
+    if (T.tensors[t].buf >= 0) ++holders[T.tensors[t].buf];
+  std::vector<int> last_read(nt, -1);
+  for (size_t f = 0; f < T.fops.size(); ++f)
+    for (int tin : {T.fops[f].in_t, T.fops[f].skip_t})
+      if (tin > 0) last_read[tin] = std::max(last_read[tin], static_cast<int>(f));
+  std::vector<std::pair<int, int>> cand;   // (writer, tensor)
+  for (int t = 1; t < nt; ++t) {
+    const Tensor& X = T.tensors[t];
+    if (X.buf < 0 || X.sliced || holders[X.buf] != 1 || X.writers.size() != 1 || T.buf_bytes[X.buf] < std::max<size_t>(1, min_bytes))
+      continue;
+    cand.push_back({X.writers[0], t});
+  }
+  std::sort(cand.begin(), cand.end());
+  struct Slot { int buf; size_t bytes; int last; std::vector<int> occ; };
+  std::vector<Slot> slots;
+  for (const auto& wt : cand) {
+    const int w = wt.first, t = wt.second;
+    Tensor& X = T.tensors[t];
+    const size_t need = T.buf_bytes[X.buf];
+    const int last = std::max(w, last_read[t]);
+    int best = -1;
+    for (int s = 0; s < static_cast<int>(slots.size()); ++s) {
+      if (slots[s].last > w - dist) continue;
+      if (best < 0) { best = s; continue; }
+      const Slot& a = slots[s];
+      const Slot& b = slots[best];
+      const bool af = a.bytes >= need, bf = b.bytes >= need;
+      if (af != bf ? af : (af ? a.bytes < b.bytes : a.bytes > b.bytes)) best = s;
+    }
+    if (best < 0) {
+      slots.push_back({X.buf, need, last, {t}});
+      continue;
+    }
+    Slot& sl = slots[best];
+    T.buf_bytes[X.buf] = 0;   // its own buffer is never allocated
+    X.buf = sl.buf;
+    X.war_prev.assign(sl.occ.rbegin(), sl.occ.rend());
+    sl.occ.push_back(t);
+    sl.bytes = std::max(sl.bytes, need);
+    sl.last = last;
+  }
+  for (const Slot& sl : slots) T.buf_bytes[sl.buf] = sl.bytes;
+}
+
 int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
   const int n = g->n_ops;
   if (n <= 0 || !g->ops) return set_err(GACER_E_INVALID_ARG, "graph has no ops");
@@ -703,6 +775,10 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
     if (X.buf >= 0 && !X.sliced)
       T.buf_bytes[X.buf] = std::max(T.buf_bytes[X.buf], static_cast<size_t>(batch) * X.H * X.W * X.ldc * elem);
   }
+  // (off by default: on D2 it cuts DRAM writes 657 -> 533 MB per round but
+  //  the write-after-read dependencies cost 1.7-2 % of the makespan, same-box
+  //  A/B; GACER_REUSE=1 enables it)
+  if (env_flag("GACER_REUSE")) reuse_buffers(T);
 
   // ---- per fused op geometry + packing
   T.flops = 0;
@@ -941,6 +1017,7 @@ int upload_tenant(Tenant& T) {
     if (T.buf_bytes[b]) CUDA_TRY(cudaMalloc(&T.bufs[b], T.buf_bytes[b]));
   for (FusedOp& F : T.fops) {
     if (!F.w_bf16.empty()) {
+      F.w_bytes = F.w_bf16.size() * 2;
       CUDA_TRY(cudaMalloc(&F.d_w, F.w_bf16.size() * 2));
       CUDA_TRY(cudaMemcpy(F.d_w, F.w_bf16.data(), F.w_bf16.size() * 2, cudaMemcpyHostToDevice));
     } else if (!F.w_f32.empty()) {
@@ -984,7 +1061,9 @@ OpDev make_opdev(const Tenant& T, int tenant_id, const FusedOp& F) {
   d.act = F.act;
   d.out_f32 = (Y.buf == -2 || f32) ? 1 : 0;
   d.f32 = f32 ? 1 : 0;
-  d.swap = F.swap ? 1 : 0;
+  // 2: swap-AB whose A operand (the weights, read once per round) is loaded
+  // with an L2 evict-first policy (GACER_NO_L2_HINT=1: plain loads)
+  d.swap = F.swap ? (env_flag("GACER_NO_L2_HINT") ? 1 : 2) : 0;
   d.cip = F.cip ? 1 : 0;
   d.has_skip = F.skip_t >= 0 ? (F.mul ? 2 : 1) : 0;
   d.affine = F.affine ? 1 : 0;
@@ -1093,6 +1172,25 @@ int rebuild_op_table() {
       fops.push_back(&F);
       tops.push_back({-1, nullptr});
     }
+    // weight prefetch targets: the next two tcgen05 GEMM ops of the tenant in
+    // issue order whose packed weights are small enough to sit in L2 ahead of
+    // use (<= 8 MB; not the swap-AB linears, which stream their weights)
+    if (!env_flag("GACER_NO_WPREFETCH")) {
+      const int nf = static_cast<int>(T.fops.size());
+      for (int f = 0; f < nf; ++f) {
+        OpDev& d = S.h_ops[T.op_base + f];
+        int k = 0;
+        for (int g2 = f + 1; g2 < nf && k < 2; ++g2) {
+          const FusedOp& G2 = T.fops[g2];
+          if (G2.kind != DK_GEMM || G2.swap || !G2.d_w) continue;
+          const size_t bytes = G2.w_bytes;
+          if (bytes == 0 || bytes > (8u << 20)) continue;
+          d.pf_ptr[k] = G2.d_w;
+          d.pf_bytes[k] = static_cast<uint32_t>(bytes & ~static_cast<size_t>(15));
+          ++k;
+        }
+      }
+    }
     for (const TrainOp& op : T.tops) {
       OpDev d;
       if (int rc = build_train_opdev(T, static_cast<int>(t), op, d, nullptr, false)) return rc;
@@ -1192,6 +1290,55 @@ int cluster_of_orig(const Plan& P, int t, int orig0) {  // orig0: 0-based op ind
   int k = 0;
   for (int c : P.cuts[t]) if (c < orig0 + 1) ++k;  // cut p = boundary after op p
   return k;
+}
+
+// Input rows a tile of fused op F reads from tensor tin, as a flattened row
+// range [lo, hi]: pixels (b*H + h)*W + w, or samples for [B][C] tensors.
+void tile_read_rows(const Tenant& T, const FusedOp& F, int mt, int ntile, int tin, long long& lo, long long& hi) {
+  long long s_lo, s_hi;   // samples
+  long long px_lo = -1, px_hi = -1;  // input pixels of in_t (-1: whole samples)
+  if (F.rows_are_pixels) {
+    const long long R = (F.kind == DK_GAP) ? 1 : static_cast<long long>(F.Ho) * F.Wo;
+    const long long r0 = static_cast<long long>(mt) * F.bm;
+    const long long r1 = std::min<long long>(F.M, r0 + F.bm);
+    s_lo = r0 / R;
+    s_hi = (r1 - 1) / R;
+    if (F.kind != DK_GAP) {
+      const long long HW = static_cast<long long>(F.H) * F.W;
+      const long long ho0 = (r0 % R) / F.Wo, ho1 = ((r1 - 1) % R) / F.Wo;
+      const long long h_lo = std::max<long long>(0, ho0 * F.stride - F.ph);
+      const long long h_hi = std::min<long long>(F.H - 1, ho1 * F.stride - F.ph + F.kh - 1);
+      px_lo = s_lo * HW + h_lo * F.W;
+      px_hi = s_hi * HW + h_hi * F.W + F.W - 1;
+    }
+  } else {
+    s_lo = static_cast<long long>(ntile) * F.bn;
+    s_hi = std::min<long long>(T.batch, static_cast<long long>(ntile + 1) * F.bn) - 1;
+  }
+  const Tensor& X = T.tensors[tin];
+  const long long XHW = static_cast<long long>(X.H) * X.W;
+  lo = s_lo * XHW;
+  hi = (s_hi + 1) * XHW - 1;
+  if (tin == F.skip_t && F.mul) {
+    // channel scale [B][C]: the samples of the tile's rows (lo, hi as set)
+  } else if (tin == F.skip_t && F.rows_are_pixels && F.kind != DK_GAP) {
+    lo = static_cast<long long>(mt) * F.bm;   // residual: same pixels as the output
+    hi = std::min<long long>(F.M, lo + F.bm) - 1;
+  } else if (px_lo >= 0 && tin == F.in_t) {
+    lo = px_lo;
+    hi = px_hi;
+  }
+}
+
+// Output rows [lo, hi] (flattened, as above) a tile of fused op F writes.
+void tile_write_rows(const Tenant& T, const FusedOp& F, int mt, int ntile, long long& lo, long long& hi) {
+  if (F.rows_are_pixels) {
+    lo = static_cast<long long>(mt) * F.bm;
+    hi = std::min<long long>(F.M, lo + F.bm) - 1;
+  } else {
+    lo = static_cast<long long>(ntile) * F.bn;
+    hi = std::min<long long>(T.batch, lo + F.bn) - 1;
+  }
 }
 
 int compile_plan(Plan& P) {
@@ -1382,6 +1529,104 @@ int compile_plan(Plan& P) {
     P.auto_share[t] = std::min(1.0, work_ns / std::max(1.0, chain_ns));
   }
 
+  // Write-after-read dependencies of reused activation buffers
+  // (reuse_buffers): a tile writing bytes [a, b) of its output buffer waits
+  // for every reader tile of the buffer's previous occupants that reads
+  // those bytes (and, for bytes no reader touches, for the occupant's writer
+  // tiles).  Older occupants matter only past the sizes of the more recent
+  // ones: a more recent occupant's writer tiles waited for them already.
+  std::vector<std::vector<int>> cdeps(P.n_chunk_counters);   // counter -> deps of its items
+  struct WarEnt { long long lo, hi; Dep d; };
+  struct WarSet { std::vector<WarEnt> rd, wr; long long span_rd = 0, span_wr = 0; };
+  std::map<std::pair<int, int>, WarSet> war_cache;
+  auto tile_dep = [&](int t, int f, const ChunkRange& q, int m) -> Dep {
+    (void)t; (void)f;
+    return q.mc.empty() ? Dep{q.counter, q.n_items} : Dep{q.mc[m - q.m0], q.mc_items};
+  };
+  auto war_set = [&](int t, int x) -> const WarSet& {
+    auto it = war_cache.find({t, x});
+    if (it != war_cache.end()) return it->second;
+    WarSet& ws = war_cache[{t, x}];
+    const Tenant& T = S.tenants[t];
+    for (size_t f = 0; f < T.fops.size(); ++f) {
+      const FusedOp& FR = T.fops[f];
+      const bool reads = FR.in_t == x || FR.skip_t == x;
+      const bool writes = FR.out_t == x;
+      if (!reads && !writes) continue;
+      for (const ChunkRange& q : cr[t][f]) {
+        if (!q.n_items) continue;
+        for (int m = q.m0; m < q.m1; ++m)
+          for (int n = q.n0; n < q.n1; ++n) {
+            const Dep d = tile_dep(t, static_cast<int>(f), q, m);
+            for (int tin : {FR.in_t, FR.skip_t}) {
+              if (tin != x) continue;
+              long long lo, hi;
+              tile_read_rows(T, FR, m, n, tin, lo, hi);
+              ws.rd.push_back({lo, hi, d});
+              ws.span_rd = std::max(ws.span_rd, hi - lo);
+            }
+            if (writes) {
+              long long lo, hi;
+              tile_write_rows(T, FR, m, n, lo, hi);
+              ws.wr.push_back({lo, hi, d});
+              ws.span_wr = std::max(ws.span_wr, hi - lo);
+            }
+          }
+      }
+    }
+    auto by_lo = [](const WarEnt& u, const WarEnt& v) { return u.lo < v.lo; };
+    std::stable_sort(ws.rd.begin(), ws.rd.end(), by_lo);
+    std::stable_sort(ws.wr.begin(), ws.wr.end(), by_lo);
+    return ws;
+  };
+  auto war_deps = [&](int t, const FusedOp& F, int mt, int ntile, const std::set<int>& dset, std::vector<Dep>& wl) {
+    const Tenant& T = S.tenants[t];
+    const Tensor& Y = T.tensors[F.out_t];
+    if (Y.war_prev.empty()) return;
+    const long long e = static_cast<long long>(elem_size(T));
+    long long wlo, whi;
+    tile_write_rows(T, F, mt, ntile, wlo, whi);
+    const long long a = wlo * Y.ldc * e, b = (whi + 1) * Y.ldc * e;   // bytes [a, b)
+    long long covered_to = 0;
+    for (int x : Y.war_prev) {
+      const Tensor& X = T.tensors[x];
+      const long long xrow = static_cast<long long>(X.ldc) * e;
+      const long long xb = static_cast<long long>(T.batch) * X.H * X.W * xrow;
+      const long long lo_b = std::max(a, covered_to), hi_b = std::min(b, xb);
+      if (lo_b < hi_b) {
+        const long long r_lo = lo_b / xrow, r_hi = (hi_b - 1) / xrow;
+        const WarSet& ws = war_set(t, x);
+        auto add = [&](const Dep& d) { if (!dset.count(d.counter)) wl.push_back(d); };
+        // reader tiles overlapping rows [r_lo, r_hi]; the rows they cover
+        std::vector<std::pair<long long, long long>> cov;
+        auto first = std::lower_bound(ws.rd.begin(), ws.rd.end(), WarEnt{r_lo - ws.span_rd, 0, {}},
+                                      [](const WarEnt& u, const WarEnt& v) { return u.lo < v.lo; });
+        for (auto itr = first; itr != ws.rd.end() && itr->lo <= r_hi; ++itr) {
+          if (itr->hi < r_lo) continue;
+          add(itr->d);
+          cov.push_back({std::max(itr->lo, r_lo), std::min(itr->hi, r_hi)});
+        }
+        // rows no reader tile reads: the occupant's writer tiles there
+        std::sort(cov.begin(), cov.end());
+        std::vector<std::pair<long long, long long>> gaps;
+        long long next = r_lo;
+        for (const auto& c : cov) {
+          if (c.first > next) gaps.push_back({next, c.first - 1});
+          next = std::max(next, c.second + 1);
+        }
+        if (next <= r_hi) gaps.push_back({next, r_hi});
+        for (const auto& gp : gaps) {
+          auto fw = std::lower_bound(ws.wr.begin(), ws.wr.end(), WarEnt{gp.first - ws.span_wr, 0, {}},
+                                     [](const WarEnt& u, const WarEnt& v) { return u.lo < v.lo; });
+          for (auto itr = fw; itr != ws.wr.end() && itr->lo <= gp.second; ++itr)
+            if (itr->hi >= gp.first) add(itr->d);
+        }
+      }
+      covered_to = std::max(covered_to, xb);
+      if (covered_to >= b) break;
+    }
+  };
+
   // items, grouped by (tenant, cluster) segment, in issue order
   std::vector<std::vector<std::vector<int32_t>>> seg_items(nt, std::vector<std::vector<int32_t>>(P.n_clusters));
   for (int t = 0; t < nt; ++t) {
@@ -1434,46 +1679,15 @@ int compile_plan(Plan& P) {
         uint32_t jchunk = 0;   // position of the next item within its chunk (queue order)
         for (int mt = r.m0; mt < r.m1; ++mt)
           for (int ntile = r.n0; ntile < r.n1; ++ntile) {
-            // input rows this tile reads, as a flattened row range of each
-            // input tensor: pixels (b*H + h)*W + w, or samples for [B][C] rows
-            long long s_lo, s_hi;   // samples
-            long long px_lo = -1, px_hi = -1;  // input pixels of in_t (-1: whole samples)
-            if (F.rows_are_pixels) {
-              const long long R = (F.kind == DK_GAP) ? 1 : static_cast<long long>(F.Ho) * F.Wo;
-              const long long r0 = static_cast<long long>(mt) * F.bm;
-              const long long r1 = std::min<long long>(F.M, r0 + F.bm);
-              s_lo = r0 / R;
-              s_hi = (r1 - 1) / R;
-              if (F.kind != DK_GAP) {
-                const long long HW = static_cast<long long>(F.H) * F.W;
-                const long long ho0 = (r0 % R) / F.Wo, ho1 = ((r1 - 1) % R) / F.Wo;
-                const long long h_lo = std::max<long long>(0, ho0 * F.stride - F.ph);
-                const long long h_hi = std::min<long long>(F.H - 1, ho1 * F.stride - F.ph + F.kh - 1);
-                px_lo = s_lo * HW + h_lo * F.W;
-                px_hi = s_hi * HW + h_hi * F.W + F.W - 1;
-              }
-            } else {
-              s_lo = static_cast<long long>(ntile) * F.bn;
-              s_hi = std::min<long long>(T.batch, static_cast<long long>(ntile + 1) * F.bn) - 1;
-            }
             std::set<int> dset;
             std::vector<Dep> dl;
+            std::vector<int> full_extra;   // WAR deps pruned as implied (still implied by this item)
             if (F.in_t == 0) dl.push_back({P.input_counter0 + t, 1u});   // input gate (epoch-valued)
             for (int tin : {F.in_t, F.skip_t}) {
               if (tin < 0 || tin == 0) continue;
-              const Tensor& X = T.tensors[tin];
-              const long long XHW = static_cast<long long>(X.H) * X.W;
-              // flattened row range [lo, hi] of tensor tin this tile reads
-              long long lo = s_lo * XHW, hi = (s_hi + 1) * XHW - 1;
-              if (tin == F.skip_t && F.mul) {
-                // channel scale [B][C]: the samples of the tile's rows (lo, hi as set)
-              } else if (tin == F.skip_t && F.rows_are_pixels && F.kind != DK_GAP) {
-                lo = static_cast<long long>(mt) * F.bm;   // residual: same pixels as the output
-                hi = std::min<long long>(F.M, lo + F.bm) - 1;
-              } else if (px_lo >= 0) {
-                lo = px_lo;
-                hi = px_hi;
-              }
+              const long long XHW = static_cast<long long>(T.tensors[tin].H) * T.tensors[tin].W;
+              long long lo, hi;
+              tile_read_rows(T, F, mt, ntile, tin, lo, hi);
               for (int w : T.tensors[tin].writers) {
                 const FusedOp& Wf = T.fops[w];
                 int wm0 = 0, wm1 = Wf.tiles_m, wn0 = 0, wn1 = Wf.tiles_n;
@@ -1499,6 +1713,29 @@ int compile_plan(Plan& P) {
                 }
               }
             }
+            {
+              std::vector<Dep> wl;
+              war_deps(t, F, mt, ntile, dset, wl);
+              if (!wl.empty()) {
+                // drop write-after-read deps already implied by the RAW deps
+                // (completion of a counter implies completion of every dep of
+                // its items: closure over cdeps, a few levels deep)
+                std::set<int> cl(dset.begin(), dset.end());
+                std::vector<int> frontier(dset.begin(), dset.end());
+                for (int depth = 0; depth < 2 && !frontier.empty() && cl.size() < 256; ++depth) {
+                  std::vector<int> nxt;
+                  for (int c : frontier)
+                    if (c >= 0 && c < static_cast<int>(cdeps.size()))
+                      for (int c2 : cdeps[c])
+                        if (cl.insert(c2).second) nxt.push_back(c2);
+                  frontier.swap(nxt);
+                }
+                for (const Dep& d : wl) {
+                  full_extra.push_back(d.counter);
+                  if (!cl.count(d.counter) && dset.insert(d.counter).second) dl.push_back(d);
+                }
+              }
+            }
             int dep_begin = 0;
             if (dl.size() > static_cast<size_t>(INLINE_DEPS)) {
               dep_begin = static_cast<int>(P.deps.size());
@@ -1514,6 +1751,13 @@ int compile_plan(Plan& P) {
               if (dl.size() <= static_cast<size_t>(INLINE_DEPS))
                 for (size_t d = 0; d < dl.size(); ++d) { it.dc[d] = dl[d].counter; it.dt[d] = dl[d].target; }
               it.chunk = r.mc.empty() ? r.counter : r.mc[mt - r.m0];
+              if (ks == 0) {
+                std::vector<int>& cd = cdeps[it.chunk];
+                for (const Dep& d : dl) cd.push_back(d.counter);
+                cd.insert(cd.end(), full_extra.begin(), full_extra.end());
+                std::sort(cd.begin(), cd.end());
+                cd.erase(std::unique(cd.begin(), cd.end()), cd.end());
+              }
               it.bud = -1;
               if (r.bud >= 0) {   // every item of the chunk counts; item j >= budget waits
                 it.bud = r.bud;
@@ -1553,6 +1797,19 @@ int compile_plan(Plan& P) {
       }
     }
   P.items = std::move(ordered);
+  if (env_flag("GACER_DEP_STATS")) {   // diagnostics: dependency-list lengths per tenant
+    for (int t = 0; t < nt; ++t) {
+      long long n = 0, tot = 0, over = 0;
+      int mx = 0;
+      for (const Item& it : P.items) {
+        if (it.op < S.tenants[t].op_base || it.op >= S.tenants[t].op_base + static_cast<int>(S.tenants[t].fops.size()))
+          continue;
+        ++n; tot += it.dep_count; over += it.dep_count > INLINE_DEPS; mx = std::max(mx, it.dep_count);
+      }
+      fprintf(stderr, "[gacer] tenant %d: %lld items, mean deps %.2f, max %d, over inline %lld\n", t, n,
+              n ? static_cast<double>(tot) / n : 0.0, mx, over);
+    }
+  }
   return 0;
 }
 
@@ -1937,7 +2194,15 @@ int gacer_get_tenant_info(int tenant, gacer_tenant_info* out) {
   out->n_steps = T.n_steps;
   out->n_params = T.train ? static_cast<int64_t>(T.tbuf_bytes[T.buf_params] / 4) : 0;
   out->op_base = T.op_base;
-  out->pad_info = 0;
+  out->reused_tensors = 0;
+  out->act_bytes = out->act_bytes_private = 0;
+  for (size_t b = 0; b < T.buf_bytes.size(); ++b) out->act_bytes += static_cast<int64_t>(T.buf_bytes[b]);
+  for (size_t t = 1; t < T.tensors.size(); ++t) {
+    const Tensor& X = T.tensors[t];
+    out->reused_tensors += X.war_prev.empty() ? 0 : 1;
+    if (X.buf >= 0 && !X.sliced)
+      out->act_bytes_private += static_cast<int64_t>(T.batch) * X.H * X.W * X.ldc * static_cast<int64_t>(elem_size(T));
+  }
   for (const TrainOp& op : T.tops) {
     if (op.kind != DK_GEMM) { ++out->cc_ops; continue; }
     ++out->gemm_ops;

@@ -92,7 +92,8 @@ class gacer_tenant_info(C.Structure):
                 ("flops", C.c_double), ("gemm_ops", C.c_int32), ("mpair_ops", C.c_int32),
                 ("split_k_ops", C.c_int32), ("swap_ops", C.c_int32), ("wide_ops", C.c_int32),
                 ("cc_ops", C.c_int32), ("train", C.c_int32), ("n_steps", C.c_int32), ("n_params", C.c_int64),
-                ("op_base", C.c_int32), ("pad_info", C.c_int32)]
+                ("op_base", C.c_int32), ("reused_tensors", C.c_int32),
+                ("act_bytes", C.c_int64), ("act_bytes_private", C.c_int64)]
 
 
 class gacer_train_state(C.Structure):

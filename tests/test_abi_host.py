@@ -253,3 +253,30 @@ def test_next2_models_lower(host):
     assert 1 + 14 + 15 + 8 * 4 + 15 + 4 + 29 == 110
     # conv0 + maxpool + 58 dense layers x 3 + 3 transitions x 3 + BN/ReLU, GAP, FC
     assert 2 + 58 * 3 + 3 * 3 + 3 == 188
+
+
+def test_buffer_reuse_footprint(host, monkeypatch):
+    """Liveness-based activation-buffer reuse: the D2
+    tenants' activation footprint drops to roughly their live set (ResNet-50
+    B=8: < 1/3 of one buffer per tensor), every reusing tensor records its
+    predecessors for the write-after-read dependencies, concat slices and
+    the graph input/output never take part, and without GACER_REUSE=1 (the
+    default) every tensor keeps its own buffer."""
+    monkeypatch.setenv("GACER_REUSE", "1")
+    for name, frac in (("resnet50", 0.34), ("vgg16", 0.5), ("mobilenet_v2", 0.34), ("densenet121", 0.34)):
+        info = G.gacer_get_tenant_info(register(workloads.build_model(name), 8))
+        assert info["reused_tensors"] > 0, name
+        assert info["act_bytes"] <= frac * info["act_bytes_private"], (name, info)
+    monkeypatch.setenv("GACER_REUSE", "0")
+    info = G.gacer_get_tenant_info(register(workloads.build_model("resnet50"), 8))
+    assert info["reused_tensors"] == 0 and info["act_bytes"] == info["act_bytes_private"]
+    # a chain of equal tensors: with distance 2, three buffers suffice
+    monkeypatch.setenv("GACER_REUSE", "1")
+    g = workloads.Graph("chain", 64, 32, 32)
+    x = 0
+    for _ in range(8):
+        x = g.relu(g.bn(g.conv(x, 64, 64, 3, 1, 1), 64))
+    g.linear(g.flatten(g.gap(x)), 64, 10)
+    info = G.gacer_get_tenant_info(register(g, 2))
+    one = 2 * 32 * 32 * 64 * 2
+    assert info["act_bytes"] == 3 * one, info   # (the small GAP output fits a freed buffer)

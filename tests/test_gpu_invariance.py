@@ -289,3 +289,23 @@ def test_bitwise_next2_mix(cuda_ok):
         out, _ = run(ts, **v)
         for t, (a, b) in enumerate(zip(ref, out)):
             assert a.tobytes() == b.tobytes(), (t, {kk: v[kk] for kk in v if kk != "plan"})
+
+
+def test_buffer_reuse_is_invisible(cuda_ok, d2, monkeypatch):
+    """Liveness-based activation-buffer reuse (host.cpp reuse_buffers) with
+    tile-level write-after-read dependencies: outputs byte-identical to
+    private buffers, also with the most aggressive reuse distance (1: a
+    buffer is taken over right after its last reader's issue slot, so the
+    WAR dependencies bind) under a strict partition, few CTAs, and random
+    plans with pointers."""
+    monkeypatch.setenv("GACER_REUSE", "0")
+    ref, _ = run(d2)
+    monkeypatch.setenv("GACER_REUSE", "1")
+    rng = np.random.default_rng(99)
+    variants = [dict(), dict(plan=random_plan(d2, rng, 2))]
+    monkeypatch.setenv("GACER_REUSE_DIST", "1")
+    variants += [dict(), dict(partition="strict", num_ctas=37), dict(plan=random_plan(d2, rng, 3), num_ctas=64)]
+    for v in variants:
+        out, _ = run(d2, **v)
+        for t, (a, b) in enumerate(zip(ref, out)):
+            assert a.tobytes() == b.tobytes(), (t, {k: v[k] for k in v if k != "plan"})
