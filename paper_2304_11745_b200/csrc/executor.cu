@@ -1150,11 +1150,8 @@ __device__ void cc_item(const OpDev& op, const Item& it, int tid, float* red) {
   const int mb = it.mt * op.bm + tid / G;
   if (c >= op.Cout) return;
   // (bf16 window ops normally run as staged items, window_smem)
-  for (int j = 0; j < CC_TASKS_PER_THREAD; ++j) {
-    const int m = mb + j * pstep;
-    if (m >= op.M) break;
-    cc_pixel<F32>(op, m, c, HoWo);
-  }
+  const int m_end = min(op.M, (it.mt + 1) * op.bm);   // bm: a multiple of pstep (host)
+  for (int m = mb; m < m_end; m += pstep) cc_pixel<F32>(op, m, c, HoWo);
 }
 
 // Eltwise ops of the NEXT-2 tenants, out of line (own register allocation):
@@ -1172,9 +1169,8 @@ __device__ __noinline__ void cc_item_ext(const OpDev& op, const Item& it, int ti
   float sc[8], bi[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) { sc[q] = op.affine ? op.scale[c + q] : 1.0f; bi[q] = op.affine ? op.bias[c + q] : 0.0f; }
-  for (int j = 0; j < CC_TASKS_PER_THREAD; ++j) {
-    const int m = mb + j * pstep;
-    if (m >= op.M) break;
+  const int m_end = min(op.M, (it.mt + 1) * op.bm);   // bm: a multiple of pstep (host)
+  for (int m = mb; m < m_end; m += pstep) {
     float y[8], s[8];
     if (op.f32) load8<true>(op.in, static_cast<size_t>(m) * op.ldi + c, y);
     else load8<false>(op.in, static_cast<size_t>(m) * op.ldi + c, y);

@@ -869,8 +869,13 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           //  would grow from 7 to 49 K-blocks)
           // (the cp.async gather fills both 128-row halves too, so a small-Cin
           //  layer keeps its short 8-channel K stride)
+          static const int mpair_per_sm = [] {   // pair items per SM required (A/B knob)
+            const char* e = getenv("GACER_MPAIR_PER_SM");
+            return e ? std::max(1, atoi(e)) : 2;
+          }();
           if (!F.swap && F.a_mode != A_IM2COL8 && F.Cout <= 128 && F.Cin <= 64 &&
-              cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= 2 * kSplitSms && !env_flag("GACER_NO_MPAIR"))
+              cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= mpair_per_sm * kSplitSms &&
+              !env_flag("GACER_NO_MPAIR"))
             F.mrep = 2;
           // 1x1 stride-1 conv over a dense NHWC tensor is a plain GEMM: tiled TMA rows
           if (!F.swap && F.kh * F.kw == 1 && F.stride == 1 && o.pad_h == 0 && o.pad_w == 0 && c64 == c8 &&
@@ -964,10 +969,29 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
       F.bn = std::min(64, pow2ceil(roundup(F.Cout, 8)));
       const int G = F.bn / 8;
       F.bm = (F.kind == DK_GAP) ? std::min(B, 64) : CC_TASKS_PER_THREAD * (CC_THREADS / G);
+      if (F.kind != DK_GAP) {
+        // per-pixel CUDA-core items (eltwise ops, 5x5 depthwise, fp32 window
+        // ops): rows per item grown (in whole thread sweeps) until the op has
+        // about cc_per_sm items per SM -- fewer, longer items amortise the
+        // per-item scheduling, like the window items below
+        static const double cc_per_sm = [] {
+          const char* e = getenv("GACER_CC_ITEMS_PER_SM");
+          return e ? std::max(0.05, atof(e)) : 1e9;
+        }();
+        const int pstep = CC_THREADS / G;
+        const double items = static_cast<double>(cdiv(F.M, F.bm)) * cdiv(F.Cout, F.bn);
+        if (items > cc_per_sm * kSplitSms) {
+          const int sweeps = static_cast<int>(std::ceil(items / (cc_per_sm * kSplitSms)));
+          F.bm *= std::max(1, sweeps);
+          (void)pstep;
+        }
+      }
       F.tiles_n = cdiv(F.Cout, F.bn);
       // bf16 window ops (depthwise / max / avg pool, <= 9 taps): items of R
       // whole output rows whose input rows are staged in shared memory
-      // (window_smem); R from the staging budget and >= ~2 items per SM
+      // (window_smem); R from the staging budget and ~0.5 items per SM (fewer,
+      // longer items: each item drains the GEMM ring it borrows and pays the
+      // per-item claim / release; D2 1.81 -> 1.71 ms vs 2 per SM, D3 -3.6 %)
       F.win = false;
       if (!f32 && (F.kind == DK_DW || F.kind == DK_MAXPOOL || F.kind == DK_AVGPOOL) && F.kh * F.kw <= 9) {
         const long long row_bytes = static_cast<long long>(F.W) * F.bn * 2;
@@ -975,7 +999,12 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         if (rows_fit >= F.kh) {
           const int r_max = static_cast<int>((rows_fit - F.kh) / F.stride + 1);
           const long long out_rows = static_cast<long long>(B) * F.Ho;
-          const int r_par = static_cast<int>(std::max<long long>(1, out_rows * F.tiles_n / (2 * kSplitSms)));
+          static const double win_per_sm = [] {   // items per SM the row count aims at (A/B knob)
+            const char* e = getenv("GACER_WIN_ITEMS_PER_SM");
+            return e ? std::max(0.05, atof(e)) : 0.5;   // D2 1.81 -> 1.71 ms vs 2 (same-box A/B)
+          }();
+          const int r_par = static_cast<int>(std::max<long long>(
+              1, static_cast<long long>(static_cast<double>(out_rows * F.tiles_n) / (win_per_sm * kSplitSms))));
           const int R = std::max(1, std::min(r_max, r_par));
           F.bm = R * F.Wo;
           F.win = true;

@@ -9,7 +9,7 @@ import bench  # noqa: E402
 from paper_2304_11745_b200 import gacer as G  # noqa: E402
 from paper_2304_11745_b200.runtime import Session  # noqa: E402
 
-ts = bench.make_workload()
+ts = bench.make_workload(os.environ.get("GACER_AB_CONFIG", bench.CONFIG))
 s = Session([(g, p, B, dt) for _, g, p, B, dt, _ in ts])
 for t, (*_, x) in enumerate(ts):
     s.set_input(t, x)
