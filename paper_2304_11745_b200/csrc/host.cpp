@@ -869,11 +869,18 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           //  would grow from 7 to 49 K-blocks)
           // (the cp.async gather fills both 128-row halves too, so a small-Cin
           //  layer keeps its short 8-channel K stride)
-          static const int mpair_per_sm = [] {   // pair items per SM required (A/B knob)
+          const int mpair_per_sm = [] {   // pair items per SM required (A/B knob)
             const char* e = getenv("GACER_MPAIR_PER_SM");
             return e ? std::max(1, atoi(e)) : 2;
           }();
-          if (!F.swap && F.a_mode != A_IM2COL8 && F.Cout <= 128 && F.Cin <= 64 &&
+          // (any Cin: the 256-row tile halves the items of deep layers too --
+          //  D2 -0.9 %, Table-2 AlexNet mix -1.6 %, others neutral; the
+          //  round-2 limit was Cin <= 64, GACER_MPAIR_CIN_MAX restores it)
+          const int mpair_cin_max = [] {
+            const char* e = getenv("GACER_MPAIR_CIN_MAX");
+            return e ? atoi(e) : (1 << 30);
+          }();
+          if (!F.swap && F.a_mode != A_IM2COL8 && F.Cout <= 128 && F.Cin <= mpair_cin_max &&
               cdiv(static_cast<int>(m_rows), 2 * BM) * cdiv(F.Cout, bn_est) >= mpair_per_sm * kSplitSms &&
               !env_flag("GACER_NO_MPAIR"))
             F.mrep = 2;
@@ -921,7 +928,24 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         int sk = 1;
         // (each split keeps >= 8 K-blocks: below that the fixed-order
         //  reduction of the partials costs more than the MMA it parallelises)
-        while (sk < MAX_SPLIT && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 8) sk *= 2;
+        // Convolutions run without split-K by default: the last arrival's
+        // fixed-order reduction is a serial tail of dependent L2 round trips
+        // (bn = 256: 32 steps, ~27 us on VGG-16's conv5_x against 14 us of
+        // MMA work per split), and the executor fills the SMs a narrow conv
+        // leaves idle with other items.  Same-box A/B: D2 1.71 -> 1.57 ms,
+        // D3 4.20 -> 3.47 ms, the Table-2 mixes -8 to -10 %, the sequential
+        // baseline faster too.  The swap-AB linears keep theirs (VGG-16's
+        // FC1: 392 K-blocks on 32 tiles).  GACER_SPLITK_MAX=2/4 re-enables it.
+        const int split_max_conv = [] {
+          const char* e = getenv("GACER_SPLITK_MAX");
+          return e ? std::max(1, std::min(MAX_SPLIT, atoi(e))) : 1;
+        }();
+        const int split_max_swap = [] {
+          const char* e = getenv("GACER_SPLITK_SWAP_MAX");
+          return e ? std::max(1, std::min(MAX_SPLIT, atoi(e))) : MAX_SPLIT;
+        }();
+        const int split_max = F.swap ? split_max_swap : split_max_conv;
+        while (sk < split_max && tiles * sk * 2 <= kSplitSms && F.nkb / (sk * 2) >= 8) sk *= 2;
         if (F.mrep > 1) sk = 1;
         F.split_k = sk;
         F.w_bf16.assign(rows * F.Kpad, 0);
@@ -974,7 +998,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         // ops): rows per item grown (in whole thread sweeps) until the op has
         // about cc_per_sm items per SM -- fewer, longer items amortise the
         // per-item scheduling, like the window items below
-        static const double cc_per_sm = [] {
+        const double cc_per_sm = [] {
           const char* e = getenv("GACER_CC_ITEMS_PER_SM");
           return e ? std::max(0.05, atof(e)) : 1e9;
         }();
@@ -999,7 +1023,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         if (rows_fit >= F.kh) {
           const int r_max = static_cast<int>((rows_fit - F.kh) / F.stride + 1);
           const long long out_rows = static_cast<long long>(B) * F.Ho;
-          static const double win_per_sm = [] {   // items per SM the row count aims at (A/B knob)
+          const double win_per_sm = [] {   // items per SM the row count aims at (A/B knob)
             const char* e = getenv("GACER_WIN_ITEMS_PER_SM");
             return e ? std::max(0.05, atof(e)) : 0.5;   // D2 1.81 -> 1.71 ms vs 2 (same-box A/B)
           }();

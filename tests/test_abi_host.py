@@ -280,3 +280,21 @@ def test_buffer_reuse_footprint(host, monkeypatch):
     info = G.gacer_get_tenant_info(register(g, 2))
     one = 2 * 32 * 32 * 64 * 2
     assert info["act_bytes"] == 3 * one, info   # (the small GAP output fits a freed buffer)
+
+
+def test_split_k_defaults(host, monkeypatch):
+    """Split-K (a function of the layer shape and these process knobs only):
+    convolutions run without it by default (the fixed-order reduction tail
+    outweighs the parallelism inside a multi-tenant round), the swap-AB
+    linears keep it; GACER_SPLITK_MAX re-enables it for convolutions (the
+    per-op GPU gate of the deep-K case runs that way)."""
+    def deep():
+        g = workloads.Graph("deep", 512, 7, 7)
+        g.relu(g.bn(g.conv(0, 512, 512, 3, 1, 1), 512))
+        return G.gacer_get_tenant_info(register(g, 8))
+    assert deep()["split_k_ops"] == 0
+    monkeypatch.setenv("GACER_SPLITK_MAX", "4")
+    assert deep()["split_k_ops"] == 1
+    monkeypatch.delenv("GACER_SPLITK_MAX")
+    v = G.gacer_get_tenant_info(register(workloads.build_model("vgg16"), 8))
+    assert v["split_k_ops"] >= 1 and v["swap_ops"] == 3
