@@ -871,7 +871,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           //  layer keeps its short 8-channel K stride)
           const int mpair_per_sm = [] {   // pair items per SM required (A/B knob)
             const char* e = getenv("GACER_MPAIR_PER_SM");
-            return e ? std::max(1, atoi(e)) : 2;
+            return e ? std::max(1, atoi(e)) : 1;   // (was 2: D3 -3 %, D2 / Table-2 neutral)
           }();
           // (any Cin: the 256-row tile halves the items of deep layers too --
           //  D2 -0.9 %, Table-2 AlexNet mix -1.6 %, others neutral; the
@@ -917,7 +917,11 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           // scripts/micro/tma_rate2.cu), so the wide tile needs ~30% less
           // SM time per FLOP; in a multi-tenant round the other tenants'
           // items fill the SMs a layer no longer covers by itself.
-          if (F.Cout >= 256 && (F.tiles_m * cdiv(F.Cout, 256) >= kSplitSms || F.flops >= 2.0e9)) F.bn = 256;
+          const double wide_gflop = [] {   // (A/B knob: FLOP threshold of the 128x256 tile)
+            const char* e = getenv("GACER_WIDE_GFLOP");
+            return e ? atof(e) : 2.0;
+          }();
+          if (F.Cout >= 256 && (F.tiles_m * cdiv(F.Cout, 256) >= kSplitSms || F.flops >= wide_gflop * 1e9)) F.bn = 256;
           else F.bn = F.Cout >= 128 ? 128 : roundup(F.Cout, 16);
           F.tiles_n = cdiv(F.Cout, F.bn);
           rows = static_cast<size_t>(F.tiles_n) * F.bn;
@@ -1000,7 +1004,10 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
         // per-item scheduling, like the window items below
         const double cc_per_sm = [] {
           const char* e = getenv("GACER_CC_ITEMS_PER_SM");
-          return e ? std::max(0.05, atof(e)) : 1e9;
+          // 1 per SM: R101+D121+M3 3.24 -> 3.02 ms, D2 / D3 neutral, the
+          // per-op baselines unchanged (0.5 gained a little more in the
+          // executor but cost the baselines 5-7 %)
+          return e ? std::max(0.05, atof(e)) : 1.0;
         }();
         const int pstep = CC_THREADS / G;
         const double items = static_cast<double>(cdiv(F.M, F.bm)) * cdiv(F.Cout, F.bn);

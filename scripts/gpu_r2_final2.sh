@@ -1,8 +1,8 @@
 #!/bin/bash
 # late-round-2 measurement set: GPU suite, bench lines (D2 default = the driver's, D4 plain and with A12,
 # D3, Table-2 mixes, D1), launch list of the bench command, ncu full set of the D2 executor, D7
-mkdir -p gpurun_out/f2
-O=gpurun_out/f2
+O=${OUT:-gpurun_out/f2}; mkdir -p $O
+
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q > $O/gputest.log 2>&1; tail -3 $O/gputest.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; tail -c 300 $O/bench.err; cut -c1-400 $O/bench.json
