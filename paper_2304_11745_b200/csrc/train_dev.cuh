@@ -984,7 +984,12 @@ VG_FN void vg_wgrad_reduce(const VArgs& a, int vb, int nvb, int tid, int nthr, u
 // thread writes each chunk back with a bulk store.  Same per-element IEEE
 // operations as the register path (results bit-identical); only the
 // element -> thread assignment differs.
-constexpr int VGS_CH = 512;                   // 16-byte groups per chunk (8 KB per tensor)
+constexpr int VGS_CH = 512;                   // min 16-byte groups per chunk (8 KB per tensor)
+#ifndef GACER_VGS_CH_MAX
+#define GACER_VGS_CH_MAX 2048
+#endif
+constexpr int VGS_CH_MAX = GACER_VGS_CH_MAX;  // max groups per chunk (32 KB per tensor)
+constexpr int VGS_MIN_STAGES = 4;
 constexpr int VGS_MAX_STAGES = 8;
 
 __device__ __forceinline__ uint32_t vgs_u32(const void* p) {
@@ -1147,12 +1152,18 @@ __device__ void vgs_run(const Op& op, int64_t g0, int64_t g1, int tid, int nthr,
   float* extra = reinterpret_cast<float*>(smem + 128);
   const int ex_bytes = (op.extra_bytes() + 127) & ~127;
   uint8_t* stages = smem + 128 + ex_bytes;
-  const int stage_bytes = op.n_in * VGS_CH * 16;
+  // chunk size: the largest that still gives VGS_MIN_STAGES stages (the
+  // per-chunk cost -- barrier, fence, bulk-store issue -- is ~0.6 us, so
+  // 8 KB chunks capped a streaming operator at ~12 GB/s per SM)
+  int ch = (smem_bytes - 128 - ex_bytes) / (VGS_MIN_STAGES * op.n_in * 16);
+  ch = ch > VGS_CH_MAX ? VGS_CH_MAX : (ch < VGS_CH ? VGS_CH : ch);
+  ch &= ~31;
+  const int stage_bytes = op.n_in * ch * 16;
   int ns = (smem_bytes - 128 - ex_bytes) / stage_bytes;
   ns = ns > VGS_MAX_STAGES ? VGS_MAX_STAGES : ns;
-  const int64_t nch = (g1 - g0 + VGS_CH - 1) / VGS_CH;
+  const int64_t nch = (g1 - g0 + ch - 1) / ch;
   auto chunk_len = [&](int64_t k) -> int {
-    const int64_t b = g0 + k * VGS_CH, e = b + VGS_CH < g1 ? b + VGS_CH : g1;
+    const int64_t b = g0 + k * ch, e = b + ch < g1 ? b + ch : g1;
     return static_cast<int>(e - b);
   };
   auto issue_load = [&](int64_t k) {
@@ -1161,8 +1172,8 @@ __device__ void vgs_run(const Op& op, int64_t g0, int64_t g1, int tid, int nthr,
     const uint32_t bytes = static_cast<uint32_t>(len) * 16u;
     vgs_mbar_expect(&bars[st], bytes * op.n_in);
     for (int t = 0; t < op.n_in; ++t)
-      vgs_load(stages + st * stage_bytes + t * VGS_CH * 16,
-               static_cast<const uint8_t*>(op.in(t)) + (g0 + k * VGS_CH) * 16, bytes, &bars[st]);
+      vgs_load(stages + st * stage_bytes + t * ch * 16,
+               static_cast<const uint8_t*>(op.in(t)) + (g0 + k * ch) * 16, bytes, &bars[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < ns; ++st) vgs_mbar_init(&bars[st], 1);
@@ -1177,9 +1188,9 @@ __device__ void vgs_run(const Op& op, int64_t g0, int64_t g1, int tid, int nthr,
     vgs_mbar_wait(&bars[st], static_cast<uint32_t>((k / ns) & 1));
     uint4* sl[3];
     for (int t = 0; t < 3; ++t)
-      sl[t] = reinterpret_cast<uint4*>(stages + st * stage_bytes + (t < op.n_in ? t : 0) * VGS_CH * 16);
+      sl[t] = reinterpret_cast<uint4*>(stages + st * stage_bytes + (t < op.n_in ? t : 0) * ch * 16);
     const int len = chunk_len(k);
-    const int64_t base = g0 + k * VGS_CH;
+    const int64_t base = g0 + k * ch;
     for (int j = tid; j < len; j += nthr) op.apply(sl, j, base + j, extra);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic smem writes -> bulk store
     vg_bar(nthr);
