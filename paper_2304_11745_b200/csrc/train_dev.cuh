@@ -58,6 +58,55 @@ __device__ __forceinline__ uint4 vg_pack8(const float* f) {
 // Thread t owns 8-channel group gl = t % G and row phase t / G.
 // a: p0 x, p1 dy, p2 ym, p3 mean, p4 var, p5 part [P][2][C] (out); n0 M;
 //    i0 mode, i1 C; f0 eps
+// BN partial sums over rows r, r + RP, ... < r1 of 8 channels (g): U rows'
+// loads in flight, summed in row order.  MODE 0: shifted sums of x - K;
+// MODE 1: sum dy' and sum dy' * xhat (dy' = dy masked by the ReLU output ym).
+template <int U, int MODE>
+__device__ __forceinline__ void bnp_rows(const __nv_bfloat16* x, const __nv_bfloat16* dy, const __nv_bfloat16* ym,
+                                         int C, int g, int64_t rbeg, int64_t r1, int RP, const float (&mu)[8],
+                                         const float (&is)[8], float (&s1)[8], float (&s2)[8]) {
+  for (int64_t r = rbeg; r < r1; r += static_cast<int64_t>(U) * RP) {
+    uint4 va[U], vd[MODE ? U : 1], vm[MODE ? U : 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t rr = r + u * RP;
+      va[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(x + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+      if (MODE == 1) {
+        vd[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(dy + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+        vm[u] = (ym && rr < r1) ? __ldcs(reinterpret_cast<const uint4*>(ym + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (r + u * RP >= r1) break;
+      float v[8];
+      vg_unpack8(va[u], v);
+      if (MODE == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = v[j] - mu[j];
+          s1[j] += d;
+          s2[j] = fmaf(d, d, s2[j]);
+        }
+      } else {
+        float d[8];
+        vg_unpack8(vd[MODE ? u : 0], d);
+        if (ym) {                        // fused ReLU backward: the mask of the BN's ReLU output
+          float mk[8];
+          vg_unpack8(vm[MODE ? u : 0], mk);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s1[j] += d[j];
+          s2[j] = fmaf(d[j], (v[j] - mu[j]) * is[j], s2[j]);
+        }
+      }
+    }
+  }
+}
+
 VG_FN void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t* smem) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   const __nv_bfloat16* dy = static_cast<const __nv_bfloat16*>(a.p[1]);
@@ -69,7 +118,6 @@ VG_FN void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, int nthr, uin
   const int mode = a.i[0], C = a.i[1];
   const float eps = a.f[0];
   float* red = reinterpret_cast<float*>(smem);           // [2][nthr * 8]
-  constexpr int kUnroll = 8;                             // rows per thread with loads in flight (summed in row order)
   const int G8 = C / 8;
   const int G = G8 < nthr ? G8 : nthr;
   const int RP = nthr / G;
@@ -94,46 +142,11 @@ VG_FN void vg_bn_partial(const VArgs& a, int vb, int nvb, int tid, int nthr, uin
       }
     }
     if (active) {
-      for (int64_t r = r0 + ph; r < r1; r += kUnroll * RP) {
-        uint4 va[kUnroll], vd[kUnroll], vm[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t rr = r + u * RP;
-          va[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(x + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
-          if (mode == 1) {
-            vd[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(dy + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
-            vm[u] = (ym && rr < r1) ? __ldcs(reinterpret_cast<const uint4*>(ym + rr * C + g * 8)) : make_uint4(0, 0, 0, 0);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          if (r + u * RP >= r1) break;
-          float v[8];
-          vg_unpack8(va[u], v);
-          if (mode == 0) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float d = v[j] - mu[j];
-              s1[j] += d;
-              s2[j] = fmaf(d, d, s2[j]);
-            }
-          } else {
-            float d[8];
-            vg_unpack8(vd[u], d);
-            if (ym) {                        // fused ReLU backward: the mask of the BN's ReLU output
-              float mk[8];
-              vg_unpack8(vm[u], mk);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) d[j] = mk[j] > 0.0f ? d[j] : 0.0f;
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              s1[j] += d[j];
-              s2[j] = fmaf(d[j], (v[j] - mu[j]) * is[j], s2[j]);
-            }
-          }
-        }
-      }
+      // rows in flight per thread: 16 for the forward statistics (one tensor),
+      // 8 for the backward sums (three tensors); each thread still sums its
+      // rows r0 + ph, + RP, ... in row order (results independent of it)
+      if (mode == 0) bnp_rows<16, 0>(x, dy, ym, C, g, r0 + ph, r1, RP, mu, is, s1, s2);
+      else bnp_rows<8, 1>(x, dy, ym, C, g, r0 + ph, r1, RP, mu, is, s1, s2);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
