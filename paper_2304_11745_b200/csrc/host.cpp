@@ -3660,7 +3660,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
       case GACER_OP_LINEAR: {
         const bool last = i == n - 1;
         const int zb = last ? TBUF_OUT : L.buf(static_cast<size_t>(B) * o.c_out * 4);
-        TrainOp a = TrainLowering::vg(VF_LINEAR_FWD, vg_grid_for(static_cast<int64_t>(B) * o.c_out * 32));
+        TrainOp a = TrainLowering::vg(VF_LINEAR_FWD, vg_grid_for(static_cast<int64_t>(B) * ((o.c_out + 3) / 4) * 32));
         a.vp[0] = bref(xb); a.vp[1] = pref(i, 0);
         if (o.flags & GACER_FLAG_BIAS) a.vp[2] = pref(i, 1);
         a.vp[3] = bref(zb);
@@ -3715,11 +3715,11 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
     switch (o.kind) {
       case GACER_OP_LINEAR: {
         const int dx = L.buf(static_cast<size_t>(B) * x.c * 4);
-        TrainOp a = TrainLowering::vg(VF_LINEAR_DX, vg_grid_for(static_cast<int64_t>(B) * x.c));
+        TrainOp a = TrainLowering::vg(VF_LINEAR_DX, vg_grid_for(static_cast<int64_t>((B + 3) / 4) * x.c));
         a.vp[0] = pref(i, 0); a.vp[1] = bref(dy); a.vp[2] = bref(dx);
         a.va.i[0] = B; a.va.i[1] = x.c; a.va.i[2] = o.c_out;
         L.add(std::move(a), {T.buf_params, dy}, {dx});
-        TrainOp w = TrainLowering::vg(VF_LINEAR_DW, vg_grid_for(static_cast<int64_t>(o.c_out) * x.c));
+        TrainOp w = TrainLowering::vg(VF_LINEAR_DW, vg_grid_for(static_cast<int64_t>((o.c_out + 3) / 4) * x.c));
         w.vp[0] = bref(xb); w.vp[1] = bref(dy); w.vp[2] = gref(i, 0);
         if (o.flags & GACER_FLAG_BIAS) w.vp[3] = gref(i, 1);
         w.va.i[0] = B; w.va.i[1] = x.c; w.va.i[2] = o.c_out;

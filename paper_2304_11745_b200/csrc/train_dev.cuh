@@ -496,23 +496,44 @@ VG_FN void vg_maxpool_bwd(const VArgs& a, int vb, int nvb, int tid, int nthr, ui
     wo0 = wo0 <= 0 ? 0 : (wo0 + S - 1) / S;
     int wo1 = (wi + pw) / S;
     wo1 = wo1 < Wo - 1 ? wo1 : Wo - 1;
-    for (int ho = ho0; ho <= ho1; ++ho)
-      for (int wo = wo0; wo <= wo1; ++wo) {
-        const int64_t o = ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * G8 + g;
-        const uint2 t = arg[o];
-        const uint32_t me = static_cast<uint32_t>((hi - (ho * S - ph)) * KW + (wi - (wo * S - pw)));
-        const uint32_t tt[8] = {t.x & 255u, (t.x >> 8) & 255u, (t.x >> 16) & 255u, t.x >> 24,
-                                t.y & 255u, (t.y >> 8) & 255u, (t.y >> 16) & 255u, t.y >> 24};
-        bool any = false;
+    auto add_window = [&](int ho, int wo, uint2 t, uint4 dv) {
+      const uint32_t me = static_cast<uint32_t>((hi - (ho * S - ph)) * KW + (wi - (wo * S - pw)));
+      const uint32_t tt[8] = {t.x & 255u, (t.x >> 8) & 255u, (t.x >> 16) & 255u, t.x >> 24,
+                              t.y & 255u, (t.y >> 8) & 255u, (t.y >> 16) & 255u, t.y >> 24};
+      float d[8];
+      vg_unpack8(dv, d);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) any |= tt[j] == me;
-        if (!any) continue;
-        float d[8];
-        vg_unpack8(dy[o], d);
+      for (int j = 0; j < 8; ++j)
+        if (tt[j] == me) acc[j] += d[j];
+    };
+    if (ho1 - ho0 <= 1 && wo1 - wo0 <= 1) {
+      // at most 2 x 2 windows (3x3 / stride 2): every window's argmax and dy
+      // loaded up front (one round trip instead of two per window); summed
+      // in the same (ho, wo) order.  (Two groups per pass, or the 3x3
+      // forward / argmax taps loaded together, spilled and ran slower.)
+      uint2 t[4];
+      uint4 dv[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (tt[j] == me) acc[j] += d[j];
+      for (int q = 0; q < 4; ++q) {
+        const int ho = ho0 + (q >> 1), wo = wo0 + (q & 1);
+        if (ho <= ho1 && wo <= wo1) {
+          const int64_t o = ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * G8 + g;
+          t[q] = arg[o];
+          dv[q] = dy[o];
+        }
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ho = ho0 + (q >> 1), wo = wo0 + (q & 1);
+        if (ho <= ho1 && wo <= wo1) add_window(ho, wo, t[q], dv[q]);
+      }
+    } else {
+      for (int ho = ho0; ho <= ho1; ++ho)
+        for (int wo = wo0; wo <= wo1; ++wo) {
+          const int64_t o = ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * G8 + g;
+          add_window(ho, wo, arg[o], dy[o]);
+        }
+    }
     dx[i] = vg_pack8(acc);
   }
 }
@@ -567,52 +588,98 @@ VG_FN void vg_linear_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, uin
   float* z = static_cast<float*>(const_cast<void*>(a.p[3]));
   const int N = a.i[0], K = a.i[1], O = a.i[2];
   const int lane = tid & 31;
+  // a warp computes 4 outputs (n, o .. o + 3) of one row (N * ceil(O/4)
+  // warp units): 4 independent FMA chains sharing the x loads; each output
+  // keeps its summation order (lane partials over k = lane, lane + 32, ...,
+  // then the xor tree)
+  const int O4 = (O + 3) / 4;
   const int64_t nw = static_cast<int64_t>(nvb) * (nthr >> 5);
-  for (int64_t wid = static_cast<int64_t>(vb) * (nthr >> 5) + (tid >> 5); wid < static_cast<int64_t>(N) * O;
+  for (int64_t wid = static_cast<int64_t>(vb) * (nthr >> 5) + (tid >> 5); wid < static_cast<int64_t>(N) * O4;
        wid += nw) {
-    const int n = static_cast<int>(wid / O), o = static_cast<int>(wid % O);
+    const int n = static_cast<int>(wid / O4), o0 = static_cast<int>(wid % O4) * 4;
     const __nv_bfloat16* xr = x + static_cast<int64_t>(n) * K;
-    const float* wr = w + static_cast<int64_t>(o) * K;
-    float s = 0.0f;
-    for (int k = lane; k < K; k += 32) s = fmaf(__bfloat162float(xr[k]), wr[k], s);
+    const float* wr[4];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) z[wid] = s + (b ? b[o] : 0.0f);
+    for (int u = 0; u < 4; ++u) wr[u] = w + static_cast<int64_t>(o0 + u < O ? o0 + u : o0) * K;
+    float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = lane; k < K; k += 32) {
+      const float xv = __bfloat162float(xr[k]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] = fmaf(xv, wr[u][k], s[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s[u] += __shfl_xor_sync(0xffffffffu, s[u], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (o0 + u < O) z[static_cast<int64_t>(n) * O + o0 + u] = s[u] + (b ? b[o0 + u] : 0.0f);
+    }
   }
 }
-
-// dx[n][k] = sum_o dy[n][o] w[o][k] in o order.  a: p0 w, p1 dy, p2 dx (f32); i0 N, i1 K, i2 O
+// a: p0 w [O][K] fp32, p1 dy [N][O] fp32, p2 dx [N][K] fp32; i0 N, i1 K, i2 O.
+// Unit: 4 rows n0..n0+3 of one column k (the grid covers ceil(N/4) * K
+// units): each weight load serves 4 independent FMA chains; every output
+// still sums over o in order.
 VG_FN void vg_linear_dx(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const float* w = static_cast<const float*>(a.p[0]);
   const float* dy = static_cast<const float*>(a.p[1]);
   float* dx = static_cast<float*>(const_cast<void*>(a.p[2]));
   const int N = a.i[0], K = a.i[1], O = a.i[2];
-  VG_LOOP(i, static_cast<int64_t>(N) * K) {
-    const int n = static_cast<int>(i / K), k = static_cast<int>(i % K);
-    float s = 0.0f;
-    for (int o = 0; o < O; ++o) s = fmaf(dy[static_cast<int64_t>(n) * O + o], w[static_cast<int64_t>(o) * K + k], s);
-    dx[i] = s;
+  const int N4 = (N + 3) / 4;
+  VG_LOOP(i, static_cast<int64_t>(N4) * K) {
+    const int n0 = static_cast<int>(i / K) * 4, k = static_cast<int>(i % K);
+    const float* dyr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dyr[u] = dy + static_cast<int64_t>(n0 + u < N ? n0 + u : n0) * O;
+    float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 4
+    for (int o = 0; o < O; ++o) {
+      const float wv = w[static_cast<int64_t>(o) * K + k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] = fmaf(dyr[u][o], wv, s[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (n0 + u < N) dx[static_cast<int64_t>(n0 + u) * K + k] = s[u];
   }
 }
 
 // dw[o][k] = sum_n dy[n][o] x[n][k], db[o] = sum_n dy[n][o] (n order).
 // a: p0 x (bf16), p1 dy, p2 dw, p3 db (nullable); i0 N, i1 K, i2 O
+// a: p0 x [N][K] bf16, p1 dy [N][O] fp32, p2 dw [O][K], p3 db [O] (or null); i0 N, i1 K, i2 O.
+// Unit: 4 outputs o0..o0+3 of one column k (ceil(O/4) * K units): each x
+// load serves 4 chains; every output sums over n in order.
 VG_FN void vg_linear_dw(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   const float* dy = static_cast<const float*>(a.p[1]);
   float* dw = static_cast<float*>(const_cast<void*>(a.p[2]));
   float* db = static_cast<float*>(const_cast<void*>(a.p[3]));
   const int N = a.i[0], K = a.i[1], O = a.i[2];
-  VG_LOOP(i, static_cast<int64_t>(O) * K) {
-    const int o = static_cast<int>(i / K), k = static_cast<int>(i % K);
-    float s = 0.0f;
-    for (int n = 0; n < N; ++n)
-      s = fmaf(dy[static_cast<int64_t>(n) * O + o], __bfloat162float(x[static_cast<int64_t>(n) * K + k]), s);
-    dw[i] = s;
+  const int O4 = (O + 3) / 4;
+  VG_LOOP(i, static_cast<int64_t>(O4) * K) {
+    const int o0 = static_cast<int>(i / K) * 4, k = static_cast<int>(i % K);
+    float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 4
+    for (int n = 0; n < N; ++n) {
+      const float xv = __bfloat162float(x[static_cast<int64_t>(n) * K + k]);
+      const float* dyr = dy + static_cast<int64_t>(n) * O + o0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] = fmaf(o0 + u < O ? dyr[u] : 0.0f, xv, s[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (o0 + u < O) dw[static_cast<int64_t>(o0 + u) * K + k] = s[u];
     if (db && k == 0) {
-      float t = 0.0f;
-      for (int n = 0; n < N; ++n) t += dy[static_cast<int64_t>(n) * O + o];
-      db[o] = t;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (o0 + u >= O) break;
+        float t = 0.0f;
+        for (int n = 0; n < N; ++n) t += dy[static_cast<int64_t>(n) * O + o0 + u];
+        db[o0 + u] = t;
+      }
     }
   }
 }

@@ -299,7 +299,7 @@ int32_t gacer_linear_fwd(const void* x_dev, const float* w_dev, const float* b_d
   if (!x_dev || !w_dev || !z_dev) return bad(GACER_E_INVALID_ARG, "linear_fwd: null pointer");
   VArgs a = vargs();
   a.p[0] = x_dev; a.p[1] = w_dev; a.p[2] = b_dev; a.p[3] = z_dev; a.i[0] = N; a.i[1] = K; a.i[2] = O;
-  vlaunch(VF_LINEAR_FWD, a, vg_grid_for(static_cast<int64_t>(N) * O * 32), static_cast<cudaStream_t>(stream));
+  vlaunch(VF_LINEAR_FWD, a, vg_grid_for(static_cast<int64_t>(N) * ((O + 3) / 4) * 32), static_cast<cudaStream_t>(stream));
   return launched("linear_fwd");
 }
 
@@ -311,11 +311,11 @@ int32_t gacer_linear_bwd(const void* x_dev, const float* w_dev, const float* dy_
   if (dx_dev) {
     VArgs a = vargs();
     a.p[0] = w_dev; a.p[1] = dy_dev; a.p[2] = dx_dev; a.i[0] = N; a.i[1] = K; a.i[2] = O;
-    vlaunch(VF_LINEAR_DX, a, vg_grid_for(static_cast<int64_t>(N) * K), s);
+    vlaunch(VF_LINEAR_DX, a, vg_grid_for(static_cast<int64_t>((N + 3) / 4) * K), s);
   }
   VArgs a = vargs();
   a.p[0] = x_dev; a.p[1] = dy_dev; a.p[2] = dw_dev; a.p[3] = db_dev; a.i[0] = N; a.i[1] = K; a.i[2] = O;
-  vlaunch(VF_LINEAR_DW, a, vg_grid_for(static_cast<int64_t>(O) * K), s);
+  vlaunch(VF_LINEAR_DW, a, vg_grid_for(static_cast<int64_t>((O + 3) / 4) * K), s);
   return launched("linear_bwd");
 }
 
