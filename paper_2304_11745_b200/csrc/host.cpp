@@ -3558,6 +3558,7 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
 
   // ---- forward
   std::vector<int> out(n, -1);   // output buffer of each op (after aliasing)
+  std::map<int, int> pool_arg;   // max-pool op -> its argmax buffer (written by the forward pool)
   auto out_of = [&](int id) { return id == 0 ? TBUF_IN : out[pos.at(id)]; };
   std::vector<std::pair<int, int>> saved(n, {-1, -1});   // BN: (mean, var)
   int logits = -1;
@@ -3639,13 +3640,19 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         break;
       }
       case GACER_OP_MAXPOOL: {
+        // the forward pool and the backward's argmax in one pass over x:
+        // y (as VF_MAXPOOL_FWD computes it) and the per-channel window argmax
+        // (as VF_MAXPOOL_ARGMAX) -- the backward then reads the stored argmax
+        // instead of re-reading x at the end of the step
         const int yb = L.buf(static_cast<size_t>(B) * y.h * y.w * x.c * 2);
-        TrainOp a = TrainLowering::vg(VF_MAXPOOL_FWD, vg_grid_for(static_cast<int64_t>(B) * y.h * y.w * (x.c / 8)));
-        a.vp[0] = bref(xb); a.vp[1] = bref(yb);
+        const int arg = L.buf(static_cast<size_t>(B) * y.h * y.w * x.c);
+        TrainOp a = TrainLowering::vg(VF_MAXPOOL_ARGMAX, vg_grid_for(static_cast<int64_t>(B) * y.h * y.w * (x.c / 8)));
+        a.vp[0] = bref(xb); a.vp[1] = bref(arg); a.vp[2] = bref(yb);
         const int iv[11] = {B, x.h, x.w, x.c, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, y.h, y.w};
         std::memcpy(a.va.i, iv, sizeof iv);
-        L.add(std::move(a), {xb}, {yb});
+        L.add(std::move(a), {xb}, {yb, arg});
         out[i] = yb;
+        pool_arg[i] = arg;
         break;
       }
       case GACER_OP_GAP: {
@@ -3786,13 +3793,9 @@ int lower_train(const gacer_graph* g, int batch, Tenant& T, const std::map<int, 
         break;
       }
       case GACER_OP_MAXPOOL: {
-        const int arg = L.buf(static_cast<size_t>(B) * y.h * y.w * x.c);
+        const int arg = pool_arg.at(i);   // written by the forward pool
         const int dx = L.buf(xbytes);
         const int iv[11] = {B, x.h, x.w, x.c, o.kh, o.kw, o.stride, o.pad_h, o.pad_w, y.h, y.w};
-        TrainOp a = TrainLowering::vg(VF_MAXPOOL_ARGMAX, vg_grid_for(static_cast<int64_t>(B) * y.h * y.w * (x.c / 8)));
-        a.vp[0] = bref(xb); a.vp[1] = bref(arg);
-        std::memcpy(a.va.i, iv, sizeof iv);
-        L.add(std::move(a), {xb}, {arg});
         TrainOp b2 = TrainLowering::vg(VF_MAXPOOL_BWD, vg_grid_for(static_cast<int64_t>(B) * x.h * x.w * (x.c / 8)));
         b2.vp[0] = bref(arg); b2.vp[1] = bref(dy); b2.vp[2] = bref(dx);
         std::memcpy(b2.va.i, iv, sizeof iv);

@@ -439,6 +439,10 @@ VG_FN void vg_maxpool_fwd(const VArgs& a, int vb, int nvb, int tid, int nthr, ui
 VG_FN void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int tid, int nthr, uint8_t*) {
   const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.p[0]);
   uint2* arg = static_cast<uint2*>(const_cast<void*>(a.p[1]));
+  // p2 (optional): also the pooled output, exactly as vg_maxpool_fwd computes
+  // it (the fmaxf chain) -- the executor's training step runs the forward
+  // pool and the backward's argmax as this one operator
+  uint4* yo = static_cast<uint4*>(const_cast<void*>(a.p[2]));
   const int N = a.i[0], H = a.i[1], W = a.i[2], C = a.i[3], KH = a.i[4], KW = a.i[5], S = a.i[6], ph = a.i[7],
             pw = a.i[8], Ho = a.i[9], Wo = a.i[10];
   const int G8 = C / 8;
@@ -450,7 +454,9 @@ VG_FN void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int tid, int nthr,
     float best[8];
     uint32_t tap[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; tap[j] = 255u; }
+    float mx[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; tap[j] = 255u; mx[j] = -INFINITY; }
     for (int r = 0; r < KH; ++r) {
       const int hh = ho * S - ph + r;
       if (hh < 0 || hh >= H) continue;
@@ -461,14 +467,17 @@ VG_FN void vg_maxpool_argmax(const VArgs& a, int vb, int nvb, int tid, int nthr,
         vg_unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hh) * W + ww) * C + g * 8), v);
         const uint32_t id = static_cast<uint32_t>(r * KW + q);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 8; ++j) {
           if (tap[j] == 255u || v[j] > best[j]) { best[j] = v[j]; tap[j] = id; }
+          mx[j] = fmaxf(mx[j], v[j]);
+        }
       }
     }
     uint2 o;
     o.x = tap[0] | (tap[1] << 8) | (tap[2] << 16) | (tap[3] << 24);
     o.y = tap[4] | (tap[5] << 8) | (tap[6] << 16) | (tap[7] << 24);
     arg[i] = o;
+    if (yo) yo[i] = vg_pack8(mx);
   }
 }
 
