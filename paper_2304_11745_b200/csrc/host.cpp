@@ -1020,7 +1020,7 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
       F.tiles_n = cdiv(F.Cout, F.bn);
       // bf16 window ops (depthwise / max / avg pool, <= 9 taps): items of R
       // whole output rows whose input rows are staged in shared memory
-      // (window_smem); R from the staging budget and ~0.5 items per SM (fewer,
+      // (window_smem); R from the staging budget and ~0.75 items per SM (fewer,
       // longer items: each item drains the GEMM ring it borrows and pays the
       // per-item claim / release; D2 1.81 -> 1.71 ms vs 2 per SM, D3 -3.6 %)
       F.win = false;
@@ -1032,7 +1032,9 @@ int lower_tenant(const gacer_graph* g, int batch, Tenant& T) {
           const long long out_rows = static_cast<long long>(B) * F.Ho;
           const double win_per_sm = [] {   // items per SM the row count aims at (A/B knob)
             const char* e = getenv("GACER_WIN_ITEMS_PER_SM");
-            return e ? std::max(0.05, atof(e)) : 0.5;   // D2 1.81 -> 1.71 ms vs 2 (same-box A/B)
+            // (0.5 first: D2 1.81 -> 1.71 ms vs 2; re-tuned after the split-K /
+            //  M-pair changes: 0.75 beats 0.5 by 1.7 % on D2, 1.2 % on D3)
+            return e ? std::max(0.05, atof(e)) : 0.75;
           }();
           const int r_par = static_cast<int>(std::max<long long>(
               1, static_cast<long long>(static_cast<double>(out_rows * F.tiles_n) / (win_per_sm * kSplitSms))));
