@@ -16,13 +16,14 @@ ts = []
 for i, (name, B) in enumerate(mix):
     g = workloads.build_model(name)
     ts.append((g, workloads.make_params(g, 7000 + i, "bf16"), B, "bf16", workloads.make_input(g, B, 7100 + i, "bf16")))
-s = Session([t[:4] for t in ts], partition=os.environ.get("GACER_PARTITION", "priority"))
+s = Session([t[:4] for t in ts], partition=os.environ.get("GACER_PARTITION", "priority"),
+            coarse_deps=os.environ.get("GACER_AB_COARSE", "0") == "1")
 for t, tt in enumerate(ts):
     s.set_input(t, tt[4])
 stream = torch.cuda.Stream()
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 res = {}
-for mode, n in (("executor", 20), ("multistream_graph", 10), ("executor", 20)):
+for mode, n in (("executor", 20), ("multistream_graph", 10), ("sequential_graph", 10), ("executor", 20)):
     res.setdefault(mode, []).append(float(np.median(bench.time_mode(G, s, torch, stream, mode, n, 3, flush))))
 s.close()
 print({k: [round(v, 4) for v in vs] for k, vs in res.items()})
