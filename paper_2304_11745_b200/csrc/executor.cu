@@ -1383,6 +1383,9 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 // any other item only when the ring is drained to depth 1, so a
 // latency-critical item of a small op never queues behind several long tiles
 // of a big op (head-of-line blocking inside the CTA).
+#ifndef GACER_BIGOP_DEPTH2
+#define GACER_BIGOP_DEPTH2 1   // a large op's first item may join one item in flight (D2 -0.6 %, D3 -0.4 %, B=64 mix -0.5 %)
+#endif
 #ifndef GACER_NEWOP_DEPTH
 #define GACER_NEWOP_DEPTH 1   // in-flight depth allowed when the candidate starts a different op
 #endif
@@ -1458,7 +1461,8 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         // the producers' tails instead of following them
         const uint32_t allowed =
             st == 3 ? 1u
-                    : (cand.op != last_op) ? static_cast<uint32_t>(GACER_NEWOP_DEPTH)
+                    : (cand.op != last_op) ? ((GACER_BIGOP_DEPTH2 && cand.op_left > big) ? 2u
+                                                                                      : static_cast<uint32_t>(GACER_NEWOP_DEPTH))
                                            : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
                                                                  : (cand.op_left > G1 ? 2u : 1u));
         sdbg(p, islot, 5, static_cast<int64_t>(allowed) * 1000 + (islot - consumed));
