@@ -1386,6 +1386,9 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 #ifndef GACER_BIGOP_DEPTH2
 #define GACER_BIGOP_DEPTH2 1   // a large op's first item may join one item in flight (D2 -0.6 %, D3 -0.4 %, B=64 mix -0.5 %)
 #endif
+#ifndef GACER_BIGOP_MULT
+#define GACER_BIGOP_MULT 4   // "large": more than this many items per CTA left in the segment
+#endif
 #ifndef GACER_NEWOP_DEPTH
 #define GACER_NEWOP_DEPTH 1   // in-flight depth allowed when the candidate starts a different op
 #endif
@@ -1461,7 +1464,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
         // the producers' tails instead of following them
         const uint32_t allowed =
             st == 3 ? 1u
-                    : (cand.op != last_op) ? ((GACER_BIGOP_DEPTH2 && cand.op_left > big) ? 2u
+                    : (cand.op != last_op) ? ((GACER_BIGOP_DEPTH2 && cand.op_left > GACER_BIGOP_MULT * G1) ? 2u
                                                                                       : static_cast<uint32_t>(GACER_NEWOP_DEPTH))
                                            : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
                                                                  : (cand.op_left > G1 ? 2u : 1u));

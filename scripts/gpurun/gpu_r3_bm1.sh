@@ -1,0 +1,10 @@
+#!/bin/bash
+# big-op threshold 1 x #CTAs vs 4 x #CTAs, same-box A/B
+for rep in 1 2; do
+  for lib in default bm1; do
+    if [ $lib = default ]; then unset GACER_LIB; else export GACER_LIB=$PWD/ab_libs/bm1.so; fi
+    timeout 300 python scripts/ab_d2.py 2>&1 | tail -1 | sed "s|^|[$lib d2] |"
+    GACER_AB_CONFIG=d3_five timeout 300 python scripts/ab_d2.py 2>&1 | tail -1 | sed "s|^|[$lib d3] |"
+    GACER_AB_CONFIG=t2_r101_d121_m3 timeout 300 python scripts/ab_d2.py 2>&1 | tail -1 | sed "s|^|[$lib t2r101] |"
+  done
+done
