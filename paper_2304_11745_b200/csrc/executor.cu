@@ -1386,6 +1386,9 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 #ifndef GACER_BIGOP_DEPTH2
 #define GACER_BIGOP_DEPTH2 1   // a large op's first item may join one item in flight (D2 -0.6 %, D3 -0.4 %, B=64 mix -0.5 %)
 #endif
+#ifndef GACER_TAIL_DEPTH
+#define GACER_TAIL_DEPTH 1   // in-flight depth for the last #CTAs items of an op (A/B knob)
+#endif
 #ifndef GACER_BIGOP_MULT
 #define GACER_BIGOP_MULT 4   // "large": more than this many items per CTA left in the segment
 #endif
@@ -1467,7 +1470,7 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
                     : (cand.op != last_op) ? ((GACER_BIGOP_DEPTH2 && cand.op_left > GACER_BIGOP_MULT * G1) ? 2u
                                                                                       : static_cast<uint32_t>(GACER_NEWOP_DEPTH))
                                            : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
-                                                                 : (cand.op_left > G1 ? 2u : 1u));
+                                                                 : (cand.op_left > G1 ? 2u : static_cast<uint32_t>(GACER_TAIL_DEPTH)));
         sdbg(p, islot, 5, static_cast<int64_t>(allowed) * 1000 + (islot - consumed));
         while (islot - consumed >= allowed) {
           mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
