@@ -1389,6 +1389,9 @@ __device__ bool wait_deps(const ExecParams& p, const Item& it) {
 #ifndef GACER_TAIL_DEPTH
 #define GACER_TAIL_DEPTH 1   // in-flight depth for the last #CTAs items of an op (A/B knob)
 #endif
+#ifndef GACER_TAIL_DEPTH_CC
+#define GACER_TAIL_DEPTH_CC 0   // depth 2 for the tail of CUDA-core ops only (A/B knob)
+#endif
 #ifndef GACER_BIGOP_MULT
 #define GACER_BIGOP_MULT 4   // "large": more than this many items per CTA left in the segment
 #endif
@@ -1470,7 +1473,10 @@ __device__ void scheduler_role(const ExecParams& p, Ctx& cx) {
                     : (cand.op != last_op) ? ((GACER_BIGOP_DEPTH2 && cand.op_left > GACER_BIGOP_MULT * G1) ? 2u
                                                                                       : static_cast<uint32_t>(GACER_NEWOP_DEPTH))
                                            : (cand.op_left > big ? static_cast<uint32_t>(LOOKAHEAD)
-                                                                 : (cand.op_left > G1 ? 2u : static_cast<uint32_t>(GACER_TAIL_DEPTH)));
+                                                                 : (cand.op_left > G1 ? 2u
+                                                                    : ((GACER_TAIL_DEPTH_CC && cand.kind != DK_GEMM)
+                                                                           ? 2u
+                                                                           : static_cast<uint32_t>(GACER_TAIL_DEPTH))));
         sdbg(p, islot, 5, static_cast<int64_t>(allowed) * 1000 + (islot - consumed));
         while (islot - consumed >= allowed) {
           mbar_wait(&ctl->rempty[consumed % ITEM_RING], (consumed / ITEM_RING) & 1);
